@@ -1,0 +1,142 @@
+/*
+ * commet.h -- C ABI of libcommet.so, the B200 (sm_100a) fused neural-
+ * constitutive-model (NCM) update + finite-element assembly library.
+ *
+ * The operation (arXiv 2510.00884, "COMMET"):
+ *   For every element e and quadrature point q (Alg. 1):
+ *     F   = I + sum_a u_a (x) GradN_a^{e,q}              (Alg. 1 l.3)
+ *     k   = (I1-3, I2-3, J-1),  C = F^T F
+ *     W   = N(k) + kappa (J-1)^2 - s0 (J-1),  N an (M)ICNN (Eq. icnn)
+ *     g = dW/dk, H = d2W/dk2 analytically, one forward value pass, one adjoint
+ *     pass and one Jacobian pass -- no autodiff ("CGO"; the
+ *     exact Hessian equals Alg. 4)
+ *     S = 2 dW/dC, CC = 4 d2W/dCdC (Eq. stress-cgo / stiffnes-cgo, PAPER.md:796-801,
+ *     material form, App. A.1)
+ *     r^a_i      += w P_iJ GradN_aJ                        (Eq. r-quad)
+ *     K^{ab}_{ik} += w GradN_aJ (d_ik S_JL + F_iI CC_IJKL F_kK) GradN_bL
+ *                                                         (Eq. k-quad)
+ *   with w = w^{e,q} the quadrature "volume" weight.  r is the
+ *   internal force only (no traction, no Dirichlet elimination).
+ *
+ * Conventions
+ *  - DOF numbering: dof = 3*node + component.  Rows of the CSR are the owned
+ *    DOFs [3*owned_node_begin, 3*owned_node_end), in order; column indices are
+ *    GLOBAL dofs, ascending within a row.  Every node pair sharing >= 1
+ *    element contributes a full 3x3 block (even if numerically zero).
+ *  - Ownership: commet_setup copies every host input; the caller may free its
+ *    arrays on return.  The library owns its device copies and the pattern
+ *    arrays (valid until commet_destroy).  Output buffers are caller-owned
+ *    device memory and are OVERWRITTEN (not accumulated) by commet_assemble.
+ *  - Asynchrony: commet_assemble is asynchronous on the given CUDA stream; it
+ *    returns COMMET_OK unless an argument is invalid.  Domain errors
+ *    (det F <= 0 at some quadrature point) are recorded on the device as the
+ *    lowest flat index e*n_q+q and reported by commet_check; the outputs are
+ *    still fully computed (reading R10).
+ *  - Errors never throw across the ABI.  commet_last_error(ctx) returns a
+ *    message naming the offending index/argument (NULL ctx: last global error).
+ *  - Threading: one ctx per device per host thread; no global state except the
+ *    CUDA context and the last-error buffer for NULL contexts.
+ *  - Multi-GPU (z-slabs): each rank passes the elements
+ *    it assembles and its owned node range; the library builds the owned-row
+ *    CSR plus the interface maps and exchanges non-owned contributions with
+ *    the owning rank over NCCL during commet_assemble.
+ */
+#ifndef COMMET_H_
+#define COMMET_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct commet_ctx_s* commet_ctx;
+
+typedef enum {
+  COMMET_OK = 0,
+  COMMET_ERR_ARG = 1,    /* invalid argument; message names it */
+  COMMET_ERR_CUDA = 2,   /* CUDA runtime error */
+  COMMET_ERR_NCCL = 3,   /* NCCL error */
+  COMMET_ERR_OOM = 4,    /* device or host allocation failed */
+  COMMET_ERR_DOMAIN = 5  /* det F <= 0 at some quadrature point (outputs still written) */
+} commet_status;
+
+enum {
+  COMMET_HEX8 = 0,  /* 8-node trilinear hexahedron, n_q = 8 (2x2x2 Gauss) */
+  COMMET_TET10 = 1  /* 10-node quadratic tetrahedron, n_q = 4 */
+};
+
+typedef struct {
+  int32_t elem_type;          /* COMMET_HEX8 | COMMET_TET10 */
+  int64_t n_nodes;            /* global node count */
+  int64_t n_elems;            /* elements assembled by THIS rank (>= 0) */
+  const int32_t* conn;        /* host [n_elems][n_en]: global node ids, 0-based */
+  const double* grad_N;       /* host [n_elems][n_q][n_en][3]: dN_a/dX (reference config) */
+  const double* qp_w;         /* host [n_elems][n_q]: Gauss weight * det(dX/dxi), > 0 */
+  int64_t owned_node_begin;   /* rows owned by this rank: nodes [begin, end) */
+  int64_t owned_node_end;     /* single GPU: [0, n_nodes) */
+} commet_mesh_desc;
+
+/* (M)ICNN inner network of Eq. icnn with softplus
+ * activation, on the kinematic inputs k = (I1-3, I2-3, J-1):
+ *   y1 = W1 k + b1;  y_l = W_l z_{l-1} + B_l k + b_l (l = 2..L);  z_l = softplus(y_l)
+ *   N  = a . z_L + skip_out . k                                                 */
+typedef struct {
+  int32_t n_hidden;            /* L >= 1 */
+  int32_t width;               /* w; multiple of 8, 8 <= w <= 128 */
+  const double* W1;            /* host [w][3] */
+  const double* W;             /* host [L-1][w][w] row-major (out, in); may be NULL if L == 1 */
+  const double* b;             /* host [L][w] */
+  const double* a;             /* host [w] output weights (no output bias: no effect on S, CC) */
+  const double* skip_out;      /* host [3] or NULL (= 0): output skip B^(n) */
+  const double* skip_hidden;   /* host [L-1][w][3] or NULL (= 0): hidden skips B^(l), l >= 2 */
+  double kappa;                /* volumetric penalty kappa (J-1)^2 */
+  double ref_shift;            /* s0: adds -s0 (J-1) to W; 0 = off (reading R11) */
+} commet_ncm_desc;
+
+/* Kernel variants (commet_set_kernel).  FUSED is the product path; SIMPLE is
+ * a one-thread-per-element CUDA kernel kept as an independent GPU cross-check. */
+enum { COMMET_KERNEL_FUSED = 0, COMMET_KERNEL_SIMPLE = 1 };
+
+/* Build the CSR pattern, element colouring and scatter maps, upload inputs.
+ *   device     CUDA device ordinal
+ *   cuda_stream  cudaStream_t for the uploads (NULL = legacy default stream)
+ *   nccl_comm  ncclComm_t of the slab group, or NULL for a single GPU; with a
+ *              comm, rank r must own the node range directly above rank r-1's.
+ *   out        receives the context on success.
+ * Errors: COMMET_ERR_ARG (bad sizes, node id out of range at element e,
+ * w <= 0 at (e,q), unsupported width), COMMET_ERR_OOM, COMMET_ERR_CUDA. */
+commet_status commet_setup(const commet_mesh_desc* mesh, const commet_ncm_desc* ncm, int device,
+                           void* cuda_stream, void* nccl_comm, commet_ctx* out);
+
+/* Device pointers to the pattern of the owned rows (valid until destroy):
+ * row_ptr int64 [n_rows+1], col_idx int32 [nnz] (global dof columns). */
+commet_status commet_csr_pattern(commet_ctx ctx, int64_t* n_rows, int64_t* nnz,
+                                 const int64_t** row_ptr, const int32_t** col_idx);
+
+/* Assemble: u device fp64 [3*n_nodes] (global, every rank passes the full
+ * vector); residual device fp64 [n_rows]; csr_values device fp64 [nnz].
+ * Asynchronous on cuda_stream. */
+commet_status commet_assemble(commet_ctx ctx, const double* u, double* residual,
+                              double* csr_values, void* cuda_stream);
+
+/* Synchronises the ctx's last assemble stream; returns COMMET_ERR_DOMAIN and
+ * *first_bad_qp = e*n_q+q (local element index) if some det F <= 0, else
+ * COMMET_OK and -1. */
+commet_status commet_check(commet_ctx ctx, int64_t* first_bad_qp);
+
+/* Select the kernel variant used by subsequent commet_assemble calls. */
+commet_status commet_set_kernel(commet_ctx ctx, int32_t variant);
+
+/* Info: n_colours, n_q, n_en and the number of kernel launches one
+ * commet_assemble issues (for the bench's gpu_launches). */
+commet_status commet_info(commet_ctx ctx, int32_t* n_colours, int32_t* n_q, int32_t* n_en,
+                          int32_t* launches_per_assemble);
+
+const char* commet_last_error(commet_ctx ctx);
+void commet_destroy(commet_ctx ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* COMMET_H_ */

@@ -1,0 +1,508 @@
+/*
+ * oracle.c -- plain, slow, obviously-correct fp64 CPU oracle for the COMMET
+ * hot path (arXiv 2510.00884): NCM constitutive update + FE residual/stiffness
+ * assembly into a global vector and a CSR matrix.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline / --impl reference legs may load this library.  It
+ * shares no code, header, table or helper with the CUDA library under
+ * paper_2510_00884_b200/ and never includes or links it.
+ *
+ * What it computes: with W(F) = N(k(F)) + kappa (J-1)^2
+ * - s0 (J-1), k = (I1-3, I2-3, J-1), and Pi(u) = sum_e sum_q w_eq W(F_eq(u)),
+ *   r = dPi/du  (Eq. apprx-r / r-quad, no traction)
+ *   K = d2Pi/du du (Eq. apprx-k / k-quad, incl. the
+ *       geometric delta_ij tau_kl term)
+ * organised exactly as Alg. 1, in MATERIAL form
+ * (App. A.1): P = F S, A_iJkL = d_ik S_JL + F_iI C_IJKL F_kK.
+ * The inner network follows Alg. 4 literally.
+ * No blocking, no fusion, no reordering beyond Alg. 1 / Alg. 4; full 3x3x3x3
+ * arrays (no Voigt).  Readings of the paper: DESIGN.md "Readings".
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+typedef struct {
+  int32_t n_hidden;          /* number of hidden layers (n-1 in Eq. icnn), >= 1 */
+  int32_t width;             /* neurons per hidden layer */
+  const double* W1;          /* [w][3]  A^(1) (+B^(1)) of Eq. icnn-mid-1 */
+  const double* W;           /* [L-1][w][w]  A^(k), k = 2..L, row-major (out,in) */
+  const double* b;           /* [L][w]  c^(k) */
+  const double* a;           /* [w]     A^(n) (output layer, Eq. icnn-output) */
+  const double* skip_out;    /* [3] or NULL: B^(n) */
+  const double* skip_hidden; /* [L-1][w][3] or NULL: B^(k), k = 2..L */
+  double kappa;              /* volumetric penalty kappa (J-1)^2 */
+  double ref_shift;          /* s0: W -= s0 (J-1) (off when 0) */
+} oracle_ncm;
+
+/* ---------------------------------------------------------------------- */
+/* activation F = softplus (BASELINE configs), F' = sigmoid, F'' = s(1-s)  */
+/* ---------------------------------------------------------------------- */
+static double softplus(double y) { return (y > 0 ? y : 0.0) + log1p(exp(-fabs(y))); }
+static double sigmoid(double y) {
+  double e = exp(-fabs(y));
+  return y >= 0 ? 1.0 / (1.0 + e) : e / (1.0 + e);
+}
+
+/*
+ * Alg. 4: one pass giving N, dN/dK, d2N/dKdK.
+ *   z <- K;  dz <- I;  d2z <- 0
+ *   for k = 1..n-1:  y = A z + B K + c;  dy = A dz + B;  d2y = A d2z
+ *                    d2z = F'(y) (.) d2y + F''(y) (.) dy (x) dy
+ *                    dz  = F'(y) (.) dy;   z = F(y)
+ *   N = A^(n) z + B^(n) K;  dN = A^(n) dz + B^(n);  d2N = A^(n) d2z
+ * Layer 1 uses A^(1) = W1 (B^(1) folded in, SURVEY s8(c) reading 7); layers
+ * k >= 2 use A^(k) = W[k-2], B^(k) = skip_hidden[k-2] (reading 6: B is the
+ * current layer's B^(k)).
+ */
+int oracle_ncm_eval(const oracle_ncm* m, const double K[3], double* N_out, double g_out[3],
+                    double H_out[9]) {
+  const int w = m->width, L = m->n_hidden;
+  if (w < 1 || L < 1) return 1;
+  const int nmax = w > 3 ? w : 3;
+  double* z = (double*)calloc(nmax, sizeof(double));
+  double* dz = (double*)calloc((size_t)nmax * 3, sizeof(double));
+  double* d2z = (double*)calloc((size_t)nmax * 9, sizeof(double));
+  double* y = (double*)calloc(nmax, sizeof(double));
+  double* dy = (double*)calloc((size_t)nmax * 3, sizeof(double));
+  double* d2y = (double*)calloc((size_t)nmax * 9, sizeof(double));
+  if (!z || !dz || !d2z || !y || !dy || !d2y) return 2;
+  int nin = 3;
+  for (int i = 0; i < 3; i++) {
+    z[i] = K[i];
+    for (int j = 0; j < 3; j++) dz[i * 3 + j] = (i == j) ? 1.0 : 0.0;
+    for (int j = 0; j < 9; j++) d2z[i * 9 + j] = 0.0;
+  }
+  for (int k = 1; k <= L; k++) {
+    const double* A = (k == 1) ? m->W1 : m->W + (size_t)(k - 2) * w * w;
+    const double* B = (k >= 2 && m->skip_hidden) ? m->skip_hidden + (size_t)(k - 2) * w * 3 : NULL;
+    const double* c = m->b + (size_t)(k - 1) * w;
+    for (int j = 0; j < w; j++) {
+      double s = c[j];
+      for (int i = 0; i < nin; i++) s += A[(size_t)j * nin + i] * z[i];
+      if (B)
+        for (int i = 0; i < 3; i++) s += B[j * 3 + i] * K[i];
+      y[j] = s;
+      for (int p = 0; p < 3; p++) {
+        double t = 0.0;
+        for (int i = 0; i < nin; i++) t += A[(size_t)j * nin + i] * dz[i * 3 + p];
+        if (B) t += B[j * 3 + p];
+        dy[j * 3 + p] = t;
+      }
+      for (int pq = 0; pq < 9; pq++) {
+        double t = 0.0;
+        for (int i = 0; i < nin; i++) t += A[(size_t)j * nin + i] * d2z[i * 9 + pq];
+        d2y[j * 9 + pq] = t;
+      }
+    }
+    for (int j = 0; j < w; j++) {
+      double f1 = sigmoid(y[j]);
+      double f2 = f1 * (1.0 - f1);
+      for (int p = 0; p < 3; p++)
+        for (int q = 0; q < 3; q++)
+          d2z[j * 9 + p * 3 + q] = f1 * d2y[j * 9 + p * 3 + q] + f2 * dy[j * 3 + p] * dy[j * 3 + q];
+      for (int p = 0; p < 3; p++) dz[j * 3 + p] = f1 * dy[j * 3 + p];
+      z[j] = softplus(y[j]);
+    }
+    nin = w;
+  }
+  double N = 0.0, g[3] = {0, 0, 0}, H[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  for (int j = 0; j < w; j++) {
+    N += m->a[j] * z[j];
+    for (int p = 0; p < 3; p++) g[p] += m->a[j] * dz[j * 3 + p];
+    for (int pq = 0; pq < 9; pq++) H[pq] += m->a[j] * d2z[j * 9 + pq];
+  }
+  if (m->skip_out)
+    for (int p = 0; p < 3; p++) {
+      N += m->skip_out[p] * K[p];
+      g[p] += m->skip_out[p];
+    }
+  *N_out = N;
+  for (int p = 0; p < 3; p++) g_out[p] = g[p];
+  for (int pq = 0; pq < 9; pq++) H_out[pq] = H[pq];
+  free(z); free(dz); free(d2z); free(y); free(dy); free(d2y);
+  return 0;
+}
+
+/* ---------------------------------------------------------------------- */
+/* kinematics + stress/tangent at one material point                       */
+/* ---------------------------------------------------------------------- */
+static double det3(const double M[9]) {
+  /* cofactor expansion along the first row */
+  return M[0] * (M[4] * M[8] - M[5] * M[7]) - M[1] * (M[3] * M[8] - M[5] * M[6]) +
+         M[2] * (M[3] * M[7] - M[4] * M[6]);
+}
+static void inv3(const double M[9], double out[9]) {
+  double d = det3(M);
+  out[0] = (M[4] * M[8] - M[5] * M[7]) / d;
+  out[1] = (M[2] * M[7] - M[1] * M[8]) / d;
+  out[2] = (M[1] * M[5] - M[2] * M[4]) / d;
+  out[3] = (M[5] * M[6] - M[3] * M[8]) / d;
+  out[4] = (M[0] * M[8] - M[2] * M[6]) / d;
+  out[5] = (M[2] * M[3] - M[0] * M[5]) / d;
+  out[6] = (M[3] * M[7] - M[4] * M[6]) / d;
+  out[7] = (M[1] * M[6] - M[0] * M[7]) / d;
+  out[8] = (M[0] * M[4] - M[1] * M[3]) / d;
+}
+#define I4(i, j, k, l) ((((i) * 3 + (j)) * 3 + (k)) * 3 + (l))
+
+/*
+ * F (row-major F[i*3+J]) -> k, W, g, H (incl. penalty), S, CC, P, A.
+ * Kinematic layer in material form:
+ *   h1 = dI1/dC = I,  h2 = dI2/dC = I1 I - C,  h3 = dJ/dC = J/2 C^-1
+ *   HH1 = 0,  HH2 = I(x)I - II,  HH3 = J/4 C^-1(x)C^-1 - J/2 II_{C^-1}
+ *   (II_X)_IJKL = 1/2 (X_IK X_JL + X_IL X_JK)   (reading 5)
+ * S = 2 sum_m g_m h_m;  CC = 4 sum_mn H_mn h_m (x) h_n + 4 sum_m g_m HH_m
+ *   (Eq. stress-cgo / stiffnes-cgo, pulled back; reading 4)
+ * P = F S;  A_iJkL = d_ik S_JL + F_iI CC_IJKL F_kK  (Eq. p-stiffness)
+ * Returns J.
+ */
+double oracle_material_point(const oracle_ncm* m, const double F[9], double k_out[3],
+                             double* W_out, double g_out[3], double H_out[9], double S[9],
+                             double CC[81], double P[9], double A[81]) {
+  double C[9], Ci[9];
+  for (int I = 0; I < 3; I++)
+    for (int J = 0; J < 3; J++) {
+      double s = 0.0;
+      for (int i = 0; i < 3; i++) s += F[i * 3 + I] * F[i * 3 + J];
+      C[I * 3 + J] = s;
+    }
+  double I1 = C[0] + C[4] + C[8];
+  double trC2 = 0.0;
+  for (int I = 0; I < 3; I++)
+    for (int J = 0; J < 3; J++) trC2 += C[I * 3 + J] * C[J * 3 + I];
+  double I2 = 0.5 * (I1 * I1 - trC2);
+  double Jd = det3(F);
+  inv3(C, Ci);
+  double k[3] = {I1 - 3.0, I2 - 3.0, Jd - 1.0};
+  double N, g[3], H[9];
+  oracle_ncm_eval(m, k, &N, g, H);
+  /* volumetric penalty (a5) and optional reference shift (reading 11) */
+  double W = N + m->kappa * (Jd - 1.0) * (Jd - 1.0) - m->ref_shift * (Jd - 1.0);
+  g[2] += 2.0 * m->kappa * (Jd - 1.0) - m->ref_shift;
+  H[8] += 2.0 * m->kappa;
+
+  double h[3][9];
+  double HHl[3][81];
+  for (int I = 0; I < 3; I++)
+    for (int J = 0; J < 3; J++) {
+      double d = (I == J) ? 1.0 : 0.0;
+      h[0][I * 3 + J] = d;
+      h[1][I * 3 + J] = I1 * d - C[I * 3 + J];
+      h[2][I * 3 + J] = 0.5 * Jd * Ci[I * 3 + J];
+    }
+  for (int I = 0; I < 3; I++)
+    for (int J = 0; J < 3; J++)
+      for (int K = 0; K < 3; K++)
+        for (int L = 0; L < 3; L++) {
+          double dIJ = (I == J), dKL = (K == L), dIK = (I == K), dJL = (J == L), dIL = (I == L),
+                 dJK = (J == K);
+          HHl[0][I4(I, J, K, L)] = 0.0;
+          HHl[1][I4(I, J, K, L)] = dIJ * dKL - 0.5 * (dIK * dJL + dIL * dJK);
+          HHl[2][I4(I, J, K, L)] =
+              0.25 * Jd * Ci[I * 3 + J] * Ci[K * 3 + L] -
+              0.5 * Jd * 0.5 * (Ci[I * 3 + K] * Ci[J * 3 + L] + Ci[I * 3 + L] * Ci[J * 3 + K]);
+        }
+  for (int IJ = 0; IJ < 9; IJ++) {
+    double s = 0.0;
+    for (int mm = 0; mm < 3; mm++) s += g[mm] * h[mm][IJ];
+    S[IJ] = 2.0 * s;
+  }
+  for (int IJ = 0; IJ < 9; IJ++)
+    for (int KL = 0; KL < 9; KL++) {
+      double s = 0.0;
+      for (int mm = 0; mm < 3; mm++)
+        for (int nn = 0; nn < 3; nn++) s += H[mm * 3 + nn] * h[mm][IJ] * h[nn][KL];
+      double t = 0.0;
+      for (int mm = 0; mm < 3; mm++) t += g[mm] * HHl[mm][IJ * 9 + KL];
+      CC[IJ * 9 + KL] = 4.0 * s + 4.0 * t;
+    }
+  for (int i = 0; i < 3; i++)
+    for (int J = 0; J < 3; J++) {
+      double s = 0.0;
+      for (int I = 0; I < 3; I++) s += F[i * 3 + I] * S[I * 3 + J];
+      P[i * 3 + J] = s;
+    }
+  for (int i = 0; i < 3; i++)
+    for (int J = 0; J < 3; J++)
+      for (int kk = 0; kk < 3; kk++)
+        for (int L = 0; L < 3; L++) {
+          double s = (i == kk) ? S[J * 3 + L] : 0.0;
+          for (int I = 0; I < 3; I++)
+            for (int K = 0; K < 3; K++)
+              s += F[i * 3 + I] * CC[I4(I, J, K, L)] * F[kk * 3 + K];
+          A[I4(i, J, kk, L)] = s;
+        }
+  if (k_out)
+    for (int p = 0; p < 3; p++) k_out[p] = k[p];
+  if (W_out) *W_out = W;
+  if (g_out)
+    for (int p = 0; p < 3; p++) g_out[p] = g[p];
+  if (H_out)
+    for (int p = 0; p < 9; p++) H_out[p] = H[p];
+  return Jd;
+}
+
+/* F at one quadrature point: F = I + sum_a u_a (x) GradN_a (Alg. 1 line 3) */
+static void qp_F(int n_en, const int32_t* conn_e, const double* gN, const double* u, double F[9]) {
+  for (int i = 0; i < 3; i++)
+    for (int J = 0; J < 3; J++) F[i * 3 + J] = (i == J) ? 1.0 : 0.0;
+  for (int a = 0; a < n_en; a++) {
+    int64_t node = conn_e[a];
+    for (int i = 0; i < 3; i++)
+      for (int J = 0; J < 3; J++) F[i * 3 + J] += u[3 * node + i] * gN[a * 3 + J];
+  }
+}
+
+/* all F's, row-major [n_el][n_q][9] (test helper: patch tests, min J) */
+void oracle_qp_F(int64_t n_el, int n_en, int n_q, const int32_t* conn, const double* gradN,
+                 const double* u, double* F_out) {
+  for (int64_t e = 0; e < n_el; e++)
+    for (int q = 0; q < n_q; q++)
+      qp_F(n_en, conn + e * n_en, gradN + ((size_t)e * n_q + q) * n_en * 3, u,
+           F_out + ((size_t)e * n_q + q) * 9);
+}
+
+/* Pi(u) = sum_e sum_q w W(F) */
+double oracle_energy(const oracle_ncm* m, int64_t n_el, int n_en, int n_q, const int32_t* conn,
+                     const double* gradN, const double* qp_w, const double* u) {
+  double Pi = 0.0;
+  double S[9], CC[81], P[9], A[81], W;
+  for (int64_t e = 0; e < n_el; e++)
+    for (int q = 0; q < n_q; q++) {
+      double F[9];
+      qp_F(n_en, conn + e * n_en, gradN + ((size_t)e * n_q + q) * n_en * 3, u, F);
+      oracle_material_point(m, F, NULL, &W, NULL, NULL, S, CC, P, A);
+      Pi += qp_w[e * n_q + q] * W;
+    }
+  return Pi;
+}
+
+/* ---------------------------------------------------------------------- */
+/* sparsity pattern                                  */
+/* ---------------------------------------------------------------------- */
+static int cmp_i64(const void* x, const void* y) {
+  int64_t a = *(const int64_t*)x, b = *(const int64_t*)y;
+  return (a > b) - (a < b);
+}
+
+/* Node adjacency: adj(a) = sorted unique nodes of all elements containing a.
+ * Outputs (malloc'd): adj_ptr [n_nodes+1], adj [adj_ptr[n_nodes]]. */
+static int node_adjacency(int64_t n_nodes, int64_t n_el, int n_en, const int32_t* conn,
+                          int64_t** adj_ptr_out, int64_t** adj_out) {
+  int64_t* cnt = (int64_t*)calloc(n_nodes + 1, sizeof(int64_t));
+  for (int64_t e = 0; e < n_el; e++)
+    for (int a = 0; a < n_en; a++) cnt[conn[e * n_en + a] + 1]++;
+  for (int64_t v = 0; v < n_nodes; v++) cnt[v + 1] += cnt[v];
+  int64_t* inc = (int64_t*)malloc(sizeof(int64_t) * (cnt[n_nodes] + 1));
+  int64_t* fill = (int64_t*)calloc(n_nodes, sizeof(int64_t));
+  for (int64_t e = 0; e < n_el; e++)
+    for (int a = 0; a < n_en; a++) {
+      int64_t v = conn[e * n_en + a];
+      inc[cnt[v] + fill[v]++] = e;
+    }
+  int64_t* adj_ptr = (int64_t*)calloc(n_nodes + 1, sizeof(int64_t));
+  /* pass 1: degree of each node */
+#pragma omp parallel for schedule(dynamic, 4096)
+  for (int64_t v = 0; v < n_nodes; v++) {
+    int64_t ne = cnt[v + 1] - cnt[v];
+    int64_t* tmp = (int64_t*)malloc(sizeof(int64_t) * (ne * n_en + 1));
+    int64_t t = 0;
+    for (int64_t p = cnt[v]; p < cnt[v + 1]; p++)
+      for (int b = 0; b < n_en; b++) tmp[t++] = conn[inc[p] * n_en + b];
+    qsort(tmp, t, sizeof(int64_t), cmp_i64);
+    int64_t u = 0;
+    for (int64_t s = 0; s < t; s++)
+      if (s == 0 || tmp[s] != tmp[s - 1]) u++;
+    adj_ptr[v + 1] = u;
+    free(tmp);
+  }
+  for (int64_t v = 0; v < n_nodes; v++) adj_ptr[v + 1] += adj_ptr[v];
+  int64_t* adj = (int64_t*)malloc(sizeof(int64_t) * (adj_ptr[n_nodes] + 1));
+#pragma omp parallel for schedule(dynamic, 4096)
+  for (int64_t v = 0; v < n_nodes; v++) {
+    int64_t ne = cnt[v + 1] - cnt[v];
+    int64_t* tmp = (int64_t*)malloc(sizeof(int64_t) * (ne * n_en + 1));
+    int64_t t = 0;
+    for (int64_t p = cnt[v]; p < cnt[v + 1]; p++)
+      for (int b = 0; b < n_en; b++) tmp[t++] = conn[inc[p] * n_en + b];
+    qsort(tmp, t, sizeof(int64_t), cmp_i64);
+    int64_t o = adj_ptr[v];
+    for (int64_t s = 0; s < t; s++)
+      if (s == 0 || tmp[s] != tmp[s - 1]) adj[o++] = tmp[s];
+    free(tmp);
+  }
+  free(cnt); free(inc); free(fill);
+  *adj_ptr_out = adj_ptr;
+  *adj_out = adj;
+  return 0;
+}
+
+/* Rows [3*node_begin, 3*node_end): row 3a+i has columns {3b+k : b in adj(a)
+ * ascending, k = 0..2}.  Call with row_ptr != NULL, col_idx == NULL to get
+ * row_ptr (and *nnz); then again with col_idx to fill it. */
+int oracle_pattern(int64_t n_nodes, int64_t n_el, int n_en, const int32_t* conn,
+                   int64_t node_begin, int64_t node_end, int64_t* row_ptr, int32_t* col_idx,
+                   int64_t* nnz) {
+  int64_t *adj_ptr, *adj;
+  node_adjacency(n_nodes, n_el, n_en, conn, &adj_ptr, &adj);
+  int64_t nr = 3 * (node_end - node_begin);
+  row_ptr[0] = 0;
+  for (int64_t a = node_begin; a < node_end; a++)
+    for (int i = 0; i < 3; i++) {
+      int64_t row = 3 * (a - node_begin) + i;
+      row_ptr[row + 1] = row_ptr[row] + 3 * (adj_ptr[a + 1] - adj_ptr[a]);
+    }
+  *nnz = row_ptr[nr];
+  if (col_idx) {
+#pragma omp parallel for schedule(static)
+    for (int64_t a = node_begin; a < node_end; a++)
+      for (int i = 0; i < 3; i++) {
+        int64_t o = row_ptr[3 * (a - node_begin) + i];
+        for (int64_t p = adj_ptr[a]; p < adj_ptr[a + 1]; p++)
+          for (int kk = 0; kk < 3; kk++) col_idx[o++] = (int32_t)(3 * adj[p] + kk);
+      }
+  }
+  free(adj_ptr); free(adj);
+  return 0;
+}
+
+/* ---------------------------------------------------------------------- */
+/* assembly: Alg. 1                                            */
+/* ---------------------------------------------------------------------- */
+static int64_t find_col(const int64_t* row_ptr, const int32_t* col_idx, int64_t row, int64_t col) {
+  int64_t lo = row_ptr[row], hi = row_ptr[row + 1] - 1;
+  while (lo <= hi) {
+    int64_t mid = lo + (hi - lo) / 2;
+    if (col_idx[mid] == col) return mid;
+    if (col_idx[mid] < col) lo = mid + 1; else hi = mid - 1;
+  }
+  return -1;
+}
+
+/* One element: loops q, I, J of Alg. 1; accumulates K_e then scatters.
+ * Rows outside [node_begin, node_end) are skipped (multi-rank ownership). */
+static void assemble_element(const oracle_ncm* m, int64_t e, int n_en, int n_q,
+                             const int32_t* conn, const double* gradN, const double* qp_w,
+                             const double* u, int64_t node_begin, int64_t node_end,
+                             const int64_t* row_ptr, const int32_t* col_idx, double* r,
+                             double* vals, int64_t* bad, int64_t* missing) {
+  const int nd = 3 * n_en;
+  double* Ke = (double*)calloc((size_t)nd * nd, sizeof(double));
+  const int32_t* ce = conn + e * n_en;
+  for (int q = 0; q < n_q; q++) {
+    const double* gN = gradN + ((size_t)e * n_q + q) * n_en * 3;
+    const double wq = qp_w[e * n_q + q];
+    double F[9], S[9], CC[81], P[9], A[81];
+    qp_F(n_en, ce, gN, u, F);
+    double Jd = oracle_material_point(m, F, NULL, NULL, NULL, NULL, S, CC, P, A);
+    if (Jd <= 0.0) {
+      int64_t flat = e * n_q + q;
+#pragma omp critical(oracle_bad)
+      { if (*bad < 0 || flat < *bad) *bad = flat; }
+    }
+    for (int a = 0; a < n_en; a++) {
+      int64_t node = ce[a];
+      for (int i = 0; i < 3; i++) {
+        double s = 0.0;
+        for (int J = 0; J < 3; J++) s += P[i * 3 + J] * gN[a * 3 + J];
+        if (node >= node_begin && node < node_end) r[3 * (node - node_begin) + i] += wq * s;
+      }
+      for (int b = 0; b < n_en; b++)
+        for (int i = 0; i < 3; i++)
+          for (int kk = 0; kk < 3; kk++) {
+            double s = 0.0;
+            for (int J = 0; J < 3; J++)
+              for (int L = 0; L < 3; L++) s += gN[a * 3 + J] * A[I4(i, J, kk, L)] * gN[b * 3 + L];
+            Ke[(a * 3 + i) * nd + b * 3 + kk] += wq * s;
+          }
+    }
+  }
+  for (int a = 0; a < n_en; a++) {
+    int64_t na = ce[a];
+    if (na < node_begin || na >= node_end) continue;
+    for (int i = 0; i < 3; i++) {
+      int64_t row = 3 * (na - node_begin) + i;
+      for (int b = 0; b < n_en; b++)
+        for (int kk = 0; kk < 3; kk++) {
+          int64_t pos = find_col(row_ptr, col_idx, row, 3 * (int64_t)ce[b] + kk);
+          if (pos < 0) { (*missing)++; continue; }
+          vals[pos] += Ke[(a * 3 + i) * nd + b * 3 + kk];
+        }
+    }
+  }
+  free(Ke);
+}
+
+/* Greedy element colouring (first colour not used by any element sharing a
+ * node), elements in index order.  Returns the number of colours. */
+static int colour_elements(int64_t n_nodes, int64_t n_el, int n_en, const int32_t* conn,
+                           int32_t* colour) {
+  /* node -> bitmask of colours already used by elements touching it (<= 64) */
+  uint64_t* used = (uint64_t*)calloc(n_nodes, sizeof(uint64_t));
+  int ncol = 0;
+  for (int64_t e = 0; e < n_el; e++) {
+    uint64_t mask = 0;
+    for (int a = 0; a < n_en; a++) mask |= used[conn[e * n_en + a]];
+    int c = 0;
+    while (c < 64 && (mask >> c) & 1ULL) c++;
+    if (c >= 64) { free(used); return -1; }
+    colour[e] = c;
+    if (c + 1 > ncol) ncol = c + 1;
+    for (int a = 0; a < n_en; a++) used[conn[e * n_en + a]] |= (1ULL << c);
+  }
+  free(used);
+  return ncol;
+}
+
+/* r and vals are OVERWRITTEN.  mode 0: serial, element order (Alg. 1 as
+ * written).  mode 1: OpenMP over the elements of one colour at a time
+ * (deterministic for any thread count).  Returns #missing pattern entries
+ * (0 expected), or -1 on colouring failure. */
+int64_t oracle_assemble(const oracle_ncm* m, int64_t n_nodes, int64_t n_el, int n_en, int n_q,
+                        const int32_t* conn, const double* gradN, const double* qp_w,
+                        const double* u, int64_t node_begin, int64_t node_end,
+                        const int64_t* row_ptr, const int32_t* col_idx, double* r, double* vals,
+                        int64_t* bad, int mode, int n_threads) {
+  int64_t nr = 3 * (node_end - node_begin);
+  memset(r, 0, sizeof(double) * nr);
+  memset(vals, 0, sizeof(double) * row_ptr[nr]);
+  *bad = -1;
+  int64_t missing = 0;
+  if (mode == 0) {
+    for (int64_t e = 0; e < n_el; e++)
+      assemble_element(m, e, n_en, n_q, conn, gradN, qp_w, u, node_begin, node_end, row_ptr,
+                       col_idx, r, vals, bad, &missing);
+    return missing;
+  }
+  int32_t* colour = (int32_t*)malloc(sizeof(int32_t) * (n_el + 1));
+  int ncol = colour_elements(n_nodes, n_el, n_en, conn, colour);
+  if (ncol < 0) { free(colour); return -1; }
+#ifdef _OPENMP
+  if (n_threads > 0) omp_set_num_threads(n_threads);
+#endif
+  for (int c = 0; c < ncol; c++) {
+    int64_t miss_c = 0;
+#pragma omp parallel for schedule(dynamic, 16) reduction(+ : miss_c)
+    for (int64_t e = 0; e < n_el; e++)
+      if (colour[e] == c)
+        assemble_element(m, e, n_en, n_q, conn, gradN, qp_w, u, node_begin, node_end, row_ptr,
+                         col_idx, r, vals, bad, &miss_c);
+    missing += miss_c;
+  }
+  free(colour);
+  return missing;
+}
+
+int oracle_max_threads(void) {
+#ifdef _OPENMP
+  return omp_get_max_threads();
+#else
+  return 1;
+#endif
+}

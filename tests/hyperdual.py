@@ -1,0 +1,108 @@
+"""Hyper-dual numbers (a + b e1 + c e2 + d e1 e2, e1^2 = e2^2 = 0) for exact
+first and second derivatives of W(F) straight from its definition -- an
+independent derivation used to PIN the oracle's G-tensor algebra (no shared
+code with oracle/ or the CUDA path).
+
+Only what W(F) = N(k(F)) + kappa (J-1)^2 - s0 (J-1) needs: +, -, *, softplus.
+Every component is a numpy array so all 81 direction pairs run at once.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+
+class HD:
+    __slots__ = ("a", "b", "c", "d")
+
+    def __init__(self, a, b=0.0, c=0.0, d=0.0):
+        self.a, self.b, self.c, self.d = a, b, c, d
+
+    @staticmethod
+    def lift(x):
+        return x if isinstance(x, HD) else HD(x)
+
+    def __add__(self, o):
+        o = HD.lift(o)
+        return HD(self.a + o.a, self.b + o.b, self.c + o.c, self.d + o.d)
+
+    __radd__ = __add__
+
+    def __neg__(self):
+        return HD(-self.a, -self.b, -self.c, -self.d)
+
+    def __sub__(self, o):
+        return self + (-HD.lift(o))
+
+    def __rsub__(self, o):
+        return HD.lift(o) - self
+
+    def __mul__(self, o):
+        o = HD.lift(o)
+        return HD(self.a * o.a, self.a * o.b + self.b * o.a, self.a * o.c + self.c * o.a,
+                  self.a * o.d + self.b * o.c + self.c * o.b + self.d * o.a)
+
+    __rmul__ = __mul__
+
+    def apply(self, f0, f1, f2):
+        """f(x) with f' = f1, f'' = f2 evaluated at the real part."""
+        fa, d1, d2 = f0(self.a), f1(self.a), f2(self.a)
+        return HD(fa, d1 * self.b, d1 * self.c, d1 * self.d + d2 * self.b * self.c)
+
+
+def _sig(y):
+    return np.where(y >= 0, 1.0 / (1.0 + np.exp(-np.abs(y))), np.exp(-np.abs(y)) / (1.0 + np.exp(-np.abs(y))))
+
+
+def softplus(x: HD) -> HD:
+    return x.apply(lambda y: np.maximum(y, 0) + np.log1p(np.exp(-np.abs(y))), _sig,
+                   lambda y: _sig(y) * (1.0 - _sig(y)))
+
+
+def energy_hd(F: list, ncm: dict):
+    """W(F) for a 3x3 list-of-lists of HD; written from the definitions:
+    C = F^T F, I1 = tr C, I2 = (I1^2 - tr C^2)/2, J = det F (Sarrus),
+    MLP/ICNN of Eq. icnn with softplus, penalty kappa (J-1)^2 - s0 (J-1)."""
+    Cm = [[sum((F[i][I] * F[i][J] for i in range(3)), HD(0.0)) for J in range(3)] for I in range(3)]
+    I1 = Cm[0][0] + Cm[1][1] + Cm[2][2]
+    trC2 = sum((Cm[I][J] * Cm[J][I] for I in range(3) for J in range(3)), HD(0.0))
+    I2 = 0.5 * (I1 * I1 - trC2)
+    J = (F[0][0] * F[1][1] * F[2][2] + F[0][1] * F[1][2] * F[2][0] + F[0][2] * F[1][0] * F[2][1]
+         - F[0][2] * F[1][1] * F[2][0] - F[0][0] * F[1][2] * F[2][1] - F[0][1] * F[1][0] * F[2][2])
+    k = [I1 - 3.0, I2 - 3.0, J - 1.0]
+    W1, b, a = ncm["W1"], ncm["b"], ncm["a"]
+    L, w = ncm["n_hidden"], ncm["width"]
+    Wh = ncm.get("W")
+    Bh = ncm.get("skip_hidden")
+    z = [sum((W1[j, i] * k[i] for i in range(3)), HD(0.0)) + b[0, j] for j in range(w)]
+    z = [softplus(v) for v in z]
+    for l in range(1, L):
+        y = []
+        for j in range(w):
+            s = HD(b[l, j])
+            for i in range(w):
+                s = s + Wh[l - 1, j, i] * z[i]
+            if Bh is not None:
+                for i in range(3):
+                    s = s + Bh[l - 1, j, i] * k[i]
+            y.append(s)
+        z = [softplus(v) for v in y]
+    N = sum((a[j] * z[j] for j in range(w)), HD(0.0))
+    if ncm.get("skip_out") is not None:
+        for i in range(3):
+            N = N + ncm["skip_out"][i] * k[i]
+    kap, s0 = ncm.get("kappa", 0.0), ncm.get("ref_shift", 0.0)
+    return N + kap * (J - 1.0) * (J - 1.0) - s0 * (J - 1.0)
+
+
+def derivatives(F0: np.ndarray, ncm: dict):
+    """-> (W, P = dW/dF (3x3), A = d2W/dFdF (3x3x3x3)) exactly (to rounding)."""
+    idx = np.arange(81)
+    p, q = idx // 9, idx % 9
+    F = [[HD(np.full(81, F0[i, J]), (p == 3 * i + J).astype(float), (q == 3 * i + J).astype(float),
+             np.zeros(81)) for J in range(3)] for i in range(3)]
+    W = energy_hd(F, ncm)
+    P = np.zeros(9)
+    for pp in range(9):
+        P[pp] = W.b[pp * 9]
+    A = W.d.reshape(9, 9)
+    return float(W.a[0]), P.reshape(3, 3), A.reshape(3, 3, 3, 3)
