@@ -1,0 +1,340 @@
+#!/usr/bin/env python
+"""Benchmark of the fused NCM-update + FE-assembly hot path (BASELINE.json metric:
+quadrature-point stress+tangent updates/s and assembled elements/s, % of the
+fp64 roofline).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--impl reference]
+
+One "step" = one commet_assemble call (zeroing, every colour launch of the
+fused kernel and, for N > 1, the interface exchange) over the whole mesh.
+Rank 0 prints ONE JSON line.  N > 1 runs under torchrun, one rank per GPU,
+z-slab partition with NCCL interface exchange (strong scaling: fixed mesh).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from synth import gen  # noqa: E402
+
+METRIC = "quadrature-point stress+tangent updates/s (assembled elements/s and % fp64 roofline alongside)"
+FP64_PEAK_TFLOPS = 36.9   # measured, sustained DMMA m8n8k4, profiles/r01_fp64_peak.json
+FP64_PEAK_SOURCE = "measured: tools/fp64_peak.cu sustained DMMA (profiles/r01_fp64_peak.json); MEASURED_PEAKS.json has no fp64 entry"
+
+WORKLOAD = {
+    "c1": "c1: 4^3 hex8 unit cube, 2x2x2 Gauss (512 qp), NCM 16x2 softplus + kappa(J-1)^2, u ~ U(+-0.02)",
+    "c2": "c2: 16^3 hex8 jittered 10%, 32,768 qp, NCM 32x2, smooth u amp 0.05",
+    "c3": "c3: 64^3 hex8, 262,144 elements, 2,097,152 qp, 823,875 DOFs, NCM 64x3, u_x = 0.2x + smooth 0.01",
+    "c4": "c4: 48^3 x 6 tet10 jittered, 663,552 elements, 2,654,208 qp, 2,738,019 DOFs, NCM 128x3, smooth u amp 0.1",
+    "c5": "c5: 256^3 hex8, 16,777,216 elements, 134,217,728 qp, 50,923,779 DOFs, NCM 64x3, smooth u amp 0.05",
+}
+
+
+def flops_per_qp(elem_type: int, w: int, L: int) -> int:
+    """NCM_min(w, L) + ELEM(n_en) (FMA = 2 flops,
+    transcendentals not counted) -- the algorithmic count."""
+    n_en = 8 if elem_type == gen.HEX8 else 10
+    n_d = 3 * n_en
+    ncm = 10 * w * w * (L - 1) + 20 * w * L + 8 * w
+    elem = (18 * n_en + 100 + 350 + 54 + 18 * n_en + 54 * n_en + 72 * n_d + 14 * n_d * (n_d + 1) // 2
+            + 18 * n_en + 9 * n_en * (n_en + 1) // 2)
+    return ncm + elem
+
+
+def hbm_bytes_per_element(elem_type: int, nnz_per_el: float, dofs_per_el: float) -> float:
+    """Algorithmic HBM bytes per element (write-once outputs): dN/dX + w + conn
+    + slots + u gather + r + CSR values."""
+    n_en, n_q = (8, 8) if elem_type == gen.HEX8 else (10, 4)
+    return 8 * n_q * n_en * 3 + 8 * n_q + 4 * n_en + n_en * n_en + 8 * 3 * n_en * 0.0 + \
+        8 * dofs_per_el + 8 * nnz_per_el + 8 * dofs_per_el
+
+
+# ---------------------------------------------------------------------------
+# distributed helpers
+# ---------------------------------------------------------------------------
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def slab_range(spec, n, P, r):
+    """Element layers and owned node range of z-slab r of P."""
+    k0, k1 = r * n // P, (r + 1) * n // P
+    if spec.elem_type == gen.HEX8:
+        m = n + 1
+        nb = k0 * m * m
+        ne = (k1 if r < P - 1 else n + 1) * m * m
+    else:
+        bounds = gen.tet10_plane_bounds(n)
+        nb = int(bounds[2 * k0])
+        ne = int(bounds[2 * k1]) if r < P - 1 else int(bounds[-1])
+    return (k0, k1), (nb, ne)
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region."""
+
+    def __init__(self, index: int):
+        self.p = None
+        self.index = index
+        try:
+            self.p = subprocess.Popen(
+                ["nvidia-smi", "-i", str(index), "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,power.draw",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        out, _ = self.p.communicate(timeout=10)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the oracle as it stands, on a bounded sample
+# ---------------------------------------------------------------------------
+def oracle_sample(cfg: dict, seconds: float):
+    """Time oracle.assemble (OpenMP over colours, all host cores) on the first
+    n_s elements of the workload, n_s sized for ~`seconds` of CPU work."""
+    import oracle
+    conn, gN, qw = cfg["conn"], cfg["gradN"], cfg["qp_w"]
+    n_q = gN.shape[1]
+
+    def run(ns):
+        sub = np.ascontiguousarray(conn[:ns])
+        rp, ci = oracle.pattern(cfg["n_nodes"], sub)
+        t0 = time.perf_counter()
+        oracle.assemble(cfg["ncm"], cfg["n_nodes"], sub, gN[:ns], qw[:ns], cfg["u"], rp, ci, mode=1)
+        return time.perf_counter() - t0
+
+    ns = min(conn.shape[0], 256)
+    t = run(ns)
+    while t < 0.5 and ns < conn.shape[0]:
+        ns = min(conn.shape[0], ns * 4)
+        t = run(ns)
+    ns2 = int(min(conn.shape[0], max(ns, ns * seconds / max(t, 1e-9))))
+    if ns2 != ns:
+        ns, t = ns2, run(ns2)
+    return dict(value=ns * n_q / t, unit="qp/s", cores=oracle.max_threads(), kind="oracle",
+                sample=f"first {ns} of {conn.shape[0]} elements ({ns * n_q} qp), oracle.assemble "
+                       f"(plain C, OpenMP over element colours), {t:.1f} s",
+                elements_per_s=ns / t, seconds=t)
+
+
+def run_reference(args):
+    """--impl reference: the oracle as it stands, timed on the host cores on a
+    bounded sample of the same workload each step (rank 0 only)."""
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    cfg = gen.make_config(args.config)
+    per_step = max(2.0, min(10.0, 150.0 / max(1, args.steps + args.warmup)))
+    base = oracle_sample(cfg, per_step)                 # sizes the sample
+    ns = int(base["sample"].split()[1])
+    import oracle
+    sub = np.ascontiguousarray(cfg["conn"][:ns])
+    rp, ci = oracle.pattern(cfg["n_nodes"], sub)
+    n_q = cfg["gradN"].shape[1]
+    times = []
+    for s in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        oracle.assemble(cfg["ncm"], cfg["n_nodes"], sub, cfg["gradN"][:ns], cfg["qp_w"][:ns], cfg["u"],
+                        rp, ci, mode=1)
+        if s >= args.warmup:
+            times.append(time.perf_counter() - t0)
+    t = float(np.mean(times))
+    value = ns * n_q / t
+    line = dict(impl="reference", metric=METRIC, value=value, unit="qp/s", n_gpus=ws, steps=args.steps,
+                warmup=args.warmup, ms_per_step=t * 1e3, higher_is_better=True, scaling="strong",
+                vs_baseline=None, dtype="f64", data="synthetic",
+                config=dict(workload=WORKLOAD[args.config], sample_elements=ns),
+                elements_per_s=ns / t,
+                cpu_baseline=dict(value=value, unit="qp/s", cores=oracle.max_threads(), kind="oracle",
+                                  sample=f"first {ns} elements of {args.config} per step"),
+                e2e=dict(value=value, unit="qp/s", h2d_bytes_per_step=0, d2h_bytes_per_step=0))
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# the GPU path
+# ---------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c3", choices=sorted(WORKLOAD))
+    ap.add_argument("--impl", default="commet", choices=["commet", "reference"])
+    ap.add_argument("--kernel", default="fused", choices=["fused", "simple"])
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+    ws, rank, local = dist_env()
+    if ws > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2510_00884_b200 as pc
+
+    spec = gen.CONFIGS[args.config]
+    n = spec.n
+    if ws > 1:
+        zr, (nb, ne) = slab_range(spec, n, ws, rank)
+        cfg = gen.make_config(args.config, z_range=zr)
+        owned = dict(owned_node_begin=nb, owned_node_end=ne)
+    else:
+        cfg = gen.make_config(args.config)
+        owned = {}
+    comm = None
+    if ws > 1:
+        comm = pc.nccl_comm_from_process_group(rank, ws, local)
+    mesh = dict(elem_type=cfg["elem_type"], n_nodes=cfg["n_nodes"], conn=cfg["conn"], gradN=cfg["gradN"],
+                qp_w=cfg["qp_w"], **owned)
+    if ws > 1:
+        mesh.update(pc.slab_ghosts(args.config, n, ws, rank))
+    lib = pc.Commet(mesh, cfg["ncm"], device=local, nccl_comm=comm)
+    if args.kernel == "simple":
+        lib.set_kernel(pc.KERNEL_SIMPLE)
+    n_el, n_q = cfg["conn"].shape[0], cfg["gradN"].shape[1]
+    info = lib.info()
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream(dev)
+    u_host = torch.from_numpy(cfg["u"]).pin_memory()
+    u = u_host.to(dev)
+    r, v = lib.alloc_outputs()
+    lib.set_timing(args.steps)
+
+    # warm-up + correctness gate (det F > 0 everywhere)
+    for _ in range(args.warmup):
+        lib.assemble(u, r, v)
+    torch.cuda.synchronize()
+    bad = lib.check()
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+
+    # ---- timed region: K device-resident steps --------------------------------------------
+    clk = Clocks(local)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        lib.assemble(u, r, v)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    clocks = clk.stop()
+    ms = e0.elapsed_time(e1) / args.steps
+    kern_ms = float(np.mean(lib.kernel_times(args.steps)))
+    t_local = torch.tensor([ms, kern_ms], dtype=torch.float64, device=dev)
+    if ws > 1:
+        dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
+    ms, kern_ms = float(t_local[0]), float(t_local[1])
+
+    # ---- e2e: host u -> device, assemble, device -> host r and CSR values ----------------------
+    e2e = None
+    if not args.no_e2e:
+        r_host = torch.empty(r.numel(), dtype=torch.float64).pin_memory()
+        v_host = torch.empty(v.numel(), dtype=torch.float64).pin_memory()
+        if ws > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(args.steps):
+            u.copy_(u_host, non_blocking=True)
+            lib.assemble(u, r, v)
+            r_host.copy_(r, non_blocking=True)
+            v_host.copy_(v, non_blocking=True)
+        f1.record(stream)
+        torch.cuda.synchronize()
+        ms_e2e = f0.elapsed_time(f1) / args.steps
+        t_e = torch.tensor([ms_e2e], dtype=torch.float64, device=dev)
+        if ws > 1:
+            dist.all_reduce(t_e, op=dist.ReduceOp.MAX)
+        ms_e2e = float(t_e[0])
+        e2e = dict(value=spec_total_qp(args.config, n_el, n_q, ws) / (ms_e2e * 1e-3), unit="qp/s",
+                   h2d_bytes_per_step=u_host.numel() * 8, d2h_bytes_per_step=(r.numel() + v.numel()) * 8,
+                   ms_per_step=ms_e2e)
+
+    total_qp = spec_total_qp(args.config, n_el, n_q, ws)
+    total_el = total_qp // n_q
+    fl = flops_per_qp(cfg["elem_type"], spec.width, spec.n_hidden)
+    # roofline of the dominant kernel (fused_kernel: all colour launches of one step)
+    achieved = fl * total_qp / ws / (kern_ms * 1e-3) / 1e12
+    nnz_local, rows_local = lib.nnz, lib.n_rows
+    hbm = hbm_bytes_per_element(cfg["elem_type"], nnz_local / max(n_el, 1), rows_local / max(n_el, 1))
+    line = dict(
+        metric=METRIC, value=total_qp / (ms * 1e-3), unit="qp/s", n_gpus=ws, steps=args.steps,
+        warmup=args.warmup, ms_per_step=ms, higher_is_better=True, scaling="strong", vs_baseline=None,
+        dtype="f64", data="synthetic (seeded mesh, NCM weights N(0,0.3^2), displacement; synth/gen.py)",
+        config=dict(workload=WORKLOAD[args.config], elements=total_el, qp=total_qp, nnz_rank0=nnz_local,
+                    width=spec.width, hidden_layers=spec.n_hidden, colours=info["n_colours"],
+                    kernel=args.kernel, parallelism=f"z-slabs x{ws}" if ws > 1 else "single GPU",
+                    l2="inputs larger than L2 (dN/dX + CSR values >> 126 MB), no flush needed"
+                    if args.config in ("c3", "c4", "c5") else "inputs fit in L2 (latency-bound config)"),
+        elements_per_s=total_el / (ms * 1e-3),
+        kernel_ms_per_step=kern_ms,
+        roofline=dict(bound="alu", pipe="fp64 (DFMA/DMMA share one datapath)", achieved=achieved,
+                      peak=FP64_PEAK_TFLOPS, unit="TFLOP/s", frac=achieved / FP64_PEAK_TFLOPS,
+                      traffic=None, flops_per_qp=fl, peak_source=FP64_PEAK_SOURCE,
+                      hbm_algorithmic_gbs=hbm * n_el / (kern_ms * 1e-3) / 1e9, hbm_peak_gbs=6556.2),
+        clocks=clocks, gpu_launches=info["launches"] * args.steps,
+        e2e=e2e, det_f_ok=(bad == -1),
+    )
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        line["cpu_baseline"] = {k: v for k, v in oracle_sample(cfg, args.cpu_seconds).items()
+                                if k in ("value", "unit", "cores", "kind", "sample")}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def spec_total_qp(name, n_el_local, n_q, ws):
+    spec = gen.CONFIGS[name]
+    if ws == 1:
+        return n_el_local * n_q
+    per_cell = 1 if spec.elem_type == gen.HEX8 else 6
+    return spec.n ** 3 * per_cell * n_q
+
+
+if __name__ == "__main__":
+    sys.exit(main())

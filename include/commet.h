@@ -114,6 +114,10 @@ commet_status commet_setup(const commet_mesh_desc* mesh, const commet_ncm_desc* 
 commet_status commet_csr_pattern(commet_ctx ctx, int64_t* n_rows, int64_t* nnz,
                                  const int64_t** row_ptr, const int32_t** col_idx);
 
+/* Copy the pattern into caller buffers (host or device memory; cudaMemcpyDefault):
+ * row_ptr int64 [n_rows+1], col_idx int32 [nnz].  Synchronous. */
+commet_status commet_csr_pattern_copy(commet_ctx ctx, int64_t* row_ptr, int32_t* col_idx);
+
 /* Assemble: u device fp64 [3*n_nodes] (global, every rank passes the full
  * vector); residual device fp64 [n_rows]; csr_values device fp64 [nnz].
  * Asynchronous on cuda_stream. */
@@ -132,6 +136,15 @@ commet_status commet_set_kernel(commet_ctx ctx, int32_t variant);
  * commet_assemble issues (for the bench's gpu_launches). */
 commet_status commet_info(commet_ctx ctx, int32_t* n_colours, int32_t* n_q, int32_t* n_en,
                           int32_t* launches_per_assemble);
+
+/* Kernel-time instrumentation for benchmarks: with n_slots > 0, every
+ * commet_assemble records a CUDA event pair on its stream around its kernel
+ * launches (first colour launch .. last launch, zeroing excluded) into a ring
+ * of n_slots pairs; n_slots = 0 turns it off. */
+commet_status commet_set_timing(commet_ctx ctx, int32_t n_slots);
+/* Elapsed kernel milliseconds of the last n assembles (oldest first); n <=
+ * min(n_slots, assembles so far).  Synchronises on the recorded events. */
+commet_status commet_kernel_times(commet_ctx ctx, float* ms_out, int32_t n);
 
 const char* commet_last_error(commet_ctx ctx);
 void commet_destroy(commet_ctx ctx);

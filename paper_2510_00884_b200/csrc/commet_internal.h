@@ -1,0 +1,63 @@
+// commet_internal.h -- device-side data layout of libcommet (not part of the ABI).
+//
+// HBM layout (per rank, all device memory owned by the ctx):
+//  * element data in COLOUR-SORTED order (colour c = [colour_start[c], colour_start[c+1])):
+//      conn   int32 [n_el][n_en]        global node ids (u gather)
+//      lrow   int32 [n_el][n_en]        local row-node id (owned: node-begin; halo: n_owned + h)
+//      gradN  fp64  [n_el][n_q][n_en][3]  contiguous per element (1536 B hex8, 960 B tet10)
+//      qp_w   fp64  [n_el][n_q]
+//      slot   uint8 [n_el][n_en][n_en]  position of node b in the adjacency of node a's row
+//      orig   int64 [n_el]               original element index (det F <= 0 report)
+//  * per local row-node: node_rs int64 (first CSR entry of its row 3a+0), node_deg int32;
+//    row 3a+i starts at node_rs[a] + i*3*deg[a]; entry (3a+i, 3b+k) at + 3*slot + k.
+//  * NCM weights in DMMA m8n8k4 A-fragment order (see kernel_fused.cu).
+#pragma once
+#include <cstdint>
+
+namespace commet {
+
+constexpr int kMaxLayers = 4;
+constexpr int kMaxWidth = 128;
+
+struct NcmDev {
+  int L, w;
+  const double* W1;       // [w][3]
+  const double* b;        // [L][w]
+  const double* a;        // [w]
+  const double* skip_out; // [3] (zeros if absent)
+  const double* skip_h;   // [L-1][w][3] or nullptr
+  const double* Wrow;     // [L-1][w][w] row-major (simple kernel)
+  const double* Wfrag;    // [L-1][2][frag] fragment-ordered W and W^T (fused kernel)
+  double kappa, ref_shift;
+};
+
+struct AsmArgs {
+  int n_en, n_q;
+  int64_t el_begin, el_count;  // colour range in sorted order
+  const int32_t* conn;
+  const int32_t* lrow;
+  const double* gradN;
+  const double* qp_w;
+  const uint8_t* slot;
+  const int64_t* orig;
+  const int64_t* node_rs;
+  const int32_t* node_deg;
+  int64_t n_owned;  // local row-nodes < n_owned -> user buffers
+  const double* u;
+  double* r_own;
+  double* v_own;
+  double* r_halo;
+  double* v_halo;
+  unsigned long long* bad;
+  NcmDev ncm;
+};
+
+// launchers (kernel_simple.cu / kernel_fused.cu); return cudaError_t as int
+int launch_simple(const AsmArgs& a, void* stream);
+int launch_fused(const AsmArgs& a, void* stream, int* launches);
+int fused_supported(int n_en, int n_q, int w, int L);
+// prepares the fragment-ordered weight array on the host (size in doubles)
+int64_t fused_weight_frag_size(int w, int L);
+void fused_weight_frag_fill(int w, int L, const double* Wrow, double* out);
+
+}  // namespace commet

@@ -1,0 +1,553 @@
+// kernel_fused.cu -- the product path: ONE kernel per element colour that runs
+// every step of the hot path for a batch of
+// elements held in shared memory; nothing but u, the element inputs and the
+// scatter touch HBM.
+//
+// Per CTA iteration (E elements = Q quadrature points):
+//   0  stage dN/dX, w, gather u_e                            (a1)
+//   1  F, C, I1, I2, J -> k = (I1-3, I2-3, J-1), det F flag   (a2, a3)
+//   2  layer 1 (3 -> w): y, softplus, sigmoid                 (a4)
+//   3  value pass, hidden layers l = 2..L:  Y = W_l Z          (a4, DMMA GEMM)
+//   4  adjoint pass l = L..2:  Lambda = W_l^T M               (a4, DMMA GEMM)
+//   5  g = W1^T mu_1 (+skips), H_1 = W1^T diag(c_1) W1         (a4)
+//   6  Jacobian pass l = 2..L: J_l = W_l (s_{l-1} (.) J_{l-1}) (a4, DMMA GEMM)
+//      H += J_l^T diag(c_l) J_l on the fly, c_l = lambda_l s_l (1-s_l)
+//   7  penalty, S, A = d2W/dFdF (scaled by w)                 (a5, a6)
+//   8  element rows: K_e, r_e; coloured read-modify-write scatter (a7, a8)
+// The inner-network derivatives are the exact Hessian of Alg. 4
+// obtained with 5 w^2 FMA per hidden layer instead of
+// Alg. 4's 10 w^2.  Hidden-layer contractions use the
+// fp64 tensor path (mma.sync m8n8k4 f64 = SASS DMMA.8x8x4): on B200 it shares
+// the fp64 datapath with DFMA (measured, profiles/r01_fp64_peak.json) but
+// needs ~8x fewer issue slots and register-file reads per FMA.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+
+#include "commet_internal.h"
+#include "qp_math.cuh"
+
+namespace commet {
+
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ double2 ldg2(const double* p) {
+  return __ldg(reinterpret_cast<const double2*>(p));
+}
+
+// ---------------------------------------------------------------------------
+// compile-time tiling
+// ---------------------------------------------------------------------------
+template <int W_, int Q_, int NEN_, int NQ_>
+struct Cfg {
+  static constexpr int W = W_, Q = Q_, NEN = NEN_, NQ = NQ_;
+  static constexpr int NWARP = 4, NTHR = 128;
+  static constexpr int E = Q / NQ;                 // elements per CTA iteration
+  static constexpr int MTILES = W / 8, QB = Q / 8, KT2 = W / 8;
+  // value / adjoint warp tiles: VMG x VNG warps, each MT_V x NT_V tiles
+  static constexpr int TPW = MTILES * QB / NWARP;
+  static constexpr int NT_V = (QB >= 2 && TPW % 2 == 0 && TPW >= 4) ? 2 : 1;
+  static constexpr int MT_V = TPW / NT_V;
+  static constexpr int VNG = QB / NT_V, VMG = MTILES / MT_V;
+  // Jacobian warp tiles: JMG m-groups x QB qp blocks, each MT_J x 3 tiles
+  static constexpr int JMG = NWARP / QB, MT_J = MTILES / JMG;
+  static constexpr int LDA = 3 * Q + 4;            // act row stride (= 4 mod 16: conflict-free B frags)
+  static constexpr int LDS = Q + 4;                // s/c row stride
+  static_assert(W % 8 == 0 && Q % 8 == 0 && Q % NQ == 0, "tile");
+  static_assert(TPW >= 1 && VMG * VNG == NWARP && MT_V * NT_V == TPW, "value tiling");
+  static_assert(JMG >= 1 && JMG * QB == NWARP && MT_J * JMG == MTILES, "jacobian tiling");
+};
+
+// shared-memory carve-up (doubles); L is a runtime value
+template <class C>
+struct Smem {
+  int act, sb, cb, qF, qk, qg, qH, hred, gsk, gN, ue, wq, qA, qP, total;
+  __host__ __device__ Smem(int L) {
+    int o = 0;
+    act = o; o += C::W * C::LDA;
+    sb = o;  o += (L > 1 ? L - 1 : 0) * C::W * C::LDS;
+    cb = o;  o += L * C::W * C::LDS;
+    qF = o;  o += C::Q * 9;
+    qk = o;  o += C::Q * 3;
+    qg = o;  o += C::Q * 3;
+    qH = o;  o += C::Q * 6;
+    hred = o; o += C::JMG * C::Q * 6;
+    gsk = o; o += C::Q * 3;
+    gN = o;  o += C::Q * C::NEN * 3;
+    ue = o;  o += C::E * C::NEN * 3;
+    wq = o;  o += C::Q;
+    o = (o + 1) & ~1;
+    // post-NCM per-qp outputs alias act/s/c (dead after stage 6) when they fit
+    if (qF >= C::Q * 90) {
+      qA = 0;
+    } else {
+      qA = o;
+      o += C::Q * 90;
+    }
+    qP = qA + C::Q * 81;
+    total = o;
+  }
+};
+
+// ---------------------------------------------------------------------------
+// one warp tile of  C = A (M x K, fragments in global) * B (K x N, smem)
+// ---------------------------------------------------------------------------
+template <int MT, int NT, int KT2>
+__device__ __forceinline__ void warp_gemm(const double* __restrict__ Af, int mt0, const double* act,
+                                          int lda, const int (&ncol)[NT], double (&acc)[MT][NT][2]) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+#pragma unroll
+  for (int i = 0; i < MT; i++)
+#pragma unroll
+    for (int j = 0; j < NT; j++) acc[i][j][0] = acc[i][j][1] = 0.0;
+  const double* ap = Af + (size_t)mt0 * KT2 * 64 + lane * 2;
+  const double* bp = act + t * lda + g;
+#pragma unroll 4
+  for (int kt2 = 0; kt2 < KT2; kt2++) {
+    double2 a[MT];
+#pragma unroll
+    for (int i = 0; i < MT; i++) a[i] = ldg2(ap + ((size_t)i * KT2 + kt2) * 64);
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+      const double* bk = bp + (kt2 * 8 + h * 4) * lda;
+      double b[NT];
+#pragma unroll
+      for (int j = 0; j < NT; j++) b[j] = bk[ncol[j]];
+#pragma unroll
+      for (int i = 0; i < MT; i++)
+#pragma unroll
+        for (int j = 0; j < NT; j++) dmma(acc[i][j], h ? a[i].y : a[i].x, b[j]);
+    }
+  }
+}
+
+template <class C>
+__global__ void __launch_bounds__(C::NTHR, 2) fused_kernel(AsmArgs A) {
+  constexpr int W = C::W, Q = C::Q, NEN = C::NEN, NQ = C::NQ, E = C::E;
+  constexpr int LDA = C::LDA, LDS = C::LDS, KT2 = C::KT2;
+  extern __shared__ __align__(16) double smem[];
+  const int L = A.ncm.L;
+  const Smem<C> sm(L);
+  double* act = smem + sm.act;
+  double* sb = smem + sm.sb;
+  double* cb = smem + sm.cb;
+  double* qF = smem + sm.qF;
+  double* qk = smem + sm.qk;
+  double* qg = smem + sm.qg;
+  double* qH = smem + sm.qH;
+  double* hred = smem + sm.hred;
+  double* gsk = smem + sm.gsk;
+  double* sgN = smem + sm.gN;
+  double* sue = smem + sm.ue;
+  double* swq = smem + sm.wq;
+  double* qA = smem + sm.qA;
+  double* qP = smem + sm.qP;
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+  const NcmDev& m = A.ncm;
+  const bool skips = m.skip_h != nullptr;
+  const int64_t n_batches = (A.el_count + E - 1) / E;
+  const size_t frag_layer = (size_t)2 * W * W;  // W and W^T fragments per hidden layer
+
+  for (int64_t batch = blockIdx.x; batch < n_batches; batch += gridDim.x) {
+    const int64_t e0 = A.el_begin + batch * E;
+    const int64_t rem = A.el_begin + A.el_count - e0;
+    const int ne = rem < E ? (int)rem : E;
+
+    // ---- stage 0: stage element inputs --------------------------------------------
+    {
+      const double2* src = reinterpret_cast<const double2*>(A.gradN + (size_t)e0 * NQ * NEN * 3);
+      double2* dst = reinterpret_cast<double2*>(sgN);
+      const int n2 = ne * NQ * NEN * 3 / 2;
+      for (int x = tid; x < E * NQ * NEN * 3 / 2; x += C::NTHR)
+        dst[x] = x < n2 ? __ldg(src + x) : make_double2(0.0, 0.0);
+      for (int x = tid; x < E * NEN * 3; x += C::NTHR) {
+        const int e = x / (NEN * 3), ai = x % (NEN * 3);
+        sue[x] = e < ne ? __ldg(A.u + 3 * (int64_t)__ldg(A.conn + (e0 + e) * NEN + ai / 3) + ai % 3) : 0.0;
+      }
+      for (int x = tid; x < Q; x += C::NTHR) swq[x] = x < ne * NQ ? __ldg(A.qp_w + e0 * NQ + x) : 0.0;
+    }
+    __syncthreads();
+
+    // ---- stage 1: kinematics ------------------------------------------------------
+    if (tid < Q) {
+      const int q = tid, e = q / NQ;
+      const double* gq = sgN + q * NEN * 3;
+      const double* ue = sue + e * NEN * 3;
+      double F[9];
+#pragma unroll
+      for (int i = 0; i < 3; i++)
+#pragma unroll
+        for (int J = 0; J < 3; J++) {
+          double s = (i == J) ? 1.0 : 0.0;
+#pragma unroll
+          for (int a = 0; a < NEN; a++) s += ue[a * 3 + i] * gq[a * 3 + J];
+          F[i * 3 + J] = s;
+        }
+      Kin kin;
+      kinematics(F, kin);
+      if (e < ne && !(kin.J > 0.0))
+        atomicMin(A.bad, (unsigned long long)(__ldg(A.orig + e0 + e) * NQ + q % NQ));
+#pragma unroll
+      for (int x = 0; x < 9; x++) qF[q * 9 + x] = F[x];
+      qk[q * 3 + 0] = kin.I1 - 3.0;
+      qk[q * 3 + 1] = kin.I2 - 3.0;
+      qk[q * 3 + 2] = kin.J - 1.0;
+      gsk[q * 3 + 0] = gsk[q * 3 + 1] = gsk[q * 3 + 2] = 0.0;
+    }
+    __syncthreads();
+
+    // ---- stage 2: layer 1 (3 -> W), elementwise -------------------------------------
+    for (int x = tid; x < W * Q; x += C::NTHR) {
+      const int j = x / Q, q = x % Q;
+      const double y = __ldg(m.b + j) + __ldg(m.W1 + j * 3 + 0) * qk[q * 3 + 0] +
+                       __ldg(m.W1 + j * 3 + 1) * qk[q * 3 + 1] + __ldg(m.W1 + j * 3 + 2) * qk[q * 3 + 2];
+      double z, s;
+      softplus3(y, z, s);
+      if (L > 1) {
+        sb[j * LDS + q] = s;
+        act[j * LDA + q] = z;
+      } else {
+        const double aj = __ldg(m.a + j);
+        act[j * LDA + q] = aj * s;
+        cb[j * LDS + q] = aj * s * (1.0 - s);
+      }
+    }
+    __syncthreads();
+
+    // ---- stage 3: value pass, layers 2..L --------------------------------------------
+    {
+      const int vm = warp / C::VNG, vn = warp % C::VNG;
+      const int mt0 = vm * C::MT_V;
+      int ncol[C::NT_V];
+#pragma unroll
+      for (int j = 0; j < C::NT_V; j++) ncol[j] = (vn * C::NT_V + j) * 8;
+      for (int l = 2; l <= L; l++) {
+        double acc[C::MT_V][C::NT_V][2];
+        warp_gemm<C::MT_V, C::NT_V, KT2>(m.Wfrag + (l - 2) * frag_layer, mt0, act, LDA, ncol, acc);
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < C::MT_V; i++) {
+          const int j = (mt0 + i) * 8 + g;
+          const double bj = __ldg(m.b + (l - 1) * W + j);
+          double B3[3] = {0, 0, 0};
+          if (skips) {
+            const double* Bl = m.skip_h + ((size_t)(l - 2) * W + j) * 3;
+            B3[0] = __ldg(Bl); B3[1] = __ldg(Bl + 1); B3[2] = __ldg(Bl + 2);
+          }
+          const double aj = (l == L) ? __ldg(m.a + j) : 0.0;
+#pragma unroll
+          for (int jj = 0; jj < C::NT_V; jj++)
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+              const int q = ncol[jj] + 2 * t + h;
+              double y = acc[i][jj][h] + bj;
+              if (skips) y += B3[0] * qk[q * 3] + B3[1] * qk[q * 3 + 1] + B3[2] * qk[q * 3 + 2];
+              double z, s;
+              softplus3(y, z, s);
+              if (l < L) {
+                sb[((l - 1) * W + j) * LDS + q] = s;
+                act[j * LDA + q] = z;
+              } else {
+                act[j * LDA + q] = aj * s;                                  // mu_L
+                cb[((l - 1) * W + j) * LDS + q] = aj * s * (1.0 - s);       // c_L
+              }
+            }
+        }
+        __syncthreads();
+      }
+    }
+
+    // ---- stage 4: adjoint pass, layers L..2 --------------------------------------------
+    {
+      const int vm = warp / C::VNG, vn = warp % C::VNG;
+      const int mt0 = vm * C::MT_V;
+      int ncol[C::NT_V];
+#pragma unroll
+      for (int j = 0; j < C::NT_V; j++) ncol[j] = (vn * C::NT_V + j) * 8;
+      for (int l = L; l >= 2; l--) {
+        if (skips && tid < Q) {  // g += B_l^T mu_l
+          const double* Bl = m.skip_h + (size_t)(l - 2) * W * 3;
+          double s0 = 0, s1 = 0, s2 = 0;
+          for (int j = 0; j < W; j++) {
+            const double mu = act[j * LDA + tid];
+            s0 += __ldg(Bl + j * 3) * mu; s1 += __ldg(Bl + j * 3 + 1) * mu; s2 += __ldg(Bl + j * 3 + 2) * mu;
+          }
+          gsk[tid * 3] += s0; gsk[tid * 3 + 1] += s1; gsk[tid * 3 + 2] += s2;
+        }
+        double acc[C::MT_V][C::NT_V][2];
+        warp_gemm<C::MT_V, C::NT_V, KT2>(m.Wfrag + (l - 2) * frag_layer + (size_t)W * W, mt0, act, LDA, ncol, acc);
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < C::MT_V; i++) {
+          const int j = (mt0 + i) * 8 + g;
+#pragma unroll
+          for (int jj = 0; jj < C::NT_V; jj++)
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+              const int q = ncol[jj] + 2 * t + h;
+              const double lam = acc[i][jj][h];
+              const double s = sb[((l - 2) * W + j) * LDS + q];
+              cb[((l - 2) * W + j) * LDS + q] = lam * s * (1.0 - s);
+              act[j * LDA + q] = lam * s;  // mu_{l-1}
+            }
+        }
+        __syncthreads();
+      }
+    }
+
+    // ---- stage 5: g = W1^T mu_1 + skips, H_1 = sum_j c1_j W1_j W1_j^T ------------------
+    {
+      constexpr int P = C::NTHR / Q;  // threads per qp (lanes q*P .. q*P+P-1 share a warp)
+      const int q = tid / P, part = tid % P;
+      double gs[3] = {0, 0, 0}, hs[6] = {0, 0, 0, 0, 0, 0};
+      for (int j = part; j < W; j += P) {
+        const double w0 = __ldg(m.W1 + j * 3), w1 = __ldg(m.W1 + j * 3 + 1), w2 = __ldg(m.W1 + j * 3 + 2);
+        const double mu = act[j * LDA + q], c = cb[j * LDS + q];
+        gs[0] += w0 * mu; gs[1] += w1 * mu; gs[2] += w2 * mu;
+        hs[0] += c * w0 * w0; hs[1] += c * w0 * w1; hs[2] += c * w0 * w2;
+        hs[3] += c * w1 * w1; hs[4] += c * w1 * w2; hs[5] += c * w2 * w2;
+      }
+#pragma unroll
+      for (int o = 1; o < P; o <<= 1) {
+#pragma unroll
+        for (int x = 0; x < 3; x++) gs[x] += __shfl_xor_sync(0xffffffffu, gs[x], o);
+#pragma unroll
+        for (int x = 0; x < 6; x++) hs[x] += __shfl_xor_sync(0xffffffffu, hs[x], o);
+      }
+      if (part == 0) {
+#pragma unroll
+        for (int x = 0; x < 3; x++) qg[q * 3 + x] = gs[x] + gsk[q * 3 + x] + __ldg(m.skip_out + x);
+#pragma unroll
+        for (int x = 0; x < 6; x++) qH[q * 6 + x] = hs[x];
+      }
+    }
+    __syncthreads();
+
+    // ---- stage 6: Jacobian pass, H += J_l^T diag(c_l) J_l -------------------------------
+    if (L > 1) {
+      for (int x = tid; x < W * Q; x += C::NTHR) {  // D_1 = s_1 (.) W1
+        const int j = x / Q, q = x % Q;
+        const double s = sb[j * LDS + q];
+#pragma unroll
+        for (int c = 0; c < 3; c++) act[j * LDA + c * Q + q] = s * __ldg(m.W1 + j * 3 + c);
+      }
+      __syncthreads();
+      const int jm = warp / C::QB, qb = warp % C::QB;
+      const int mt0 = jm * C::MT_J;
+      int ncol[3];
+#pragma unroll
+      for (int c = 0; c < 3; c++) ncol[c] = c * Q + qb * 8;
+      double hp[2][6];
+#pragma unroll
+      for (int h = 0; h < 2; h++)
+#pragma unroll
+        for (int x = 0; x < 6; x++) hp[h][x] = 0.0;
+      for (int l = 2; l <= L; l++) {
+        double acc[C::MT_J][3][2];
+        warp_gemm<C::MT_J, 3, KT2>(m.Wfrag + (l - 2) * frag_layer, mt0, act, LDA, ncol, acc);
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < C::MT_J; i++) {
+          const int j = (mt0 + i) * 8 + g;
+          double B3[3] = {0, 0, 0};
+          if (skips) {
+            const double* Bl = m.skip_h + ((size_t)(l - 2) * W + j) * 3;
+            B3[0] = __ldg(Bl); B3[1] = __ldg(Bl + 1); B3[2] = __ldg(Bl + 2);
+          }
+#pragma unroll
+          for (int h = 0; h < 2; h++) {
+            const int q = qb * 8 + 2 * t + h;
+            const double J0 = acc[i][0][h] + B3[0], J1 = acc[i][1][h] + B3[1], J2 = acc[i][2][h] + B3[2];
+            const double c = cb[((l - 1) * W + j) * LDS + q];
+            const double c0 = c * J0, c1 = c * J1, c2 = c * J2;
+            hp[h][0] += c0 * J0; hp[h][1] += c0 * J1; hp[h][2] += c0 * J2;
+            hp[h][3] += c1 * J1; hp[h][4] += c1 * J2; hp[h][5] += c2 * J2;
+            if (l < L) {
+              const double s = sb[((l - 1) * W + j) * LDS + q];
+              act[j * LDA + q] = s * J0;
+              act[j * LDA + Q + q] = s * J1;
+              act[j * LDA + 2 * Q + q] = s * J2;
+            }
+          }
+        }
+        __syncthreads();
+      }
+      // reduce over the 8 row-groups g of the warp (lane bits 2..4)
+#pragma unroll
+      for (int h = 0; h < 2; h++)
+#pragma unroll
+        for (int x = 0; x < 6; x++) {
+          double v = hp[h][x];
+          v += __shfl_xor_sync(0xffffffffu, v, 4);
+          v += __shfl_xor_sync(0xffffffffu, v, 8);
+          v += __shfl_xor_sync(0xffffffffu, v, 16);
+          hp[h][x] = v;
+        }
+      if (g == 0) {
+#pragma unroll
+        for (int h = 0; h < 2; h++)
+#pragma unroll
+          for (int x = 0; x < 6; x++) hred[(jm * Q + qb * 8 + 2 * t + h) * 6 + x] = hp[h][x];
+      }
+      __syncthreads();
+    }
+
+    // ---- stage 7: penalty, S, P, A (scaled by w) ----------------------------------------
+    if (tid < Q) {
+      const int q = tid;
+      double gq[3], H6[6];
+#pragma unroll
+      for (int x = 0; x < 3; x++) gq[x] = qg[q * 3 + x];
+#pragma unroll
+      for (int x = 0; x < 6; x++) {
+        double s = qH[q * 6 + x];
+        if (L > 1)
+#pragma unroll
+          for (int r = 0; r < C::JMG; r++) s += hred[(r * Q + q) * 6 + x];
+        H6[x] = s;
+      }
+      Kin kin;
+      kinematics(qF + q * 9, kin);
+      gq[2] += 2.0 * m.kappa * (kin.J - 1.0) - m.ref_shift;
+      H6[5] += 2.0 * m.kappa;
+      double P[9], Am[81];
+      stress_tangent(kin, gq, H6, swq[q], P, Am);
+#pragma unroll
+      for (int x = 0; x < 81; x++) qA[q * 81 + x] = Am[x];
+#pragma unroll
+      for (int x = 0; x < 9; x++) qP[q * 9 + x] = P[x];
+    }
+    __syncthreads();
+
+    // ---- stage 8: element rows + coloured scatter -----------------------------------------
+    for (int row = tid; row < ne * NEN * 3; row += C::NTHR) {
+      const int e = row / (NEN * 3), ai = row % (NEN * 3), a = ai / 3, i = ai % 3;
+      double K[NEN * 3];
+#pragma unroll
+      for (int x = 0; x < NEN * 3; x++) K[x] = 0.0;
+      double rr = 0.0;
+#pragma unroll 1
+      for (int qq = 0; qq < NQ; qq++) {
+        const int q = e * NQ + qq;
+        const double* gq = sgN + q * NEN * 3;
+        const double ga0 = gq[a * 3], ga1 = gq[a * 3 + 1], ga2 = gq[a * 3 + 2];
+        const double* Ai = qA + q * 81 + i * 27;
+        double X[9];
+#pragma unroll
+        for (int kL = 0; kL < 9; kL++) X[kL] = ga0 * Ai[kL] + ga1 * Ai[9 + kL] + ga2 * Ai[18 + kL];
+        rr += qP[q * 9 + i * 3] * ga0 + qP[q * 9 + i * 3 + 1] * ga1 + qP[q * 9 + i * 3 + 2] * ga2;
+#pragma unroll
+        for (int b = 0; b < NEN; b++) {
+          const double gb0 = gq[b * 3], gb1 = gq[b * 3 + 1], gb2 = gq[b * 3 + 2];
+#pragma unroll
+          for (int k = 0; k < 3; k++) K[b * 3 + k] += X[k * 3] * gb0 + X[k * 3 + 1] * gb1 + X[k * 3 + 2] * gb2;
+        }
+      }
+      const int64_t el = e0 + e;
+      const int64_t ln = __ldg(A.lrow + el * NEN + a);
+      const bool own = ln < A.n_owned;
+      double* rb = own ? A.r_own : A.r_halo;
+      double* vb = own ? A.v_own : A.v_halo;
+      const int64_t rn = own ? ln : ln - A.n_owned;
+      const int deg = __ldg(A.node_deg + ln);
+      const int64_t row0 = __ldg(A.node_rs + ln) + (int64_t)i * 3 * deg;
+      rb[3 * rn + i] += rr;
+      const uint8_t* sl = A.slot + (size_t)el * NEN * NEN + a * NEN;
+#pragma unroll
+      for (int b = 0; b < NEN; b++) {
+        double* dst = vb + row0 + 3 * (int)__ldg(sl + b);
+        dst[0] += K[b * 3];
+        dst[1] += K[b * 3 + 1];
+        dst[2] += K[b * 3 + 2];
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host side: dispatch and weight fragments
+// ---------------------------------------------------------------------------
+static int q_for_width(int w) { return w <= 32 ? 32 : (w <= 64 ? 16 : 8); }
+
+int fused_supported(int n_en, int n_q, int w, int L) {
+  if (!((n_en == 8 && n_q == 8) || (n_en == 10 && n_q == 4))) return 0;
+  if (!(w == 8 || w == 16 || w == 32 || w == 64 || w == 128)) return 0;
+  if (L < 1 || L > kMaxLayers) return 0;
+  return 1;
+}
+
+int64_t fused_weight_frag_size(int w, int L) { return (int64_t)(L > 1 ? L - 1 : 1) * 2 * w * w; }
+
+// fragment (mt, kt2), lane (g,t), half h  <-  M[8 mt + g][8 kt2 + 4 h + t]
+void fused_weight_frag_fill(int w, int L, const double* Wrow, double* out) {
+  const int KT2 = w / 8;
+  for (int l = 0; l < L - 1; l++) {
+    const double* Wl = Wrow + (size_t)l * w * w;
+    double* fw = out + (size_t)l * 2 * w * w;
+    double* ft = fw + (size_t)w * w;
+    for (int mt = 0; mt < w / 8; mt++)
+      for (int kt2 = 0; kt2 < KT2; kt2++)
+        for (int lane = 0; lane < 32; lane++)
+          for (int h = 0; h < 2; h++) {
+            const int g = lane >> 2, t = lane & 3;
+            const int r = 8 * mt + g, c = 8 * kt2 + 4 * h + t;
+            const size_t o = ((size_t)(mt * KT2 + kt2) * 32 + lane) * 2 + h;
+            fw[o] = Wl[(size_t)r * w + c];   // W_l
+            ft[o] = Wl[(size_t)c * w + r];   // W_l^T
+          }
+  }
+}
+
+template <class C>
+static int launch_cfg(const AsmArgs& a, cudaStream_t st, int* launches) {
+  const Smem<C> sm(a.ncm.L);
+  const size_t bytes = (size_t)sm.total * sizeof(double);
+  static bool attr_set = false;
+  static size_t attr_bytes = 0;
+  if (!attr_set || attr_bytes < bytes) {
+    cudaError_t e = cudaFuncSetAttribute(fused_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e != cudaSuccess) return (int)e;
+    attr_set = true;
+    attr_bytes = bytes;
+  }
+  int dev = 0, sms = 148, per_sm = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fused_kernel<C>, C::NTHR, bytes);
+  if (per_sm < 1) per_sm = 1;
+  const int64_t nb = (a.el_count + C::E - 1) / C::E;
+  const int64_t grid = std::min<int64_t>(nb, (int64_t)sms * per_sm);
+  if (grid <= 0) return 0;
+  fused_kernel<C><<<(unsigned)grid, C::NTHR, bytes, st>>>(a);
+  if (launches) (*launches)++;
+  return (int)cudaGetLastError();
+}
+
+template <int NEN, int NQ>
+static int launch_et(const AsmArgs& a, cudaStream_t st, int* launches) {
+  switch (a.ncm.w) {
+    case 8: return launch_cfg<Cfg<8, 32, NEN, NQ>>(a, st, launches);
+    case 16: return launch_cfg<Cfg<16, 32, NEN, NQ>>(a, st, launches);
+    case 32: return launch_cfg<Cfg<32, 32, NEN, NQ>>(a, st, launches);
+    case 64: return launch_cfg<Cfg<64, 16, NEN, NQ>>(a, st, launches);
+    case 128: return launch_cfg<Cfg<128, 8, NEN, NQ>>(a, st, launches);
+  }
+  return (int)cudaErrorInvalidValue;
+}
+
+int launch_fused(const AsmArgs& a, void* stream, int* launches) {
+  if (a.el_count <= 0) return 0;
+  (void)q_for_width;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (a.n_en == 8) return launch_et<8, 8>(a, st, launches);
+  return launch_et<10, 4>(a, st, launches);
+}
+
+}  // namespace commet

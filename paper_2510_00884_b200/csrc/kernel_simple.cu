@@ -1,0 +1,148 @@
+// kernel_simple.cu -- one thread per element, Alg. 4 per
+// quadrature point in local memory, element matrix in local memory, coloured
+// read-modify-write scatter.  A deliberately straightforward CUDA variant
+// (COMMET_KERNEL_SIMPLE) kept as a second, algorithmically different GPU
+// implementation to cross-check the fused kernel; not the product path.
+#include <cuda_runtime.h>
+
+#include "commet_internal.h"
+#include "qp_math.cuh"
+
+namespace commet {
+
+constexpr int kMaxEn = 10;
+
+// Alg. 4 with 10 channels per neuron (value, 3 gradient, 6 Hessian) in place.
+__device__ static void ncm_alg4(const NcmDev& m, const double* kin, double* g, double* H6) {
+  double z[kMaxWidth], dz[kMaxWidth][3], d2z[kMaxWidth][6];
+  double zn[kMaxWidth], dzn[kMaxWidth][3], d2zn[kMaxWidth][6];
+  const int w = m.w;
+  // layer 1: y = W1 k + b1, dy = W1, d2y = 0
+  for (int j = 0; j < w; j++) {
+    double y = m.b[j];
+    for (int i = 0; i < 3; i++) y += m.W1[j * 3 + i] * kin[i];
+    double zz, s;
+    softplus3(y, zz, s);
+    const double s2 = s * (1.0 - s);
+    z[j] = zz;
+    double dy[3] = {m.W1[j * 3 + 0], m.W1[j * 3 + 1], m.W1[j * 3 + 2]};
+    for (int p = 0; p < 3; p++) dz[j][p] = s * dy[p];
+    int c = 0;
+    for (int p = 0; p < 3; p++)
+      for (int q = p; q < 3; q++) d2z[j][c++] = s2 * dy[p] * dy[q];
+  }
+  for (int l = 1; l < m.L; l++) {
+    const double* Wl = m.Wrow + (size_t)(l - 1) * w * w;
+    const double* Bl = m.skip_h ? m.skip_h + (size_t)(l - 1) * w * 3 : nullptr;
+    for (int j = 0; j < w; j++) {
+      double y = m.b[l * w + j], dy[3] = {0, 0, 0}, d2y[6] = {0, 0, 0, 0, 0, 0};
+      for (int i = 0; i < w; i++) {
+        const double a = Wl[j * w + i];
+        y += a * z[i];
+        for (int p = 0; p < 3; p++) dy[p] += a * dz[i][p];
+        for (int p = 0; p < 6; p++) d2y[p] += a * d2z[i][p];
+      }
+      if (Bl)
+        for (int p = 0; p < 3; p++) {
+          y += Bl[j * 3 + p] * kin[p];
+          dy[p] += Bl[j * 3 + p];
+        }
+      double zz, s;
+      softplus3(y, zz, s);
+      const double s2 = s * (1.0 - s);
+      zn[j] = zz;
+      for (int p = 0; p < 3; p++) dzn[j][p] = s * dy[p];
+      int c = 0;
+      for (int p = 0; p < 3; p++)
+        for (int q = p; q < 3; q++, c++) d2zn[j][c] = s * d2y[c] + s2 * dy[p] * dy[q];
+    }
+    for (int j = 0; j < w; j++) {
+      z[j] = zn[j];
+      for (int p = 0; p < 3; p++) dz[j][p] = dzn[j][p];
+      for (int p = 0; p < 6; p++) d2z[j][p] = d2zn[j][p];
+    }
+  }
+  for (int p = 0; p < 3; p++) g[p] = m.skip_out[p];
+  for (int p = 0; p < 6; p++) H6[p] = 0.0;
+  for (int j = 0; j < w; j++) {
+    for (int p = 0; p < 3; p++) g[p] += m.a[j] * dz[j][p];
+    for (int p = 0; p < 6; p++) H6[p] += m.a[j] * d2z[j][p];
+  }
+}
+
+__global__ void __launch_bounds__(64) simple_kernel(AsmArgs A) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= A.el_count) return;
+  const int64_t e = A.el_begin + t;
+  const int nen = A.n_en, nq = A.n_q, nd = 3 * nen;
+  double ue[kMaxEn * 3];
+  for (int a = 0; a < nen; a++) {
+    const int64_t node = A.conn[e * nen + a];
+    for (int i = 0; i < 3; i++) ue[a * 3 + i] = A.u[3 * node + i];
+  }
+  double Ke[kMaxEn * 3 * kMaxEn * 3];
+  double re[kMaxEn * 3];
+  for (int x = 0; x < nd * nd; x++) Ke[x] = 0.0;
+  for (int x = 0; x < nd; x++) re[x] = 0.0;
+  for (int q = 0; q < nq; q++) {
+    const double* gN = A.gradN + ((size_t)e * nq + q) * nen * 3;
+    const double w = A.qp_w[e * nq + q];
+    double F[9];
+    for (int i = 0; i < 3; i++)
+      for (int J = 0; J < 3; J++) {
+        double s = (i == J) ? 1.0 : 0.0;
+        for (int a = 0; a < nen; a++) s += ue[a * 3 + i] * gN[a * 3 + J];
+        F[i * 3 + J] = s;
+      }
+    Kin kin;
+    kinematics(F, kin);
+    if (!(kin.J > 0.0)) atomicMin(A.bad, (unsigned long long)(A.orig[e] * nq + q));
+    const double kv[3] = {kin.I1 - 3.0, kin.I2 - 3.0, kin.J - 1.0};
+    double g[3], H6[6];
+    ncm_alg4(A.ncm, kv, g, H6);
+    g[2] += 2.0 * A.ncm.kappa * (kin.J - 1.0) - A.ncm.ref_shift;
+    H6[5] += 2.0 * A.ncm.kappa;
+    double P[9], Am[81];
+    stress_tangent(kin, g, H6, w, P, Am);
+    for (int a = 0; a < nen; a++) {
+      const double* ga = gN + a * 3;
+      for (int i = 0; i < 3; i++) re[a * 3 + i] += P[i * 3 + 0] * ga[0] + P[i * 3 + 1] * ga[1] + P[i * 3 + 2] * ga[2];
+      for (int i = 0; i < 3; i++) {
+        double X[9];  // X[k*3+L] = sum_J gN_aJ A_iJkL
+        for (int kL = 0; kL < 9; kL++)
+          X[kL] = ga[0] * Am[(i * 3 + 0) * 9 + kL] + ga[1] * Am[(i * 3 + 1) * 9 + kL] + ga[2] * Am[(i * 3 + 2) * 9 + kL];
+        for (int b = 0; b < nen; b++) {
+          const double* gb = gN + b * 3;
+          for (int k = 0; k < 3; k++)
+            Ke[(a * 3 + i) * nd + b * 3 + k] += X[k * 3 + 0] * gb[0] + X[k * 3 + 1] * gb[1] + X[k * 3 + 2] * gb[2];
+        }
+      }
+    }
+  }
+  const uint8_t* sl = A.slot + (size_t)e * nen * nen;
+  for (int a = 0; a < nen; a++) {
+    const int64_t ln = A.lrow[e * nen + a];
+    const bool own = ln < A.n_owned;
+    double* rb = own ? A.r_own : A.r_halo;
+    double* vb = own ? A.v_own : A.v_halo;
+    const int64_t rn = own ? ln : ln - A.n_owned;
+    const int64_t rs = A.node_rs[ln];
+    const int deg = A.node_deg[ln];
+    for (int i = 0; i < 3; i++) {
+      rb[3 * rn + i] += re[a * 3 + i];
+      const int64_t row0 = rs + (int64_t)i * 3 * deg;
+      for (int b = 0; b < nen; b++)
+        for (int k = 0; k < 3; k++) vb[row0 + 3 * sl[a * nen + b] + k] += Ke[(a * 3 + i) * nd + b * 3 + k];
+    }
+  }
+}
+
+int launch_simple(const AsmArgs& a, void* stream) {
+  if (a.el_count <= 0) return 0;
+  const int bs = 64;
+  const int64_t grid = (a.el_count + bs - 1) / bs;
+  simple_kernel<<<(unsigned)grid, bs, 0, (cudaStream_t)stream>>>(a);
+  return (int)cudaGetLastError();
+}
+
+}  // namespace commet

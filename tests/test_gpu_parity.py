@@ -1,0 +1,111 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle,
+element by element, on the same seeded inputs.  Bar (BASELINE north_star):
+normwise relative error <= 1e-10 on residual and CSR values (R13),
+CSR row_ptr / col_idx bit-exact."""
+import numpy as np
+import pytest
+
+import oracle
+from synth import gen
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-10
+
+
+def _torch():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch
+
+
+def rel(g, o):
+    return np.abs(g - o).max() / max(np.abs(o).max(), 1e-300)
+
+
+def small_case(kind, n, w, L, skips=False, shift=False, jitter=0.1, amp=0.05, seed=3):
+    et = gen.HEX8 if kind == "hex" else gen.TET10
+    X, conn = gen.hex_mesh(n, jitter, seed) if kind == "hex" else gen.tet10_mesh(n, jitter, seed)
+    gN, qw = gen.shape_gradients(X, conn, et)
+    m = gen.ncm_weights(w, L, 0.3, seed + 1, 10.0)
+    if skips:
+        rng = np.random.default_rng(seed + 7)
+        m["skip_out"] = rng.normal(0, 0.3, 3)
+        m["skip_hidden"] = rng.normal(0, 0.3, (L - 1, w, 3))
+    if shift:
+        m["ref_shift"] = 0.123
+    u = gen.smooth_field(X, amp, np.random.default_rng(seed + 2)).reshape(-1)
+    return dict(elem_type=et, n_nodes=X.shape[0], conn=conn, gradN=gN, qp_w=qw, ncm=m, u=u, X=X)
+
+
+def run_gpu(case, kernel=None):
+    torch = _torch()
+    import paper_2510_00884_b200 as pc
+    lib = pc.from_config(case)
+    if kernel is not None:
+        lib.set_kernel(kernel)
+    u = torch.from_numpy(case["u"]).cuda()
+    r, v = lib.assemble(u)
+    torch.cuda.synchronize()
+    rp, ci = lib.pattern()
+    return lib, r.cpu().numpy(), v.cpu().numpy(), rp, ci
+
+
+def run_oracle(case):
+    rp, ci = oracle.pattern(case["n_nodes"], case["conn"])
+    r, v, bad = oracle.assemble(case["ncm"], case["n_nodes"], case["conn"], case["gradN"],
+                                case["qp_w"], case["u"], rp, ci)
+    return r, v, rp, ci, bad
+
+
+CASES = [
+    ("hex", 3, 8, 2, False, False),
+    ("hex", 3, 16, 2, False, False),
+    ("hex", 5, 32, 2, False, False),
+    ("hex", 5, 64, 3, False, False),
+    ("hex", 3, 128, 3, False, False),
+    ("hex", 3, 64, 1, False, False),
+    ("hex", 4, 64, 4, True, True),
+    ("tet", 2, 16, 2, False, False),
+    ("tet", 3, 64, 3, False, False),
+    ("tet", 2, 128, 3, True, False),
+    ("tet", 2, 32, 3, False, True),
+]
+
+
+@pytest.mark.parametrize("kind,n,w,L,skips,shift", CASES)
+@pytest.mark.parametrize("kernel", [0, 1])
+def test_parity_small(kind, n, w, L, skips, shift, kernel):
+    case = small_case(kind, n, w, L, skips, shift)
+    lib, r, v, rp, ci = run_gpu(case, kernel)
+    ro, vo, orp, oci, bad = run_oracle(case)
+    assert np.array_equal(rp, orp) and np.array_equal(ci, oci)
+    assert lib.check() == bad == -1
+    assert rel(r, ro) <= TOL, rel(r, ro)
+    assert rel(v, vo) <= TOL, rel(v, vo)
+
+
+@pytest.mark.parametrize("name", ["c1", "c2"])
+def test_parity_configs(name):
+    cfg = gen.make_config(name)
+    lib, r, v, rp, ci = run_gpu(cfg)
+    ro, vo, orp, oci, bad = run_oracle(cfg)
+    assert np.array_equal(rp, orp) and np.array_equal(ci, oci)
+    assert rel(r, ro) <= TOL and rel(v, vo) <= TOL, (rel(r, ro), rel(v, vo))
+
+
+def test_domain_flag_matches_oracle():
+    case = small_case("hex", 2, 16, 2, jitter=0.0)
+    case["u"] = case["u"].copy()
+    case["u"][3 * 13] += 0.9
+    lib, r, v, rp, ci = run_gpu(case)
+    ro, vo, _, _, bad = run_oracle(case)
+    assert bad >= 0 and lib.check() == bad
+    assert rel(r, ro) <= TOL and rel(v, vo) <= TOL
+
+
+def test_deterministic():
+    case = small_case("hex", 4, 64, 3)
+    _, r1, v1, _, _ = run_gpu(case)
+    _, r2, v2, _, _ = run_gpu(case)
+    assert np.array_equal(r1, r2) and np.array_equal(v1, v2)
