@@ -63,15 +63,18 @@ struct Cfg {
   static_assert(JMG >= 1 && JMG * QB == NWARP && MT_J * JMG == MTILES, "jacobian tiling");
 };
 
-// shared-memory carve-up (doubles); L is a runtime value
+// shared-memory carve-up (doubles); L is a runtime value.  The post-NCM
+// buffers (qP, post/X, qA) alias act/s/c, which are dead after stage 6.
 template <class C>
 struct Smem {
-  int act, sb, cb, qF, qk, qg, qH, hred, gsk, gN, ue, wq, qA, qP, total;
+  static constexpr int PS = 101;  // per-qp stride of the stage-7a outputs (odd: bank spread)
+  int act, sb, cb, qF, qk, qg, qH, hred, gsk, gN, ue, wq, tab, qP, post, X, qA, total;
   __host__ __device__ Smem(int L) {
     int o = 0;
     act = o; o += C::W * C::LDA;
     sb = o;  o += (L > 1 ? L - 1 : 0) * C::W * C::LDS;
     cb = o;  o += L * C::W * C::LDS;
+    const int dead = o;
     qF = o;  o += C::Q * 9;
     qk = o;  o += C::Q * 3;
     qg = o;  o += C::Q * 3;
@@ -81,15 +84,15 @@ struct Smem {
     gN = o;  o += C::Q * C::NEN * 3;
     ue = o;  o += C::E * C::NEN * 3;
     wq = o;  o += C::Q;
+    tab = o; o += kActTabSize;
     o = (o + 1) & ~1;
-    // post-NCM per-qp outputs alias act/s/c (dead after stage 6) when they fit
-    if (qF >= C::Q * 90) {
-      qA = 0;
-    } else {
-      qA = o;
-      o += C::Q * 90;
-    }
-    qP = qA + C::Q * 81;
+    const int px = C::Q * PS > C::Q * C::NEN * 27 ? C::Q * PS : C::Q * C::NEN * 27;
+    const int need = C::Q * 9 + px + C::Q * 81;
+    int base = 0;
+    if (need > dead) { base = o; o += need; }
+    qP = base;
+    post = X = base + C::Q * 9;
+    qA = post + px;
     total = o;
   }
 };
@@ -107,11 +110,16 @@ __device__ __forceinline__ void warp_gemm(const double* __restrict__ Af, int mt0
     for (int j = 0; j < NT; j++) acc[i][j][0] = acc[i][j][1] = 0.0;
   const double* ap = Af + (size_t)mt0 * KT2 * 64 + lane * 2;
   const double* bp = act + t * lda + g;
-#pragma unroll 4
-  for (int kt2 = 0; kt2 < KT2; kt2++) {
-    double2 a[MT];
+  double2 a[2][MT];
 #pragma unroll
-    for (int i = 0; i < MT; i++) a[i] = ldg2(ap + ((size_t)i * KT2 + kt2) * 64);
+  for (int i = 0; i < MT; i++) a[0][i] = ldg2(ap + (size_t)i * KT2 * 64);
+#pragma unroll
+  for (int kt2 = 0; kt2 < KT2; kt2++) {
+    const int cur = kt2 & 1;
+    if (kt2 + 1 < KT2) {
+#pragma unroll
+      for (int i = 0; i < MT; i++) a[cur ^ 1][i] = ldg2(ap + ((size_t)i * KT2 + kt2 + 1) * 64);
+    }
 #pragma unroll
     for (int h = 0; h < 2; h++) {
       const double* bk = bp + (kt2 * 8 + h * 4) * lda;
@@ -121,7 +129,7 @@ __device__ __forceinline__ void warp_gemm(const double* __restrict__ Af, int mt0
 #pragma unroll
       for (int i = 0; i < MT; i++)
 #pragma unroll
-        for (int j = 0; j < NT; j++) dmma(acc[i][j], h ? a[i].y : a[i].x, b[j]);
+        for (int j = 0; j < NT; j++) dmma(acc[i][j], h ? a[cur][i].y : a[cur][i].x, b[j]);
     }
   }
 }
@@ -145,14 +153,20 @@ __global__ void __launch_bounds__(C::NTHR, 2) fused_kernel(AsmArgs A) {
   double* sgN = smem + sm.gN;
   double* sue = smem + sm.ue;
   double* swq = smem + sm.wq;
+  double* stab = smem + sm.tab;
   double* qA = smem + sm.qA;
   double* qP = smem + sm.qP;
+  double* post = smem + sm.post;
+  double* Xb = smem + sm.X;
+  constexpr int PS = Smem<C>::PS;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
   const NcmDev& m = A.ncm;
   const bool skips = m.skip_h != nullptr;
   const int64_t n_batches = (A.el_count + E - 1) / E;
   const size_t frag_layer = (size_t)2 * W * W;  // W and W^T fragments per hidden layer
+  for (int x = threadIdx.x; x < kActTabSize; x += C::NTHR) stab[x] = __ldg(A.ncm.act_tab + x);
+  // (made visible by the first __syncthreads of the batch loop)
 
   for (int64_t batch = blockIdx.x; batch < n_batches; batch += gridDim.x) {
     const int64_t e0 = A.el_begin + batch * E;
@@ -208,7 +222,7 @@ __global__ void __launch_bounds__(C::NTHR, 2) fused_kernel(AsmArgs A) {
       const double y = __ldg(m.b + j) + __ldg(m.W1 + j * 3 + 0) * qk[q * 3 + 0] +
                        __ldg(m.W1 + j * 3 + 1) * qk[q * 3 + 1] + __ldg(m.W1 + j * 3 + 2) * qk[q * 3 + 2];
       double z, s;
-      softplus3(y, z, s);
+      softplus_sig(y, stab, z, s);
       if (L > 1) {
         sb[j * LDS + q] = s;
         act[j * LDA + q] = z;
@@ -249,7 +263,7 @@ __global__ void __launch_bounds__(C::NTHR, 2) fused_kernel(AsmArgs A) {
               double y = acc[i][jj][h] + bj;
               if (skips) y += B3[0] * qk[q * 3] + B3[1] * qk[q * 3 + 1] + B3[2] * qk[q * 3 + 2];
               double z, s;
-              softplus3(y, z, s);
+              softplus_sig(y, stab, z, s);
               if (l < L) {
                 sb[((l - 1) * W + j) * LDS + q] = s;
                 act[j * LDA + q] = z;
@@ -398,7 +412,7 @@ __global__ void __launch_bounds__(C::NTHR, 2) fused_kernel(AsmArgs A) {
       __syncthreads();
     }
 
-    // ---- stage 7: penalty, S, P, A (scaled by w) ----------------------------------------
+    // ---- stage 7a: per qp -- penalty, S, T, Phi_m, Psi_m, b, P (all scaled by w) --------
     if (tid < Q) {
       const int q = tid;
       double gq[3], H6[6];
@@ -416,55 +430,61 @@ __global__ void __launch_bounds__(C::NTHR, 2) fused_kernel(AsmArgs A) {
       kinematics(qF + q * 9, kin);
       gq[2] += 2.0 * m.kappa * (kin.J - 1.0) - m.ref_shift;
       H6[5] += 2.0 * m.kappa;
-      double P[9], Am[81];
-      stress_tangent(kin, gq, H6, swq[q], P, Am);
-#pragma unroll
-      for (int x = 0; x < 81; x++) qA[q * 81 + x] = Am[x];
-#pragma unroll
-      for (int x = 0; x < 9; x++) qP[q * 9 + x] = P[x];
+      post_qp(kin, gq, H6, swq[q], post + q * PS, qP + q * 9);
     }
     __syncthreads();
 
-    // ---- stage 8: element rows + coloured scatter -----------------------------------------
-    for (int row = tid; row < ne * NEN * 3; row += C::NTHR) {
-      const int e = row / (NEN * 3), ai = row % (NEN * 3), a = ai / 3, i = ai % 3;
-      double K[NEN * 3];
+    // ---- stage 7b: A_q (81 entries, scaled by w), one (q, iJ) row per item ------------------
+    for (int it = tid; it < Q * 9; it += C::NTHR) {
+      const int q = it / 9, iJ = it % 9;
+      tangent_row(post + q * PS, iJ, qA + q * 81 + iJ * 9);
+    }
+    __syncthreads();
+
+    // ---- stage 8a: X[q][a][i][kL] = sum_J dN_aJ A_q[iJ][kL] -----------------------------------
+    for (int it = tid; it < Q * 3 * NEN; it += C::NTHR) {
+      const int a = it % NEN, qi = it / NEN, i = qi % 3, q = qi / 3;
+      const double* ga = sgN + (q * NEN + a) * 3;
+      const double g0 = ga[0], g1 = ga[1], g2 = ga[2];
+      const double* Ai = qA + q * 81 + i * 27;
+      double* Xo = Xb + ((q * NEN + a) * 3 + i) * 9;
 #pragma unroll
-      for (int x = 0; x < NEN * 3; x++) K[x] = 0.0;
-      double rr = 0.0;
-#pragma unroll 1
+      for (int kL = 0; kL < 9; kL++) Xo[kL] = g0 * Ai[kL] + g1 * Ai[9 + kL] + g2 * Ai[18 + kL];
+    }
+    __syncthreads();
+
+    // ---- stage 8b: K_e[ai][bk] = sum_q sum_L X dN_bL, r_e; coloured RMW scatter ----------------
+    for (int it = tid; it < ne * NEN * 3 * NEN; it += C::NTHR) {
+      const int b = it % NEN, row = it / NEN, e = row / (NEN * 3), ai = row % (NEN * 3), a = ai / 3, i = ai % 3;
+      double K0 = 0.0, K1 = 0.0, K2 = 0.0, rr = 0.0;
+#pragma unroll
       for (int qq = 0; qq < NQ; qq++) {
         const int q = e * NQ + qq;
-        const double* gq = sgN + q * NEN * 3;
-        const double ga0 = gq[a * 3], ga1 = gq[a * 3 + 1], ga2 = gq[a * 3 + 2];
-        const double* Ai = qA + q * 81 + i * 27;
-        double X[9];
-#pragma unroll
-        for (int kL = 0; kL < 9; kL++) X[kL] = ga0 * Ai[kL] + ga1 * Ai[9 + kL] + ga2 * Ai[18 + kL];
-        rr += qP[q * 9 + i * 3] * ga0 + qP[q * 9 + i * 3 + 1] * ga1 + qP[q * 9 + i * 3 + 2] * ga2;
-#pragma unroll
-        for (int b = 0; b < NEN; b++) {
-          const double gb0 = gq[b * 3], gb1 = gq[b * 3 + 1], gb2 = gq[b * 3 + 2];
-#pragma unroll
-          for (int k = 0; k < 3; k++) K[b * 3 + k] += X[k * 3] * gb0 + X[k * 3 + 1] * gb1 + X[k * 3 + 2] * gb2;
+        const double* gb = sgN + (q * NEN + b) * 3;
+        const double h0 = gb[0], h1 = gb[1], h2 = gb[2];
+        const double* Xr = Xb + ((q * NEN + a) * 3 + i) * 9;
+        K0 += Xr[0] * h0 + Xr[1] * h1 + Xr[2] * h2;
+        K1 += Xr[3] * h0 + Xr[4] * h1 + Xr[5] * h2;
+        K2 += Xr[6] * h0 + Xr[7] * h1 + Xr[8] * h2;
+        if (b == 0) {
+          const double* ga = sgN + (q * NEN + a) * 3;
+          rr += qP[q * 9 + i * 3] * ga[0] + qP[q * 9 + i * 3 + 1] * ga[1] + qP[q * 9 + i * 3 + 2] * ga[2];
         }
       }
       const int64_t el = e0 + e;
       const int64_t ln = __ldg(A.lrow + el * NEN + a);
       const bool own = ln < A.n_owned;
-      double* rb = own ? A.r_own : A.r_halo;
       double* vb = own ? A.v_own : A.v_halo;
-      const int64_t rn = own ? ln : ln - A.n_owned;
       const int deg = __ldg(A.node_deg + ln);
       const int64_t row0 = __ldg(A.node_rs + ln) + (int64_t)i * 3 * deg;
-      rb[3 * rn + i] += rr;
-      const uint8_t* sl = A.slot + (size_t)el * NEN * NEN + a * NEN;
-#pragma unroll
-      for (int b = 0; b < NEN; b++) {
-        double* dst = vb + row0 + 3 * (int)__ldg(sl + b);
-        dst[0] += K[b * 3];
-        dst[1] += K[b * 3 + 1];
-        dst[2] += K[b * 3 + 2];
+      double* dst = vb + row0 + 3 * (int)__ldg(A.slot + ((size_t)el * NEN + a) * NEN + b);
+      dst[0] += K0;
+      dst[1] += K1;
+      dst[2] += K2;
+      if (b == 0) {
+        double* rb = own ? A.r_own : A.r_halo;
+        const int64_t rn = own ? ln : ln - A.n_owned;
+        rb[3 * rn + i] += rr;
       }
     }
     __syncthreads();

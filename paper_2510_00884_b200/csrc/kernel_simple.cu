@@ -22,7 +22,7 @@ __device__ static void ncm_alg4(const NcmDev& m, const double* kin, double* g, d
     double y = m.b[j];
     for (int i = 0; i < 3; i++) y += m.W1[j * 3 + i] * kin[i];
     double zz, s;
-    softplus3(y, zz, s);
+    softplus_sig(y, m.act_tab, zz, s);
     const double s2 = s * (1.0 - s);
     z[j] = zz;
     double dy[3] = {m.W1[j * 3 + 0], m.W1[j * 3 + 1], m.W1[j * 3 + 2]};
@@ -48,7 +48,7 @@ __device__ static void ncm_alg4(const NcmDev& m, const double* kin, double* g, d
           dy[p] += Bl[j * 3 + p];
         }
       double zz, s;
-      softplus3(y, zz, s);
+      softplus_sig(y, m.act_tab, zz, s);
       const double s2 = s * (1.0 - s);
       zn[j] = zz;
       for (int p = 0; p < 3; p++) dzn[j][p] = s * dy[p];
@@ -135,6 +135,18 @@ __global__ void __launch_bounds__(64) simple_kernel(AsmArgs A) {
         for (int k = 0; k < 3; k++) vb[row0 + 3 * sl[a * nen + b] + k] += Ke[(a * 3 + i) * nd + b * 3 + k];
     }
   }
+}
+
+__global__ void activation_kernel(const double* __restrict__ y, double* __restrict__ z, double* __restrict__ s,
+                                  int64_t n, const double* __restrict__ tab) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) softplus_sig(y[i], tab, z[i], s[i]);
+}
+
+int launch_activation(const double* y, double* z, double* s, int64_t n, const double* tab, void* stream) {
+  if (n <= 0) return 0;
+  activation_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(y, z, s, n, tab);
+  return (int)cudaGetLastError();
 }
 
 int launch_simple(const AsmArgs& a, void* stream) {

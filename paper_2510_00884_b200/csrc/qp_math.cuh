@@ -13,6 +13,7 @@
 //  Phi_1 = F, Phi_2 = I1 F - F C, Phi_3 = J/2 F^-T,
 //  H' = H + diag(g2, 0, g3/J),  T = S - g3 J C^-1,  b = F F^T.
 #pragma once
+#include <cmath>
 #include <cstdint>
 
 namespace commet {
@@ -64,65 +65,56 @@ __device__ __forceinline__ void kinematics(const double* __restrict__ F, Kin& k)
   k.I2 = 0.5 * (k.I1 * k.I1 - trC2);
 }
 
-// g[3] = dW/dk, H[6] = d2W/dk2 (upper: 00,01,02,11,12,22), penalty included.
-// Outputs P[9] = F S and A[81] (A[(i*3+J)*9 + k*3+L]), both scaled by w.
-__device__ __forceinline__ void stress_tangent(const Kin& k, const double* __restrict__ g,
-                                               const double* __restrict__ H6, double w,
-                                               double* __restrict__ P, double* __restrict__ A) {
+// Per-qp part of the tangent: from g[3] = dW/dk and H[6] = d2W/dk2 (upper
+// 00,01,02,11,12,22; penalty included) and the weight w, writes
+//   post[0..8] F, [9..17] F^-T, [18..26] w T, [27..53] Phi_m, [54..80] Psi_m = 4w sum_n H'_mn Phi_n,
+//   [81..89] b = F F^T, [90] c2 = -2 g2 w, [91] c3 = -g3 J w;   P[9] = w F S.
+__device__ __forceinline__ void post_qp(const Kin& k, const double* __restrict__ g, const double* __restrict__ H6,
+                                        double w, double* __restrict__ post, double* __restrict__ P) {
   const double* F = k.F;
-  double S[9], T[9], Phi[3][9], Psi[3][9];
   const double hJ = 0.5 * k.J;
+  double S[9];
 #pragma unroll
   for (int I = 0; I < 3; I++)
 #pragma unroll
     for (int J = 0; J < 3; J++) {
       const double d = (I == J) ? 1.0 : 0.0;
       S[I * 3 + J] = 2.0 * (g[0] * d + g[1] * (k.I1 * d - k.C[I * 3 + J]) + g[2] * hJ * k.Ci[I * 3 + J]);
-      T[I * 3 + J] = S[I * 3 + J] - g[2] * k.J * k.Ci[I * 3 + J];
+      post[18 + I * 3 + J] = w * (S[I * 3 + J] - g[2] * k.J * k.Ci[I * 3 + J]);
     }
-  // Phi_1 = F, Phi_2 = I1 F - F C, Phi_3 = J/2 F^-T
+  double Phi[3][9];
 #pragma unroll
   for (int i = 0; i < 3; i++)
 #pragma unroll
     for (int J = 0; J < 3; J++) {
-      double FC = F[i * 3 + 0] * k.C[0 * 3 + J] + F[i * 3 + 1] * k.C[1 * 3 + J] + F[i * 3 + 2] * k.C[2 * 3 + J];
+      const double FC = F[i * 3 + 0] * k.C[0 * 3 + J] + F[i * 3 + 1] * k.C[1 * 3 + J] + F[i * 3 + 2] * k.C[2 * 3 + J];
       Phi[0][i * 3 + J] = F[i * 3 + J];
       Phi[1][i * 3 + J] = k.I1 * F[i * 3 + J] - FC;
       Phi[2][i * 3 + J] = hJ * k.FiT[i * 3 + J];
     }
-  // H' (symmetric) with the folded g2 and g3/J terms; Psi_m = 4 w sum_n H'_mn Phi_n
   double Hp[9];
   Hp[0] = H6[0] + g[1]; Hp[1] = H6[1]; Hp[2] = H6[2];
   Hp[3] = H6[1]; Hp[4] = H6[3]; Hp[5] = H6[4];
   Hp[6] = H6[2]; Hp[7] = H6[4]; Hp[8] = H6[5] + g[2] / k.J;
   const double w4 = 4.0 * w;
 #pragma unroll
-  for (int m = 0; m < 3; m++)
+  for (int x = 0; x < 9; x++) {
+    post[x] = F[x];
+    post[9 + x] = k.FiT[x];
+    post[27 + x] = Phi[0][x];
+    post[36 + x] = Phi[1][x];
+    post[45 + x] = Phi[2][x];
 #pragma unroll
-    for (int x = 0; x < 9; x++)
-      Psi[m][x] = w4 * (Hp[m * 3 + 0] * Phi[0][x] + Hp[m * 3 + 1] * Phi[1][x] + Hp[m * 3 + 2] * Phi[2][x]);
-  double b[9];
+    for (int m = 0; m < 3; m++)
+      post[54 + m * 9 + x] = w4 * (Hp[m * 3 + 0] * Phi[0][x] + Hp[m * 3 + 1] * Phi[1][x] + Hp[m * 3 + 2] * Phi[2][x]);
+  }
 #pragma unroll
   for (int i = 0; i < 3; i++)
 #pragma unroll
     for (int kk = 0; kk < 3; kk++)
-      b[i * 3 + kk] = F[i * 3 + 0] * F[kk * 3 + 0] + F[i * 3 + 1] * F[kk * 3 + 1] + F[i * 3 + 2] * F[kk * 3 + 2];
-  const double c2 = -2.0 * g[1] * w, c3 = -g[2] * k.J * w;
-#pragma unroll
-  for (int i = 0; i < 3; i++)
-#pragma unroll
-    for (int J = 0; J < 3; J++)
-#pragma unroll
-      for (int kk = 0; kk < 3; kk++)
-#pragma unroll
-        for (int L = 0; L < 3; L++) {
-          double v = Phi[0][i * 3 + J] * Psi[0][kk * 3 + L] + Phi[1][i * 3 + J] * Psi[1][kk * 3 + L] +
-                     Phi[2][i * 3 + J] * Psi[2][kk * 3 + L];
-          v += c2 * F[i * 3 + L] * F[kk * 3 + J] + c3 * k.FiT[i * 3 + L] * k.FiT[kk * 3 + J];
-          if (J == L) v += c2 * b[i * 3 + kk];
-          if (i == kk) v += w * T[J * 3 + L];
-          A[(i * 3 + J) * 9 + kk * 3 + L] = v;
-        }
+      post[81 + i * 3 + kk] = F[i * 3 + 0] * F[kk * 3 + 0] + F[i * 3 + 1] * F[kk * 3 + 1] + F[i * 3 + 2] * F[kk * 3 + 2];
+  post[90] = -2.0 * g[1] * w;
+  post[91] = -g[2] * k.J * w;
 #pragma unroll
   for (int i = 0; i < 3; i++)
 #pragma unroll
@@ -130,12 +122,87 @@ __device__ __forceinline__ void stress_tangent(const Kin& k, const double* __res
       P[i * 3 + J] = w * (F[i * 3 + 0] * S[0 * 3 + J] + F[i * 3 + 1] * S[1 * 3 + J] + F[i * 3 + 2] * S[2 * 3 + J]);
 }
 
-// softplus and its first two derivatives (stable forms, SURVEY s7 hard part 3)
-__device__ __forceinline__ void softplus3(double y, double& z, double& s) {
-  const double e = exp(-fabs(y));
-  const double inv = 1.0 / (1.0 + e);
-  z = fmax(y, 0.0) + log1p(e);
-  s = (y >= 0.0) ? inv : e * inv;
+// Row iJ of w A:  A_iJkL = 4 sum_m Phi_m,iJ Psi_m,kL / (4w) ... (see header), kL = 0..8
+__device__ __forceinline__ void tangent_row(const double* __restrict__ post, int iJ, double* __restrict__ out) {
+  const int i = iJ / 3, J = iJ % 3;
+  const double p0 = post[27 + iJ], p1 = post[36 + iJ], p2 = post[45 + iJ];
+  const double c2 = post[90], c3 = post[91];
+#pragma unroll
+  for (int kk = 0; kk < 3; kk++) {
+    const double FkJ = post[kk * 3 + J], GkJ = post[9 + kk * 3 + J];
+#pragma unroll
+    for (int L = 0; L < 3; L++) {
+      const int kL = kk * 3 + L;
+      double v = p0 * post[54 + kL] + p1 * post[63 + kL] + p2 * post[72 + kL];
+      v += c2 * post[i * 3 + L] * FkJ + c3 * post[9 + i * 3 + L] * GkJ;
+      if (J == L) v += c2 * post[81 + i * 3 + kk];
+      if (i == kk) v += post[18 + J * 3 + L];
+      out[kL] = v;
+    }
+  }
+}
+
+// Whole tangent of one qp (simple kernel): P[9] and A[81], both scaled by w.
+__device__ __forceinline__ void stress_tangent(const Kin& k, const double* __restrict__ g,
+                                               const double* __restrict__ H6, double w,
+                                               double* __restrict__ P, double* __restrict__ A) {
+  double post[92];
+  post_qp(k, g, H6, w, post, P);
+  for (int iJ = 0; iJ < 9; iJ++) tangent_row(post, iJ, A + iJ * 9);
+}
+
+// ---------------------------------------------------------------------------
+// softplus z = log(1 + e^y) and sigmoid s = softplus' (SURVEY s7 hard part 3),
+// branch-free, fp64 FMA + integer ops only (no MUFU, no F2I, no libdevice slow
+// paths).  e = exp(-|y|) by table (2^(j/64)) + degree-5 polynomial on
+// |r| <= ln2/128; log1p(e) by table (1/c_j, log c_j, c_j = 1 + j/64) + degree-7
+// log1p polynomial on |r2| <= 1/128 with the rounding of u = 1 + e corrected;
+// 1/u = invc / (1 + r2) by its 8-term series.  Relative error ~1e-16.
+// tab layout (kActTabSize doubles): [0,64) 2^(j/64); [64,129) invc_j; [129,194) -log(invc_j)
+constexpr int kActTabSize = 194;
+
+__device__ __forceinline__ void softplus_sig(double y, const double* __restrict__ tab, double& z, double& s) {
+  const double MAGIC = 6755399441055744.0;  // 1.5 * 2^52: round-to-integer by addition
+  const double x = fmax(-fabs(y), -708.0);
+  double kd = fma(x, 92.33248261689366, MAGIC);  // 64 / ln2
+  const int k = __double2loint(kd);
+  kd -= MAGIC;
+  double r = fma(kd, -0.010830424696249145, x);  // ln2/64 hi
+  r = fma(kd, -3.623510646634843e-19, r);        // ln2/64 lo
+  double p = fma(r, 1.0 / 120.0, 1.0 / 24.0);
+  p = fma(p, r, 1.0 / 6.0);
+  p = fma(p, r, 0.5);
+  p = fma(p, r, 1.0);
+  p = fma(p, r, 1.0);
+  double e = tab[k & 63] * p;
+  e = __hiloint2double(__double2hiint(e) + (k >> 6) * 1048576, __double2loint(e));  // * 2^(k >> 6)
+  const double u = 1.0 + e;
+  const int j = __double2loint(fma(e, 64.0, MAGIC));  // round(64 e) in [0, 64]
+  const double invc = tab[64 + j], logc = tab[129 + j];
+  const double r2 = fma(u, invc, -1.0);
+  double q = fma(r2, 1.0 / 7.0, -1.0 / 6.0);
+  q = fma(q, r2, 0.2);
+  q = fma(q, r2, -0.25);
+  q = fma(q, r2, 1.0 / 3.0);
+  q = fma(q, r2, -0.5);
+  const double r2s = r2 * r2;
+  const double lp = fma(q, r2s, r2);                 // log1p(r2)
+  const double d = e - (u - 1.0);                    // rounding error of u (exact)
+  z = fmax(y, 0.0) + (logc + fma(d, invc, lp));      // max(y,0) + log1p(e)
+  const double r4 = r2s * r2s;
+  const double v = (1.0 - r2) * (1.0 + r2s) * (1.0 + r4);  // 1/(1 + r2), error r2^8
+  const double iu = invc * v;                        // 1 / u
+  s = (y >= 0.0 ? 1.0 : e) * iu;
+}
+
+// host: fill the table (long double for the reference values)
+inline void fill_act_table(double* tab) {
+  for (int j = 0; j < 64; j++) tab[j] = (double)exp2l((long double)j / 64.0L);
+  for (int j = 0; j <= 64; j++) {
+    const double invc = (double)(1.0L / (1.0L + (long double)j / 64.0L));
+    tab[64 + j] = invc;
+    tab[129 + j] = (double)(-logl((long double)invc));
+  }
 }
 
 }  // namespace commet

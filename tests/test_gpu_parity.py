@@ -109,3 +109,22 @@ def test_deterministic():
     _, r1, v1, _, _ = run_gpu(case)
     _, r2, v2, _, _ = run_gpu(case)
     assert np.array_equal(r1, r2) and np.array_equal(v1, v2)
+
+
+def test_activation_table_accuracy():
+    """The fused kernel's branch-free softplus/sigmoid (qp_math.cuh) against
+    numpy's logaddexp / exp on a sweep of y, incl. the extremes."""
+    torch = _torch()
+    import paper_2510_00884_b200 as pc
+    rng = np.random.default_rng(0)
+    y = np.concatenate([np.linspace(-40, 40, 200001), rng.normal(0, 3, 100000), rng.uniform(-800, 800, 10000),
+                        np.array([0.0, -0.0, 1e-300, -1e-300, 708.0, -708.0, 750.0, -750.0, 1e-8, -1e-8])])
+    z, s = pc.activation(torch.from_numpy(y).cuda())
+    z, s = z.cpu().numpy(), s.cpu().numpy()
+    zr = np.logaddexp(0.0, y)
+    sr = np.where(y >= 0, 1.0 / (1.0 + np.exp(-np.abs(y))), np.exp(-np.abs(y)) / (1.0 + np.exp(-np.abs(y))))
+    mask = np.abs(y) < 700
+    assert np.max(np.abs(z - zr)[mask] / np.maximum(zr[mask], 1e-300)) < 1e-15
+    assert np.max(np.abs(s - sr)[mask] / np.maximum(sr[mask], 1e-300)) < 1e-15
+    assert np.max(np.abs(z - zr)) < 1e-300 + 1e-15 * np.abs(zr).max()
+    assert np.all(np.isfinite(z)) and np.all(np.isfinite(s))
