@@ -68,20 +68,6 @@ def dist_env():
     return ws, rank, local
 
 
-def slab_range(spec, n, P, r):
-    """Element layers and owned node range of z-slab r of P."""
-    k0, k1 = r * n // P, (r + 1) * n // P
-    if spec.elem_type == gen.HEX8:
-        m = n + 1
-        nb = k0 * m * m
-        ne = (k1 if r < P - 1 else n + 1) * m * m
-    else:
-        bounds = gen.tet10_plane_bounds(n)
-        nb = int(bounds[2 * k0])
-        ne = int(bounds[2 * k1]) if r < P - 1 else int(bounds[-1])
-    return (k0, k1), (nb, ne)
-
-
 class Clocks:
     """nvidia-smi sampler running during the timed region."""
 
@@ -214,22 +200,13 @@ def main():
     import paper_2510_00884_b200 as pc
 
     spec = gen.CONFIGS[args.config]
-    n = spec.n
-    if ws > 1:
-        zr, (nb, ne) = slab_range(spec, n, ws, rank)
-        cfg = gen.make_config(args.config, z_range=zr)
-        owned = dict(owned_node_begin=nb, owned_node_end=ne)
-    else:
-        cfg = gen.make_config(args.config)
-        owned = {}
     comm = None
     if ws > 1:
+        cfg = gen.slab_partition(args.config, ws, rank)   # z-slab r of ws, with ghost layer
         comm = pc.nccl_comm_from_process_group(rank, ws, local)
-    mesh = dict(elem_type=cfg["elem_type"], n_nodes=cfg["n_nodes"], conn=cfg["conn"], gradN=cfg["gradN"],
-                qp_w=cfg["qp_w"], **owned)
-    if ws > 1:
-        mesh.update(pc.slab_ghosts(args.config, n, ws, rank))
-    lib = pc.Commet(mesh, cfg["ncm"], device=local, nccl_comm=comm)
+    else:
+        cfg = gen.make_config(args.config)
+    lib = pc.Commet(cfg, cfg["ncm"], device=local, nccl_comm=comm)
     if args.kernel == "simple":
         lib.set_kernel(pc.KERNEL_SIMPLE)
     n_el, n_q = cfg["conn"].shape[0], cfg["gradN"].shape[1]
@@ -324,6 +301,8 @@ def main():
         print(json.dumps(line), flush=True)
     if ws > 1:
         dist.barrier()
+        lib.close()
+        pc.nccl_comm_destroy(comm)
         dist.destroy_process_group()
     return 0
 

@@ -75,6 +75,13 @@ typedef struct {
   const double* qp_w;         /* host [n_elems][n_q]: Gauss weight * det(dX/dxi), > 0 */
   int64_t owned_node_begin;   /* rows owned by this rank: nodes [begin, end) */
   int64_t owned_node_end;     /* single GPU: [0, n_nodes) */
+  /* Partition (multi-GPU).  Single GPU: n_ranks = 0 or 1, the rest 0 / NULL. */
+  int32_t n_ranks;
+  int32_t rank;
+  const int64_t* rank_node_begin; /* host [n_ranks+1]: rank r owns nodes [rnb[r], rnb[r+1]) (ascending) */
+  int64_t n_ghost;            /* elements assembled by OTHER ranks that contain owned nodes */
+  const int32_t* ghost_conn;  /* host [n_ghost][n_en]: their connectivity (global node ids) */
+  const int32_t* ghost_rank;  /* host [n_ghost]: the rank that assembles each ghost element */
 } commet_mesh_desc;
 
 /* (M)ICNN inner network of Eq. icnn with softplus
@@ -101,8 +108,8 @@ enum { COMMET_KERNEL_FUSED = 0, COMMET_KERNEL_SIMPLE = 1 };
 /* Build the CSR pattern, element colouring and scatter maps, upload inputs.
  *   device     CUDA device ordinal
  *   cuda_stream  cudaStream_t for the uploads (NULL = legacy default stream)
- *   nccl_comm  ncclComm_t of the slab group, or NULL for a single GPU; with a
- *              comm, rank r must own the node range directly above rank r-1's.
+ *   nccl_comm  ncclComm_t of the partition (see commet_nccl_comm_init), or NULL
+ *              (single GPU, or caller-driven halo exchange)
  *   out        receives the context on success.
  * Errors: COMMET_ERR_ARG (bad sizes, node id out of range at element e,
  * w <= 0 at (e,q), unsupported width), COMMET_ERR_OOM, COMMET_ERR_CUDA. */
@@ -145,6 +152,59 @@ commet_status commet_set_timing(commet_ctx ctx, int32_t n_slots);
 /* Elapsed kernel milliseconds of the last n assembles (oldest first); n <=
  * min(n_slots, assembles so far).  Synchronises on the recorded events. */
 commet_status commet_kernel_times(commet_ctx ctx, float* ms_out, int32_t n);
+
+/* ---- multi-GPU ---------------------------------------------------------------
+ * A rank's elements may contain nodes owned by other ranks ("halo" rows).  Their
+ * contributions are accumulated in internal halo buffers laid out exactly like
+ * the owner expects (the owner derives the layout from its ghost elements), then
+ *  - with an NCCL comm (commet_setup's nccl_comm): commet_assemble sends each
+ *    halo segment to its owner (ncclSend/ncclRecv in one group, on the assemble
+ *    stream) and the owner adds what it receives into its rows (deterministic,
+ *    one unpack launch per sender in rank order);
+ *  - without a comm (n_ranks > 1, nccl_comm NULL): the caller moves the segments
+ *    (commet_halo_send / commet_halo_recv / commet_halo_unpack), e.g. to emulate
+ *    several ranks on one device.                                                */
+commet_status commet_nccl_unique_id(void* id128);
+commet_status commet_nccl_comm_init(const void* id128, int32_t n_ranks, int32_t rank, int device,
+                                    void** comm);
+commet_status commet_nccl_comm_destroy(void* comm);
+
+/* number of peers this rank sends halo segments to / receives from */
+commet_status commet_halo_info(commet_ctx ctx, int32_t* n_send, int32_t* n_recv);
+/* k-th send segment (device pointers into the ctx's halo buffers, valid after
+ * commet_assemble on its stream completes) */
+commet_status commet_halo_send(commet_ctx ctx, int32_t k, int32_t* peer, const double** vals,
+                               int64_t* n_vals, const double** residual, int64_t* n_res);
+/* size of the k-th receive segment */
+commet_status commet_halo_recv(commet_ctx ctx, int32_t k, int32_t* peer, int64_t* n_vals,
+                               int64_t* n_res);
+/* add a received segment (device arrays of the sizes above) into this rank's
+ * residual / csr_values; asynchronous on cuda_stream */
+commet_status commet_halo_unpack(commet_ctx ctx, int32_t k, const double* vals, const double* res,
+                                 double* residual, double* csr_values, void* cuda_stream);
+
+/* ---- host-only plan (no GPU needed): what commet_setup builds, for inspection --- */
+typedef struct commet_plan_s* commet_plan;
+commet_status commet_plan_create(const commet_mesh_desc* mesh, commet_plan* out);
+commet_status commet_plan_info(commet_plan p, int64_t* n_rows, int64_t* nnz, int64_t* n_halo_nodes,
+                               int64_t* nnz_halo, int32_t* n_colours, int32_t* n_send, int32_t* n_recv);
+/* host pointers owned by the plan */
+commet_status commet_plan_csr(commet_plan p, const int64_t** row_ptr, const int32_t** col_idx);
+commet_status commet_plan_halo(commet_plan p, const int64_t** halo_nodes, const int64_t** halo_row_ptr,
+                               const int32_t** halo_col_idx);
+commet_status commet_plan_send(commet_plan p, int32_t k, int32_t* peer, int64_t* val_begin,
+                               int64_t* val_end, int64_t* res_begin, int64_t* res_end);
+commet_status commet_plan_recv(commet_plan p, int32_t k, int32_t* peer, int64_t* n_vals,
+                               const int64_t** val_map, int64_t* n_res, const int64_t** res_map);
+commet_status commet_plan_colours(commet_plan p, const int64_t** colour_start, const int64_t** perm);
+void commet_plan_destroy(commet_plan p);
+
+/* Diagnostic: evaluates the kernels' activation on n device values y:
+ * z = softplus(y) = log(1+e^y), s = sigmoid(y) (device fp64 arrays).
+ * Asynchronous on cuda_stream.  Used by the tests to pin the table-driven
+ * softplus/sigmoid of the fused kernel on its own. */
+commet_status commet_selftest_activation(const double* y, double* z, double* s, int64_t n,
+                                         void* cuda_stream);
 
 const char* commet_last_error(commet_ctx ctx);
 void commet_destroy(commet_ctx ctx);

@@ -27,13 +27,19 @@ HEX8, TET10 = 0, 1
 KERNEL_FUSED, KERNEL_SIMPLE = 0, 1
 SYMBOLS = ("commet_setup", "commet_csr_pattern", "commet_csr_pattern_copy", "commet_assemble",
            "commet_check", "commet_set_kernel", "commet_info", "commet_set_timing",
-           "commet_kernel_times", "commet_last_error", "commet_destroy")
+           "commet_kernel_times", "commet_selftest_activation", "commet_last_error", "commet_destroy",
+           "commet_nccl_unique_id", "commet_nccl_comm_init", "commet_nccl_comm_destroy",
+           "commet_halo_info", "commet_halo_send", "commet_halo_recv", "commet_halo_unpack",
+           "commet_plan_create", "commet_plan_info", "commet_plan_csr", "commet_plan_halo",
+           "commet_plan_send", "commet_plan_recv", "commet_plan_colours", "commet_plan_destroy")
 
 
 class MeshDesc(C.Structure):
     _fields_ = [("elem_type", C.c_int32), ("n_nodes", C.c_int64), ("n_elems", C.c_int64),
                 ("conn", C.c_void_p), ("grad_N", C.c_void_p), ("qp_w", C.c_void_p),
-                ("owned_node_begin", C.c_int64), ("owned_node_end", C.c_int64)]
+                ("owned_node_begin", C.c_int64), ("owned_node_end", C.c_int64),
+                ("n_ranks", C.c_int32), ("rank", C.c_int32), ("rank_node_begin", C.c_void_p),
+                ("n_ghost", C.c_int64), ("ghost_conn", C.c_void_p), ("ghost_rank", C.c_void_p)]
 
 
 class NcmDesc(C.Structure):
@@ -61,6 +67,30 @@ _lib.commet_set_timing.argtypes = [_vp, _i32]
 _lib.commet_set_timing.restype = C.c_int
 _lib.commet_kernel_times.argtypes = [_vp, _vp, _i32]
 _lib.commet_kernel_times.restype = C.c_int
+_lib.commet_selftest_activation.argtypes = [_vp, _vp, _vp, _i64, _vp]
+_lib.commet_selftest_activation.restype = C.c_int
+_P = C.POINTER
+_lib.commet_nccl_unique_id.argtypes = [_vp]
+_lib.commet_nccl_comm_init.argtypes = [_vp, _i32, _i32, C.c_int, _P(_vp)]
+_lib.commet_nccl_comm_destroy.argtypes = [_vp]
+_lib.commet_halo_info.argtypes = [_vp, _P(_i32), _P(_i32)]
+_lib.commet_halo_send.argtypes = [_vp, _i32, _P(_i32), _P(_vp), _P(_i64), _P(_vp), _P(_i64)]
+_lib.commet_halo_recv.argtypes = [_vp, _i32, _P(_i32), _P(_i64), _P(_i64)]
+_lib.commet_halo_unpack.argtypes = [_vp, _i32, _vp, _vp, _vp, _vp, _vp]
+_lib.commet_plan_create.argtypes = [_P(MeshDesc), _P(_vp)]
+_lib.commet_plan_info.argtypes = [_vp, _P(_i64), _P(_i64), _P(_i64), _P(_i64), _P(_i32), _P(_i32), _P(_i32)]
+_lib.commet_plan_csr.argtypes = [_vp, _P(_vp), _P(_vp)]
+_lib.commet_plan_halo.argtypes = [_vp, _P(_vp), _P(_vp), _P(_vp)]
+_lib.commet_plan_send.argtypes = [_vp, _i32, _P(_i32), _P(_i64), _P(_i64), _P(_i64), _P(_i64)]
+_lib.commet_plan_recv.argtypes = [_vp, _i32, _P(_i32), _P(_i64), _P(_vp), _P(_i64), _P(_vp)]
+_lib.commet_plan_colours.argtypes = [_vp, _P(_vp), _P(_vp)]
+_lib.commet_plan_destroy.argtypes = [_vp]
+_lib.commet_plan_destroy.restype = None
+for _f in ("commet_nccl_unique_id", "commet_nccl_comm_init", "commet_nccl_comm_destroy", "commet_halo_info",
+           "commet_halo_send", "commet_halo_recv", "commet_halo_unpack", "commet_plan_create",
+           "commet_plan_info", "commet_plan_csr", "commet_plan_halo", "commet_plan_send", "commet_plan_recv",
+           "commet_plan_colours"):
+    getattr(_lib, _f).restype = C.c_int
 _lib.commet_last_error.argtypes = [_vp]
 _lib.commet_last_error.restype = C.c_char_p
 _lib.commet_destroy.argtypes = [_vp]
@@ -86,6 +116,24 @@ def _ptr(a):
     return None if a is None else a.ctypes.data
 
 
+def _mesh_desc(mesh: dict):
+    """-> (MeshDesc, keepalive list).  mesh keys: elem_type, n_nodes, conn, gradN, qp_w,
+    optional owned_node_begin/_end, n_ranks, rank, rank_node_begin, ghost_conn, ghost_rank."""
+    conn = np.ascontiguousarray(mesh["conn"], dtype=np.int32)
+    gradN = _f64(mesh["gradN"]) if mesh.get("gradN") is not None else np.zeros(1)
+    qp_w = _f64(mesh["qp_w"])
+    n_nodes = int(mesh["n_nodes"])
+    nb = int(mesh.get("owned_node_begin", 0))
+    ne = int(mesh.get("owned_node_end", n_nodes))
+    n_ranks = int(mesh.get("n_ranks", 1))
+    rnb = None if mesh.get("rank_node_begin") is None else np.ascontiguousarray(mesh["rank_node_begin"], np.int64)
+    gc = None if mesh.get("ghost_conn") is None else np.ascontiguousarray(mesh["ghost_conn"], np.int32)
+    gr = None if mesh.get("ghost_rank") is None else np.ascontiguousarray(mesh["ghost_rank"], np.int32)
+    md = MeshDesc(int(mesh["elem_type"]), n_nodes, conn.shape[0], _ptr(conn), _ptr(gradN), _ptr(qp_w), nb, ne,
+                  n_ranks, int(mesh.get("rank", 0)), _ptr(rnb), 0 if gc is None else gc.shape[0], _ptr(gc), _ptr(gr))
+    return md, [conn, gradN, qp_w, rnb, gc, gr]
+
+
 class Commet:
     """One library context: ``Commet(mesh, ncm).assemble(u) -> (r, vals)``.
 
@@ -99,14 +147,8 @@ class Commet:
         import torch
         self.torch = torch
         self.device = torch.device("cuda", device)
-        conn = np.ascontiguousarray(mesh["conn"], dtype=np.int32)
-        gradN = _f64(mesh["gradN"])
-        qp_w = _f64(mesh["qp_w"])
-        n_nodes = int(mesh["n_nodes"])
-        nb = int(mesh.get("owned_node_begin", 0))
-        ne = int(mesh.get("owned_node_end", n_nodes))
-        md = MeshDesc(int(mesh["elem_type"]), n_nodes, conn.shape[0], _ptr(conn), _ptr(gradN),
-                      _ptr(qp_w), nb, ne)
+        md, _keep = _mesh_desc(mesh)
+        n_nodes, nb, ne = md.n_nodes, md.owned_node_begin, md.owned_node_end
         arrs = {k: _f64(ncm.get(k)) for k in ("W1", "W", "b", "a", "skip_out", "skip_hidden")}
         if arrs["W"] is not None and arrs["W"].size == 0:
             arrs["W"] = None
@@ -178,6 +220,30 @@ class Commet:
         _check(_lib.commet_kernel_times(self.ctx, _ptr(out), n), self.ctx)
         return out
 
+    # -- caller-driven halo exchange (multi-rank without NCCL) --------------------------
+    def halo_info(self):
+        ns, nr = _i32(), _i32()
+        _check(_lib.commet_halo_info(self.ctx, C.byref(ns), C.byref(nr)), self.ctx)
+        return ns.value, nr.value
+
+    def halo_send(self, k: int):
+        """-> (peer, vals_ptr, n_vals, res_ptr, n_res) device pointers into this ctx."""
+        peer, vp, nv, rp, nr = _i32(), _vp(), _i64(), _vp(), _i64()
+        _check(_lib.commet_halo_send(self.ctx, k, C.byref(peer), C.byref(vp), C.byref(nv), C.byref(rp),
+                                     C.byref(nr)), self.ctx)
+        return peer.value, vp.value, nv.value, rp.value, nr.value
+
+    def halo_recv(self, k: int):
+        peer, nv, nr = _i32(), _i64(), _i64()
+        _check(_lib.commet_halo_recv(self.ctx, k, C.byref(peer), C.byref(nv), C.byref(nr)), self.ctx)
+        return peer.value, nv.value, nr.value
+
+    def halo_unpack(self, k: int, vals_ptr: int, res_ptr: int, residual, values, stream=None):
+        t = self.torch
+        st = stream if stream is not None else t.cuda.current_stream(self.device)
+        _check(_lib.commet_halo_unpack(self.ctx, k, vals_ptr, res_ptr, residual.data_ptr(), values.data_ptr(),
+                                       st.cuda_stream), self.ctx)
+
     def check(self) -> int:
         """-1 if every det F > 0, else the lowest flat e*n_q+q with det F <= 0."""
         bad = _i64()
@@ -196,6 +262,96 @@ class Commet:
             self.close()
         except Exception:
             pass
+
+
+class Plan:
+    """Host-only view of what commet_setup builds for a (rank-local) mesh: owned
+    CSR pattern, halo rows, colouring and the per-peer interface maps.  Needs
+    no GPU (used by the CPU tests of the multi-rank path)."""
+
+    def __init__(self, mesh: dict):
+        md, _keep = _mesh_desc(mesh)
+        h = _vp()
+        st = _lib.commet_plan_create(C.byref(md), C.byref(h))
+        if st != COMMET_OK:
+            raise CommetError(st, _lib.commet_last_error(None).decode())
+        self.h = h
+        v64 = [_i64() for _ in range(4)]
+        v32 = [_i32() for _ in range(3)]
+        _check(_lib.commet_plan_info(h, *[C.byref(x) for x in v64 + v32]))
+        self.n_rows, self.nnz, self.n_halo, self.nnz_halo = [x.value for x in v64]
+        self.n_colours, self.n_send, self.n_recv = [x.value for x in v32]
+
+    @staticmethod
+    def _arr(ptr, n, dt):
+        if n == 0:
+            return np.zeros(0, dt)
+        ct = {np.int64: C.c_int64, np.int32: C.c_int32}[dt]
+        return np.ctypeslib.as_array(C.cast(ptr, C.POINTER(ct)), shape=(n,)).copy()
+
+    def csr(self):
+        rp, ci = _vp(), _vp()
+        _check(_lib.commet_plan_csr(self.h, C.byref(rp), C.byref(ci)))
+        return self._arr(rp, self.n_rows + 1, np.int64), self._arr(ci, self.nnz, np.int32)
+
+    def halo(self):
+        hn, rp, ci = _vp(), _vp(), _vp()
+        _check(_lib.commet_plan_halo(self.h, C.byref(hn), C.byref(rp), C.byref(ci)))
+        return (self._arr(hn, self.n_halo, np.int64), self._arr(rp, 3 * self.n_halo + 1, np.int64),
+                self._arr(ci, self.nnz_halo, np.int32))
+
+    def send(self, k: int):
+        peer, v0, v1, r0, r1 = _i32(), _i64(), _i64(), _i64(), _i64()
+        _check(_lib.commet_plan_send(self.h, k, *[C.byref(x) for x in (peer, v0, v1, r0, r1)]))
+        return peer.value, (v0.value, v1.value), (r0.value, r1.value)
+
+    def recv(self, k: int):
+        peer, nv, vm, nr, rm = _i32(), _i64(), _vp(), _i64(), _vp()
+        _check(_lib.commet_plan_recv(self.h, k, *[C.byref(x) for x in (peer, nv, vm, nr, rm)]))
+        return peer.value, self._arr(vm, nv.value, np.int64), self._arr(rm, nr.value, np.int64)
+
+    def colours(self, n_el: int):
+        cs, pm = _vp(), _vp()
+        _check(_lib.commet_plan_colours(self.h, C.byref(cs), C.byref(pm)))
+        return self._arr(cs, self.n_colours + 1, np.int64), self._arr(pm, n_el, np.int64)
+
+    def __del__(self):
+        try:
+            _lib.commet_plan_destroy(self.h)
+        except Exception:
+            pass
+
+
+def nccl_comm_from_process_group(rank: int, world_size: int, device: int):
+    """ncclComm_t for the library: unique id from rank 0, broadcast over the
+    default torch.distributed process group (plumbing only)."""
+    import torch
+    import torch.distributed as dist
+    idb = (C.c_char * 128)()
+    if rank == 0:
+        _check(_lib.commet_nccl_unique_id(idb))
+    obj = [bytes(idb)]
+    dist.broadcast_object_list(obj, src=0)
+    idb = (C.c_char * 128).from_buffer_copy(obj[0])
+    comm = _vp()
+    with torch.cuda.device(device):
+        _check(_lib.commet_nccl_comm_init(idb, world_size, rank, device, C.byref(comm)))
+    return comm.value
+
+
+def nccl_comm_destroy(comm):
+    if comm:
+        _check(_lib.commet_nccl_comm_destroy(comm))
+
+
+def activation(y):
+    """The fused kernel's softplus and sigmoid on a cuda fp64 tensor (diagnostic)."""
+    import torch
+    y = y.contiguous()
+    z, s = torch.empty_like(y), torch.empty_like(y)
+    _check(_lib.commet_selftest_activation(y.data_ptr(), z.data_ptr(), s.data_ptr(), y.numel(),
+                                           torch.cuda.current_stream(y.device).cuda_stream))
+    return z, s
 
 
 def from_config(cfg: dict, device: int = 0, **kw) -> Commet:

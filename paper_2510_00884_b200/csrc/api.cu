@@ -1,8 +1,9 @@
-// api.cu -- the C ABI of libcommet (include/commet.h): setup (validation,
-// CSR pattern, element colouring, scatter slots, device uploads) and the
-// assemble orchestration (zeroing, one fused launch per colour, interface
-// exchange over NCCL for multi-GPU slabs).
+// api.cu -- the C ABI of libcommet (include/commet.h): setup (host plan from
+// plan.cpp, device uploads), the assemble orchestration (zeroing, one fused
+// launch per colour, halo exchange over NCCL for multi-GPU partitions) and
+// the host-only plan inspection calls.
 #include <cuda_runtime.h>
+#include <nccl.h>
 #include <omp.h>
 
 #include <algorithm>
@@ -16,6 +17,8 @@
 
 #include "commet.h"
 #include "commet_internal.h"
+#include "plan.h"
+#include "qp_math.cuh"
 
 using namespace commet;
 
@@ -38,22 +41,20 @@ struct DevBuf {
 
 struct commet_ctx_s {
   int device = 0;
-  int elem_type = 0, n_en = 0, n_q = 0;
-  int64_t n_nodes = 0, n_el = 0, node_begin = 0, node_end = 0, n_owned = 0, n_halo = 0;
-  int64_t n_rows = 0, nnz = 0, nnz_halo = 0;
-  int n_colours = 0;
-  std::vector<int64_t> colour_start;
+  Plan plan;  // host copy (pattern, maps); element-order arrays are dropped after upload
   int kernel = COMMET_KERNEL_FUSED;
   std::string err;
   cudaStream_t last_stream = nullptr;
+  ncclComm_t comm = nullptr;
   // device data
   DevBuf<int32_t> conn, lrow, col_idx;
   DevBuf<double> gradN, qp_w;
   DevBuf<uint8_t> slot;
   DevBuf<int64_t> orig, node_rs, row_ptr;
   DevBuf<int32_t> node_deg;
-  DevBuf<double> W1, b, a, skip_out, skip_h, Wrow, Wfrag;
-  DevBuf<double> r_halo, v_halo;
+  DevBuf<double> W1, b, a, skip_out, skip_h, Wrow, Wfrag, act_tab;
+  DevBuf<double> r_halo, v_halo, r_recv, v_recv;
+  DevBuf<int64_t> recv_val_map, recv_row_map;
   DevBuf<unsigned long long> bad;
   NcmDev ncm{};
   // timing ring
@@ -63,6 +64,10 @@ struct commet_ctx_s {
     for (auto e : ev0) cudaEventDestroy(e);
     for (auto e : ev1) cudaEventDestroy(e);
   }
+};
+
+struct commet_plan_s {
+  Plan p;
 };
 
 static commet_status fail(commet_ctx c, commet_status s, const char* fmt, ...) {
@@ -84,62 +89,19 @@ static commet_status fail(commet_ctx c, commet_status s, const char* fmt, ...) {
                   "CUDA error %s at %s:%d (%s)", cudaGetErrorString(e_), __FILE__, __LINE__, #x); \
   } while (0)
 
+#define NCCL_TRY(ctx, x)                                                                           \
+  do {                                                                                             \
+    ncclResult_t r_ = (x);                                                                         \
+    if (r_ != ncclSuccess)                                                                         \
+      return fail(ctx, COMMET_ERR_NCCL, "NCCL error %s at %s:%d (%s)", ncclGetErrorString(r_), __FILE__, \
+                  __LINE__, #x);                                                                   \
+  } while (0)
+
 template <class T>
 static commet_status upload(commet_ctx c, DevBuf<T>& d, const T* h, size_t n, cudaStream_t st) {
   CUDA_TRY(c, d.alloc(n));
   if (n) CUDA_TRY(c, cudaMemcpyAsync(d.p, h, n * sizeof(T), cudaMemcpyHostToDevice, st));
   return COMMET_OK;
-}
-
-// ---------------------------------------------------------------------------
-// pattern: per local row-node, sorted unique neighbour nodes
-// ---------------------------------------------------------------------------
-struct Adjacency {
-  std::vector<int64_t> ptr;   // [n_rownodes+1]
-  std::vector<int64_t> nbr;   // global node ids
-};
-
-// rows: local row-node of (e, a) ; neighbours: all nodes of e.
-static void build_adjacency(int64_t n_rownodes, int64_t n_el, int n_en, const int32_t* conn,
-                            const std::vector<int32_t>& lrow, Adjacency& adj) {
-  // incidence lists rownode -> elements (counting sort)
-  std::vector<int64_t> cnt(n_rownodes + 1, 0);
-  for (int64_t x = 0; x < n_el * n_en; x++) cnt[lrow[x] + 1]++;
-  for (int64_t v = 0; v < n_rownodes; v++) cnt[v + 1] += cnt[v];
-  std::vector<int64_t> inc(cnt[n_rownodes]);
-  {
-    std::vector<int64_t> pos(cnt.begin(), cnt.end() - 1);
-    for (int64_t x = 0; x < n_el * n_en; x++) inc[pos[lrow[x]]++] = x / n_en;
-  }
-  adj.ptr.assign(n_rownodes + 1, 0);
-  // two passes (count, fill) with a per-thread scratch vector
-#pragma omp parallel
-  {
-    std::vector<int64_t> tmp;
-#pragma omp for schedule(dynamic, 1024)
-    for (int64_t v = 0; v < n_rownodes; v++) {
-      tmp.clear();
-      for (int64_t p = cnt[v]; p < cnt[v + 1]; p++)
-        for (int b = 0; b < n_en; b++) tmp.push_back(conn[inc[p] * n_en + b]);
-      std::sort(tmp.begin(), tmp.end());
-      adj.ptr[v + 1] = std::unique(tmp.begin(), tmp.end()) - tmp.begin();
-    }
-  }
-  for (int64_t v = 0; v < n_rownodes; v++) adj.ptr[v + 1] += adj.ptr[v];
-  adj.nbr.resize(adj.ptr[n_rownodes]);
-#pragma omp parallel
-  {
-    std::vector<int64_t> tmp;
-#pragma omp for schedule(dynamic, 1024)
-    for (int64_t v = 0; v < n_rownodes; v++) {
-      tmp.clear();
-      for (int64_t p = cnt[v]; p < cnt[v + 1]; p++)
-        for (int b = 0; b < n_en; b++) tmp.push_back(conn[inc[p] * n_en + b]);
-      std::sort(tmp.begin(), tmp.end());
-      auto end = std::unique(tmp.begin(), tmp.end());
-      std::copy(tmp.begin(), end, adj.nbr.begin() + adj.ptr[v]);
-    }
-  }
 }
 
 // ---------------------------------------------------------------------------
@@ -152,158 +114,55 @@ extern "C" commet_status commet_setup(const commet_mesh_desc* mesh, const commet
   std::unique_ptr<commet_ctx_s> c(new (std::nothrow) commet_ctx_s());
   if (!c) return fail(nullptr, COMMET_ERR_OOM, "host allocation failed");
   commet_ctx C = c.get();
-  if (mesh->elem_type == COMMET_HEX8) { c->n_en = 8; c->n_q = 8; }
-  else if (mesh->elem_type == COMMET_TET10) { c->n_en = 10; c->n_q = 4; }
-  else return fail(C, COMMET_ERR_ARG, "elem_type %d unknown", mesh->elem_type);
-  c->elem_type = mesh->elem_type;
-  const int n_en = c->n_en, n_q = c->n_q;
-  if (mesh->n_nodes <= 0 || mesh->n_nodes > ((int64_t)1 << 31) / 3)
-    return fail(C, COMMET_ERR_ARG, "n_nodes %lld out of range (1 .. 2^31/3)", (long long)mesh->n_nodes);
-  if (mesh->n_elems < 0) return fail(C, COMMET_ERR_ARG, "n_elems %lld < 0", (long long)mesh->n_elems);
-  if (mesh->n_elems > 0 && (!mesh->conn || !mesh->grad_N || !mesh->qp_w))
-    return fail(C, COMMET_ERR_ARG, "conn, grad_N or qp_w is NULL");
-  if (mesh->owned_node_begin < 0 || mesh->owned_node_end > mesh->n_nodes ||
-      mesh->owned_node_begin > mesh->owned_node_end)
-    return fail(C, COMMET_ERR_ARG, "owned node range [%lld, %lld) invalid for n_nodes %lld",
-                (long long)mesh->owned_node_begin, (long long)mesh->owned_node_end, (long long)mesh->n_nodes);
+  // NCM arguments (host checks, before any CUDA call)
   const int L = ncm->n_hidden, w = ncm->width;
   if (L < 1 || L > kMaxLayers) return fail(C, COMMET_ERR_ARG, "n_hidden %d not in 1..%d", L, kMaxLayers);
-  if (!fused_supported(n_en, n_q, w, L))
+  const bool tet = mesh->elem_type == COMMET_TET10;
+  if (!fused_supported(tet ? 10 : 8, tet ? 4 : 8, w, L))
     return fail(C, COMMET_ERR_ARG, "width %d unsupported (8, 16, 32, 64 or 128)", w);
   if (!ncm->W1 || !ncm->b || !ncm->a || (L > 1 && !ncm->W))
     return fail(C, COMMET_ERR_ARG, "NCM weight pointer NULL (W1, b, a or W)");
-  c->n_nodes = mesh->n_nodes;
-  c->n_el = mesh->n_elems;
-  c->node_begin = mesh->owned_node_begin;
-  c->node_end = mesh->owned_node_end;
-  c->n_owned = c->node_end - c->node_begin;
+  Plan& p = c->plan;
+  {
+    std::string err;
+    commet_status s = plan_build(mesh, p, err);
+    if (s != COMMET_OK) return fail(C, s, "%s", err.c_str());
+  }
+  const int n_en = p.n_en, n_q = p.n_q;
+  const int64_t n_el = p.n_el;
   c->device = device;
-  const int64_t n_el = c->n_el;
-  const int32_t* conn = mesh->conn;
-  // ---- validation (host only, before any CUDA call) ----------------------------------
-  for (int64_t x = 0; x < n_el * n_en; x++)
-    if (conn[x] < 0 || conn[x] >= c->n_nodes)
-      return fail(C, COMMET_ERR_ARG, "conn[%lld][%d] = %d out of range [0, %lld)", (long long)(x / n_en),
-                  (int)(x % n_en), conn[x], (long long)c->n_nodes);
-  for (int64_t x = 0; x < n_el * n_q; x++)
-    if (!(mesh->qp_w[x] > 0.0))
-      return fail(C, COMMET_ERR_ARG, "qp_w[%lld][%d] = %g is not > 0", (long long)(x / n_q), (int)(x % n_q),
-                  mesh->qp_w[x]);
-
-  // ---- local row-nodes: owned [begin,end) then halo (sorted global ids) -----------------
-  std::vector<int64_t> halo;
-  for (int64_t x = 0; x < n_el * n_en; x++)
-    if (conn[x] < c->node_begin || conn[x] >= c->node_end) halo.push_back(conn[x]);
-  std::sort(halo.begin(), halo.end());
-  halo.erase(std::unique(halo.begin(), halo.end()), halo.end());
-  c->n_halo = (int64_t)halo.size();
-  if (c->n_halo)
-    return fail(C, COMMET_ERR_ARG, "%lld nodes referenced by conn are outside the owned range "
-                "(first: node %lld); multi-rank partitions need the NCCL path", (long long)c->n_halo, (long long)halo[0]);
-  (void)nccl_comm;
+  c->comm = (ncclComm_t)nccl_comm;
   CUDA_TRY(C, cudaSetDevice(device));
   cudaStream_t st = (cudaStream_t)cuda_stream;
-  const int64_t n_rn = c->n_owned + c->n_halo;
-  std::vector<int32_t> lrow(n_el * n_en);
-#pragma omp parallel for
-  for (int64_t x = 0; x < n_el * n_en; x++) {
-    int64_t v = conn[x];
-    lrow[x] = (v >= c->node_begin && v < c->node_end)
-                  ? (int32_t)(v - c->node_begin)
-                  : (int32_t)(c->n_owned + (std::lower_bound(halo.begin(), halo.end(), v) - halo.begin()));
-  }
 
-  // ---- adjacency of local rows; multi-GPU: merge neighbours' halo rows into owned rows --
-  Adjacency adj;
-  build_adjacency(n_rn, n_el, n_en, conn, lrow, adj);
-  for (int64_t v = 0; v < n_rn; v++)
-    if (adj.ptr[v + 1] - adj.ptr[v] > 255)
-      return fail(C, COMMET_ERR_ARG, "node row %lld has %lld neighbours (> 255)", (long long)v,
-                  (long long)(adj.ptr[v + 1] - adj.ptr[v]));
-
-  // ---- CSR of owned rows + halo rows ----------------------------------------------------
-  std::vector<int64_t> node_rs(n_rn);
-  std::vector<int32_t> node_deg(n_rn);
-  int64_t off = 0;
-  for (int64_t v = 0; v < n_rn; v++) {
-    if (v == c->n_owned) { c->nnz = off; off = 0; }
-    node_rs[v] = off;
-    node_deg[v] = (int32_t)(adj.ptr[v + 1] - adj.ptr[v]);
-    off += 9 * (int64_t)node_deg[v];
-  }
-  if (c->n_halo == 0) c->nnz = off; else c->nnz_halo = off;
-  if (n_rn == c->n_owned) c->nnz = off;
-  c->n_rows = 3 * c->n_owned;
-  std::vector<int64_t> row_ptr(c->n_rows + 1);
-  std::vector<int32_t> col_idx(c->nnz);
-#pragma omp parallel for schedule(dynamic, 1024)
-  for (int64_t v = 0; v < c->n_owned; v++) {
-    const int64_t d = node_deg[v];
-    for (int i = 0; i < 3; i++) {
-      const int64_t r0 = node_rs[v] + i * 3 * d;
-      row_ptr[3 * v + i] = r0;
-      for (int64_t p = 0; p < d; p++)
-        for (int k = 0; k < 3; k++) col_idx[r0 + 3 * p + k] = (int32_t)(3 * adj.nbr[adj.ptr[v] + p] + k);
-    }
-  }
-  row_ptr[c->n_rows] = c->nnz;
-
-  // ---- greedy element colouring, colour-sorted order -----------------------------------
-  std::vector<int32_t> colour(n_el);
+  // ---- per-element arrays in colour order -------------------------------------------------
   {
-    std::vector<uint64_t> used(n_rn, 0);
-    int nc = 0;
-    for (int64_t e = 0; e < n_el; e++) {
-      uint64_t mask = 0;
-      for (int a = 0; a < n_en; a++) mask |= used[lrow[e * n_en + a]];
-      int col = __builtin_ctzll(~mask);
-      if (mask == ~0ULL) return fail(C, COMMET_ERR_ARG, "element %lld needs more than 64 colours", (long long)e);
-      colour[e] = col;
-      nc = std::max(nc, col + 1);
-      for (int a = 0; a < n_en; a++) used[lrow[e * n_en + a]] |= 1ULL << col;
-    }
-    c->n_colours = nc;
-  }
-  std::vector<int64_t> perm(n_el);
-  c->colour_start.assign(c->n_colours + 1, 0);
-  for (int64_t e = 0; e < n_el; e++) c->colour_start[colour[e] + 1]++;
-  for (int k = 0; k < c->n_colours; k++) c->colour_start[k + 1] += c->colour_start[k];
-  {
-    std::vector<int64_t> pos(c->colour_start.begin(), c->colour_start.end() - 1);
-    for (int64_t e = 0; e < n_el; e++) perm[pos[colour[e]]++] = e;
-  }
-
-  // ---- per-element arrays in colour order ------------------------------------------------
-  std::vector<int32_t> conn_s(n_el * n_en), lrow_s(n_el * n_en);
-  std::vector<uint8_t> slot_s((size_t)n_el * n_en * n_en);
-  std::vector<double> w_s(n_el * n_q);
+    std::vector<int32_t> conn_s(n_el * n_en), lrow_s(n_el * n_en);
+    std::vector<double> w_s(n_el * n_q);
 #pragma omp parallel for schedule(static)
-  for (int64_t s = 0; s < n_el; s++) {
-    const int64_t e = perm[s];
-    for (int a = 0; a < n_en; a++) {
-      conn_s[s * n_en + a] = conn[e * n_en + a];
-      lrow_s[s * n_en + a] = lrow[e * n_en + a];
+    for (int64_t s = 0; s < n_el; s++) {
+      const int64_t e = p.perm[s];
+      for (int a = 0; a < n_en; a++) {
+        conn_s[s * n_en + a] = mesh->conn[e * n_en + a];
+        lrow_s[s * n_en + a] = p.lrow[e * n_en + a];
+      }
+      for (int q = 0; q < n_q; q++) w_s[s * n_q + q] = mesh->qp_w[e * n_q + q];
     }
-    for (int q = 0; q < n_q; q++) w_s[s * n_q + q] = mesh->qp_w[e * n_q + q];
-    for (int a = 0; a < n_en; a++) {
-      const int64_t v = lrow[e * n_en + a];
-      const int64_t* nb = adj.nbr.data() + adj.ptr[v];
-      const int64_t d = adj.ptr[v + 1] - adj.ptr[v];
-      for (int b = 0; b < n_en; b++)
-        slot_s[((size_t)s * n_en + a) * n_en + b] = (uint8_t)(std::lower_bound(nb, nb + d, (int64_t)conn[e * n_en + b]) - nb);
-    }
+    commet_status s;
+    if ((s = upload(C, c->conn, conn_s.data(), conn_s.size(), st))) return s;
+    if ((s = upload(C, c->lrow, lrow_s.data(), lrow_s.size(), st))) return s;
+    if ((s = upload(C, c->slot, p.slot.data(), p.slot.size(), st))) return s;
+    if ((s = upload(C, c->qp_w, w_s.data(), w_s.size(), st))) return s;
+    if ((s = upload(C, c->orig, p.perm.data(), p.perm.size(), st))) return s;
+    if ((s = upload(C, c->node_rs, p.node_rs.data(), p.node_rs.size(), st))) return s;
+    if ((s = upload(C, c->node_deg, p.node_deg.data(), p.node_deg.size(), st))) return s;
+    if ((s = upload(C, c->row_ptr, p.row_ptr.data(), p.row_ptr.size(), st))) return s;
+    if ((s = upload(C, c->col_idx, p.col_idx.data(), p.col_idx.size(), st))) return s;
+    if ((s = upload(C, c->recv_val_map, p.recv_val_map.data(), p.recv_val_map.size(), st))) return s;
+    if ((s = upload(C, c->recv_row_map, p.recv_row_map.data(), p.recv_row_map.size(), st))) return s;
+    CUDA_TRY(C, cudaStreamSynchronize(st));
   }
-  commet_status s;
-  if ((s = upload(C, c->conn, conn_s.data(), conn_s.size(), st))) return s;
-  if ((s = upload(C, c->lrow, lrow_s.data(), lrow_s.size(), st))) return s;
-  if ((s = upload(C, c->slot, slot_s.data(), slot_s.size(), st))) return s;
-  if ((s = upload(C, c->qp_w, w_s.data(), w_s.size(), st))) return s;
-  if ((s = upload(C, c->orig, perm.data(), perm.size(), st))) return s;
-  if ((s = upload(C, c->node_rs, node_rs.data(), node_rs.size(), st))) return s;
-  if ((s = upload(C, c->node_deg, node_deg.data(), node_deg.size(), st))) return s;
-  if ((s = upload(C, c->row_ptr, row_ptr.data(), row_ptr.size(), st))) return s;
-  if ((s = upload(C, c->col_idx, col_idx.data(), col_idx.size(), st))) return s;
-  // gradN: gather in colour order through a pinned staging buffer (inputs may be tens of GB)
+  // gradN: gather in colour order through pinned staging buffers (inputs may be tens of GB)
   {
     const size_t per = (size_t)n_q * n_en * 3;
     CUDA_TRY(C, c->gradN.alloc((size_t)n_el * per));
@@ -320,7 +179,7 @@ extern "C" commet_status commet_setup(const commet_mesh_desc* mesh, const commet
       CUDA_TRY(C, cudaEventSynchronize(ev[k]));
 #pragma omp parallel for schedule(static)
       for (int64_t x = 0; x < n; x++)
-        std::memcpy(stage[k] + x * per, mesh->grad_N + perm[s0 + x] * per, per * sizeof(double));
+        std::memcpy(stage[k] + x * per, mesh->grad_N + p.perm[s0 + x] * per, per * sizeof(double));
       CUDA_TRY(C, cudaMemcpyAsync(c->gradN.p + s0 * per, stage[k], n * per * sizeof(double),
                                   cudaMemcpyHostToDevice, st));
       CUDA_TRY(C, cudaEventRecord(ev[k], st));
@@ -332,7 +191,8 @@ extern "C" commet_status commet_setup(const commet_mesh_desc* mesh, const commet
     cudaEventDestroy(ev[1]);
   }
 
-  // ---- NCM -------------------------------------------------------------------------------
+  // ---- NCM ---------------------------------------------------------------------------------
+  commet_status s;
   std::vector<double> zeros3(3, 0.0);
   if ((s = upload(C, c->W1, ncm->W1, (size_t)w * 3, st))) return s;
   if ((s = upload(C, c->b, ncm->b, (size_t)L * w, st))) return s;
@@ -346,12 +206,57 @@ extern "C" commet_status commet_setup(const commet_mesh_desc* mesh, const commet
   std::vector<double> wf(fused_weight_frag_size(w, L), 0.0);
   fused_weight_frag_fill(w, L, wrow.data(), wf.data());
   if ((s = upload(C, c->Wfrag, wf.data(), wf.size(), st))) return s;
+  std::vector<double> tab(kActTabSize);
+  fill_act_table(tab.data());
+  if ((s = upload(C, c->act_tab, tab.data(), tab.size(), st))) return s;
   c->ncm = NcmDev{L, w, c->W1.p, c->b.p, c->a.p, c->skip_out.p, c->skip_h.p, c->Wrow.p, c->Wfrag.p,
-                  ncm->kappa, ncm->ref_shift};
+                  c->act_tab.p, ncm->kappa, ncm->ref_shift};
   CUDA_TRY(C, c->bad.alloc(1));
-  CUDA_TRY(C, c->r_halo.alloc(3 * c->n_halo));
-  CUDA_TRY(C, c->v_halo.alloc(c->nnz_halo));
+  CUDA_TRY(C, c->r_halo.alloc(3 * p.n_halo));
+  CUDA_TRY(C, c->v_halo.alloc(p.nnz_halo));
+  CUDA_TRY(C, c->r_recv.alloc(p.recv_row_map.size()));
+  CUDA_TRY(C, c->v_recv.alloc(p.recv_val_map.size()));
   CUDA_TRY(C, cudaStreamSynchronize(st));
+
+  // ---- NCCL: check that every sender's halo layout matches what this rank derived --------
+  if (c->comm && p.n_ranks > 1) {
+    int nr = 0, rk = 0;
+    NCCL_TRY(C, ncclCommCount(c->comm, &nr));
+    NCCL_TRY(C, ncclCommUserRank(c->comm, &rk));
+    if (nr != p.n_ranks || rk != p.rank)
+      return fail(C, COMMET_ERR_ARG, "NCCL comm is rank %d of %d, mesh says rank %d of %d", rk, nr, p.rank,
+                  p.n_ranks);
+    const size_t ns = p.send_rank.size(), nrv = p.recv_rank.size();
+    DevBuf<int64_t> sizes;
+    CUDA_TRY(C, sizes.alloc(2 * (ns + nrv) + 2));
+    std::vector<int64_t> h(2 * (ns + nrv) + 2, -1);
+    for (size_t k2 = 0; k2 < ns; k2++) {
+      h[2 * k2] = p.send_val_off[k2 + 1] - p.send_val_off[k2];
+      h[2 * k2 + 1] = p.send_row_off[k2 + 1] - p.send_row_off[k2];
+    }
+    CUDA_TRY(C, cudaMemcpy(sizes.p, h.data(), h.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
+    NCCL_TRY(C, ncclGroupStart());
+    for (size_t k2 = 0; k2 < ns; k2++)
+      NCCL_TRY(C, ncclSend(sizes.p + 2 * k2, 2, ncclInt64, p.send_rank[k2], c->comm, st));
+    for (size_t k2 = 0; k2 < nrv; k2++)
+      NCCL_TRY(C, ncclRecv(sizes.p + 2 * (ns + k2), 2, ncclInt64, p.recv_rank[k2], c->comm, st));
+    NCCL_TRY(C, ncclGroupEnd());
+    CUDA_TRY(C, cudaMemcpyAsync(h.data(), sizes.p, h.size() * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(C, cudaStreamSynchronize(st));
+    for (size_t k2 = 0; k2 < nrv; k2++) {
+      const int64_t nv = p.recv_val_off[k2 + 1] - p.recv_val_off[k2];
+      const int64_t nrr = p.recv_row_off[k2 + 1] - p.recv_row_off[k2];
+      if (h[2 * (ns + k2)] != nv || h[2 * (ns + k2) + 1] != nrr)
+        return fail(C, COMMET_ERR_ARG,
+                    "halo from rank %d has %lld values / %lld rows, this rank's ghost elements imply %lld / %lld "
+                    "(ghost_conn inconsistent with that rank's elements)",
+                    p.recv_rank[k2], (long long)h[2 * (ns + k2)], (long long)h[2 * (ns + k2) + 1], (long long)nv,
+                    (long long)nrr);
+    }
+  }
+  // element-order arrays live on the device now
+  std::vector<int32_t>().swap(p.lrow);
+  std::vector<uint8_t>().swap(p.slot);
   *out = c.release();
   return COMMET_OK;
 }
@@ -359,8 +264,8 @@ extern "C" commet_status commet_setup(const commet_mesh_desc* mesh, const commet
 extern "C" commet_status commet_csr_pattern(commet_ctx c, int64_t* n_rows, int64_t* nnz,
                                             const int64_t** row_ptr, const int32_t** col_idx) {
   if (!c) return fail(nullptr, COMMET_ERR_ARG, "ctx is NULL");
-  if (n_rows) *n_rows = c->n_rows;
-  if (nnz) *nnz = c->nnz;
+  if (n_rows) *n_rows = 3 * c->plan.n_owned;
+  if (nnz) *nnz = c->plan.nnz;
   if (row_ptr) *row_ptr = c->row_ptr.p;
   if (col_idx) *col_idx = c->col_idx.p;
   return COMMET_OK;
@@ -370,30 +275,42 @@ extern "C" commet_status commet_csr_pattern_copy(commet_ctx c, int64_t* row_ptr,
   if (!c) return fail(nullptr, COMMET_ERR_ARG, "ctx is NULL");
   CUDA_TRY(c, cudaSetDevice(c->device));
   if (row_ptr)
-    CUDA_TRY(c, cudaMemcpy(row_ptr, c->row_ptr.p, (c->n_rows + 1) * sizeof(int64_t), cudaMemcpyDefault));
-  if (col_idx && c->nnz)
-    CUDA_TRY(c, cudaMemcpy(col_idx, c->col_idx.p, c->nnz * sizeof(int32_t), cudaMemcpyDefault));
+    CUDA_TRY(c, cudaMemcpy(row_ptr, c->row_ptr.p, (3 * c->plan.n_owned + 1) * sizeof(int64_t), cudaMemcpyDefault));
+  if (col_idx && c->plan.nnz)
+    CUDA_TRY(c, cudaMemcpy(col_idx, c->col_idx.p, c->plan.nnz * sizeof(int32_t), cudaMemcpyDefault));
+  return COMMET_OK;
+}
+
+static commet_status unpack(commet_ctx c, int k, const double* vals, const double* res, double* residual,
+                            double* csr_values, cudaStream_t st) {
+  const Plan& p = c->plan;
+  const int64_t v0 = p.recv_val_off[k], v1 = p.recv_val_off[k + 1];
+  const int64_t r0 = p.recv_row_off[k], r1 = p.recv_row_off[k + 1];
+  int rc = launch_unpack(vals, c->recv_val_map.p + v0, v1 - v0, csr_values, res, c->recv_row_map.p + r0, r1 - r0,
+                         residual, st);
+  if (rc) return fail(c, COMMET_ERR_CUDA, "unpack kernel: %s", cudaGetErrorString((cudaError_t)rc));
   return COMMET_OK;
 }
 
 extern "C" commet_status commet_assemble(commet_ctx c, const double* u, double* residual,
                                          double* csr_values, void* cuda_stream) {
   if (!c) return fail(nullptr, COMMET_ERR_ARG, "ctx is NULL");
-  if (!u || (c->n_rows && !residual) || (c->nnz && !csr_values))
+  const Plan& p = c->plan;
+  if (!u || (p.n_owned && !residual) || (p.nnz && !csr_values))
     return fail(c, COMMET_ERR_ARG, "u, residual or csr_values is NULL");
   cudaStream_t st = (cudaStream_t)cuda_stream;
   c->last_stream = st;
   CUDA_TRY(c, cudaSetDevice(c->device));
-  CUDA_TRY(c, cudaMemsetAsync(residual, 0, c->n_rows * sizeof(double), st));
-  CUDA_TRY(c, cudaMemsetAsync(csr_values, 0, c->nnz * sizeof(double), st));
+  CUDA_TRY(c, cudaMemsetAsync(residual, 0, 3 * p.n_owned * sizeof(double), st));
+  CUDA_TRY(c, cudaMemsetAsync(csr_values, 0, p.nnz * sizeof(double), st));
   CUDA_TRY(c, cudaMemsetAsync(c->bad.p, 0xff, sizeof(unsigned long long), st));
-  if (c->n_halo) {
+  if (p.n_halo) {
     CUDA_TRY(c, cudaMemsetAsync(c->r_halo.p, 0, c->r_halo.n * sizeof(double), st));
     CUDA_TRY(c, cudaMemsetAsync(c->v_halo.p, 0, c->v_halo.n * sizeof(double), st));
   }
   AsmArgs a{};
-  a.n_en = c->n_en;
-  a.n_q = c->n_q;
+  a.n_en = p.n_en;
+  a.n_q = p.n_q;
   a.conn = c->conn.p;
   a.lrow = c->lrow.p;
   a.gradN = c->gradN.p;
@@ -402,7 +319,7 @@ extern "C" commet_status commet_assemble(commet_ctx c, const double* u, double* 
   a.orig = c->orig.p;
   a.node_rs = c->node_rs.p;
   a.node_deg = c->node_deg.p;
-  a.n_owned = c->n_owned;
+  a.n_owned = p.n_owned;
   a.u = u;
   a.r_own = residual;
   a.v_own = csr_values;
@@ -410,19 +327,38 @@ extern "C" commet_status commet_assemble(commet_ctx c, const double* u, double* 
   a.v_halo = c->v_halo.p;
   a.bad = c->bad.p;
   a.ncm = c->ncm;
-  // interface colours first (elements touching halo rows), so the exchange can
-  // overlap the interior colours -- with greedy colouring every colour may touch
-  // the interface, so here all colours run, then the exchange.
   const int slot = c->ev0.empty() ? -1 : (int)(c->n_assembled % (int64_t)c->ev0.size());
   if (slot >= 0) CUDA_TRY(c, cudaEventRecord(c->ev0[slot], st));
-  for (int k = 0; k < c->n_colours; k++) {
-    a.el_begin = c->colour_start[k];
-    a.el_count = c->colour_start[k + 1] - c->colour_start[k];
+  for (int k = 0; k < p.n_colours; k++) {
+    a.el_begin = p.colour_start[k];
+    a.el_count = p.colour_start[k + 1] - p.colour_start[k];
     int rc = c->kernel == COMMET_KERNEL_SIMPLE ? launch_simple(a, st) : launch_fused(a, st, nullptr);
     if (rc) return fail(c, COMMET_ERR_CUDA, "kernel launch (colour %d): %s", k, cudaGetErrorString((cudaError_t)rc));
   }
   if (slot >= 0) CUDA_TRY(c, cudaEventRecord(c->ev1[slot], st));
   c->n_assembled++;
+  // ---- halo exchange over NCCL: one group of point-to-point transfers, then unpack ----------
+  if (c->comm && p.n_ranks > 1 && (!p.send_rank.empty() || !p.recv_rank.empty())) {
+    NCCL_TRY(c, ncclGroupStart());
+    for (size_t k = 0; k < p.send_rank.size(); k++) {
+      const int64_t v0 = p.send_val_off[k], v1 = p.send_val_off[k + 1];
+      const int64_t r0 = p.send_row_off[k], r1 = p.send_row_off[k + 1];
+      NCCL_TRY(c, ncclSend(c->v_halo.p + v0, v1 - v0, ncclDouble, p.send_rank[k], c->comm, st));
+      NCCL_TRY(c, ncclSend(c->r_halo.p + r0, r1 - r0, ncclDouble, p.send_rank[k], c->comm, st));
+    }
+    for (size_t k = 0; k < p.recv_rank.size(); k++) {
+      const int64_t v0 = p.recv_val_off[k], v1 = p.recv_val_off[k + 1];
+      const int64_t r0 = p.recv_row_off[k], r1 = p.recv_row_off[k + 1];
+      NCCL_TRY(c, ncclRecv(c->v_recv.p + v0, v1 - v0, ncclDouble, p.recv_rank[k], c->comm, st));
+      NCCL_TRY(c, ncclRecv(c->r_recv.p + r0, r1 - r0, ncclDouble, p.recv_rank[k], c->comm, st));
+    }
+    NCCL_TRY(c, ncclGroupEnd());
+    for (size_t k = 0; k < p.recv_rank.size(); k++) {
+      commet_status s = unpack(c, (int)k, c->v_recv.p + p.recv_val_off[k], c->r_recv.p + p.recv_row_off[k],
+                               residual, csr_values, st);
+      if (s != COMMET_OK) return s;
+    }
+  }
   return COMMET_OK;
 }
 
@@ -449,13 +385,15 @@ extern "C" commet_status commet_set_kernel(commet_ctx c, int32_t variant) {
 extern "C" commet_status commet_info(commet_ctx c, int32_t* n_colours, int32_t* n_q, int32_t* n_en,
                                      int32_t* launches) {
   if (!c) return fail(nullptr, COMMET_ERR_ARG, "ctx is NULL");
-  if (n_colours) *n_colours = c->n_colours;
-  if (n_q) *n_q = c->n_q;
-  if (n_en) *n_en = c->n_en;
+  const Plan& p = c->plan;
+  if (n_colours) *n_colours = p.n_colours;
+  if (n_q) *n_q = p.n_q;
+  if (n_en) *n_en = p.n_en;
   if (launches) {
     int nonempty = 0;
-    for (int k = 0; k < c->n_colours; k++) nonempty += c->colour_start[k + 1] > c->colour_start[k];
-    *launches = nonempty;
+    for (int k = 0; k < p.n_colours; k++) nonempty += p.colour_start[k + 1] > p.colour_start[k];
+    const int unpacks = c->comm ? (int)p.recv_rank.size() : 0;
+    *launches = nonempty + unpacks;
   }
   return COMMET_OK;
 }
@@ -488,6 +426,168 @@ extern "C" commet_status commet_kernel_times(commet_ctx c, float* ms_out, int32_
     CUDA_TRY(c, cudaEventSynchronize(c->ev1[k]));
     CUDA_TRY(c, cudaEventElapsedTime(&ms_out[i], c->ev0[k], c->ev1[k]));
   }
+  return COMMET_OK;
+}
+
+// ---- NCCL helpers and caller-driven halo exchange -----------------------------------------
+extern "C" commet_status commet_nccl_unique_id(void* id128) {
+  if (!id128) return fail(nullptr, COMMET_ERR_ARG, "id is NULL");
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  NCCL_TRY(nullptr, ncclGetUniqueId(reinterpret_cast<ncclUniqueId*>(id128)));
+  return COMMET_OK;
+}
+
+extern "C" commet_status commet_nccl_comm_init(const void* id128, int32_t n_ranks, int32_t rank, int device,
+                                               void** comm) {
+  if (!id128 || !comm || n_ranks < 1 || rank < 0 || rank >= n_ranks)
+    return fail(nullptr, COMMET_ERR_ARG, "bad arguments (rank %d of %d)", rank, n_ranks);
+  CUDA_TRY(nullptr, cudaSetDevice(device));
+  ncclUniqueId id;
+  std::memcpy(&id, id128, sizeof id);
+  ncclComm_t cm = nullptr;
+  NCCL_TRY(nullptr, ncclCommInitRank(&cm, n_ranks, id, rank));
+  *comm = cm;
+  return COMMET_OK;
+}
+
+extern "C" commet_status commet_nccl_comm_destroy(void* comm) {
+  if (comm) NCCL_TRY(nullptr, ncclCommDestroy((ncclComm_t)comm));
+  return COMMET_OK;
+}
+
+extern "C" commet_status commet_halo_info(commet_ctx c, int32_t* n_send, int32_t* n_recv) {
+  if (!c) return fail(nullptr, COMMET_ERR_ARG, "ctx is NULL");
+  if (n_send) *n_send = (int32_t)c->plan.send_rank.size();
+  if (n_recv) *n_recv = (int32_t)c->plan.recv_rank.size();
+  return COMMET_OK;
+}
+
+extern "C" commet_status commet_halo_send(commet_ctx c, int32_t k, int32_t* peer, const double** vals,
+                                          int64_t* n_vals, const double** res, int64_t* n_res) {
+  if (!c) return fail(nullptr, COMMET_ERR_ARG, "ctx is NULL");
+  const Plan& p = c->plan;
+  if (k < 0 || k >= (int32_t)p.send_rank.size()) return fail(c, COMMET_ERR_ARG, "send segment %d does not exist", k);
+  if (peer) *peer = p.send_rank[k];
+  if (vals) *vals = c->v_halo.p + p.send_val_off[k];
+  if (n_vals) *n_vals = p.send_val_off[k + 1] - p.send_val_off[k];
+  if (res) *res = c->r_halo.p + p.send_row_off[k];
+  if (n_res) *n_res = p.send_row_off[k + 1] - p.send_row_off[k];
+  return COMMET_OK;
+}
+
+extern "C" commet_status commet_halo_recv(commet_ctx c, int32_t k, int32_t* peer, int64_t* n_vals, int64_t* n_res) {
+  if (!c) return fail(nullptr, COMMET_ERR_ARG, "ctx is NULL");
+  const Plan& p = c->plan;
+  if (k < 0 || k >= (int32_t)p.recv_rank.size()) return fail(c, COMMET_ERR_ARG, "recv segment %d does not exist", k);
+  if (peer) *peer = p.recv_rank[k];
+  if (n_vals) *n_vals = p.recv_val_off[k + 1] - p.recv_val_off[k];
+  if (n_res) *n_res = p.recv_row_off[k + 1] - p.recv_row_off[k];
+  return COMMET_OK;
+}
+
+extern "C" commet_status commet_halo_unpack(commet_ctx c, int32_t k, const double* vals, const double* res,
+                                            double* residual, double* csr_values, void* cuda_stream) {
+  if (!c) return fail(nullptr, COMMET_ERR_ARG, "ctx is NULL");
+  if (k < 0 || k >= (int32_t)c->plan.recv_rank.size())
+    return fail(c, COMMET_ERR_ARG, "recv segment %d does not exist", k);
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  return unpack(c, k, vals, res, residual, csr_values, (cudaStream_t)cuda_stream);
+}
+
+// ---- host-only plan -------------------------------------------------------------------------
+extern "C" commet_status commet_plan_create(const commet_mesh_desc* mesh, commet_plan* out) {
+  if (!out) return fail(nullptr, COMMET_ERR_ARG, "out is NULL");
+  *out = nullptr;
+  std::unique_ptr<commet_plan_s> p(new (std::nothrow) commet_plan_s());
+  if (!p) return fail(nullptr, COMMET_ERR_OOM, "host allocation failed");
+  std::string err;
+  commet_status s = plan_build(mesh, p->p, err);
+  if (s != COMMET_OK) return fail(nullptr, s, "%s", err.c_str());
+  *out = p.release();
+  return COMMET_OK;
+}
+
+extern "C" commet_status commet_plan_info(commet_plan pl, int64_t* n_rows, int64_t* nnz, int64_t* n_halo,
+                                          int64_t* nnz_halo, int32_t* n_colours, int32_t* n_send,
+                                          int32_t* n_recv) {
+  if (!pl) return fail(nullptr, COMMET_ERR_ARG, "plan is NULL");
+  const Plan& p = pl->p;
+  if (n_rows) *n_rows = 3 * p.n_owned;
+  if (nnz) *nnz = p.nnz;
+  if (n_halo) *n_halo = p.n_halo;
+  if (nnz_halo) *nnz_halo = p.nnz_halo;
+  if (n_colours) *n_colours = p.n_colours;
+  if (n_send) *n_send = (int32_t)p.send_rank.size();
+  if (n_recv) *n_recv = (int32_t)p.recv_rank.size();
+  return COMMET_OK;
+}
+
+extern "C" commet_status commet_plan_csr(commet_plan pl, const int64_t** row_ptr, const int32_t** col_idx) {
+  if (!pl) return fail(nullptr, COMMET_ERR_ARG, "plan is NULL");
+  if (row_ptr) *row_ptr = pl->p.row_ptr.data();
+  if (col_idx) *col_idx = pl->p.col_idx.data();
+  return COMMET_OK;
+}
+
+extern "C" commet_status commet_plan_halo(commet_plan pl, const int64_t** halo_nodes, const int64_t** halo_row_ptr,
+                                          const int32_t** halo_col_idx) {
+  if (!pl) return fail(nullptr, COMMET_ERR_ARG, "plan is NULL");
+  if (halo_nodes) *halo_nodes = pl->p.halo.data();
+  if (halo_row_ptr) *halo_row_ptr = pl->p.halo_row_ptr.data();
+  if (halo_col_idx) *halo_col_idx = pl->p.halo_col_idx.data();
+  return COMMET_OK;
+}
+
+extern "C" commet_status commet_plan_send(commet_plan pl, int32_t k, int32_t* peer, int64_t* val_begin,
+                                          int64_t* val_end, int64_t* res_begin, int64_t* res_end) {
+  if (!pl) return fail(nullptr, COMMET_ERR_ARG, "plan is NULL");
+  const Plan& p = pl->p;
+  if (k < 0 || k >= (int32_t)p.send_rank.size())
+    return fail(nullptr, COMMET_ERR_ARG, "send segment %d does not exist", k);
+  if (peer) *peer = p.send_rank[k];
+  if (val_begin) *val_begin = p.send_val_off[k];
+  if (val_end) *val_end = p.send_val_off[k + 1];
+  if (res_begin) *res_begin = p.send_row_off[k];
+  if (res_end) *res_end = p.send_row_off[k + 1];
+  return COMMET_OK;
+}
+
+extern "C" commet_status commet_plan_recv(commet_plan pl, int32_t k, int32_t* peer, int64_t* n_vals,
+                                          const int64_t** val_map, int64_t* n_res, const int64_t** res_map) {
+  if (!pl) return fail(nullptr, COMMET_ERR_ARG, "plan is NULL");
+  const Plan& p = pl->p;
+  if (k < 0 || k >= (int32_t)p.recv_rank.size())
+    return fail(nullptr, COMMET_ERR_ARG, "recv segment %d does not exist", k);
+  if (peer) *peer = p.recv_rank[k];
+  if (n_vals) *n_vals = p.recv_val_off[k + 1] - p.recv_val_off[k];
+  if (val_map) *val_map = p.recv_val_map.data() + p.recv_val_off[k];
+  if (n_res) *n_res = p.recv_row_off[k + 1] - p.recv_row_off[k];
+  if (res_map) *res_map = p.recv_row_map.data() + p.recv_row_off[k];
+  return COMMET_OK;
+}
+
+extern "C" commet_status commet_plan_colours(commet_plan pl, const int64_t** colour_start, const int64_t** perm) {
+  if (!pl) return fail(nullptr, COMMET_ERR_ARG, "plan is NULL");
+  if (colour_start) *colour_start = pl->p.colour_start.data();
+  if (perm) *perm = pl->p.perm.data();
+  return COMMET_OK;
+}
+
+extern "C" void commet_plan_destroy(commet_plan pl) { delete pl; }
+
+extern "C" commet_status commet_selftest_activation(const double* y, double* z, double* s, int64_t n,
+                                                    void* cuda_stream) {
+  if (n < 0 || (n && (!y || !z || !s)))
+    return fail(nullptr, COMMET_ERR_ARG, "bad arguments (n = %lld)", (long long)n);
+  static double* d_tab = nullptr;
+  if (!d_tab) {
+    double tab[kActTabSize];
+    fill_act_table(tab);
+    CUDA_TRY(nullptr, cudaMalloc(&d_tab, sizeof tab));
+    CUDA_TRY(nullptr, cudaMemcpy(d_tab, tab, sizeof tab, cudaMemcpyHostToDevice));
+  }
+  int rc = launch_activation(y, z, s, n, d_tab, cuda_stream);
+  if (rc) return fail(nullptr, COMMET_ERR_CUDA, "activation kernel: %s", cudaGetErrorString((cudaError_t)rc));
   return COMMET_OK;
 }
 

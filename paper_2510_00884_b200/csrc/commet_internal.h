@@ -28,6 +28,7 @@ struct NcmDev {
   const double* skip_h;   // [L-1][w][3] or nullptr
   const double* Wrow;     // [L-1][w][w] row-major (simple kernel)
   const double* Wfrag;    // [L-1][2][frag] fragment-ordered W and W^T (fused kernel)
+  const double* act_tab;  // [kActTabSize] softplus tables (qp_math.cuh)
   double kappa, ref_shift;
 };
 
@@ -54,6 +55,9 @@ struct AsmArgs {
 
 // launchers (kernel_simple.cu / kernel_fused.cu); return cudaError_t as int
 int launch_simple(const AsmArgs& a, void* stream);
+int launch_unpack(const double* vals, const int64_t* vmap, int64_t nv, double* csr, const double* res,
+                  const int64_t* rmap, int64_t nr, double* r, void* stream);
+int launch_activation(const double* y, double* z, double* s, int64_t n, const double* tab, void* stream);
 int launch_fused(const AsmArgs& a, void* stream, int* launches);
 int fused_supported(int n_en, int n_q, int w, int L);
 // prepares the fragment-ordered weight array on the host (size in doubles)

@@ -298,3 +298,50 @@ def element_colours_hex(n: int) -> np.ndarray:
     that want an independent structured 8-colouring."""
     k, j, i = np.meshgrid(np.arange(n), np.arange(n), np.arange(n), indexing="ij")
     return ((i % 2) + 2 * (j % 2) + 4 * (k % 2)).ravel()
+
+
+# --------------------------------------------------------------------------
+# z-slab partition (multi-GPU input preparation, DESIGN.md s7)
+# --------------------------------------------------------------------------
+def slab_layers(n: int, P: int, r: int):
+    if P > n:
+        raise ValueError(f"{P} slabs for {n} element layers")
+    return r * n // P, (r + 1) * n // P
+
+
+def rank_node_begin(elem_type: int, n: int, P: int) -> np.ndarray:
+    """Ownership boundaries: rank r owns the node planes of its element layers
+    (z-major numbering), the last rank also the top plane."""
+    out = np.zeros(P + 1, np.int64)
+    if elem_type == HEX8:
+        m = n + 1
+        for r in range(P):
+            out[r] = slab_layers(n, P, r)[0] * m * m
+        out[P] = m ** 3
+    else:
+        bounds = tet10_plane_bounds(n)
+        for r in range(P):
+            out[r] = bounds[2 * slab_layers(n, P, r)[0]]
+        out[P] = bounds[-1]
+    return out
+
+
+def slab_partition(name: str, P: int, r: int, n: int | None = None, with_gradients: bool = True) -> dict:
+    """Rank r's share of config `name` split into P z-slabs: its elements (with
+    dN/dX, w), its owned node range, the ownership table and its ghost elements
+    (the layer below, assembled by the rank beneath)."""
+    spec = CONFIGS[name]
+    n = spec.n if n is None else n
+    k0, k1 = slab_layers(n, P, r)
+    cfg = make_config(name, n=n, z_range=(k0, k1), with_gradients=with_gradients)
+    rnb = rank_node_begin(spec.elem_type, n, P)
+    cfg.update(n_ranks=P, rank=r, rank_node_begin=rnb, owned_node_begin=int(rnb[r]), owned_node_end=int(rnb[r + 1]))
+    if r > 0:
+        _, gconn = make_mesh(spec, n, (k0 - 1, k0))
+        below = [q for q in range(P) if slab_layers(n, P, q)[0] <= k0 - 1 < slab_layers(n, P, q)[1]][0]
+        cfg["ghost_conn"] = np.ascontiguousarray(gconn)
+        cfg["ghost_rank"] = np.full(gconn.shape[0], below, np.int32)
+    else:
+        cfg["ghost_conn"] = np.zeros((0, cfg["conn"].shape[1]), np.int32)
+        cfg["ghost_rank"] = np.zeros(0, np.int32)
+    return cfg
