@@ -181,7 +181,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="c3", choices=sorted(WORKLOAD))
+    ap.add_argument("--config", default="c5", choices=sorted(WORKLOAD))
     ap.add_argument("--impl", default="commet", choices=["commet", "reference"])
     ap.add_argument("--kernel", default="fused", choices=["fused", "simple"])
     ap.add_argument("--cpu-seconds", type=float, default=15.0)

@@ -47,6 +47,7 @@ template <int W_, int Q_, int NEN_, int NQ_>
 struct Cfg {
   static constexpr int W = W_, Q = Q_, NEN = NEN_, NQ = NQ_;
   static constexpr int NWARP = 4, NTHR = 128;
+  static constexpr int MINB = 3;                   // CTAs per SM the register budget targets (<= 168 regs)
   static constexpr int E = Q / NQ;                 // elements per CTA iteration
   static constexpr int MTILES = W / 8, QB = Q / 8, KT2 = W / 8;
   // value / adjoint warp tiles: VMG x VNG warps, each MT_V x NT_V tiles
@@ -57,10 +58,11 @@ struct Cfg {
   // Jacobian warp tiles: JMG m-groups x QB qp blocks, each MT_J x 3 tiles
   static constexpr int JMG = NWARP / QB, MT_J = MTILES / JMG;
   static constexpr int LDA = 3 * Q + 4;            // act row stride (= 4 mod 16: conflict-free B frags)
-  static constexpr int LDS = Q + 4;                // s/c row stride
+  static constexpr int LDS = Q + 2;                // s/c row stride (2-way conflicts at most)
   static_assert(W % 8 == 0 && Q % 8 == 0 && Q % NQ == 0, "tile");
   static_assert(TPW >= 1 && VMG * VNG == NWARP && MT_V * NT_V == TPW, "value tiling");
   static_assert(JMG >= 1 && JMG * QB == NWARP && MT_J * JMG == MTILES, "jacobian tiling");
+  static_assert(VMG * Q * 9 <= W * LDA, "adjoint partials must fit in act");
 };
 
 // shared-memory carve-up (doubles); L is a runtime value.  The post-NCM
@@ -72,14 +74,15 @@ struct Smem {
   __host__ __device__ Smem(int L) {
     int o = 0;
     act = o; o += C::W * C::LDA;
-    sb = o;  o += (L > 1 ? L - 1 : 0) * C::W * C::LDS;
-    cb = o;  o += L * C::W * C::LDS;
+    sb = o;  o += (L > 1 ? L - 1 : 0) * C::W * C::LDS;   // s_l, l = 1..L-1
+    cb = o;  o += (L > 1 ? L - 1 : 1) * C::W * C::LDS;   // c_l, l = 2..L (L == 1: c_1)
     const int dead = o;
     qF = o;  o += C::Q * 9;
     qk = o;  o += C::Q * 3;
     qg = o;  o += C::Q * 3;
     qH = o;  o += C::Q * 6;
-    hred = o; o += C::JMG * C::Q * 6;
+    hred = o; o += C::JMG * C::Q * 6;  // Jacobian-pass H partials per warp row group
+    // (the adjoint-pass g/H_1 partials, VMG x Q x 9, live in act: dead at that point)
     gsk = o; o += C::Q * 3;
     gN = o;  o += C::Q * C::NEN * 3;
     ue = o;  o += C::E * C::NEN * 3;
@@ -135,7 +138,7 @@ __device__ __forceinline__ void warp_gemm(const double* __restrict__ Af, int mt0
 }
 
 template <class C>
-__global__ void __launch_bounds__(C::NTHR, 2) fused_kernel(AsmArgs A) {
+__global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
   constexpr int W = C::W, Q = C::Q, NEN = C::NEN, NQ = C::NQ, E = C::E;
   constexpr int LDA = C::LDA, LDS = C::LDS, KT2 = C::KT2;
   extern __shared__ __align__(16) double smem[];
@@ -269,7 +272,7 @@ __global__ void __launch_bounds__(C::NTHR, 2) fused_kernel(AsmArgs A) {
                 act[j * LDA + q] = z;
               } else {
                 act[j * LDA + q] = aj * s;                                  // mu_L
-                cb[((l - 1) * W + j) * LDS + q] = aj * s * (1.0 - s);       // c_L
+                cb[((l - 2) * W + j) * LDS + q] = aj * s * (1.0 - s);       // c_L
               }
             }
         }
@@ -297,26 +300,92 @@ __global__ void __launch_bounds__(C::NTHR, 2) fused_kernel(AsmArgs A) {
         double acc[C::MT_V][C::NT_V][2];
         warp_gemm<C::MT_V, C::NT_V, KT2>(m.Wfrag + (l - 2) * frag_layer + (size_t)W * W, mt0, act, LDA, ncol, acc);
         __syncthreads();
+        if (l > 2) {
 #pragma unroll
-        for (int i = 0; i < C::MT_V; i++) {
-          const int j = (mt0 + i) * 8 + g;
+          for (int i = 0; i < C::MT_V; i++) {
+            const int j = (mt0 + i) * 8 + g;
+#pragma unroll
+            for (int jj = 0; jj < C::NT_V; jj++)
+#pragma unroll
+              for (int h = 0; h < 2; h++) {
+                const int q = ncol[jj] + 2 * t + h;
+                const double lam = acc[i][jj][h];
+                const double s = sb[((l - 2) * W + j) * LDS + q];
+                cb[((l - 3) * W + j) * LDS + q] = lam * s * (1.0 - s);  // c_{l-1}
+                act[j * LDA + q] = lam * s;                              // mu_{l-1}
+              }
+          }
+        } else {
+          // l == 2: lambda_1 -> mu_1, c_1 consumed here: g = W1^T mu_1, H_1 = W1^T diag(c_1) W1,
+          // partial over this thread's rows, reduced over the warp's row groups g
+          double pg[C::NT_V][2][9];
 #pragma unroll
           for (int jj = 0; jj < C::NT_V; jj++)
 #pragma unroll
-            for (int h = 0; h < 2; h++) {
-              const int q = ncol[jj] + 2 * t + h;
-              const double lam = acc[i][jj][h];
-              const double s = sb[((l - 2) * W + j) * LDS + q];
-              cb[((l - 2) * W + j) * LDS + q] = lam * s * (1.0 - s);
-              act[j * LDA + q] = lam * s;  // mu_{l-1}
-            }
+            for (int h = 0; h < 2; h++)
+#pragma unroll
+              for (int x = 0; x < 9; x++) pg[jj][h][x] = 0.0;
+#pragma unroll
+          for (int i = 0; i < C::MT_V; i++) {
+            const int j = (mt0 + i) * 8 + g;
+            const double w0 = __ldg(m.W1 + j * 3), w1 = __ldg(m.W1 + j * 3 + 1), w2 = __ldg(m.W1 + j * 3 + 2);
+#pragma unroll
+            for (int jj = 0; jj < C::NT_V; jj++)
+#pragma unroll
+              for (int h = 0; h < 2; h++) {
+                const int q = ncol[jj] + 2 * t + h;
+                const double lam = acc[i][jj][h];
+                const double s = sb[j * LDS + q];
+                const double mu = lam * s, c = mu * (1.0 - s);
+                double* P9 = pg[jj][h];
+                P9[0] += w0 * mu; P9[1] += w1 * mu; P9[2] += w2 * mu;
+                const double c0 = c * w0, c1 = c * w1;
+                P9[3] += c0 * w0; P9[4] += c0 * w1; P9[5] += c0 * w2;
+                P9[6] += c1 * w1; P9[7] += c1 * w2; P9[8] += c * w2 * w2;
+              }
+          }
+#pragma unroll
+          for (int jj = 0; jj < C::NT_V; jj++)
+#pragma unroll
+            for (int h = 0; h < 2; h++)
+#pragma unroll
+              for (int x = 0; x < 9; x++) {
+                double v = pg[jj][h][x];
+                v += __shfl_xor_sync(0xffffffffu, v, 4);
+                v += __shfl_xor_sync(0xffffffffu, v, 8);
+                v += __shfl_xor_sync(0xffffffffu, v, 16);
+                pg[jj][h][x] = v;
+              }
+          if (g == 0) {
+#pragma unroll
+            for (int jj = 0; jj < C::NT_V; jj++)
+#pragma unroll
+              for (int h = 0; h < 2; h++)
+#pragma unroll
+                for (int x = 0; x < 9; x++) act[(vm * Q + ncol[jj] + 2 * t + h) * 9 + x] = pg[jj][h][x];
+          }
         }
         __syncthreads();
       }
     }
 
     // ---- stage 5: g = W1^T mu_1 + skips, H_1 = sum_j c1_j W1_j W1_j^T ------------------
-    {
+    if (L > 1) {
+      if (tid < Q) {
+        const int q = tid;
+        double v[9];
+#pragma unroll
+        for (int x = 0; x < 9; x++) v[x] = 0.0;
+#pragma unroll
+        for (int r = 0; r < C::VMG; r++)
+#pragma unroll
+          for (int x = 0; x < 9; x++) v[x] += act[(r * Q + q) * 9 + x];
+#pragma unroll
+        for (int x = 0; x < 3; x++) qg[q * 3 + x] = v[x] + gsk[q * 3 + x] + __ldg(m.skip_out + x);
+#pragma unroll
+        for (int x = 0; x < 6; x++) qH[q * 6 + x] = v[3 + x];
+      }
+    } else {
       constexpr int P = C::NTHR / Q;  // threads per qp (lanes q*P .. q*P+P-1 share a warp)
       const int q = tid / P, part = tid % P;
       double gs[3] = {0, 0, 0}, hs[6] = {0, 0, 0, 0, 0, 0};
@@ -378,7 +447,7 @@ __global__ void __launch_bounds__(C::NTHR, 2) fused_kernel(AsmArgs A) {
           for (int h = 0; h < 2; h++) {
             const int q = qb * 8 + 2 * t + h;
             const double J0 = acc[i][0][h] + B3[0], J1 = acc[i][1][h] + B3[1], J2 = acc[i][2][h] + B3[2];
-            const double c = cb[((l - 1) * W + j) * LDS + q];
+            const double c = cb[((l - 2) * W + j) * LDS + q];
             const double c0 = c * J0, c1 = c * J1, c2 = c * J2;
             hp[h][0] += c0 * J0; hp[h][1] += c0 * J1; hp[h][2] += c0 * J2;
             hp[h][3] += c1 * J1; hp[h][4] += c1 * J2; hp[h][5] += c2 * J2;
@@ -477,14 +546,17 @@ __global__ void __launch_bounds__(C::NTHR, 2) fused_kernel(AsmArgs A) {
       double* vb = own ? A.v_own : A.v_halo;
       const int deg = __ldg(A.node_deg + ln);
       const int64_t row0 = __ldg(A.node_rs + ln) + (int64_t)i * 3 * deg;
+      // fire-and-forget RED.ADD.F64: the colouring makes the updates conflict-free (and the
+      // per-entry summation order deterministic: one update per colour launch); RED avoids the
+      // load round trip of a read-modify-write
       double* dst = vb + row0 + 3 * (int)__ldg(A.slot + ((size_t)el * NEN + a) * NEN + b);
-      dst[0] += K0;
-      dst[1] += K1;
-      dst[2] += K2;
+      atomicAdd(dst, K0);
+      atomicAdd(dst + 1, K1);
+      atomicAdd(dst + 2, K2);
       if (b == 0) {
         double* rb = own ? A.r_own : A.r_halo;
         const int64_t rn = own ? ln : ln - A.n_owned;
-        rb[3 * rn + i] += rr;
+        atomicAdd(rb + 3 * rn + i, rr);
       }
     }
     __syncthreads();
@@ -494,7 +566,6 @@ __global__ void __launch_bounds__(C::NTHR, 2) fused_kernel(AsmArgs A) {
 // ---------------------------------------------------------------------------
 // host side: dispatch and weight fragments
 // ---------------------------------------------------------------------------
-static int q_for_width(int w) { return w <= 32 ? 32 : (w <= 64 ? 16 : 8); }
 
 int fused_supported(int n_en, int n_q, int w, int L) {
   if (!((n_en == 8 && n_q == 8) || (n_en == 10 && n_q == 4))) return 0;
@@ -554,8 +625,8 @@ template <int NEN, int NQ>
 static int launch_et(const AsmArgs& a, cudaStream_t st, int* launches) {
   switch (a.ncm.w) {
     case 8: return launch_cfg<Cfg<8, 32, NEN, NQ>>(a, st, launches);
-    case 16: return launch_cfg<Cfg<16, 32, NEN, NQ>>(a, st, launches);
-    case 32: return launch_cfg<Cfg<32, 32, NEN, NQ>>(a, st, launches);
+    case 16: return launch_cfg<Cfg<16, 16, NEN, NQ>>(a, st, launches);
+    case 32: return launch_cfg<Cfg<32, 16, NEN, NQ>>(a, st, launches);
     case 64: return launch_cfg<Cfg<64, 16, NEN, NQ>>(a, st, launches);
     case 128: return launch_cfg<Cfg<128, 8, NEN, NQ>>(a, st, launches);
   }
@@ -564,7 +635,6 @@ static int launch_et(const AsmArgs& a, cudaStream_t st, int* launches) {
 
 int launch_fused(const AsmArgs& a, void* stream, int* launches) {
   if (a.el_count <= 0) return 0;
-  (void)q_for_width;
   cudaStream_t st = (cudaStream_t)stream;
   if (a.n_en == 8) return launch_et<8, 8>(a, st, launches);
   return launch_et<10, 4>(a, st, launches);
