@@ -52,7 +52,7 @@ struct commet_ctx_s {
   DevBuf<uint8_t> slot;
   DevBuf<int64_t> orig, node_rs, row_ptr;
   DevBuf<int32_t> node_deg;
-  DevBuf<double> W1, b, a, skip_out, skip_h, Wrow, Wfrag, act_tab;
+  DevBuf<double> W1, b, a, skip_out, skip_h, Wrow, Wfrag, act_tab, gfrag;
   DevBuf<double> r_halo, v_halo, r_recv, v_recv;
   DevBuf<int64_t> recv_val_map, recv_row_map;
   DevBuf<unsigned long long> bad;
@@ -209,8 +209,11 @@ extern "C" commet_status commet_setup(const commet_mesh_desc* mesh, const commet
   std::vector<double> tab(kActTabSize);
   fill_act_table(tab.data());
   if ((s = upload(C, c->act_tab, tab.data(), tab.size(), st))) return s;
+  std::vector<double> gf((size_t)2 * 16 * w);
+  fused_gfrag_fill(w, ncm->W1, gf.data());
+  if ((s = upload(C, c->gfrag, gf.data(), gf.size(), st))) return s;
   c->ncm = NcmDev{L, w, c->W1.p, c->b.p, c->a.p, c->skip_out.p, c->skip_h.p, c->Wrow.p, c->Wfrag.p,
-                  c->act_tab.p, ncm->kappa, ncm->ref_shift};
+                  c->act_tab.p, c->gfrag.p, ncm->kappa, ncm->ref_shift};
   CUDA_TRY(C, c->bad.alloc(1));
   CUDA_TRY(C, c->r_halo.alloc(3 * p.n_halo));
   CUDA_TRY(C, c->v_halo.alloc(p.nnz_halo));

@@ -29,6 +29,7 @@ struct NcmDev {
   const double* Wrow;     // [L-1][w][w] row-major (simple kernel)
   const double* Wfrag;    // [L-1][2][frag] fragment-ordered W and W^T (fused kernel)
   const double* act_tab;  // [kActTabSize] softplus tables (qp_math.cuh)
+  const double* gfrag;    // [2][16 x w] fragments of [W1^T | 0] and [0 | V] (stage 5)
   double kappa, ref_shift;
 };
 
@@ -63,5 +64,7 @@ int fused_supported(int n_en, int n_q, int w, int L);
 // prepares the fragment-ordered weight array on the host (size in doubles)
 int64_t fused_weight_frag_size(int w, int L);
 void fused_weight_frag_fill(int w, int L, const double* Wrow, double* out);
+// stage-5 fragments: 2 matrices of 16 x w (rows 0-2 W1^T; rows 3-8 W1_jm W1_jn)
+void fused_gfrag_fill(int w, const double* W1, double* out);
 
 }  // namespace commet

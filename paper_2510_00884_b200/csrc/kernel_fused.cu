@@ -62,7 +62,6 @@ struct Cfg {
   static_assert(W % 8 == 0 && Q % 8 == 0 && Q % NQ == 0, "tile");
   static_assert(TPW >= 1 && VMG * VNG == NWARP && MT_V * NT_V == TPW, "value tiling");
   static_assert(JMG >= 1 && JMG * QB == NWARP && MT_J * JMG == MTILES, "jacobian tiling");
-  static_assert(VMG * Q * 9 <= W * LDA, "adjoint partials must fit in act");
 };
 
 // shared-memory carve-up (doubles); L is a runtime value.  The post-NCM
@@ -75,7 +74,7 @@ struct Smem {
     int o = 0;
     act = o; o += C::W * C::LDA;
     sb = o;  o += (L > 1 ? L - 1 : 0) * C::W * C::LDS;   // s_l, l = 1..L-1
-    cb = o;  o += (L > 1 ? L - 1 : 1) * C::W * C::LDS;   // c_l, l = 2..L (L == 1: c_1)
+    cb = o;  o += (L > 1 ? L - 1 : 0) * C::W * C::LDS;   // c_l, l = 2..L
     const int dead = o;
     qF = o;  o += C::Q * 9;
     qk = o;  o += C::Q * 3;
@@ -231,8 +230,8 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
         act[j * LDA + q] = z;
       } else {
         const double aj = __ldg(m.a + j);
-        act[j * LDA + q] = aj * s;
-        cb[j * LDS + q] = aj * s * (1.0 - s);
+        act[j * LDA + q] = aj * s;                  // mu_1
+        act[j * LDA + Q + q] = aj * s * (1.0 - s);  // c_1
       }
     }
     __syncthreads();
@@ -265,12 +264,13 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
               const int q = ncol[jj] + 2 * t + h;
               double y = acc[i][jj][h] + bj;
               if (skips) y += B3[0] * qk[q * 3] + B3[1] * qk[q * 3 + 1] + B3[2] * qk[q * 3 + 2];
-              double z, s;
-              softplus_sig(y, stab, z, s);
               if (l < L) {
+                double z, s;
+                softplus_sig(y, stab, z, s);
                 sb[((l - 1) * W + j) * LDS + q] = s;
                 act[j * LDA + q] = z;
-              } else {
+              } else {  // z_L is not needed (only dN/dz_L = a), so no log
+                const double s = sigmoid_tab(y, stab);
                 act[j * LDA + q] = aj * s;                                  // mu_L
                 cb[((l - 2) * W + j) * LDS + q] = aj * s * (1.0 - s);       // c_L
               }
@@ -316,19 +316,10 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
               }
           }
         } else {
-          // l == 2: lambda_1 -> mu_1, c_1 consumed here: g = W1^T mu_1, H_1 = W1^T diag(c_1) W1,
-          // partial over this thread's rows, reduced over the warp's row groups g
-          double pg[C::NT_V][2][9];
-#pragma unroll
-          for (int jj = 0; jj < C::NT_V; jj++)
-#pragma unroll
-            for (int h = 0; h < 2; h++)
-#pragma unroll
-              for (int x = 0; x < 9; x++) pg[jj][h][x] = 0.0;
+          // l == 2: lambda_1 -> mu_1 (act cols [0,Q)) and c_1 (act cols [Q,2Q)) for stage 5
 #pragma unroll
           for (int i = 0; i < C::MT_V; i++) {
             const int j = (mt0 + i) * 8 + g;
-            const double w0 = __ldg(m.W1 + j * 3), w1 = __ldg(m.W1 + j * 3 + 1), w2 = __ldg(m.W1 + j * 3 + 2);
 #pragma unroll
             for (int jj = 0; jj < C::NT_V; jj++)
 #pragma unroll
@@ -336,78 +327,34 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
                 const int q = ncol[jj] + 2 * t + h;
                 const double lam = acc[i][jj][h];
                 const double s = sb[j * LDS + q];
-                const double mu = lam * s, c = mu * (1.0 - s);
-                double* P9 = pg[jj][h];
-                P9[0] += w0 * mu; P9[1] += w1 * mu; P9[2] += w2 * mu;
-                const double c0 = c * w0, c1 = c * w1;
-                P9[3] += c0 * w0; P9[4] += c0 * w1; P9[5] += c0 * w2;
-                P9[6] += c1 * w1; P9[7] += c1 * w2; P9[8] += c * w2 * w2;
+                const double mu = lam * s;
+                act[j * LDA + q] = mu;
+                act[j * LDA + Q + q] = mu * (1.0 - s);
               }
-          }
-#pragma unroll
-          for (int jj = 0; jj < C::NT_V; jj++)
-#pragma unroll
-            for (int h = 0; h < 2; h++)
-#pragma unroll
-              for (int x = 0; x < 9; x++) {
-                double v = pg[jj][h][x];
-                v += __shfl_xor_sync(0xffffffffu, v, 4);
-                v += __shfl_xor_sync(0xffffffffu, v, 8);
-                v += __shfl_xor_sync(0xffffffffu, v, 16);
-                pg[jj][h][x] = v;
-              }
-          if (g == 0) {
-#pragma unroll
-            for (int jj = 0; jj < C::NT_V; jj++)
-#pragma unroll
-              for (int h = 0; h < 2; h++)
-#pragma unroll
-                for (int x = 0; x < 9; x++) act[(vm * Q + ncol[jj] + 2 * t + h) * 9 + x] = pg[jj][h][x];
           }
         }
         __syncthreads();
       }
     }
 
-    // ---- stage 5: g = W1^T mu_1 + skips, H_1 = sum_j c1_j W1_j W1_j^T ------------------
-    if (L > 1) {
-      if (tid < Q) {
-        const int q = tid;
-        double v[9];
+    // ---- stage 5: [g; H_1] = [W1^T 0; 0 V] [mu_1; c_1] as one DMMA GEMM --------------------
+    // (rows 0-2: g_m = sum_j W1_jm mu_1j; rows 3-8: H_1,mn = sum_j W1_jm W1_jn c_1j; 16 x 2W
+    //  fragments prepared at setup; one 8x8 tile per warp while tiles remain)
+    for (int tile = warp; tile < 2 * C::QB; tile += C::NWARP) {
+      const int mt = tile / C::QB, nt = tile % C::QB;
+      double acc5[1][1][2];
+      int nc0[1] = {nt * 8};
+      warp_gemm<1, 1, KT2>(m.gfrag, mt, act, LDA, nc0, acc5);
+      double acc6[1][1][2];
+      int nc1[1] = {Q + nt * 8};
+      warp_gemm<1, 1, KT2>(m.gfrag + (size_t)16 * W, mt, act, LDA, nc1, acc6);
+      const int row = mt * 8 + g;
 #pragma unroll
-        for (int x = 0; x < 9; x++) v[x] = 0.0;
-#pragma unroll
-        for (int r = 0; r < C::VMG; r++)
-#pragma unroll
-          for (int x = 0; x < 9; x++) v[x] += act[(r * Q + q) * 9 + x];
-#pragma unroll
-        for (int x = 0; x < 3; x++) qg[q * 3 + x] = v[x] + gsk[q * 3 + x] + __ldg(m.skip_out + x);
-#pragma unroll
-        for (int x = 0; x < 6; x++) qH[q * 6 + x] = v[3 + x];
-      }
-    } else {
-      constexpr int P = C::NTHR / Q;  // threads per qp (lanes q*P .. q*P+P-1 share a warp)
-      const int q = tid / P, part = tid % P;
-      double gs[3] = {0, 0, 0}, hs[6] = {0, 0, 0, 0, 0, 0};
-      for (int j = part; j < W; j += P) {
-        const double w0 = __ldg(m.W1 + j * 3), w1 = __ldg(m.W1 + j * 3 + 1), w2 = __ldg(m.W1 + j * 3 + 2);
-        const double mu = act[j * LDA + q], c = cb[j * LDS + q];
-        gs[0] += w0 * mu; gs[1] += w1 * mu; gs[2] += w2 * mu;
-        hs[0] += c * w0 * w0; hs[1] += c * w0 * w1; hs[2] += c * w0 * w2;
-        hs[3] += c * w1 * w1; hs[4] += c * w1 * w2; hs[5] += c * w2 * w2;
-      }
-#pragma unroll
-      for (int o = 1; o < P; o <<= 1) {
-#pragma unroll
-        for (int x = 0; x < 3; x++) gs[x] += __shfl_xor_sync(0xffffffffu, gs[x], o);
-#pragma unroll
-        for (int x = 0; x < 6; x++) hs[x] += __shfl_xor_sync(0xffffffffu, hs[x], o);
-      }
-      if (part == 0) {
-#pragma unroll
-        for (int x = 0; x < 3; x++) qg[q * 3 + x] = gs[x] + gsk[q * 3 + x] + __ldg(m.skip_out + x);
-#pragma unroll
-        for (int x = 0; x < 6; x++) qH[q * 6 + x] = hs[x];
+      for (int h = 0; h < 2; h++) {
+        const int q = nt * 8 + 2 * t + h;
+        const double v = acc5[0][0][h] + acc6[0][0][h];
+        if (row < 3) qg[q * 3 + row] = v + gsk[q * 3 + row] + __ldg(m.skip_out + row);
+        else if (row < 9) qH[q * 6 + row - 3] = v;
       }
     }
     __syncthreads();
@@ -592,6 +539,27 @@ void fused_weight_frag_fill(int w, int L, const double* Wrow, double* out) {
             const size_t o = ((size_t)(mt * KT2 + kt2) * 32 + lane) * 2 + h;
             fw[o] = Wl[(size_t)r * w + c];   // W_l
             ft[o] = Wl[(size_t)c * w + r];   // W_l^T
+          }
+  }
+}
+
+void fused_gfrag_fill(int w, const double* W1, double* out) {
+  const int KT2 = w / 8;
+  for (int which = 0; which < 2; which++) {
+    double* f = out + (size_t)which * 16 * w;
+    for (int mt = 0; mt < 2; mt++)
+      for (int kt2 = 0; kt2 < KT2; kt2++)
+        for (int lane = 0; lane < 32; lane++)
+          for (int h = 0; h < 2; h++) {
+            const int g = lane >> 2, t = lane & 3;
+            const int r = 8 * mt + g, j = 8 * kt2 + 4 * h + t;
+            double v = 0.0;
+            if (which == 0 && r < 3) v = W1[j * 3 + r];
+            if (which == 1 && r >= 3 && r < 9) {
+              static const int pm[6] = {0, 0, 0, 1, 1, 2}, pn[6] = {0, 1, 2, 1, 2, 2};
+              v = W1[j * 3 + pm[r - 3]] * W1[j * 3 + pn[r - 3]];
+            }
+            f[((size_t)(mt * KT2 + kt2) * 32 + lane) * 2 + h] = v;
           }
   }
 }

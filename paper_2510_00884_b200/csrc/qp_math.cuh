@@ -195,6 +195,31 @@ __device__ __forceinline__ void softplus_sig(double y, const double* __restrict_
   s = (y >= 0.0 ? 1.0 : e) * iu;
 }
 
+// sigmoid only (the last hidden layer needs s, not z): e = exp(-|y|) and 1/(1+e) as above
+__device__ __forceinline__ double sigmoid_tab(double y, const double* __restrict__ tab) {
+  const double MAGIC = 6755399441055744.0;
+  const double x = fmax(-fabs(y), -708.0);
+  double kd = fma(x, 92.33248261689366, MAGIC);
+  const int k = __double2loint(kd);
+  kd -= MAGIC;
+  double r = fma(kd, -0.010830424696249145, x);
+  r = fma(kd, -3.623510646634843e-19, r);
+  double p = fma(r, 1.0 / 120.0, 1.0 / 24.0);
+  p = fma(p, r, 1.0 / 6.0);
+  p = fma(p, r, 0.5);
+  p = fma(p, r, 1.0);
+  p = fma(p, r, 1.0);
+  double e = tab[k & 63] * p;
+  e = __hiloint2double(__double2hiint(e) + (k >> 6) * 1048576, __double2loint(e));
+  const double u = 1.0 + e;
+  const int j = __double2loint(fma(e, 64.0, MAGIC));
+  const double invc = tab[64 + j];
+  const double r2 = fma(u, invc, -1.0);
+  const double r2s = r2 * r2;
+  const double v = (1.0 - r2) * (1.0 + r2s) * (1.0 + r2s * r2s);
+  return (y >= 0.0 ? 1.0 : e) * (invc * v);
+}
+
 // host: fill the table (long double for the reference values)
 inline void fill_act_table(double* tab) {
   for (int j = 0; j < 64; j++) tab[j] = (double)exp2l((long double)j / 64.0L);
