@@ -211,6 +211,7 @@ def main():
         lib.set_kernel(pc.KERNEL_SIMPLE)
     n_el, n_q = cfg["conn"].shape[0], cfg["gradN"].shape[1]
     info = lib.info()
+    kinfo = lib.kernel_info()
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream(dev)
     u_host = torch.from_numpy(cfg["u"]).pin_memory()
@@ -282,7 +283,7 @@ def main():
         dtype="f64", data="synthetic (seeded mesh, NCM weights N(0,0.3^2), displacement; synth/gen.py)",
         config=dict(workload=WORKLOAD[args.config], elements=total_el, qp=total_qp, nnz_rank0=nnz_local,
                     width=spec.width, hidden_layers=spec.n_hidden, colours=info["n_colours"],
-                    kernel=args.kernel, parallelism=f"z-slabs x{ws}" if ws > 1 else "single GPU",
+                    kernel=args.kernel, launch=kinfo, parallelism=f"z-slabs x{ws}" if ws > 1 else "single GPU",
                     l2="inputs larger than L2 (dN/dX + CSR values >> 126 MB), no flush needed"
                     if args.config in ("c3", "c4", "c5") else "inputs fit in L2 (latency-bound config)"),
         elements_per_s=total_el / (ms * 1e-3),

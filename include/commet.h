@@ -144,6 +144,11 @@ commet_status commet_set_kernel(commet_ctx ctx, int32_t variant);
 commet_status commet_info(commet_ctx ctx, int32_t* n_colours, int32_t* n_q, int32_t* n_en,
                           int32_t* launches_per_assemble);
 
+/* Launch shape of the fused kernel for this ctx: dynamic shared memory per CTA,
+ * resident CTAs per SM and registers per thread (diagnostics). */
+commet_status commet_kernel_info(commet_ctx ctx, int32_t* smem_bytes, int32_t* ctas_per_sm,
+                                 int32_t* regs_per_thread);
+
 /* Kernel-time instrumentation for benchmarks: with n_slots > 0, every
  * commet_assemble records a CUDA event pair on its stream around its kernel
  * launches (first colour launch .. last launch, zeroing excluded) into a ring

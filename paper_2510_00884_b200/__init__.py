@@ -31,7 +31,8 @@ SYMBOLS = ("commet_setup", "commet_csr_pattern", "commet_csr_pattern_copy", "com
            "commet_nccl_unique_id", "commet_nccl_comm_init", "commet_nccl_comm_destroy",
            "commet_halo_info", "commet_halo_send", "commet_halo_recv", "commet_halo_unpack",
            "commet_plan_create", "commet_plan_info", "commet_plan_csr", "commet_plan_halo",
-           "commet_plan_send", "commet_plan_recv", "commet_plan_colours", "commet_plan_destroy")
+           "commet_plan_send", "commet_plan_recv", "commet_plan_colours", "commet_plan_destroy",
+           "commet_kernel_info")
 
 
 class MeshDesc(C.Structure):
@@ -91,6 +92,8 @@ for _f in ("commet_nccl_unique_id", "commet_nccl_comm_init", "commet_nccl_comm_d
            "commet_plan_info", "commet_plan_csr", "commet_plan_halo", "commet_plan_send", "commet_plan_recv",
            "commet_plan_colours"):
     getattr(_lib, _f).restype = C.c_int
+_lib.commet_kernel_info.argtypes = [_vp, _P(_i32), _P(_i32), _P(_i32)]
+_lib.commet_kernel_info.restype = C.c_int
 _lib.commet_last_error.argtypes = [_vp]
 _lib.commet_last_error.restype = C.c_char_p
 _lib.commet_destroy.argtypes = [_vp]
@@ -187,6 +190,11 @@ class Commet:
         v = [_i32() for _ in range(4)]
         _check(_lib.commet_info(self.ctx, *[C.byref(x) for x in v]), self.ctx)
         return dict(n_colours=v[0].value, n_q=v[1].value, n_en=v[2].value, launches=v[3].value)
+
+    def kernel_info(self):
+        v = [_i32() for _ in range(3)]
+        _check(_lib.commet_kernel_info(self.ctx, *[C.byref(x) for x in v]), self.ctx)
+        return dict(smem_bytes=v[0].value, ctas_per_sm=v[1].value, regs_per_thread=v[2].value)
 
     def set_kernel(self, variant: int):
         _check(_lib.commet_set_kernel(self.ctx, variant), self.ctx)

@@ -401,6 +401,18 @@ extern "C" commet_status commet_info(commet_ctx c, int32_t* n_colours, int32_t* 
   return COMMET_OK;
 }
 
+extern "C" commet_status commet_kernel_info(commet_ctx c, int32_t* smem_bytes, int32_t* ctas_per_sm,
+                                            int32_t* regs_per_thread) {
+  if (!c) return fail(nullptr, COMMET_ERR_ARG, "ctx is NULL");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  int a = 0, b = 0, r = 0;
+  fused_occupancy(c->plan.n_en, c->ncm.w, c->ncm.L, &a, &b, &r);
+  if (smem_bytes) *smem_bytes = a;
+  if (ctas_per_sm) *ctas_per_sm = b;
+  if (regs_per_thread) *regs_per_thread = r;
+  return COMMET_OK;
+}
+
 extern "C" commet_status commet_set_timing(commet_ctx c, int32_t n_slots) {
   if (!c) return fail(nullptr, COMMET_ERR_ARG, "ctx is NULL");
   if (n_slots < 0 || n_slots > 100000) return fail(c, COMMET_ERR_ARG, "n_slots %d out of range", n_slots);

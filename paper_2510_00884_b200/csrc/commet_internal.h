@@ -61,6 +61,7 @@ int launch_unpack(const double* vals, const int64_t* vmap, int64_t nv, double* c
 int launch_activation(const double* y, double* z, double* s, int64_t n, const double* tab, void* stream);
 int launch_fused(const AsmArgs& a, void* stream, int* launches);
 int fused_supported(int n_en, int n_q, int w, int L);
+void fused_occupancy(int n_en, int w, int L, int* smem_bytes, int* ctas_per_sm, int* regs);
 // prepares the fragment-ordered weight array on the host (size in doubles)
 int64_t fused_weight_frag_size(int w, int L);
 void fused_weight_frag_fill(int w, int L, const double* Wrow, double* out);

@@ -69,7 +69,7 @@ struct Cfg {
 template <class C>
 struct Smem {
   static constexpr int PS = 101;  // per-qp stride of the stage-7a outputs (odd: bank spread)
-  int act, sb, cb, qF, qk, qg, qH, hred, gsk, gN, ue, wq, tab, qP, post, X, qA, total;
+  int act, sb, cb, qF, qk, qg, qH, hred, gsk, gN, ue, wq, tab, vbase, rbase, rstr, slt, qP, post, X, qA, total;
   __host__ __device__ Smem(int L) {
     int o = 0;
     act = o; o += C::W * C::LDA;
@@ -88,6 +88,10 @@ struct Smem {
     wq = o;  o += C::Q;
     tab = o; o += kActTabSize;
     o = (o + 1) & ~1;
+    vbase = o; o += C::E * C::NEN;          // double* : CSR value base of row 3a (own or halo buffer)
+    rbase = o; o += C::E * C::NEN;          // double* : residual entry of row 3a
+    rstr = o;  o += (C::E * C::NEN + 1) / 2;  // int : 3 * deg (row stride of components)
+    slt = o;   o += (C::E * C::NEN * C::NEN + 7) / 8;  // uint8 slots
     const int px = C::Q * PS > C::Q * C::NEN * 27 ? C::Q * PS : C::Q * C::NEN * 27;
     const int need = C::Q * 9 + px + C::Q * 81;
     int base = 0;
@@ -156,6 +160,10 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
   double* sue = smem + sm.ue;
   double* swq = smem + sm.wq;
   double* stab = smem + sm.tab;
+  double** svb = reinterpret_cast<double**>(smem + sm.vbase);
+  double** srb = reinterpret_cast<double**>(smem + sm.rbase);
+  int* srs = reinterpret_cast<int*>(smem + sm.rstr);
+  uint8_t* sslot = reinterpret_cast<uint8_t*>(smem + sm.slt);
   double* qA = smem + sm.qA;
   double* qP = smem + sm.qP;
   double* post = smem + sm.post;
@@ -187,6 +195,18 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
         sue[x] = e < ne ? __ldg(A.u + 3 * (int64_t)__ldg(A.conn + (e0 + e) * NEN + ai / 3) + ai % 3) : 0.0;
       }
       for (int x = tid; x < Q; x += C::NTHR) swq[x] = x < ne * NQ ? __ldg(A.qp_w + e0 * NQ + x) : 0.0;
+      for (int x = tid; x < ne * NEN; x += C::NTHR) {
+        const int64_t ln = __ldg(A.lrow + e0 * NEN + x);
+        const bool own = ln < A.n_owned;
+        svb[x] = (own ? A.v_own : A.v_halo) + __ldg(A.node_rs + ln);
+        srb[x] = (own ? A.r_own : A.r_halo) + 3 * (own ? ln : ln - A.n_owned);
+        srs[x] = 3 * __ldg(A.node_deg + ln);
+      }
+      {
+        const uint32_t* src32 = reinterpret_cast<const uint32_t*>(A.slot + (size_t)e0 * NEN * NEN);
+        uint32_t* dst32 = reinterpret_cast<uint32_t*>(sslot);
+        for (int x = tid; x < ne * NEN * NEN / 4; x += C::NTHR) dst32[x] = __ldg(src32 + x);
+      }
     }
     __syncthreads();
 
@@ -219,7 +239,10 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
     __syncthreads();
 
     // ---- stage 2: layer 1 (3 -> W), elementwise -------------------------------------
-    for (int x = tid; x < W * Q; x += C::NTHR) {
+    static_assert((W * Q) % C::NTHR == 0, "layer-1 items per thread");
+#pragma unroll
+    for (int it = 0; it < W * Q / C::NTHR; it++) {
+      const int x = tid + it * C::NTHR;
       const int j = x / Q, q = x % Q;
       const double y = __ldg(m.b + j) + __ldg(m.W1 + j * 3 + 0) * qk[q * 3 + 0] +
                        __ldg(m.W1 + j * 3 + 1) * qk[q * 3 + 1] + __ldg(m.W1 + j * 3 + 2) * qk[q * 3 + 2];
@@ -487,24 +510,15 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
           rr += qP[q * 9 + i * 3] * ga[0] + qP[q * 9 + i * 3 + 1] * ga[1] + qP[q * 9 + i * 3 + 2] * ga[2];
         }
       }
-      const int64_t el = e0 + e;
-      const int64_t ln = __ldg(A.lrow + el * NEN + a);
-      const bool own = ln < A.n_owned;
-      double* vb = own ? A.v_own : A.v_halo;
-      const int deg = __ldg(A.node_deg + ln);
-      const int64_t row0 = __ldg(A.node_rs + ln) + (int64_t)i * 3 * deg;
       // fire-and-forget RED.ADD.F64: the colouring makes the updates conflict-free (and the
       // per-entry summation order deterministic: one update per colour launch); RED avoids the
       // load round trip of a read-modify-write
-      double* dst = vb + row0 + 3 * (int)__ldg(A.slot + ((size_t)el * NEN + a) * NEN + b);
+      const int ea = e * NEN + a;
+      double* dst = svb[ea] + i * srs[ea] + 3 * (int)sslot[ea * NEN + b];
       atomicAdd(dst, K0);
       atomicAdd(dst + 1, K1);
       atomicAdd(dst + 2, K2);
-      if (b == 0) {
-        double* rb = own ? A.r_own : A.r_halo;
-        const int64_t rn = own ? ln : ln - A.n_owned;
-        atomicAdd(rb + 3 * rn + i, rr);
-      }
+      if (b == 0) atomicAdd(srb[ea] + i, rr);
     }
     __syncthreads();
   }
@@ -587,6 +601,36 @@ static int launch_cfg(const AsmArgs& a, cudaStream_t st, int* launches) {
   fused_kernel<C><<<(unsigned)grid, C::NTHR, bytes, st>>>(a);
   if (launches) (*launches)++;
   return (int)cudaGetLastError();
+}
+
+template <class C>
+static void occ_cfg(int L, int* smem_bytes, int* ctas_per_sm, int* regs) {
+  const Smem<C> sm(L);
+  const size_t bytes = (size_t)sm.total * sizeof(double);
+  cudaFuncSetAttribute(fused_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fused_kernel<C>, C::NTHR, bytes);
+  cudaFuncAttributes fa{};
+  cudaFuncGetAttributes(&fa, fused_kernel<C>);
+  *smem_bytes = (int)bytes;
+  *ctas_per_sm = per_sm;
+  *regs = fa.numRegs;
+}
+
+template <int NEN, int NQ>
+static void occ_et(int w, int L, int* a, int* b, int* c) {
+  switch (w) {
+    case 8: occ_cfg<Cfg<8, 32, NEN, NQ>>(L, a, b, c); break;
+    case 16: occ_cfg<Cfg<16, 16, NEN, NQ>>(L, a, b, c); break;
+    case 32: occ_cfg<Cfg<32, 16, NEN, NQ>>(L, a, b, c); break;
+    case 64: occ_cfg<Cfg<64, 16, NEN, NQ>>(L, a, b, c); break;
+    case 128: occ_cfg<Cfg<128, 8, NEN, NQ>>(L, a, b, c); break;
+  }
+}
+
+void fused_occupancy(int n_en, int w, int L, int* smem_bytes, int* ctas_per_sm, int* regs) {
+  if (n_en == 8) occ_et<8, 8>(w, L, smem_bytes, ctas_per_sm, regs);
+  else occ_et<10, 4>(w, L, smem_bytes, ctas_per_sm, regs);
 }
 
 template <int NEN, int NQ>
