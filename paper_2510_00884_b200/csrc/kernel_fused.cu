@@ -24,6 +24,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 
 #include "commet_internal.h"
 #include "qp_math.cuh"
@@ -43,11 +44,11 @@ __device__ __forceinline__ double2 ldg2(const double* p) {
 // ---------------------------------------------------------------------------
 // compile-time tiling
 // ---------------------------------------------------------------------------
-template <int W_, int Q_, int NEN_, int NQ_>
+template <int W_, int Q_, int NEN_, int NQ_, int MINB_ = 3>
 struct Cfg {
   static constexpr int W = W_, Q = Q_, NEN = NEN_, NQ = NQ_;
   static constexpr int NWARP = 4, NTHR = 128;
-  static constexpr int MINB = 3;                   // CTAs per SM the register budget targets (<= 168 regs)
+  static constexpr int MINB = MINB_;               // CTAs per SM the register budget targets
   static constexpr int E = Q / NQ;                 // elements per CTA iteration
   static constexpr int MTILES = W / 8, QB = Q / 8, KT2 = W / 8;
   // value / adjoint warp tiles: VMG x VNG warps, each MT_V x NT_V tiles
@@ -58,7 +59,7 @@ struct Cfg {
   // Jacobian warp tiles: JMG m-groups x QB qp blocks, each MT_J x 3 tiles
   static constexpr int JMG = NWARP / QB, MT_J = MTILES / JMG;
   static constexpr int LDA = 3 * Q + 4;            // act row stride (= 4 mod 16: conflict-free B frags)
-  static constexpr int LDS = Q + 2;                // s/c row stride (2-way conflicts at most)
+  static constexpr int LDS = Q + 1;                // s/c row stride (odd: <= 2-way conflicts)
   static_assert(W % 8 == 0 && Q % 8 == 0 && Q % NQ == 0, "tile");
   static_assert(TPW >= 1 && VMG * VNG == NWARP && MT_V * NT_V == TPW, "value tiling");
   static_assert(JMG >= 1 && JMG * QB == NWARP && MT_J * JMG == MTILES, "jacobian tiling");
@@ -603,6 +604,17 @@ static int launch_cfg(const AsmArgs& a, cudaStream_t st, int* launches) {
   return (int)cudaGetLastError();
 }
 
+// COMMET_FUSED_VARIANT=1 (environment, read once): alternative tiling for tuning
+// experiments (w = 64: one element per batch, 4 CTAs/SM at <= 128 registers).
+static int fused_variant() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("COMMET_FUSED_VARIANT");
+    v = e ? atoi(e) : 0;
+  }
+  return v;
+}
+
 template <class C>
 static void occ_cfg(int L, int* smem_bytes, int* ctas_per_sm, int* regs) {
   const Smem<C> sm(L);
@@ -623,7 +635,10 @@ static void occ_et(int w, int L, int* a, int* b, int* c) {
     case 8: occ_cfg<Cfg<8, 32, NEN, NQ>>(L, a, b, c); break;
     case 16: occ_cfg<Cfg<16, 16, NEN, NQ>>(L, a, b, c); break;
     case 32: occ_cfg<Cfg<32, 16, NEN, NQ>>(L, a, b, c); break;
-    case 64: occ_cfg<Cfg<64, 16, NEN, NQ>>(L, a, b, c); break;
+    case 64:
+      if (fused_variant() == 1) occ_cfg<Cfg<64, 8, NEN, NQ, 4>>(L, a, b, c);
+      else occ_cfg<Cfg<64, 16, NEN, NQ>>(L, a, b, c);
+      break;
     case 128: occ_cfg<Cfg<128, 8, NEN, NQ>>(L, a, b, c); break;
   }
 }
@@ -639,7 +654,9 @@ static int launch_et(const AsmArgs& a, cudaStream_t st, int* launches) {
     case 8: return launch_cfg<Cfg<8, 32, NEN, NQ>>(a, st, launches);
     case 16: return launch_cfg<Cfg<16, 16, NEN, NQ>>(a, st, launches);
     case 32: return launch_cfg<Cfg<32, 16, NEN, NQ>>(a, st, launches);
-    case 64: return launch_cfg<Cfg<64, 16, NEN, NQ>>(a, st, launches);
+    case 64:
+      if (fused_variant() == 1) return launch_cfg<Cfg<64, 8, NEN, NQ, 4>>(a, st, launches);
+      return launch_cfg<Cfg<64, 16, NEN, NQ>>(a, st, launches);
     case 128: return launch_cfg<Cfg<128, 8, NEN, NQ>>(a, st, launches);
   }
   return (int)cudaErrorInvalidValue;
