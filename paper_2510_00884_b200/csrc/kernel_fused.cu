@@ -4,22 +4,23 @@
 // scatter touch HBM.
 //
 // Per CTA iteration (E elements = Q quadrature points):
-//   0  stage dN/dX, w, gather u_e                            (a1)
-//   1  F, C, I1, I2, J -> k = (I1-3, I2-3, J-1), det F flag   (a2, a3)
-//   2  layer 1 (3 -> w): y, softplus, sigmoid                 (a4)
-//   3  value pass, hidden layers l = 2..L:  Y = W_l Z          (a4, DMMA GEMM)
-//   4  adjoint pass l = L..2:  Lambda = W_l^T M               (a4, DMMA GEMM)
-//   5  g = W1^T mu_1 (+skips), H_1 = W1^T diag(c_1) W1         (a4)
-//   6  Jacobian pass l = 2..L: J_l = W_l (s_{l-1} (.) J_{l-1}) (a4, DMMA GEMM)
+//   0  wait for this batch's inputs (cp.async, issued one batch ahead), issue
+//      the next batch's                                         (a1)
+//   2  per qp: F, C, I1, I2, J -> k, det F flag; layer 1 (3 -> w) (a2, a3, a4)
+//   3  value pass, hidden layers l = 2..L:  Y = W_l Z           (a4, DMMA GEMM)
+//   4  adjoint pass l = L..2:  Lambda = W_l^T M                 (a4, DMMA GEMM)
+//   5  [g; H_1] = [W1^T 0; 0 V] [mu_1; c_1]                     (a4, DMMA GEMM)
+//   6  Jacobian pass l = 2..L: J_l = W_l (s_{l-1} (.) J_{l-1})   (a4, DMMA GEMM)
 //      H += J_l^T diag(c_l) J_l on the fly, c_l = lambda_l s_l (1-s_l)
-//   7  penalty, S, A = d2W/dFdF (scaled by w)                 (a5, a6)
-//   8  element rows: K_e, r_e; coloured read-modify-write scatter (a7, a8)
+//   7  penalty, S and the F-space tangent factors per qp        (a5, a6)
+//   8a X[q][a][i][kL] = sum_J dN_aJ A_q[iJ][kL] from the factors (a6, a7)
+//   8b K_e, r_e; coloured RED scatter                           (a7, a8)
 // The inner-network derivatives are the exact Hessian of Alg. 4
 // obtained with 5 w^2 FMA per hidden layer instead of
-// Alg. 4's 10 w^2.  Hidden-layer contractions use the
-// fp64 tensor path (mma.sync m8n8k4 f64 = SASS DMMA.8x8x4): on B200 it shares
-// the fp64 datapath with DFMA (measured, profiles/r01_fp64_peak.json) but
-// needs ~8x fewer issue slots and register-file reads per FMA.
+// Alg. 4's 10 w^2.  Hidden-layer contractions use the fp64
+// tensor path (mma.sync m8n8k4 f64 = SASS DMMA.8x8x4): on B200 it shares the
+// fp64 datapath with DFMA (measured, profiles/r01_fp64_peak.json) but needs
+// ~8x fewer issue slots and register-file reads per FMA.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -41,6 +42,19 @@ __device__ __forceinline__ double2 ldg2(const double* p) {
   return __ldg(reinterpret_cast<const double2*>(p));
 }
 
+// global -> shared asynchronous copies (LDGSTS), 16 / 8 / 4 bytes
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src));
+}
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src));
+}
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
 // ---------------------------------------------------------------------------
 // compile-time tiling
 // ---------------------------------------------------------------------------
@@ -58,19 +72,39 @@ struct Cfg {
   static constexpr int VNG = QB / NT_V, VMG = MTILES / MT_V;
   // Jacobian warp tiles: JMG m-groups x QB qp blocks, each MT_J x 3 tiles
   static constexpr int JMG = NWARP / QB, MT_J = MTILES / JMG;
-  static constexpr int LDA = 3 * Q + 4;            // act row stride (= 4 mod 16: conflict-free B frags)
+  // stage 5: 2 m-tiles x QB n-tiles, K split over the remaining warps
+  static constexpr int G5T = 2 * QB;
+  static constexpr int G5S = NWARP > G5T ? NWARP / G5T : 1;
+  static constexpr int LDA = 3 * Q + 4;            // act row stride (2 LDA = 8 or 24 mod 32: conflict-free B frags)
   static constexpr int LDS = Q + 1;                // s/c row stride (odd: <= 2-way conflicts)
-  static_assert(W % 8 == 0 && Q % 8 == 0 && Q % NQ == 0, "tile");
+  static constexpr int UPT = (E * NEN * 3 + NTHR - 1) / NTHR;  // prefetched u values per thread
+  static_assert(W % 8 == 0 && Q % 8 == 0 && Q % NQ == 0 && NTHR % Q == 0, "tile");
   static_assert(TPW >= 1 && VMG * VNG == NWARP && MT_V * NT_V == TPW, "value tiling");
   static_assert(JMG >= 1 && JMG * QB == NWARP && MT_J * JMG == MTILES, "jacobian tiling");
+  static_assert((KT2 % G5S) == 0 && (G5S == 1 || W >= 16 * G5S), "stage-5 split");
+  static_assert(E * NEN <= NTHR, "one scatter base per thread");
+  static_assert((W * Q) % NTHR == 0, "layer-1 items per thread");
 };
 
-// shared-memory carve-up (doubles); L is a runtime value.  The post-NCM
-// buffers (qP, post/X, qA) alias act/s/c, which are dead after stage 6.
+// shared-memory carve-up (doubles); L is a runtime value.  act/s/c are dead
+// after stage 6 and host the post-NCM buffers (qP, post/X, qA) and the
+// Jacobian-pass partials.  Per-batch inputs are double-buffered.
 template <class C>
 struct Smem {
-  static constexpr int PS = 101;  // per-qp stride of the stage-7a outputs (odd: bank spread)
-  int act, sb, cb, qF, qk, qg, qH, hred, gsk, gN, ue, wq, tab, vbase, rbase, rstr, slt, qP, post, X, qA, total;
+  static constexpr int PS = 101;  // per-qp stride of the stage-7 outputs (odd: bank spread)
+  // per-batch input block (doubles): gN, w, u_e, CSR value / residual bases, row strides,
+  // conn, lrow, slots
+  static constexpr int IN_GN = 0;
+  static constexpr int IN_W = IN_GN + C::Q * C::NEN * 3;
+  static constexpr int IN_U = IN_W + C::Q;
+  static constexpr int IN_VB = IN_U + C::E * C::NEN * 3;
+  static constexpr int IN_RB = IN_VB + C::E * C::NEN;
+  static constexpr int IN_RS = IN_RB + C::E * C::NEN;                 // int
+  static constexpr int IN_CONN = IN_RS + (C::E * C::NEN + 1) / 2;     // int
+  static constexpr int IN_LROW = IN_CONN + (C::E * C::NEN + 1) / 2;   // int
+  static constexpr int IN_SLOT = IN_LROW + (C::E * C::NEN + 1) / 2;   // uint8
+  static constexpr int IN_SIZE = ((IN_SLOT + (C::E * C::NEN * C::NEN + 7) / 8) + 1) & ~1;
+  int act, sb, cb, qF, qk, qg, qH, hred, gsk, in0, qP, post, X, total;
   __host__ __device__ Smem(int L) {
     int o = 0;
     act = o; o += C::W * C::LDA;
@@ -81,49 +115,44 @@ struct Smem {
     qk = o;  o += C::Q * 3;
     qg = o;  o += C::Q * 3;
     qH = o;  o += C::Q * 6;
-    hred = o; o += C::JMG * C::Q * 6;  // Jacobian-pass H partials per warp row group
-    // (the adjoint-pass g/H_1 partials, VMG x Q x 9, live in act: dead at that point)
     gsk = o; o += C::Q * 3;
-    gN = o;  o += C::Q * C::NEN * 3;
-    ue = o;  o += C::E * C::NEN * 3;
-    wq = o;  o += C::Q;
-    tab = o; o += kActTabSize;
     o = (o + 1) & ~1;
-    vbase = o; o += C::E * C::NEN;          // double* : CSR value base of row 3a (own or halo buffer)
-    rbase = o; o += C::E * C::NEN;          // double* : residual entry of row 3a
-    rstr = o;  o += (C::E * C::NEN + 1) / 2;  // int : 3 * deg (row stride of components)
-    slt = o;   o += (C::E * C::NEN * C::NEN + 7) / 8;  // uint8 slots
-    const int px = C::Q * PS > C::Q * C::NEN * 27 ? C::Q * PS : C::Q * C::NEN * 27;
-    const int need = C::Q * 9 + px + C::Q * 81;
+    in0 = o; o += 2 * IN_SIZE;
+    const int need = C::Q * 9 + C::Q * PS + C::Q * C::NEN * 27 + C::JMG * C::Q * 6;
     int base = 0;
     if (need > dead) { base = o; o += need; }
     qP = base;
-    post = X = base + C::Q * 9;
-    qA = post + px;
+    post = qP + C::Q * 9;
+    X = post + C::Q * PS;
+    hred = X + C::Q * C::NEN * 27;
     total = o;
   }
 };
 
 // ---------------------------------------------------------------------------
-// one warp tile of  C = A (M x K, fragments in global) * B (K x N, smem)
+// one warp tile of  C (+)= A (M x K, fragments in global) * B (K x N, smem)
+// KS k-pair steps starting at fragment column k0 of a matrix with KT2 pairs
 // ---------------------------------------------------------------------------
-template <int MT, int NT, int KT2>
+template <int MT, int NT, int KS, int KT2, bool ACC = false>
 __device__ __forceinline__ void warp_gemm(const double* __restrict__ Af, int mt0, const double* act,
-                                          int lda, const int (&ncol)[NT], double (&acc)[MT][NT][2]) {
+                                          int lda, const int (&ncol)[NT], double (&acc)[MT][NT][2],
+                                          int k0 = 0) {
   const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  if (!ACC) {
 #pragma unroll
-  for (int i = 0; i < MT; i++)
+    for (int i = 0; i < MT; i++)
 #pragma unroll
-    for (int j = 0; j < NT; j++) acc[i][j][0] = acc[i][j][1] = 0.0;
-  const double* ap = Af + (size_t)mt0 * KT2 * 64 + lane * 2;
-  const double* bp = act + t * lda + g;
+      for (int j = 0; j < NT; j++) acc[i][j][0] = acc[i][j][1] = 0.0;
+  }
+  const double* ap = Af + ((size_t)mt0 * KT2 + k0) * 64 + lane * 2;
+  const double* bp = act + (k0 * 8 + t) * lda + g;
   double2 a[2][MT];
 #pragma unroll
   for (int i = 0; i < MT; i++) a[0][i] = ldg2(ap + (size_t)i * KT2 * 64);
 #pragma unroll
-  for (int kt2 = 0; kt2 < KT2; kt2++) {
+  for (int kt2 = 0; kt2 < KS; kt2++) {
     const int cur = kt2 & 1;
-    if (kt2 + 1 < KT2) {
+    if (kt2 + 1 < KS) {
 #pragma unroll
       for (int i = 0; i < MT; i++) a[cur ^ 1][i] = ldg2(ap + ((size_t)i * KT2 + kt2 + 1) * 64);
     }
@@ -141,13 +170,102 @@ __device__ __forceinline__ void warp_gemm(const double* __restrict__ Af, int mt0
   }
 }
 
+// issue the asynchronous copies of batch `batch`'s contiguous inputs into block `in`
+template <class C>
+__device__ __forceinline__ void stage_inputs(const AsmArgs& A, int64_t batch, double* in) {
+  using S = Smem<C>;
+  constexpr int NEN = C::NEN, NQ = C::NQ, E = C::E, Q = C::Q;
+  const int64_t e0 = A.el_begin + batch * E;
+  const int64_t rem = A.el_begin + A.el_count - e0;
+  const int ne = rem < E ? (int)rem : E;
+  const int tid = threadIdx.x;
+  {
+    const double* src = A.gradN + (size_t)e0 * NQ * NEN * 3;
+    double* dst = in + S::IN_GN;
+    const int n2 = ne * NQ * NEN * 3 / 2;
+    for (int x = tid; x < E * NQ * NEN * 3 / 2; x += C::NTHR) {
+      if (x < n2) cp_async16(dst + 2 * x, src + 2 * x);
+      else dst[2 * x] = dst[2 * x + 1] = 0.0;
+    }
+  }
+  for (int x = tid; x < Q; x += C::NTHR) {
+    if (x < ne * NQ) cp_async8(in + S::IN_W + x, A.qp_w + e0 * NQ + x);
+    else in[S::IN_W + x] = 0.0;
+  }
+  int* conn = reinterpret_cast<int*>(in + S::IN_CONN);
+  int* lrow = reinterpret_cast<int*>(in + S::IN_LROW);
+  for (int x = tid; x < ne * NEN; x += C::NTHR) {
+    cp_async4(conn + x, A.conn + e0 * NEN + x);
+    cp_async4(lrow + x, A.lrow + e0 * NEN + x);
+  }
+  {
+    const uint32_t* src32 = reinterpret_cast<const uint32_t*>(A.slot + (size_t)e0 * NEN * NEN);
+    uint32_t* dst32 = reinterpret_cast<uint32_t*>(in + S::IN_SLOT);
+    for (int x = tid; x < ne * NEN * NEN / 4; x += C::NTHR) cp_async4(dst32 + x, src32 + x);
+  }
+  cp_async_commit();
+}
+
+// dependent gathers of a batch whose conn/lrow are in `in`: u_e (returned in registers,
+// stored by commit_gathers) and the CSR scatter bases (stored directly)
+template <class C>
+struct Gathered {
+  double u[C::UPT];
+  double* vb;
+  double* rb;
+  int rs;
+};
+
+template <class C>
+__device__ __forceinline__ void issue_gathers(const AsmArgs& A, int ne, const double* in, Gathered<C>& G) {
+  using S = Smem<C>;
+  constexpr int NEN = C::NEN;
+  const int tid = threadIdx.x;
+  const int* conn = reinterpret_cast<const int*>(in + S::IN_CONN);
+  const int* lrow = reinterpret_cast<const int*>(in + S::IN_LROW);
+#pragma unroll
+  for (int k = 0; k < C::UPT; k++) {
+    const int x = tid + k * C::NTHR;
+    const int e = x / (NEN * 3), ai = x % (NEN * 3);
+    G.u[k] = (x < C::E * NEN * 3 && e < ne) ? __ldg(A.u + 3 * (int64_t)conn[e * NEN + ai / 3] + ai % 3) : 0.0;
+  }
+  G.vb = nullptr;
+  G.rb = nullptr;
+  G.rs = 0;
+  if (tid < ne * NEN) {
+    const int64_t ln = lrow[tid];
+    const bool own = ln < A.n_owned;
+    G.vb = (own ? A.v_own : A.v_halo) + __ldg(A.node_rs + ln);
+    G.rb = (own ? A.r_own : A.r_halo) + 3 * (own ? ln : ln - A.n_owned);
+    G.rs = 3 * __ldg(A.node_deg + ln);
+  }
+}
+
+template <class C>
+__device__ __forceinline__ void commit_gathers(int ne, double* in, const Gathered<C>& G) {
+  using S = Smem<C>;
+  const int tid = threadIdx.x;
+#pragma unroll
+  for (int k = 0; k < C::UPT; k++) {
+    const int x = tid + k * C::NTHR;
+    if (x < C::E * C::NEN * 3) in[S::IN_U + x] = G.u[k];
+  }
+  if (tid < ne * C::NEN) {
+    reinterpret_cast<double**>(in + S::IN_VB)[tid] = G.vb;
+    reinterpret_cast<double**>(in + S::IN_RB)[tid] = G.rb;
+    reinterpret_cast<int*>(in + S::IN_RS)[tid] = G.rs;
+  }
+}
+
 template <class C>
 __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
+  using S = Smem<C>;
   constexpr int W = C::W, Q = C::Q, NEN = C::NEN, NQ = C::NQ, E = C::E;
   constexpr int LDA = C::LDA, LDS = C::LDS, KT2 = C::KT2;
+  constexpr int PS = S::PS;
   extern __shared__ __align__(16) double smem[];
   const int L = A.ncm.L;
-  const Smem<C> sm(L);
+  const S sm(L);
   double* act = smem + sm.act;
   double* sb = smem + sm.sb;
   double* cb = smem + sm.cb;
@@ -157,63 +275,59 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
   double* qH = smem + sm.qH;
   double* hred = smem + sm.hred;
   double* gsk = smem + sm.gsk;
-  double* sgN = smem + sm.gN;
-  double* sue = smem + sm.ue;
-  double* swq = smem + sm.wq;
-  double* stab = smem + sm.tab;
-  double** svb = reinterpret_cast<double**>(smem + sm.vbase);
-  double** srb = reinterpret_cast<double**>(smem + sm.rbase);
-  int* srs = reinterpret_cast<int*>(smem + sm.rstr);
-  uint8_t* sslot = reinterpret_cast<uint8_t*>(smem + sm.slt);
-  double* qA = smem + sm.qA;
   double* qP = smem + sm.qP;
   double* post = smem + sm.post;
   double* Xb = smem + sm.X;
-  constexpr int PS = Smem<C>::PS;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
   const NcmDev& m = A.ncm;
+  const double* __restrict__ tab = m.act_tab;
   const bool skips = m.skip_h != nullptr;
   const int64_t n_batches = (A.el_count + E - 1) / E;
   const size_t frag_layer = (size_t)2 * W * W;  // W and W^T fragments per hidden layer
-  for (int x = threadIdx.x; x < kActTabSize; x += C::NTHR) stab[x] = __ldg(A.ncm.act_tab + x);
-  // (made visible by the first __syncthreads of the batch loop)
+  if ((int64_t)blockIdx.x >= n_batches) return;
 
-  for (int64_t batch = blockIdx.x; batch < n_batches; batch += gridDim.x) {
+  // prologue: inputs of the first batch, synchronously
+  {
+    double* in = smem + sm.in0;
+    stage_inputs<C>(A, blockIdx.x, in);
+    cp_async_wait_all();
+    __syncthreads();
+    const int64_t rem = A.el_count - (int64_t)blockIdx.x * E;
+    Gathered<C> G;
+    issue_gathers<C>(A, rem < E ? (int)rem : E, in, G);
+    commit_gathers<C>(rem < E ? (int)rem : E, in, G);
+  }
+
+  int buf = 0;
+  for (int64_t batch = blockIdx.x; batch < n_batches; batch += gridDim.x, buf ^= 1) {
     const int64_t e0 = A.el_begin + batch * E;
     const int64_t rem = A.el_begin + A.el_count - e0;
     const int ne = rem < E ? (int)rem : E;
-
-    // ---- stage 0: stage element inputs --------------------------------------------
-    {
-      const double2* src = reinterpret_cast<const double2*>(A.gradN + (size_t)e0 * NQ * NEN * 3);
-      double2* dst = reinterpret_cast<double2*>(sgN);
-      const int n2 = ne * NQ * NEN * 3 / 2;
-      for (int x = tid; x < E * NQ * NEN * 3 / 2; x += C::NTHR)
-        dst[x] = x < n2 ? __ldg(src + x) : make_double2(0.0, 0.0);
-      for (int x = tid; x < E * NEN * 3; x += C::NTHR) {
-        const int e = x / (NEN * 3), ai = x % (NEN * 3);
-        sue[x] = e < ne ? __ldg(A.u + 3 * (int64_t)__ldg(A.conn + (e0 + e) * NEN + ai / 3) + ai % 3) : 0.0;
-      }
-      for (int x = tid; x < Q; x += C::NTHR) swq[x] = x < ne * NQ ? __ldg(A.qp_w + e0 * NQ + x) : 0.0;
-      for (int x = tid; x < ne * NEN; x += C::NTHR) {
-        const int64_t ln = __ldg(A.lrow + e0 * NEN + x);
-        const bool own = ln < A.n_owned;
-        svb[x] = (own ? A.v_own : A.v_halo) + __ldg(A.node_rs + ln);
-        srb[x] = (own ? A.r_own : A.r_halo) + 3 * (own ? ln : ln - A.n_owned);
-        srs[x] = 3 * __ldg(A.node_deg + ln);
-      }
-      {
-        const uint32_t* src32 = reinterpret_cast<const uint32_t*>(A.slot + (size_t)e0 * NEN * NEN);
-        uint32_t* dst32 = reinterpret_cast<uint32_t*>(sslot);
-        for (int x = tid; x < ne * NEN * NEN / 4; x += C::NTHR) dst32[x] = __ldg(src32 + x);
-      }
+    double* in = smem + sm.in0 + buf * S::IN_SIZE;
+    double* nin = smem + sm.in0 + (buf ^ 1) * S::IN_SIZE;
+    const double* sgN = in + S::IN_GN;
+    const double* swq = in + S::IN_W;
+    const double* sue = in + S::IN_U;
+    double* const* svb = reinterpret_cast<double* const*>(in + S::IN_VB);
+    double* const* srb = reinterpret_cast<double* const*>(in + S::IN_RB);
+    const int* srs = reinterpret_cast<const int*>(in + S::IN_RS);
+    const uint8_t* sslot = reinterpret_cast<const uint8_t*>(in + S::IN_SLOT);
+    const int64_t nbatch = batch + gridDim.x;
+    const bool has_next = nbatch < n_batches;
+    int nne = 0;
+    if (has_next) {
+      const int64_t nrem = A.el_begin + A.el_count - (A.el_begin + nbatch * E);
+      nne = nrem < E ? (int)nrem : E;
     }
-    __syncthreads();
 
-    // ---- stage 1: kinematics ------------------------------------------------------
-    if (tid < Q) {
-      const int q = tid, e = q / NQ;
+    // ---- stage 0: this batch's inputs are resident; prefetch the next batch's ---------
+    __syncthreads();
+    if (has_next) stage_inputs<C>(A, nbatch, nin);
+
+    // ---- stage 2: per-qp kinematics (every thread, for its qp q = tid % Q) + layer 1 -------
+    {
+      const int q = tid % Q, e = q / NQ;
       const double* gq = sgN + q * NEN * 3;
       const double* ue = sue + e * NEN * 3;
       double F[9];
@@ -226,36 +340,43 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
           for (int a = 0; a < NEN; a++) s += ue[a * 3 + i] * gq[a * 3 + J];
           F[i * 3 + J] = s;
         }
-      Kin kin;
-      kinematics(F, kin);
-      if (e < ne && !(kin.J > 0.0))
-        atomicMin(A.bad, (unsigned long long)(__ldg(A.orig + e0 + e) * NQ + q % NQ));
+      // k = (I1-3, I2-3, J-1), J by cofactor expansion
+      double C6[6];
+      C6[0] = F[0] * F[0] + F[3] * F[3] + F[6] * F[6];
+      C6[1] = F[1] * F[1] + F[4] * F[4] + F[7] * F[7];
+      C6[2] = F[2] * F[2] + F[5] * F[5] + F[8] * F[8];
+      C6[3] = F[0] * F[1] + F[3] * F[4] + F[6] * F[7];
+      C6[4] = F[1] * F[2] + F[4] * F[5] + F[7] * F[8];
+      C6[5] = F[0] * F[2] + F[3] * F[5] + F[6] * F[8];
+      const double I1 = C6[0] + C6[1] + C6[2];
+      const double trC2 = C6[0] * C6[0] + C6[1] * C6[1] + C6[2] * C6[2] + 2.0 * (C6[3] * C6[3] + C6[4] * C6[4] + C6[5] * C6[5]);
+      const double Jd = F[0] * (F[4] * F[8] - F[5] * F[7]) + F[1] * (F[5] * F[6] - F[3] * F[8]) +
+                        F[2] * (F[3] * F[7] - F[4] * F[6]);
+      const double k0 = I1 - 3.0, k1 = 0.5 * (I1 * I1 - trC2) - 3.0, k2 = Jd - 1.0;
+      if (tid < Q) {
+        if (e < ne && !(Jd > 0.0)) atomicMin(A.bad, (unsigned long long)(__ldg(A.orig + e0 + e) * NQ + q % NQ));
 #pragma unroll
-      for (int x = 0; x < 9; x++) qF[q * 9 + x] = F[x];
-      qk[q * 3 + 0] = kin.I1 - 3.0;
-      qk[q * 3 + 1] = kin.I2 - 3.0;
-      qk[q * 3 + 2] = kin.J - 1.0;
-      gsk[q * 3 + 0] = gsk[q * 3 + 1] = gsk[q * 3 + 2] = 0.0;
-    }
-    __syncthreads();
-
-    // ---- stage 2: layer 1 (3 -> W), elementwise -------------------------------------
-    static_assert((W * Q) % C::NTHR == 0, "layer-1 items per thread");
+        for (int x = 0; x < 9; x++) qF[q * 9 + x] = F[x];
+        qk[q * 3 + 0] = k0;
+        qk[q * 3 + 1] = k1;
+        qk[q * 3 + 2] = k2;
+        gsk[q * 3 + 0] = gsk[q * 3 + 1] = gsk[q * 3 + 2] = 0.0;
+      }
 #pragma unroll
-    for (int it = 0; it < W * Q / C::NTHR; it++) {
-      const int x = tid + it * C::NTHR;
-      const int j = x / Q, q = x % Q;
-      const double y = __ldg(m.b + j) + __ldg(m.W1 + j * 3 + 0) * qk[q * 3 + 0] +
-                       __ldg(m.W1 + j * 3 + 1) * qk[q * 3 + 1] + __ldg(m.W1 + j * 3 + 2) * qk[q * 3 + 2];
-      double z, s;
-      softplus_sig(y, stab, z, s);
-      if (L > 1) {
-        sb[j * LDS + q] = s;
-        act[j * LDA + q] = z;
-      } else {
-        const double aj = __ldg(m.a + j);
-        act[j * LDA + q] = aj * s;                  // mu_1
-        act[j * LDA + Q + q] = aj * s * (1.0 - s);  // c_1
+      for (int it = 0; it < W * Q / C::NTHR; it++) {
+        const int j = (tid + it * C::NTHR) / Q;
+        const double y = __ldg(m.b + j) + __ldg(m.W1 + j * 3 + 0) * k0 + __ldg(m.W1 + j * 3 + 1) * k1 +
+                         __ldg(m.W1 + j * 3 + 2) * k2;
+        if (L > 1) {
+          double z, s;
+          softplus_sig(y, tab, z, s);
+          sb[j * LDS + q] = s;
+          act[j * LDA + q] = z;
+        } else {
+          const double s = sigmoid_tab(y, tab), aj = __ldg(m.a + j);
+          act[j * LDA + q] = aj * s;                  // mu_1
+          act[j * LDA + Q + q] = aj * s * (1.0 - s);  // c_1
+        }
       }
     }
     __syncthreads();
@@ -269,7 +390,7 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
       for (int j = 0; j < C::NT_V; j++) ncol[j] = (vn * C::NT_V + j) * 8;
       for (int l = 2; l <= L; l++) {
         double acc[C::MT_V][C::NT_V][2];
-        warp_gemm<C::MT_V, C::NT_V, KT2>(m.Wfrag + (l - 2) * frag_layer, mt0, act, LDA, ncol, acc);
+        warp_gemm<C::MT_V, C::NT_V, KT2, KT2>(m.Wfrag + (l - 2) * frag_layer, mt0, act, LDA, ncol, acc);
         __syncthreads();
 #pragma unroll
         for (int i = 0; i < C::MT_V; i++) {
@@ -290,11 +411,11 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
               if (skips) y += B3[0] * qk[q * 3] + B3[1] * qk[q * 3 + 1] + B3[2] * qk[q * 3 + 2];
               if (l < L) {
                 double z, s;
-                softplus_sig(y, stab, z, s);
+                softplus_sig(y, tab, z, s);
                 sb[((l - 1) * W + j) * LDS + q] = s;
                 act[j * LDA + q] = z;
               } else {  // z_L is not needed (only dN/dz_L = a), so no log
-                const double s = sigmoid_tab(y, stab);
+                const double s = sigmoid_tab(y, tab);
                 act[j * LDA + q] = aj * s;                                  // mu_L
                 cb[((l - 2) * W + j) * LDS + q] = aj * s * (1.0 - s);       // c_L
               }
@@ -322,66 +443,79 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
           gsk[tid * 3] += s0; gsk[tid * 3 + 1] += s1; gsk[tid * 3 + 2] += s2;
         }
         double acc[C::MT_V][C::NT_V][2];
-        warp_gemm<C::MT_V, C::NT_V, KT2>(m.Wfrag + (l - 2) * frag_layer + (size_t)W * W, mt0, act, LDA, ncol, acc);
+        warp_gemm<C::MT_V, C::NT_V, KT2, KT2>(m.Wfrag + (l - 2) * frag_layer + (size_t)W * W, mt0, act, LDA,
+                                              ncol, acc);
         __syncthreads();
-        if (l > 2) {
 #pragma unroll
-          for (int i = 0; i < C::MT_V; i++) {
-            const int j = (mt0 + i) * 8 + g;
+        for (int i = 0; i < C::MT_V; i++) {
+          const int j = (mt0 + i) * 8 + g;
 #pragma unroll
-            for (int jj = 0; jj < C::NT_V; jj++)
+          for (int jj = 0; jj < C::NT_V; jj++)
 #pragma unroll
-              for (int h = 0; h < 2; h++) {
-                const int q = ncol[jj] + 2 * t + h;
-                const double lam = acc[i][jj][h];
-                const double s = sb[((l - 2) * W + j) * LDS + q];
-                cb[((l - 3) * W + j) * LDS + q] = lam * s * (1.0 - s);  // c_{l-1}
-                act[j * LDA + q] = lam * s;                              // mu_{l-1}
-              }
-          }
-        } else {
-          // l == 2: lambda_1 -> mu_1 (act cols [0,Q)) and c_1 (act cols [Q,2Q)) for stage 5
-#pragma unroll
-          for (int i = 0; i < C::MT_V; i++) {
-            const int j = (mt0 + i) * 8 + g;
-#pragma unroll
-            for (int jj = 0; jj < C::NT_V; jj++)
-#pragma unroll
-              for (int h = 0; h < 2; h++) {
-                const int q = ncol[jj] + 2 * t + h;
-                const double lam = acc[i][jj][h];
-                const double s = sb[j * LDS + q];
-                const double mu = lam * s;
+            for (int h = 0; h < 2; h++) {
+              const int q = ncol[jj] + 2 * t + h;
+              const double lam = acc[i][jj][h];
+              const double s = sb[((l - 2) * W + j) * LDS + q];
+              const double mu = lam * s, c = mu * (1.0 - s);
+              if (l > 2) {
+                cb[((l - 3) * W + j) * LDS + q] = c;  // c_{l-1}
+                act[j * LDA + q] = mu;                 // mu_{l-1}
+              } else {                                 // mu_1, c_1 for stage 5
                 act[j * LDA + q] = mu;
-                act[j * LDA + Q + q] = mu * (1.0 - s);
+                act[j * LDA + Q + q] = c;
               }
-          }
+            }
         }
         __syncthreads();
       }
     }
 
-    // ---- stage 5: [g; H_1] = [W1^T 0; 0 V] [mu_1; c_1] as one DMMA GEMM --------------------
-    // (rows 0-2: g_m = sum_j W1_jm mu_1j; rows 3-8: H_1,mn = sum_j W1_jm W1_jn c_1j; 16 x 2W
-    //  fragments prepared at setup; one 8x8 tile per warp while tiles remain)
-    for (int tile = warp; tile < 2 * C::QB; tile += C::NWARP) {
+    // ---- stage 5: [g; H_1] = [W1^T 0; 0 V] [mu_1; c_1] (16 x 2W fragments, DMMA) ----------
+    // rows 0-2: g_m = sum_j W1_jm mu_1j; rows 3-8: H_1,mn = sum_j W1_jm W1_jn c_1j.  Tiles
+    // 2 x QB; with fewer tiles than warps K is split and the partials meet in act[:, 2Q..3Q)
+    for (int task = warp; task < C::G5T * C::G5S; task += C::NWARP) {
+      const int tile = task % C::G5T, split = task / C::G5T;
       const int mt = tile / C::QB, nt = tile % C::QB;
+      constexpr int KS = KT2 / C::G5S;
       double acc5[1][1][2];
-      int nc0[1] = {nt * 8};
-      warp_gemm<1, 1, KT2>(m.gfrag, mt, act, LDA, nc0, acc5);
-      double acc6[1][1][2];
-      int nc1[1] = {Q + nt * 8};
-      warp_gemm<1, 1, KT2>(m.gfrag + (size_t)16 * W, mt, act, LDA, nc1, acc6);
+      const int nc0[1] = {nt * 8};
+      const int nc1[1] = {Q + nt * 8};
+      warp_gemm<1, 1, KS, KT2>(m.gfrag, mt, act, LDA, nc0, acc5, split * KS);
+      warp_gemm<1, 1, KS, KT2, true>(m.gfrag + (size_t)16 * W, mt, act, LDA, nc1, acc5, split * KS);
       const int row = mt * 8 + g;
 #pragma unroll
       for (int h = 0; h < 2; h++) {
         const int q = nt * 8 + 2 * t + h;
-        const double v = acc5[0][0][h] + acc6[0][0][h];
+        if (C::G5S == 1) {
+          const double v = acc5[0][0][h];
+          if (row < 3) qg[q * 3 + row] = v + gsk[q * 3 + row] + __ldg(m.skip_out + row);
+          else if (row < 9) qH[q * 6 + row - 3] = v;
+        } else {
+          act[(split * 16 + row) * LDA + 2 * Q + q] = acc5[0][0][h];
+        }
+      }
+    }
+    if (C::G5S > 1) {
+      __syncthreads();
+      for (int x = tid; x < 9 * Q; x += C::NTHR) {
+        const int row = x / Q, q = x % Q;
+        double v = 0.0;
+#pragma unroll
+        for (int s = 0; s < C::G5S; s++) v += act[(s * 16 + row) * LDA + 2 * Q + q];
         if (row < 3) qg[q * 3 + row] = v + gsk[q * 3 + row] + __ldg(m.skip_out + row);
-        else if (row < 9) qH[q * 6 + row - 3] = v;
+        else qH[q * 6 + row - 3] = v;
       }
     }
     __syncthreads();
+
+    // ---- mid-batch: the next batch's conn/lrow have landed -> issue its dependent gathers --
+    // (u_e and CSR bases; the loads complete under stages 6-8, stored at the end of the batch)
+    Gathered<C> G;
+    if (has_next) {
+      cp_async_wait_all();
+      __syncthreads();
+      issue_gathers<C>(A, nne, nin, G);
+    }
 
     // ---- stage 6: Jacobian pass, H += J_l^T diag(c_l) J_l -------------------------------
     if (L > 1) {
@@ -404,7 +538,7 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
         for (int x = 0; x < 6; x++) hp[h][x] = 0.0;
       for (int l = 2; l <= L; l++) {
         double acc[C::MT_J][3][2];
-        warp_gemm<C::MT_J, 3, KT2>(m.Wfrag + (l - 2) * frag_layer, mt0, act, LDA, ncol, acc);
+        warp_gemm<C::MT_J, 3, KT2, KT2>(m.Wfrag + (l - 2) * frag_layer, mt0, act, LDA, ncol, acc);
         __syncthreads();
 #pragma unroll
         for (int i = 0; i < C::MT_J; i++) {
@@ -432,7 +566,7 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
         }
         __syncthreads();
       }
-      // reduce over the 8 row-groups g of the warp (lane bits 2..4)
+      // reduce over the 8 row groups g of the warp (lane bits 2..4); act/s/c are dead now
 #pragma unroll
       for (int h = 0; h < 2; h++)
 #pragma unroll
@@ -452,7 +586,7 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
       __syncthreads();
     }
 
-    // ---- stage 7a: per qp -- penalty, S, T, Phi_m, Psi_m, b, P (all scaled by w) --------
+    // ---- stage 7: per qp -- penalty, S, T, Phi_m, Psi_m, b, P (all scaled by w) ------------
     if (tid < Q) {
       const int q = tid;
       double gq[3], H6[6];
@@ -474,26 +608,43 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
     }
     __syncthreads();
 
-    // ---- stage 7b: A_q (81 entries, scaled by w), one (q, iJ) row per item ------------------
-    for (int it = tid; it < Q * 9; it += C::NTHR) {
-      const int q = it / 9, iJ = it % 9;
-      tangent_row(post + q * PS, iJ, qA + q * 81 + iJ * 9);
-    }
-    __syncthreads();
-
-    // ---- stage 8a: X[q][a][i][kL] = sum_J dN_aJ A_q[iJ][kL] -----------------------------------
-    for (int it = tid; it < Q * 3 * NEN; it += C::NTHR) {
-      const int a = it % NEN, qi = it / NEN, i = qi % 3, q = qi / 3;
+    // ---- stage 8a: X[q][a][i][kL] = sum_J dN_aJ A_q[iJ][kL] straight from the factors -------
+    //   = d_ik t_L + sum_m phi_m,i Psi_m,kL + c2 F_iL p_k + c3 F^-T_iL r_k + c2 dN_aL b_ik
+    //   phi_m = Phi_m dN_a, p = F dN_a, r = F^-T dN_a, t = (wT) dN_a
+    for (int it = tid; it < Q * NEN; it += C::NTHR) {
+      const int q = it / NEN, a = it % NEN;
+      const double* P = post + q * PS;
       const double* ga = sgN + (q * NEN + a) * 3;
-      const double g0 = ga[0], g1 = ga[1], g2 = ga[2];
-      const double* Ai = qA + q * 81 + i * 27;
-      double* Xo = Xb + ((q * NEN + a) * 3 + i) * 9;
+      const double n0 = ga[0], n1 = ga[1], n2 = ga[2];
+      double phi[3][3], pv[3], rv[3], tv[3];
 #pragma unroll
-      for (int kL = 0; kL < 9; kL++) Xo[kL] = g0 * Ai[kL] + g1 * Ai[9 + kL] + g2 * Ai[18 + kL];
+      for (int i = 0; i < 3; i++) {
+#pragma unroll
+        for (int mm = 0; mm < 3; mm++)
+          phi[mm][i] = P[27 + mm * 9 + i * 3] * n0 + P[27 + mm * 9 + i * 3 + 1] * n1 + P[27 + mm * 9 + i * 3 + 2] * n2;
+        pv[i] = phi[0][i];  // Phi_1 = F
+        rv[i] = P[9 + i * 3] * n0 + P[9 + i * 3 + 1] * n1 + P[9 + i * 3 + 2] * n2;
+        tv[i] = P[18 + i] * n0 + P[18 + 3 + i] * n1 + P[18 + 6 + i] * n2;
+      }
+      const double c2 = P[90], c3 = P[91];
+      const double nv[3] = {n0, n1, n2};
+      double* Xo = Xb + (q * NEN + a) * 27;
+#pragma unroll
+      for (int i = 0; i < 3; i++)
+#pragma unroll
+        for (int kk = 0; kk < 3; kk++)
+#pragma unroll
+          for (int Lx = 0; Lx < 3; Lx++) {
+            const int kL = kk * 3 + Lx;
+            double v = phi[0][i] * P[54 + kL] + phi[1][i] * P[63 + kL] + phi[2][i] * P[72 + kL];
+            v += c2 * P[i * 3 + Lx] * pv[kk] + c3 * P[9 + i * 3 + Lx] * rv[kk] + c2 * nv[Lx] * P[81 + i * 3 + kk];
+            if (i == kk) v += tv[Lx];
+            Xo[i * 9 + kL] = v;
+          }
     }
     __syncthreads();
 
-    // ---- stage 8b: K_e[ai][bk] = sum_q sum_L X dN_bL, r_e; coloured RMW scatter ----------------
+    // ---- stage 8b: K_e[ai][bk] = sum_q sum_L X dN_bL, r_e; coloured RED scatter -------------
     for (int it = tid; it < ne * NEN * 3 * NEN; it += C::NTHR) {
       const int b = it % NEN, row = it / NEN, e = row / (NEN * 3), ai = row % (NEN * 3), a = ai / 3, i = ai % 3;
       double K0 = 0.0, K1 = 0.0, K2 = 0.0, rr = 0.0;
@@ -512,8 +663,7 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
         }
       }
       // fire-and-forget RED.ADD.F64: the colouring makes the updates conflict-free (and the
-      // per-entry summation order deterministic: one update per colour launch); RED avoids the
-      // load round trip of a read-modify-write
+      // per-entry summation order deterministic: one update per colour launch)
       const int ea = e * NEN + a;
       double* dst = svb[ea] + i * srs[ea] + 3 * (int)sslot[ea * NEN + b];
       atomicAdd(dst, K0);
@@ -521,7 +671,8 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
       atomicAdd(dst + 2, K2);
       if (b == 0) atomicAdd(srb[ea] + i, rr);
     }
-    __syncthreads();
+    // the next batch's gathered inputs go to its buffer (made visible by the next stage-0 sync)
+    if (has_next) commit_gathers<C>(nne, nin, G);
   }
 }
 
