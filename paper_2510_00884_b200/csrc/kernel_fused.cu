@@ -104,7 +104,7 @@ struct Smem {
   static constexpr int IN_LROW = IN_CONN + (C::E * C::NEN + 1) / 2;   // int
   static constexpr int IN_SLOT = IN_LROW + (C::E * C::NEN + 1) / 2;   // uint8
   static constexpr int IN_SIZE = ((IN_SLOT + (C::E * C::NEN * C::NEN + 7) / 8) + 1) & ~1;
-  int act, sb, cb, qF, qk, qg, qH, hred, gsk, in0, qP, post, X, total;
+  int act, sb, cb, qF, qk, qg, qH, hred, gsk, tab, in0, qP, post, X, total;
   __host__ __device__ Smem(int L) {
     int o = 0;
     act = o; o += C::W * C::LDA;
@@ -116,6 +116,7 @@ struct Smem {
     qg = o;  o += C::Q * 3;
     qH = o;  o += C::Q * 6;
     gsk = o; o += C::Q * 3;
+    tab = o; o += kActTabSize;
     o = (o + 1) & ~1;
     in0 = o; o += 2 * IN_SIZE;
     const int need = C::Q * 9 + C::Q * PS + C::Q * C::NEN * 27 + C::JMG * C::Q * 6;
@@ -146,15 +147,20 @@ __device__ __forceinline__ void warp_gemm(const double* __restrict__ Af, int mt0
   }
   const double* ap = Af + ((size_t)mt0 * KT2 + k0) * 64 + lane * 2;
   const double* bp = act + (k0 * 8 + t) * lda + g;
-  double2 a[2][MT];
+  // A fragments stream from L2 (L1 is mostly shared memory): 3-deep register pipeline
+  double2 a[3][MT];
 #pragma unroll
   for (int i = 0; i < MT; i++) a[0][i] = ldg2(ap + (size_t)i * KT2 * 64);
+  if (KS > 1) {
+#pragma unroll
+    for (int i = 0; i < MT; i++) a[1][i] = ldg2(ap + ((size_t)i * KT2 + 1) * 64);
+  }
 #pragma unroll
   for (int kt2 = 0; kt2 < KS; kt2++) {
-    const int cur = kt2 & 1;
-    if (kt2 + 1 < KS) {
+    const int cur = kt2 % 3;
+    if (kt2 + 2 < KS) {
 #pragma unroll
-      for (int i = 0; i < MT; i++) a[cur ^ 1][i] = ldg2(ap + ((size_t)i * KT2 + kt2 + 1) * 64);
+      for (int i = 0; i < MT; i++) a[(kt2 + 2) % 3][i] = ldg2(ap + ((size_t)i * KT2 + kt2 + 2) * 64);
     }
 #pragma unroll
     for (int h = 0; h < 2; h++) {
@@ -281,7 +287,8 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
   const NcmDev& m = A.ncm;
-  const double* __restrict__ tab = m.act_tab;
+  double* tab = smem + sm.tab;  // softplus tables (L1 is mostly carved out as shared memory)
+  for (int x = tid; x < kActTabSize; x += C::NTHR) tab[x] = __ldg(m.act_tab + x);
   const bool skips = m.skip_h != nullptr;
   const int64_t n_batches = (A.el_count + E - 1) / E;
   const size_t frag_layer = (size_t)2 * W * W;  // W and W^T fragments per hidden layer
@@ -389,19 +396,25 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
 #pragma unroll
       for (int j = 0; j < C::NT_V; j++) ncol[j] = (vn * C::NT_V + j) * 8;
       for (int l = 2; l <= L; l++) {
+        double bias[C::MT_V], aw[C::MT_V];  // issued before the GEMM: L2 latency hidden behind it
+#pragma unroll
+        for (int i = 0; i < C::MT_V; i++) {
+          bias[i] = __ldg(m.b + (l - 1) * W + (mt0 + i) * 8 + g);
+          aw[i] = (l == L) ? __ldg(m.a + (mt0 + i) * 8 + g) : 0.0;
+        }
         double acc[C::MT_V][C::NT_V][2];
         warp_gemm<C::MT_V, C::NT_V, KT2, KT2>(m.Wfrag + (l - 2) * frag_layer, mt0, act, LDA, ncol, acc);
         __syncthreads();
 #pragma unroll
         for (int i = 0; i < C::MT_V; i++) {
           const int j = (mt0 + i) * 8 + g;
-          const double bj = __ldg(m.b + (l - 1) * W + j);
+          const double bj = bias[i];
           double B3[3] = {0, 0, 0};
           if (skips) {
             const double* Bl = m.skip_h + ((size_t)(l - 2) * W + j) * 3;
             B3[0] = __ldg(Bl); B3[1] = __ldg(Bl + 1); B3[2] = __ldg(Bl + 2);
           }
-          const double aj = (l == L) ? __ldg(m.a + j) : 0.0;
+          const double aj = aw[i];
 #pragma unroll
           for (int jj = 0; jj < C::NT_V; jj++)
 #pragma unroll
