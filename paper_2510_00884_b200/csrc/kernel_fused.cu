@@ -332,21 +332,33 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
     __syncthreads();
     if (has_next) stage_inputs<C>(A, nbatch, nin);
 
-    // ---- stage 2: per-qp kinematics (every thread, for its qp q = tid % Q) + layer 1 -------
+    // ---- stage 2: per-qp kinematics + layer 1 --------------------------------------------
+    // TPQ consecutive lanes per qp: F's 9 entries are split over them and shared by
+    // shuffles; each lane then forms k and evaluates W/TPQ neurons of layer 1
     {
-      const int q = tid % Q, e = q / NQ;
+      constexpr int TPQ = C::NTHR / Q;
+      const int q = tid / TPQ, r = tid % TPQ, e = q / NQ;
+      const int gbase = lane & ~(TPQ - 1);
       const double* gq = sgN + q * NEN * 3;
       const double* ue = sue + e * NEN * 3;
-      double F[9];
+      constexpr int NV = (9 + TPQ - 1) / TPQ;
+      double fv[NV];
 #pragma unroll
-      for (int i = 0; i < 3; i++)
-#pragma unroll
-        for (int J = 0; J < 3; J++) {
+      for (int h = 0; h < NV; h++) {
+        fv[h] = 0.0;
+        const int x = r + h * TPQ;
+        if (x < 9) {
+          const int i = x / 3, J = x % 3;
           double s = (i == J) ? 1.0 : 0.0;
 #pragma unroll
           for (int a = 0; a < NEN; a++) s += ue[a * 3 + i] * gq[a * 3 + J];
-          F[i * 3 + J] = s;
+          fv[h] = s;
         }
+      }
+      double F[9];
+#pragma unroll
+      for (int x = 0; x < 9; x++)
+        F[x] = __shfl_sync(0xffffffffu, fv[x / TPQ], gbase + x % TPQ);
       // k = (I1-3, I2-3, J-1), J by cofactor expansion
       double C6[6];
       C6[0] = F[0] * F[0] + F[3] * F[3] + F[6] * F[6];
@@ -360,7 +372,7 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
       const double Jd = F[0] * (F[4] * F[8] - F[5] * F[7]) + F[1] * (F[5] * F[6] - F[3] * F[8]) +
                         F[2] * (F[3] * F[7] - F[4] * F[6]);
       const double k0 = I1 - 3.0, k1 = 0.5 * (I1 * I1 - trC2) - 3.0, k2 = Jd - 1.0;
-      if (tid < Q) {
+      if (r == 0) {
         if (e < ne && !(Jd > 0.0)) atomicMin(A.bad, (unsigned long long)(__ldg(A.orig + e0 + e) * NQ + q % NQ));
 #pragma unroll
         for (int x = 0; x < 9; x++) qF[q * 9 + x] = F[x];
@@ -370,8 +382,8 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
         gsk[q * 3 + 0] = gsk[q * 3 + 1] = gsk[q * 3 + 2] = 0.0;
       }
 #pragma unroll
-      for (int it = 0; it < W * Q / C::NTHR; it++) {
-        const int j = (tid + it * C::NTHR) / Q;
+      for (int it = 0; it < W / TPQ; it++) {
+        const int j = r + it * TPQ;
         const double y = __ldg(m.b + j) + __ldg(m.W1 + j * 3 + 0) * k0 + __ldg(m.W1 + j * 3 + 1) * k1 +
                          __ldg(m.W1 + j * 3 + 2) * k2;
         if (L > 1) {
@@ -483,40 +495,33 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
       }
     }
 
-    // ---- stage 5: [g; H_1] = [W1^T 0; 0 V] [mu_1; c_1] (16 x 2W fragments, DMMA) ----------
-    // rows 0-2: g_m = sum_j W1_jm mu_1j; rows 3-8: H_1,mn = sum_j W1_jm W1_jn c_1j.  Tiles
-    // 2 x QB; with fewer tiles than warps K is split and the partials meet in act[:, 2Q..3Q)
-    for (int task = warp; task < C::G5T * C::G5S; task += C::NWARP) {
-      const int tile = task % C::G5T, split = task / C::G5T;
-      const int mt = tile / C::QB, nt = tile % C::QB;
-      constexpr int KS = KT2 / C::G5S;
-      double acc5[1][1][2];
-      const int nc0[1] = {nt * 8};
-      const int nc1[1] = {Q + nt * 8};
-      warp_gemm<1, 1, KS, KT2>(m.gfrag, mt, act, LDA, nc0, acc5, split * KS);
-      warp_gemm<1, 1, KS, KT2, true>(m.gfrag + (size_t)16 * W, mt, act, LDA, nc1, acc5, split * KS);
-      const int row = mt * 8 + g;
-#pragma unroll
-      for (int h = 0; h < 2; h++) {
-        const int q = nt * 8 + 2 * t + h;
-        if (C::G5S == 1) {
-          const double v = acc5[0][0][h];
-          if (row < 3) qg[q * 3 + row] = v + gsk[q * 3 + row] + __ldg(m.skip_out + row);
-          else if (row < 9) qH[q * 6 + row - 3] = v;
-        } else {
-          act[(split * 16 + row) * LDA + 2 * Q + q] = acc5[0][0][h];
-        }
+    // ---- stage 5: g = W1^T mu_1 (+skips), H_1 = W1^T diag(c_1) W1 --------------------------
+    // P consecutive lanes per qp split the sum over j, then reduce with shuffles
+    {
+      constexpr int P = C::NTHR / Q;
+      const int q = tid / P, part = tid % P;
+      double gs[3] = {0, 0, 0}, hs[6] = {0, 0, 0, 0, 0, 0};
+#pragma unroll 4
+      for (int j = part; j < W; j += P) {
+        const double w0 = __ldg(m.W1 + j * 3), w1 = __ldg(m.W1 + j * 3 + 1), w2 = __ldg(m.W1 + j * 3 + 2);
+        const double mu = act[j * LDA + q], c = act[j * LDA + Q + q];
+        gs[0] += w0 * mu; gs[1] += w1 * mu; gs[2] += w2 * mu;
+        const double c0 = c * w0, c1 = c * w1;
+        hs[0] += c0 * w0; hs[1] += c0 * w1; hs[2] += c0 * w2;
+        hs[3] += c1 * w1; hs[4] += c1 * w2; hs[5] += c * w2 * w2;
       }
-    }
-    if (C::G5S > 1) {
-      __syncthreads();
-      for (int x = tid; x < 9 * Q; x += C::NTHR) {
-        const int row = x / Q, q = x % Q;
-        double v = 0.0;
 #pragma unroll
-        for (int s = 0; s < C::G5S; s++) v += act[(s * 16 + row) * LDA + 2 * Q + q];
-        if (row < 3) qg[q * 3 + row] = v + gsk[q * 3 + row] + __ldg(m.skip_out + row);
-        else qH[q * 6 + row - 3] = v;
+      for (int o = 1; o < P; o <<= 1) {
+#pragma unroll
+        for (int x = 0; x < 3; x++) gs[x] += __shfl_xor_sync(0xffffffffu, gs[x], o);
+#pragma unroll
+        for (int x = 0; x < 6; x++) hs[x] += __shfl_xor_sync(0xffffffffu, hs[x], o);
+      }
+      if (part == 0) {
+#pragma unroll
+        for (int x = 0; x < 3; x++) qg[q * 3 + x] = gs[x] + gsk[q * 3 + x] + __ldg(m.skip_out + x);
+#pragma unroll
+        for (int x = 0; x < 6; x++) qH[q * 6 + x] = hs[x];
       }
     }
     __syncthreads();
@@ -657,32 +662,47 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
     }
     __syncthreads();
 
-    // ---- stage 8b: K_e[ai][bk] = sum_q sum_L X dN_bL, r_e; coloured RED scatter -------------
-    for (int it = tid; it < ne * NEN * 3 * NEN; it += C::NTHR) {
-      const int b = it % NEN, row = it / NEN, e = row / (NEN * 3), ai = row % (NEN * 3), a = ai / 3, i = ai % 3;
-      double K0 = 0.0, K1 = 0.0, K2 = 0.0, rr = 0.0;
+    // ---- stage 8b: K_e[ai][bk] = sum_q sum_L X dN_bL for node pairs b >= a (K_e = K_e^T), r_e;
+    //      coloured RED scatter of both (ai, bk) and its mirror (bk, ai)
+    {
+      constexpr int NP = NEN * (NEN + 1) / 2;
+      for (int it = tid; it < ne * NP * 3; it += C::NTHR) {
+        const int i = it % 3, ep = it / 3, e = ep / NP;
+        int p = ep % NP, a = 0;
+        while (p >= NEN - a) { p -= NEN - a; a++; }
+        const int b = a + p;
+        double K0 = 0.0, K1 = 0.0, K2 = 0.0, rr = 0.0;
 #pragma unroll
-      for (int qq = 0; qq < NQ; qq++) {
-        const int q = e * NQ + qq;
-        const double* gb = sgN + (q * NEN + b) * 3;
-        const double h0 = gb[0], h1 = gb[1], h2 = gb[2];
-        const double* Xr = Xb + ((q * NEN + a) * 3 + i) * 9;
-        K0 += Xr[0] * h0 + Xr[1] * h1 + Xr[2] * h2;
-        K1 += Xr[3] * h0 + Xr[4] * h1 + Xr[5] * h2;
-        K2 += Xr[6] * h0 + Xr[7] * h1 + Xr[8] * h2;
-        if (b == 0) {
-          const double* ga = sgN + (q * NEN + a) * 3;
-          rr += qP[q * 9 + i * 3] * ga[0] + qP[q * 9 + i * 3 + 1] * ga[1] + qP[q * 9 + i * 3 + 2] * ga[2];
+        for (int qq = 0; qq < NQ; qq++) {
+          const int q = e * NQ + qq;
+          const double* gb = sgN + (q * NEN + b) * 3;
+          const double h0 = gb[0], h1 = gb[1], h2 = gb[2];
+          const double* Xr = Xb + ((q * NEN + a) * 3 + i) * 9;
+          K0 += Xr[0] * h0 + Xr[1] * h1 + Xr[2] * h2;
+          K1 += Xr[3] * h0 + Xr[4] * h1 + Xr[5] * h2;
+          K2 += Xr[6] * h0 + Xr[7] * h1 + Xr[8] * h2;
+          if (b == a) {
+            const double* ga = sgN + (q * NEN + a) * 3;
+            rr += qP[q * 9 + i * 3] * ga[0] + qP[q * 9 + i * 3 + 1] * ga[1] + qP[q * 9 + i * 3 + 2] * ga[2];
+          }
+        }
+        // fire-and-forget RED.ADD.F64: the colouring makes the updates conflict-free (and the
+        // per-entry summation order deterministic: one update per colour launch)
+        const int ea = e * NEN + a, eb = e * NEN + b;
+        double* dst = svb[ea] + i * srs[ea] + 3 * (int)sslot[ea * NEN + b];
+        atomicAdd(dst, K0);
+        atomicAdd(dst + 1, K1);
+        atomicAdd(dst + 2, K2);
+        if (b == a) {
+          atomicAdd(srb[ea] + i, rr);
+        } else {
+          double* mir = svb[eb] + 3 * (int)sslot[eb * NEN + a] + i;
+          const int st = srs[eb];
+          atomicAdd(mir, K0);
+          atomicAdd(mir + st, K1);
+          atomicAdd(mir + 2 * st, K2);
         }
       }
-      // fire-and-forget RED.ADD.F64: the colouring makes the updates conflict-free (and the
-      // per-entry summation order deterministic: one update per colour launch)
-      const int ea = e * NEN + a;
-      double* dst = svb[ea] + i * srs[ea] + 3 * (int)sslot[ea * NEN + b];
-      atomicAdd(dst, K0);
-      atomicAdd(dst + 1, K1);
-      atomicAdd(dst + 2, K2);
-      if (b == 0) atomicAdd(srb[ea] + i, rr);
     }
     // the next batch's gathered inputs go to its buffer (made visible by the next stage-0 sync)
     if (has_next) commit_gathers<C>(nne, nin, G);
