@@ -1,0 +1,67 @@
+#!/usr/bin/env python
+"""A/B timing of libcommet builds (tuning tool): assemble a config with each
+given .so through the minimal C ABI and print kernel ms / qp/s.
+usage: ab_bench.py c3 lib1.so lib2.so ..."""
+import ctypes as C
+import sys
+import os
+import numpy as np
+import torch
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from synth import gen
+
+
+class MeshDesc(C.Structure):
+    _fields_ = [("elem_type", C.c_int32), ("n_nodes", C.c_int64), ("n_elems", C.c_int64),
+                ("conn", C.c_void_p), ("grad_N", C.c_void_p), ("qp_w", C.c_void_p),
+                ("owned_node_begin", C.c_int64), ("owned_node_end", C.c_int64),
+                ("n_ranks", C.c_int32), ("rank", C.c_int32), ("rank_node_begin", C.c_void_p),
+                ("n_ghost", C.c_int64), ("ghost_conn", C.c_void_p), ("ghost_rank", C.c_void_p)]
+
+
+class NcmDesc(C.Structure):
+    _fields_ = [("n_hidden", C.c_int32), ("width", C.c_int32), ("W1", C.c_void_p), ("W", C.c_void_p),
+                ("b", C.c_void_p), ("a", C.c_void_p), ("skip_out", C.c_void_p),
+                ("skip_hidden", C.c_void_p), ("kappa", C.c_double), ("ref_shift", C.c_double)]
+
+
+def run(path, cfg, steps=20):
+    lib = C.CDLL(path)
+    conn = np.ascontiguousarray(cfg["conn"], np.int32)
+    md = MeshDesc(cfg["elem_type"], cfg["n_nodes"], conn.shape[0], conn.ctypes.data, cfg["gradN"].ctypes.data,
+                  cfg["qp_w"].ctypes.data, 0, cfg["n_nodes"], 1, 0, None, 0, None, None)
+    m = cfg["ncm"]
+    keep = [np.ascontiguousarray(m[k]) for k in ("W1", "W", "b", "a")]
+    nd = NcmDesc(m["n_hidden"], m["width"], *[k.ctypes.data for k in keep], None, None, m["kappa"], 0.0)
+    ctx = C.c_void_p()
+    st = torch.cuda.current_stream().cuda_stream
+    assert lib.commet_setup(C.byref(md), C.byref(nd), 0, C.c_void_p(st), None, C.byref(ctx)) == 0
+    nr, nnz = C.c_int64(), C.c_int64()
+    lib.commet_csr_pattern(ctx, C.byref(nr), C.byref(nnz), None, None)
+    u = torch.from_numpy(cfg["u"]).cuda()
+    r = torch.empty(nr.value, dtype=torch.float64, device="cuda")
+    v = torch.empty(nnz.value, dtype=torch.float64, device="cuda")
+    lib.commet_set_timing(ctx, steps)
+    for _ in range(3):
+        lib.commet_assemble(ctx, C.c_void_p(u.data_ptr()), C.c_void_p(r.data_ptr()), C.c_void_p(v.data_ptr()), C.c_void_p(st))
+    torch.cuda.synchronize()
+    for _ in range(steps):
+        lib.commet_assemble(ctx, C.c_void_p(u.data_ptr()), C.c_void_p(r.data_ptr()), C.c_void_p(v.data_ptr()), C.c_void_p(st))
+    ms = (C.c_float * steps)()
+    lib.commet_kernel_times(ctx, ms, steps)
+    torch.cuda.synchronize()
+    t = float(np.median(list(ms)))
+    res = (r.cpu().numpy(), v.cpu().numpy())
+    lib.commet_destroy(ctx)
+    return t, res
+
+
+if __name__ == "__main__":
+    cfg = gen.make_config(sys.argv[1])
+    nq = cfg["gradN"].shape[1] * cfg["conn"].shape[0]
+    ref = None
+    for p in sys.argv[2:]:
+        t, res = run(p, cfg)
+        d = "" if ref is None else " max|dv|/max|v| %.2e" % (np.abs(res[1] - ref[1]).max() / np.abs(ref[1]).max())
+        ref = ref or res
+        print(f"{os.path.basename(p):28s} {sys.argv[1]} kernel {t:8.3f} ms  {nq / t * 1e3:.4e} qp/s{d}", flush=True)
