@@ -32,6 +32,10 @@
 #ifndef COMMET_SIGMOID_LAST
 #define COMMET_SIGMOID_LAST 1
 #endif
+// element stage on DMMA: 1 = hex8 only (measured: +6% c3, -4% c4 where 10 nodes pad to 16)
+#ifndef COMMET_DMMA_ELEM
+#define COMMET_DMMA_ELEM 1
+#endif
 #ifndef COMMET_SYM_KE
 #define COMMET_SYM_KE 1
 #endif
@@ -56,6 +60,7 @@ struct Cfg {
   static constexpr int W = W_, Q = Q_, NEN = NEN_, NQ = NQ_;
   static constexpr int NWARP = 4, NTHR = 128;
   static constexpr int MINB = MINB_;               // CTAs per SM the register budget targets (3: <= 168 regs)
+  static constexpr bool DMMA_ELEM = COMMET_DMMA_ELEM == 2 || (COMMET_DMMA_ELEM == 1 && NEN == 8);
   static constexpr int E = Q / NQ;                 // elements per CTA iteration
   static constexpr int MTILES = W / 8, QB = Q / 8, KT2 = W / 8;
   // value / adjoint warp tiles: VMG x VNG warps, each MT_V x NT_V tiles
@@ -531,6 +536,84 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
     }
     __syncthreads();
 
+    if constexpr (C::DMMA_ELEM) {
+    // ---- stage 8a (DMMA): X_q[a][(i,k,L)] = sum_J dN_q[a][J] A_q[(i,J)][(k,L)]: per qp one
+    //      m8n8k4 per (node tile, 8 columns of the 27), J padded to 4 with zeros
+    {
+      constexpr int MTE = (NEN + 7) / 8;
+      for (int task = warp; task < Q * MTE * 4; task += C::NWARP) {
+        const int nt = task % 4, mt = (task / 4) % MTE, q = task / (4 * MTE);
+        const int a = 8 * mt + g, n = 8 * nt + g;
+        const double av = (t < 3 && a < NEN) ? sgN[(q * NEN + a) * 3 + t] : 0.0;
+        const double bv = (t < 3 && n < 27) ? qA[q * 81 + (3 * (n / 9) + t) * 9 + n % 9] : 0.0;
+        double c[2] = {0.0, 0.0};
+        dmma(c, av, bv);
+        const int ar = 8 * mt + g;
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+          const int nc = 8 * nt + 2 * t + h;
+          if (ar < NEN && nc < 27) Xb[(q * NEN + ar) * 27 + nc] = c[h];
+        }
+      }
+    }
+    __syncthreads();
+
+    // ---- stage 8b (DMMA): K_ik[a][b] = sum_(q,L) X_q[a][(i,k,L)] dN_q[b][L] for i <= k
+    //      (K_ki = K_ik^T), M = a, N = b, K = (q, L); r_e; RED scatter (+ mirror for i < k)
+    {
+      constexpr int MTE = (NEN + 7) / 8, KS = NQ * 3 / 4;
+      constexpr int NIK = 6;
+      static_assert((NQ * 3) % 4 == 0, "k-steps");
+      for (int task = warp; task < ne * NIK * MTE * MTE; task += C::NWARP) {
+        const int nt = task % MTE, mt = (task / MTE) % MTE, ik = (task / (MTE * MTE)) % NIK,
+                  e = task / (MTE * MTE * NIK);
+        const int i = ik < 3 ? 0 : (ik < 5 ? 1 : 2);
+        const int k = ik < 3 ? ik : (ik < 5 ? ik - 2 : 2);
+        double c[2] = {0.0, 0.0};
+        const int a = 8 * mt + g, bq = 8 * nt + g;
+#pragma unroll
+        for (int kt = 0; kt < KS; kt++) {
+          const int kk = 4 * kt + t, q = e * NQ + kk / 3, L = kk % 3;
+          const double av = a < NEN ? Xb[(q * NEN + a) * 27 + 9 * i + 3 * k + L] : 0.0;
+          const double bv = bq < NEN ? sgN[(q * NEN + bq) * 3 + L] : 0.0;
+          dmma(c, av, bv);
+        }
+        const int64_t el = e0 + e;
+        if (a < NEN) {
+          const int64_t la = __ldg(A.lrow + el * NEN + a);
+          double* va = ((la < A.n_owned) ? A.v_own : A.v_halo) + __ldg(A.node_rs + la);
+          const int sa = 3 * __ldg(A.node_deg + la);
+#pragma unroll
+          for (int h = 0; h < 2; h++) {
+            const int b = 8 * nt + 2 * t + h;
+            if (b < NEN) {
+              atomicAdd(va + i * sa + 3 * (int)__ldg(A.slot + ((size_t)el * NEN + a) * NEN + b) + k, c[h]);
+              if (i < k) {
+                const int64_t lb = __ldg(A.lrow + el * NEN + b);
+                double* vb2 = ((lb < A.n_owned) ? A.v_own : A.v_halo) + __ldg(A.node_rs + lb);
+                const int sb3 = 3 * __ldg(A.node_deg + lb);
+                atomicAdd(vb2 + k * sb3 + 3 * (int)__ldg(A.slot + ((size_t)el * NEN + b) * NEN + a) + i, c[h]);
+              }
+            }
+          }
+        }
+      }
+      // residual r_e[a][i] = sum_q P_q[i][:] . dN_q[a][:]
+      for (int it = tid; it < ne * NEN * 3; it += C::NTHR) {
+        const int i = it % 3, a = (it / 3) % NEN, e = it / (3 * NEN);
+        double rr = 0.0;
+#pragma unroll
+        for (int qq = 0; qq < NQ; qq++) {
+          const int q = e * NQ + qq;
+          const double* ga = sgN + (q * NEN + a) * 3;
+          rr += qP[q * 9 + i * 3] * ga[0] + qP[q * 9 + i * 3 + 1] * ga[1] + qP[q * 9 + i * 3 + 2] * ga[2];
+        }
+        const int64_t la = __ldg(A.lrow + (e0 + e) * NEN + a);
+        const bool own = la < A.n_owned;
+        atomicAdd((own ? A.r_own : A.r_halo) + 3 * (own ? la : la - A.n_owned) + i, rr);
+      }
+    }
+    } else {
     // ---- stage 8a: X[q][a][i][kL] = sum_J dN_aJ A_q[iJ][kL] -----------------------------------
     for (int it = tid; it < Q * 3 * NEN; it += C::NTHR) {
       const int a = it % NEN, qi = it / NEN, i = qi % 3, q = qi / 3;
@@ -629,6 +712,7 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
       }
     }
 #endif
+    }  // DMMA_ELEM
     __syncthreads();
   }
 }

@@ -62,6 +62,7 @@ if __name__ == "__main__":
     ref = None
     for p in sys.argv[2:]:
         t, res = run(p, cfg)
-        d = "" if ref is None else " max|dv|/max|v| %.2e" % (np.abs(res[1] - ref[1]).max() / np.abs(ref[1]).max())
+        d = "" if ref is None else " dv %.2e dr %.2e" % (np.abs(res[1] - ref[1]).max() / np.abs(ref[1]).max(),
+                                                        np.abs(res[0] - ref[0]).max() / np.abs(ref[0]).max())
         ref = ref or res
         print(f"{os.path.basename(p):28s} {sys.argv[1]} kernel {t:8.3f} ms  {nq / t * 1e3:.4e} qp/s{d}", flush=True)
