@@ -82,7 +82,15 @@ typedef struct {
   int64_t n_ghost;            /* elements assembled by OTHER ranks that contain owned nodes */
   const int32_t* ghost_conn;  /* host [n_ghost][n_en]: their connectivity (global node ids) */
   const int32_t* ghost_rank;  /* host [n_ghost]: the rank that assembles each ghost element */
+  /* Scatter order.  COMMET_ORDER_COLOURED: one launch per element colour, each CSR
+   * entry gets at most one update per launch -> bitwise reproducible results.
+   * COMMET_ORDER_ELEMENT: one launch in element order, concurrent updates resolved by
+   * the fp64 L2 reductions (RED.ADD.F64): neighbouring elements run together, so
+   * the CSR rows stay in L2, but the summation order (last bits) varies run to run. */
+  int32_t scatter_order;
 } commet_mesh_desc;
+
+enum { COMMET_ORDER_COLOURED = 0, COMMET_ORDER_ELEMENT = 1 };
 
 /* (M)ICNN inner network of Eq. icnn with softplus
  * activation, on the kinematic inputs k = (I1-3, I2-3, J-1):

@@ -25,6 +25,7 @@ _lib = C.CDLL(LIB_PATH)
 COMMET_OK, COMMET_ERR_ARG, COMMET_ERR_CUDA, COMMET_ERR_NCCL, COMMET_ERR_OOM, COMMET_ERR_DOMAIN = range(6)
 HEX8, TET10 = 0, 1
 KERNEL_FUSED, KERNEL_SIMPLE = 0, 1
+ORDER_COLOURED, ORDER_ELEMENT = 0, 1
 SYMBOLS = ("commet_setup", "commet_csr_pattern", "commet_csr_pattern_copy", "commet_assemble",
            "commet_check", "commet_set_kernel", "commet_info", "commet_set_timing",
            "commet_kernel_times", "commet_selftest_activation", "commet_last_error", "commet_destroy",
@@ -40,7 +41,8 @@ class MeshDesc(C.Structure):
                 ("conn", C.c_void_p), ("grad_N", C.c_void_p), ("qp_w", C.c_void_p),
                 ("owned_node_begin", C.c_int64), ("owned_node_end", C.c_int64),
                 ("n_ranks", C.c_int32), ("rank", C.c_int32), ("rank_node_begin", C.c_void_p),
-                ("n_ghost", C.c_int64), ("ghost_conn", C.c_void_p), ("ghost_rank", C.c_void_p)]
+                ("n_ghost", C.c_int64), ("ghost_conn", C.c_void_p), ("ghost_rank", C.c_void_p),
+                ("scatter_order", C.c_int32)]
 
 
 class NcmDesc(C.Structure):
@@ -133,7 +135,8 @@ def _mesh_desc(mesh: dict):
     gc = None if mesh.get("ghost_conn") is None else np.ascontiguousarray(mesh["ghost_conn"], np.int32)
     gr = None if mesh.get("ghost_rank") is None else np.ascontiguousarray(mesh["ghost_rank"], np.int32)
     md = MeshDesc(int(mesh["elem_type"]), n_nodes, conn.shape[0], _ptr(conn), _ptr(gradN), _ptr(qp_w), nb, ne,
-                  n_ranks, int(mesh.get("rank", 0)), _ptr(rnb), 0 if gc is None else gc.shape[0], _ptr(gc), _ptr(gr))
+                  n_ranks, int(mesh.get("rank", 0)), _ptr(rnb), 0 if gc is None else gc.shape[0], _ptr(gc), _ptr(gr),
+                  int(mesh.get("scatter_order", ORDER_COLOURED)))
     return md, [conn, gradN, qp_w, rnb, gc, gr]
 
 
@@ -362,7 +365,8 @@ def activation(y):
     return z, s
 
 
-def from_config(cfg: dict, device: int = 0, **kw) -> Commet:
+def from_config(cfg: dict, device: int = 0, scatter_order: int = ORDER_COLOURED, **kw) -> Commet:
     """Convenience: a context for a ``synth.gen.make_config`` dict."""
     return Commet(dict(elem_type=cfg["elem_type"], n_nodes=cfg["n_nodes"], conn=cfg["conn"],
-                       gradN=cfg["gradN"], qp_w=cfg["qp_w"]), cfg["ncm"], device=device, **kw)
+                       gradN=cfg["gradN"], qp_w=cfg["qp_w"], scatter_order=scatter_order), cfg["ncm"],
+                  device=device, **kw)

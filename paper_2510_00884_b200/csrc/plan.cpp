@@ -186,8 +186,13 @@ commet_status plan_build(const commet_mesh_desc* mesh, Plan& p, std::string& err
   fill_csr(p.n_owned, n_rn, p.halo_row_ptr, p.halo_col_idx, p.nnz_halo);
 
   // ---- greedy element colouring (local row-nodes shared => conflict), colour-sorted order -
-  std::vector<int32_t> colour(n_el);
-  {
+  //      (element order: a single "colour" holding every element in input order)
+  std::vector<int32_t> colour(n_el, 0);
+  if (mesh->scatter_order == COMMET_ORDER_ELEMENT) {
+    p.n_colours = n_el > 0 ? 1 : 0;
+  } else if (mesh->scatter_order != COMMET_ORDER_COLOURED) {
+    return perr(err, COMMET_ERR_ARG, "scatter_order %d unknown", mesh->scatter_order);
+  } else {
     std::vector<uint64_t> used(n_rn, 0);
     int nc = 0;
     for (int64_t e = 0; e < n_el; e++) {

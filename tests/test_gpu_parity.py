@@ -38,10 +38,10 @@ def small_case(kind, n, w, L, skips=False, shift=False, jitter=0.1, amp=0.05, se
     return dict(elem_type=et, n_nodes=X.shape[0], conn=conn, gradN=gN, qp_w=qw, ncm=m, u=u, X=X)
 
 
-def run_gpu(case, kernel=None):
+def run_gpu(case, kernel=None, order=0):
     torch = _torch()
     import paper_2510_00884_b200 as pc
-    lib = pc.from_config(case)
+    lib = pc.from_config(case, scatter_order=order)
     if kernel is not None:
         lib.set_kernel(kernel)
     u = torch.from_numpy(case["u"]).cuda()
@@ -83,6 +83,18 @@ def test_parity_small(kind, n, w, L, skips, shift, kernel):
     assert lib.check() == bad == -1
     assert rel(r, ro) <= TOL, rel(r, ro)
     assert rel(v, vo) <= TOL, rel(v, vo)
+
+
+@pytest.mark.parametrize("kind,n,w,L,skips,shift", [CASES[3], CASES[8], CASES[6]])
+def test_parity_element_order(kind, n, w, L, skips, shift):
+    """COMMET_ORDER_ELEMENT: one launch, concurrent RED updates (non-deterministic
+    summation order) -- same parity bar."""
+    case = small_case(kind, n, w, L, skips, shift)
+    lib, r, v, rp, ci = run_gpu(case, order=1)
+    ro, vo, orp, oci, bad = run_oracle(case)
+    assert np.array_equal(rp, orp) and np.array_equal(ci, oci)
+    assert lib.info()["n_colours"] == 1
+    assert rel(r, ro) <= TOL and rel(v, vo) <= TOL, (rel(r, ro), rel(v, vo))
 
 
 @pytest.mark.parametrize("name", ["c1", "c2"])

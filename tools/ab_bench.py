@@ -16,7 +16,8 @@ class MeshDesc(C.Structure):
                 ("conn", C.c_void_p), ("grad_N", C.c_void_p), ("qp_w", C.c_void_p),
                 ("owned_node_begin", C.c_int64), ("owned_node_end", C.c_int64),
                 ("n_ranks", C.c_int32), ("rank", C.c_int32), ("rank_node_begin", C.c_void_p),
-                ("n_ghost", C.c_int64), ("ghost_conn", C.c_void_p), ("ghost_rank", C.c_void_p)]
+                ("n_ghost", C.c_int64), ("ghost_conn", C.c_void_p), ("ghost_rank", C.c_void_p),
+                ("scatter_order", C.c_int32)]
 
 
 class NcmDesc(C.Structure):
@@ -29,7 +30,8 @@ def run(path, cfg, steps=20):
     lib = C.CDLL(path)
     conn = np.ascontiguousarray(cfg["conn"], np.int32)
     md = MeshDesc(cfg["elem_type"], cfg["n_nodes"], conn.shape[0], conn.ctypes.data, cfg["gradN"].ctypes.data,
-                  cfg["qp_w"].ctypes.data, 0, cfg["n_nodes"], 1, 0, None, 0, None, None)
+                  cfg["qp_w"].ctypes.data, 0, cfg["n_nodes"], 1, 0, None, 0, None, None,
+                  int(os.environ.get("AB_ORDER", "0")))
     m = cfg["ncm"]
     keep = [np.ascontiguousarray(m[k]) for k in ("W1", "W", "b", "a")]
     nd = NcmDesc(m["n_hidden"], m["width"], *[k.ctypes.data for k in keep], None, None, m["kappa"], 0.0)
