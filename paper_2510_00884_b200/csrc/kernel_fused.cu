@@ -36,16 +36,61 @@
 #ifndef COMMET_DMMA_ELEM
 #define COMMET_DMMA_ELEM 1
 #endif
+#ifndef COMMET_L1_UNROLL
+#define COMMET_L1_UNROLL 1
+#endif
+#ifndef COMMET_PREFETCH
+#define COMMET_PREFETCH 1
+#endif
+#ifndef COMMET_FRAG_PF
+#define COMMET_FRAG_PF 2
+#endif
+#ifndef COMMET_PD_V
+#define COMMET_PD_V 2
+#endif
+#ifndef COMMET_PD_J
+#define COMMET_PD_J 2
+#endif
 #ifndef COMMET_SYM_KE
 #define COMMET_SYM_KE 1
 #endif
 
 namespace commet {
 
+#ifdef COMMET_STAGE_PROF
+// tuning builds only: per-stage wall cycles seen by thread 0 of every CTA (summed over CTAs)
+__device__ unsigned long long g_stage_cycles[16];
+#define STAGE_MARK(i)                               \
+  if (tid == 0) {                                   \
+    const long long now_ = clock64();               \
+    st_acc[i] += now_ - st_acc[15];                 \
+    st_acc[15] = now_;                              \
+  }
+#else
+#define STAGE_MARK(i)
+#endif
+
 __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                : "+d"(c[0]), "+d"(c[1])
                : "d"(a), "d"(b));
+}
+
+// L1 prefetch of the first NK k-steps of a warp's A fragments for the NEXT GEMM, issued at the
+// start of the current epilogue so the GEMM after the barrier does not start on an L2 round trip
+// (measured: +1.6% at w = 128, -0.5% at w = 64 -> w >= 128 only)
+template <int MT, int KT2, int NK>
+__device__ __forceinline__ void frag_prefetch(const double* __restrict__ Af, int mt0) {
+#if COMMET_FRAG_PF
+  if (KT2 < 16) return;
+  const int lane = threadIdx.x & 31;
+  constexpr int NL = MT * NK * 4;  // 128-byte lines (a fragment is 512 bytes)
+#pragma unroll
+  for (int x = lane; x < NL; x += 32) {
+    const int i = x / (NK * 4), r = x % (NK * 4);
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(Af + ((size_t)(mt0 + i) * KT2 + r / 4) * 64 + (r % 4) * 16));
+  }
+#endif
 }
 
 __device__ __forceinline__ double2 ldg2(const double* p) {
@@ -70,6 +115,8 @@ struct Cfg {
   static constexpr int VNG = QB / NT_V, VMG = MTILES / MT_V;
   // Jacobian warp tiles: JMG m-groups x QB qp blocks, each MT_J x 3 tiles
   static constexpr int JMG = NWARP / QB, MT_J = MTILES / JMG;
+  // A-fragment register ring depth (k-steps) of the value/adjoint and Jacobian GEMMs
+  static constexpr int PD_V = COMMET_PD_V, PD_J = COMMET_PD_J;
   static constexpr int LDA = 3 * Q + 4;            // act row stride (= 4 mod 16: conflict-free B frags)
   static constexpr int LDS = Q + 2;                // s/c row stride (2-way conflicts at most)
   static_assert(W % 8 == 0 && Q % 8 == 0 && Q % NQ == 0, "tile");
@@ -116,7 +163,8 @@ struct Smem {
 // ---------------------------------------------------------------------------
 // one warp tile of  C = A (M x K, fragments in global) * B (K x N, smem)
 // ---------------------------------------------------------------------------
-template <int MT, int NT, int KT2>
+// A fragments stream from L2/L1 through a register ring of PD k-steps (PD - 1 in flight)
+template <int MT, int NT, int KT2, int PD = 2>
 __device__ __forceinline__ void warp_gemm(const double* __restrict__ Af, int mt0, const double* act,
                                           int lda, const int (&ncol)[NT], double (&acc)[MT][NT][2]) {
   const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
@@ -126,15 +174,17 @@ __device__ __forceinline__ void warp_gemm(const double* __restrict__ Af, int mt0
     for (int j = 0; j < NT; j++) acc[i][j][0] = acc[i][j][1] = 0.0;
   const double* ap = Af + (size_t)mt0 * KT2 * 64 + lane * 2;
   const double* bp = act + t * lda + g;
-  double2 a[2][MT];
+  double2 a[PD][MT];
 #pragma unroll
-  for (int i = 0; i < MT; i++) a[0][i] = ldg2(ap + (size_t)i * KT2 * 64);
+  for (int p = 0; p < PD - 1 && p < KT2; p++)
+#pragma unroll
+    for (int i = 0; i < MT; i++) a[p][i] = ldg2(ap + ((size_t)i * KT2 + p) * 64);
 #pragma unroll
   for (int kt2 = 0; kt2 < KT2; kt2++) {
-    const int cur = kt2 & 1;
-    if (kt2 + 1 < KT2) {
+    const int cur = kt2 % PD;
+    if (kt2 + PD - 1 < KT2) {
 #pragma unroll
-      for (int i = 0; i < MT; i++) a[cur ^ 1][i] = ldg2(ap + ((size_t)i * KT2 + kt2 + 1) * 64);
+      for (int i = 0; i < MT; i++) a[(kt2 + PD - 1) % PD][i] = ldg2(ap + ((size_t)i * KT2 + kt2 + PD - 1) * 64);
     }
 #pragma unroll
     for (int h = 0; h < 2; h++) {
@@ -183,6 +233,60 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
   const size_t frag_layer = (size_t)2 * W * W;  // W and W^T fragments per hidden layer
   for (int x = threadIdx.x; x < kActTabSize; x += C::NTHR) stab[x] = __ldg(A.ncm.act_tab + x);
   // (made visible by the first __syncthreads of the batch loop)
+#ifdef COMMET_STAGE_PROF
+  __shared__ long long st_acc[16];  // thread 0 only; [15] = previous mark
+  if (tid == 0) {
+    for (int i = 0; i < 15; i++) st_acc[i] = 0;
+    st_acc[15] = clock64();
+  }
+#endif
+
+#if COMMET_PREFETCH
+  // register prefetch of one batch's element inputs: (a) dN/dX, w, conn; (b) the u gather
+  constexpr int NG2 = E * NQ * NEN * 3 / 2, NU = E * NEN * 3;
+  constexpr int PG = (NG2 + C::NTHR - 1) / C::NTHR, PU = (NU + C::NTHR - 1) / C::NTHR;
+  double2 pf_g[PG];
+  double pf_u[PU], pf_w = 0.0;
+  int pf_c[PU];
+  auto pf_load_a = [&](int64_t b) {
+    const int64_t f0 = A.el_begin + b * E;
+    const int64_t frem = A.el_begin + A.el_count - f0;
+    const int fne = frem < E ? (int)frem : E;
+    const double2* src = reinterpret_cast<const double2*>(A.gradN + (size_t)f0 * NQ * NEN * 3);
+    const int n2 = fne * NQ * NEN * 3 / 2;
+#pragma unroll
+    for (int i = 0; i < PG; i++) {
+      const int x = tid + i * C::NTHR;
+      pf_g[i] = x < n2 ? __ldg(src + x) : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int i = 0; i < PU; i++) {
+      const int x = tid + i * C::NTHR;
+      const int e = x / (NEN * 3), ai = x % (NEN * 3);
+      pf_c[i] = (x < NU && e < fne) ? __ldg(A.conn + (f0 + e) * NEN + ai / 3) : -1;  // raw: no use here
+    }
+    if (tid < Q) pf_w = tid < fne * NQ ? __ldg(A.qp_w + f0 * NQ + tid) : 0.0;
+  };
+  auto pf_load_b = [&]() {
+#pragma unroll
+    for (int i = 0; i < PU; i++)
+      pf_u[i] = pf_c[i] >= 0 ? __ldg(A.u + 3 * (int64_t)pf_c[i] + (tid + i * C::NTHR) % 3) : 0.0;
+  };
+  auto pf_store = [&]() {
+    double2* dst = reinterpret_cast<double2*>(sgN);
+#pragma unroll
+    for (int i = 0; i < PG; i++) {
+      const int x = tid + i * C::NTHR;
+      if (x < NG2) dst[x] = pf_g[i];
+    }
+#pragma unroll
+    for (int i = 0; i < PU; i++) {
+      const int x = tid + i * C::NTHR;
+      if (x < NU) sue[x] = pf_u[i];
+    }
+    if (tid < Q) swq[tid] = pf_w;
+  };
+#endif
 
   for (int64_t batch = blockIdx.x; batch < n_batches; batch += gridDim.x) {
     const int64_t e0 = A.el_begin + batch * E;
@@ -190,6 +294,15 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
     const int ne = rem < E ? (int)rem : E;
 
     // ---- stage 0: stage element inputs --------------------------------------------
+#if COMMET_PREFETCH
+    // the first batch loads here; later batches were loaded into registers during the
+    // previous batch's element stage (pf_*), so only the shared-memory stores remain
+    if (batch == blockIdx.x) {
+      pf_load_a(batch);
+      pf_load_b();
+    }
+    pf_store();
+#else
     {
       const double2* src = reinterpret_cast<const double2*>(A.gradN + (size_t)e0 * NQ * NEN * 3);
       double2* dst = reinterpret_cast<double2*>(sgN);
@@ -202,7 +315,9 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
       }
       for (int x = tid; x < Q; x += C::NTHR) swq[x] = x < ne * NQ ? __ldg(A.qp_w + e0 * NQ + x) : 0.0;
     }
+#endif
     __syncthreads();
+    STAGE_MARK(0)
 
     // ---- stage 1: kinematics ------------------------------------------------------
     if (tid < Q) {
@@ -231,8 +346,45 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
       gsk[q * 3 + 0] = gsk[q * 3 + 1] = gsk[q * 3 + 2] = 0.0;
     }
     __syncthreads();
+    STAGE_MARK(1)
 
+#ifdef COMMET_EXP_SKIP_NCM
+    if (false) {
+#endif
     // ---- stage 2: layer 1 (3 -> W), elementwise -------------------------------------
+    if (L > 1) frag_prefetch<C::MT_V, KT2, COMMET_FRAG_PF + (COMMET_FRAG_PF == 0)>(m.Wfrag, (warp / C::VNG) * C::MT_V);
+#if COMMET_L1_UNROLL
+    // each thread: one qp, neurons j0, j0 + NTHR/Q, ... -- all loads issued up front and the
+    // NIT activations interleaved (independent chains)
+    {
+      constexpr int NIT = W * Q / C::NTHR, JS = C::NTHR / Q;
+      static_assert(W * Q % C::NTHR == 0 && C::NTHR % Q == 0, "layer-1 split");
+      const int q = tid % Q, j0 = tid / Q;
+      const double k0 = qk[q * 3 + 0], k1 = qk[q * 3 + 1], k2 = qk[q * 3 + 2];
+      double yv[NIT];
+#pragma unroll
+      for (int i = 0; i < NIT; i++) {
+        const int j = j0 + i * JS;
+        yv[i] = __ldg(m.b + j) + __ldg(m.W1 + j * 3 + 0) * k0 + __ldg(m.W1 + j * 3 + 1) * k1 +
+                __ldg(m.W1 + j * 3 + 2) * k2;
+      }
+#pragma unroll
+      for (int i = 0; i < NIT; i++) {
+        const int j = j0 + i * JS;
+        double z, s;
+        softplus_sig(yv[i], stab, z, s);
+        if (L > 1) {
+          sb[j * LDS + q] = s;
+          act[j * LDA + q] = z;
+        } else {
+          const double aj = __ldg(m.a + j);
+          act[j * LDA + q] = aj * s;
+          cb[j * LDS + q] = aj * s * (1.0 - s);
+        }
+      }
+    }
+    if (false)
+#endif
     for (int x = tid; x < W * Q; x += C::NTHR) {
       const int j = x / Q, q = x % Q;
       const double y = __ldg(m.b + j) + __ldg(m.W1 + j * 3 + 0) * qk[q * 3 + 0] +
@@ -249,6 +401,7 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
       }
     }
     __syncthreads();
+    STAGE_MARK(2)
 
     // ---- stage 3: value pass, layers 2..L --------------------------------------------
     {
@@ -259,8 +412,10 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
       for (int j = 0; j < C::NT_V; j++) ncol[j] = (vn * C::NT_V + j) * 8;
       for (int l = 2; l <= L; l++) {
         double acc[C::MT_V][C::NT_V][2];
-        warp_gemm<C::MT_V, C::NT_V, KT2>(m.Wfrag + (l - 2) * frag_layer, mt0, act, LDA, ncol, acc);
+        warp_gemm<C::MT_V, C::NT_V, KT2, C::PD_V>(m.Wfrag + (l - 2) * frag_layer, mt0, act, LDA, ncol, acc);
         __syncthreads();
+        frag_prefetch<C::MT_V, KT2, COMMET_FRAG_PF + (COMMET_FRAG_PF == 0)>(
+            m.Wfrag + (l < L ? (l - 1) * frag_layer : (L - 2) * frag_layer + (size_t)W * W), mt0);
 #pragma unroll
         for (int i = 0; i < C::MT_V; i++) {
           const int j = (mt0 + i) * 8 + g;
@@ -306,6 +461,7 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
       }
     }
 
+    STAGE_MARK(3)
     // ---- stage 4: adjoint pass, layers L..2 --------------------------------------------
     {
       const int vm = warp / C::VNG, vn = warp % C::VNG;
@@ -324,8 +480,14 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
           gsk[tid * 3] += s0; gsk[tid * 3 + 1] += s1; gsk[tid * 3 + 2] += s2;
         }
         double acc[C::MT_V][C::NT_V][2];
-        warp_gemm<C::MT_V, C::NT_V, KT2>(m.Wfrag + (l - 2) * frag_layer + (size_t)W * W, mt0, act, LDA, ncol, acc);
+        warp_gemm<C::MT_V, C::NT_V, KT2, C::PD_V>(m.Wfrag + (l - 2) * frag_layer + (size_t)W * W, mt0, act, LDA, ncol,
+                                                 acc);
         __syncthreads();
+        if (l > 2)
+          frag_prefetch<C::MT_V, KT2, COMMET_FRAG_PF + (COMMET_FRAG_PF == 0)>(
+              m.Wfrag + (l - 3) * frag_layer + (size_t)W * W, mt0);
+        else
+          frag_prefetch<C::MT_J, KT2, (COMMET_FRAG_PF + 1) / 2>(m.Wfrag, (warp / C::QB) * C::MT_J);
         if (l > 2) {
 #pragma unroll
           for (int i = 0; i < C::MT_V; i++) {
@@ -395,6 +557,7 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
       }
     }
 
+    STAGE_MARK(4)
     // ---- stage 5: g = W1^T mu_1 + skips, H_1 = sum_j c1_j W1_j W1_j^T ------------------
     if (L > 1) {
       if (tid < Q) {
@@ -438,13 +601,24 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
     }
     __syncthreads();
 
+    STAGE_MARK(5)
     // ---- stage 6: Jacobian pass, H += J_l^T diag(c_l) J_l -------------------------------
     if (L > 1) {
-      for (int x = tid; x < W * Q; x += C::NTHR) {  // D_1 = s_1 (.) W1
-        const int j = x / Q, q = x % Q;
-        const double s = sb[j * LDS + q];
+      {  // D_1 = s_1 (.) W1: one qp per thread, weights loaded up front
+        constexpr int NIT = W * Q / C::NTHR, JS = C::NTHR / Q;
+        const int q = tid % Q, j0 = tid / Q;
+        double w1v[NIT][3];
 #pragma unroll
-        for (int c = 0; c < 3; c++) act[j * LDA + c * Q + q] = s * __ldg(m.W1 + j * 3 + c);
+        for (int i = 0; i < NIT; i++)
+#pragma unroll
+          for (int c = 0; c < 3; c++) w1v[i][c] = __ldg(m.W1 + (j0 + i * JS) * 3 + c);
+#pragma unroll
+        for (int i = 0; i < NIT; i++) {
+          const int j = j0 + i * JS;
+          const double s = sb[j * LDS + q];
+#pragma unroll
+          for (int c = 0; c < 3; c++) act[j * LDA + c * Q + q] = s * w1v[i][c];
+        }
       }
       __syncthreads();
       const int jm = warp / C::QB, qb = warp % C::QB;
@@ -459,8 +633,9 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
         for (int x = 0; x < 6; x++) hp[h][x] = 0.0;
       for (int l = 2; l <= L; l++) {
         double acc[C::MT_J][3][2];
-        warp_gemm<C::MT_J, 3, KT2>(m.Wfrag + (l - 2) * frag_layer, mt0, act, LDA, ncol, acc);
+        warp_gemm<C::MT_J, 3, KT2, C::PD_J>(m.Wfrag + (l - 2) * frag_layer, mt0, act, LDA, ncol, acc);
         __syncthreads();
+        if (l < L) frag_prefetch<C::MT_J, KT2, (COMMET_FRAG_PF + 1) / 2>(m.Wfrag + (l - 1) * frag_layer, mt0);
 #pragma unroll
         for (int i = 0; i < C::MT_J; i++) {
           const int j = (mt0 + i) * 8 + g;
@@ -507,7 +682,17 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
       __syncthreads();
     }
 
+    STAGE_MARK(6)
+#ifdef COMMET_EXP_SKIP_NCM
+    }
+#endif
+#ifdef COMMET_EXP_SKIP_ELEM
+    if (false) {
+#endif
     // ---- stage 7a: per qp -- penalty, S, T, Phi_m, Psi_m, b, P (all scaled by w) --------
+#if COMMET_PREFETCH
+    if (batch + gridDim.x < n_batches) pf_load_a(batch + gridDim.x);
+#endif
     if (tid < Q) {
       const int q = tid;
       double gq[3], H6[6];
@@ -529,6 +714,7 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
     }
     __syncthreads();
 
+    STAGE_MARK(7)
     // ---- stage 7b: A_q (81 entries, scaled by w), one (q, iJ) row per item ------------------
     for (int it = tid; it < Q * 9; it += C::NTHR) {
       const int q = it / 9, iJ = it % 9;
@@ -536,30 +722,14 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
     }
     __syncthreads();
 
+    STAGE_MARK(8)
+#if COMMET_PREFETCH
+    if (batch + gridDim.x < n_batches) pf_load_b();
+#endif
     if constexpr (C::DMMA_ELEM) {
-    // ---- stage 8a (DMMA): X_q[a][(i,k,L)] = sum_J dN_q[a][J] A_q[(i,J)][(k,L)]: per qp one
-    //      m8n8k4 per (node tile, 8 columns of the 27), J padded to 4 with zeros
-    {
-      constexpr int MTE = (NEN + 7) / 8;
-      for (int task = warp; task < Q * MTE * 4; task += C::NWARP) {
-        const int nt = task % 4, mt = (task / 4) % MTE, q = task / (4 * MTE);
-        const int a = 8 * mt + g, n = 8 * nt + g;
-        const double av = (t < 3 && a < NEN) ? sgN[(q * NEN + a) * 3 + t] : 0.0;
-        const double bv = (t < 3 && n < 27) ? qA[q * 81 + (3 * (n / 9) + t) * 9 + n % 9] : 0.0;
-        double c[2] = {0.0, 0.0};
-        dmma(c, av, bv);
-        const int ar = 8 * mt + g;
-#pragma unroll
-        for (int h = 0; h < 2; h++) {
-          const int nc = 8 * nt + 2 * t + h;
-          if (ar < NEN && nc < 27) Xb[(q * NEN + ar) * 27 + nc] = c[h];
-        }
-      }
-    }
-    __syncthreads();
-
-    // ---- stage 8b (DMMA): K_ik[a][b] = sum_(q,L) X_q[a][(i,k,L)] dN_q[b][L] for i <= k
-    //      (K_ki = K_ik^T), M = a, N = b, K = (q, L); r_e; RED scatter (+ mirror for i < k)
+    // ---- stage 8 (DMMA): K_ik[a][b] = sum_(q,J) dN_q[a][J] Y_q[J][b] for i <= k (K_ki = K_ik^T),
+    //      Y_q[J][b] = sum_L A_q[(i,J),(k,L)] dN_q[b][L] formed in the B fragment (3 FMA per
+    //      element); M = a, N = b, K = (q, J); r_e; RED scatter (+ mirror for i < k)
     {
       constexpr int MTE = (NEN + 7) / 8, KS = NQ * 3 / 4;
       constexpr int NIK = 6;
@@ -573,9 +743,14 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
         const int a = 8 * mt + g, bq = 8 * nt + g;
 #pragma unroll
         for (int kt = 0; kt < KS; kt++) {
-          const int kk = 4 * kt + t, q = e * NQ + kk / 3, L = kk % 3;
-          const double av = a < NEN ? Xb[(q * NEN + a) * 27 + 9 * i + 3 * k + L] : 0.0;
-          const double bv = bq < NEN ? sgN[(q * NEN + bq) * 3 + L] : 0.0;
+          const int kk = 4 * kt + t, q = e * NQ + kk / 3, J = kk % 3;
+          const double av = a < NEN ? sgN[(q * NEN + a) * 3 + J] : 0.0;
+          double bv = 0.0;
+          if (bq < NEN) {
+            const double* Ar = qA + q * 81 + (3 * i + J) * 9 + 3 * k;
+            const double* Gb = sgN + (q * NEN + bq) * 3;
+            bv = Ar[0] * Gb[0] + Ar[1] * Gb[1] + Ar[2] * Gb[2];
+          }
           dmma(c, av, bv);
         }
         const int64_t el = e0 + e;
@@ -713,13 +888,35 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
     }
 #endif
     }  // DMMA_ELEM
+#ifdef COMMET_EXP_SKIP_ELEM
+    }
+#endif
     __syncthreads();
+    STAGE_MARK(10)
   }
+#ifdef COMMET_STAGE_PROF
+  if (tid == 0)
+    for (int i = 0; i < 11; i++) atomicAdd(&g_stage_cycles[i], (unsigned long long)st_acc[i]);
+#endif
 }
 
 // ---------------------------------------------------------------------------
 // host side: dispatch and weight fragments
 // ---------------------------------------------------------------------------
+
+#ifdef COMMET_STAGE_PROF
+}  // namespace commet
+extern "C" int commet_debug_stage_cycles(unsigned long long* out, int reset) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out, commet::g_stage_cycles, 11 * sizeof(unsigned long long));
+  if (reset) {
+    unsigned long long z[16] = {0};
+    cudaMemcpyToSymbol(commet::g_stage_cycles, z, sizeof(z));
+  }
+  return 0;
+}
+namespace commet {
+#endif
 
 int fused_supported(int n_en, int n_q, int w, int L) {
   if (!((n_en == 8 && n_q == 8) || (n_en == 10 && n_q == 4))) return 0;

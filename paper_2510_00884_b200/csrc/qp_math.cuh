@@ -142,6 +142,16 @@ __device__ __forceinline__ void tangent_row(const double* __restrict__ post, int
   }
 }
 
+// One entry (iJ, kL) of w A (= tangent_row(post, 3 i + J, .)[kL])
+__device__ __forceinline__ double tangent_entry(const double* __restrict__ post, int i, int J, int kL) {
+  const int iJ = 3 * i + J, kk = kL / 3, L = kL % 3;
+  double v = post[27 + iJ] * post[54 + kL] + post[36 + iJ] * post[63 + kL] + post[45 + iJ] * post[72 + kL];
+  v += post[90] * post[i * 3 + L] * post[kk * 3 + J] + post[91] * post[9 + i * 3 + L] * post[9 + kk * 3 + J];
+  if (J == L) v += post[90] * post[81 + i * 3 + kk];
+  if (i == kk) v += post[18 + J * 3 + L];
+  return v;
+}
+
 // Whole tangent of one qp (simple kernel): P[9] and A[81], both scaled by w.
 __device__ __forceinline__ void stress_tangent(const Kin& k, const double* __restrict__ g,
                                                const double* __restrict__ H6, double w,

@@ -53,6 +53,15 @@ def run(path, cfg, steps=20):
     lib.commet_kernel_times(ctx, ms, steps)
     torch.cuda.synchronize()
     t = float(np.median(list(ms)))
+    if hasattr(lib, "commet_debug_stage_cycles") and os.environ.get("AB_STAGES"):
+        cyc = (C.c_ulonglong * 11)()
+        lib.commet_debug_stage_cycles(cyc, 1)
+        tot = sum(cyc)
+        names = ["0 stage-in", "1 kinem", "2 layer1", "3 value", "4 adjoint", "5 g/H1", "6 jacobian",
+                 "7a post", "7b A_q", "8a X", "8b K/scatter"]
+        print("  stage cycles (thread 0, summed over CTAs, %d steps + 3 warm-ups):" % steps)
+        for n_, c_ in zip(names, cyc):
+            print(f"    {n_:14s} {100.0 * c_ / tot:6.2f} %")
     res = (r.cpu().numpy(), v.cpu().numpy())
     lib.commet_destroy(ctx)
     return t, res
