@@ -212,6 +212,76 @@ commet_status commet_plan_recv(commet_plan p, int32_t k, int32_t* peer, int64_t*
 commet_status commet_plan_colours(commet_plan p, const int64_t** colour_start, const int64_t** perm);
 void commet_plan_destroy(commet_plan p);
 
+/* Max over all quadrature points of tr C = I1 at the last commet_assemble
+ * (synchronises its stream).  The paper's twist-cube robustness check reports
+ * tr C > 16 (Fig. 7 caption). */
+commet_status commet_max_trace_C(commet_ctx ctx, double* max_trC);
+
+/* ---- material-point calls on the ctx's NCM ------------------------------------
+ * The inner network's gradient g = dN/dk [n][3] and Hessian H [n][6] (upper:
+ * 00,01,02,11,12,22) at n invariant inputs k = (I1-3, I2-3, J-1) [n][3] (device
+ * arrays), by Alg. 4; output skip included, penalty and
+ * ref_shift excluded.  Asynchronous on cuda_stream. */
+commet_status commet_ncm_eval(commet_ctx ctx, const double* k, double* g, double* H, int64_t n,
+                              void* cuda_stream);
+/* Stress-free reference (reading R11): sets the ctx's ref_shift to
+ * s0 = 2 g1 + 4 g2 + g3 at k = 0, so that S(F = I) = 0 for subsequent assembles,
+ * and returns it in *s0 (may be NULL).  Synchronous. */
+commet_status commet_normalize_reference(commet_ctx ctx, double* s0);
+
+/* ---- Newton-Raphson around the assembly --------------
+ * d <- d + Delta d with K Delta d = -r, the linear system solved
+ * by conjugate gradients with Jacobi preconditioning, all on the
+ * GPU.  Single GPU only (n_ranks <= 1; otherwise COMMET_ERR_ARG).
+ *
+ * Dirichlet conditions are a fixed set of constrained GLOBAL dofs.  Elimination is
+ * the symmetric one for Newton increments: once u carries the prescribed values the
+ * increment vanishes on constrained dofs, so their rows AND columns of K are zeroed,
+ * the diagonal set to 1 and the residual entries set to 0 (K stays SPD when the
+ * free block is). */
+commet_status commet_set_dirichlet(commet_ctx ctx, const int64_t* dofs /* host [n] */, int64_t n);
+/* Eliminate in place: csr_values device [nnz] (this ctx's pattern), residual device
+ * [n_rows] or NULL.  Asynchronous on cuda_stream. */
+commet_status commet_apply_dirichlet(commet_ctx ctx, double* residual, double* csr_values, void* cuda_stream);
+/* Solve K x = b (K: csr_values on this ctx's pattern, device; b, x device [n_rows])
+ * from x = 0 with Jacobi-preconditioned CG until ||b - K x||_2 <= rtol ||b||_2.
+ * Synchronous.  *iters, *rel_res (may be NULL) report the outcome.  Errors:
+ * COMMET_ERR_DOMAIN if a diagonal entry is <= 0 (message names the row) or the
+ * tolerance is not met in max_iter iterations (x holds the last iterate). */
+commet_status commet_cg_jacobi(commet_ctx ctx, const double* csr_values, const double* b, double* x,
+                               double rtol, int32_t max_iter, int32_t* iters, double* rel_res,
+                               void* cuda_stream);
+
+#define COMMET_NEWTON_MAX_LOG 64
+typedef struct {
+  double atol, rtol;      /* converged when ||r_free||_2 <= max(atol, rtol ||r_free^(0)||_2) */
+  int32_t max_iter;       /* linear solves per call, 1 .. COMMET_NEWTON_MAX_LOG-1 */
+  double cg_rtol;         /* CG relative tolerance per linear solve */
+  int32_t cg_max_iter;
+} commet_newton_cfg;
+
+typedef struct {
+  int32_t iters;          /* linear solves performed */
+  int32_t converged;      /* 1 if the residual criterion was met */
+  int32_t n_assemble;     /* assemblies (= iters + 1) */
+  int64_t cg_iters_total;
+  double res_norm[COMMET_NEWTON_MAX_LOG];  /* ||r_free|| after each assembly, [0..iters] */
+  int32_t cg_iters[COMMET_NEWTON_MAX_LOG]; /* CG iterations of each linear solve */
+  double max_trC;         /* max tr C over qps at the final iterate */
+  double ms_assemble;     /* device time: assembly + elimination, summed */
+  double ms_solve;        /* device time: CG + update, summed */
+} commet_newton_report;
+
+/* One load step of Newton-Raphson to u[dirichlet dofs] = bc_values (host [n]):
+ * iteration 0 is the consistent predictor -- r, K = assemble(u) at the previous u,
+ * r += K dc with dc the prescribed increment (zero on free dofs), u[dofs] = bc_values
+ * (reading R20) -- then every iteration: eliminate; stop if converged;
+ * CG: K du = r; u -= du; r, K = assemble(u).
+ * u: device [3 n_nodes], in/out.  Synchronous.  Errors: COMMET_ERR_DOMAIN (det F <= 0
+ * at some qp, or CG failure; the message says which), COMMET_ERR_ARG. */
+commet_status commet_newton_step(commet_ctx ctx, const double* bc_values, const commet_newton_cfg* cfg,
+                                 double* u, commet_newton_report* report, void* cuda_stream);
+
 /* Diagnostic: evaluates the kernels' activation on n device values y:
  * z = softplus(y) = log(1+e^y), s = sigmoid(y) (device fp64 arrays).
  * Asynchronous on cuda_stream.  Used by the tests to pin the table-driven

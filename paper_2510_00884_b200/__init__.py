@@ -33,7 +33,9 @@ SYMBOLS = ("commet_setup", "commet_csr_pattern", "commet_csr_pattern_copy", "com
            "commet_halo_info", "commet_halo_send", "commet_halo_recv", "commet_halo_unpack",
            "commet_plan_create", "commet_plan_info", "commet_plan_csr", "commet_plan_halo",
            "commet_plan_send", "commet_plan_recv", "commet_plan_colours", "commet_plan_destroy",
-           "commet_kernel_info")
+           "commet_kernel_info", "commet_max_trace_C", "commet_set_dirichlet", "commet_apply_dirichlet",
+           "commet_cg_jacobi", "commet_newton_step", "commet_ncm_eval", "commet_normalize_reference")
+NEWTON_MAX_LOG = 64
 
 
 class MeshDesc(C.Structure):
@@ -49,6 +51,18 @@ class NcmDesc(C.Structure):
     _fields_ = [("n_hidden", C.c_int32), ("width", C.c_int32), ("W1", C.c_void_p), ("W", C.c_void_p),
                 ("b", C.c_void_p), ("a", C.c_void_p), ("skip_out", C.c_void_p),
                 ("skip_hidden", C.c_void_p), ("kappa", C.c_double), ("ref_shift", C.c_double)]
+
+
+class NewtonCfg(C.Structure):
+    _fields_ = [("atol", C.c_double), ("rtol", C.c_double), ("max_iter", C.c_int32), ("cg_rtol", C.c_double),
+                ("cg_max_iter", C.c_int32)]
+
+
+class NewtonReport(C.Structure):
+    _fields_ = [("iters", C.c_int32), ("converged", C.c_int32), ("n_assemble", C.c_int32),
+                ("cg_iters_total", C.c_int64), ("res_norm", C.c_double * NEWTON_MAX_LOG),
+                ("cg_iters", C.c_int32 * NEWTON_MAX_LOG), ("max_trC", C.c_double), ("ms_assemble", C.c_double),
+                ("ms_solve", C.c_double)]
 
 
 _vp, _i64, _i32 = C.c_void_p, C.c_int64, C.c_int32
@@ -96,6 +110,16 @@ for _f in ("commet_nccl_unique_id", "commet_nccl_comm_init", "commet_nccl_comm_d
     getattr(_lib, _f).restype = C.c_int
 _lib.commet_kernel_info.argtypes = [_vp, _P(_i32), _P(_i32), _P(_i32)]
 _lib.commet_kernel_info.restype = C.c_int
+_lib.commet_max_trace_C.argtypes = [_vp, _P(C.c_double)]
+_lib.commet_set_dirichlet.argtypes = [_vp, _vp, _i64]
+_lib.commet_apply_dirichlet.argtypes = [_vp, _vp, _vp, _vp]
+_lib.commet_cg_jacobi.argtypes = [_vp, _vp, _vp, _vp, C.c_double, _i32, _P(_i32), _P(C.c_double), _vp]
+_lib.commet_newton_step.argtypes = [_vp, _vp, _P(NewtonCfg), _vp, _P(NewtonReport), _vp]
+_lib.commet_ncm_eval.argtypes = [_vp, _vp, _vp, _vp, _i64, _vp]
+_lib.commet_normalize_reference.argtypes = [_vp, _P(C.c_double)]
+for _f in ("commet_ncm_eval", "commet_normalize_reference", "commet_max_trace_C", "commet_set_dirichlet", "commet_apply_dirichlet", "commet_cg_jacobi",
+           "commet_newton_step"):
+    getattr(_lib, _f).restype = C.c_int
 _lib.commet_last_error.argtypes = [_vp]
 _lib.commet_last_error.restype = C.c_char_p
 _lib.commet_destroy.argtypes = [_vp]
@@ -254,6 +278,71 @@ class Commet:
         st = stream if stream is not None else t.cuda.current_stream(self.device)
         _check(_lib.commet_halo_unpack(self.ctx, k, vals_ptr, res_ptr, residual.data_ptr(), values.data_ptr(),
                                        st.cuda_stream), self.ctx)
+
+    def max_trace_C(self) -> float:
+        """max over qps of tr C at the last assemble (synchronises)."""
+        v = C.c_double()
+        _check(_lib.commet_max_trace_C(self.ctx, C.byref(v)), self.ctx)
+        return v.value
+
+    # -- material-point calls ----------------------------------------------------------
+    def ncm_eval(self, k, stream=None):
+        """Inner-network gradient [n,3] and Hessian [n,6] at invariant inputs k (cuda [n,3])."""
+        t = self.torch
+        k = k.contiguous()
+        n = k.shape[0]
+        g = t.empty((n, 3), dtype=t.float64, device=k.device)
+        H = t.empty((n, 6), dtype=t.float64, device=k.device)
+        st = stream if stream is not None else t.cuda.current_stream(self.device)
+        _check(_lib.commet_ncm_eval(self.ctx, k.data_ptr(), g.data_ptr(), H.data_ptr(), n, st.cuda_stream),
+               self.ctx)
+        return g, H
+
+    def normalize_reference(self) -> float:
+        """Make F = I stress-free (sets ref_shift); returns s0."""
+        v = C.c_double()
+        _check(_lib.commet_normalize_reference(self.ctx, C.byref(v)), self.ctx)
+        return v.value
+
+    # -- Newton-Raphson around the assembly (single GPU) -----------------------------
+    def set_dirichlet(self, dofs):
+        """Constrained global dofs (host int array)."""
+        d = np.ascontiguousarray(dofs, dtype=np.int64)
+        _check(_lib.commet_set_dirichlet(self.ctx, _ptr(d), d.size), self.ctx)
+        self.n_dirichlet = d.size
+
+    def apply_dirichlet(self, residual, values, stream=None):
+        t = self.torch
+        st = stream if stream is not None else t.cuda.current_stream(self.device)
+        _check(_lib.commet_apply_dirichlet(self.ctx, None if residual is None else residual.data_ptr(),
+                                           values.data_ptr(), st.cuda_stream), self.ctx)
+
+    def cg_jacobi(self, values, b, rtol=1e-10, max_iter=100000, x=None, stream=None):
+        """Solve K x = b on this ctx's pattern (device tensors). -> (x, iters, rel_res)."""
+        t = self.torch
+        if x is None:
+            x = t.empty_like(b)
+        st = stream if stream is not None else t.cuda.current_stream(self.device)
+        it, rel = _i32(), C.c_double()
+        _check(_lib.commet_cg_jacobi(self.ctx, values.data_ptr(), b.data_ptr(), x.data_ptr(), rtol, max_iter,
+                                     C.byref(it), C.byref(rel), st.cuda_stream), self.ctx)
+        return x, it.value, rel.value
+
+    def newton_step(self, u, bc_values, atol=1e-10, rtol=1e-10, max_iter=30, cg_rtol=1e-10,
+                    cg_max_iter=200000, stream=None):
+        """One load step: u[dirichlet] = bc_values, Newton iterations until converged.
+        u: cuda fp64 tensor [3 n_nodes] (in/out).  -> report dict."""
+        t = self.torch
+        bv = np.ascontiguousarray(bc_values, dtype=np.float64)
+        cfg = NewtonCfg(atol, rtol, max_iter, cg_rtol, cg_max_iter)
+        rep = NewtonReport()
+        st = stream if stream is not None else t.cuda.current_stream(self.device)
+        _check(_lib.commet_newton_step(self.ctx, _ptr(bv), C.byref(cfg), u.data_ptr(), C.byref(rep),
+                                       st.cuda_stream), self.ctx)
+        n = rep.iters
+        return dict(iters=n, converged=bool(rep.converged), res_norm=list(rep.res_norm[:n + 1]),
+                    cg_iters=list(rep.cg_iters[:n]), cg_iters_total=rep.cg_iters_total, max_trC=rep.max_trC,
+                    ms_assemble=rep.ms_assemble, ms_solve=rep.ms_solve)
 
     def check(self) -> int:
         """-1 if every det F > 0, else the lowest flat e*n_q+q with det F <= 0."""

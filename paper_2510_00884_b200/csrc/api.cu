@@ -17,92 +17,13 @@
 
 #include "commet.h"
 #include "commet_internal.h"
+#include "ctx.h"
 #include "plan.h"
 #include "qp_math.cuh"
 
 using namespace commet;
 
-namespace {
-
-thread_local std::string g_last_error;
-
-template <class T>
-struct DevBuf {
-  T* p = nullptr;
-  size_t n = 0;
-  ~DevBuf() { if (p) cudaFree(p); }
-  cudaError_t alloc(size_t count) {
-    n = count;
-    return count ? cudaMalloc(&p, count * sizeof(T)) : cudaSuccess;
-  }
-};
-
-}  // namespace
-
-struct commet_ctx_s {
-  int device = 0;
-  Plan plan;  // host copy (pattern, maps); element-order arrays are dropped after upload
-  int kernel = COMMET_KERNEL_FUSED;
-  std::string err;
-  cudaStream_t last_stream = nullptr;
-  ncclComm_t comm = nullptr;
-  // device data
-  DevBuf<int32_t> conn, lrow, col_idx;
-  DevBuf<double> gradN, qp_w;
-  DevBuf<uint8_t> slot;
-  DevBuf<int64_t> orig, node_rs, row_ptr;
-  DevBuf<int32_t> node_deg;
-  DevBuf<double> W1, b, a, skip_out, skip_h, Wrow, Wfrag, act_tab, gfrag;
-  DevBuf<double> r_halo, v_halo, r_recv, v_recv;
-  DevBuf<int64_t> recv_val_map, recv_row_map;
-  DevBuf<unsigned long long> bad;
-  NcmDev ncm{};
-  // timing ring
-  std::vector<cudaEvent_t> ev0, ev1;
-  int64_t n_assembled = 0;
-  ~commet_ctx_s() {
-    for (auto e : ev0) cudaEventDestroy(e);
-    for (auto e : ev1) cudaEventDestroy(e);
-  }
-};
-
-struct commet_plan_s {
-  Plan p;
-};
-
-static commet_status fail(commet_ctx c, commet_status s, const char* fmt, ...) {
-  char buf[512];
-  va_list ap;
-  va_start(ap, fmt);
-  vsnprintf(buf, sizeof buf, fmt, ap);
-  va_end(ap);
-  if (c) c->err = buf;
-  g_last_error = buf;
-  return s;
-}
-
-#define CUDA_TRY(ctx, x)                                                                     \
-  do {                                                                                       \
-    cudaError_t e_ = (x);                                                                    \
-    if (e_ != cudaSuccess)                                                                   \
-      return fail(ctx, e_ == cudaErrorMemoryAllocation ? COMMET_ERR_OOM : COMMET_ERR_CUDA,    \
-                  "CUDA error %s at %s:%d (%s)", cudaGetErrorString(e_), __FILE__, __LINE__, #x); \
-  } while (0)
-
-#define NCCL_TRY(ctx, x)                                                                           \
-  do {                                                                                             \
-    ncclResult_t r_ = (x);                                                                         \
-    if (r_ != ncclSuccess)                                                                         \
-      return fail(ctx, COMMET_ERR_NCCL, "NCCL error %s at %s:%d (%s)", ncclGetErrorString(r_), __FILE__, \
-                  __LINE__, #x);                                                                   \
-  } while (0)
-
-template <class T>
-static commet_status upload(commet_ctx c, DevBuf<T>& d, const T* h, size_t n, cudaStream_t st) {
-  CUDA_TRY(c, d.alloc(n));
-  if (n) CUDA_TRY(c, cudaMemcpyAsync(d.p, h, n * sizeof(T), cudaMemcpyHostToDevice, st));
-  return COMMET_OK;
-}
+thread_local std::string commet_detail::g_last_error;
 
 // ---------------------------------------------------------------------------
 extern "C" commet_status commet_setup(const commet_mesh_desc* mesh, const commet_ncm_desc* ncm,
@@ -215,6 +136,7 @@ extern "C" commet_status commet_setup(const commet_mesh_desc* mesh, const commet
   c->ncm = NcmDev{L, w, c->W1.p, c->b.p, c->a.p, c->skip_out.p, c->skip_h.p, c->Wrow.p, c->Wfrag.p,
                   c->act_tab.p, c->gfrag.p, ncm->kappa, ncm->ref_shift};
   CUDA_TRY(C, c->bad.alloc(1));
+  CUDA_TRY(C, c->max_trc.alloc(1));
   CUDA_TRY(C, c->r_halo.alloc(3 * p.n_halo));
   CUDA_TRY(C, c->v_halo.alloc(p.nnz_halo));
   CUDA_TRY(C, c->r_recv.alloc(p.recv_row_map.size()));
@@ -307,6 +229,7 @@ extern "C" commet_status commet_assemble(commet_ctx c, const double* u, double* 
   CUDA_TRY(c, cudaMemsetAsync(residual, 0, 3 * p.n_owned * sizeof(double), st));
   CUDA_TRY(c, cudaMemsetAsync(csr_values, 0, p.nnz * sizeof(double), st));
   CUDA_TRY(c, cudaMemsetAsync(c->bad.p, 0xff, sizeof(unsigned long long), st));
+  CUDA_TRY(c, cudaMemsetAsync(c->max_trc.p, 0, sizeof(unsigned long long), st));
   if (p.n_halo) {
     CUDA_TRY(c, cudaMemsetAsync(c->r_halo.p, 0, c->r_halo.n * sizeof(double), st));
     CUDA_TRY(c, cudaMemsetAsync(c->v_halo.p, 0, c->v_halo.n * sizeof(double), st));
@@ -329,6 +252,7 @@ extern "C" commet_status commet_assemble(commet_ctx c, const double* u, double* 
   a.r_halo = c->r_halo.p;
   a.v_halo = c->v_halo.p;
   a.bad = c->bad.p;
+  a.max_trc = c->max_trc.p;
   a.ncm = c->ncm;
   const int slot = c->ev0.empty() ? -1 : (int)(c->n_assembled % (int64_t)c->ev0.size());
   if (slot >= 0) CUDA_TRY(c, cudaEventRecord(c->ev0[slot], st));
@@ -374,6 +298,18 @@ extern "C" commet_status commet_check(commet_ctx c, int64_t* first_bad_qp) {
   const int64_t r = v == ~0ULL ? -1 : (int64_t)v;
   if (first_bad_qp) *first_bad_qp = r;
   if (r >= 0) return fail(c, COMMET_ERR_DOMAIN, "det F <= 0 at flat quadrature point %lld", (long long)r);
+  return COMMET_OK;
+}
+
+extern "C" commet_status commet_max_trace_C(commet_ctx c, double* max_trC) {
+  if (!c || !max_trC) return fail(c, COMMET_ERR_ARG, "ctx or max_trC is NULL");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  CUDA_TRY(c, cudaStreamSynchronize(c->last_stream));
+  unsigned long long v = 0;
+  CUDA_TRY(c, cudaMemcpy(&v, c->max_trc.p, sizeof v, cudaMemcpyDeviceToHost));
+  double d;
+  std::memcpy(&d, &v, sizeof d);
+  *max_trC = d;
   return COMMET_OK;
 }
 
@@ -607,7 +543,7 @@ extern "C" commet_status commet_selftest_activation(const double* y, double* z, 
 }
 
 extern "C" const char* commet_last_error(commet_ctx c) {
-  return c ? c->err.c_str() : g_last_error.c_str();
+  return c ? c->err.c_str() : commet_detail::g_last_error.c_str();
 }
 
 extern "C" void commet_destroy(commet_ctx c) {

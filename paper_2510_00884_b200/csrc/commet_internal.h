@@ -51,6 +51,7 @@ struct AsmArgs {
   double* r_halo;
   double* v_halo;
   unsigned long long* bad;
+  unsigned long long* max_trc;  // max over qps of tr C = I1 (> 0: the bit pattern orders like the value)
   NcmDev ncm;
 };
 

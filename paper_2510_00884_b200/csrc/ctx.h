@@ -1,0 +1,106 @@
+// ctx.h -- the library context (struct commet_ctx_s) and the error helpers
+// shared by the C ABI implementation files (api.cu, solver.cu).  Internal.
+#pragma once
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "commet.h"
+#include "commet_internal.h"
+#include "plan.h"
+
+using namespace commet;
+
+namespace commet_detail {
+extern thread_local std::string g_last_error;
+
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  ~DevBuf() { if (p) cudaFree(p); }
+  cudaError_t alloc(size_t count) {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = count;
+    return count ? cudaMalloc(&p, count * sizeof(T)) : cudaSuccess;
+  }
+};
+
+}  // namespace commet_detail
+using commet_detail::DevBuf;
+
+struct SolverWork;  // solver.cu: Dirichlet set, CG / Newton workspace
+void solver_work_free(SolverWork* w);
+
+struct commet_ctx_s {
+  int device = 0;
+  Plan plan;  // host copy (pattern, maps); element-order arrays are dropped after upload
+  int kernel = COMMET_KERNEL_FUSED;
+  std::string err;
+  cudaStream_t last_stream = nullptr;
+  ncclComm_t comm = nullptr;
+  // device data
+  DevBuf<int32_t> conn, lrow, col_idx;
+  DevBuf<double> gradN, qp_w;
+  DevBuf<uint8_t> slot;
+  DevBuf<int64_t> orig, node_rs, row_ptr;
+  DevBuf<int32_t> node_deg;
+  DevBuf<double> W1, b, a, skip_out, skip_h, Wrow, Wfrag, act_tab, gfrag;
+  DevBuf<double> r_halo, v_halo, r_recv, v_recv;
+  DevBuf<int64_t> recv_val_map, recv_row_map;
+  DevBuf<unsigned long long> bad, max_trc;
+  SolverWork* solver = nullptr;
+  NcmDev ncm{};
+  // timing ring
+  std::vector<cudaEvent_t> ev0, ev1;
+  int64_t n_assembled = 0;
+  ~commet_ctx_s() {
+    solver_work_free(solver);
+    for (auto e : ev0) cudaEventDestroy(e);
+    for (auto e : ev1) cudaEventDestroy(e);
+  }
+};
+
+struct commet_plan_s {
+  Plan p;
+};
+
+inline commet_status fail(commet_ctx c, commet_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (c) c->err = buf;
+  commet_detail::g_last_error = buf;
+  return s;
+}
+
+#define CUDA_TRY(ctx, x)                                                                     \
+  do {                                                                                       \
+    cudaError_t e_ = (x);                                                                    \
+    if (e_ != cudaSuccess)                                                                   \
+      return fail(ctx, e_ == cudaErrorMemoryAllocation ? COMMET_ERR_OOM : COMMET_ERR_CUDA,    \
+                  "CUDA error %s at %s:%d (%s)", cudaGetErrorString(e_), __FILE__, __LINE__, #x); \
+  } while (0)
+
+#define NCCL_TRY(ctx, x)                                                                           \
+  do {                                                                                             \
+    ncclResult_t r_ = (x);                                                                         \
+    if (r_ != ncclSuccess)                                                                         \
+      return fail(ctx, COMMET_ERR_NCCL, "NCCL error %s at %s:%d (%s)", ncclGetErrorString(r_), __FILE__, \
+                  __LINE__, #x);                                                                   \
+  } while (0)
+
+template <class T>
+inline commet_status upload(commet_ctx c, DevBuf<T>& d, const T* h, size_t n, cudaStream_t st) {
+  CUDA_TRY(c, d.alloc(n));
+  if (n) CUDA_TRY(c, cudaMemcpyAsync(d.p, h, n * sizeof(T), cudaMemcpyHostToDevice, st));
+  return COMMET_OK;
+}
+

@@ -336,8 +336,10 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
         }
       Kin kin;
       kinematics(F, kin);
-      if (e < ne && !(kin.J > 0.0))
-        atomicMin(A.bad, (unsigned long long)(__ldg(A.orig + e0 + e) * NQ + q % NQ));
+      if (e < ne) {
+        if (!(kin.J > 0.0)) atomicMin(A.bad, (unsigned long long)(__ldg(A.orig + e0 + e) * NQ + q % NQ));
+        atomicMax(A.max_trc, (unsigned long long)__double_as_longlong(kin.I1));
+      }
 #pragma unroll
       for (int x = 0; x < 9; x++) qF[q * 9 + x] = F[x];
       qk[q * 3 + 0] = kin.I1 - 3.0;

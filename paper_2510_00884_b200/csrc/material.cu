@@ -1,0 +1,57 @@
+// material.cu -- material-point calls on the ctx's NCM (SURVEY.md s8(f) rank 3
+// groundwork): the inner network's gradient and Hessian on a batch of invariant
+// inputs k (Alg. 4), and the stress-free reference
+// normalisation of DESIGN.md reading R11 (s0 = 2 g1 + 4 g2 + g3 at k = 0, so that
+// S(F = I) = (2 g1 + 4 g2 + g3 - s0) I = 0).
+#include <cuda_runtime.h>
+
+#include "ctx.h"
+#include "ncm_alg4.cuh"
+
+namespace {
+
+__global__ void ncm_eval_kernel(NcmDev m, const double* __restrict__ k, double* __restrict__ g,
+                                double* __restrict__ H, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double gi[3], Hi[6];
+    ncm_alg4(m, k + 3 * i, gi, Hi);
+    for (int p = 0; p < 3; p++) g[3 * i + p] = gi[p];
+    for (int p = 0; p < 6; p++) H[6 * i + p] = Hi[p];
+  }
+}
+
+__global__ void ref_shift_kernel(NcmDev m, double* out) {
+  const double k0[3] = {0.0, 0.0, 0.0};
+  double g[3], H[6];
+  ncm_alg4(m, k0, g, H);
+  out[0] = 2.0 * g[0] + 4.0 * g[1] + g[2];  // the penalty's 2 kappa (J - 1) vanishes at J = 1
+}
+
+}  // namespace
+
+extern "C" commet_status commet_ncm_eval(commet_ctx c, const double* k, double* g, double* H, int64_t n,
+                                         void* cuda_stream) {
+  if (!c) return fail(nullptr, COMMET_ERR_ARG, "ctx is NULL");
+  if (n < 0 || (n > 0 && (!k || !g || !H))) return fail(c, COMMET_ERR_ARG, "k, g or H NULL, or n < 0");
+  if (n == 0) return COMMET_OK;
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  const int64_t nb = std::min<int64_t>((n + 63) / 64, 148 * 16);
+  ncm_eval_kernel<<<(unsigned)nb, 64, 0, (cudaStream_t)cuda_stream>>>(c->ncm, k, g, H, n);
+  CUDA_TRY(c, cudaGetLastError());
+  return COMMET_OK;
+}
+
+extern "C" commet_status commet_normalize_reference(commet_ctx c, double* s0) {
+  if (!c) return fail(nullptr, COMMET_ERR_ARG, "ctx is NULL");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  DevBuf<double> d;
+  CUDA_TRY(c, d.alloc(1));
+  NcmDev m = c->ncm;
+  ref_shift_kernel<<<1, 1>>>(m, d.p);
+  CUDA_TRY(c, cudaGetLastError());
+  double h = 0.0;
+  CUDA_TRY(c, cudaMemcpy(&h, d.p, sizeof h, cudaMemcpyDeviceToHost));
+  c->ncm.ref_shift = h;
+  if (s0) *s0 = h;
+  return COMMET_OK;
+}
