@@ -107,7 +107,22 @@ typedef struct {
   const double* skip_hidden;   /* host [L-1][w][3] or NULL (= 0): hidden skips B^(l), l >= 2 */
   double kappa;                /* volumetric penalty kappa (J-1)^2 */
   double ref_shift;            /* s0: adds -s0 (J-1) to W; 0 = off (reading R11) */
+  /* ---- variants; a zero-initialised tail = the ICNN on k above ---- */
+  int32_t kinematics;          /* COMMET_KIN_STANDARD: k = (I1-3, I2-3, J-1);
+                                  COMMET_KIN_ISOCHORIC: k = (Ibar1-3, Ibar2-3, J-1), Ibar1 = J^-2/3 I1,
+                                  Ibar2 = J^-4/3 I2 (App. A.2.2) */
+  int32_t network;             /* COMMET_NET_ICNN (the fields above), COMMET_NET_CANN, COMMET_NET_GENT_THOMAS */
+  int32_t cann_n;              /* CANN: branches per kinematic input, 1..16 */
+  const int32_t* cann_f;       /* CANN host [3][cann_n][3]: f0 (0 x, 1 <x>, 2 |x|), f1 power (1..3),
+                                  f2 (0 w1 x, 1 exp(w1 x) - 1, 2 -ln(1 - w1 x))  (Eq. cann-fs) */
+  const double* cann_w1;       /* CANN host [3][cann_n] */
+  const double* cann_w2;       /* CANN host [3][cann_n]: N = sum_m sum_b w2 f2(f1(f0(k_m)); w1)  (Eq. cann-def) */
+  double gt[3];                /* Gent-Thomas (App. C): N = gt0 k1 + gt1 ln(1 + k2/3) + gt2 k3^2
+                                  (the paper's model: gt = (0.5, 1, 1), isochoric kinematics, kappa = 0) */
 } commet_ncm_desc;
+
+enum { COMMET_KIN_STANDARD = 0, COMMET_KIN_ISOCHORIC = 1 };
+enum { COMMET_NET_ICNN = 0, COMMET_NET_CANN = 1, COMMET_NET_GENT_THOMAS = 2 };
 
 /* Kernel variants (commet_set_kernel).  FUSED is the product path; SIMPLE is
  * a one-thread-per-element CUDA kernel kept as an independent GPU cross-check. */

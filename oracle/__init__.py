@@ -31,7 +31,13 @@ class _Ncm(C.Structure):
     _fields_ = [("n_hidden", C.c_int32), ("width", C.c_int32),
                 ("W1", C.c_void_p), ("W", C.c_void_p), ("b", C.c_void_p), ("a", C.c_void_p),
                 ("skip_out", C.c_void_p), ("skip_hidden", C.c_void_p),
-                ("kappa", C.c_double), ("ref_shift", C.c_double)]
+                ("kappa", C.c_double), ("ref_shift", C.c_double),
+                ("kinematics", C.c_int32), ("network", C.c_int32), ("cann_n", C.c_int32),
+                ("cann_f", C.c_void_p), ("cann_w1", C.c_void_p), ("cann_w2", C.c_void_p),
+                ("gt", C.c_double * 3)]
+
+KIN = {"standard": 0, "isochoric": 1}
+NET = {"icnn": 0, "cann": 1, "gent_thomas": 2}
 
 
 _lib = None
@@ -70,9 +76,18 @@ class Ncm:
         self.arrays = {k: f(ncm.get(k)) for k in ("W1", "W", "b", "a", "skip_out", "skip_hidden")}
         if self.arrays["W"] is None or self.arrays["W"].size == 0:
             self.arrays["W"] = np.zeros(1)
-        self.s = _Ncm(int(ncm["n_hidden"]), int(ncm["width"]),
+        kin = ncm.get("kinematics", "standard")
+        net = ncm.get("network", "icnn")
+        self.cann_f = None if ncm.get("cann_f") is None else np.ascontiguousarray(ncm["cann_f"], dtype=np.int32)
+        for k in ("cann_w1", "cann_w2"):
+            self.arrays[k] = f(ncm.get(k))
+        gt = (C.c_double * 3)(*(ncm.get("gt") if ncm.get("gt") is not None else (0.0, 0.0, 0.0)))
+        self.s = _Ncm(int(ncm.get("n_hidden", 1)), int(ncm.get("width", 8)),
                       *[_p(self.arrays[k]) for k in ("W1", "W", "b", "a", "skip_out", "skip_hidden")],
-                      float(ncm.get("kappa", 0.0)), float(ncm.get("ref_shift", 0.0)))
+                      float(ncm.get("kappa", 0.0)), float(ncm.get("ref_shift", 0.0)),
+                      KIN[kin] if isinstance(kin, str) else int(kin), NET[net] if isinstance(net, str) else int(net),
+                      0 if self.cann_f is None else self.cann_f.shape[1], _p(self.cann_f),
+                      _p(self.arrays["cann_w1"]), _p(self.arrays["cann_w2"]), gt)
 
     @property
     def ptr(self):

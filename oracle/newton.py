@@ -57,9 +57,10 @@ def cg_jacobi(A, b, rtol=1e-10, max_iter=100000):
 
 
 def reference_shift(ncm: dict) -> float:
-    """s0 = 2 g1 + 4 g2 + g3 at k = 0 (R11): S(F = I) = 0 with -s0 (J - 1)."""
-    _, g, _ = oracle.ncm_eval(dict(ncm, ref_shift=0.0), np.zeros(3))
-    return 2.0 * g[0] + 4.0 * g[1] + g[2]
+    """s0 with S(F = I) = 0 once W gets -s0 (J - 1) (R11).  At F = I the
+    term adds -s0 J C^-1 = -s0 I to S, and S(I) = sigma I for an isotropic W, so
+    s0 = S_11(I) of the unshifted model (= 2 g1 + 4 g2 + g3 for standard inputs)."""
+    return float(oracle.material_point(dict(ncm, ref_shift=0.0), np.eye(3))["S"][0, 0])
 
 
 def newton_step(ncm, mesh, row_ptr, col_idx, u, dofs, values, atol=1e-10, rtol=1e-10, max_iter=30):

@@ -38,6 +38,14 @@ typedef struct {
   const double* skip_hidden; /* [L-1][w][3] or NULL: B^(k), k = 2..L */
   double kappa;              /* volumetric penalty kappa (J-1)^2 */
   double ref_shift;          /* s0: W -= s0 (J-1) (off when 0) */
+  int32_t kinematics;        /* 0: K = (I1-3, I2-3, J-1); 1: isochoric (Ibar1-3, Ibar2-3, J-1) (App. A.2.2) */
+  int32_t network;           /* 0: ICNN (Eq. icnn, Alg. 4); 1: CANN (Eq. cann-def); 2: Gent-Thomas (App. C) */
+  int32_t cann_n;            /* CANN: branches per kinematic input */
+  const int32_t* cann_f;     /* CANN [3][n][3]: f0 (0 id, 1 Macaulay, 2 abs), f1 power (1..3),
+                                f2 (0: w1 x, 1: exp(w1 x) - 1, 2: -ln(1 - w1 x))  (Eq. cann-fs) */
+  const double* cann_w1;     /* CANN [3][n] */
+  const double* cann_w2;     /* CANN [3][n] */
+  double gt[3];              /* Gent-Thomas: N = gt0 K1 + gt1 ln(1 + K2/3) + gt2 K3^2 */
 } oracle_ncm;
 
 /* ---------------------------------------------------------------------- */
@@ -60,8 +68,8 @@ static double sigmoid(double y) {
  * k >= 2 use A^(k) = W[k-2], B^(k) = skip_hidden[k-2] (reading 6: B is the
  * current layer's B^(k)).
  */
-int oracle_ncm_eval(const oracle_ncm* m, const double K[3], double* N_out, double g_out[3],
-                    double H_out[9]) {
+static int icnn_eval(const oracle_ncm* m, const double K[3], double* N_out, double g_out[3],
+                     double H_out[9]) {
   const int w = m->width, L = m->n_hidden;
   if (w < 1 || L < 1) return 1;
   const int nmax = w > 3 ? w : 3;
@@ -129,6 +137,70 @@ int oracle_ncm_eval(const oracle_ncm* m, const double K[3], double* N_out, doubl
   return 0;
 }
 
+/*
+ * CANN (Eq. cann-def / cann-chain-rule):
+ *   N = sum_m sum_k w2_km f2(f1(f0(K_m)); w1_km)
+ *   dN/dK_m   = sum_k w2 f2' f1' f0'
+ *   d2N/dK_m2 = sum_k w2 ((f2'' f1'^2 + f2' f1'') f0'^2 + f2' f1' f0''),  d2N/dK_m dK_n = 0 (m != n)
+ * f0 in {x, <x>, |x|} with f0' = {1, (1 + sign x)/2, sign x}, f0'' = 0; f1 = x^p;
+ * f2 in {w1 x, exp(w1 x) - 1, -ln(1 - w1 x)} with f2'' = {0, w1^2 exp(w1 x),
+ * +w1^2/(1 - w1 x)^2} (reading R22: the paper prints a minus sign on the last).
+ */
+static double sgn(double x) { return (x > 0) - (x < 0); }
+static int cann_eval(const oracle_ncm* m, const double K[3], double* N_out, double g[3], double H[9]) {
+  const int n = m->cann_n;
+  double N = 0.0;
+  for (int p = 0; p < 9; p++) H[p] = 0.0;
+  for (int mm = 0; mm < 3; mm++) {
+    g[mm] = 0.0;
+    for (int k = 0; k < n; k++) {
+      const int32_t* f = m->cann_f + ((size_t)mm * n + k) * 3;
+      const double w1 = m->cann_w1[mm * n + k], w2 = m->cann_w2[mm * n + k];
+      const double x = K[mm];
+      double v0, d0;
+      if (f[0] == 0) { v0 = x; d0 = 1.0; }
+      else if (f[0] == 1) { v0 = x > 0 ? x : 0.0; d0 = 0.5 * (1.0 + sgn(x)); }
+      else { v0 = fabs(x); d0 = sgn(x); }
+      const int pw = f[1];
+      const double v1 = pow(v0, pw), d1 = pw * pow(v0, pw - 1), dd1 = pw * (pw - 1) * (pw >= 2 ? pow(v0, pw - 2) : 0.0);
+      double v2, d2, dd2;
+      if (f[2] == 0) { v2 = w1 * v1; d2 = w1; dd2 = 0.0; }
+      else if (f[2] == 1) { v2 = exp(w1 * v1) - 1.0; d2 = w1 * exp(w1 * v1); dd2 = w1 * w1 * exp(w1 * v1); }
+      else { v2 = -log(1.0 - w1 * v1); d2 = w1 / (1.0 - w1 * v1); dd2 = w1 * w1 / ((1.0 - w1 * v1) * (1.0 - w1 * v1)); }
+      N += w2 * v2;
+      g[mm] += w2 * d2 * d1 * d0;
+      H[mm * 3 + mm] += w2 * ((dd2 * d1 * d1 + d2 * dd1) * d0 * d0 + d2 * d1 * 0.0);
+    }
+  }
+  if (m->skip_out)
+    for (int p = 0; p < 3; p++) {
+      N += m->skip_out[p] * K[p];
+      g[p] += m->skip_out[p];
+    }
+  *N_out = N;
+  return 0;
+}
+
+/* Gent-Thomas (App. C): Psi = 0.5 (Ibar1 - 3) + ln(Ibar2 / 3) + (J - 1)^2,
+ * i.e. N(K) = gt0 K1 + gt1 ln((K2 + 3) / 3) + gt2 K3^2 with gt = (0.5, 1, 1). */
+static int gt_eval(const oracle_ncm* m, const double K[3], double* N_out, double g[3], double H[9]) {
+  for (int p = 0; p < 9; p++) H[p] = 0.0;
+  *N_out = m->gt[0] * K[0] + m->gt[1] * log((K[1] + 3.0) / 3.0) + m->gt[2] * K[2] * K[2];
+  g[0] = m->gt[0];
+  g[1] = m->gt[1] / (K[1] + 3.0);
+  g[2] = 2.0 * m->gt[2] * K[2];
+  H[4] = -m->gt[1] / ((K[1] + 3.0) * (K[1] + 3.0));
+  H[8] = 2.0 * m->gt[2];
+  return 0;
+}
+
+int oracle_ncm_eval(const oracle_ncm* m, const double K[3], double* N_out, double g_out[3],
+                    double H_out[9]) {
+  if (m->network == 1) return cann_eval(m, K, N_out, g_out, H_out);
+  if (m->network == 2) return gt_eval(m, K, N_out, g_out, H_out);
+  return icnn_eval(m, K, N_out, g_out, H_out);
+}
+
 /* ---------------------------------------------------------------------- */
 /* kinematics + stress/tangent at one material point                       */
 /* ---------------------------------------------------------------------- */
@@ -150,6 +222,107 @@ static void inv3(const double M[9], double out[9]) {
   out[8] = (M[0] * M[4] - M[1] * M[3]) / d;
 }
 #define I4(i, j, k, l) ((((i) * 3 + (j)) * 3 + (k)) * 3 + (l))
+
+/*
+ * Isochoric kinematics (App. A.2.2) in the paper's SPATIAL form,
+ * pulled back to S and CC for the material-form assembly:
+ *   Fbar = J^-1/3 F, Bbar = Fbar Fbar^T, Ibar1 = tr Bbar, Ibar2 = (tr Bbar^2 - tr(Bbar^2))/2
+ *   Gbar1 = Bbar, GGbar1 = O;  Gbar2 = Bbar tr Bbar - Bbar^2, GGbar2 = Bbar(x)Bbar - Bbar(x)_Bbar
+ *   G^m = Gbar^m + e_m Ibar_m I,  e = (-1/3, -2/3)
+ *   GG^m = GGbar^m + e_m (I(x)Gbar^m + Gbar^m(x)I + Ibar_m (e_m I(x)I - I(x)_I))
+ *   J: G = J/2 I, GG = J/4 (I(x)I - 2 I(x)_I)
+ *   tau = 2 sum_m g_m G^m;  c = 4 sum_mn H_mn G^m(x)G^n + 4 sum_m g_m GG^m   (Eq. stress-cgo)
+ *   S = F^-1 tau F^-T;  CC_IJKL = F^-1_Ii F^-1_Jj F^-1_Kk F^-1_Ll c_ijkl  (App. A.1 pull-back)
+ * with (A(x)_B)_ijkl = 1/2 (A_ik B_jl + A_il B_jk) (reading 5).
+ */
+static void isochoric_S_CC(const double F[9], double Jd, const double g[3], const double H[9], double S[9],
+                           double CC[81]) {
+  const double a = pow(Jd, -2.0 / 3.0);
+  double Bb[9], Bb2[9], G[3][9], GG[3][81], Fi[9];
+  for (int i = 0; i < 3; i++)
+    for (int j = 0; j < 3; j++) {
+      double t = 0.0;
+      for (int K = 0; K < 3; K++) t += F[i * 3 + K] * F[j * 3 + K];
+      Bb[i * 3 + j] = a * t;
+    }
+  for (int i = 0; i < 3; i++)
+    for (int j = 0; j < 3; j++) {
+      double t = 0.0;
+      for (int k = 0; k < 3; k++) t += Bb[i * 3 + k] * Bb[k * 3 + j];
+      Bb2[i * 3 + j] = t;
+    }
+  const double Ib1 = Bb[0] + Bb[4] + Bb[8];
+  const double Ib2 = 0.5 * (Ib1 * Ib1 - (Bb2[0] + Bb2[4] + Bb2[8]));
+  const double Ib[2] = {Ib1, Ib2}, e[2] = {-1.0 / 3.0, -2.0 / 3.0};
+  double Gb[2][9], GGb[2][81];
+  for (int ij = 0; ij < 9; ij++) {
+    Gb[0][ij] = Bb[ij];
+    Gb[1][ij] = Bb[ij] * Ib1 - Bb2[ij];
+  }
+  for (int i = 0; i < 3; i++)
+    for (int j = 0; j < 3; j++)
+      for (int k = 0; k < 3; k++)
+        for (int l = 0; l < 3; l++) {
+          GGb[0][I4(i, j, k, l)] = 0.0;
+          GGb[1][I4(i, j, k, l)] = Bb[i * 3 + j] * Bb[k * 3 + l] -
+                                   0.5 * (Bb[i * 3 + k] * Bb[j * 3 + l] + Bb[i * 3 + l] * Bb[j * 3 + k]);
+        }
+  for (int mm = 0; mm < 2; mm++)
+    for (int i = 0; i < 3; i++)
+      for (int j = 0; j < 3; j++) {
+        G[mm][i * 3 + j] = Gb[mm][i * 3 + j] + e[mm] * Ib[mm] * (i == j);
+        for (int k = 0; k < 3; k++)
+          for (int l = 0; l < 3; l++) {
+            const double II = (double)((i == j) * (k == l));
+            const double IsI = 0.5 * ((i == k) * (j == l) + (i == l) * (j == k));
+            GG[mm][I4(i, j, k, l)] =
+                GGb[mm][I4(i, j, k, l)] +
+                e[mm] * ((i == j) * Gb[mm][k * 3 + l] + Gb[mm][i * 3 + j] * (k == l) + Ib[mm] * (e[mm] * II - IsI));
+          }
+      }
+  for (int i = 0; i < 3; i++)
+    for (int j = 0; j < 3; j++) {
+      G[2][i * 3 + j] = 0.5 * Jd * (i == j);
+      for (int k = 0; k < 3; k++)
+        for (int l = 0; l < 3; l++)
+          GG[2][I4(i, j, k, l)] = 0.25 * Jd * ((double)((i == j) * (k == l)) -
+                                                 ((i == k) * (j == l) + (i == l) * (j == k)));
+    }
+  double tau[9], c[81];
+  for (int ij = 0; ij < 9; ij++) {
+    double t = 0.0;
+    for (int mm = 0; mm < 3; mm++) t += g[mm] * G[mm][ij];
+    tau[ij] = 2.0 * t;
+  }
+  for (int ij = 0; ij < 9; ij++)
+    for (int kl = 0; kl < 9; kl++) {
+      double t = 0.0;
+      for (int mm = 0; mm < 3; mm++)
+        for (int nn = 0; nn < 3; nn++) t += H[mm * 3 + nn] * G[mm][ij] * G[nn][kl];
+      for (int mm = 0; mm < 3; mm++) t += g[mm] * GG[mm][ij * 9 + kl];
+      c[ij * 9 + kl] = 4.0 * t;
+    }
+  inv3(F, Fi);
+  for (int I = 0; I < 3; I++)
+    for (int J = 0; J < 3; J++) {
+      double t = 0.0;
+      for (int i = 0; i < 3; i++)
+        for (int j = 0; j < 3; j++) t += Fi[I * 3 + i] * tau[i * 3 + j] * Fi[J * 3 + j];
+      S[I * 3 + J] = t;
+    }
+  for (int I = 0; I < 3; I++)
+    for (int J = 0; J < 3; J++)
+      for (int K = 0; K < 3; K++)
+        for (int L = 0; L < 3; L++) {
+          double t = 0.0;
+          for (int i = 0; i < 3; i++)
+            for (int j = 0; j < 3; j++)
+              for (int k = 0; k < 3; k++)
+                for (int l = 0; l < 3; l++)
+                  t += Fi[I * 3 + i] * Fi[J * 3 + j] * Fi[K * 3 + k] * Fi[L * 3 + l] * c[I4(i, j, k, l)];
+          CC[I4(I, J, K, L)] = t;
+        }
+}
 
 /*
  * F (row-major F[i*3+J]) -> k, W, g, H (incl. penalty), S, CC, P, A.
@@ -180,12 +353,21 @@ double oracle_material_point(const oracle_ncm* m, const double F[9], double k_ou
   double Jd = det3(F);
   inv3(C, Ci);
   double k[3] = {I1 - 3.0, I2 - 3.0, Jd - 1.0};
+  if (m->kinematics == 1) {  /* isochoric invariants (App. A.2.2): Ibar1 = J^-2/3 I1, Ibar2 = J^-4/3 I2 */
+    const double a = pow(Jd, -2.0 / 3.0);
+    k[0] = a * I1 - 3.0;
+    k[1] = a * a * I2 - 3.0;
+  }
   double N, g[3], H[9];
   oracle_ncm_eval(m, k, &N, g, H);
   /* volumetric penalty (a5) and optional reference shift (reading 11) */
   double W = N + m->kappa * (Jd - 1.0) * (Jd - 1.0) - m->ref_shift * (Jd - 1.0);
   g[2] += 2.0 * m->kappa * (Jd - 1.0) - m->ref_shift;
   H[8] += 2.0 * m->kappa;
+  if (m->kinematics == 1) {
+    isochoric_S_CC(F, Jd, g, H, S, CC);
+    goto push;
+  }
 
   double h[3][9];
   double HHl[3][81];
@@ -222,6 +404,7 @@ double oracle_material_point(const oracle_ncm* m, const double F[9], double k_ou
       for (int mm = 0; mm < 3; mm++) t += g[mm] * HHl[mm][IJ * 9 + KL];
       CC[IJ * 9 + KL] = 4.0 * s + 4.0 * t;
     }
+push:
   for (int i = 0; i < 3; i++)
     for (int J = 0; J < 3; J++) {
       double s = 0.0;

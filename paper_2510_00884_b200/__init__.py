@@ -50,7 +50,35 @@ class MeshDesc(C.Structure):
 class NcmDesc(C.Structure):
     _fields_ = [("n_hidden", C.c_int32), ("width", C.c_int32), ("W1", C.c_void_p), ("W", C.c_void_p),
                 ("b", C.c_void_p), ("a", C.c_void_p), ("skip_out", C.c_void_p),
-                ("skip_hidden", C.c_void_p), ("kappa", C.c_double), ("ref_shift", C.c_double)]
+                ("skip_hidden", C.c_void_p), ("kappa", C.c_double), ("ref_shift", C.c_double),
+                ("kinematics", C.c_int32), ("network", C.c_int32), ("cann_n", C.c_int32),
+                ("cann_f", C.c_void_p), ("cann_w1", C.c_void_p), ("cann_w2", C.c_void_p),
+                ("gt", C.c_double * 3)]
+
+
+KIN_STANDARD, KIN_ISOCHORIC = 0, 1
+NET_ICNN, NET_CANN, NET_GENT_THOMAS = 0, 1, 2
+_KIN = {"standard": KIN_STANDARD, "isochoric": KIN_ISOCHORIC}
+_NET = {"icnn": NET_ICNN, "cann": NET_CANN, "gent_thomas": NET_GENT_THOMAS}
+
+
+def ncm_desc(ncm: dict):
+    """-> (NcmDesc, keepalive).  ncm keys: width, n_hidden, W1, W, b, a, optional skip_out,
+    skip_hidden, kappa, ref_shift, kinematics ("standard" | "isochoric"), network ("icnn" |
+    "cann" | "gent_thomas"), cann_f [3, n, 3] int, cann_w1 / cann_w2 [3, n], gt [3]."""
+    arrs = {k: _f64(ncm.get(k)) for k in ("W1", "W", "b", "a", "skip_out", "skip_hidden", "cann_w1", "cann_w2")}
+    if arrs["W"] is not None and arrs["W"].size == 0:
+        arrs["W"] = None
+    cf = None if ncm.get("cann_f") is None else np.ascontiguousarray(ncm["cann_f"], dtype=np.int32)
+    kin, net = ncm.get("kinematics", "standard"), ncm.get("network", "icnn")
+    gt = ncm.get("gt")
+    nd = NcmDesc(int(ncm.get("n_hidden", 1)), int(ncm.get("width", 16)),
+                 *[_ptr(arrs[k]) for k in ("W1", "W", "b", "a", "skip_out", "skip_hidden")],
+                 float(ncm.get("kappa", 0.0)), float(ncm.get("ref_shift", 0.0)),
+                 _KIN[kin] if isinstance(kin, str) else int(kin), _NET[net] if isinstance(net, str) else int(net),
+                 0 if cf is None else cf.shape[1], _ptr(cf), _ptr(arrs["cann_w1"]), _ptr(arrs["cann_w2"]),
+                 (C.c_double * 3)(*(gt if gt is not None else (0.0, 0.0, 0.0))))
+    return nd, [arrs, cf]
 
 
 class NewtonCfg(C.Structure):
@@ -179,12 +207,7 @@ class Commet:
         self.device = torch.device("cuda", device)
         md, _keep = _mesh_desc(mesh)
         n_nodes, nb, ne = md.n_nodes, md.owned_node_begin, md.owned_node_end
-        arrs = {k: _f64(ncm.get(k)) for k in ("W1", "W", "b", "a", "skip_out", "skip_hidden")}
-        if arrs["W"] is not None and arrs["W"].size == 0:
-            arrs["W"] = None
-        nd = NcmDesc(int(ncm["n_hidden"]), int(ncm["width"]), *[_ptr(arrs[k]) for k in
-                     ("W1", "W", "b", "a", "skip_out", "skip_hidden")],
-                     float(ncm.get("kappa", 0.0)), float(ncm.get("ref_shift", 0.0)))
+        nd, _keep_ncm = ncm_desc(ncm)
         st = stream if stream is not None else torch.cuda.current_stream(self.device)
         ctx = C.c_void_p()
         with torch.cuda.device(self.device):

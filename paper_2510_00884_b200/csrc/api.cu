@@ -36,13 +36,32 @@ extern "C" commet_status commet_setup(const commet_mesh_desc* mesh, const commet
   if (!c) return fail(nullptr, COMMET_ERR_OOM, "host allocation failed");
   commet_ctx C = c.get();
   // NCM arguments (host checks, before any CUDA call)
-  const int L = ncm->n_hidden, w = ncm->width;
-  if (L < 1 || L > kMaxLayers) return fail(C, COMMET_ERR_ARG, "n_hidden %d not in 1..%d", L, kMaxLayers);
+  const int net = ncm->network, kin = ncm->kinematics;
+  if (kin != COMMET_KIN_STANDARD && kin != COMMET_KIN_ISOCHORIC)
+    return fail(C, COMMET_ERR_ARG, "kinematics %d unknown", kin);
+  if (net != COMMET_NET_ICNN && net != COMMET_NET_CANN && net != COMMET_NET_GENT_THOMAS)
+    return fail(C, COMMET_ERR_ARG, "network %d unknown", net);
+  // analytic networks use no hidden layers (the ICNN fields are ignored)
+  const int L = net == COMMET_NET_ICNN ? ncm->n_hidden : 1, w = net == COMMET_NET_ICNN ? ncm->width : 16;
   const bool tet = mesh->elem_type == COMMET_TET10;
-  if (!fused_supported(tet ? 10 : 8, tet ? 4 : 8, w, L))
-    return fail(C, COMMET_ERR_ARG, "width %d unsupported (8, 16, 32, 64 or 128)", w);
-  if (!ncm->W1 || !ncm->b || !ncm->a || (L > 1 && !ncm->W))
-    return fail(C, COMMET_ERR_ARG, "NCM weight pointer NULL (W1, b, a or W)");
+  if (net == COMMET_NET_ICNN) {
+    if (L < 1 || L > kMaxLayers) return fail(C, COMMET_ERR_ARG, "n_hidden %d not in 1..%d", L, kMaxLayers);
+    if (!fused_supported(tet ? 10 : 8, tet ? 4 : 8, w, L))
+      return fail(C, COMMET_ERR_ARG, "width %d unsupported (8, 16, 32, 64 or 128)", w);
+    if (!ncm->W1 || !ncm->b || !ncm->a || (L > 1 && !ncm->W))
+      return fail(C, COMMET_ERR_ARG, "NCM weight pointer NULL (W1, b, a or W)");
+  }
+  if (net == COMMET_NET_CANN) {
+    if (ncm->cann_n < 1 || ncm->cann_n > 16) return fail(C, COMMET_ERR_ARG, "cann_n %d not in 1..16", ncm->cann_n);
+    if (!ncm->cann_f || !ncm->cann_w1 || !ncm->cann_w2)
+      return fail(C, COMMET_ERR_ARG, "CANN pointer NULL (cann_f, cann_w1 or cann_w2)");
+    for (int x = 0; x < 3 * ncm->cann_n; x++) {
+      const int32_t* f = ncm->cann_f + 3 * x;
+      if (f[0] < 0 || f[0] > 2 || f[1] < 1 || f[1] > 3 || f[2] < 0 || f[2] > 2)
+        return fail(C, COMMET_ERR_ARG, "cann_f entry %d = (%d, %d, %d) outside the menus (f0 0..2, f1 1..3, f2 0..2)",
+                    x, f[0], f[1], f[2]);
+    }
+  }
   Plan& p = c->plan;
   {
     std::string err;
@@ -114,15 +133,22 @@ extern "C" commet_status commet_setup(const commet_mesh_desc* mesh, const commet
 
   // ---- NCM ---------------------------------------------------------------------------------
   commet_status s;
-  std::vector<double> zeros3(3, 0.0);
-  if ((s = upload(C, c->W1, ncm->W1, (size_t)w * 3, st))) return s;
-  if ((s = upload(C, c->b, ncm->b, (size_t)L * w, st))) return s;
-  if ((s = upload(C, c->a, ncm->a, (size_t)w, st))) return s;
+  std::vector<double> zeros3(3, 0.0), zw((size_t)L * w * 3 + 3, 0.0);
+  const bool icnn = net == COMMET_NET_ICNN;
+  if ((s = upload(C, c->W1, icnn ? ncm->W1 : zw.data(), (size_t)w * 3, st))) return s;
+  if ((s = upload(C, c->b, icnn ? ncm->b : zw.data(), (size_t)L * w, st))) return s;
+  if ((s = upload(C, c->a, icnn ? ncm->a : zw.data(), (size_t)w, st))) return s;
+  if (net == COMMET_NET_CANN) {
+    const size_t nb = (size_t)3 * ncm->cann_n;
+    if ((s = upload(C, c->cann_f, ncm->cann_f, 3 * nb, st))) return s;
+    if ((s = upload(C, c->cann_w1, ncm->cann_w1, nb, st))) return s;
+    if ((s = upload(C, c->cann_w2, ncm->cann_w2, nb, st))) return s;
+  }
   if ((s = upload(C, c->skip_out, ncm->skip_out ? ncm->skip_out : zeros3.data(), 3, st))) return s;
-  if (ncm->skip_hidden && L > 1)
+  if (icnn && ncm->skip_hidden && L > 1)
     if ((s = upload(C, c->skip_h, ncm->skip_hidden, (size_t)(L - 1) * w * 3, st))) return s;
   std::vector<double> wrow((size_t)std::max(L - 1, 1) * w * w, 0.0);
-  if (L > 1) std::memcpy(wrow.data(), ncm->W, (size_t)(L - 1) * w * w * sizeof(double));
+  if (icnn && L > 1) std::memcpy(wrow.data(), ncm->W, (size_t)(L - 1) * w * w * sizeof(double));
   if ((s = upload(C, c->Wrow, wrow.data(), wrow.size(), st))) return s;
   std::vector<double> wf(fused_weight_frag_size(w, L), 0.0);
   fused_weight_frag_fill(w, L, wrow.data(), wf.data());
@@ -131,10 +157,12 @@ extern "C" commet_status commet_setup(const commet_mesh_desc* mesh, const commet
   fill_act_table(tab.data());
   if ((s = upload(C, c->act_tab, tab.data(), tab.size(), st))) return s;
   std::vector<double> gf((size_t)2 * 16 * w);
-  fused_gfrag_fill(w, ncm->W1, gf.data());
+  fused_gfrag_fill(w, icnn ? ncm->W1 : zw.data(), gf.data());
   if ((s = upload(C, c->gfrag, gf.data(), gf.size(), st))) return s;
   c->ncm = NcmDev{L, w, c->W1.p, c->b.p, c->a.p, c->skip_out.p, c->skip_h.p, c->Wrow.p, c->Wfrag.p,
-                  c->act_tab.p, c->gfrag.p, ncm->kappa, ncm->ref_shift};
+                  c->act_tab.p, c->gfrag.p, ncm->kappa, ncm->ref_shift, kin, net,
+                  net == COMMET_NET_CANN ? ncm->cann_n : 0, c->cann_f.p, c->cann_w1.p, c->cann_w2.p,
+                  {ncm->gt[0], ncm->gt[1], ncm->gt[2]}};
   CUDA_TRY(C, c->bad.alloc(1));
   CUDA_TRY(C, c->max_trc.alloc(1));
   CUDA_TRY(C, c->r_halo.alloc(3 * p.n_halo));
@@ -342,7 +370,7 @@ extern "C" commet_status commet_kernel_info(commet_ctx c, int32_t* smem_bytes, i
   if (!c) return fail(nullptr, COMMET_ERR_ARG, "ctx is NULL");
   CUDA_TRY(c, cudaSetDevice(c->device));
   int a = 0, b = 0, r = 0;
-  fused_occupancy(c->plan.n_en, c->ncm.w, c->ncm.L, &a, &b, &r);
+  fused_occupancy(c->plan.n_en, c->ncm.net ? 0 : c->ncm.w, c->ncm.L, &a, &b, &r);
   if (smem_bytes) *smem_bytes = a;
   if (ctas_per_sm) *ctas_per_sm = b;
   if (regs_per_thread) *regs_per_thread = r;

@@ -31,6 +31,11 @@ struct NcmDev {
   const double* act_tab;  // [kActTabSize] softplus tables (qp_math.cuh)
   const double* gfrag;    // [2][16 x w] fragments of [W1^T | 0] and [0 | V] (stage 5)
   double kappa, ref_shift;
+  int kin, net, cann_n;   // variants (commet.h COMMET_KIN_* / COMMET_NET_*)
+  const int32_t* cann_f;  // [3][n][3]
+  const double* cann_w1;  // [3][n]
+  const double* cann_w2;  // [3][n]
+  double gt[3];
 };
 
 struct AsmArgs {

@@ -100,9 +100,12 @@ __device__ __forceinline__ double2 ldg2(const double* p) {
 // ---------------------------------------------------------------------------
 // compile-time tiling
 // ---------------------------------------------------------------------------
-template <int W_, int Q_, int NEN_, int NQ_, int MINB_ = 3>
+// NET_: 0 = ICNN (DMMA network stages 2-6), 1 = analytic inner network (CANN or
+// Gent-Thomas, evaluated per qp in stage 7a; W is then unused).  KIN_: 0 standard
+// invariants, 1 isochoric (compile-time, so the standard path carries no extra code)
+template <int W_, int Q_, int NEN_, int NQ_, int MINB_ = 3, int NET_ = 0, int KIN_ = 0>
 struct Cfg {
-  static constexpr int W = W_, Q = Q_, NEN = NEN_, NQ = NQ_;
+  static constexpr int W = W_, Q = Q_, NEN = NEN_, NQ = NQ_, NET = NET_, KIN = KIN_;
   static constexpr int NWARP = 4, NTHR = 128;
   static constexpr int MINB = MINB_;               // CTAs per SM the register budget targets (3: <= 168 regs)
   static constexpr bool DMMA_ELEM = COMMET_DMMA_ELEM == 2 || (COMMET_DMMA_ELEM == 1 && NEN == 8);
@@ -120,6 +123,7 @@ struct Cfg {
   static constexpr int LDA = 3 * Q + 4;            // act row stride (= 4 mod 16: conflict-free B frags)
   static constexpr int LDS = Q + 2;                // s/c row stride (2-way conflicts at most)
   static_assert(W % 8 == 0 && Q % 8 == 0 && Q % NQ == 0, "tile");
+  static_assert(Q <= 32, "stage-1 threads (one per qp) must sit in warp 0");
   static_assert(TPW >= 1 && VMG * VNG == NWARP && MT_V * NT_V == TPW, "value tiling");
   static_assert(JMG >= 1 && JMG * QB == NWARP && MT_J * JMG == MTILES, "jacobian tiling");
   static_assert(VMG * Q * 9 <= W * LDA, "adjoint partials must fit in act");
@@ -149,7 +153,8 @@ struct Smem {
     wq = o;  o += C::Q;
     tab = o; o += kActTabSize;
     o = (o + 1) & ~1;
-    const int px = C::Q * PS > C::Q * C::NEN * 27 ? C::Q * PS : C::Q * C::NEN * 27;
+    const int xs = C::DMMA_ELEM ? 0 : C::Q * C::NEN * 27;  // X only for the scalar element path
+    const int px = C::Q * PS > xs ? C::Q * PS : xs;
     const int need = C::Q * 9 + px + C::Q * 81;
     int base = 0;
     if (need > dead) { base = o; o += need; }
@@ -241,6 +246,7 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
   }
 #endif
 
+  double trc_max = 0.0;  // running max of tr C = I1 over this thread's qps (stage 1 threads)
 #if COMMET_PREFETCH
   // register prefetch of one batch's element inputs: (a) dN/dX, w, conn; (b) the u gather
   constexpr int NG2 = E * NQ * NEN * 3 / 2, NU = E * NEN * 3;
@@ -338,13 +344,22 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
       kinematics(F, kin);
       if (e < ne) {
         if (!(kin.J > 0.0)) atomicMin(A.bad, (unsigned long long)(__ldg(A.orig + e0 + e) * NQ + q % NQ));
-        atomicMax(A.max_trc, (unsigned long long)__double_as_longlong(kin.I1));
+        trc_max = fmax(trc_max, kin.I1);  // one atomic per CTA at the end (a per-qp atomic on one
+                                          // address serialises in L2: measured -6% on c3)
       }
 #pragma unroll
       for (int x = 0; x < 9; x++) qF[q * 9 + x] = F[x];
-      qk[q * 3 + 0] = kin.I1 - 3.0;
-      qk[q * 3 + 1] = kin.I2 - 3.0;
-      qk[q * 3 + 2] = kin.J - 1.0;
+      if constexpr (C::KIN == 1) {  // isochoric inputs (App. A.2.2)
+        double kb[3];
+        isochoric_inputs(kin, kb);
+        qk[q * 3 + 0] = kb[0];
+        qk[q * 3 + 1] = kb[1];
+        qk[q * 3 + 2] = kb[2];
+      } else {
+        qk[q * 3 + 0] = kin.I1 - 3.0;
+        qk[q * 3 + 1] = kin.I2 - 3.0;
+        qk[q * 3 + 2] = kin.J - 1.0;
+      }
       gsk[q * 3 + 0] = gsk[q * 3 + 1] = gsk[q * 3 + 2] = 0.0;
     }
     __syncthreads();
@@ -353,6 +368,7 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
 #ifdef COMMET_EXP_SKIP_NCM
     if (false) {
 #endif
+    if constexpr (C::NET == 0) {
     // ---- stage 2: layer 1 (3 -> W), elementwise -------------------------------------
     if (L > 1) frag_prefetch<C::MT_V, KT2, COMMET_FRAG_PF + (COMMET_FRAG_PF == 0)>(m.Wfrag, (warp / C::VNG) * C::MT_V);
 #if COMMET_L1_UNROLL
@@ -684,6 +700,7 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
       __syncthreads();
     }
 
+    }  // NET == 0
     STAGE_MARK(6)
 #ifdef COMMET_EXP_SKIP_NCM
     }
@@ -698,18 +715,23 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
     if (tid < Q) {
       const int q = tid;
       double gq[3], H6[6];
+      if constexpr (C::NET == 0) {
 #pragma unroll
-      for (int x = 0; x < 3; x++) gq[x] = qg[q * 3 + x];
+        for (int x = 0; x < 3; x++) gq[x] = qg[q * 3 + x];
 #pragma unroll
-      for (int x = 0; x < 6; x++) {
-        double s = qH[q * 6 + x];
-        if (L > 1)
+        for (int x = 0; x < 6; x++) {
+          double s = qH[q * 6 + x];
+          if (L > 1)
 #pragma unroll
-          for (int r = 0; r < C::JMG; r++) s += hred[(r * Q + q) * 6 + x];
-        H6[x] = s;
+            for (int r = 0; r < C::JMG; r++) s += hred[(r * Q + q) * 6 + x];
+          H6[x] = s;
+        }
+      } else {
+        analytic_net(m.net, m.cann_n, m.cann_f, m.cann_w1, m.cann_w2, m.gt, m.skip_out, qk + q * 3, gq, H6);
       }
       Kin kin;
       kinematics(qF + q * 9, kin);
+      if constexpr (C::KIN == 1) isochoric_to_standard(kin, gq, H6);
       gq[2] += 2.0 * m.kappa * (kin.J - 1.0) - m.ref_shift;
       H6[5] += 2.0 * m.kappa;
       post_qp(kin, gq, H6, swq[q], post + q * PS, qP + q * 9);
@@ -896,6 +918,11 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
     __syncthreads();
     STAGE_MARK(10)
   }
+  if (warp == 0) {  // stage-1 threads are tid < Q <= 32
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) trc_max = fmax(trc_max, __shfl_xor_sync(0xffffffffu, trc_max, o));
+    if (lane == 0 && trc_max > 0.0) atomicMax(A.max_trc, (unsigned long long)__double_as_longlong(trc_max));
+  }
 #ifdef COMMET_STAGE_PROF
   if (tid == 0)
     for (int i = 0; i < 11; i++) atomicAdd(&g_stage_cycles[i], (unsigned long long)st_acc[i]);
@@ -995,17 +1022,6 @@ static int launch_cfg(const AsmArgs& a, cudaStream_t st, int* launches) {
   return (int)cudaGetLastError();
 }
 
-// COMMET_FUSED_VARIANT=1 (environment, read once): alternative tiling for tuning
-// experiments (w = 64: one element per batch, 4 CTAs/SM at <= 128 registers).
-static int fused_variant() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("COMMET_FUSED_VARIANT");
-    v = e ? atoi(e) : 0;
-  }
-  return v;
-}
-
 template <class C>
 static void occ_cfg(int L, int* smem_bytes, int* ctas_per_sm, int* regs) {
   const Smem<C> sm(L);
@@ -1022,14 +1038,12 @@ static void occ_cfg(int L, int* smem_bytes, int* ctas_per_sm, int* regs) {
 
 template <int NEN, int NQ>
 static void occ_et(int w, int L, int* a, int* b, int* c) {
+  if (w == 0) return occ_cfg<Cfg<16, 16, NEN, NQ, 3, 1>>(1, a, b, c);  // analytic networks
   switch (w) {
     case 8: occ_cfg<Cfg<8, 32, NEN, NQ>>(L, a, b, c); break;
     case 16: occ_cfg<Cfg<16, 16, NEN, NQ>>(L, a, b, c); break;
     case 32: occ_cfg<Cfg<32, 16, NEN, NQ>>(L, a, b, c); break;
-    case 64:
-      if (fused_variant() == 1) occ_cfg<Cfg<64, 8, NEN, NQ, 4>>(L, a, b, c);
-      else occ_cfg<Cfg<64, 16, NEN, NQ>>(L, a, b, c);
-      break;
+    case 64: occ_cfg<Cfg<64, 16, NEN, NQ>>(L, a, b, c); break;
     case 128: occ_cfg<Cfg<128, 8, NEN, NQ>>(L, a, b, c); break;
   }
 }
@@ -1039,18 +1053,22 @@ void fused_occupancy(int n_en, int w, int L, int* smem_bytes, int* ctas_per_sm, 
   else occ_et<10, 4>(w, L, smem_bytes, ctas_per_sm, regs);
 }
 
-template <int NEN, int NQ>
-static int launch_et(const AsmArgs& a, cudaStream_t st, int* launches) {
+template <int NEN, int NQ, int K>
+static int launch_k(const AsmArgs& a, cudaStream_t st, int* launches) {
+  if (a.ncm.net != 0) return launch_cfg<Cfg<16, 16, NEN, NQ, 3, 1, K>>(a, st, launches);
   switch (a.ncm.w) {
-    case 8: return launch_cfg<Cfg<8, 32, NEN, NQ>>(a, st, launches);
-    case 16: return launch_cfg<Cfg<16, 16, NEN, NQ>>(a, st, launches);
-    case 32: return launch_cfg<Cfg<32, 16, NEN, NQ>>(a, st, launches);
-    case 64:
-      if (fused_variant() == 1) return launch_cfg<Cfg<64, 8, NEN, NQ, 4>>(a, st, launches);
-      return launch_cfg<Cfg<64, 16, NEN, NQ>>(a, st, launches);
-    case 128: return launch_cfg<Cfg<128, 8, NEN, NQ>>(a, st, launches);
+    case 8: return launch_cfg<Cfg<8, 32, NEN, NQ, 3, 0, K>>(a, st, launches);
+    case 16: return launch_cfg<Cfg<16, 16, NEN, NQ, 3, 0, K>>(a, st, launches);
+    case 32: return launch_cfg<Cfg<32, 16, NEN, NQ, 3, 0, K>>(a, st, launches);
+    case 64: return launch_cfg<Cfg<64, 16, NEN, NQ, 3, 0, K>>(a, st, launches);
+    case 128: return launch_cfg<Cfg<128, 8, NEN, NQ, 3, 0, K>>(a, st, launches);
   }
   return (int)cudaErrorInvalidValue;
+}
+
+template <int NEN, int NQ>
+static int launch_et(const AsmArgs& a, cudaStream_t st, int* launches) {
+  return a.ncm.kin == 1 ? launch_k<NEN, NQ, 1>(a, st, launches) : launch_k<NEN, NQ, 0>(a, st, launches);
 }
 
 int launch_fused(const AsmArgs& a, void* stream, int* launches) {

@@ -27,6 +27,7 @@ __global__ void __launch_bounds__(64) simple_kernel(AsmArgs A) {
   double re[kMaxEn * 3];
   for (int x = 0; x < nd * nd; x++) Ke[x] = 0.0;
   for (int x = 0; x < nd; x++) re[x] = 0.0;
+  double trc = 0.0;
   for (int q = 0; q < nq; q++) {
     const double* gN = A.gradN + ((size_t)e * nq + q) * nen * 3;
     const double w = A.qp_w[e * nq + q];
@@ -40,10 +41,12 @@ __global__ void __launch_bounds__(64) simple_kernel(AsmArgs A) {
     Kin kin;
     kinematics(F, kin);
     if (!(kin.J > 0.0)) atomicMin(A.bad, (unsigned long long)(A.orig[e] * nq + q));
-    atomicMax(A.max_trc, (unsigned long long)__double_as_longlong(kin.I1));
-    const double kv[3] = {kin.I1 - 3.0, kin.I2 - 3.0, kin.J - 1.0};
+    trc = fmax(trc, kin.I1);
+    double kv[3] = {kin.I1 - 3.0, kin.I2 - 3.0, kin.J - 1.0};
+    if (A.ncm.kin == 1) isochoric_inputs(kin, kv);
     double g[3], H6[6];
-    ncm_alg4(A.ncm, kv, g, H6);
+    ncm_point(A.ncm, kv, g, H6);
+    if (A.ncm.kin == 1) isochoric_to_standard(kin, g, H6);
     g[2] += 2.0 * A.ncm.kappa * (kin.J - 1.0) - A.ncm.ref_shift;
     H6[5] += 2.0 * A.ncm.kappa;
     double P[9], Am[81];
@@ -63,6 +66,7 @@ __global__ void __launch_bounds__(64) simple_kernel(AsmArgs A) {
       }
     }
   }
+  atomicMax(A.max_trc, (unsigned long long)__double_as_longlong(trc));
   const uint8_t* sl = A.slot + (size_t)e * nen * nen;
   for (int a = 0; a < nen; a++) {
     const int64_t ln = A.lrow[e * nen + a];

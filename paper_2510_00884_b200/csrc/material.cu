@@ -1,6 +1,7 @@
 // material.cu -- material-point calls on the ctx's NCM (SURVEY.md s8(f) rank 3
-// groundwork): the inner network's gradient and Hessian on a batch of invariant
-// inputs k (Alg. 4), and the stress-free reference
+// groundwork): the inner network's gradient and Hessian on a batch of network
+// inputs k (Alg. 4, or the CANN / Gent-Thomas closed forms),
+// and the stress-free reference
 // normalisation of DESIGN.md reading R11 (s0 = 2 g1 + 4 g2 + g3 at k = 0, so that
 // S(F = I) = (2 g1 + 4 g2 + g3 - s0) I = 0).
 #include <cuda_runtime.h>
@@ -14,7 +15,7 @@ __global__ void ncm_eval_kernel(NcmDev m, const double* __restrict__ k, double* 
                                 double* __restrict__ H, int64_t n) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     double gi[3], Hi[6];
-    ncm_alg4(m, k + 3 * i, gi, Hi);
+    ncm_point(m, k + 3 * i, gi, Hi);
     for (int p = 0; p < 3; p++) g[3 * i + p] = gi[p];
     for (int p = 0; p < 6; p++) H[6 * i + p] = Hi[p];
   }
@@ -23,7 +24,14 @@ __global__ void ncm_eval_kernel(NcmDev m, const double* __restrict__ k, double* 
 __global__ void ref_shift_kernel(NcmDev m, double* out) {
   const double k0[3] = {0.0, 0.0, 0.0};
   double g[3], H[6];
-  ncm_alg4(m, k0, g, H);
+  ncm_point(m, k0, g, H);
+  if (m.kin == 1) {  // isochoric inputs: carry the gradient to (I1, I2, J) at F = I
+    Kin ki{};
+    ki.I1 = 3.0;
+    ki.I2 = 3.0;
+    ki.J = 1.0;
+    isochoric_to_standard(ki, g, H);
+  }
   out[0] = 2.0 * g[0] + 4.0 * g[1] + g[2];  // the penalty's 2 kappa (J - 1) vanishes at J = 1
 }
 

@@ -67,4 +67,12 @@ __device__ __forceinline__ void ncm_alg4(const NcmDev& m, const double* kin, dou
   }
 }
 
+// the ctx's inner network at inputs k: Alg. 4 for the ICNN, closed forms for CANN / Gent-Thomas
+__device__ __forceinline__ void ncm_point(const NcmDev& m, const double* kin, double* g, double* H6) {
+  if (m.net == 0)
+    ncm_alg4(m, kin, g, H6);
+  else
+    analytic_net(m.net, m.cann_n, m.cann_f, m.cann_w1, m.cann_w2, m.gt, m.skip_out, kin, g, H6);
+}
+
 }  // namespace commet

@@ -142,16 +142,6 @@ __device__ __forceinline__ void tangent_row(const double* __restrict__ post, int
   }
 }
 
-// One entry (iJ, kL) of w A (= tangent_row(post, 3 i + J, .)[kL])
-__device__ __forceinline__ double tangent_entry(const double* __restrict__ post, int i, int J, int kL) {
-  const int iJ = 3 * i + J, kk = kL / 3, L = kL % 3;
-  double v = post[27 + iJ] * post[54 + kL] + post[36 + iJ] * post[63 + kL] + post[45 + iJ] * post[72 + kL];
-  v += post[90] * post[i * 3 + L] * post[kk * 3 + J] + post[91] * post[9 + i * 3 + L] * post[9 + kk * 3 + J];
-  if (J == L) v += post[90] * post[81 + i * 3 + kk];
-  if (i == kk) v += post[18 + J * 3 + L];
-  return v;
-}
-
 // Whole tangent of one qp (simple kernel): P[9] and A[81], both scaled by w.
 __device__ __forceinline__ void stress_tangent(const Kin& k, const double* __restrict__ g,
                                                const double* __restrict__ H6, double w,
@@ -159,6 +149,103 @@ __device__ __forceinline__ void stress_tangent(const Kin& k, const double* __res
   double post[92];
   post_qp(k, g, H6, w, post, P);
   for (int iJ = 0; iJ < 9; iJ++) tangent_row(post, iJ, A + iJ * 9);
+}
+
+// ---------------------------------------------------------------------------
+// kinematic variant: isochoric inputs (App. A.2.2)
+//   kbar = (Ibar1 - 3, Ibar2 - 3, J - 1),  Ibar1 = J^-2/3 I1,  Ibar2 = J^-4/3 I2.
+// The network's (gbar, Hbar) w.r.t. kbar are carried to (g, H) w.r.t. the standard
+// k = (I1 - 3, I2 - 3, J - 1) by the chain rule, so S and the F-space tangent above
+// apply unchanged (the oracle instead follows the paper's spatial G-tensor table):
+//   g = D^T gbar,  H = D^T Hbar D + sum_m gbar_m d2y_m,  D = d(Ibar1, Ibar2, J)/d(I1, I2, J)
+//   D = [[a, 0, c1], [0, b, c2], [0, 0, 1]],  a = J^-2/3, b = J^-4/3, c1 = -2/3 Ibar1/J, c2 = -4/3 Ibar2/J
+//   d2Ibar1: (I1,J) = -2/3 a/J, (J,J) = 10/9 Ibar1/J^2;  d2Ibar2: (I2,J) = -4/3 b/J, (J,J) = 28/9 Ibar2/J^2
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void isochoric_inputs(const Kin& k, double kb[3]) {
+  const double a = 1.0 / (cbrt(k.J) * cbrt(k.J));
+  kb[0] = a * k.I1 - 3.0;
+  kb[1] = a * a * k.I2 - 3.0;
+  kb[2] = k.J - 1.0;
+}
+
+// in place: g[3], H6[6] (upper 00,01,02,11,12,22) from kbar- to k-derivatives
+__device__ __forceinline__ void isochoric_to_standard(const Kin& k, double* __restrict__ g, double* __restrict__ H6) {
+  const double a = 1.0 / (cbrt(k.J) * cbrt(k.J)), b = a * a, iJ = 1.0 / k.J;
+  const double Ib1 = a * k.I1, Ib2 = b * k.I2;
+  const double c1 = -2.0 / 3.0 * Ib1 * iJ, c2 = -4.0 / 3.0 * Ib2 * iJ;
+  const double g0 = g[0], g1 = g[1], g2 = g[2];
+  const double h00 = H6[0], h01 = H6[1], h02 = H6[2], h11 = H6[3], h12 = H6[4], h22 = H6[5];
+  g[0] = a * g0;
+  g[1] = b * g1;
+  g[2] = c1 * g0 + c2 * g1 + g2;
+  const double t0 = h00 * c1 + h01 * c2 + h02;  // (Hbar col3)_0
+  const double t1 = h01 * c1 + h11 * c2 + h12;  // (Hbar col3)_1
+  const double t2 = h02 * c1 + h12 * c2 + h22;  // (Hbar col3)_2
+  H6[0] = a * a * h00;
+  H6[1] = a * b * h01;
+  H6[2] = a * t0 - 2.0 / 3.0 * a * iJ * g0;
+  H6[3] = b * b * h11;
+  H6[4] = b * t1 - 4.0 / 3.0 * b * iJ * g1;
+  H6[5] = c1 * t0 + c2 * t1 + t2 + (10.0 / 9.0 * Ib1 * g0 + 28.0 / 9.0 * Ib2 * g1) * iJ * iJ;
+}
+
+// analytic inner networks: gradient and Hessian w.r.t. the inputs
+//  CANN (Eq. cann-def / cann-chain-rule): diagonal Hessian
+//  Gent-Thomas (App. C): N = gt0 k1 + gt1 ln(1 + k2/3) + gt2 k3^2
+__device__ __forceinline__ void analytic_net(int net, int n, const int32_t* __restrict__ f,
+                                             const double* __restrict__ w1, const double* __restrict__ w2,
+                                             const double* __restrict__ gt, const double* __restrict__ skip,
+                                             const double* kin, double* __restrict__ g, double* __restrict__ H6) {
+  if (net == 2) {
+    const double u = 1.0 / (kin[1] + 3.0);
+    g[0] = gt[0];
+    g[1] = gt[1] * u;
+    g[2] = 2.0 * gt[2] * kin[2];
+    H6[0] = H6[1] = H6[2] = H6[4] = 0.0;
+    H6[3] = -gt[1] * u * u;
+    H6[5] = 2.0 * gt[2];
+    return;
+  }
+  double hd[3];
+  for (int m = 0; m < 3; m++) {
+    const double x = kin[m];
+    double gm = skip[m], hm = 0.0;
+    for (int bb = 0; bb < n; bb++) {
+      const int32_t* fb = f + (m * n + bb) * 3;
+      const int t0 = __ldg(fb), p = __ldg(fb + 1), t2 = __ldg(fb + 2);
+      const double a1 = __ldg(w1 + m * n + bb), a2 = __ldg(w2 + m * n + bb);
+      // f0 and its slope (f0'' = 0)
+      const double v0 = t0 == 0 ? x : (t0 == 1 ? fmax(x, 0.0) : fabs(x));
+      const double d0 = t0 == 0 ? 1.0 : (t0 == 1 ? (x > 0.0 ? 1.0 : (x < 0.0 ? 0.0 : 0.5))
+                                                  : (x > 0.0 ? 1.0 : (x < 0.0 ? -1.0 : 0.0)));
+      // f1 = v0^p
+      const double v1 = p == 1 ? v0 : (p == 2 ? v0 * v0 : v0 * v0 * v0);
+      const double d1 = p == 1 ? 1.0 : (p == 2 ? 2.0 * v0 : 3.0 * v0 * v0);
+      const double dd1 = p == 1 ? 0.0 : (p == 2 ? 2.0 : 6.0 * v0);
+      // f2 (weight w1 inside)
+      double d2, dd2;
+      if (t2 == 0) {
+        d2 = a1;
+        dd2 = 0.0;
+      } else if (t2 == 1) {
+        const double e = exp(a1 * v1);
+        d2 = a1 * e;
+        dd2 = a1 * a1 * e;
+      } else {
+        const double r = 1.0 / (1.0 - a1 * v1);
+        d2 = a1 * r;
+        dd2 = a1 * a1 * r * r;
+      }
+      gm += a2 * d2 * d1 * d0;
+      hm += a2 * (dd2 * d1 * d1 + d2 * dd1) * d0 * d0;
+    }
+    g[m] = gm;
+    hd[m] = hm;
+  }
+  H6[0] = hd[0];
+  H6[3] = hd[1];
+  H6[5] = hd[2];
+  H6[1] = H6[2] = H6[4] = 0.0;
 }
 
 // ---------------------------------------------------------------------------

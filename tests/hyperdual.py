@@ -3,7 +3,9 @@ first and second derivatives of W(F) straight from its definition -- an
 independent derivation used to PIN the oracle's G-tensor algebra (no shared
 code with oracle/ or the CUDA path).
 
-Only what W(F) = N(k(F)) + kappa (J-1)^2 - s0 (J-1) needs: +, -, *, softplus.
+Only what W(F) = N(k(F)) + kappa (J-1)^2 - s0 (J-1) needs: +, -, *, softplus,
+powers, exp, log and the CANN activations (for the isochoric / CANN /
+Gent-Thomas variants of SURVEY.md s8(f) rank 2).
 Every component is a numpy array so all 81 direction pairs run at once.
 """
 from __future__ import annotations
@@ -58,6 +60,43 @@ def softplus(x: HD) -> HD:
                    lambda y: _sig(y) * (1.0 - _sig(y)))
 
 
+def hd_pow(x: HD, p: float) -> HD:
+    return x.apply(lambda a: a ** p, lambda a: p * a ** (p - 1), lambda a: p * (p - 1) * a ** (p - 2))
+
+
+def hd_exp(x: HD) -> HD:
+    return x.apply(np.exp, np.exp, np.exp)
+
+
+def hd_log(x: HD) -> HD:
+    return x.apply(np.log, lambda a: 1.0 / a, lambda a: -1.0 / (a * a))
+
+
+def _cann_hd(k, ncm):
+    """N = sum_m sum_b w2 f2(f1(f0(K_m))) written from Eq. cann-def / cann-fs."""
+    f, w1, w2 = ncm["cann_f"], ncm["cann_w1"], ncm["cann_w2"]
+    N = HD(0.0)
+    for m in range(3):
+        for b in range(f.shape[1]):
+            t0, p, t2 = f[m, b]
+            x = k[m]
+            if t0 == 1:
+                x = x.apply(lambda a: np.maximum(a, 0.0), lambda a: 0.5 * (1 + np.sign(a)), lambda a: 0.0 * a)
+            elif t0 == 2:
+                x = x.apply(np.abs, np.sign, lambda a: 0.0 * a)
+            y = HD(1.0)
+            for _ in range(p):
+                y = y * x
+            if t2 == 0:
+                z = w1[m, b] * y
+            elif t2 == 1:
+                z = hd_exp(w1[m, b] * y) - 1.0
+            else:
+                z = -1.0 * hd_log(1.0 - w1[m, b] * y)
+            N = N + w2[m, b] * z
+    return N
+
+
 def energy_hd(F: list, ncm: dict):
     """W(F) for a 3x3 list-of-lists of HD; written from the definitions:
     C = F^T F, I1 = tr C, I2 = (I1^2 - tr C^2)/2, J = det F (Sarrus),
@@ -69,6 +108,21 @@ def energy_hd(F: list, ncm: dict):
     J = (F[0][0] * F[1][1] * F[2][2] + F[0][1] * F[1][2] * F[2][0] + F[0][2] * F[1][0] * F[2][1]
          - F[0][2] * F[1][1] * F[2][0] - F[0][0] * F[1][2] * F[2][1] - F[0][1] * F[1][0] * F[2][2])
     k = [I1 - 3.0, I2 - 3.0, J - 1.0]
+    if ncm.get("kinematics", "standard") == "isochoric":
+        a23 = hd_pow(J, -2.0 / 3.0)
+        k = [a23 * I1 - 3.0, a23 * a23 * I2 - 3.0, J - 1.0]
+    kap, s0 = ncm.get("kappa", 0.0), ncm.get("ref_shift", 0.0)
+    net = ncm.get("network", "icnn")
+    if net == "cann":
+        N = _cann_hd(k, ncm)
+        if ncm.get("skip_out") is not None:
+            for i in range(3):
+                N = N + ncm["skip_out"][i] * k[i]
+        return N + kap * (J - 1.0) * (J - 1.0) - s0 * (J - 1.0)
+    if net == "gent_thomas":
+        c = ncm["gt"]
+        N = c[0] * k[0] + c[1] * hd_log((k[1] + 3.0) * (1.0 / 3.0)) + c[2] * k[2] * k[2]
+        return N + kap * (J - 1.0) * (J - 1.0) - s0 * (J - 1.0)
     W1, b, a = ncm["W1"], ncm["b"], ncm["a"]
     L, w = ncm["n_hidden"], ncm["width"]
     Wh = ncm.get("W")

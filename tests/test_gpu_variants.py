@@ -1,0 +1,96 @@
+"""GPU parity of the kinematic and inner-network variants (SURVEY.md s8(f) rank
+2) through the C ABI: isochoric invariants + J, CANN and Gent-Thomas in the
+fused kernel (and the one-thread-per-element cross-check kernel) against the
+oracle's spatial G-tensor / Eq. cann-chain-rule implementation."""
+import numpy as np
+import pytest
+
+import oracle
+from oracle import newton as on
+from synth.gen import (HEX8, TET10, cann_params, gent_thomas_params, hex_mesh, ncm_weights, shape_gradients,
+                       smooth_field, tet10_mesh)
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+TOL = 1e-10
+
+
+@pytest.fixture(scope="module")
+def pc():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2510_00884_b200 as pc
+    return pc
+
+
+def _iso_icnn(w, L):
+    m = ncm_weights(w, L, 0.3, 11, 10.0)
+    m["kinematics"] = "isochoric"
+    return m
+
+
+VARIANTS = {
+    "gent_thomas": lambda: gent_thomas_params(),
+    "cann_standard": lambda: cann_params(4, seed=3),
+    "cann_isochoric": lambda: cann_params(5, seed=4, kinematics="isochoric"),
+    "icnn_isochoric_16x2": lambda: _iso_icnn(16, 2),
+    "icnn_isochoric_64x3": lambda: _iso_icnn(64, 3),
+}
+
+
+def _mesh(elem_type, n):
+    if elem_type == HEX8:
+        X, conn = hex_mesh(n, 0.1, seed=5)
+    else:
+        X, conn = tet10_mesh(n, 0.1, seed=5)
+    gN, w = shape_gradients(X, conn, elem_type)
+    u = smooth_field(X, 0.06, np.random.default_rng(7)).reshape(-1)
+    return dict(elem_type=elem_type, n_nodes=X.shape[0], conn=np.ascontiguousarray(conn), gradN=gN, qp_w=w), u
+
+
+def _rel(a, b):
+    return np.abs(a - b).max() / np.abs(b).max()
+
+
+@pytest.mark.parametrize("elem_type,n", [(HEX8, 4), (TET10, 2)])
+@pytest.mark.parametrize("name", sorted(VARIANTS))
+@pytest.mark.parametrize("kernel", [0, 1])
+def test_variant_assembly_matches_oracle(pc, name, elem_type, n, kernel):
+    ncm = VARIANTS[name]()
+    mesh, u = _mesh(elem_type, n)
+    lib = pc.Commet(mesh, ncm)
+    lib.set_kernel(kernel)
+    r, v = lib.assemble(torch.from_numpy(u).cuda())
+    assert lib.check() == -1
+    rp, ci = lib.pattern()
+    ro, vo, bad = oracle.assemble(ncm, mesh["n_nodes"], mesh["conn"], mesh["gradN"], mesh["qp_w"], u, rp, ci)
+    assert bad == -1
+    assert _rel(r.cpu().numpy(), ro) <= TOL and _rel(v.cpu().numpy(), vo) <= TOL
+
+
+@pytest.mark.parametrize("name", ["gent_thomas", "cann_standard", "cann_isochoric"])
+def test_analytic_ncm_eval_matches_oracle(pc, name):
+    ncm = VARIANTS[name]()
+    mesh, _ = _mesh(HEX8, 1)
+    lib = pc.Commet(mesh, ncm)
+    rng = np.random.default_rng(12)
+    k = rng.uniform(-0.4, 0.4, size=(25, 3))
+    g, H = lib.ncm_eval(torch.from_numpy(k).cuda())
+    g, H = g.cpu().numpy(), H.cpu().numpy()
+    for i in range(k.shape[0]):
+        _, go, Ho = oracle.ncm_eval(dict(ncm, kappa=0.0), k[i])
+        assert np.abs(g[i] - go).max() <= 1e-14 * max(1.0, np.abs(go).max())
+        assert np.abs(H[i] - Ho[np.triu_indices(3)]).max() <= 1e-14 * max(1.0, np.abs(Ho).max())
+
+
+@pytest.mark.parametrize("name", ["gent_thomas", "icnn_isochoric_16x2", "cann_isochoric"])
+def test_normalize_reference_variants(pc, name):
+    ncm = VARIANTS[name]()
+    mesh, _ = _mesh(HEX8, 1)
+    lib = pc.Commet(mesh, ncm)
+    s0 = lib.normalize_reference()
+    ref = on.reference_shift(ncm)
+    assert abs(s0 - ref) <= 1e-13 * max(1.0, abs(ref))
+    if name == "gent_thomas":
+        assert s0 == 0.0  # stress-free by construction (App. C)

@@ -1,0 +1,121 @@
+"""Pins of the oracle's kinematic and inner-network variants (SURVEY.md s8(f)
+rank 2): isochoric invariants + J (App. A.2.2, written in the
+paper's spatial G-tensor form and pulled back), CANN (Eq. cann-def /
+cann-chain-rule) and the Gent-Thomas reference model (App. C,
+PAPER.md:1075-1079).  Each is checked against hyper-dual derivatives of W(F)
+written from the definitions (tests/hyperdual.py), closed forms and the values
+SPEC.md fixes."""
+import numpy as np
+import pytest
+
+import oracle
+from synth.gen import cann_params, gent_thomas_params, hex_mesh, ncm_weights, shape_gradients
+from tests import hyperdual
+from tests.test_oracle_material import I3, rand_F, rot
+
+
+def isochoric_icnn():
+    m = ncm_weights(8, 2, 0.3, 11, 10.0)
+    m["kinematics"] = "isochoric"
+    return m
+
+
+VARIANTS = {
+    "gent_thomas": lambda: gent_thomas_params(),
+    "cann_standard": lambda: cann_params(4, seed=3),
+    "cann_isochoric": lambda: cann_params(5, seed=4, kinematics="isochoric"),
+    "icnn_isochoric": isochoric_icnn,
+}
+
+
+# ---- Gent-Thomas values the paper / SPEC fix ------------------------------------------
+def test_gent_thomas_reference_values():
+    m = gent_thomas_params()
+    o = oracle.material_point(m, I3)
+    assert o["W"] == 0.0 and np.abs(o["S"]).max() < 1e-15          # Psi(I) = 0, tau(I) = 0
+    o = oracle.material_point(m, 2.0 * I3)
+    assert abs(o["W"] - 49.0) < 1e-12                               # Psi(diag(2,2,2)) = (8-1)^2
+    assert np.allclose(o["k"], [0.0, 0.0, 7.0], atol=1e-13)         # Ibar1 = 3, J = 8
+
+
+def test_isochoric_invariance_and_objectivity():
+    rng = np.random.default_rng(8)
+    m = isochoric_icnn()
+    for _ in range(4):
+        F = rand_F(rng)
+        k = oracle.material_point(m, F)["k"]
+        for c in (0.7, 1.9):
+            kc = oracle.material_point(m, c * F)["k"]
+            assert np.abs(kc[:2] - k[:2]).max() < 1e-13            # Ibar_m(cF) = Ibar_m(F)
+        kq = oracle.material_point(m, rot(rng) @ F)["k"]
+        assert np.abs(kq - k).max() < 1e-13
+
+
+# ---- CANN -------------------------------------------------------------------------
+def test_cann_hessian_is_diagonal():
+    m = cann_params(6, seed=2)
+    rng = np.random.default_rng(1)
+    for _ in range(5):
+        _, g, H = oracle.ncm_eval(m, rng.uniform(-0.4, 0.4, 3))
+        assert not (H - np.diag(np.diag(H))).any()
+
+
+def test_cann_single_branch_closed_forms():
+    base = dict(network="cann", kinematics="standard", width=8, n_hidden=1, W1=None, W=None, b=None, a=None,
+                skip_out=None, skip_hidden=None, kappa=0.0, ref_shift=0.0)
+    K = np.array([0.3, -0.2, 0.15])
+    w1 = np.full((3, 1), 0.2)
+    w2 = np.array([[1.5], [0.5], [2.0]])
+    # identity, x^1, linear: N = sum_m w2 w1 K_m
+    m = dict(base, cann_f=np.tile(np.array([0, 1, 0], np.int32), (3, 1, 1)), cann_w1=w1, cann_w2=w2)
+    N, g, H = oracle.ncm_eval(m, K)
+    assert np.allclose(g, (w2 * w1)[:, 0], rtol=0, atol=1e-16) and not H.any()
+    # Macaulay, x^2, exp: N = sum_m w2 (exp(w1 <K_m>^2) - 1)
+    m = dict(base, cann_f=np.tile(np.array([1, 2, 1], np.int32), (3, 1, 1)), cann_w1=w1, cann_w2=w2)
+    N, g, H = oracle.ncm_eval(m, K)
+    Kp = np.maximum(K, 0)
+    e = np.exp(0.2 * Kp ** 2)
+    assert abs(N - np.sum(w2[:, 0] * (e - 1))) < 1e-15
+    assert np.allclose(g, w2[:, 0] * e * 0.4 * Kp, rtol=1e-14, atol=0)
+    assert np.allclose(np.diag(H), w2[:, 0] * (e * 0.4 + e * (0.4 * Kp) ** 2) * (K > 0), rtol=1e-14, atol=0)
+    # abs, x^3, -ln(1 - w1 x): second derivative w1^2/(1 - w1 x)^2 f1'^2 + ... (reading R22)
+    m = dict(base, cann_f=np.tile(np.array([2, 3, 2], np.int32), (3, 1, 1)), cann_w1=w1, cann_w2=w2)
+    N, g, H = oracle.ncm_eval(m, K)
+    x = np.abs(K) ** 3
+    d1, dd1 = 3 * K ** 2 * np.sign(K), 6 * np.abs(K)
+    q = 1 - 0.2 * x
+    assert np.allclose(g, w2[:, 0] * 0.2 / q * d1, rtol=1e-14, atol=0)
+    assert np.allclose(np.diag(H), w2[:, 0] * (0.04 / q ** 2 * d1 ** 2 + 0.2 / q * dd1), rtol=1e-14, atol=0)
+
+
+# ---- every variant: P and A exact from W(F) ------------------------------------------------
+@pytest.mark.parametrize("name", sorted(VARIANTS))
+def test_hyperdual_P_and_A_variants(name):
+    m = VARIANTS[name]()
+    rng = np.random.default_rng(21)
+    for F in [I3 + 1e-3 * rng.normal(size=(3, 3))] + [rand_F(rng) for _ in range(3)]:
+        W, P, A = hyperdual.derivatives(F, m)
+        o = oracle.material_point(m, F)
+        assert abs(o["W"] - W) < 1e-13 * max(1, abs(W))
+        assert np.max(np.abs(o["P"] - P)) < 1e-12 * max(1e-3, np.abs(P).max())
+        assert np.max(np.abs(o["A"] - A)) < 1e-12 * np.abs(A).max()
+
+
+@pytest.mark.parametrize("name", sorted(VARIANTS))
+def test_assembly_residual_is_energy_gradient(name):
+    """r = dPi/du by central differences of the oracle energy on a 2^3 mesh."""
+    m = VARIANTS[name]()
+    X, conn = hex_mesh(2, 0.1, seed=3)
+    gN, w = shape_gradients(X, conn, 0)
+    rng = np.random.default_rng(6)
+    u = rng.uniform(-0.03, 0.03, size=X.size)
+    rp, ci = oracle.pattern(X.shape[0], conn)
+    r, vals, bad = oracle.assemble(m, X.shape[0], conn, gN, w, u, rp, ci)
+    assert bad == -1
+    h = 1e-6
+    for i in rng.choice(u.size, 6, replace=False):
+        up, um = u.copy(), u.copy()
+        up[i] += h
+        um[i] -= h
+        fd = (oracle.energy(m, conn, gN, w, up) - oracle.energy(m, conn, gN, w, um)) / (2 * h)
+        assert abs(fd - r[i]) <= 1e-7 * max(1e-3, np.abs(r).max())

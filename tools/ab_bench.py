@@ -11,19 +11,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from synth import gen
 
 
-class MeshDesc(C.Structure):
-    _fields_ = [("elem_type", C.c_int32), ("n_nodes", C.c_int64), ("n_elems", C.c_int64),
-                ("conn", C.c_void_p), ("grad_N", C.c_void_p), ("qp_w", C.c_void_p),
-                ("owned_node_begin", C.c_int64), ("owned_node_end", C.c_int64),
-                ("n_ranks", C.c_int32), ("rank", C.c_int32), ("rank_node_begin", C.c_void_p),
-                ("n_ghost", C.c_int64), ("ghost_conn", C.c_void_p), ("ghost_rank", C.c_void_p),
-                ("scatter_order", C.c_int32)]
-
-
-class NcmDesc(C.Structure):
-    _fields_ = [("n_hidden", C.c_int32), ("width", C.c_int32), ("W1", C.c_void_p), ("W", C.c_void_p),
-                ("b", C.c_void_p), ("a", C.c_void_p), ("skip_out", C.c_void_p),
-                ("skip_hidden", C.c_void_p), ("kappa", C.c_double), ("ref_shift", C.c_double)]
+from paper_2510_00884_b200 import MeshDesc, NcmDesc  # noqa: E402  (struct layouts of include/commet.h)
 
 
 def run(path, cfg, steps=20):
