@@ -128,7 +128,8 @@ enum { COMMET_NET_ICNN = 0, COMMET_NET_CANN = 1, COMMET_NET_GENT_THOMAS = 2 };
  * a one-thread-per-element CUDA kernel kept as an independent GPU cross-check. */
 enum { COMMET_KERNEL_FUSED = 0, COMMET_KERNEL_SIMPLE = 1 };
 
-/* Build the CSR pattern, element colouring and scatter maps, upload inputs.
+/* Build the CSR pattern, element colouring and scatter maps, upload inputs
+ * (mesh may be NULL: a ctx for the material-point calls only).
  *   device     CUDA device ordinal
  *   cuda_stream  cudaStream_t for the uploads (NULL = legacy default stream)
  *   nccl_comm  ncclComm_t of the partition (see commet_nccl_comm_init), or NULL
@@ -239,6 +240,18 @@ commet_status commet_max_trace_C(commet_ctx ctx, double* max_trC);
  * ref_shift excluded.  Asynchronous on cuda_stream. */
 commet_status commet_ncm_eval(commet_ctx ctx, const double* k, double* g, double* H, int64_t n,
                               void* cuda_stream);
+/* Material-point batch (the paper's material point
+ * benchmarks): for n deformation gradients F (device [n][9],
+ * row-major F_iJ) the strain energy density Psi (device [n]), the Kirchhoff stress
+ * tau = F S F^T (device [n][6], Voigt order 00, 11, 22, 12, 02, 01) and the spatial
+ * tangent c_ijkl = F_iI F_jJ F_kK F_lL CC_IJKL (device [n][21]: the upper triangle
+ * of its 6x6 Voigt matrix, row-major) -- the (Psi, tau, c) tables of Alg. 2/3
+ * (PAPER.md:254-327).  Any output may be NULL.  Runs the fused kernel's network
+ * stages on batches of points; works on a ctx set up with mesh = NULL.
+ * Asynchronous; det F <= 0 is reported by commet_check as the point index. */
+commet_status commet_material_eval(commet_ctx ctx, const double* F, int64_t n, double* W, double* tau,
+                                   double* c, void* cuda_stream);
+
 /* Stress-free reference (reading R11): sets the ctx's ref_shift to
  * s0 = 2 g1 + 4 g2 + g3 at k = 0, so that S(F = I) = 0 for subsequent assembles,
  * and returns it in *s0 (may be NULL).  Synchronous. */

@@ -34,7 +34,8 @@ SYMBOLS = ("commet_setup", "commet_csr_pattern", "commet_csr_pattern_copy", "com
            "commet_plan_create", "commet_plan_info", "commet_plan_csr", "commet_plan_halo",
            "commet_plan_send", "commet_plan_recv", "commet_plan_colours", "commet_plan_destroy",
            "commet_kernel_info", "commet_max_trace_C", "commet_set_dirichlet", "commet_apply_dirichlet",
-           "commet_cg_jacobi", "commet_newton_step", "commet_ncm_eval", "commet_normalize_reference")
+           "commet_cg_jacobi", "commet_newton_step", "commet_ncm_eval", "commet_normalize_reference",
+           "commet_material_eval")
 NEWTON_MAX_LOG = 64
 
 
@@ -145,6 +146,8 @@ _lib.commet_cg_jacobi.argtypes = [_vp, _vp, _vp, _vp, C.c_double, _i32, _P(_i32)
 _lib.commet_newton_step.argtypes = [_vp, _vp, _P(NewtonCfg), _vp, _P(NewtonReport), _vp]
 _lib.commet_ncm_eval.argtypes = [_vp, _vp, _vp, _vp, _i64, _vp]
 _lib.commet_normalize_reference.argtypes = [_vp, _P(C.c_double)]
+_lib.commet_material_eval.argtypes = [_vp, _vp, _i64, _vp, _vp, _vp, _vp]
+_lib.commet_material_eval.restype = C.c_int
 for _f in ("commet_ncm_eval", "commet_normalize_reference", "commet_max_trace_C", "commet_set_dirichlet", "commet_apply_dirichlet", "commet_cg_jacobi",
            "commet_newton_step"):
     getattr(_lib, _f).restype = C.c_int
@@ -201,17 +204,20 @@ class Commet:
     W, b, a, optional skip_out, skip_hidden, kappa, ref_shift.
     """
 
-    def __init__(self, mesh: dict, ncm: dict, device: int = 0, stream=None, nccl_comm=None):
+    def __init__(self, mesh: dict | None, ncm: dict, device: int = 0, stream=None, nccl_comm=None):
         import torch
         self.torch = torch
         self.device = torch.device("cuda", device)
-        md, _keep = _mesh_desc(mesh)
-        n_nodes, nb, ne = md.n_nodes, md.owned_node_begin, md.owned_node_end
+        if mesh is None:  # material-point calls only
+            md, _keep, n_nodes, nb, ne = None, None, 0, 0, 0
+        else:
+            md, _keep = _mesh_desc(mesh)
+            n_nodes, nb, ne = md.n_nodes, md.owned_node_begin, md.owned_node_end
         nd, _keep_ncm = ncm_desc(ncm)
         st = stream if stream is not None else torch.cuda.current_stream(self.device)
         ctx = C.c_void_p()
         with torch.cuda.device(self.device):
-            status = _lib.commet_setup(C.byref(md), C.byref(nd), device, st.cuda_stream,
+            status = _lib.commet_setup(None if md is None else C.byref(md), C.byref(nd), device, st.cuda_stream,
                                        nccl_comm, C.byref(ctx))
         if status != COMMET_OK:
             raise CommetError(status, _lib.commet_last_error(None).decode())
@@ -320,6 +326,19 @@ class Commet:
         _check(_lib.commet_ncm_eval(self.ctx, k.data_ptr(), g.data_ptr(), H.data_ptr(), n, st.cuda_stream),
                self.ctx)
         return g, H
+
+    def material_eval(self, F, want_c=True, stream=None):
+        """Psi [n], tau [n,6] (Voigt 00,11,22,12,02,01), c [n,21] (upper 6x6 Voigt) at F (cuda [n,3,3])."""
+        t = self.torch
+        F = F.contiguous()
+        n = F.shape[0]
+        W = t.empty(n, dtype=t.float64, device=F.device)
+        tau = t.empty((n, 6), dtype=t.float64, device=F.device)
+        c = t.empty((n, 21), dtype=t.float64, device=F.device) if want_c else None
+        st = stream if stream is not None else t.cuda.current_stream(self.device)
+        _check(_lib.commet_material_eval(self.ctx, F.data_ptr(), n, W.data_ptr(), tau.data_ptr(),
+                                         None if c is None else c.data_ptr(), st.cuda_stream), self.ctx)
+        return W, tau, c
 
     def normalize_reference(self) -> float:
         """Make F = I stress-free (sets ref_shift); returns s0."""

@@ -31,7 +31,7 @@ extern "C" commet_status commet_setup(const commet_mesh_desc* mesh, const commet
                                       commet_ctx* out) {
   if (!out) return fail(nullptr, COMMET_ERR_ARG, "out is NULL");
   *out = nullptr;
-  if (!mesh || !ncm) return fail(nullptr, COMMET_ERR_ARG, "mesh or ncm descriptor is NULL");
+  if (!ncm) return fail(nullptr, COMMET_ERR_ARG, "ncm descriptor is NULL");
   std::unique_ptr<commet_ctx_s> c(new (std::nothrow) commet_ctx_s());
   if (!c) return fail(nullptr, COMMET_ERR_OOM, "host allocation failed");
   commet_ctx C = c.get();
@@ -43,7 +43,7 @@ extern "C" commet_status commet_setup(const commet_mesh_desc* mesh, const commet
     return fail(C, COMMET_ERR_ARG, "network %d unknown", net);
   // analytic networks use no hidden layers (the ICNN fields are ignored)
   const int L = net == COMMET_NET_ICNN ? ncm->n_hidden : 1, w = net == COMMET_NET_ICNN ? ncm->width : 16;
-  const bool tet = mesh->elem_type == COMMET_TET10;
+  const bool tet = mesh && mesh->elem_type == COMMET_TET10;
   if (net == COMMET_NET_ICNN) {
     if (L < 1 || L > kMaxLayers) return fail(C, COMMET_ERR_ARG, "n_hidden %d not in 1..%d", L, kMaxLayers);
     if (!fused_supported(tet ? 10 : 8, tet ? 4 : 8, w, L))
@@ -63,7 +63,8 @@ extern "C" commet_status commet_setup(const commet_mesh_desc* mesh, const commet
     }
   }
   Plan& p = c->plan;
-  {
+  c->material_only = (mesh == nullptr);
+  if (mesh) {
     std::string err;
     commet_status s = plan_build(mesh, p, err);
     if (s != COMMET_OK) return fail(C, s, "%s", err.c_str());
@@ -76,7 +77,7 @@ extern "C" commet_status commet_setup(const commet_mesh_desc* mesh, const commet
   cudaStream_t st = (cudaStream_t)cuda_stream;
 
   // ---- per-element arrays in colour order -------------------------------------------------
-  {
+  if (mesh) {
     std::vector<int32_t> conn_s(n_el * n_en), lrow_s(n_el * n_en);
     std::vector<double> w_s(n_el * n_q);
 #pragma omp parallel for schedule(static)
@@ -103,7 +104,7 @@ extern "C" commet_status commet_setup(const commet_mesh_desc* mesh, const commet
     CUDA_TRY(C, cudaStreamSynchronize(st));
   }
   // gradN: gather in colour order through pinned staging buffers (inputs may be tens of GB)
-  {
+  if (mesh) {
     const size_t per = (size_t)n_q * n_en * 3;
     CUDA_TRY(C, c->gradN.alloc((size_t)n_el * per));
     const int64_t chunk = std::max<int64_t>(1, (64 << 20) / (int64_t)(per * sizeof(double)));
@@ -249,6 +250,7 @@ extern "C" commet_status commet_assemble(commet_ctx c, const double* u, double* 
                                          double* csr_values, void* cuda_stream) {
   if (!c) return fail(nullptr, COMMET_ERR_ARG, "ctx is NULL");
   const Plan& p = c->plan;
+  if (c->material_only) return fail(c, COMMET_ERR_ARG, "ctx was set up without a mesh (material points only)");
   if (!u || (p.n_owned && !residual) || (p.nnz && !csr_values))
     return fail(c, COMMET_ERR_ARG, "u, residual or csr_values is NULL");
   cudaStream_t st = (cudaStream_t)cuda_stream;

@@ -57,6 +57,11 @@ struct AsmArgs {
   double* v_halo;
   unsigned long long* bad;
   unsigned long long* max_trc;  // max over qps of tr C = I1 (> 0: the bit pattern orders like the value)
+  // material-point mode (launch_material): F [n][9] in; Psi [n], tau [n][6], c [n][21] out (each may be NULL)
+  const double* Fin;
+  double* Wout;
+  double* tau_out;
+  double* c_out;
   NcmDev ncm;
 };
 
@@ -66,6 +71,7 @@ int launch_unpack(const double* vals, const int64_t* vmap, int64_t nv, double* c
                   const int64_t* rmap, int64_t nr, double* r, void* stream);
 int launch_activation(const double* y, double* z, double* s, int64_t n, const double* tab, void* stream);
 int launch_fused(const AsmArgs& a, void* stream, int* launches);
+int launch_material(const AsmArgs& a, void* stream);
 int fused_supported(int n_en, int n_q, int w, int L);
 void fused_occupancy(int n_en, int w, int L, int* smem_bytes, int* ctas_per_sm, int* regs);
 // prepares the fragment-ordered weight array on the host (size in doubles)

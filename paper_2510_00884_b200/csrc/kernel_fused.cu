@@ -103,12 +103,13 @@ __device__ __forceinline__ double2 ldg2(const double* p) {
 // NET_: 0 = ICNN (DMMA network stages 2-6), 1 = analytic inner network (CANN or
 // Gent-Thomas, evaluated per qp in stage 7a; W is then unused).  KIN_: 0 standard
 // invariants, 1 isochoric (compile-time, so the standard path carries no extra code)
-template <int W_, int Q_, int NEN_, int NQ_, int MINB_ = 3, int NET_ = 0, int KIN_ = 0>
+// MODE_: 0 = FE assembly; 1 = material points (F in; Psi, tau, c out; NEN = NQ = 1)
+template <int W_, int Q_, int NEN_, int NQ_, int MINB_ = 3, int NET_ = 0, int KIN_ = 0, int MODE_ = 0>
 struct Cfg {
-  static constexpr int W = W_, Q = Q_, NEN = NEN_, NQ = NQ_, NET = NET_, KIN = KIN_;
+  static constexpr int W = W_, Q = Q_, NEN = NEN_, NQ = NQ_, NET = NET_, KIN = KIN_, MODE = MODE_;
   static constexpr int NWARP = 4, NTHR = 128;
   static constexpr int MINB = MINB_;               // CTAs per SM the register budget targets (3: <= 168 regs)
-  static constexpr bool DMMA_ELEM = COMMET_DMMA_ELEM == 2 || (COMMET_DMMA_ELEM == 1 && NEN == 8);
+  static constexpr bool DMMA_ELEM = MODE == 0 && (COMMET_DMMA_ELEM == 2 || (COMMET_DMMA_ELEM == 1 && NEN == 8));
   static constexpr int E = Q / NQ;                 // elements per CTA iteration
   static constexpr int MTILES = W / 8, QB = Q / 8, KT2 = W / 8;
   // value / adjoint warp tiles: VMG x VNG warps, each MT_V x NT_V tiles
@@ -116,6 +117,8 @@ struct Cfg {
   static constexpr int NT_V = (QB >= 2 && TPW % 2 == 0 && TPW >= 4) ? 2 : 1;
   static constexpr int MT_V = TPW / NT_V;
   static constexpr int VNG = QB / NT_V, VMG = MTILES / MT_V;
+  // material mode: rows of per-qp partial sums of the network value a . z_L
+  static constexpr int NPR = MODE == 0 ? 0 : (VMG > NTHR / Q ? VMG : NTHR / Q);
   // Jacobian warp tiles: JMG m-groups x QB qp blocks, each MT_J x 3 tiles
   static constexpr int JMG = NWARP / QB, MT_J = MTILES / JMG;
   // A-fragment register ring depth (k-steps) of the value/adjoint and Jacobian GEMMs
@@ -134,7 +137,7 @@ struct Cfg {
 template <class C>
 struct Smem {
   static constexpr int PS = 101;  // per-qp stride of the stage-7a outputs (odd: bank spread)
-  int act, sb, cb, qF, qk, qg, qH, hred, gsk, gN, ue, wq, tab, qP, post, X, qA, total;
+  int act, sb, cb, qF, qk, qg, qH, hred, gsk, gN, ue, wq, qN, tab, qP, post, X, qA, total;
   __host__ __device__ Smem(int L) {
     int o = 0;
     act = o; o += C::W * C::LDA;
@@ -151,6 +154,7 @@ struct Smem {
     gN = o;  o += C::Q * C::NEN * 3;
     ue = o;  o += C::E * C::NEN * 3;
     wq = o;  o += C::Q;
+    qN = o;  o += C::NPR * C::Q;
     tab = o; o += kActTabSize;
     o = (o + 1) & ~1;
     const int xs = C::DMMA_ELEM ? 0 : C::Q * C::NEN * 27;  // X only for the scalar element path
@@ -205,6 +209,91 @@ __device__ __forceinline__ void warp_gemm(const double* __restrict__ Af, int mt0
   }
 }
 
+// Material-point outputs of one batch (MODE 1): per point
+// Psi = N + kappa (J-1)^2 - s0 (J-1), tau = F S F^T = P F^T and the spatial tangent
+// c_ijkl = sum_JL A_iJkL F_jJ F_lL - d_ik tau_jl (App. A.1), Voigt
+// order (00, 11, 22, 12, 02, 01); c as the 21 upper-triangle entries, row-major.
+__constant__ int kVoigt[6][2] = {{0, 0}, {1, 1}, {2, 2}, {1, 2}, {0, 2}, {0, 1}};
+__constant__ int kVoigtPair[21][2] = {{0, 0}, {0, 1}, {0, 2}, {0, 3}, {0, 4}, {0, 5}, {1, 1}, {1, 2}, {1, 3},
+                                      {1, 4}, {1, 5}, {2, 2}, {2, 3}, {2, 4}, {2, 5}, {3, 3}, {3, 4}, {3, 5},
+                                      {4, 4}, {4, 5}, {5, 5}};
+
+template <class C>
+__device__ __forceinline__ void material_outputs(const AsmArgs& A, const NcmDev& m, int L, int64_t e0, int ne,
+                                                 const double* qF, const double* qk, const double* qg,
+                                                 const double* qH, const double* hred, const double* qNp,
+                                                 double* qP, double* post, double* qA) {
+  constexpr int Q = C::Q, PS = Smem<C>::PS;
+  const int tid = threadIdx.x;
+  if (tid < Q) {
+    const int q = tid;
+    double gq[3], H6[6], N = 0.0;
+    const double* kq = qk + q * 3;
+    if constexpr (C::NET == 0) {
+#pragma unroll
+      for (int x = 0; x < 3; x++) gq[x] = qg[q * 3 + x];
+#pragma unroll
+      for (int x = 0; x < 6; x++) {
+        double s = qH[q * 6 + x];
+        if (L > 1)
+#pragma unroll
+          for (int r = 0; r < C::JMG; r++) s += hred[(r * Q + q) * 6 + x];
+        H6[x] = s;
+      }
+      const int rows = L > 1 ? C::VMG : C::NTHR / Q;
+      for (int r = 0; r < rows; r++) N += qNp[r * Q + q];
+      N += __ldg(m.skip_out) * kq[0] + __ldg(m.skip_out + 1) * kq[1] + __ldg(m.skip_out + 2) * kq[2];
+    } else {
+      analytic_net(m.net, m.cann_n, m.cann_f, m.cann_w1, m.cann_w2, m.gt, m.skip_out, kq, gq, H6);
+      N = analytic_value(m.net, m.cann_n, m.cann_f, m.cann_w1, m.cann_w2, m.gt, m.skip_out, kq);
+    }
+    Kin kin;
+    kinematics(qF + q * 9, kin);
+    if constexpr (C::KIN == 1) isochoric_to_standard(kin, gq, H6);
+    const double jm1 = kin.J - 1.0;
+    const double Wv = N + m.kappa * jm1 * jm1 - m.ref_shift * jm1;
+    gq[2] += 2.0 * m.kappa * jm1 - m.ref_shift;
+    H6[5] += 2.0 * m.kappa;
+    post_qp(kin, gq, H6, 1.0, post + q * PS, qP + q * 9);
+    double tau[9];
+#pragma unroll
+    for (int i = 0; i < 3; i++)
+#pragma unroll
+      for (int j = 0; j < 3; j++)
+        tau[i * 3 + j] = qP[q * 9 + i * 3] * kin.F[j * 3] + qP[q * 9 + i * 3 + 1] * kin.F[j * 3 + 1] +
+                         qP[q * 9 + i * 3 + 2] * kin.F[j * 3 + 2];
+#pragma unroll
+    for (int x = 0; x < 9; x++) qP[q * 9 + x] = tau[x];
+    if (q < ne) {
+      if (A.Wout) A.Wout[e0 + q] = Wv;
+      if (A.tau_out)
+#pragma unroll
+        for (int v = 0; v < 6; v++) A.tau_out[(e0 + q) * 6 + v] = tau[kVoigt[v][0] * 3 + kVoigt[v][1]];
+    }
+  }
+  __syncthreads();
+  if (!A.c_out) return;
+  for (int it = tid; it < Q * 9; it += C::NTHR) {
+    const int q = it / 9, iJ = it % 9;
+    tangent_row(post + q * PS, iJ, qA + q * 81 + iJ * 9);
+  }
+  __syncthreads();
+  for (int it = tid; it < Q * 21; it += C::NTHR) {
+    const int q = it / 21, vw = it % 21;
+    if (q >= ne) continue;
+    const int i = kVoigt[kVoigtPair[vw][0]][0], j = kVoigt[kVoigtPair[vw][0]][1];
+    const int k = kVoigt[kVoigtPair[vw][1]][0], l = kVoigt[kVoigtPair[vw][1]][1];
+    const double* F = qF + q * 9;
+    const double* Aq = qA + q * 81;
+    double c = (i == k) ? -qP[q * 9 + j * 3 + l] : 0.0;
+#pragma unroll
+    for (int J = 0; J < 3; J++)
+#pragma unroll
+      for (int Lx = 0; Lx < 3; Lx++) c += Aq[(i * 3 + J) * 9 + k * 3 + Lx] * F[j * 3 + J] * F[l * 3 + Lx];
+    A.c_out[(e0 + q) * 21 + vw] = c;
+  }
+}
+
 template <class C>
 __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
   constexpr int W = C::W, Q = C::Q, NEN = C::NEN, NQ = C::NQ, E = C::E;
@@ -224,6 +313,7 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
   double* sgN = smem + sm.gN;
   double* sue = smem + sm.ue;
   double* swq = smem + sm.wq;
+  double* qNp = smem + sm.qN;
   double* stab = smem + sm.tab;
   double* qA = smem + sm.qA;
   double* qP = smem + sm.qP;
@@ -300,6 +390,10 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
     const int ne = rem < E ? (int)rem : E;
 
     // ---- stage 0: stage element inputs --------------------------------------------
+    if constexpr (C::MODE == 1) {  // material points: F rows (tail points get F = I)
+      for (int x = tid; x < Q * 9; x += C::NTHR)
+        qF[x] = x / 9 < ne ? __ldg(A.Fin + e0 * 9 + x) : ((x % 9) % 4 == 0 ? 1.0 : 0.0);
+    } else {
 #if COMMET_PREFETCH
     // the first batch loads here; later batches were loaded into registers during the
     // previous batch's element stage (pf_*), so only the shared-memory stores remain
@@ -322,6 +416,7 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
       for (int x = tid; x < Q; x += C::NTHR) swq[x] = x < ne * NQ ? __ldg(A.qp_w + e0 * NQ + x) : 0.0;
     }
 #endif
+    }  // MODE
     __syncthreads();
     STAGE_MARK(0)
 
@@ -331,19 +426,26 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
       const double* gq = sgN + q * NEN * 3;
       const double* ue = sue + e * NEN * 3;
       double F[9];
+      if constexpr (C::MODE == 1) {
 #pragma unroll
-      for (int i = 0; i < 3; i++)
+        for (int x = 0; x < 9; x++) F[x] = qF[q * 9 + x];
+      } else {
 #pragma unroll
-        for (int J = 0; J < 3; J++) {
-          double s = (i == J) ? 1.0 : 0.0;
+        for (int i = 0; i < 3; i++)
 #pragma unroll
-          for (int a = 0; a < NEN; a++) s += ue[a * 3 + i] * gq[a * 3 + J];
-          F[i * 3 + J] = s;
-        }
+          for (int J = 0; J < 3; J++) {
+            double s = (i == J) ? 1.0 : 0.0;
+#pragma unroll
+            for (int a = 0; a < NEN; a++) s += ue[a * 3 + i] * gq[a * 3 + J];
+            F[i * 3 + J] = s;
+          }
+      }
       Kin kin;
       kinematics(F, kin);
       if (e < ne) {
-        if (!(kin.J > 0.0)) atomicMin(A.bad, (unsigned long long)(__ldg(A.orig + e0 + e) * NQ + q % NQ));
+        if (!(kin.J > 0.0))
+          atomicMin(A.bad, C::MODE == 1 ? (unsigned long long)(e0 + q)
+                                        : (unsigned long long)(__ldg(A.orig + e0 + e) * NQ + q % NQ));
         trc_max = fmax(trc_max, kin.I1);  // one atomic per CTA at the end (a per-qp atomic on one
                                           // address serialises in L2: measured -6% on c3)
       }
@@ -386,6 +488,7 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
         yv[i] = __ldg(m.b + j) + __ldg(m.W1 + j * 3 + 0) * k0 + __ldg(m.W1 + j * 3 + 1) * k1 +
                 __ldg(m.W1 + j * 3 + 2) * k2;
       }
+      double nv = 0.0;  // material mode, L == 1: partial a . z_1 of this thread's neurons
 #pragma unroll
       for (int i = 0; i < NIT; i++) {
         const int j = j0 + i * JS;
@@ -398,8 +501,11 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
           const double aj = __ldg(m.a + j);
           act[j * LDA + q] = aj * s;
           cb[j * LDS + q] = aj * s * (1.0 - s);
+          nv += aj * z;
         }
       }
+      if constexpr (C::MODE == 1)
+        if (L == 1) qNp[j0 * Q + q] = nv;
     }
     if (false)
 #endif
@@ -428,6 +534,9 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
       int ncol[C::NT_V];
 #pragma unroll
       for (int j = 0; j < C::NT_V; j++) ncol[j] = (vn * C::NT_V + j) * 8;
+      double nacc[C::NT_V][2];  // material mode: partial a . z_L per owned qp column
+#pragma unroll
+      for (int jj = 0; jj < C::NT_V; jj++) nacc[jj][0] = nacc[jj][1] = 0.0;
       for (int l = 2; l <= L; l++) {
         double acc[C::MT_V][C::NT_V][2];
         warp_gemm<C::MT_V, C::NT_V, KT2, C::PD_V>(m.Wfrag + (l - 2) * frag_layer, mt0, act, LDA, ncol, acc);
@@ -451,6 +560,16 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
               const int q = ncol[jj] + 2 * t + h;
               double y = acc[i][jj][h] + bj;
               if (skips) y += B3[0] * qk[q * 3] + B3[1] * qk[q * 3 + 1] + B3[2] * qk[q * 3 + 2];
+              if constexpr (C::MODE == 1) {  // material points need the value: z_L too
+                if (l == L) {
+                  double z, s;
+                  softplus_sig(y, stab, z, s);
+                  act[j * LDA + q] = aj * s;
+                  cb[((l - 2) * W + j) * LDS + q] = aj * s * (1.0 - s);
+                  nacc[jj][h] += aj * z;
+                  continue;
+                }
+              }
 #if COMMET_SIGMOID_LAST
               if (l < L) {
                 double z, s;
@@ -476,6 +595,20 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
             }
         }
         __syncthreads();
+      }
+      if constexpr (C::MODE == 1) {
+        if (L > 1) {  // reduce the 8 row groups g of the warp, one partial per (vm, q)
+#pragma unroll
+          for (int jj = 0; jj < C::NT_V; jj++)
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+              double v = nacc[jj][h];
+              v += __shfl_xor_sync(0xffffffffu, v, 4);
+              v += __shfl_xor_sync(0xffffffffu, v, 8);
+              v += __shfl_xor_sync(0xffffffffu, v, 16);
+              if (g == 0) qNp[vm * Q + ncol[jj] + 2 * t + h] = v;
+            }
+        }
       }
     }
 
@@ -708,6 +841,9 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
 #ifdef COMMET_EXP_SKIP_ELEM
     if (false) {
 #endif
+    if constexpr (C::MODE == 1) {
+      material_outputs<C>(A, m, L, e0, ne, qF, qk, qg, qH, hred, qNp, qP, post, qA);
+    } else {
     // ---- stage 7a: per qp -- penalty, S, T, Phi_m, Psi_m, b, P (all scaled by w) --------
 #if COMMET_PREFETCH
     if (batch + gridDim.x < n_batches) pf_load_a(batch + gridDim.x);
@@ -912,6 +1048,7 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
     }
 #endif
     }  // DMMA_ELEM
+    }  // MODE
 #ifdef COMMET_EXP_SKIP_ELEM
     }
 #endif
@@ -1064,6 +1201,26 @@ static int launch_k(const AsmArgs& a, cudaStream_t st, int* launches) {
     case 128: return launch_cfg<Cfg<128, 8, NEN, NQ, 3, 0, K>>(a, st, launches);
   }
   return (int)cudaErrorInvalidValue;
+}
+
+// material points: NEN = NQ = 1, one "element" per point
+template <int K>
+static int launch_mat_k(const AsmArgs& a, cudaStream_t st) {
+  if (a.ncm.net != 0) return launch_cfg<Cfg<16, 16, 1, 1, 3, 1, K, 1>>(a, st, nullptr);
+  switch (a.ncm.w) {
+    case 8: return launch_cfg<Cfg<8, 32, 1, 1, 3, 0, K, 1>>(a, st, nullptr);
+    case 16: return launch_cfg<Cfg<16, 16, 1, 1, 3, 0, K, 1>>(a, st, nullptr);
+    case 32: return launch_cfg<Cfg<32, 16, 1, 1, 3, 0, K, 1>>(a, st, nullptr);
+    case 64: return launch_cfg<Cfg<64, 16, 1, 1, 3, 0, K, 1>>(a, st, nullptr);
+    case 128: return launch_cfg<Cfg<128, 8, 1, 1, 3, 0, K, 1>>(a, st, nullptr);
+  }
+  return (int)cudaErrorInvalidValue;
+}
+
+int launch_material(const AsmArgs& a, void* stream) {
+  if (a.el_count <= 0) return 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  return a.ncm.kin == 1 ? launch_mat_k<1>(a, st) : launch_mat_k<0>(a, st);
 }
 
 template <int NEN, int NQ>

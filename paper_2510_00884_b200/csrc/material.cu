@@ -63,3 +63,30 @@ extern "C" commet_status commet_normalize_reference(commet_ctx c, double* s0) {
   if (s0) *s0 = h;
   return COMMET_OK;
 }
+
+extern "C" commet_status commet_material_eval(commet_ctx c, const double* F, int64_t n, double* W, double* tau,
+                                              double* cc, void* cuda_stream) {
+  if (!c) return fail(nullptr, COMMET_ERR_ARG, "ctx is NULL");
+  if (n < 0 || (n > 0 && !F)) return fail(c, COMMET_ERR_ARG, "F is NULL or n = %lld < 0", (long long)n);
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  c->last_stream = st;
+  CUDA_TRY(c, cudaMemsetAsync(c->bad.p, 0xff, sizeof(unsigned long long), st));
+  CUDA_TRY(c, cudaMemsetAsync(c->max_trc.p, 0, sizeof(unsigned long long), st));
+  if (n == 0) return COMMET_OK;
+  AsmArgs a{};
+  a.n_en = 1;
+  a.n_q = 1;
+  a.el_begin = 0;
+  a.el_count = n;
+  a.Fin = F;
+  a.Wout = W;
+  a.tau_out = tau;
+  a.c_out = cc;
+  a.bad = c->bad.p;
+  a.max_trc = c->max_trc.p;
+  a.ncm = c->ncm;
+  const int rc = launch_material(a, st);
+  if (rc) return fail(c, COMMET_ERR_CUDA, "material kernel launch: %s", cudaGetErrorString((cudaError_t)rc));
+  return COMMET_OK;
+}

@@ -248,6 +248,27 @@ __device__ __forceinline__ void analytic_net(int net, int n, const int32_t* __re
   H6[1] = H6[2] = H6[4] = 0.0;
 }
 
+// value of the analytic networks (material-point outputs): same closed forms as above
+__device__ __forceinline__ double analytic_value(int net, int n, const int32_t* __restrict__ f,
+                                                 const double* __restrict__ w1, const double* __restrict__ w2,
+                                                 const double* __restrict__ gt, const double* __restrict__ skip,
+                                                 const double* kin) {
+  if (net == 2) return gt[0] * kin[0] + gt[1] * log1p(kin[1] / 3.0) + gt[2] * kin[2] * kin[2];
+  double N = skip[0] * kin[0] + skip[1] * kin[1] + skip[2] * kin[2];
+  for (int m = 0; m < 3; m++) {
+    const double x = kin[m];
+    for (int bb = 0; bb < n; bb++) {
+      const int32_t* fb = f + (m * n + bb) * 3;
+      const int t0 = __ldg(fb), p = __ldg(fb + 1), t2 = __ldg(fb + 2);
+      const double a1 = __ldg(w1 + m * n + bb), a2 = __ldg(w2 + m * n + bb);
+      const double v0 = t0 == 0 ? x : (t0 == 1 ? fmax(x, 0.0) : fabs(x));
+      const double v1 = p == 1 ? v0 : (p == 2 ? v0 * v0 : v0 * v0 * v0);
+      N += a2 * (t2 == 0 ? a1 * v1 : (t2 == 1 ? expm1(a1 * v1) : -log1p(-a1 * v1)));
+    }
+  }
+  return N;
+}
+
 // ---------------------------------------------------------------------------
 // softplus z = log(1 + e^y) and sigmoid s = softplus' (SURVEY s7 hard part 3),
 // branch-free, fp64 FMA + integer ops only (no MUFU, no F2I, no libdevice slow
