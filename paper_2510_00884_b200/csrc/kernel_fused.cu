@@ -1138,21 +1138,30 @@ template <class C>
 static int launch_cfg(const AsmArgs& a, cudaStream_t st, int* launches) {
   const Smem<C> sm(a.ncm.L);
   const size_t bytes = (size_t)sm.total * sizeof(double);
-  static bool attr_set = false;
-  static size_t attr_bytes = 0;
-  if (!attr_set || attr_bytes < bytes) {
+  // per device: the shared-memory attribute, SM count and occupancy are queried once per
+  // (device, smem size) -- the host-side launch cost matters for small batches
+  constexpr int kDev = 16;
+  static size_t attr_bytes[kDev] = {0};
+  static int sms_c[kDev] = {0}, per_sm_c[kDev] = {0};
+  static size_t occ_bytes[kDev] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= kDev) return (int)cudaErrorInvalidDevice;
+  if (attr_bytes[dev] < bytes) {
     cudaError_t e = cudaFuncSetAttribute(fused_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     if (e != cudaSuccess) return (int)e;
-    attr_set = true;
-    attr_bytes = bytes;
+    attr_bytes[dev] = bytes;
   }
-  int dev = 0, sms = 148, per_sm = 1;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fused_kernel<C>, C::NTHR, bytes);
-  if (per_sm < 1) per_sm = 1;
+  if (occ_bytes[dev] != bytes) {
+    int sms = 148, per_sm = 1;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fused_kernel<C>, C::NTHR, bytes);
+    sms_c[dev] = sms;
+    per_sm_c[dev] = per_sm < 1 ? 1 : per_sm;
+    occ_bytes[dev] = bytes;
+  }
   const int64_t nb = (a.el_count + C::E - 1) / C::E;
-  const int64_t grid = std::min<int64_t>(nb, (int64_t)sms * per_sm);
+  const int64_t grid = std::min<int64_t>(nb, (int64_t)sms_c[dev] * per_sm_c[dev]);
   if (grid <= 0) return 0;
   fused_kernel<C><<<(unsigned)grid, C::NTHR, bytes, st>>>(a);
   if (launches) (*launches)++;
