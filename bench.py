@@ -29,6 +29,9 @@ from synth import gen  # noqa: E402
 METRIC = "quadrature-point stress+tangent updates/s (assembled elements/s and % fp64 roofline alongside)"
 FP64_PEAK_TFLOPS = 36.9   # measured, sustained DMMA m8n8k4, profiles/r01_fp64_peak.json
 FP64_PEAK_SOURCE = "measured: tools/fp64_peak.cu sustained DMMA (profiles/r01_fp64_peak.json); MEASURED_PEAKS.json has no fp64 entry"
+# DRAM bytes (read + write) per colour launch of the fused kernel, from ncu captures of this
+# kernel version (profiles/r01_ncu_c5_dram.csv, profiles/r01_ncu_full_c3_s2.txt); 8 equal colours
+NCU_DRAM_PER_LAUNCH = {"c3": 362.99e6 + 198.65e6, "c5": 23.43e9 + 14.88e9}
 
 WORKLOAD = {
     "c1": "c1: 4^3 hex8 unit cube, 2x2x2 Gauss (512 qp), NCM 16x2 softplus + kappa(J-1)^2, u ~ U(+-0.02)",
@@ -307,7 +310,11 @@ def main():
         kernel_ms_per_step=kern_ms,
         roofline=dict(bound="alu", pipe="fp64 (DFMA/DMMA share one datapath)", achieved=achieved,
                       peak=FP64_PEAK_TFLOPS, unit="TFLOP/s", frac=achieved / FP64_PEAK_TFLOPS,
-                      traffic=None, flops_per_qp=fl, peak_source=FP64_PEAK_SOURCE,
+                      traffic=(NCU_DRAM_PER_LAUNCH[args.config] * info["n_colours"]
+                               if args.config in NCU_DRAM_PER_LAUNCH and ws == 1 and args.kernel == "fused" else None),
+                      traffic_unit="bytes per step (all colour launches; ncu dram__bytes_read+write, "
+                                   "profiles/); algorithmic per step: hbm_algorithmic_gbs x kernel time",
+                      flops_per_qp=fl, peak_source=FP64_PEAK_SOURCE,
                       hbm_algorithmic_gbs=hbm * n_el / (kern_ms * 1e-3) / 1e9, hbm_peak_gbs=6556.2),
         clocks=clocks, gpu_launches=info["launches"] * args.steps,
         e2e=e2e, det_f_ok=(bad == -1),
