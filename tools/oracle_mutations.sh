@@ -15,7 +15,8 @@ p = 'oracle/oracle.c'; s = open(p).read(); a, b = sys.argv[1], sys.argv[2]
 assert a in s, a
 open(p, 'w').write(s.replace(a, b, 1))
 PY
-  if timeout 600 python -m pytest tests/test_oracle_material.py tests/test_oracle_assembly.py -q -x -m "not slow" >/dev/null 2>&1; then
+  if timeout 600 python -m pytest tests/test_oracle_material.py tests/test_oracle_assembly.py \
+      tests/test_oracle_variants.py tests/test_oracle_newton.py -q -x -m "not slow" >/dev/null 2>&1; then
     echo "NOT CAUGHT: $1 -> $2"; fail=1
   else
     echo "caught:     $1 -> $2"
@@ -31,4 +32,12 @@ mut "if (B) t += B[j * 3 + p];" ""
 mut "F[i * 3 + J] += u[3 * node + i] * gN[a * 3 + J];" "F[i * 3 + J] += u[3 * node + J] * gN[a * 3 + i];"
 mut "r[3 * (node - node_begin) + i] += wq * s;" "r[3 * (node - node_begin) + i] += s;"
 mut "double I2 = 0.5 * (I1 * I1 - trC2);" "double I2 = 0.5 * (I1 * I1 + trC2);"
+# the s8(f) variants: isochoric G-tensor table, CANN chain rule, Gent-Thomas
+mut "const double Ib[2] = {Ib1, Ib2}, e[2] = {-1.0 / 3.0, -2.0 / 3.0};" "const double Ib[2] = {Ib1, Ib2}, e[2] = {-1.0 / 3.0, -1.0 / 3.0};"
+mut "GGb[1][I4(i, j, k, l)] = Bb[i * 3 + j] * Bb[k * 3 + l] -" "GGb[1][I4(i, j, k, l)] = Bb[i * 3 + j] * Bb[k * 3 + l] +"
+mut "e[mm] * ((i == j) * Gb[mm][k * 3 + l] + Gb[mm][i * 3 + j] * (k == l)" "e[mm] * ((i == j) * Gb[mm][k * 3 + l]"
+mut "t += Fi[I * 3 + i] * Fi[J * 3 + j] * Fi[K * 3 + k] * Fi[L * 3 + l] * c[I4(i, j, k, l)];" "t += Fi[I * 3 + i] * Fi[J * 3 + j] * Fi[K * 3 + l] * Fi[L * 3 + k] * c[I4(i, j, k, l)] * 1.0000001;"
+mut "dd2 = w1 * w1 / ((1.0 - w1 * v1) * (1.0 - w1 * v1));" "dd2 = -w1 * w1 / ((1.0 - w1 * v1) * (1.0 - w1 * v1));"
+mut "H[mm * 3 + mm] += w2 * ((dd2 * d1 * d1 + d2 * dd1) * d0 * d0" "H[mm * 3 + mm] += w2 * ((dd2 * d1 + d2 * dd1) * d0 * d0"
+mut "H[4] = -m->gt[1] / ((K[1] + 3.0) * (K[1] + 3.0));" "H[4] = m->gt[1] / ((K[1] + 3.0) * (K[1] + 3.0));"
 exit $fail
