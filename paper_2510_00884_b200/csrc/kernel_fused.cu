@@ -51,6 +51,9 @@
 #ifndef COMMET_PD_J
 #define COMMET_PD_J 2
 #endif
+#ifndef COMMET_PINGPONG
+#define COMMET_PINGPONG 0  // measured neutral (c3 10.31 vs 10.26 ms): barriers kept
+#endif
 #ifndef COMMET_SYM_KE
 #define COMMET_SYM_KE 1
 #endif
@@ -129,7 +132,10 @@ struct Cfg {
   static_assert(Q <= 32, "stage-1 threads (one per qp) must sit in warp 0");
   static_assert(TPW >= 1 && VMG * VNG == NWARP && MT_V * NT_V == TPW, "value tiling");
   static_assert(JMG >= 1 && JMG * QB == NWARP && MT_J * JMG == MTILES, "jacobian tiling");
-  static_assert(VMG * Q * 9 <= W * LDA, "adjoint partials must fit in act");
+  // ping-pong of the value / adjoint passes between act column blocks [0, Q) and [Q, 2Q), the
+  // adjoint-pass g/H_1 partials in rows 9 vm + x of the free block [2Q, 3Q) (needs VMG*9 <= W)
+  static constexpr bool PP = COMMET_PINGPONG && VMG * 9 <= W;
+  static_assert(PP || VMG * Q * 9 <= W * LDA, "adjoint partials must fit in act");
 };
 
 // shared-memory carve-up (doubles); L is a runtime value.  The post-NCM
@@ -384,10 +390,15 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
   };
 #endif
 
+  // adjoint-pass g/H_1 partial (row group r, qp q, entry x): with ping-pong in the block
+  // [2Q, 3Q) of act, free during the value and adjoint passes; otherwise packed at the start
+  auto part_at = [&](int r, int q, int x) { return C::PP ? (r * 9 + x) * LDA + 2 * Q + q : (r * Q + q) * 9 + x; };
+
   for (int64_t batch = blockIdx.x; batch < n_batches; batch += gridDim.x) {
     const int64_t e0 = A.el_begin + batch * E;
     const int64_t rem = A.el_begin + A.el_count - e0;
     const int ne = rem < E ? (int)rem : E;
+    int cur = 0;  // act column block holding the current layer's input (value / adjoint passes)
 
     // ---- stage 0: stage element inputs --------------------------------------------
     if constexpr (C::MODE == 1) {  // material points: F rows (tail points get F = I)
@@ -538,9 +549,16 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
 #pragma unroll
       for (int jj = 0; jj < C::NT_V; jj++) nacc[jj][0] = nacc[jj][1] = 0.0;
       for (int l = 2; l <= L; l++) {
+        // ping-pong between act column blocks [0, Q) and [Q, 2Q): layer l reads block cur and
+        // writes block cur ^ 1, so one barrier per layer suffices (the write of a fast warp
+        // cannot hit the block a slow warp is still reading)
         double acc[C::MT_V][C::NT_V][2];
-        warp_gemm<C::MT_V, C::NT_V, KT2, C::PD_V>(m.Wfrag + (l - 2) * frag_layer, mt0, act, LDA, ncol, acc);
-        __syncthreads();
+        int ncr[C::NT_V];
+#pragma unroll
+        for (int j = 0; j < C::NT_V; j++) ncr[j] = ncol[j] + cur * Q;
+        warp_gemm<C::MT_V, C::NT_V, KT2, C::PD_V>(m.Wfrag + (l - 2) * frag_layer, mt0, act, LDA, ncr, acc);
+        if constexpr (!C::PP) __syncthreads();
+        const int wof = C::PP ? (cur ^ 1) * Q : 0;  // write block
         frag_prefetch<C::MT_V, KT2, COMMET_FRAG_PF + (COMMET_FRAG_PF == 0)>(
             m.Wfrag + (l < L ? (l - 1) * frag_layer : (L - 2) * frag_layer + (size_t)W * W), mt0);
 #pragma unroll
@@ -564,7 +582,7 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
                 if (l == L) {
                   double z, s;
                   softplus_sig(y, stab, z, s);
-                  act[j * LDA + q] = aj * s;
+                  act[j * LDA + wof + q] = aj * s;
                   cb[((l - 2) * W + j) * LDS + q] = aj * s * (1.0 - s);
                   nacc[jj][h] += aj * z;
                   continue;
@@ -575,26 +593,27 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
                 double z, s;
                 softplus_sig(y, stab, z, s);
                 sb[((l - 1) * W + j) * LDS + q] = s;
-                act[j * LDA + q] = z;
+                act[j * LDA + wof + q] = z;
               } else {  // z_L is not needed (only dN/dz_L = a): no log
                 const double s = sigmoid_tab(y, stab);
-                act[j * LDA + q] = aj * s;                                  // mu_L
-                cb[((l - 2) * W + j) * LDS + q] = aj * s * (1.0 - s);       // c_L
+                act[j * LDA + wof + q] = aj * s;                             // mu_L
+                cb[((l - 2) * W + j) * LDS + q] = aj * s * (1.0 - s);        // c_L
               }
 #else
               double z, s;
               softplus_sig(y, stab, z, s);
               if (l < L) {
                 sb[((l - 1) * W + j) * LDS + q] = s;
-                act[j * LDA + q] = z;
+                act[j * LDA + wof + q] = z;
               } else {
-                act[j * LDA + q] = aj * s;                                  // mu_L
-                cb[((l - 2) * W + j) * LDS + q] = aj * s * (1.0 - s);       // c_L
+                act[j * LDA + wof + q] = aj * s;                             // mu_L
+                cb[((l - 2) * W + j) * LDS + q] = aj * s * (1.0 - s);        // c_L
               }
 #endif
             }
         }
         __syncthreads();
+        if constexpr (C::PP) cur ^= 1;
       }
       if constexpr (C::MODE == 1) {
         if (L > 1) {  // reduce the 8 row groups g of the warp, one partial per (vm, q)
@@ -625,15 +644,19 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
           const double* Bl = m.skip_h + (size_t)(l - 2) * W * 3;
           double s0 = 0, s1 = 0, s2 = 0;
           for (int j = 0; j < W; j++) {
-            const double mu = act[j * LDA + tid];
+            const double mu = act[j * LDA + cur * Q + tid];
             s0 += __ldg(Bl + j * 3) * mu; s1 += __ldg(Bl + j * 3 + 1) * mu; s2 += __ldg(Bl + j * 3 + 2) * mu;
           }
           gsk[tid * 3] += s0; gsk[tid * 3 + 1] += s1; gsk[tid * 3 + 2] += s2;
         }
         double acc[C::MT_V][C::NT_V][2];
-        warp_gemm<C::MT_V, C::NT_V, KT2, C::PD_V>(m.Wfrag + (l - 2) * frag_layer + (size_t)W * W, mt0, act, LDA, ncol,
-                                                 acc);
-        __syncthreads();
+        int ncr[C::NT_V];
+#pragma unroll
+        for (int j = 0; j < C::NT_V; j++) ncr[j] = ncol[j] + cur * Q;
+        warp_gemm<C::MT_V, C::NT_V, KT2, C::PD_V>(m.Wfrag + (l - 2) * frag_layer + (size_t)W * W, mt0, act, LDA,
+                                                 ncr, acc);
+        if constexpr (!C::PP) __syncthreads();
+        const int wof = C::PP ? (cur ^ 1) * Q : 0;  // write block
         if (l > 2)
           frag_prefetch<C::MT_V, KT2, COMMET_FRAG_PF + (COMMET_FRAG_PF == 0)>(
               m.Wfrag + (l - 3) * frag_layer + (size_t)W * W, mt0);
@@ -651,7 +674,7 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
                 const double lam = acc[i][jj][h];
                 const double s = sb[((l - 2) * W + j) * LDS + q];
                 cb[((l - 3) * W + j) * LDS + q] = lam * s * (1.0 - s);  // c_{l-1}
-                act[j * LDA + q] = lam * s;                              // mu_{l-1}
+                act[j * LDA + wof + q] = lam * s;                        // mu_{l-1}
               }
           }
         } else {
@@ -701,10 +724,11 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
 #pragma unroll
               for (int h = 0; h < 2; h++)
 #pragma unroll
-                for (int x = 0; x < 9; x++) act[(vm * Q + ncol[jj] + 2 * t + h) * 9 + x] = pg[jj][h][x];
+                for (int x = 0; x < 9; x++) act[part_at(vm, ncol[jj] + 2 * t + h, x)] = pg[jj][h][x];
           }
         }
         __syncthreads();
+        if constexpr (C::PP) cur ^= 1;
       }
     }
 
@@ -719,7 +743,7 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
 #pragma unroll
         for (int r = 0; r < C::VMG; r++)
 #pragma unroll
-          for (int x = 0; x < 9; x++) v[x] += act[(r * Q + q) * 9 + x];
+          for (int x = 0; x < 9; x++) v[x] += act[part_at(r, q, x)];
 #pragma unroll
         for (int x = 0; x < 3; x++) qg[q * 3 + x] = v[x] + gsk[q * 3 + x] + __ldg(m.skip_out + x);
 #pragma unroll
