@@ -386,6 +386,34 @@ class Commet:
                     cg_iters=list(rep.cg_iters[:n]), cg_iters_total=rep.cg_iters_total, max_trC=rep.max_trC,
                     ms_assemble=rep.ms_assemble, ms_solve=rep.ms_solve)
 
+    def newton_solve(self, u, bc_values_at, n_steps=10, max_halvings=4, **kw):
+        """Load stepping around newton_step (host loop, no compute): t = k / n_steps,
+        u[dirichlet] = bc_values_at(t).  A step that fails (det F <= 0, CG or Newton
+        non-convergence) is retried from the last converged u with half the increment,
+        up to max_halvings times (SPEC's step-halving).  -> list of per-step reports."""
+        t_done, dt, reports = 0.0, 1.0 / n_steps, []
+        u_ok = u.clone()
+        while t_done < 1.0 - 1e-12:
+            t = min(1.0, t_done + dt)
+            try:
+                rep = self.newton_step(u, bc_values_at(t), **kw)
+                ok = rep["converged"]
+            except CommetError as e:
+                if e.status != COMMET_ERR_DOMAIN:
+                    raise
+                rep, ok = dict(error=str(e)), False
+            rep["t"] = t
+            reports.append(rep)
+            if ok:
+                t_done = t
+                u_ok.copy_(u)
+                continue
+            u.copy_(u_ok)
+            dt *= 0.5
+            if dt < 1.0 / n_steps / 2 ** max_halvings:
+                raise CommetError(COMMET_ERR_DOMAIN, f"load step at t = {t:.6g} failed after {max_halvings} halvings")
+        return reports
+
     def check(self) -> int:
         """-1 if every det F > 0, else the lowest flat e*n_q+q with det F <= 0."""
         bad = _i64()

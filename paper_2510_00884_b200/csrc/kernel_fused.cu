@@ -1161,7 +1161,10 @@ void fused_gfrag_fill(int w, const double* W1, double* out) {
 template <class C>
 static int launch_cfg(const AsmArgs& a, cudaStream_t st, int* launches) {
   const Smem<C> sm(a.ncm.L);
-  const size_t bytes = (size_t)sm.total * sizeof(double);
+  size_t bytes = (size_t)sm.total * sizeof(double);
+#ifdef COMMET_EXP_SMEM_PAD
+  bytes += COMMET_EXP_SMEM_PAD;  // experiments only: limit resident CTAs per SM
+#endif
   // per device: the shared-memory attribute, SM count and occupancy are queried once per
   // (device, smem size) -- the host-side launch cost matters for small batches
   constexpr int kDev = 16;

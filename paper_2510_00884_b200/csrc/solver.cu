@@ -5,17 +5,20 @@
 // symmetrically (rows and columns zeroed, unit diagonal, zero residual), all on
 // the GPU.  Single GPU (n_ranks <= 1).
 //
-// CG kernels (HBM-bound):
-//  * spmv_dot: q = K p and the block partials of p.q.  One warp per node row
+// CG kernels (HBM-bound), three launches per iteration k:
+//  * update_p (k): from the partials of the previous update, rz_k = r.z and r.r
+//    (every block reduces the same partials in the same order: deterministic),
+//    the convergence test, beta = rz_k / rz_{k-1}, p = z + beta p.
+//  * spmv_dot (k): q = K p and the partials of p.q.  One warp per node-row
 //    triple: rows 3a, 3a+1, 3a+2 share their column list (every node pair is a
 //    full 3x3 block), so col_idx and the gathered p are read once for three
-//    rows: 8 + 4/3 bytes of matrix per nonzero.
-//  * update_xr: alpha = rz / pq (every block reduces the same partials in the
-//    same order: deterministic), x += alpha p, r -= alpha q, z = D^-1 r,
+//    rows: 8 + 4/3 bytes of matrix per nonzero.  (Forming p = z + beta p at the
+//    gathered columns instead, to drop update_p, measured slower: two gathered
+//    vectors per nonzero through L2.)
+//  * update_xr (k): alpha = rz_k / p.q, x += alpha p, r -= alpha q, z = D^-1 r,
 //    partials of r.z and r.r.
-//  * update_p: beta = rz' / rz, p = z + beta p; block 0 records rr and raises
-//    the converged flag; every kernel returns at once when the flag is set, so
-//    the host only synchronises every kCheck iterations.
+//  Block 0 of update_p raises the converged flag; every kernel returns at once
+//  when it is set, so the host only synchronises every kCheck iterations.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -167,23 +170,61 @@ __global__ void cg_init_scal_kernel(const double* part, int nb, double rtol, CgS
   }
 }
 
-// q = K p for node-row triples; partials of p.q
+// iteration k, first: rz_k = r.z and r.r from the previous update's partials, the convergence test,
+// beta = rz_k / rz_{k-1}, p_k = z + beta p_{k-1} in place (k = 0: p = z)
+__global__ void cg_update_p_kernel(double* __restrict__ p, const double* __restrict__ z, int64_t n,
+                                   const double* part2, int nb, CgScal* s, int k, int max_iter) {
+  if (s->done) return;
+  double t[2];
+  sum_partials<2>(part2, nb, t);  // (r.z, r.r) of the current residual (k = 0: (r.z, b.b) from init)
+  if (t[1] <= s->tol2 || k >= max_iter) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      s->rr = t[1];
+      s->it = k;
+      s->done = k > 0 ? k : -1;
+    }
+    return;
+  }
+  const double beta = k == 0 ? 0.0 : t[0] / s->rz[(k - 1) & 1];
+  if (blockIdx.x == 0 && threadIdx.x == 0) s->rz[k & 1] = t[0];  // the other slot from the one read above
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = fma(beta, p[i], z[i]);
+}
+
+// q = K p, partials of p.q.  A contiguous node range per block (neighbouring nodes share most of
+// their stencil columns: the p gathers hit L1); the matrix streams with evict-first loads, all
+// lane loads of a row triple issued before the FMAs
 __global__ void cg_spmv_dot_kernel(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col_idx,
                                    const double* __restrict__ vals, const double* __restrict__ p,
                                    double* __restrict__ q, int64_t n_nodes, double* part, const CgScal* s) {
   if (s->done) return;
-  const int lane = threadIdx.x & 31;
-  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwb = blockDim.x >> 5;
+  const int64_t chunk = (n_nodes + gridDim.x - 1) / gridDim.x;
+  const int64_t a_end = min(n_nodes, (int64_t)(blockIdx.x + 1) * chunk);
   double v[1] = {0.0};
-  for (int64_t a = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; a < n_nodes; a += nw) {
+  for (int64_t a = (int64_t)blockIdx.x * chunk + wid; a < a_end; a += nwb) {
     const int64_t r0 = row_ptr[3 * a], r1 = row_ptr[3 * a + 1], r2 = row_ptr[3 * a + 2];
     const int64_t len = r1 - r0;
     double s0 = 0.0, s1 = 0.0, s2 = 0.0;
-    for (int64_t j = lane; j < len; j += 32) {
-      const double pv = __ldg(p + __ldg(col_idx + r0 + j));
-      s0 = fma(__ldg(vals + r0 + j), pv, s0);
-      s1 = fma(__ldg(vals + r1 + j), pv, s1);
-      s2 = fma(__ldg(vals + r2 + j), pv, s2);
+    for (int64_t j0 = 0; j0 < len; j0 += 96) {  // up to three lane passes with their loads in flight
+      int32_t c[3];
+      double v0[3], v1[3], v2[3];
+#pragma unroll
+      for (int u = 0; u < 3; u++) {
+        const int64_t j = j0 + u * 32 + lane;
+        const bool in = j < len;
+        c[u] = in ? __ldcs(col_idx + r0 + j) : 0;
+        v0[u] = in ? __ldcs(vals + r0 + j) : 0.0;
+        v1[u] = in ? __ldcs(vals + r1 + j) : 0.0;
+        v2[u] = in ? __ldcs(vals + r2 + j) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 3; u++) {
+        const double pv = __ldg(p + c[u]);
+        s0 = fma(v0[u], pv, s0);
+        s1 = fma(v1[u], pv, s1);
+        s2 = fma(v2[u], pv, s2);
+      }
     }
     s0 = warp_sum(s0);
     s1 = warp_sum(s1);
@@ -217,24 +258,6 @@ __global__ void cg_update_xr_kernel(double* __restrict__ x, double* __restrict__
     v[1] += ri * ri;
   }
   block_partials<2>(v, part);
-}
-
-__global__ void cg_update_p_kernel(double* __restrict__ p, const double* __restrict__ z, int64_t n,
-                                   const double* part, int nb, CgScal* s, int it, int max_iter) {
-  if (s->done) return;
-  double t[2];
-  sum_partials<2>(part, nb, t);
-  const double beta = t[0] / s->rz[it & 1];
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    p[i] = fma(beta, p[i], z[i]);
-  // block 0 publishes the next iteration's scalars for the NEXT launch: rz goes to the other
-  // ping-pong slot (this launch's blocks read rz[it & 1]); the iteration index is a launch argument
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    s->rz[(it + 1) & 1] = t[0];
-    s->rr = t[1];
-    s->it = it + 1;
-    if (t[1] <= s->tol2 || it + 1 >= max_iter) s->done = it + 1;
-  }
 }
 
 // increment of the constrained dofs: d = 0, d[dofs] = v - u[dofs]
@@ -406,24 +429,25 @@ static commet_status cg(commet_ctx c, SolverWork* w, const double* vals, const d
   CUDA_TRY(c, cudaStreamSynchronize(st));
   if (bad != ~0ULL) return fail(c, COMMET_ERR_DOMAIN, "CG-Jacobi: diagonal entry of row %llu is not positive", bad);
   CgScal hs{};
-  for (int it0 = 0; it0 < max_iter; it0 += kCheck) {
-    const int nk = std::min(kCheck, max_iter - it0);
-    for (int k = 0; k < nk; k++) {
+  for (int it0 = 0; it0 <= max_iter; it0 += kCheck) {
+    const int nk = std::min(kCheck, max_iter + 1 - it0);
+    for (int kk = 0; kk < nk; kk++) {
+      const int k = it0 + kk;
+      cg_update_p_kernel<<<nb, kThreads, 0, st>>>(w->p.p, w->z.p, n, w->part2.p, nb, w->scal.p, k, max_iter);
       cg_spmv_dot_kernel<<<nb, kThreads, 0, st>>>(c->row_ptr.p, c->col_idx.p, vals, w->p.p, w->q.p, n_nodes,
                                                   w->part.p, w->scal.p);
       cg_update_xr_kernel<<<nb, kThreads, 0, st>>>(x, w->cr.p, w->z.p, w->p.p, w->q.p, w->dinv.p, n, w->part.p, nb,
-                                                   w->part2.p, w->scal.p, it0 + k);
-      cg_update_p_kernel<<<nb, kThreads, 0, st>>>(w->p.p, w->z.p, n, w->part2.p, nb, w->scal.p, it0 + k, max_iter);
+                                                   w->part2.p, w->scal.p, k);
     }
     CUDA_TRY(c, cudaGetLastError());
     CUDA_TRY(c, cudaMemcpyAsync(&hs, w->scal.p, sizeof hs, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(c, cudaStreamSynchronize(st));
     if (hs.done) break;
   }
-  if (iters) *iters = hs.done < 0 ? 0 : hs.it;
-  const double rr = hs.done < 0 ? 0.0 : hs.rr;
+  if (iters) *iters = hs.it;
+  const double rr = hs.rr;
   if (rel_res) *rel_res = hs.bb > 0.0 ? std::sqrt(rr / hs.bb) : 0.0;
-  if (!(rr <= hs.tol2) && hs.done >= 0)
+  if (!(rr <= hs.tol2))
     return fail(c, COMMET_ERR_DOMAIN, "CG-Jacobi did not reach rtol %.3g in %d iterations (rel. residual %.3g)", rtol,
                 max_iter, hs.bb > 0 ? std::sqrt(rr / hs.bb) : 0.0);
   return COMMET_OK;

@@ -142,3 +142,23 @@ def test_newton_twist_matches_oracle(pc):
         d = np.abs(ug.cpu().numpy() - uo).max() / np.abs(uo).max()
         assert d <= 1e-9, (s, d)
     assert abs(rep["max_trC"] - on.max_trace_C(mesh, uo)) <= 1e-8 * rep["max_trC"]
+
+
+def test_newton_solve_step_halving(pc):
+    """Two load steps for the whole twist: the first fails (inverted elements) and is
+    halved; the converged end state equals the oracle's 10-step solution."""
+    n = 4
+    mesh, ncm, lib, dofs, _ = _twist_setup(pc, n)
+    rp, ci = oracle.pattern(mesh["n_nodes"], mesh["conn"])
+    uo = np.zeros(3 * mesh["n_nodes"])
+    for s in range(1, 11):
+        uo, norms, ok = on.newton_step(ncm, mesh, rp, ci, uo, dofs, twist.twist_values(mesh["X"], dofs, s / 10),
+                                       atol=1e-11, rtol=1e-12)
+        assert ok
+    ug = torch.zeros(3 * mesh["n_nodes"], dtype=torch.float64, device="cuda")
+    reps = lib.newton_solve(ug, lambda t: twist.twist_values(mesh["X"], dofs, t), n_steps=1, max_halvings=6,
+                            atol=1e-11, rtol=1e-12, cg_rtol=1e-13)
+    assert abs(reps[-1]["t"] - 1.0) < 1e-12 and reps[-1]["converged"]
+    assert any("error" in r or not r["converged"] for r in reps)  # at least one halving happened
+    d = np.abs(ug.cpu().numpy() - uo).max() / np.abs(uo).max()
+    assert d <= 1e-8, d
