@@ -119,10 +119,22 @@ typedef struct {
   const double* cann_w2;       /* CANN host [3][cann_n]: N = sum_m sum_b w2 f2(f1(f0(k_m)); w1)  (Eq. cann-def) */
   double gt[3];                /* Gent-Thomas (App. C): N = gt0 k1 + gt1 ln(1 + k2/3) + gt2 k3^2
                                   (the paper's model: gt = (0.5, 1, 1), isochoric kinematics, kappa = 0) */
+  /* ICKAN (App. B.3): R layers of widths n_0 = 3, n_1, ..., n_R = 1; edge (r, i, j)
+   * (output i of layer r+1, input j of layer r) carries s(x) = w psi(x), psi a B-spline of order kan_k
+   * with kan_nb control points on the uniform knots of layer r's interval [xmin, xmax] (kan_k extra
+   * knots on each side); outside the interval psi continues linearly with its end slope (SPEC's reading);
+   * z^(r+1)_i = sum_j s_rij(z^(r)_j), N = z^(R)_0.  The CUDA path supports kan_k = 3 (cubic). */
+  int32_t kan_layers;          /* R, 1..4 */
+  const int32_t* kan_width;    /* host [R+1]: n_0 = 3, ..., n_R = 1, each <= 16 */
+  int32_t kan_nb;              /* control points per edge, kan_k+1 .. 32 */
+  int32_t kan_k;               /* spline order (3) */
+  const double* kan_grid;      /* host [R][2]: xmin, xmax of layer r's inputs */
+  const double* kan_w;         /* host [edges]: spline weights, edges in (r, i, j) order */
+  const double* kan_c;         /* host [edges][kan_nb]: control points */
 } commet_ncm_desc;
 
 enum { COMMET_KIN_STANDARD = 0, COMMET_KIN_ISOCHORIC = 1 };
-enum { COMMET_NET_ICNN = 0, COMMET_NET_CANN = 1, COMMET_NET_GENT_THOMAS = 2 };
+enum { COMMET_NET_ICNN = 0, COMMET_NET_CANN = 1, COMMET_NET_GENT_THOMAS = 2, COMMET_NET_ICKAN = 3 };
 
 /* Kernel variants (commet_set_kernel).  FUSED is the product path; SIMPLE is
  * a one-thread-per-element CUDA kernel kept as an independent GPU cross-check. */

@@ -34,10 +34,12 @@ class _Ncm(C.Structure):
                 ("kappa", C.c_double), ("ref_shift", C.c_double),
                 ("kinematics", C.c_int32), ("network", C.c_int32), ("cann_n", C.c_int32),
                 ("cann_f", C.c_void_p), ("cann_w1", C.c_void_p), ("cann_w2", C.c_void_p),
-                ("gt", C.c_double * 3)]
+                ("gt", C.c_double * 3), ("kan_layers", C.c_int32), ("kan_width", C.c_void_p),
+                ("kan_nb", C.c_int32), ("kan_k", C.c_int32), ("kan_grid", C.c_void_p), ("kan_w", C.c_void_p),
+                ("kan_c", C.c_void_p)]
 
 KIN = {"standard": 0, "isochoric": 1}
-NET = {"icnn": 0, "cann": 1, "gent_thomas": 2}
+NET = {"icnn": 0, "cann": 1, "gent_thomas": 2, "ickan": 3}
 
 
 _lib = None
@@ -82,12 +84,18 @@ class Ncm:
         for k in ("cann_w1", "cann_w2"):
             self.arrays[k] = f(ncm.get(k))
         gt = (C.c_double * 3)(*(ncm.get("gt") if ncm.get("gt") is not None else (0.0, 0.0, 0.0)))
+        self.kan_width = None if ncm.get("kan_width") is None else np.ascontiguousarray(ncm["kan_width"], np.int32)
+        for k in ("kan_grid", "kan_w", "kan_c"):
+            self.arrays[k] = f(ncm.get(k))
         self.s = _Ncm(int(ncm.get("n_hidden", 1)), int(ncm.get("width", 8)),
                       *[_p(self.arrays[k]) for k in ("W1", "W", "b", "a", "skip_out", "skip_hidden")],
                       float(ncm.get("kappa", 0.0)), float(ncm.get("ref_shift", 0.0)),
                       KIN[kin] if isinstance(kin, str) else int(kin), NET[net] if isinstance(net, str) else int(net),
                       0 if self.cann_f is None else self.cann_f.shape[1], _p(self.cann_f),
-                      _p(self.arrays["cann_w1"]), _p(self.arrays["cann_w2"]), gt)
+                      _p(self.arrays["cann_w1"]), _p(self.arrays["cann_w2"]), gt,
+                      0 if self.kan_width is None else self.kan_width.size - 1, _p(self.kan_width),
+                      int(ncm.get("kan_nb", 0)), int(ncm.get("kan_k", 3)), _p(self.arrays["kan_grid"]),
+                      _p(self.arrays["kan_w"]), _p(self.arrays["kan_c"]))
 
     @property
     def ptr(self):

@@ -46,6 +46,12 @@ typedef struct {
   const double* cann_w1;     /* CANN [3][n] */
   const double* cann_w2;     /* CANN [3][n] */
   double gt[3];              /* Gent-Thomas: N = gt0 K1 + gt1 ln(1 + K2/3) + gt2 K3^2 */
+  int32_t kan_layers;        /* ICKAN (App. B.3): R layers */
+  const int32_t* kan_width;  /* [R+1], n_0 = 3, n_R = 1 */
+  int32_t kan_nb, kan_k;     /* control points per edge, spline order */
+  const double* kan_grid;    /* [R][2] xmin, xmax */
+  const double* kan_w;       /* [edges] */
+  const double* kan_c;       /* [edges][nb] */
 } oracle_ncm;
 
 /* ---------------------------------------------------------------------- */
@@ -194,10 +200,119 @@ static int gt_eval(const oracle_ncm* m, const double K[3], double* N_out, double
   return 0;
 }
 
+/*
+ * ICKAN (App. B.3).  B-spline psi(x) = sum_i c_i B_{i,k}(x) on the uniform knots
+ * t_i = xmin + (i - k) h, h = (xmax - xmin) / (nb - k), i = 0..nb+k, by De Boor's recursion
+ * (B_{i,0} = 1 on the knot span holding x, B_{i,k} = (x - t_i)/(t_{i+k} - t_i) B_{i,k-1}
+ * + (t_{i+k+1} - x)/(t_{i+k+1} - t_{i+1}) B_{i+1,k-1}) and the textbook derivative
+ * B'_{i,k} = k/(t_{i+k} - t_i) B_{i,k-1} - k/(t_{i+k+1} - t_{i+1}) B_{i+1,k-1}, applied twice for
+ * psi''.  Outside [xmin, xmax]: linear continuation with the end slope (SPEC's reading).
+ */
+static void bspline_basis(const double* t, int nb, int k, int span, double x, double* B /* [k+1][nb+k] */) {
+  const int nt = nb + k + 1;
+  for (int p = 0; p <= k; p++)
+    for (int i = 0; i < nt; i++) B[p * nt + i] = 0.0;
+  B[span] = 1.0;
+  for (int p = 1; p <= k; p++)
+    for (int i = 0; i + p + 1 < nt; i++) {
+      double v = 0.0;
+      if (t[i + p] > t[i]) v += (x - t[i]) / (t[i + p] - t[i]) * B[(p - 1) * nt + i];
+      if (t[i + p + 1] > t[i + 1]) v += (t[i + p + 1] - x) / (t[i + p + 1] - t[i + 1]) * B[(p - 1) * nt + i + 1];
+      B[p * nt + i] = v;
+    }
+}
+static void spline_eval(const double* c, int nb, int k, double xmin, double xmax, double x, double* v, double* d1,
+                        double* d2) {
+  double t[64], B[4 * 64];
+  const int nt = nb + k + 1;
+  const double h = (xmax - xmin) / (nb - k);
+  for (int i = 0; i < nt; i++) t[i] = xmin + (i - k) * h;
+  const double xe = x < xmin ? xmin : (x > xmax ? xmax : x);
+  int span = k;
+  while (span < nb - 1 && xe >= t[span + 1]) span++;
+  bspline_basis(t, nb, k, span, xe, B);
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+  for (int i = 0; i < nb; i++) {
+    s0 += c[i] * B[k * nt + i];
+    /* B'_{i,k} */
+    double b1 = 0.0;
+    if (t[i + k] > t[i]) b1 += k / (t[i + k] - t[i]) * B[(k - 1) * nt + i];
+    if (t[i + k + 1] > t[i + 1]) b1 -= k / (t[i + k + 1] - t[i + 1]) * B[(k - 1) * nt + i + 1];
+    s1 += c[i] * b1;
+    /* B''_{i,k} = k/(t_{i+k}-t_i) B'_{i,k-1} - k/(t_{i+k+1}-t_{i+1}) B'_{i+1,k-1} */
+    double b2 = 0.0;
+    for (int side = 0; side < 2; side++) {
+      const int ii = i + side;
+      const double den = side ? t[i + k + 1] - t[i + 1] : t[i + k] - t[i];
+      if (!(den > 0)) continue;
+      double bp = 0.0; /* B'_{ii,k-1} */
+      if (t[ii + k - 1] > t[ii]) bp += (k - 1) / (t[ii + k - 1] - t[ii]) * B[(k - 2) * nt + ii];
+      if (t[ii + k] > t[ii + 1]) bp -= (k - 1) / (t[ii + k] - t[ii + 1]) * B[(k - 2) * nt + ii + 1];
+      b2 += (side ? -1.0 : 1.0) * k / den * bp;
+    }
+    s2 += c[i] * b2;
+  }
+  if (x != xe) { /* linear continuation */
+    *v = s0 + s1 * (x - xe);
+    *d1 = s1;
+    *d2 = 0.0;
+  } else {
+    *v = s0;
+    *d1 = s1;
+    *d2 = s2;
+  }
+}
+/* forward mode through the layers: z, dz/dK (3), d2z/dK2 (3x3) per node, as Alg. 4 does for the ICNN */
+static int ickan_eval(const oracle_ncm* m, const double K[3], double* N_out, double g[3], double H[9]) {
+  const int R = m->kan_layers, nb = m->kan_nb, k = m->kan_k;
+  double z[32], dz[32][3], d2z[32][9], y[32], dy[32][3], d2y[32][9];
+  int nin = m->kan_width[0];
+  for (int j = 0; j < nin; j++) {
+    z[j] = K[j];
+    for (int p = 0; p < 3; p++) dz[j][p] = (p == j);
+    for (int pq = 0; pq < 9; pq++) d2z[j][pq] = 0.0;
+  }
+  size_t e = 0;
+  for (int r = 0; r < R; r++) {
+    const int nout = m->kan_width[r + 1];
+    const double xmin = m->kan_grid[2 * r], xmax = m->kan_grid[2 * r + 1];
+    for (int i = 0; i < nout; i++) {
+      y[i] = 0.0;
+      for (int p = 0; p < 3; p++) dy[i][p] = 0.0;
+      for (int pq = 0; pq < 9; pq++) d2y[i][pq] = 0.0;
+      for (int j = 0; j < nin; j++, e++) {
+        double v, d1, d2;
+        spline_eval(m->kan_c + e * nb, nb, k, xmin, xmax, z[j], &v, &d1, &d2);
+        const double w = m->kan_w[e];
+        y[i] += w * v;
+        for (int p = 0; p < 3; p++) dy[i][p] += w * d1 * dz[j][p];
+        for (int p = 0; p < 3; p++)
+          for (int q = 0; q < 3; q++) d2y[i][p * 3 + q] += w * (d2 * dz[j][p] * dz[j][q] + d1 * d2z[j][p * 3 + q]);
+      }
+    }
+    for (int i = 0; i < nout; i++) {
+      z[i] = y[i];
+      for (int p = 0; p < 3; p++) dz[i][p] = dy[i][p];
+      for (int pq = 0; pq < 9; pq++) d2z[i][pq] = d2y[i][pq];
+    }
+    nin = nout;
+  }
+  *N_out = z[0];
+  for (int p = 0; p < 3; p++) g[p] = dz[0][p];
+  for (int pq = 0; pq < 9; pq++) H[pq] = d2z[0][pq];
+  if (m->skip_out)
+    for (int p = 0; p < 3; p++) {
+      *N_out += m->skip_out[p] * K[p];
+      g[p] += m->skip_out[p];
+    }
+  return 0;
+}
+
 int oracle_ncm_eval(const oracle_ncm* m, const double K[3], double* N_out, double g_out[3],
                     double H_out[9]) {
   if (m->network == 1) return cann_eval(m, K, N_out, g_out, H_out);
   if (m->network == 2) return gt_eval(m, K, N_out, g_out, H_out);
+  if (m->network == 3) return ickan_eval(m, K, N_out, g_out, H_out);
   return icnn_eval(m, K, N_out, g_out, H_out);
 }
 

@@ -54,23 +54,27 @@ class NcmDesc(C.Structure):
                 ("skip_hidden", C.c_void_p), ("kappa", C.c_double), ("ref_shift", C.c_double),
                 ("kinematics", C.c_int32), ("network", C.c_int32), ("cann_n", C.c_int32),
                 ("cann_f", C.c_void_p), ("cann_w1", C.c_void_p), ("cann_w2", C.c_void_p),
-                ("gt", C.c_double * 3)]
+                ("gt", C.c_double * 3), ("kan_layers", C.c_int32), ("kan_width", C.c_void_p),
+                ("kan_nb", C.c_int32), ("kan_k", C.c_int32), ("kan_grid", C.c_void_p), ("kan_w", C.c_void_p),
+                ("kan_c", C.c_void_p)]
 
 
 KIN_STANDARD, KIN_ISOCHORIC = 0, 1
-NET_ICNN, NET_CANN, NET_GENT_THOMAS = 0, 1, 2
+NET_ICNN, NET_CANN, NET_GENT_THOMAS, NET_ICKAN = 0, 1, 2, 3
 _KIN = {"standard": KIN_STANDARD, "isochoric": KIN_ISOCHORIC}
-_NET = {"icnn": NET_ICNN, "cann": NET_CANN, "gent_thomas": NET_GENT_THOMAS}
+_NET = {"icnn": NET_ICNN, "cann": NET_CANN, "gent_thomas": NET_GENT_THOMAS, "ickan": NET_ICKAN}
 
 
 def ncm_desc(ncm: dict):
     """-> (NcmDesc, keepalive).  ncm keys: width, n_hidden, W1, W, b, a, optional skip_out,
     skip_hidden, kappa, ref_shift, kinematics ("standard" | "isochoric"), network ("icnn" |
     "cann" | "gent_thomas"), cann_f [3, n, 3] int, cann_w1 / cann_w2 [3, n], gt [3]."""
-    arrs = {k: _f64(ncm.get(k)) for k in ("W1", "W", "b", "a", "skip_out", "skip_hidden", "cann_w1", "cann_w2")}
+    arrs = {k: _f64(ncm.get(k)) for k in ("W1", "W", "b", "a", "skip_out", "skip_hidden", "cann_w1", "cann_w2",
+                                          "kan_grid", "kan_w", "kan_c")}
     if arrs["W"] is not None and arrs["W"].size == 0:
         arrs["W"] = None
     cf = None if ncm.get("cann_f") is None else np.ascontiguousarray(ncm["cann_f"], dtype=np.int32)
+    kw = None if ncm.get("kan_width") is None else np.ascontiguousarray(ncm["kan_width"], dtype=np.int32)
     kin, net = ncm.get("kinematics", "standard"), ncm.get("network", "icnn")
     gt = ncm.get("gt")
     nd = NcmDesc(int(ncm.get("n_hidden", 1)), int(ncm.get("width", 16)),
@@ -78,8 +82,10 @@ def ncm_desc(ncm: dict):
                  float(ncm.get("kappa", 0.0)), float(ncm.get("ref_shift", 0.0)),
                  _KIN[kin] if isinstance(kin, str) else int(kin), _NET[net] if isinstance(net, str) else int(net),
                  0 if cf is None else cf.shape[1], _ptr(cf), _ptr(arrs["cann_w1"]), _ptr(arrs["cann_w2"]),
-                 (C.c_double * 3)(*(gt if gt is not None else (0.0, 0.0, 0.0))))
-    return nd, [arrs, cf]
+                 (C.c_double * 3)(*(gt if gt is not None else (0.0, 0.0, 0.0))),
+                 0 if kw is None else kw.size - 1, _ptr(kw), int(ncm.get("kan_nb", 0)), int(ncm.get("kan_k", 3)),
+                 _ptr(arrs["kan_grid"]), _ptr(arrs["kan_w"]), _ptr(arrs["kan_c"]))
+    return nd, [arrs, cf, kw]
 
 
 class NewtonCfg(C.Structure):

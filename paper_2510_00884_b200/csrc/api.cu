@@ -39,7 +39,7 @@ extern "C" commet_status commet_setup(const commet_mesh_desc* mesh, const commet
   const int net = ncm->network, kin = ncm->kinematics;
   if (kin != COMMET_KIN_STANDARD && kin != COMMET_KIN_ISOCHORIC)
     return fail(C, COMMET_ERR_ARG, "kinematics %d unknown", kin);
-  if (net != COMMET_NET_ICNN && net != COMMET_NET_CANN && net != COMMET_NET_GENT_THOMAS)
+  if (net != COMMET_NET_ICNN && net != COMMET_NET_CANN && net != COMMET_NET_GENT_THOMAS && net != COMMET_NET_ICKAN)
     return fail(C, COMMET_ERR_ARG, "network %d unknown", net);
   // analytic networks use no hidden layers (the ICNN fields are ignored)
   const int L = net == COMMET_NET_ICNN ? ncm->n_hidden : 1, w = net == COMMET_NET_ICNN ? ncm->width : 16;
@@ -50,6 +50,25 @@ extern "C" commet_status commet_setup(const commet_mesh_desc* mesh, const commet
       return fail(C, COMMET_ERR_ARG, "width %d unsupported (8, 16, 32, 64 or 128)", w);
     if (!ncm->W1 || !ncm->b || !ncm->a || (L > 1 && !ncm->W))
       return fail(C, COMMET_ERR_ARG, "NCM weight pointer NULL (W1, b, a or W)");
+  }
+  int64_t kan_edges = 0;
+  if (net == COMMET_NET_ICKAN) {
+    const int R = ncm->kan_layers;
+    if (R < 1 || R > 4) return fail(C, COMMET_ERR_ARG, "kan_layers %d not in 1..4", R);
+    if (!ncm->kan_width || !ncm->kan_grid || !ncm->kan_w || !ncm->kan_c)
+      return fail(C, COMMET_ERR_ARG, "ICKAN pointer NULL (kan_width, kan_grid, kan_w or kan_c)");
+    if (ncm->kan_width[0] != 3 || ncm->kan_width[R] != 1)
+      return fail(C, COMMET_ERR_ARG, "kan_width must start at 3 inputs and end at 1 output");
+    for (int r = 0; r <= R; r++)
+      if (ncm->kan_width[r] < 1 || ncm->kan_width[r] > 16)
+        return fail(C, COMMET_ERR_ARG, "kan_width[%d] = %d not in 1..16", r, ncm->kan_width[r]);
+    if (ncm->kan_k != 3) return fail(C, COMMET_ERR_ARG, "kan_k %d: the CUDA path evaluates cubic splines (3)", ncm->kan_k);
+    if (ncm->kan_nb < 4 || ncm->kan_nb > 32) return fail(C, COMMET_ERR_ARG, "kan_nb %d not in 4..32", ncm->kan_nb);
+    for (int r = 0; r < R; r++) {
+      if (!(ncm->kan_grid[2 * r + 1] > ncm->kan_grid[2 * r]))
+        return fail(C, COMMET_ERR_ARG, "kan_grid layer %d: xmax <= xmin", r);
+      kan_edges += (int64_t)ncm->kan_width[r] * ncm->kan_width[r + 1];
+    }
   }
   if (net == COMMET_NET_CANN) {
     if (ncm->cann_n < 1 || ncm->cann_n > 16) return fail(C, COMMET_ERR_ARG, "cann_n %d not in 1..16", ncm->cann_n);
@@ -139,6 +158,11 @@ extern "C" commet_status commet_setup(const commet_mesh_desc* mesh, const commet
   if ((s = upload(C, c->W1, icnn ? ncm->W1 : zw.data(), (size_t)w * 3, st))) return s;
   if ((s = upload(C, c->b, icnn ? ncm->b : zw.data(), (size_t)L * w, st))) return s;
   if ((s = upload(C, c->a, icnn ? ncm->a : zw.data(), (size_t)w, st))) return s;
+  if (net == COMMET_NET_ICKAN) {
+    if ((s = upload(C, c->kan_grid, ncm->kan_grid, (size_t)2 * ncm->kan_layers, st))) return s;
+    if ((s = upload(C, c->kan_w, ncm->kan_w, (size_t)kan_edges, st))) return s;
+    if ((s = upload(C, c->kan_c, ncm->kan_c, (size_t)kan_edges * ncm->kan_nb, st))) return s;
+  }
   if (net == COMMET_NET_CANN) {
     const size_t nb = (size_t)3 * ncm->cann_n;
     if ((s = upload(C, c->cann_f, ncm->cann_f, 3 * nb, st))) return s;
@@ -163,7 +187,11 @@ extern "C" commet_status commet_setup(const commet_mesh_desc* mesh, const commet
   c->ncm = NcmDev{L, w, c->W1.p, c->b.p, c->a.p, c->skip_out.p, c->skip_h.p, c->Wrow.p, c->Wfrag.p,
                   c->act_tab.p, c->gfrag.p, ncm->kappa, ncm->ref_shift, kin, net,
                   net == COMMET_NET_CANN ? ncm->cann_n : 0, c->cann_f.p, c->cann_w1.p, c->cann_w2.p,
-                  {ncm->gt[0], ncm->gt[1], ncm->gt[2]}};
+                  {ncm->gt[0], ncm->gt[1], ncm->gt[2]},
+                  net == COMMET_NET_ICKAN ? ncm->kan_layers : 0, net == COMMET_NET_ICKAN ? ncm->kan_nb : 0,
+                  {0, 0, 0, 0, 0}, c->kan_grid.p, c->kan_w.p, c->kan_c.p};
+  if (net == COMMET_NET_ICKAN)
+    for (int r = 0; r <= ncm->kan_layers; r++) c->ncm.kan_width[r] = ncm->kan_width[r];
   CUDA_TRY(C, c->bad.alloc(1));
   CUDA_TRY(C, c->max_trc.alloc(1));
   CUDA_TRY(C, c->r_halo.alloc(3 * p.n_halo));

@@ -36,6 +36,11 @@ struct NcmDev {
   const double* cann_w1;  // [3][n]
   const double* cann_w2;  // [3][n]
   double gt[3];
+  int kan_R, kan_nb;      // ICKAN (net 3)
+  int kan_width[5];
+  const double* kan_grid;  // [R][2]
+  const double* kan_w;     // [edges]
+  const double* kan_c;     // [edges][nb]
 };
 
 struct AsmArgs {

@@ -53,7 +53,7 @@ struct commet_ctx_s {
   DevBuf<int32_t> node_deg;
   DevBuf<double> W1, b, a, skip_out, skip_h, Wrow, Wfrag, act_tab, gfrag;
   DevBuf<int32_t> cann_f;
-  DevBuf<double> cann_w1, cann_w2;
+  DevBuf<double> cann_w1, cann_w2, kan_grid, kan_w, kan_c;
   DevBuf<double> r_halo, v_halo, r_recv, v_recv;
   DevBuf<int64_t> recv_val_map, recv_row_map;
   DevBuf<unsigned long long> bad, max_trc;

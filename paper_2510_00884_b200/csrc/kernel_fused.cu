@@ -28,6 +28,7 @@
 
 #include "commet_internal.h"
 #include "qp_math.cuh"
+#include "ickan.cuh"
 
 #ifndef COMMET_SIGMOID_LAST
 #define COMMET_SIGMOID_LAST 1
@@ -250,8 +251,7 @@ __device__ __forceinline__ void material_outputs(const AsmArgs& A, const NcmDev&
       for (int r = 0; r < rows; r++) N += qNp[r * Q + q];
       N += __ldg(m.skip_out) * kq[0] + __ldg(m.skip_out + 1) * kq[1] + __ldg(m.skip_out + 2) * kq[2];
     } else {
-      analytic_net(m.net, m.cann_n, m.cann_f, m.cann_w1, m.cann_w2, m.gt, m.skip_out, kq, gq, H6);
-      N = analytic_value(m.net, m.cann_n, m.cann_f, m.cann_w1, m.cann_w2, m.gt, m.skip_out, kq);
+      analytic_point(m, kq, gq, H6, &N);
     }
     Kin kin;
     kinematics(qF + q * 9, kin);
@@ -887,7 +887,7 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
           H6[x] = s;
         }
       } else {
-        analytic_net(m.net, m.cann_n, m.cann_f, m.cann_w1, m.cann_w2, m.gt, m.skip_out, qk + q * 3, gq, H6);
+        analytic_point(m, qk + q * 3, gq, H6, nullptr);
       }
       Kin kin;
       kinematics(qF + q * 9, kin);

@@ -6,6 +6,7 @@
 #pragma once
 #include "commet_internal.h"
 #include "qp_math.cuh"
+#include "ickan.cuh"
 
 namespace commet {
 
@@ -72,7 +73,7 @@ __device__ __forceinline__ void ncm_point(const NcmDev& m, const double* kin, do
   if (m.net == 0)
     ncm_alg4(m, kin, g, H6);
   else
-    analytic_net(m.net, m.cann_n, m.cann_f, m.cann_w1, m.cann_w2, m.gt, m.skip_out, kin, g, H6);
+    analytic_point(m, kin, g, H6, nullptr);
 }
 
 }  // namespace commet

@@ -275,6 +275,24 @@ def gent_thomas_params(coef=(0.5, 1.0, 1.0), kappa: float = 0.0) -> dict:
                 ref_shift=0.0)
 
 
+def ickan_params(widths=(3, 6, 6, 1), nb: int = 8, k: int = 3, seed: int = SEED_W, kinematics: str = "standard",
+                 kappa: float = 10.0, std: float = 0.3) -> dict:
+    """ICKAN (App. B.3) parameters: per edge a weight |N(0, std^2)| and nb control points that
+    increase with nondecreasing steps (convex, monotone: the paper's c_{i+2}-c_{i+1} >= c_{i+1}-c_i
+    >= 0); knot intervals [-1, 1] for layer 0 (the invariant inputs) and [-2, 2] after it."""
+    rng = np.random.default_rng(seed)
+    widths = tuple(int(x) for x in widths)
+    n_edges = sum(widths[r] * widths[r + 1] for r in range(len(widths) - 1))
+    w = np.abs(rng.normal(0.0, std, size=n_edges))
+    d0 = rng.uniform(0.0, 0.2, size=(n_edges, 1))
+    steps = np.concatenate([d0, rng.uniform(0.0, 0.15, size=(n_edges, nb - 2))], axis=1).cumsum(axis=1)
+    c = np.concatenate([rng.normal(0.0, std, size=(n_edges, 1)), steps], axis=1).cumsum(axis=1)
+    grid = np.array([[-1.0, 1.0]] + [[-2.0, 2.0]] * (len(widths) - 2), dtype=np.float64)
+    return dict(network="ickan", kinematics=kinematics, width=8, n_hidden=1, W1=None, W=None, b=None, a=None,
+                skip_out=None, skip_hidden=None, kan_width=np.array(widths, np.int32), kan_nb=nb, kan_k=k,
+                kan_grid=grid, kan_w=w, kan_c=np.ascontiguousarray(c), kappa=float(kappa), ref_shift=0.0)
+
+
 def smooth_field(X: np.ndarray, amp: float, rng) -> np.ndarray:
     """u_i = amp * phi_i / max|phi_i|, phi_i = sum_{m<4} c sin(2 pi k.X + th),
     k uniform on {0,1}^3 minus 0, c ~ N(0,1), th ~ U[0, 2pi)."""

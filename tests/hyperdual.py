@@ -97,6 +97,57 @@ def _cann_hd(k, ncm):
     return N
 
 
+def _bspline(c, k, t, span, x):
+    """sum_i c_i B_{i,k}(x) by De Boor's recursion (B_{i,0} = 1 on the given knot span);
+    x may be a float or an HD number."""
+    nt = len(t)
+    B = [HD(1.0) if i == span else HD(0.0) for i in range(nt)]
+    for p in range(1, k + 1):
+        Bn = []
+        for i in range(nt - p - 1):
+            v = HD(0.0)
+            if t[i + p] > t[i]:
+                v = v + (x - t[i]) * (1.0 / (t[i + p] - t[i])) * B[i]
+            if t[i + p + 1] > t[i + 1]:
+                v = v + (t[i + p + 1] - x) * (1.0 / (t[i + p + 1] - t[i + 1])) * B[i + 1]
+            Bn.append(v)
+        B = Bn
+    return sum((c[i] * B[i] for i in range(len(c))), HD(0.0))
+
+
+def _spline_hd(c, k, xmin, xmax, x: HD) -> HD:
+    nb = len(c)
+    h = (xmax - xmin) / (nb - k)
+    t = [xmin + (i - k) * h for i in range(nb + k + 1)]
+    xa = float(np.ravel(x.a)[0])
+    xe = min(max(xa, xmin), xmax)
+    span = k
+    while span < nb - 1 and xe >= t[span + 1]:
+        span += 1
+    if xe == xa:
+        return _bspline(c, k, t, span, x)
+    # linear continuation with the end value and slope (one dual direction at the boundary)
+    e = _bspline(c, k, t, span, HD(xe, 1.0, 0.0, 0.0))
+    return e.a + e.b * (x - xe)
+
+
+def _ickan_hd(k, ncm):
+    widths, nb, kk = list(ncm["kan_width"]), int(ncm["kan_nb"]), int(ncm["kan_k"])
+    z = list(k)
+    e = 0
+    for r in range(len(widths) - 1):
+        xmin, xmax = ncm["kan_grid"][r]
+        y = []
+        for i in range(widths[r + 1]):
+            s = HD(0.0)
+            for j in range(widths[r]):
+                s = s + ncm["kan_w"][e] * _spline_hd(ncm["kan_c"][e], kk, xmin, xmax, z[j])
+                e += 1
+            y.append(s)
+        z = y
+    return z[0]
+
+
 def energy_hd(F: list, ncm: dict):
     """W(F) for a 3x3 list-of-lists of HD; written from the definitions:
     C = F^T F, I1 = tr C, I2 = (I1^2 - tr C^2)/2, J = det F (Sarrus),
@@ -118,6 +169,9 @@ def energy_hd(F: list, ncm: dict):
         if ncm.get("skip_out") is not None:
             for i in range(3):
                 N = N + ncm["skip_out"][i] * k[i]
+        return N + kap * (J - 1.0) * (J - 1.0) - s0 * (J - 1.0)
+    if net == "ickan":
+        N = _ickan_hd(k, ncm)
         return N + kap * (J - 1.0) * (J - 1.0) - s0 * (J - 1.0)
     if net == "gent_thomas":
         c = ncm["gt"]

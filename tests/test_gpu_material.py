@@ -7,7 +7,7 @@ import numpy as np
 import pytest
 
 import oracle
-from synth.gen import cann_params, gent_thomas_params, ncm_weights
+from synth.gen import cann_params, gent_thomas_params, ickan_params, ncm_weights
 from tests.test_oracle_material import rand_F
 from tests.test_oracle_variants import isochoric_icnn
 
@@ -40,6 +40,7 @@ MODELS = {
     "icnn_iso_16x2": isochoric_icnn,
     "cann": lambda: cann_params(4, seed=3),
     "gent_thomas": gent_thomas_params,
+    "ickan": lambda: ickan_params(),
 }
 
 

@@ -7,8 +7,8 @@ import pytest
 
 import oracle
 from oracle import newton as on
-from synth.gen import (HEX8, TET10, cann_params, gent_thomas_params, hex_mesh, ncm_weights, shape_gradients,
-                       smooth_field, tet10_mesh)
+from synth.gen import (HEX8, TET10, cann_params, gent_thomas_params, hex_mesh, ickan_params, ncm_weights,
+                       shape_gradients, smooth_field, tet10_mesh)
 
 pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")
@@ -36,6 +36,8 @@ VARIANTS = {
     "cann_isochoric": lambda: cann_params(5, seed=4, kinematics="isochoric"),
     "icnn_isochoric_16x2": lambda: _iso_icnn(16, 2),
     "icnn_isochoric_64x3": lambda: _iso_icnn(64, 3),
+    "ickan": lambda: ickan_params(),
+    "ickan_isochoric": lambda: ickan_params((3, 5, 1), nb=7, seed=5, kinematics="isochoric"),
 }
 
 
@@ -69,7 +71,7 @@ def test_variant_assembly_matches_oracle(pc, name, elem_type, n, kernel):
     assert _rel(r.cpu().numpy(), ro) <= TOL and _rel(v.cpu().numpy(), vo) <= TOL
 
 
-@pytest.mark.parametrize("name", ["gent_thomas", "cann_standard", "cann_isochoric"])
+@pytest.mark.parametrize("name", ["gent_thomas", "cann_standard", "cann_isochoric", "ickan"])
 def test_analytic_ncm_eval_matches_oracle(pc, name):
     ncm = VARIANTS[name]()
     mesh, _ = _mesh(HEX8, 1)
@@ -84,7 +86,7 @@ def test_analytic_ncm_eval_matches_oracle(pc, name):
         assert np.abs(H[i] - Ho[np.triu_indices(3)]).max() <= 1e-14 * max(1.0, np.abs(Ho).max())
 
 
-@pytest.mark.parametrize("name", ["gent_thomas", "icnn_isochoric_16x2", "cann_isochoric"])
+@pytest.mark.parametrize("name", ["gent_thomas", "icnn_isochoric_16x2", "cann_isochoric", "ickan"])
 def test_normalize_reference_variants(pc, name):
     ncm = VARIANTS[name]()
     mesh, _ = _mesh(HEX8, 1)

@@ -9,7 +9,7 @@ import numpy as np
 import pytest
 
 import oracle
-from synth.gen import cann_params, gent_thomas_params, hex_mesh, ncm_weights, shape_gradients
+from synth.gen import cann_params, gent_thomas_params, hex_mesh, ickan_params, ncm_weights, shape_gradients
 from tests import hyperdual
 from tests.test_oracle_material import I3, rand_F, rot
 
@@ -25,6 +25,8 @@ VARIANTS = {
     "cann_standard": lambda: cann_params(4, seed=3),
     "cann_isochoric": lambda: cann_params(5, seed=4, kinematics="isochoric"),
     "icnn_isochoric": isochoric_icnn,
+    "ickan": lambda: ickan_params(),
+    "ickan_isochoric": lambda: ickan_params((3, 5, 1), nb=7, seed=5, kinematics="isochoric"),
 }
 
 
@@ -119,3 +121,35 @@ def test_assembly_residual_is_energy_gradient(name):
         um[i] -= h
         fd = (oracle.energy(m, conn, gN, w, up) - oracle.energy(m, conn, gN, w, um)) / (2 * h)
         assert abs(fd - r[i]) <= 1e-7 * max(1e-3, np.abs(r).max())
+
+
+# ---- ICKAN -----------------------------------------------------------------------------
+def test_ickan_linear_spline_closed_form():
+    """Control points on a line reproduce it exactly (B-spline partition of unity and
+    linear precision): N = sum_j w_j (a_j + b_j k_j) for a one-layer ICKAN, inside and
+    outside the knot interval (linear continuation), so g = w b and H = 0."""
+    nb, k = 7, 3
+    xmin, xmax = -1.0, 1.0
+    h = (xmax - xmin) / (nb - k)
+    # Greville abscissae of uniform cubic knots: xi_i = xmin + (i - 1) h
+    xi = xmin + (np.arange(nb) - 1.0) * h
+    a = np.array([0.3, -0.1, 0.2])
+    b = np.array([1.5, 0.5, 2.0])
+    c = np.stack([a[j] + b[j] * xi for j in range(3)])
+    w = np.array([0.7, 1.1, 0.4])
+    m = dict(network="ickan", kinematics="standard", width=8, n_hidden=1, W1=None, W=None, b=None, a=None,
+             skip_out=None, skip_hidden=None, kan_width=np.array([3, 1], np.int32), kan_nb=nb, kan_k=k,
+             kan_grid=np.array([[xmin, xmax]]), kan_w=w, kan_c=c, kappa=0.0, ref_shift=0.0)
+    for K in ([0.1, -0.3, 0.7], [1.4, -1.8, 0.0]):
+        N, g, H = oracle.ncm_eval(m, np.array(K))
+        assert abs(N - np.sum(w * (a + b * np.array(K)))) < 1e-14
+        assert np.allclose(g, w * b, rtol=0, atol=1e-14) and np.abs(H).max() < 1e-13
+
+
+def test_ickan_convex_in_inputs():
+    """Monotone convex splines with positive weights: H positive semi-definite (App. B.3)."""
+    m = ickan_params()
+    rng = np.random.default_rng(3)
+    for _ in range(20):
+        _, g, H = oracle.ncm_eval(m, rng.uniform(-0.8, 0.8, 3))
+        assert np.linalg.eigvalsh(H).min() >= -1e-14 and (g >= 0).all()

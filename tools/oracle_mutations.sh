@@ -40,4 +40,7 @@ mut "t += Fi[I * 3 + i] * Fi[J * 3 + j] * Fi[K * 3 + k] * Fi[L * 3 + l] * c[I4(i
 mut "dd2 = w1 * w1 / ((1.0 - w1 * v1) * (1.0 - w1 * v1));" "dd2 = -w1 * w1 / ((1.0 - w1 * v1) * (1.0 - w1 * v1));"
 mut "H[mm * 3 + mm] += w2 * ((dd2 * d1 * d1 + d2 * dd1) * d0 * d0" "H[mm * 3 + mm] += w2 * ((dd2 * d1 + d2 * dd1) * d0 * d0"
 mut "H[4] = -m->gt[1] / ((K[1] + 3.0) * (K[1] + 3.0));" "H[4] = m->gt[1] / ((K[1] + 3.0) * (K[1] + 3.0));"
+# ICKAN: De Boor recursion and spline derivatives
+mut "if (t[i + p + 1] > t[i + 1]) v += (t[i + p + 1] - x) / (t[i + p + 1] - t[i + 1]) * B[(p - 1) * nt + i + 1];" "if (t[i + p + 1] > t[i + 1]) v += (t[i + p + 1] - x) / (t[i + p + 1] - t[i]) * B[(p - 1) * nt + i + 1];"
+mut "for (int q = 0; q < 3; q++) d2y[i][p * 3 + q] += w * (d2 * dz[j][p] * dz[j][q] + d1 * d2z[j][p * 3 + q]);" "for (int q = 0; q < 3; q++) d2y[i][p * 3 + q] += w * (d2 * dz[j][p] * dz[j][q]);"
 exit $fail
