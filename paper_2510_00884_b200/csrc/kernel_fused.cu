@@ -30,15 +30,9 @@
 #include "qp_math.cuh"
 #include "ickan.cuh"
 
-#ifndef COMMET_SIGMOID_LAST
-#define COMMET_SIGMOID_LAST 1
-#endif
 // element stage on DMMA: 1 = hex8 only (measured: +6% c3, -4% c4 where 10 nodes pad to 16)
 #ifndef COMMET_DMMA_ELEM
 #define COMMET_DMMA_ELEM 1
-#endif
-#ifndef COMMET_L1_UNROLL
-#define COMMET_L1_UNROLL 1
 #endif
 #ifndef COMMET_PREFETCH
 #define COMMET_PREFETCH 1
@@ -54,9 +48,6 @@
 #endif
 #ifndef COMMET_PINGPONG
 #define COMMET_PINGPONG 0  // measured neutral (c3 10.31 vs 10.26 ms): barriers kept
-#endif
-#ifndef COMMET_SYM_KE
-#define COMMET_SYM_KE 1
 #endif
 
 namespace commet {
@@ -484,7 +475,6 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
     if constexpr (C::NET == 0) {
     // ---- stage 2: layer 1 (3 -> W), elementwise -------------------------------------
     if (L > 1) frag_prefetch<C::MT_V, KT2, COMMET_FRAG_PF + (COMMET_FRAG_PF == 0)>(m.Wfrag, (warp / C::VNG) * C::MT_V);
-#if COMMET_L1_UNROLL
     // each thread: one qp, neurons j0, j0 + NTHR/Q, ... -- all loads issued up front and the
     // NIT activations interleaved (independent chains)
     {
@@ -517,23 +507,6 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
       }
       if constexpr (C::MODE == 1)
         if (L == 1) qNp[j0 * Q + q] = nv;
-    }
-    if (false)
-#endif
-    for (int x = tid; x < W * Q; x += C::NTHR) {
-      const int j = x / Q, q = x % Q;
-      const double y = __ldg(m.b + j) + __ldg(m.W1 + j * 3 + 0) * qk[q * 3 + 0] +
-                       __ldg(m.W1 + j * 3 + 1) * qk[q * 3 + 1] + __ldg(m.W1 + j * 3 + 2) * qk[q * 3 + 2];
-      double z, s;
-      softplus_sig(y, stab, z, s);
-      if (L > 1) {
-        sb[j * LDS + q] = s;
-        act[j * LDA + q] = z;
-      } else {
-        const double aj = __ldg(m.a + j);
-        act[j * LDA + q] = aj * s;
-        cb[j * LDS + q] = aj * s * (1.0 - s);
-      }
     }
     __syncthreads();
     STAGE_MARK(2)
@@ -588,7 +561,6 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
                   continue;
                 }
               }
-#if COMMET_SIGMOID_LAST
               if (l < L) {
                 double z, s;
                 softplus_sig(y, stab, z, s);
@@ -599,17 +571,6 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
                 act[j * LDA + wof + q] = aj * s;                             // mu_L
                 cb[((l - 2) * W + j) * LDS + q] = aj * s * (1.0 - s);        // c_L
               }
-#else
-              double z, s;
-              softplus_sig(y, stab, z, s);
-              if (l < L) {
-                sb[((l - 1) * W + j) * LDS + q] = s;
-                act[j * LDA + wof + q] = z;
-              } else {
-                act[j * LDA + wof + q] = aj * s;                             // mu_L
-                cb[((l - 2) * W + j) * LDS + q] = aj * s * (1.0 - s);        // c_L
-              }
-#endif
             }
         }
         __syncthreads();
@@ -985,7 +946,6 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
     }
     __syncthreads();
 
-#if COMMET_SYM_KE
     // ---- stage 8b: K_e[ai][bk] for node pairs b >= a only (K_e = K_e^T), r_e; RED scatter of
     //      (ai, bk) and its mirror (bk, ai)
     {
@@ -1032,45 +992,6 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
         }
       }
     }
-#else
-    // ---- stage 8b: K_e[ai][bk] = sum_q sum_L X dN_bL, r_e; coloured RMW scatter ----------------
-    for (int it = tid; it < ne * NEN * 3 * NEN; it += C::NTHR) {
-      const int b = it % NEN, row = it / NEN, e = row / (NEN * 3), ai = row % (NEN * 3), a = ai / 3, i = ai % 3;
-      double K0 = 0.0, K1 = 0.0, K2 = 0.0, rr = 0.0;
-#pragma unroll
-      for (int qq = 0; qq < NQ; qq++) {
-        const int q = e * NQ + qq;
-        const double* gb = sgN + (q * NEN + b) * 3;
-        const double h0 = gb[0], h1 = gb[1], h2 = gb[2];
-        const double* Xr = Xb + ((q * NEN + a) * 3 + i) * 9;
-        K0 += Xr[0] * h0 + Xr[1] * h1 + Xr[2] * h2;
-        K1 += Xr[3] * h0 + Xr[4] * h1 + Xr[5] * h2;
-        K2 += Xr[6] * h0 + Xr[7] * h1 + Xr[8] * h2;
-        if (b == 0) {
-          const double* ga = sgN + (q * NEN + a) * 3;
-          rr += qP[q * 9 + i * 3] * ga[0] + qP[q * 9 + i * 3 + 1] * ga[1] + qP[q * 9 + i * 3 + 2] * ga[2];
-        }
-      }
-      const int64_t el = e0 + e;
-      const int64_t ln = __ldg(A.lrow + el * NEN + a);
-      const bool own = ln < A.n_owned;
-      double* vb = own ? A.v_own : A.v_halo;
-      const int deg = __ldg(A.node_deg + ln);
-      const int64_t row0 = __ldg(A.node_rs + ln) + (int64_t)i * 3 * deg;
-      // fire-and-forget RED.ADD.F64: the colouring makes the updates conflict-free (and the
-      // per-entry summation order deterministic: one update per colour launch); RED avoids the
-      // load round trip of a read-modify-write
-      double* dst = vb + row0 + 3 * (int)__ldg(A.slot + ((size_t)el * NEN + a) * NEN + b);
-      atomicAdd(dst, K0);
-      atomicAdd(dst + 1, K1);
-      atomicAdd(dst + 2, K2);
-      if (b == 0) {
-        double* rb = own ? A.r_own : A.r_halo;
-        const int64_t rn = own ? ln : ln - A.n_owned;
-        atomicAdd(rb + 3 * rn + i, rr);
-      }
-    }
-#endif
     }  // DMMA_ELEM
     }  // MODE
 #ifdef COMMET_EXP_SKIP_ELEM
