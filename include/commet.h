@@ -108,12 +108,12 @@ typedef struct {
   double kappa;                /* volumetric penalty kappa (J-1)^2 */
   double ref_shift;            /* s0: adds -s0 (J-1) to W; 0 = off (reading R11) */
   /* ---- variants; a zero-initialised tail = the ICNN on k above ---- */
-  int32_t kinematics;          /* COMMET_KIN_STANDARD: k = (I1-3, I2-3, J-1);
+  int32_t kinematics;          /* COMMET_KIN_STANDARD: k = (I1-3, I2-3, J-1); COMMET_KIN_ANISOTROPIC: see a0;
                                   COMMET_KIN_ISOCHORIC: k = (Ibar1-3, Ibar2-3, J-1), Ibar1 = J^-2/3 I1,
                                   Ibar2 = J^-4/3 I2 (App. A.2.2) */
   int32_t network;             /* COMMET_NET_ICNN (the fields above), COMMET_NET_CANN, COMMET_NET_GENT_THOMAS */
   int32_t cann_n;              /* CANN: branches per kinematic input, 1..16 */
-  const int32_t* cann_f;       /* CANN host [3][cann_n][3]: f0 (0 x, 1 <x>, 2 |x|), f1 power (1..3),
+  const int32_t* cann_f;       /* CANN host [n_in][cann_n][3] (n_in = 3, or 5 anisotropic): f0 (0 x, 1 <x>, 2 |x|), f1 power (1..3),
                                   f2 (0 w1 x, 1 exp(w1 x) - 1, 2 -ln(1 - w1 x))  (Eq. cann-fs) */
   const double* cann_w1;       /* CANN host [3][cann_n] */
   const double* cann_w2;       /* CANN host [3][cann_n]: N = sum_m sum_b w2 f2(f1(f0(k_m)); w1)  (Eq. cann-def) */
@@ -131,9 +131,13 @@ typedef struct {
   const double* kan_grid;      /* host [R][2]: xmin, xmax of layer r's inputs */
   const double* kan_w;         /* host [edges]: spline weights, edges in (r, i, j) order */
   const double* kan_c;         /* host [edges][kan_nb]: control points */
+  /* COMMET_KIN_ANISOTROPIC: one structural vector A0 (reference configuration); the network
+   * inputs are k = (I1-3, I2-3, J-1, I4-1, I5-1), I4 = A0.C A0, I5 = A0.C^2 A0 (App. A.2.1,
+   * PAPER.md:810-826) -- CANN (cann_* arrays over 5 inputs) or ICKAN (kan_width[0] = 5) only. */
+  double a0[3];
 } commet_ncm_desc;
 
-enum { COMMET_KIN_STANDARD = 0, COMMET_KIN_ISOCHORIC = 1 };
+enum { COMMET_KIN_STANDARD = 0, COMMET_KIN_ISOCHORIC = 1, COMMET_KIN_ANISOTROPIC = 2 };
 enum { COMMET_NET_ICNN = 0, COMMET_NET_CANN = 1, COMMET_NET_GENT_THOMAS = 2, COMMET_NET_ICKAN = 3 };
 
 /* Kernel variants (commet_set_kernel).  FUSED is the product path; SIMPLE is
@@ -246,10 +250,11 @@ void commet_plan_destroy(commet_plan p);
 commet_status commet_max_trace_C(commet_ctx ctx, double* max_trC);
 
 /* ---- material-point calls on the ctx's NCM ------------------------------------
- * The inner network's gradient g = dN/dk [n][3] and Hessian H [n][6] (upper:
- * 00,01,02,11,12,22) at n invariant inputs k = (I1-3, I2-3, J-1) [n][3] (device
- * arrays), by Alg. 4; output skip included, penalty and
- * ref_shift excluded.  Asynchronous on cuda_stream. */
+ * The inner network's gradient g = dN/dk [n][nk] and Hessian H [n][nk(nk+1)/2] (packed
+ * upper triangle, row by row: 00,01,02,11,12,22 for nk = 3) at n network inputs k [n][nk]
+ * (device arrays; nk = 3, or 5 for anisotropic kinematics), by Alg. 4
+ * or the analytic networks' closed forms; output skip included, penalty and ref_shift
+ * excluded.  Asynchronous on cuda_stream. */
 commet_status commet_ncm_eval(commet_ctx ctx, const double* k, double* g, double* H, int64_t n,
                               void* cuda_stream);
 /* Material-point batch (the paper's material point
@@ -266,7 +271,8 @@ commet_status commet_material_eval(commet_ctx ctx, const double* F, int64_t n, d
 
 /* Stress-free reference (reading R11): sets the ctx's ref_shift to
  * s0 = 2 g1 + 4 g2 + g3 at k = 0, so that S(F = I) = 0 for subsequent assembles,
- * and returns it in *s0 (may be NULL).  Synchronous. */
+ * and returns it in *s0 (may be NULL).  Synchronous.  COMMET_ERR_ARG for anisotropic
+ * kinematics (S(I) then has a structural part no volumetric term cancels). */
 commet_status commet_normalize_reference(commet_ctx ctx, double* s0);
 
 /* ---- Newton-Raphson around the assembly --------------

@@ -36,9 +36,9 @@ class _Ncm(C.Structure):
                 ("cann_f", C.c_void_p), ("cann_w1", C.c_void_p), ("cann_w2", C.c_void_p),
                 ("gt", C.c_double * 3), ("kan_layers", C.c_int32), ("kan_width", C.c_void_p),
                 ("kan_nb", C.c_int32), ("kan_k", C.c_int32), ("kan_grid", C.c_void_p), ("kan_w", C.c_void_p),
-                ("kan_c", C.c_void_p)]
+                ("kan_c", C.c_void_p), ("a0", C.c_double * 3)]
 
-KIN = {"standard": 0, "isochoric": 1}
+KIN = {"standard": 0, "isochoric": 1, "anisotropic": 2}
 NET = {"icnn": 0, "cann": 1, "gent_thomas": 2, "ickan": 3}
 
 
@@ -51,6 +51,8 @@ def lib():
         _lib = C.CDLL(build())
         d, i64, i32, vp = C.c_double, C.c_int64, C.c_int, C.c_void_p
         _lib.oracle_ncm_eval.argtypes = [vp, vp, vp, vp, vp]
+        _lib.oracle_ncm_eval_n.argtypes = [vp, i32, vp, vp, vp, vp]
+        _lib.oracle_ncm_eval_n.restype = i32
         _lib.oracle_ncm_eval.restype = i32
         _lib.oracle_material_point.argtypes = [vp] * 10
         _lib.oracle_material_point.restype = d
@@ -95,7 +97,8 @@ class Ncm:
                       _p(self.arrays["cann_w1"]), _p(self.arrays["cann_w2"]), gt,
                       0 if self.kan_width is None else self.kan_width.size - 1, _p(self.kan_width),
                       int(ncm.get("kan_nb", 0)), int(ncm.get("kan_k", 3)), _p(self.arrays["kan_grid"]),
-                      _p(self.arrays["kan_w"]), _p(self.arrays["kan_c"]))
+                      _p(self.arrays["kan_w"]), _p(self.arrays["kan_c"]),
+                      (C.c_double * 3)(*(ncm.get("a0") if ncm.get("a0") is not None else (0.0, 0.0, 0.0))))
 
     @property
     def ptr(self):
@@ -109,6 +112,17 @@ def ncm_eval(ncm: dict, k):
     rc = lib().oracle_ncm_eval(m.ptr, _p(k), _p(N), _p(g), _p(H))
     assert rc == 0
     return N[0], g, H.reshape(3, 3)
+
+
+def ncm_eval_n(ncm: dict, k):
+    """Inner network on nin = len(k) inputs (3, or 5 for CANN / ICKAN on anisotropic inputs)."""
+    m = Ncm(ncm)
+    k = np.ascontiguousarray(k, dtype=np.float64)
+    n = k.size
+    N, g, H = np.zeros(1), np.zeros(n), np.zeros(n * n)
+    rc = lib().oracle_ncm_eval_n(m.ptr, n, _p(k), _p(N), _p(g), _p(H))
+    assert rc == 0, rc
+    return N[0], g, H.reshape(n, n)
 
 
 def material_point(ncm: dict, F):

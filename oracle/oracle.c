@@ -52,6 +52,7 @@ typedef struct {
   const double* kan_grid;    /* [R][2] xmin, xmax */
   const double* kan_w;       /* [edges] */
   const double* kan_c;       /* [edges][nb] */
+  double a0[3];              /* anisotropic kinematics (kinematics = 2): structural vector A0 (reference) */
 } oracle_ncm;
 
 /* ---------------------------------------------------------------------- */
@@ -153,11 +154,11 @@ static int icnn_eval(const oracle_ncm* m, const double K[3], double* N_out, doub
  * +w1^2/(1 - w1 x)^2} (reading R22: the paper prints a minus sign on the last).
  */
 static double sgn(double x) { return (x > 0) - (x < 0); }
-static int cann_eval(const oracle_ncm* m, const double K[3], double* N_out, double g[3], double H[9]) {
+static int cann_eval(const oracle_ncm* m, int nin, const double* K, double* N_out, double* g, double* H) {
   const int n = m->cann_n;
   double N = 0.0;
-  for (int p = 0; p < 9; p++) H[p] = 0.0;
-  for (int mm = 0; mm < 3; mm++) {
+  for (int p = 0; p < nin * nin; p++) H[p] = 0.0;
+  for (int mm = 0; mm < nin; mm++) {
     g[mm] = 0.0;
     for (int k = 0; k < n; k++) {
       const int32_t* f = m->cann_f + ((size_t)mm * n + k) * 3;
@@ -175,7 +176,7 @@ static int cann_eval(const oracle_ncm* m, const double K[3], double* N_out, doub
       else { v2 = -log(1.0 - w1 * v1); d2 = w1 / (1.0 - w1 * v1); dd2 = w1 * w1 / ((1.0 - w1 * v1) * (1.0 - w1 * v1)); }
       N += w2 * v2;
       g[mm] += w2 * d2 * d1 * d0;
-      H[mm * 3 + mm] += w2 * ((dd2 * d1 * d1 + d2 * dd1) * d0 * d0 + d2 * d1 * 0.0);
+      H[mm * nin + mm] += w2 * ((dd2 * d1 * d1 + d2 * dd1) * d0 * d0 + d2 * d1 * 0.0);
     }
   }
   if (m->skip_out)
@@ -263,14 +264,15 @@ static void spline_eval(const double* c, int nb, int k, double xmin, double xmax
   }
 }
 /* forward mode through the layers: z, dz/dK (3), d2z/dK2 (3x3) per node, as Alg. 4 does for the ICNN */
-static int ickan_eval(const oracle_ncm* m, const double K[3], double* N_out, double g[3], double H[9]) {
+static int ickan_eval(const oracle_ncm* m, int nk, const double* K, double* N_out, double* g, double* H) {
   const int R = m->kan_layers, nb = m->kan_nb, k = m->kan_k;
-  double z[32], dz[32][3], d2z[32][9], y[32], dy[32][3], d2y[32][9];
+  double z[32], dz[32][5], d2z[32][25], y[32], dy[32][5], d2y[32][25];
   int nin = m->kan_width[0];
+  if (nin != nk) return 3;
   for (int j = 0; j < nin; j++) {
     z[j] = K[j];
-    for (int p = 0; p < 3; p++) dz[j][p] = (p == j);
-    for (int pq = 0; pq < 9; pq++) d2z[j][pq] = 0.0;
+    for (int p = 0; p < nk; p++) dz[j][p] = (p == j);
+    for (int pq = 0; pq < nk * nk; pq++) d2z[j][pq] = 0.0;
   }
   size_t e = 0;
   for (int r = 0; r < R; r++) {
@@ -278,28 +280,28 @@ static int ickan_eval(const oracle_ncm* m, const double K[3], double* N_out, dou
     const double xmin = m->kan_grid[2 * r], xmax = m->kan_grid[2 * r + 1];
     for (int i = 0; i < nout; i++) {
       y[i] = 0.0;
-      for (int p = 0; p < 3; p++) dy[i][p] = 0.0;
-      for (int pq = 0; pq < 9; pq++) d2y[i][pq] = 0.0;
+      for (int p = 0; p < nk; p++) dy[i][p] = 0.0;
+      for (int pq = 0; pq < nk * nk; pq++) d2y[i][pq] = 0.0;
       for (int j = 0; j < nin; j++, e++) {
         double v, d1, d2;
         spline_eval(m->kan_c + e * nb, nb, k, xmin, xmax, z[j], &v, &d1, &d2);
         const double w = m->kan_w[e];
         y[i] += w * v;
-        for (int p = 0; p < 3; p++) dy[i][p] += w * d1 * dz[j][p];
-        for (int p = 0; p < 3; p++)
-          for (int q = 0; q < 3; q++) d2y[i][p * 3 + q] += w * (d2 * dz[j][p] * dz[j][q] + d1 * d2z[j][p * 3 + q]);
+        for (int p = 0; p < nk; p++) dy[i][p] += w * d1 * dz[j][p];
+        for (int p = 0; p < nk; p++)
+          for (int q = 0; q < nk; q++) d2y[i][p * nk + q] += w * (d2 * dz[j][p] * dz[j][q] + d1 * d2z[j][p * nk + q]);
       }
     }
     for (int i = 0; i < nout; i++) {
       z[i] = y[i];
-      for (int p = 0; p < 3; p++) dz[i][p] = dy[i][p];
-      for (int pq = 0; pq < 9; pq++) d2z[i][pq] = d2y[i][pq];
+      for (int p = 0; p < nk; p++) dz[i][p] = dy[i][p];
+      for (int pq = 0; pq < nk * nk; pq++) d2z[i][pq] = d2y[i][pq];
     }
     nin = nout;
   }
   *N_out = z[0];
-  for (int p = 0; p < 3; p++) g[p] = dz[0][p];
-  for (int pq = 0; pq < 9; pq++) H[pq] = d2z[0][pq];
+  for (int p = 0; p < nk; p++) g[p] = dz[0][p];
+  for (int pq = 0; pq < nk * nk; pq++) H[pq] = d2z[0][pq];
   if (m->skip_out)
     for (int p = 0; p < 3; p++) {
       *N_out += m->skip_out[p] * K[p];
@@ -308,12 +310,19 @@ static int ickan_eval(const oracle_ncm* m, const double K[3], double* N_out, dou
   return 0;
 }
 
+/* the inner network on nin = 3 inputs (standard / isochoric kinematics) or 5 (anisotropic:
+ * CANN and ICKAN only); g [nin], H [nin][nin] */
+int oracle_ncm_eval_n(const oracle_ncm* m, int nin, const double* K, double* N_out, double* g_out, double* H_out) {
+  if (m->network == 1) return cann_eval(m, nin, K, N_out, g_out, H_out);
+  if (m->network == 3) return ickan_eval(m, nin, K, N_out, g_out, H_out);
+  if (nin != 3) return 4;
+  if (m->network == 2) return gt_eval(m, K, N_out, g_out, H_out);
+  return icnn_eval(m, K, N_out, g_out, H_out);
+}
+
 int oracle_ncm_eval(const oracle_ncm* m, const double K[3], double* N_out, double g_out[3],
                     double H_out[9]) {
-  if (m->network == 1) return cann_eval(m, K, N_out, g_out, H_out);
-  if (m->network == 2) return gt_eval(m, K, N_out, g_out, H_out);
-  if (m->network == 3) return ickan_eval(m, K, N_out, g_out, H_out);
-  return icnn_eval(m, K, N_out, g_out, H_out);
+  return oracle_ncm_eval_n(m, 3, K, N_out, g_out, H_out);
 }
 
 /* ---------------------------------------------------------------------- */
@@ -350,10 +359,12 @@ static void inv3(const double M[9], double out[9]) {
  *   S = F^-1 tau F^-T;  CC_IJKL = F^-1_Ii F^-1_Jj F^-1_Kk F^-1_Ll c_ijkl  (App. A.1 pull-back)
  * with (A(x)_B)_ijkl = 1/2 (A_ik B_jl + A_il B_jk) (reading 5).
  */
+static void spatial_to_material(const double F[9], int n, double G[][9], double GG[][81], const double* g,
+                                const double* H, double S[9], double CC[81]);
 static void isochoric_S_CC(const double F[9], double Jd, const double g[3], const double H[9], double S[9],
                            double CC[81]) {
   const double a = pow(Jd, -2.0 / 3.0);
-  double Bb[9], Bb2[9], G[3][9], GG[3][81], Fi[9];
+  double Bb[9], Bb2[9], G[3][9], GG[3][81];
   for (int i = 0; i < 3; i++)
     for (int j = 0; j < 3; j++) {
       double t = 0.0;
@@ -403,18 +414,25 @@ static void isochoric_S_CC(const double F[9], double Jd, const double g[3], cons
           GG[2][I4(i, j, k, l)] = 0.25 * Jd * ((double)((i == j) * (k == l)) -
                                                  ((i == k) * (j == l) + (i == l) * (j == k)));
     }
-  double tau[9], c[81];
+  spatial_to_material(F, 3, G, GG, g, H, S, CC);
+}
+
+/* tau = 2 sum_m g_m G^m, c = 4 sum_mn H_mn G^m (x) G^n + 4 sum_m g_m GG^m (Eq. stress-cgo /
+ * stiffnes-cgo), pulled back: S = F^-1 tau F^-T, CC = F^-1 F^-1 F^-1 F^-1 c (App. A.1) */
+static void spatial_to_material(const double F[9], int n, double G[][9], double GG[][81], const double* g,
+                                const double* H, double S[9], double CC[81]) {
+  double tau[9], c[81], Fi[9];
   for (int ij = 0; ij < 9; ij++) {
     double t = 0.0;
-    for (int mm = 0; mm < 3; mm++) t += g[mm] * G[mm][ij];
+    for (int mm = 0; mm < n; mm++) t += g[mm] * G[mm][ij];
     tau[ij] = 2.0 * t;
   }
   for (int ij = 0; ij < 9; ij++)
     for (int kl = 0; kl < 9; kl++) {
       double t = 0.0;
-      for (int mm = 0; mm < 3; mm++)
-        for (int nn = 0; nn < 3; nn++) t += H[mm * 3 + nn] * G[mm][ij] * G[nn][kl];
-      for (int mm = 0; mm < 3; mm++) t += g[mm] * GG[mm][ij * 9 + kl];
+      for (int mm = 0; mm < n; mm++)
+        for (int nn = 0; nn < n; nn++) t += H[mm * n + nn] * G[mm][ij] * G[nn][kl];
+      for (int mm = 0; mm < n; mm++) t += g[mm] * GG[mm][ij * 9 + kl];
       c[ij * 9 + kl] = 4.0 * t;
     }
   inv3(F, Fi);
@@ -437,6 +455,50 @@ static void isochoric_S_CC(const double F[9], double Jd, const double g[3], cons
                   t += Fi[I * 3 + i] * Fi[J * 3 + j] * Fi[K * 3 + k] * Fi[L * 3 + l] * c[I4(i, j, k, l)];
           CC[I4(I, J, K, L)] = t;
         }
+}
+
+/*
+ * Anisotropic kinematics (one structural vector A0; App. A.2.1 table) in the
+ * paper's spatial form, a = F A0:
+ *   I1: G = B, GG = O;  I2: G = B tr B - B^2, GG = B(x)B - B(x)_B;  J: G = J/2 I, GG = J/4 (I(x)I - 2 I(x)_I)
+ *   I4 = A0.C A0: G = sym(a (x) a), GG = O;  I5 = A0.C^2 A0: G = 2 sym(a (x) B a),
+ *   GG = B (x)_ sym(a (x) a) + sym(a (x) a) (x)_ B
+ * then tau, c and the pull-back as above.  Inputs K = (I1-3, I2-3, J-1, I4-1, I5-1).
+ */
+static void anisotropic_S_CC(const double F[9], double Jd, const double a0[3], const double g[5], const double H[25],
+                             double S[9], double CC[81]) {
+  double B[9], B2[9], a[3], Ba[3], A[9], G[5][9], GG[5][81];
+  for (int i = 0; i < 3; i++) {
+    a[i] = F[i * 3] * a0[0] + F[i * 3 + 1] * a0[1] + F[i * 3 + 2] * a0[2];
+    for (int j = 0; j < 3; j++) B[i * 3 + j] = F[i * 3] * F[j * 3] + F[i * 3 + 1] * F[j * 3 + 1] + F[i * 3 + 2] * F[j * 3 + 2];
+  }
+  for (int i = 0; i < 3; i++) {
+    Ba[i] = B[i * 3] * a[0] + B[i * 3 + 1] * a[1] + B[i * 3 + 2] * a[2];
+    for (int j = 0; j < 3; j++) B2[i * 3 + j] = B[i * 3] * B[j] + B[i * 3 + 1] * B[3 + j] + B[i * 3 + 2] * B[6 + j];
+  }
+  const double trB = B[0] + B[4] + B[8];
+  for (int i = 0; i < 3; i++)
+    for (int j = 0; j < 3; j++) {
+      A[i * 3 + j] = a[i] * a[j];  /* sym(a (x) a) */
+      G[0][i * 3 + j] = B[i * 3 + j];
+      G[1][i * 3 + j] = B[i * 3 + j] * trB - B2[i * 3 + j];
+      G[2][i * 3 + j] = 0.5 * Jd * (i == j);
+      G[3][i * 3 + j] = a[i] * a[j];
+      G[4][i * 3 + j] = a[i] * Ba[j] + Ba[i] * a[j];  /* 2 sym(a (x) B a) */
+    }
+  for (int i = 0; i < 3; i++)
+    for (int j = 0; j < 3; j++)
+      for (int k = 0; k < 3; k++)
+        for (int l = 0; l < 3; l++) {
+          const int x = I4(i, j, k, l);
+          GG[0][x] = 0.0;
+          GG[1][x] = B[i * 3 + j] * B[k * 3 + l] - 0.5 * (B[i * 3 + k] * B[j * 3 + l] + B[i * 3 + l] * B[j * 3 + k]);
+          GG[2][x] = 0.25 * Jd * ((double)((i == j) * (k == l)) - ((i == k) * (j == l) + (i == l) * (j == k)));
+          GG[3][x] = 0.0;
+          GG[4][x] = 0.5 * (B[i * 3 + k] * A[j * 3 + l] + B[i * 3 + l] * A[j * 3 + k]) +
+                     0.5 * (A[i * 3 + k] * B[j * 3 + l] + A[i * 3 + l] * B[j * 3 + k]);
+        }
+  spatial_to_material(F, 5, G, GG, g, H, S, CC);
 }
 
 /*
@@ -467,6 +529,45 @@ double oracle_material_point(const oracle_ncm* m, const double F[9], double k_ou
   double I2 = 0.5 * (I1 * I1 - trC2);
   double Jd = det3(F);
   inv3(C, Ci);
+  if (m->kinematics == 2) { /* anisotropic: K = (I1-3, I2-3, J-1, I4-1, I5-1) */
+    double CA[3], C2A = 0.0, I4v = 0.0;
+    for (int I = 0; I < 3; I++) CA[I] = C[I * 3] * m->a0[0] + C[I * 3 + 1] * m->a0[1] + C[I * 3 + 2] * m->a0[2];
+    for (int I = 0; I < 3; I++) {
+      I4v += m->a0[I] * CA[I];
+      C2A += CA[I] * CA[I]; /* A0.C^2 A0 = |C A0|^2 */
+    }
+    const double k5[5] = {I1 - 3.0, I2 - 3.0, Jd - 1.0, I4v - 1.0, C2A - 1.0};
+    double N5, g5[5], H5[25];
+    oracle_ncm_eval_n(m, 5, k5, &N5, g5, H5);
+    const double W5 = N5 + m->kappa * (Jd - 1.0) * (Jd - 1.0) - m->ref_shift * (Jd - 1.0);
+    g5[2] += 2.0 * m->kappa * (Jd - 1.0) - m->ref_shift;
+    H5[12] += 2.0 * m->kappa;
+    anisotropic_S_CC(F, Jd, m->a0, g5, H5, S, CC);
+    for (int i = 0; i < 3; i++)
+      for (int J = 0; J < 3; J++) {
+        double t = 0.0;
+        for (int I = 0; I < 3; I++) t += F[i * 3 + I] * S[I * 3 + J];
+        P[i * 3 + J] = t;
+      }
+    for (int i = 0; i < 3; i++)
+      for (int J = 0; J < 3; J++)
+        for (int kk = 0; kk < 3; kk++)
+          for (int L = 0; L < 3; L++) {
+            double t = (i == kk) ? S[J * 3 + L] : 0.0;
+            for (int I = 0; I < 3; I++)
+              for (int K = 0; K < 3; K++) t += F[i * 3 + I] * CC[I4(I, J, K, L)] * F[kk * 3 + K];
+            A[I4(i, J, kk, L)] = t;
+          }
+    if (k_out)
+      for (int p = 0; p < 3; p++) k_out[p] = k5[p];
+    if (W_out) *W_out = W5;
+    if (g_out)
+      for (int p = 0; p < 3; p++) g_out[p] = g5[p];
+    if (H_out)
+      for (int p = 0; p < 3; p++)
+        for (int q = 0; q < 3; q++) H_out[p * 3 + q] = H5[p * 5 + q];
+    return Jd;
+  }
   double k[3] = {I1 - 3.0, I2 - 3.0, Jd - 1.0};
   if (m->kinematics == 1) {  /* isochoric invariants (App. A.2.2): Ibar1 = J^-2/3 I1, Ibar2 = J^-4/3 I2 */
     const double a = pow(Jd, -2.0 / 3.0);

@@ -56,12 +56,12 @@ class NcmDesc(C.Structure):
                 ("cann_f", C.c_void_p), ("cann_w1", C.c_void_p), ("cann_w2", C.c_void_p),
                 ("gt", C.c_double * 3), ("kan_layers", C.c_int32), ("kan_width", C.c_void_p),
                 ("kan_nb", C.c_int32), ("kan_k", C.c_int32), ("kan_grid", C.c_void_p), ("kan_w", C.c_void_p),
-                ("kan_c", C.c_void_p)]
+                ("kan_c", C.c_void_p), ("a0", C.c_double * 3)]
 
 
-KIN_STANDARD, KIN_ISOCHORIC = 0, 1
+KIN_STANDARD, KIN_ISOCHORIC, KIN_ANISOTROPIC = 0, 1, 2
 NET_ICNN, NET_CANN, NET_GENT_THOMAS, NET_ICKAN = 0, 1, 2, 3
-_KIN = {"standard": KIN_STANDARD, "isochoric": KIN_ISOCHORIC}
+_KIN = {"standard": KIN_STANDARD, "isochoric": KIN_ISOCHORIC, "anisotropic": KIN_ANISOTROPIC}
 _NET = {"icnn": NET_ICNN, "cann": NET_CANN, "gent_thomas": NET_GENT_THOMAS, "ickan": NET_ICKAN}
 
 
@@ -84,7 +84,8 @@ def ncm_desc(ncm: dict):
                  0 if cf is None else cf.shape[1], _ptr(cf), _ptr(arrs["cann_w1"]), _ptr(arrs["cann_w2"]),
                  (C.c_double * 3)(*(gt if gt is not None else (0.0, 0.0, 0.0))),
                  0 if kw is None else kw.size - 1, _ptr(kw), int(ncm.get("kan_nb", 0)), int(ncm.get("kan_k", 3)),
-                 _ptr(arrs["kan_grid"]), _ptr(arrs["kan_w"]), _ptr(arrs["kan_c"]))
+                 _ptr(arrs["kan_grid"]), _ptr(arrs["kan_w"]), _ptr(arrs["kan_c"]),
+                 (C.c_double * 3)(*(ncm.get("a0") if ncm.get("a0") is not None else (0.0, 0.0, 0.0))))
     return nd, [arrs, cf, kw]
 
 
@@ -325,9 +326,9 @@ class Commet:
         """Inner-network gradient [n,3] and Hessian [n,6] at invariant inputs k (cuda [n,3])."""
         t = self.torch
         k = k.contiguous()
-        n = k.shape[0]
-        g = t.empty((n, 3), dtype=t.float64, device=k.device)
-        H = t.empty((n, 6), dtype=t.float64, device=k.device)
+        n, nk = k.shape[0], k.shape[1]
+        g = t.empty((n, nk), dtype=t.float64, device=k.device)
+        H = t.empty((n, nk * (nk + 1) // 2), dtype=t.float64, device=k.device)
         st = stream if stream is not None else t.cuda.current_stream(self.device)
         _check(_lib.commet_ncm_eval(self.ctx, k.data_ptr(), g.data_ptr(), H.data_ptr(), n, st.cuda_stream),
                self.ctx)

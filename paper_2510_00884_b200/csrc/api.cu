@@ -37,8 +37,11 @@ extern "C" commet_status commet_setup(const commet_mesh_desc* mesh, const commet
   commet_ctx C = c.get();
   // NCM arguments (host checks, before any CUDA call)
   const int net = ncm->network, kin = ncm->kinematics;
-  if (kin != COMMET_KIN_STANDARD && kin != COMMET_KIN_ISOCHORIC)
+  if (kin != COMMET_KIN_STANDARD && kin != COMMET_KIN_ISOCHORIC && kin != COMMET_KIN_ANISOTROPIC)
     return fail(C, COMMET_ERR_ARG, "kinematics %d unknown", kin);
+  const int nk = kin == COMMET_KIN_ANISOTROPIC ? 5 : 3;  // network inputs
+  if (nk == 5 && net != COMMET_NET_CANN && net != COMMET_NET_ICKAN)
+    return fail(C, COMMET_ERR_ARG, "anisotropic kinematics need a CANN or ICKAN inner network (5 inputs)");
   if (net != COMMET_NET_ICNN && net != COMMET_NET_CANN && net != COMMET_NET_GENT_THOMAS && net != COMMET_NET_ICKAN)
     return fail(C, COMMET_ERR_ARG, "network %d unknown", net);
   // analytic networks use no hidden layers (the ICNN fields are ignored)
@@ -57,8 +60,8 @@ extern "C" commet_status commet_setup(const commet_mesh_desc* mesh, const commet
     if (R < 1 || R > 4) return fail(C, COMMET_ERR_ARG, "kan_layers %d not in 1..4", R);
     if (!ncm->kan_width || !ncm->kan_grid || !ncm->kan_w || !ncm->kan_c)
       return fail(C, COMMET_ERR_ARG, "ICKAN pointer NULL (kan_width, kan_grid, kan_w or kan_c)");
-    if (ncm->kan_width[0] != 3 || ncm->kan_width[R] != 1)
-      return fail(C, COMMET_ERR_ARG, "kan_width must start at 3 inputs and end at 1 output");
+    if (ncm->kan_width[0] != nk || ncm->kan_width[R] != 1)
+      return fail(C, COMMET_ERR_ARG, "kan_width must start at %d inputs and end at 1 output", nk);
     for (int r = 0; r <= R; r++)
       if (ncm->kan_width[r] < 1 || ncm->kan_width[r] > 16)
         return fail(C, COMMET_ERR_ARG, "kan_width[%d] = %d not in 1..16", r, ncm->kan_width[r]);
@@ -74,7 +77,7 @@ extern "C" commet_status commet_setup(const commet_mesh_desc* mesh, const commet
     if (ncm->cann_n < 1 || ncm->cann_n > 16) return fail(C, COMMET_ERR_ARG, "cann_n %d not in 1..16", ncm->cann_n);
     if (!ncm->cann_f || !ncm->cann_w1 || !ncm->cann_w2)
       return fail(C, COMMET_ERR_ARG, "CANN pointer NULL (cann_f, cann_w1 or cann_w2)");
-    for (int x = 0; x < 3 * ncm->cann_n; x++) {
+    for (int x = 0; x < nk * ncm->cann_n; x++) {
       const int32_t* f = ncm->cann_f + 3 * x;
       if (f[0] < 0 || f[0] > 2 || f[1] < 1 || f[1] > 3 || f[2] < 0 || f[2] > 2)
         return fail(C, COMMET_ERR_ARG, "cann_f entry %d = (%d, %d, %d) outside the menus (f0 0..2, f1 1..3, f2 0..2)",
@@ -164,7 +167,7 @@ extern "C" commet_status commet_setup(const commet_mesh_desc* mesh, const commet
     if ((s = upload(C, c->kan_c, ncm->kan_c, (size_t)kan_edges * ncm->kan_nb, st))) return s;
   }
   if (net == COMMET_NET_CANN) {
-    const size_t nb = (size_t)3 * ncm->cann_n;
+    const size_t nb = (size_t)nk * ncm->cann_n;
     if ((s = upload(C, c->cann_f, ncm->cann_f, 3 * nb, st))) return s;
     if ((s = upload(C, c->cann_w1, ncm->cann_w1, nb, st))) return s;
     if ((s = upload(C, c->cann_w2, ncm->cann_w2, nb, st))) return s;
@@ -189,7 +192,7 @@ extern "C" commet_status commet_setup(const commet_mesh_desc* mesh, const commet
                   net == COMMET_NET_CANN ? ncm->cann_n : 0, c->cann_f.p, c->cann_w1.p, c->cann_w2.p,
                   {ncm->gt[0], ncm->gt[1], ncm->gt[2]},
                   net == COMMET_NET_ICKAN ? ncm->kan_layers : 0, net == COMMET_NET_ICKAN ? ncm->kan_nb : 0,
-                  {0, 0, 0, 0, 0}, c->kan_grid.p, c->kan_w.p, c->kan_c.p};
+                  {0, 0, 0, 0, 0}, c->kan_grid.p, c->kan_w.p, c->kan_c.p, {ncm->a0[0], ncm->a0[1], ncm->a0[2]}};
   if (net == COMMET_NET_ICKAN)
     for (int r = 0; r <= ncm->kan_layers; r++) c->ncm.kan_width[r] = ncm->kan_width[r];
   CUDA_TRY(C, c->bad.alloc(1));

@@ -41,6 +41,7 @@ struct NcmDev {
   const double* kan_grid;  // [R][2]
   const double* kan_w;     // [edges]
   const double* kan_c;     // [edges][nb]
+  double a0[3];            // anisotropic kinematics: structural vector (reference configuration)
 };
 
 struct AsmArgs {

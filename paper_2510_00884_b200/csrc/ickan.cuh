@@ -34,63 +34,66 @@ __device__ __forceinline__ void cubic_spline(const double* __restrict__ c, int n
   }
 }
 
-template <class M>
+template <int NK, class M>
 __device__ __forceinline__ double ickan_eval(const M& m, const double* kin, double* __restrict__ g,
                                              double* __restrict__ H6) {
-  constexpr int MW = 16;
-  double z[MW], dz[MW][3], hz[MW][6], y[MW], dy[MW][3], hy[MW][6];
-  int nin = 3;
-  for (int j = 0; j < 3; j++) {
+  constexpr int MW = 16, NH = NK * (NK + 1) / 2;
+  double z[MW], dz[MW][NK], hz[MW][NH], y[MW], dy[MW][NK], hy[MW][NH];
+  int nin = NK;
+  for (int j = 0; j < NK; j++) {
     z[j] = kin[j];
-    for (int p = 0; p < 3; p++) dz[j][p] = (p == j) ? 1.0 : 0.0;
-    for (int p = 0; p < 6; p++) hz[j][p] = 0.0;
+    for (int p = 0; p < NK; p++) dz[j][p] = (p == j) ? 1.0 : 0.0;
+    for (int p = 0; p < NH; p++) hz[j][p] = 0.0;
   }
   int e = 0;
   for (int r = 0; r < m.kan_R; r++) {
     const int nout = m.kan_width[r + 1];
     const double xmin = __ldg(m.kan_grid + 2 * r), xmax = __ldg(m.kan_grid + 2 * r + 1);
     for (int i = 0; i < nout; i++) {
-      double yy = 0.0, d[3] = {0.0, 0.0, 0.0}, hh[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+      double yy = 0.0, d[NK], hh[NH];
+      for (int p = 0; p < NK; p++) d[p] = 0.0;
+      for (int p = 0; p < NH; p++) hh[p] = 0.0;
       for (int j = 0; j < nin; j++, e++) {
         double v, d1, d2;
         cubic_spline(m.kan_c + (size_t)e * m.kan_nb, m.kan_nb, xmin, xmax, z[j], v, d1, d2);
         const double w = __ldg(m.kan_w + e), wd1 = w * d1, wd2 = w * d2;
         yy += w * v;
-        for (int p = 0; p < 3; p++) d[p] += wd1 * dz[j][p];
+        for (int p = 0; p < NK; p++) d[p] += wd1 * dz[j][p];
         int x = 0;
-        for (int p = 0; p < 3; p++)
-          for (int q = p; q < 3; q++, x++) hh[x] += wd2 * dz[j][p] * dz[j][q] + wd1 * hz[j][x];
+        for (int p = 0; p < NK; p++)
+          for (int q = p; q < NK; q++, x++) hh[x] += wd2 * dz[j][p] * dz[j][q] + wd1 * hz[j][x];
       }
       y[i] = yy;
-      for (int p = 0; p < 3; p++) dy[i][p] = d[p];
-      for (int p = 0; p < 6; p++) hy[i][p] = hh[p];
+      for (int p = 0; p < NK; p++) dy[i][p] = d[p];
+      for (int p = 0; p < NH; p++) hy[i][p] = hh[p];
     }
     for (int i = 0; i < nout; i++) {
       z[i] = y[i];
-      for (int p = 0; p < 3; p++) dz[i][p] = dy[i][p];
-      for (int p = 0; p < 6; p++) hz[i][p] = hy[i][p];
+      for (int p = 0; p < NK; p++) dz[i][p] = dy[i][p];
+      for (int p = 0; p < NH; p++) hz[i][p] = hy[i][p];
     }
     nin = nout;
   }
   double N = z[0];
+  for (int p = 0; p < NK; p++) g[p] = dz[0][p];
   for (int p = 0; p < 3; p++) {
-    g[p] = dz[0][p] + m.skip_out[p];
+    g[p] += m.skip_out[p];
     N += m.skip_out[p] * kin[p];
   }
-  for (int p = 0; p < 6; p++) H6[p] = hz[0][p];
+  for (int p = 0; p < NH; p++) H6[p] = hz[0][p];
   return N;
 }
 
-// analytic networks (NET = 1 path): gradient / Hessian (and value if N != nullptr)
-template <class M>
+// analytic networks (NET = 1 path) on NK inputs: gradient / packed Hessian (and value if N != nullptr)
+template <int NK = 3, class M>
 __device__ __forceinline__ void analytic_point(const M& m, const double* kin, double* g, double* H6, double* N) {
   if (m.net == 3) {
-    const double v = ickan_eval(m, kin, g, H6);
+    const double v = ickan_eval<NK>(m, kin, g, H6);
     if (N) *N = v;
     return;
   }
-  analytic_net(m.net, m.cann_n, m.cann_f, m.cann_w1, m.cann_w2, m.gt, m.skip_out, kin, g, H6);
-  if (N) *N = analytic_value(m.net, m.cann_n, m.cann_f, m.cann_w1, m.cann_w2, m.gt, m.skip_out, kin);
+  analytic_net(m.net, m.cann_n, m.cann_f, m.cann_w1, m.cann_w2, m.gt, m.skip_out, kin, g, H6, NK);
+  if (N) *N = analytic_value(m.net, m.cann_n, m.cann_f, m.cann_w1, m.cann_w2, m.gt, m.skip_out, kin, NK);
 }
 
 }  // namespace commet

@@ -102,6 +102,9 @@ __device__ __forceinline__ double2 ldg2(const double* p) {
 template <int W_, int Q_, int NEN_, int NQ_, int MINB_ = 3, int NET_ = 0, int KIN_ = 0, int MODE_ = 0>
 struct Cfg {
   static constexpr int W = W_, Q = Q_, NEN = NEN_, NQ = NQ_, NET = NET_, KIN = KIN_, MODE = MODE_;
+  // network inputs per qp: 3 (standard / isochoric invariants) or 5 (anisotropic: + I4, I5)
+  static constexpr int NK = KIN == 2 ? 5 : 3, NH = NK * (NK + 1) / 2;
+  static_assert(KIN != 2 || NET == 1, "anisotropic inputs: analytic networks only");
   static constexpr int NWARP = 4, NTHR = 128;
   static constexpr int MINB = MINB_;               // CTAs per SM the register budget targets (3: <= 168 regs)
   static constexpr bool DMMA_ELEM = MODE == 0 && (COMMET_DMMA_ELEM == 2 || (COMMET_DMMA_ELEM == 1 && NEN == 8));
@@ -134,7 +137,8 @@ struct Cfg {
 // buffers (qP, post/X, qA) alias act/s/c, which are dead after stage 6.
 template <class C>
 struct Smem {
-  static constexpr int PS = 101;  // per-qp stride of the stage-7a outputs (odd: bank spread)
+  // per-qp stride of the stage-7a outputs (odd: bank spread); anisotropic: 5 factor pairs
+  static constexpr int PS = C::KIN == 2 ? kPostAniso : 101;
   int act, sb, cb, qF, qk, qg, qH, hred, gsk, gN, ue, wq, qN, tab, qP, post, X, qA, total;
   __host__ __device__ Smem(int L) {
     int o = 0;
@@ -143,7 +147,7 @@ struct Smem {
     cb = o;  o += (L > 1 ? L - 1 : 1) * C::W * C::LDS;   // c_l, l = 2..L (L == 1: c_1)
     const int dead = o;
     qF = o;  o += C::Q * 9;
-    qk = o;  o += C::Q * 3;
+    qk = o;  o += C::Q * C::NK;
     qg = o;  o += C::Q * 3;
     qH = o;  o += C::Q * 6;
     hred = o; o += C::JMG * C::Q * 6;  // Jacobian-pass H partials per warp row group
@@ -225,8 +229,8 @@ __device__ __forceinline__ void material_outputs(const AsmArgs& A, const NcmDev&
   const int tid = threadIdx.x;
   if (tid < Q) {
     const int q = tid;
-    double gq[3], H6[6], N = 0.0;
-    const double* kq = qk + q * 3;
+    double gq[C::NK], H6[C::NH], N = 0.0;
+    const double* kq = qk + q * C::NK;
     if constexpr (C::NET == 0) {
 #pragma unroll
       for (int x = 0; x < 3; x++) gq[x] = qg[q * 3 + x];
@@ -242,7 +246,7 @@ __device__ __forceinline__ void material_outputs(const AsmArgs& A, const NcmDev&
       for (int r = 0; r < rows; r++) N += qNp[r * Q + q];
       N += __ldg(m.skip_out) * kq[0] + __ldg(m.skip_out + 1) * kq[1] + __ldg(m.skip_out + 2) * kq[2];
     } else {
-      analytic_point(m, kq, gq, H6, &N);
+      analytic_point<C::NK>(m, kq, gq, H6, &N);
     }
     Kin kin;
     kinematics(qF + q * 9, kin);
@@ -250,8 +254,11 @@ __device__ __forceinline__ void material_outputs(const AsmArgs& A, const NcmDev&
     const double jm1 = kin.J - 1.0;
     const double Wv = N + m.kappa * jm1 * jm1 - m.ref_shift * jm1;
     gq[2] += 2.0 * m.kappa * jm1 - m.ref_shift;
-    H6[5] += 2.0 * m.kappa;
-    post_qp(kin, gq, H6, 1.0, post + q * PS, qP + q * 9);
+    H6[packed_index(C::NK, 2, 2)] += 2.0 * m.kappa;
+    if constexpr (C::KIN == 2)
+      post_qp_aniso(kin, m.a0, gq, H6, 1.0, post + q * PS, qP + q * 9);
+    else
+      post_qp(kin, gq, H6, 1.0, post + q * PS, qP + q * 9);
     double tau[9];
 #pragma unroll
     for (int i = 0; i < 3; i++)
@@ -272,7 +279,10 @@ __device__ __forceinline__ void material_outputs(const AsmArgs& A, const NcmDev&
   if (!A.c_out) return;
   for (int it = tid; it < Q * 9; it += C::NTHR) {
     const int q = it / 9, iJ = it % 9;
-    tangent_row(post + q * PS, iJ, qA + q * 81 + iJ * 9);
+    if constexpr (C::KIN == 2)
+      tangent_row_aniso(post + q * PS, iJ, qA + q * 81 + iJ * 9);
+    else
+      tangent_row(post + q * PS, iJ, qA + q * 81 + iJ * 9);
   }
   __syncthreads();
   for (int it = tid; it < Q * 21; it += C::NTHR) {
@@ -453,7 +463,12 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
       }
 #pragma unroll
       for (int x = 0; x < 9; x++) qF[q * 9 + x] = F[x];
-      if constexpr (C::KIN == 1) {  // isochoric inputs (App. A.2.2)
+      if constexpr (C::KIN == 2) {  // anisotropic inputs (+ I4, I5)
+        double kb[5];
+        anisotropic_inputs(kin, m.a0, kb);
+#pragma unroll
+        for (int x = 0; x < 5; x++) qk[q * 5 + x] = kb[x];
+      } else if constexpr (C::KIN == 1) {  // isochoric inputs (App. A.2.2)
         double kb[3];
         isochoric_inputs(kin, kb);
         qk[q * 3 + 0] = kb[0];
@@ -835,7 +850,7 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
 #endif
     if (tid < Q) {
       const int q = tid;
-      double gq[3], H6[6];
+      double gq[C::NK], H6[C::NH];
       if constexpr (C::NET == 0) {
 #pragma unroll
         for (int x = 0; x < 3; x++) gq[x] = qg[q * 3 + x];
@@ -848,14 +863,17 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
           H6[x] = s;
         }
       } else {
-        analytic_point(m, qk + q * 3, gq, H6, nullptr);
+        analytic_point<C::NK>(m, qk + q * C::NK, gq, H6, nullptr);
       }
       Kin kin;
       kinematics(qF + q * 9, kin);
       if constexpr (C::KIN == 1) isochoric_to_standard(kin, gq, H6);
       gq[2] += 2.0 * m.kappa * (kin.J - 1.0) - m.ref_shift;
-      H6[5] += 2.0 * m.kappa;
-      post_qp(kin, gq, H6, swq[q], post + q * PS, qP + q * 9);
+      H6[packed_index(C::NK, 2, 2)] += 2.0 * m.kappa;
+      if constexpr (C::KIN == 2)
+        post_qp_aniso(kin, m.a0, gq, H6, swq[q], post + q * PS, qP + q * 9);
+      else
+        post_qp(kin, gq, H6, swq[q], post + q * PS, qP + q * 9);
     }
     __syncthreads();
 
@@ -863,7 +881,10 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
     // ---- stage 7b: A_q (81 entries, scaled by w), one (q, iJ) row per item ------------------
     for (int it = tid; it < Q * 9; it += C::NTHR) {
       const int q = it / 9, iJ = it % 9;
-      tangent_row(post + q * PS, iJ, qA + q * 81 + iJ * 9);
+      if constexpr (C::KIN == 2)
+        tangent_row_aniso(post + q * PS, iJ, qA + q * 81 + iJ * 9);
+      else
+        tangent_row(post + q * PS, iJ, qA + q * 81 + iJ * 9);
     }
     __syncthreads();
 
@@ -1149,7 +1170,8 @@ void fused_occupancy(int n_en, int w, int L, int* smem_bytes, int* ctas_per_sm, 
 
 template <int NEN, int NQ, int K>
 static int launch_k(const AsmArgs& a, cudaStream_t st, int* launches) {
-  if (a.ncm.net != 0) return launch_cfg<Cfg<16, 16, NEN, NQ, 3, 1, K>>(a, st, launches);
+  if (a.ncm.net != 0 || K == 2) return launch_cfg<Cfg<16, 16, NEN, NQ, 3, 1, K>>(a, st, launches);
+  if constexpr (K != 2)
   switch (a.ncm.w) {
     case 8: return launch_cfg<Cfg<8, 32, NEN, NQ, 3, 0, K>>(a, st, launches);
     case 16: return launch_cfg<Cfg<16, 16, NEN, NQ, 3, 0, K>>(a, st, launches);
@@ -1163,7 +1185,8 @@ static int launch_k(const AsmArgs& a, cudaStream_t st, int* launches) {
 // material points: NEN = NQ = 1, one "element" per point
 template <int K>
 static int launch_mat_k(const AsmArgs& a, cudaStream_t st) {
-  if (a.ncm.net != 0) return launch_cfg<Cfg<16, 16, 1, 1, 3, 1, K, 1>>(a, st, nullptr);
+  if (a.ncm.net != 0 || K == 2) return launch_cfg<Cfg<16, 16, 1, 1, 3, 1, K, 1>>(a, st, nullptr);
+  if constexpr (K != 2)
   switch (a.ncm.w) {
     case 8: return launch_cfg<Cfg<8, 32, 1, 1, 3, 0, K, 1>>(a, st, nullptr);
     case 16: return launch_cfg<Cfg<16, 16, 1, 1, 3, 0, K, 1>>(a, st, nullptr);
@@ -1177,11 +1200,12 @@ static int launch_mat_k(const AsmArgs& a, cudaStream_t st) {
 int launch_material(const AsmArgs& a, void* stream) {
   if (a.el_count <= 0) return 0;
   cudaStream_t st = (cudaStream_t)stream;
-  return a.ncm.kin == 1 ? launch_mat_k<1>(a, st) : launch_mat_k<0>(a, st);
+  return a.ncm.kin == 2 ? launch_mat_k<2>(a, st) : a.ncm.kin == 1 ? launch_mat_k<1>(a, st) : launch_mat_k<0>(a, st);
 }
 
 template <int NEN, int NQ>
 static int launch_et(const AsmArgs& a, cudaStream_t st, int* launches) {
+  if (a.ncm.kin == 2) return launch_k<NEN, NQ, 2>(a, st, launches);
   return a.ncm.kin == 1 ? launch_k<NEN, NQ, 1>(a, st, launches) : launch_k<NEN, NQ, 0>(a, st, launches);
 }
 

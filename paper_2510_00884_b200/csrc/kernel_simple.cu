@@ -42,15 +42,20 @@ __global__ void __launch_bounds__(64) simple_kernel(AsmArgs A) {
     kinematics(F, kin);
     if (!(kin.J > 0.0)) atomicMin(A.bad, (unsigned long long)(A.orig[e] * nq + q));
     trc = fmax(trc, kin.I1);
-    double kv[3] = {kin.I1 - 3.0, kin.I2 - 3.0, kin.J - 1.0};
+    double kv[5] = {kin.I1 - 3.0, kin.I2 - 3.0, kin.J - 1.0, 0.0, 0.0};
     if (A.ncm.kin == 1) isochoric_inputs(kin, kv);
-    double g[3], H6[6];
+    if (A.ncm.kin == 2) anisotropic_inputs(kin, A.ncm.a0, kv);
+    double g[5], H6[15];
     ncm_point(A.ncm, kv, g, H6);
     if (A.ncm.kin == 1) isochoric_to_standard(kin, g, H6);
+    const int nk = A.ncm.kin == 2 ? 5 : 3;
     g[2] += 2.0 * A.ncm.kappa * (kin.J - 1.0) - A.ncm.ref_shift;
-    H6[5] += 2.0 * A.ncm.kappa;
+    H6[packed_index(nk, 2, 2)] += 2.0 * A.ncm.kappa;
     double P[9], Am[81];
-    stress_tangent(kin, g, H6, w, P, Am);
+    if (A.ncm.kin == 2)
+      stress_tangent_aniso(kin, A.ncm.a0, g, H6, w, P, Am);
+    else
+      stress_tangent(kin, g, H6, w, P, Am);
     for (int a = 0; a < nen; a++) {
       const double* ga = gN + a * 3;
       for (int i = 0; i < 3; i++) re[a * 3 + i] += P[i * 3 + 0] * ga[0] + P[i * 3 + 1] * ga[1] + P[i * 3 + 2] * ga[2];

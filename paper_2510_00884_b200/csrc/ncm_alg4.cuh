@@ -68,12 +68,15 @@ __device__ __forceinline__ void ncm_alg4(const NcmDev& m, const double* kin, dou
   }
 }
 
-// the ctx's inner network at inputs k: Alg. 4 for the ICNN, closed forms for CANN / Gent-Thomas
+// the ctx's inner network at its inputs k (3, or 5 for anisotropic kinematics): Alg. 4 for the
+// ICNN, closed forms for CANN / Gent-Thomas / ICKAN; H6 = packed upper triangle of the Hessian
 __device__ __forceinline__ void ncm_point(const NcmDev& m, const double* kin, double* g, double* H6) {
   if (m.net == 0)
     ncm_alg4(m, kin, g, H6);
+  else if (m.kin == 2)
+    analytic_point<5>(m, kin, g, H6, nullptr);
   else
-    analytic_point(m, kin, g, H6, nullptr);
+    analytic_point<3>(m, kin, g, H6, nullptr);
 }
 
 }  // namespace commet

@@ -152,6 +152,140 @@ __device__ __forceinline__ void stress_tangent(const Kin& k, const double* __res
 }
 
 // ---------------------------------------------------------------------------
+// anisotropic inputs (App. A.2.1): one structural vector A0,
+//   K = (I1-3, I2-3, J-1, I4-1, I5-1),  I4 = A0.C A0,  I5 = A0.C^2 A0 = |C A0|^2.
+// Tangent: the F-space factors above extended by Phi_4 = F h4 = a (x) A0 (a = F A0) and
+// Phi_5 = F h5 = a (x) C A0 + F C A0 (x) A0, plus the second-derivative term of I5,
+//   4 g5 F_iI HH5_IJKL F_kK = 2 g5 (a_i F_kJ A0_L + a_i a_k d_JL + b_ik A0_J A0_L + F_iL a_k A0_J)
+// (HH4 = 0).  H6 below is the packed upper triangle of the 5x5 Hessian (15 entries).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void anisotropic_inputs(const Kin& k, const double* a0, double kk[5]) {
+  double CA[3];
+#pragma unroll
+  for (int I = 0; I < 3; I++) CA[I] = k.C[I * 3] * a0[0] + k.C[I * 3 + 1] * a0[1] + k.C[I * 3 + 2] * a0[2];
+  kk[0] = k.I1 - 3.0;
+  kk[1] = k.I2 - 3.0;
+  kk[2] = k.J - 1.0;
+  kk[3] = a0[0] * CA[0] + a0[1] * CA[1] + a0[2] * CA[2] - 1.0;
+  kk[4] = CA[0] * CA[0] + CA[1] * CA[1] + CA[2] * CA[2] - 1.0;
+}
+
+__host__ __device__ constexpr int packed_index(int n, int p, int q) { return p * n - p * (p - 1) / 2 + (q - p); }
+
+// post layout (per qp, PSA = 137): [0..8] F, [9..17] F^-T, [18..26] w T, [27..71] Phi_1..5,
+// [72..116] Psi_m = 4w sum_n H'_mn Phi_n, [117..125] b, [126] c2 = -2 g2 w, [127] c3 = -g3 J w,
+// [128..130] a = F A0, [131..133] A0, [134] c5 = 2 g5 w;  P[9] = w F S.
+constexpr int kPostAniso = 137;
+__device__ __forceinline__ void post_qp_aniso(const Kin& k, const double* a0, const double* __restrict__ g,
+                                              const double* __restrict__ H15, double w, double* __restrict__ post,
+                                              double* __restrict__ P) {
+  const double* F = k.F;
+  const double hJ = 0.5 * k.J;
+  double CA[3], a[3], FCA[3];
+#pragma unroll
+  for (int I = 0; I < 3; I++) CA[I] = k.C[I * 3] * a0[0] + k.C[I * 3 + 1] * a0[1] + k.C[I * 3 + 2] * a0[2];
+#pragma unroll
+  for (int i = 0; i < 3; i++) {
+    a[i] = F[i * 3] * a0[0] + F[i * 3 + 1] * a0[1] + F[i * 3 + 2] * a0[2];
+    FCA[i] = F[i * 3] * CA[0] + F[i * 3 + 1] * CA[1] + F[i * 3 + 2] * CA[2];
+  }
+  double S[9];
+#pragma unroll
+  for (int I = 0; I < 3; I++)
+#pragma unroll
+    for (int J = 0; J < 3; J++) {
+      const double d = (I == J) ? 1.0 : 0.0;
+      S[I * 3 + J] = 2.0 * (g[0] * d + g[1] * (k.I1 * d - k.C[I * 3 + J]) + g[2] * hJ * k.Ci[I * 3 + J] +
+                            g[3] * a0[I] * a0[J] + g[4] * (a0[I] * CA[J] + CA[I] * a0[J]));
+      post[18 + I * 3 + J] = w * (S[I * 3 + J] - g[2] * k.J * k.Ci[I * 3 + J]);
+    }
+  double Phi[5][9];
+#pragma unroll
+  for (int i = 0; i < 3; i++)
+#pragma unroll
+    for (int J = 0; J < 3; J++) {
+      const double FC = F[i * 3 + 0] * k.C[0 * 3 + J] + F[i * 3 + 1] * k.C[1 * 3 + J] + F[i * 3 + 2] * k.C[2 * 3 + J];
+      Phi[0][i * 3 + J] = F[i * 3 + J];
+      Phi[1][i * 3 + J] = k.I1 * F[i * 3 + J] - FC;
+      Phi[2][i * 3 + J] = hJ * k.FiT[i * 3 + J];
+      Phi[3][i * 3 + J] = a[i] * a0[J];
+      Phi[4][i * 3 + J] = a[i] * CA[J] + FCA[i] * a0[J];
+    }
+  double Hp[25];
+#pragma unroll
+  for (int p = 0; p < 5; p++)
+#pragma unroll
+    for (int q = 0; q < 5; q++) Hp[p * 5 + q] = H15[p <= q ? packed_index(5, p, q) : packed_index(5, q, p)];
+  Hp[0] += g[1];
+  Hp[12] += g[2] / k.J;
+  const double w4 = 4.0 * w;
+#pragma unroll
+  for (int x = 0; x < 9; x++) {
+    post[x] = F[x];
+    post[9 + x] = k.FiT[x];
+#pragma unroll
+    for (int m = 0; m < 5; m++) {
+      post[27 + m * 9 + x] = Phi[m][x];
+      double t = 0.0;
+#pragma unroll
+      for (int n = 0; n < 5; n++) t += Hp[m * 5 + n] * Phi[n][x];
+      post[72 + m * 9 + x] = w4 * t;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 3; i++)
+#pragma unroll
+    for (int kk = 0; kk < 3; kk++)
+      post[117 + i * 3 + kk] = F[i * 3 + 0] * F[kk * 3 + 0] + F[i * 3 + 1] * F[kk * 3 + 1] + F[i * 3 + 2] * F[kk * 3 + 2];
+  post[126] = -2.0 * g[1] * w;
+  post[127] = -g[2] * k.J * w;
+#pragma unroll
+  for (int i = 0; i < 3; i++) {
+    post[128 + i] = a[i];
+    post[131 + i] = a0[i];
+  }
+  post[134] = 2.0 * g[4] * w;
+#pragma unroll
+  for (int i = 0; i < 3; i++)
+#pragma unroll
+    for (int J = 0; J < 3; J++)
+      P[i * 3 + J] = w * (F[i * 3 + 0] * S[0 * 3 + J] + F[i * 3 + 1] * S[1 * 3 + J] + F[i * 3 + 2] * S[2 * 3 + J]);
+}
+
+__device__ __forceinline__ void tangent_row_aniso(const double* __restrict__ post, int iJ, double* __restrict__ out) {
+  const int i = iJ / 3, J = iJ % 3;
+  double p[5];
+#pragma unroll
+  for (int m = 0; m < 5; m++) p[m] = post[27 + m * 9 + iJ];
+  const double c2 = post[126], c3 = post[127], c5 = post[134];
+  const double ai = post[128 + i], A0J = post[131 + J];
+#pragma unroll
+  for (int kk = 0; kk < 3; kk++) {
+    const double FkJ = post[kk * 3 + J], GkJ = post[9 + kk * 3 + J], ak = post[128 + kk], bik = post[117 + i * 3 + kk];
+#pragma unroll
+    for (int L = 0; L < 3; L++) {
+      const int kL = kk * 3 + L;
+      double v = 0.0;
+#pragma unroll
+      for (int m = 0; m < 5; m++) v += p[m] * post[72 + m * 9 + kL];
+      v += c2 * post[i * 3 + L] * FkJ + c3 * post[9 + i * 3 + L] * GkJ;
+      const double A0L = post[131 + L];
+      v += c5 * (ai * FkJ * A0L + bik * A0J * A0L + post[i * 3 + L] * ak * A0J);
+      if (J == L) v += c2 * bik + c5 * ai * ak;
+      if (i == kk) v += post[18 + J * 3 + L];
+      out[kL] = v;
+    }
+  }
+}
+
+__device__ __forceinline__ void stress_tangent_aniso(const Kin& k, const double* a0, const double* g,
+                                                     const double* H15, double w, double* P, double* A) {
+  double post[kPostAniso];
+  post_qp_aniso(k, a0, g, H15, w, post, P);
+  for (int iJ = 0; iJ < 9; iJ++) tangent_row_aniso(post, iJ, A + iJ * 9);
+}
+
+// ---------------------------------------------------------------------------
 // kinematic variant: isochoric inputs (App. A.2.2)
 //   kbar = (Ibar1 - 3, Ibar2 - 3, J - 1),  Ibar1 = J^-2/3 I1,  Ibar2 = J^-4/3 I2.
 // The network's (gbar, Hbar) w.r.t. kbar are carried to (g, H) w.r.t. the standard
@@ -192,10 +326,13 @@ __device__ __forceinline__ void isochoric_to_standard(const Kin& k, double* __re
 // analytic inner networks: gradient and Hessian w.r.t. the inputs
 //  CANN (Eq. cann-def / cann-chain-rule): diagonal Hessian
 //  Gent-Thomas (App. C): N = gt0 k1 + gt1 ln(1 + k2/3) + gt2 k3^2
+// nk network inputs (3, or 5 for anisotropic kinematics; Gent-Thomas: 3); H6 packed upper
+// triangle of the nk x nk Hessian
 __device__ __forceinline__ void analytic_net(int net, int n, const int32_t* __restrict__ f,
                                              const double* __restrict__ w1, const double* __restrict__ w2,
                                              const double* __restrict__ gt, const double* __restrict__ skip,
-                                             const double* kin, double* __restrict__ g, double* __restrict__ H6) {
+                                             const double* kin, double* __restrict__ g, double* __restrict__ H6,
+                                             int nk = 3) {
   if (net == 2) {
     const double u = 1.0 / (kin[1] + 3.0);
     g[0] = gt[0];
@@ -206,10 +343,10 @@ __device__ __forceinline__ void analytic_net(int net, int n, const int32_t* __re
     H6[5] = 2.0 * gt[2];
     return;
   }
-  double hd[3];
-  for (int m = 0; m < 3; m++) {
+  for (int x = 0; x < nk * (nk + 1) / 2; x++) H6[x] = 0.0;
+  for (int m = 0; m < nk; m++) {
     const double x = kin[m];
-    double gm = skip[m], hm = 0.0;
+    double gm = m < 3 ? skip[m] : 0.0, hm = 0.0;
     for (int bb = 0; bb < n; bb++) {
       const int32_t* fb = f + (m * n + bb) * 3;
       const int t0 = __ldg(fb), p = __ldg(fb + 1), t2 = __ldg(fb + 2);
@@ -240,22 +377,18 @@ __device__ __forceinline__ void analytic_net(int net, int n, const int32_t* __re
       hm += a2 * (dd2 * d1 * d1 + d2 * dd1) * d0 * d0;
     }
     g[m] = gm;
-    hd[m] = hm;
+    H6[m * nk - m * (m - 1) / 2] = hm;  // diagonal (m, m) of the packed triangle
   }
-  H6[0] = hd[0];
-  H6[3] = hd[1];
-  H6[5] = hd[2];
-  H6[1] = H6[2] = H6[4] = 0.0;
 }
 
 // value of the analytic networks (material-point outputs): same closed forms as above
 __device__ __forceinline__ double analytic_value(int net, int n, const int32_t* __restrict__ f,
                                                  const double* __restrict__ w1, const double* __restrict__ w2,
                                                  const double* __restrict__ gt, const double* __restrict__ skip,
-                                                 const double* kin) {
+                                                 const double* kin, int nk = 3) {
   if (net == 2) return gt[0] * kin[0] + gt[1] * log1p(kin[1] / 3.0) + gt[2] * kin[2] * kin[2];
   double N = skip[0] * kin[0] + skip[1] * kin[1] + skip[2] * kin[2];
-  for (int m = 0; m < 3; m++) {
+  for (int m = 0; m < nk; m++) {
     const double x = kin[m];
     for (int bb = 0; bb < n; bb++) {
       const int32_t* fb = f + (m * n + bb) * 3;

@@ -249,22 +249,28 @@ def ncm_weights(width: int, n_hidden: int, std: float = 0.3, seed: int = SEED_W,
 
 
 def cann_params(n_branch: int = 4, seed: int = SEED_W, kinematics: str = "standard", kappa: float = 10.0,
-                std: float = 0.3) -> dict:
+                std: float = 0.3, n_in: int = 3) -> dict:
     """CANN (Eq. cann-def) parameters: per kinematic input m and branch b the
     activation triple (f0, f1 power, f2) cycles through the paper's menus
     (f0: identity, Macaulay, abs; f1: powers 1..3; f2: linear, exp - 1, -ln(1 - .))
     with a seeded offset; w1 ~ U(0.05, 0.3) (keeps 1 - w1 x > 0 on the benchmark
     ranges), w2 ~ |N(0, std^2)|."""
     rng = np.random.default_rng(seed)
-    f = np.empty((3, n_branch, 3), np.int32)
+    f = np.empty((n_in, n_branch, 3), np.int32)
     off = rng.integers(0, 3, size=3)
-    for m in range(3):
+    for m in range(n_in):
         for b in range(n_branch):
             f[m, b] = ((b + off[0] + m) % 3, 1 + (b + off[1]) % 3, (b + off[2] + 2 * m) % 3)
-    w1 = rng.uniform(0.05, 0.3, size=(3, n_branch))
-    w2 = np.abs(rng.normal(0.0, std, size=(3, n_branch)))
+    w1 = rng.uniform(0.05, 0.3, size=(n_in, n_branch))
+    w2 = np.abs(rng.normal(0.0, std, size=(n_in, n_branch)))
     return dict(network="cann", kinematics=kinematics, width=8, n_hidden=1, W1=None, W=None, b=None, a=None,
                 skip_out=None, skip_hidden=None, cann_f=f, cann_w1=w1, cann_w2=w2, kappa=float(kappa), ref_shift=0.0)
+
+
+def anisotropic(ncm: dict, a0=(0.6, 0.8, 0.0)) -> dict:
+    """The same network on anisotropic inputs K = (I1-3, I2-3, J-1, I4-1, I5-1) with one
+    structural vector A0 (unit; reference configuration)."""
+    return dict(ncm, kinematics="anisotropic", a0=np.array(a0, np.float64))
 
 
 def gent_thomas_params(coef=(0.5, 1.0, 1.0), kappa: float = 0.0) -> dict:

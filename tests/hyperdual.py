@@ -76,7 +76,7 @@ def _cann_hd(k, ncm):
     """N = sum_m sum_b w2 f2(f1(f0(K_m))) written from Eq. cann-def / cann-fs."""
     f, w1, w2 = ncm["cann_f"], ncm["cann_w1"], ncm["cann_w2"]
     N = HD(0.0)
-    for m in range(3):
+    for m in range(len(k)):
         for b in range(f.shape[1]):
             t0, p, t2 = f[m, b]
             x = k[m]
@@ -159,6 +159,12 @@ def energy_hd(F: list, ncm: dict):
     J = (F[0][0] * F[1][1] * F[2][2] + F[0][1] * F[1][2] * F[2][0] + F[0][2] * F[1][0] * F[2][1]
          - F[0][2] * F[1][1] * F[2][0] - F[0][0] * F[1][2] * F[2][1] - F[0][1] * F[1][0] * F[2][2])
     k = [I1 - 3.0, I2 - 3.0, J - 1.0]
+    if ncm.get("kinematics", "standard") == "anisotropic":
+        a0 = ncm["a0"]
+        CA = [sum((Cm[I][J] * a0[J] for J in range(3)), HD(0.0)) for I in range(3)]
+        I4 = sum((a0[I] * CA[I] for I in range(3)), HD(0.0))
+        I5 = sum((CA[I] * CA[I] for I in range(3)), HD(0.0))
+        k = [I1 - 3.0, I2 - 3.0, J - 1.0, I4 - 1.0, I5 - 1.0]
     if ncm.get("kinematics", "standard") == "isochoric":
         a23 = hd_pow(J, -2.0 / 3.0)
         k = [a23 * I1 - 3.0, a23 * a23 * I2 - 3.0, J - 1.0]

@@ -7,7 +7,7 @@ import numpy as np
 import pytest
 
 import oracle
-from synth.gen import cann_params, gent_thomas_params, ickan_params, ncm_weights
+from synth.gen import anisotropic, cann_params, gent_thomas_params, ickan_params, ncm_weights
 from tests.test_oracle_material import rand_F
 from tests.test_oracle_variants import isochoric_icnn
 
@@ -41,6 +41,7 @@ MODELS = {
     "cann": lambda: cann_params(4, seed=3),
     "gent_thomas": gent_thomas_params,
     "ickan": lambda: ickan_params(),
+    "cann_anisotropic": lambda: anisotropic(cann_params(4, seed=6, n_in=5)),
 }
 
 

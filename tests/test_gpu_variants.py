@@ -7,8 +7,8 @@ import pytest
 
 import oracle
 from oracle import newton as on
-from synth.gen import (HEX8, TET10, cann_params, gent_thomas_params, hex_mesh, ickan_params, ncm_weights,
-                       shape_gradients, smooth_field, tet10_mesh)
+from synth.gen import (HEX8, TET10, anisotropic, cann_params, gent_thomas_params, hex_mesh, ickan_params,
+                       ncm_weights, shape_gradients, smooth_field, tet10_mesh)
 
 pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")
@@ -38,6 +38,8 @@ VARIANTS = {
     "icnn_isochoric_64x3": lambda: _iso_icnn(64, 3),
     "ickan": lambda: ickan_params(),
     "ickan_isochoric": lambda: ickan_params((3, 5, 1), nb=7, seed=5, kinematics="isochoric"),
+    "cann_anisotropic": lambda: anisotropic(cann_params(4, seed=6, n_in=5)),
+    "ickan_anisotropic": lambda: anisotropic(ickan_params((5, 4, 1), nb=7, seed=7)),
 }
 
 
@@ -71,19 +73,28 @@ def test_variant_assembly_matches_oracle(pc, name, elem_type, n, kernel):
     assert _rel(r.cpu().numpy(), ro) <= TOL and _rel(v.cpu().numpy(), vo) <= TOL
 
 
-@pytest.mark.parametrize("name", ["gent_thomas", "cann_standard", "cann_isochoric", "ickan"])
+@pytest.mark.parametrize("name", ["gent_thomas", "cann_standard", "cann_isochoric", "ickan", "cann_anisotropic",
+                                  "ickan_anisotropic"])
 def test_analytic_ncm_eval_matches_oracle(pc, name):
     ncm = VARIANTS[name]()
+    nk = 5 if ncm.get("kinematics") == "anisotropic" else 3
     mesh, _ = _mesh(HEX8, 1)
     lib = pc.Commet(mesh, ncm)
     rng = np.random.default_rng(12)
-    k = rng.uniform(-0.4, 0.4, size=(25, 3))
+    k = rng.uniform(-0.4, 0.4, size=(25, nk))
     g, H = lib.ncm_eval(torch.from_numpy(k).cuda())
     g, H = g.cpu().numpy(), H.cpu().numpy()
     for i in range(k.shape[0]):
-        _, go, Ho = oracle.ncm_eval(dict(ncm, kappa=0.0), k[i])
+        _, go, Ho = oracle.ncm_eval_n(dict(ncm, kappa=0.0), k[i])
         assert np.abs(g[i] - go).max() <= 1e-14 * max(1.0, np.abs(go).max())
-        assert np.abs(H[i] - Ho[np.triu_indices(3)]).max() <= 1e-14 * max(1.0, np.abs(Ho).max())
+        assert np.abs(H[i] - Ho[np.triu_indices(nk)]).max() <= 1e-14 * max(1.0, np.abs(Ho).max())
+
+
+def test_normalize_reference_rejects_anisotropic(pc):
+    mesh, _ = _mesh(HEX8, 1)
+    lib = pc.Commet(mesh, VARIANTS["cann_anisotropic"]())
+    with pytest.raises(pc.CommetError):
+        lib.normalize_reference()
 
 
 @pytest.mark.parametrize("name", ["gent_thomas", "icnn_isochoric_16x2", "cann_isochoric", "ickan"])

@@ -9,7 +9,8 @@ import numpy as np
 import pytest
 
 import oracle
-from synth.gen import cann_params, gent_thomas_params, hex_mesh, ickan_params, ncm_weights, shape_gradients
+from synth.gen import (anisotropic, cann_params, gent_thomas_params, hex_mesh, ickan_params, ncm_weights,
+                       shape_gradients)
 from tests import hyperdual
 from tests.test_oracle_material import I3, rand_F, rot
 
@@ -27,6 +28,8 @@ VARIANTS = {
     "icnn_isochoric": isochoric_icnn,
     "ickan": lambda: ickan_params(),
     "ickan_isochoric": lambda: ickan_params((3, 5, 1), nb=7, seed=5, kinematics="isochoric"),
+    "cann_anisotropic": lambda: anisotropic(cann_params(4, seed=6, n_in=5)),
+    "ickan_anisotropic": lambda: anisotropic(ickan_params((5, 4, 1), nb=7, seed=7)),
 }
 
 
@@ -153,3 +156,28 @@ def test_ickan_convex_in_inputs():
     for _ in range(20):
         _, g, H = oracle.ncm_eval(m, rng.uniform(-0.8, 0.8, 3))
         assert np.linalg.eigvalsh(H).min() >= -1e-14 and (g >= 0).all()
+
+
+# ---- anisotropic I4 / I5 -----------------------------------------------------------------
+def test_anisotropic_invariants_values():
+    """I4 = A0.C A0 and I5 = A0.C^2 A0 (App. A.2.1) on closed forms: a stretch lambda along A0
+    gives I4 = lambda^2, I5 = lambda^4; a rotation leaves both at 1 (k4 = k5 = 0)."""
+    a0 = np.array([0.6, 0.8, 0.0])
+    m = anisotropic(cann_params(3, seed=1, n_in=5), a0)
+    lam = 1.3
+    F = np.eye(3) + (lam - 1.0) * np.outer(a0, a0)
+    k5 = np.array([np.trace(F.T @ F) - 3.0, 0.0, np.linalg.det(F) - 1.0, lam ** 2 - 1.0, lam ** 4 - 1.0])
+    C = F.T @ F
+    k5[1] = 0.5 * (np.trace(C) ** 2 - np.trace(C @ C)) - 3.0
+    _, g_ref, _ = oracle.ncm_eval_n(m, k5)
+    o = oracle.material_point(dict(m, kappa=0.0), F)
+    # S from the definition: S = 2 sum_m g_m dK_m/dC, dI4/dC = A0 A0, dI5/dC = A0 (C A0) + (C A0) A0
+    Ci = np.linalg.inv(C)
+    h = [np.eye(3), np.trace(C) * np.eye(3) - C, 0.5 * np.linalg.det(F) * Ci, np.outer(a0, a0),
+         np.outer(a0, C @ a0) + np.outer(C @ a0, a0)]
+    S = 2 * sum(g_ref[i] * h[i] for i in range(5))
+    assert np.abs(o["S"] - S).max() < 1e-13 * np.abs(S).max()
+    Q, _ = np.linalg.qr(np.random.default_rng(2).normal(size=(3, 3)))
+    Q *= np.sign(np.linalg.det(Q))
+    o = oracle.material_point(dict(m, kappa=0.0), Q)
+    assert np.abs(o["k"]).max() < 1e-14

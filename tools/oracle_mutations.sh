@@ -42,5 +42,8 @@ mut "H[mm * 3 + mm] += w2 * ((dd2 * d1 * d1 + d2 * dd1) * d0 * d0" "H[mm * 3 + m
 mut "H[4] = -m->gt[1] / ((K[1] + 3.0) * (K[1] + 3.0));" "H[4] = m->gt[1] / ((K[1] + 3.0) * (K[1] + 3.0));"
 # ICKAN: De Boor recursion and spline derivatives
 mut "if (t[i + p + 1] > t[i + 1]) v += (t[i + p + 1] - x) / (t[i + p + 1] - t[i + 1]) * B[(p - 1) * nt + i + 1];" "if (t[i + p + 1] > t[i + 1]) v += (t[i + p + 1] - x) / (t[i + p + 1] - t[i]) * B[(p - 1) * nt + i + 1];"
-mut "for (int q = 0; q < 3; q++) d2y[i][p * 3 + q] += w * (d2 * dz[j][p] * dz[j][q] + d1 * d2z[j][p * 3 + q]);" "for (int q = 0; q < 3; q++) d2y[i][p * 3 + q] += w * (d2 * dz[j][p] * dz[j][q]);"
+mut "for (int q = 0; q < nk; q++) d2y[i][p * nk + q] += w * (d2 * dz[j][p] * dz[j][q] + d1 * d2z[j][p * nk + q]);" "for (int q = 0; q < nk; q++) d2y[i][p * nk + q] += w * (d2 * dz[j][p] * dz[j][q]);"
+# anisotropic I4 / I5 (the paper's G-tensor table)
+mut "G[4][i * 3 + j] = a[i] * Ba[j] + Ba[i] * a[j];  /* 2 sym(a (x) B a) */" "G[4][i * 3 + j] = a[i] * Ba[j] + B[i * 3 + j];"
+mut "GG[4][x] = 0.5 * (B[i * 3 + k] * A[j * 3 + l] + B[i * 3 + l] * A[j * 3 + k]) +" "GG[4][x] = 0.5 * (B[i * 3 + k] * A[j * 3 + l] + B[i * 3 + l] * A[j * 3 + k]) * 0.0 +"
 exit $fail
