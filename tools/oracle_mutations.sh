@@ -38,7 +38,7 @@ mut "GGb[1][I4(i, j, k, l)] = Bb[i * 3 + j] * Bb[k * 3 + l] -" "GGb[1][I4(i, j, 
 mut "e[mm] * ((i == j) * Gb[mm][k * 3 + l] + Gb[mm][i * 3 + j] * (k == l)" "e[mm] * ((i == j) * Gb[mm][k * 3 + l]"
 mut "t += Fi[I * 3 + i] * Fi[J * 3 + j] * Fi[K * 3 + k] * Fi[L * 3 + l] * c[I4(i, j, k, l)];" "t += Fi[I * 3 + i] * Fi[J * 3 + j] * Fi[K * 3 + l] * Fi[L * 3 + k] * c[I4(i, j, k, l)] * 1.0000001;"
 mut "dd2 = w1 * w1 / ((1.0 - w1 * v1) * (1.0 - w1 * v1));" "dd2 = -w1 * w1 / ((1.0 - w1 * v1) * (1.0 - w1 * v1));"
-mut "H[mm * 3 + mm] += w2 * ((dd2 * d1 * d1 + d2 * dd1) * d0 * d0" "H[mm * 3 + mm] += w2 * ((dd2 * d1 + d2 * dd1) * d0 * d0"
+mut "H[mm * nin + mm] += w2 * ((dd2 * d1 * d1 + d2 * dd1) * d0 * d0" "H[mm * nin + mm] += w2 * ((dd2 * d1 + d2 * dd1) * d0 * d0"
 mut "H[4] = -m->gt[1] / ((K[1] + 3.0) * (K[1] + 3.0));" "H[4] = m->gt[1] / ((K[1] + 3.0) * (K[1] + 3.0));"
 # ICKAN: De Boor recursion and spline derivatives
 mut "if (t[i + p + 1] > t[i + 1]) v += (t[i + p + 1] - x) / (t[i + p + 1] - t[i + 1]) * B[(p - 1) * nt + i + 1];" "if (t[i + p + 1] > t[i + 1]) v += (t[i + p + 1] - x) / (t[i + p + 1] - t[i]) * B[(p - 1) * nt + i + 1];"
