@@ -99,13 +99,13 @@ __device__ __forceinline__ double2 ldg2(const double* p) {
 // Gent-Thomas, evaluated per qp in stage 7a; W is then unused).  KIN_: 0 standard
 // invariants, 1 isochoric (compile-time, so the standard path carries no extra code)
 // MODE_: 0 = FE assembly; 1 = material points (F in; Psi, tau, c out; NEN = NQ = 1)
-template <int W_, int Q_, int NEN_, int NQ_, int MINB_ = 3, int NET_ = 0, int KIN_ = 0, int MODE_ = 0>
+template <int W_, int Q_, int NEN_, int NQ_, int MINB_ = 3, int NET_ = 0, int KIN_ = 0, int MODE_ = 0, int NW_ = 4>
 struct Cfg {
   static constexpr int W = W_, Q = Q_, NEN = NEN_, NQ = NQ_, NET = NET_, KIN = KIN_, MODE = MODE_;
   // network inputs per qp: 3 (standard / isochoric invariants) or 5 (anisotropic: + I4, I5)
   static constexpr int NK = KIN == 2 ? 5 : 3, NH = NK * (NK + 1) / 2;
   static_assert(KIN != 2 || NET == 1, "anisotropic inputs: analytic networks only");
-  static constexpr int NWARP = 4, NTHR = 128;
+  static constexpr int NWARP = NW_, NTHR = 32 * NW_;
   static constexpr int MINB = MINB_;               // CTAs per SM the register budget targets (3: <= 168 regs)
   static constexpr bool DMMA_ELEM = MODE == 0 && (COMMET_DMMA_ELEM == 2 || (COMMET_DMMA_ELEM == 1 && NEN == 8));
   static constexpr int E = Q / NQ;                 // elements per CTA iteration
