@@ -190,6 +190,9 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--exchange", default="nccl", choices=["nccl", "peer"],
+                    help="N > 1: interface rows over NCCL send/recv + unpack (default), or added straight "
+                         "into the owner's buffers by the kernels over NVLink P2P (CUDA IPC)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -220,6 +223,9 @@ def main():
     u_host = torch.from_numpy(cfg["u"]).pin_memory()
     u = u_host.to(dev)
     r, v = lib.alloc_outputs()
+    peer = ws > 1 and args.exchange == "peer"
+    if peer:  # the kernels add halo rows into the owners' (r, v) over NVLink; barriers inside assemble
+        pc.setup_peer_exchange(lib, r, v, rank, ws)
     lib.set_timing(args.steps)
 
     # warm-up + correctness gate (det F > 0 everywhere)
@@ -254,10 +260,17 @@ def main():
     if not args.no_e2e:
         r_host = torch.empty(r.numel(), dtype=torch.float64).pin_memory()
         v_host = torch.empty(v.numel(), dtype=torch.float64).pin_memory()
-        sets = [(r, v), lib.alloc_outputs()]
-        copy_stream = torch.cuda.Stream(dev)
+        # peer mode: the peers hold this rank's registered (r, v), so one output set (the
+        # read-back of step s finishes before step s+1 assembles)
+        sets = [(r, v), (r, v) if peer else lib.alloc_outputs()]
+        # the read-back is split over NCS copy streams (chunks of the CSR values round-robin):
+        # one cudaMemcpyAsync uses one copy engine, several keep the host link busier
+        NCS = int(os.environ.get("COMMET_E2E_STREAMS", "2"))
+        copy_streams = [torch.cuda.Stream(dev) for _ in range(NCS)]
         done_c = [torch.cuda.Event(), torch.cuda.Event()]
-        done_d = [torch.cuda.Event(), torch.cuda.Event()]
+        done_d = [[torch.cuda.Event() for _ in range(NCS)] for _ in range(2)]
+        nchunk = 4 * NCS
+        vchunks = [(i * v.numel() // nchunk, (i + 1) * v.numel() // nchunk) for i in range(nchunk)]
         if ws > 1:
             dist.barrier()
         torch.cuda.synchronize()
@@ -266,16 +279,25 @@ def main():
         for s_ in range(args.steps):
             k = s_ % 2
             if s_ >= 2:
-                stream.wait_event(done_d[k])
+                for ev in done_d[k]:
+                    stream.wait_event(ev)
+            if peer and s_ >= 1:  # single output set: the previous read-back must be done
+                for ev in done_d[1 - k]:
+                    stream.wait_event(ev)
             u.copy_(u_host, non_blocking=True)
             lib.assemble(u, *sets[k])
             done_c[k].record(stream)
-            copy_stream.wait_event(done_c[k])
-            with torch.cuda.stream(copy_stream):
+            for cs in copy_streams:
+                cs.wait_event(done_c[k])
+            with torch.cuda.stream(copy_streams[0]):
                 r_host.copy_(sets[k][0], non_blocking=True)
-                v_host.copy_(sets[k][1], non_blocking=True)
-            done_d[k].record(copy_stream)
-        stream.wait_stream(copy_stream)
+            for ci, (a0, a1) in enumerate(vchunks):
+                with torch.cuda.stream(copy_streams[ci % NCS]):
+                    v_host[a0:a1].copy_(sets[k][1][a0:a1], non_blocking=True)
+            for ci, cs in enumerate(copy_streams):
+                done_d[k][ci].record(cs)
+        for cs in copy_streams:
+            stream.wait_stream(cs)
         f1.record(stream)
         torch.cuda.synchronize()
         ms_e2e = f0.elapsed_time(f1) / args.steps
@@ -286,8 +308,8 @@ def main():
         e2e = dict(value=spec_total_qp(args.config, n_el, n_q, ws) / (ms_e2e * 1e-3), unit="qp/s",
                    h2d_bytes_per_step=u_host.numel() * 8, d2h_bytes_per_step=(r.numel() + v.numel()) * 8,
                    ms_per_step=ms_e2e,
-                   note="pinned host buffers; D2H of step s overlaps the assembly of step s+1 "
-                        "(two device output sets, copy stream)")
+                   note=f"pinned host buffers; D2H of step s overlaps the assembly of step s+1 "
+                        f"(two device output sets, {NCS} copy streams)")
         del sets
 
     total_qp = spec_total_qp(args.config, n_el, n_q, ws)
@@ -303,7 +325,9 @@ def main():
         dtype="f64", data="synthetic (seeded mesh, NCM weights N(0,0.3^2), displacement; synth/gen.py)",
         config=dict(workload=WORKLOAD[args.config], elements=total_el, qp=total_qp, nnz_rank0=nnz_local,
                     width=spec.width, hidden_layers=spec.n_hidden, colours=info["n_colours"],
-                    kernel=args.kernel, launch=kinfo, parallelism=f"z-slabs x{ws}" if ws > 1 else "single GPU",
+                    kernel=args.kernel, launch=kinfo,
+                    parallelism=(f"z-slabs x{ws}, interface rows over " + ("NVLink P2P (peer mode)" if peer else "NCCL"))
+                    if ws > 1 else "single GPU",
                     l2="inputs larger than L2 (dN/dX + CSR values >> 126 MB), no flush needed"
                     if args.config in ("c3", "c4", "c5") else "inputs fit in L2 (latency-bound config)"),
         elements_per_s=total_el / (ms * 1e-3),

@@ -228,6 +228,26 @@ commet_status commet_halo_recv(commet_ctx ctx, int32_t k, int32_t* peer, int64_t
 commet_status commet_halo_unpack(commet_ctx ctx, int32_t k, const double* vals, const double* res,
                                  double* residual, double* csr_values, void* cuda_stream);
 
+/* ---- fused interface reduction over peer memory (NVLink P2P) ----------
+ * Instead of halo buffers + NCCL send/recv + unpack, the colour kernels add every halo-row
+ * contribution straight into the owning rank's residual / CSR values (RED.ADD.F64 through
+ * peer pointers), so the transfer overlaps the element math.  Per send segment k
+ * (0 <= k < n_send of commet_halo_info):
+ *   commet_set_peer(ctx, k, owner_residual, owner_csr_values, val_map, n_vals, row_map, n_res)
+ * with the owner's output buffers mapped into this process (e.g. CUDA IPC through torch) and
+ * the owner's receive maps for this rank (commet_halo_recv_maps on the owner: its segment for
+ * this sender).  commet_set_peer_mode(ctx, 1) then switches commet_assemble to peer mode; its
+ * output buffers must stay the ones the peers were given.  With an NCCL comm, commet_assemble
+ * zeroes its outputs and brackets the kernels with two NCCL barriers (all ranks zeroed before
+ * any rank adds; all added before the step ends).  Without a comm it does NOT zero: the caller
+ * runs commet_zero_outputs on every rank, synchronises the ranks, assembles, synchronises.
+ * The fused kernel only (its halo writes are atomic); at most 8 send segments. */
+commet_status commet_halo_recv_maps(commet_ctx ctx, int32_t k, const int64_t** val_map, const int64_t** row_map);
+commet_status commet_set_peer(commet_ctx ctx, int32_t k, double* peer_residual, double* peer_csr_values,
+                              const int64_t* val_map, int64_t n_vals, const int64_t* row_map, int64_t n_res);
+commet_status commet_set_peer_mode(commet_ctx ctx, int32_t on);
+commet_status commet_zero_outputs(commet_ctx ctx, double* residual, double* csr_values, void* cuda_stream);
+
 /* ---- host-only plan (no GPU needed): what commet_setup builds, for inspection --- */
 typedef struct commet_plan_s* commet_plan;
 commet_status commet_plan_create(const commet_mesh_desc* mesh, commet_plan* out);

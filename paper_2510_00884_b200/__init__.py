@@ -35,7 +35,8 @@ SYMBOLS = ("commet_setup", "commet_csr_pattern", "commet_csr_pattern_copy", "com
            "commet_plan_send", "commet_plan_recv", "commet_plan_colours", "commet_plan_destroy",
            "commet_kernel_info", "commet_max_trace_C", "commet_set_dirichlet", "commet_apply_dirichlet",
            "commet_cg_jacobi", "commet_newton_step", "commet_ncm_eval", "commet_normalize_reference",
-           "commet_material_eval")
+           "commet_material_eval", "commet_halo_recv_maps", "commet_set_peer", "commet_set_peer_mode",
+           "commet_zero_outputs")
 NEWTON_MAX_LOG = 64
 
 
@@ -155,6 +156,12 @@ _lib.commet_ncm_eval.argtypes = [_vp, _vp, _vp, _vp, _i64, _vp]
 _lib.commet_normalize_reference.argtypes = [_vp, _P(C.c_double)]
 _lib.commet_material_eval.argtypes = [_vp, _vp, _i64, _vp, _vp, _vp, _vp]
 _lib.commet_material_eval.restype = C.c_int
+_lib.commet_halo_recv_maps.argtypes = [_vp, _i32, _P(_vp), _P(_vp)]
+_lib.commet_set_peer.argtypes = [_vp, _i32, _vp, _vp, _vp, _i64, _vp, _i64]
+_lib.commet_set_peer_mode.argtypes = [_vp, _i32]
+_lib.commet_zero_outputs.argtypes = [_vp, _vp, _vp, _vp]
+for _f in ("commet_halo_recv_maps", "commet_set_peer", "commet_set_peer_mode", "commet_zero_outputs"):
+    getattr(_lib, _f).restype = C.c_int
 for _f in ("commet_ncm_eval", "commet_normalize_reference", "commet_max_trace_C", "commet_set_dirichlet", "commet_apply_dirichlet", "commet_cg_jacobi",
            "commet_newton_step"):
     getattr(_lib, _f).restype = C.c_int
@@ -308,6 +315,27 @@ class Commet:
         peer, nv, nr = _i32(), _i64(), _i64()
         _check(_lib.commet_halo_recv(self.ctx, k, C.byref(peer), C.byref(nv), C.byref(nr)), self.ctx)
         return peer.value, nv.value, nr.value
+
+    def halo_recv_maps(self, k: int):
+        """(sender rank, val_map, row_map) of receive segment k (host int64 copies)."""
+        peer, nv, nr = self.halo_recv(k)
+        vp, rp = _vp(), _vp()
+        _check(_lib.commet_halo_recv_maps(self.ctx, k, C.byref(vp), C.byref(rp)), self.ctx)
+        return peer, Plan._arr(vp, nv, np.int64), Plan._arr(rp, nr, np.int64)
+
+    def set_peer(self, k: int, peer_residual_ptr: int, peer_values_ptr: int, val_map, row_map):
+        vm = np.ascontiguousarray(val_map, np.int64)
+        rm = np.ascontiguousarray(row_map, np.int64)
+        _check(_lib.commet_set_peer(self.ctx, k, peer_residual_ptr, peer_values_ptr, _ptr(vm), vm.size, _ptr(rm),
+                                    rm.size), self.ctx)
+
+    def set_peer_mode(self, on: bool = True):
+        _check(_lib.commet_set_peer_mode(self.ctx, 1 if on else 0), self.ctx)
+
+    def zero_outputs(self, residual, values, stream=None):
+        t = self.torch
+        st = stream if stream is not None else t.cuda.current_stream(self.device)
+        _check(_lib.commet_zero_outputs(self.ctx, residual.data_ptr(), values.data_ptr(), st.cuda_stream), self.ctx)
 
     def halo_unpack(self, k: int, vals_ptr: int, res_ptr: int, residual, values, stream=None):
         t = self.torch
@@ -514,6 +542,35 @@ def nccl_comm_from_process_group(rank: int, world_size: int, device: int):
     with torch.cuda.device(device):
         _check(_lib.commet_nccl_comm_init(idb, world_size, rank, device, C.byref(comm)))
     return comm.value
+
+
+def setup_peer_exchange(lib: "Commet", residual, values, rank: int, world_size: int):
+    """Peer mode over torch.distributed (plumbing only): every rank shares its output tensors
+    through CUDA IPC (torch.multiprocessing reductions) and the receive maps it holds for
+    each sender; each rank then points its send segments at the owners' buffers."""
+    import torch.distributed as dist
+    from torch.multiprocessing.reductions import reduce_tensor
+    n_send, n_recv = lib.halo_info()
+    maps = {}
+    for k in range(n_recv):
+        sender, vm, rm = lib.halo_recv_maps(k)
+        maps[sender] = (vm, rm)
+    mine = dict(rank=rank, r=reduce_tensor(residual), v=reduce_tensor(values), maps=maps)
+    everyone = [None] * world_size
+    dist.all_gather_object(everyone, mine)
+    keep = []
+    for k in range(n_send):
+        peer = lib.halo_send(k)[0]
+        owner = everyone[peer]
+        fr, ar = owner["r"]
+        fv, av = owner["v"]
+        r_peer, v_peer = fr(*ar), fv(*av)
+        vm, rm = owner["maps"][rank]
+        lib.set_peer(k, r_peer.data_ptr(), v_peer.data_ptr(), vm, rm)
+        keep += [r_peer, v_peer]
+    lib.set_peer_mode(True)
+    lib._peer_keepalive = keep
+    return keep
 
 
 def nccl_comm_destroy(comm):

@@ -287,11 +287,21 @@ extern "C" commet_status commet_assemble(commet_ctx c, const double* u, double* 
   cudaStream_t st = (cudaStream_t)cuda_stream;
   c->last_stream = st;
   CUDA_TRY(c, cudaSetDevice(c->device));
-  CUDA_TRY(c, cudaMemsetAsync(residual, 0, 3 * p.n_owned * sizeof(double), st));
-  CUDA_TRY(c, cudaMemsetAsync(csr_values, 0, p.nnz * sizeof(double), st));
+  if (c->peer && c->kernel != COMMET_KERNEL_FUSED)
+    return fail(c, COMMET_ERR_ARG, "peer mode needs the fused kernel (its halo-row writes are atomic)");
+  // peer mode: other ranks add into these buffers -- every rank must have zeroed its outputs
+  // before any rank's kernels run (NCCL barrier with a comm; the caller's job without one, see
+  // commet_zero_outputs), and the step ends only when every rank's kernels are done
+  const bool zero_here = !(c->peer && !c->comm);
+  if (zero_here) {
+    CUDA_TRY(c, cudaMemsetAsync(residual, 0, 3 * p.n_owned * sizeof(double), st));
+    CUDA_TRY(c, cudaMemsetAsync(csr_values, 0, p.nnz * sizeof(double), st));
+  }
+  if (c->peer && c->comm)
+    NCCL_TRY(c, ncclAllReduce(c->barrier_buf.p, c->barrier_buf.p, 1, ncclFloat, ncclSum, c->comm, st));
   CUDA_TRY(c, cudaMemsetAsync(c->bad.p, 0xff, sizeof(unsigned long long), st));
   CUDA_TRY(c, cudaMemsetAsync(c->max_trc.p, 0, sizeof(unsigned long long), st));
-  if (p.n_halo) {
+  if (p.n_halo && !c->peer) {
     CUDA_TRY(c, cudaMemsetAsync(c->r_halo.p, 0, c->r_halo.n * sizeof(double), st));
     CUDA_TRY(c, cudaMemsetAsync(c->v_halo.p, 0, c->v_halo.n * sizeof(double), st));
   }
@@ -314,6 +324,16 @@ extern "C" commet_status commet_assemble(commet_ctx c, const double* u, double* 
   a.v_halo = c->v_halo.p;
   a.bad = c->bad.p;
   a.max_trc = c->max_trc.p;
+  if (c->peer) {
+    a.peer = 1;
+    a.halo_peer = c->halo_peer.p;
+    a.peer_vmap = c->peer_vmap.p;
+    a.peer_rmap = c->peer_rmap.p;
+    for (size_t k = 0; k < c->peer_v.size(); k++) {
+      a.peer_v[k] = c->peer_v[k];
+      a.peer_r[k] = c->peer_r[k];
+    }
+  }
   a.ncm = c->ncm;
   const int slot = c->ev0.empty() ? -1 : (int)(c->n_assembled % (int64_t)c->ev0.size());
   if (slot >= 0) CUDA_TRY(c, cudaEventRecord(c->ev0[slot], st));
@@ -325,6 +345,10 @@ extern "C" commet_status commet_assemble(commet_ctx c, const double* u, double* 
   }
   if (slot >= 0) CUDA_TRY(c, cudaEventRecord(c->ev1[slot], st));
   c->n_assembled++;
+  if (c->peer) {  // halo rows went straight to their owners: only the closing barrier
+    if (c->comm) NCCL_TRY(c, ncclAllReduce(c->barrier_buf.p, c->barrier_buf.p, 1, ncclFloat, ncclSum, c->comm, st));
+    return COMMET_OK;
+  }
   // ---- halo exchange over NCCL: one group of point-to-point transfers, then unpack ----------
   if (c->comm && p.n_ranks > 1 && (!p.send_rank.empty() || !p.recv_rank.empty())) {
     NCCL_TRY(c, ncclGroupStart());
@@ -494,6 +518,83 @@ extern "C" commet_status commet_halo_recv(commet_ctx c, int32_t k, int32_t* peer
   if (peer) *peer = p.recv_rank[k];
   if (n_vals) *n_vals = p.recv_val_off[k + 1] - p.recv_val_off[k];
   if (n_res) *n_res = p.recv_row_off[k + 1] - p.recv_row_off[k];
+  return COMMET_OK;
+}
+
+extern "C" commet_status commet_halo_recv_maps(commet_ctx c, int32_t k, const int64_t** val_map,
+                                               const int64_t** row_map) {
+  if (!c) return fail(nullptr, COMMET_ERR_ARG, "ctx is NULL");
+  const Plan& p = c->plan;
+  if (k < 0 || k >= (int)p.recv_rank.size()) return fail(c, COMMET_ERR_ARG, "recv segment %d out of range", k);
+  if (val_map) *val_map = p.recv_val_map.data() + p.recv_val_off[k];
+  if (row_map) *row_map = p.recv_row_map.data() + p.recv_row_off[k];
+  return COMMET_OK;
+}
+
+extern "C" commet_status commet_set_peer(commet_ctx c, int32_t k, double* peer_residual, double* peer_csr_values,
+                                         const int64_t* val_map, int64_t n_vals, const int64_t* row_map,
+                                         int64_t n_res) {
+  if (!c) return fail(nullptr, COMMET_ERR_ARG, "ctx is NULL");
+  const Plan& p = c->plan;
+  const int ns = (int)p.send_rank.size();
+  if (k < 0 || k >= ns) return fail(c, COMMET_ERR_ARG, "send segment %d out of range (%d)", k, ns);
+  if (ns > kMaxPeers) return fail(c, COMMET_ERR_ARG, "%d send segments > %d", ns, kMaxPeers);
+  const int64_t v0 = p.send_val_off[k], v1 = p.send_val_off[k + 1], r0 = p.send_row_off[k], r1 = p.send_row_off[k + 1];
+  if (n_vals != v1 - v0 || n_res != r1 - r0)
+    return fail(c, COMMET_ERR_ARG, "segment %d: maps of %lld values / %lld rows, the segment has %lld / %lld", k,
+                (long long)n_vals, (long long)n_res, (long long)(v1 - v0), (long long)(r1 - r0));
+  if (!peer_residual || !peer_csr_values || (n_vals && !val_map) || (n_res && !row_map))
+    return fail(c, COMMET_ERR_ARG, "peer pointer or map is NULL");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  if (c->peer_v.empty()) {
+    c->peer_v.assign(ns, nullptr);
+    c->peer_r.assign(ns, nullptr);
+    c->peer_set.assign(ns, 0);
+    CUDA_TRY(c, c->peer_vmap.alloc(std::max<int64_t>(1, p.nnz_halo)));
+    CUDA_TRY(c, c->peer_rmap.alloc(std::max<int64_t>(1, 3 * p.n_halo)));
+    std::vector<int8_t> hp(std::max<int64_t>(1, p.n_halo), 0);
+    for (int kk = 0; kk < ns; kk++)
+      for (int64_t r = p.send_row_off[kk]; r < p.send_row_off[kk + 1]; r += 3) hp[r / 3] = (int8_t)kk;
+    CUDA_TRY(c, c->halo_peer.alloc(hp.size()));
+    CUDA_TRY(c, cudaMemcpy(c->halo_peer.p, hp.data(), hp.size(), cudaMemcpyHostToDevice));
+    CUDA_TRY(c, c->barrier_buf.alloc(1));
+    CUDA_TRY(c, cudaMemset(c->barrier_buf.p, 0, sizeof(float)));
+  }
+  if (n_vals) CUDA_TRY(c, cudaMemcpy(c->peer_vmap.p + v0, val_map, n_vals * sizeof(int64_t), cudaMemcpyHostToDevice));
+  if (n_res) CUDA_TRY(c, cudaMemcpy(c->peer_rmap.p + r0, row_map, n_res * sizeof(int64_t), cudaMemcpyHostToDevice));
+  c->peer_v[k] = peer_csr_values;
+  c->peer_r[k] = peer_residual;
+  c->peer_set[k] = 1;
+  return COMMET_OK;
+}
+
+extern "C" commet_status commet_set_peer_mode(commet_ctx c, int32_t on) {
+  if (!c) return fail(nullptr, COMMET_ERR_ARG, "ctx is NULL");
+  if (!on) {
+    c->peer = false;
+    return COMMET_OK;
+  }
+  const Plan& p = c->plan;
+  if (p.n_ranks <= 1) return fail(c, COMMET_ERR_ARG, "peer mode needs a multi-rank partition");
+  for (size_t k = 0; k < p.send_rank.size(); k++)
+    if (k >= c->peer_set.size() || !c->peer_set[k])
+      return fail(c, COMMET_ERR_ARG, "send segment %zu (to rank %d) has no peer (commet_set_peer)", k, p.send_rank[k]);
+  if (c->peer_v.empty()) {  // no send segments (the top slab): only the barrier buffer is needed
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    CUDA_TRY(c, c->barrier_buf.alloc(1));
+    CUDA_TRY(c, cudaMemset(c->barrier_buf.p, 0, sizeof(float)));
+  }
+  c->peer = true;
+  return COMMET_OK;
+}
+
+extern "C" commet_status commet_zero_outputs(commet_ctx c, double* residual, double* csr_values, void* cuda_stream) {
+  if (!c) return fail(nullptr, COMMET_ERR_ARG, "ctx is NULL");
+  const Plan& p = c->plan;
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  if (residual) CUDA_TRY(c, cudaMemsetAsync(residual, 0, 3 * p.n_owned * sizeof(double), st));
+  if (csr_values) CUDA_TRY(c, cudaMemsetAsync(csr_values, 0, p.nnz * sizeof(double), st));
   return COMMET_OK;
 }
 

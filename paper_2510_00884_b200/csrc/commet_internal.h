@@ -18,6 +18,7 @@ namespace commet {
 
 constexpr int kMaxLayers = 4;
 constexpr int kMaxWidth = 128;
+constexpr int kMaxPeers = 8;  // send segments (peer ranks) of the peer-mode scatter
 
 struct NcmDev {
   int L, w;
@@ -63,6 +64,13 @@ struct AsmArgs {
   double* v_halo;
   unsigned long long* bad;
   unsigned long long* max_trc;  // max over qps of tr C = I1 (> 0: the bit pattern orders like the value)
+  // peer mode (multi-GPU over NVLink P2P): halo rows added straight into the owners' buffers
+  int peer;
+  const int8_t* halo_peer;      // [n_halo] send segment (= peer slot) of each halo row-node
+  const int64_t* peer_vmap;     // [nnz_halo] halo value -> position in the owner's CSR values
+  const int64_t* peer_rmap;     // [3 n_halo] halo row -> position in the owner's residual
+  double* peer_v[kMaxPeers];
+  double* peer_r[kMaxPeers];
   // material-point mode (launch_material): F [n][9] in; Psi [n], tau [n][6], c [n][21] out (each may be NULL)
   const double* Fin;
   double* Wout;

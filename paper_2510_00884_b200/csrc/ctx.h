@@ -57,6 +57,13 @@ struct commet_ctx_s {
   DevBuf<double> r_halo, v_halo, r_recv, v_recv;
   DevBuf<int64_t> recv_val_map, recv_row_map;
   DevBuf<unsigned long long> bad, max_trc;
+  // peer mode (fused interface reduction over NVLink P2P)
+  bool peer = false;
+  std::vector<double*> peer_v, peer_r;  // per send segment: the owner's output buffers
+  std::vector<char> peer_set;
+  DevBuf<int8_t> halo_peer;
+  DevBuf<int64_t> peer_vmap, peer_rmap;
+  DevBuf<float> barrier_buf;
   SolverWork* solver = nullptr;
   NcmDev ncm{};
   // timing ring

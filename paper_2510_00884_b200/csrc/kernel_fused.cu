@@ -88,6 +88,22 @@ __device__ __forceinline__ void frag_prefetch(const double* __restrict__ Af, int
 #endif
 }
 
+// Output addresses of the scatter.  off: offset of the entry in this rank's owned CSR values,
+// or in the halo buffer for halo rows (row-nodes la >= n_owned).  Peer mode (multi-GPU, NVLink
+// P2P): halo rows go straight to the owning rank's buffers through the owner's receive maps,
+// replacing the NCCL exchange + unpack.
+__device__ __forceinline__ double* vout(const AsmArgs& A, int64_t la, int64_t off) {
+  if (la < A.n_owned) return A.v_own + off;
+  if (!A.peer) return A.v_halo + off;
+  return A.peer_v[__ldg(A.halo_peer + (la - A.n_owned))] + __ldg(A.peer_vmap + off);
+}
+__device__ __forceinline__ double* rout(const AsmArgs& A, int64_t la, int i) {
+  if (la < A.n_owned) return A.r_own + 3 * la + i;
+  const int64_t hr = 3 * (la - A.n_owned) + i;
+  if (!A.peer) return A.r_halo + hr;
+  return A.peer_r[__ldg(A.halo_peer + (la - A.n_owned))] + __ldg(A.peer_rmap + hr);
+}
+
 __device__ __forceinline__ double2 ldg2(const double* p) {
   return __ldg(reinterpret_cast<const double2*>(p));
 }
@@ -922,18 +938,19 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
         const int64_t el = e0 + e;
         if (a < NEN) {
           const int64_t la = __ldg(A.lrow + el * NEN + a);
-          double* va = ((la < A.n_owned) ? A.v_own : A.v_halo) + __ldg(A.node_rs + la);
+          const int64_t rsa = __ldg(A.node_rs + la);
           const int sa = 3 * __ldg(A.node_deg + la);
 #pragma unroll
           for (int h = 0; h < 2; h++) {
             const int b = 8 * nt + 2 * t + h;
             if (b < NEN) {
-              atomicAdd(va + i * sa + 3 * (int)__ldg(A.slot + ((size_t)el * NEN + a) * NEN + b) + k, c[h]);
+              atomicAdd(vout(A, la, rsa + i * sa + 3 * (int)__ldg(A.slot + ((size_t)el * NEN + a) * NEN + b) + k), c[h]);
               if (i < k) {
                 const int64_t lb = __ldg(A.lrow + el * NEN + b);
-                double* vb2 = ((lb < A.n_owned) ? A.v_own : A.v_halo) + __ldg(A.node_rs + lb);
                 const int sb3 = 3 * __ldg(A.node_deg + lb);
-                atomicAdd(vb2 + k * sb3 + 3 * (int)__ldg(A.slot + ((size_t)el * NEN + b) * NEN + a) + i, c[h]);
+                atomicAdd(vout(A, lb, __ldg(A.node_rs + lb) + k * sb3 +
+                                          3 * (int)__ldg(A.slot + ((size_t)el * NEN + b) * NEN + a) + i),
+                          c[h]);
               }
             }
           }
@@ -949,9 +966,7 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
           const double* ga = sgN + (q * NEN + a) * 3;
           rr += qP[q * 9 + i * 3] * ga[0] + qP[q * 9 + i * 3 + 1] * ga[1] + qP[q * 9 + i * 3 + 2] * ga[2];
         }
-        const int64_t la = __ldg(A.lrow + (e0 + e) * NEN + a);
-        const bool own = la < A.n_owned;
-        atomicAdd((own ? A.r_own : A.r_halo) + 3 * (own ? la : la - A.n_owned) + i, rr);
+        atomicAdd(rout(A, __ldg(A.lrow + (e0 + e) * NEN + a), i), rr);
       }
     }
     } else {
@@ -993,23 +1008,19 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
         }
         const int64_t el = e0 + e;
         const int64_t la = __ldg(A.lrow + el * NEN + a), lb = __ldg(A.lrow + el * NEN + b);
-        const bool owna = la < A.n_owned, ownb = lb < A.n_owned;
-        double* va = (owna ? A.v_own : A.v_halo) + __ldg(A.node_rs + la);
         const int sa = 3 * __ldg(A.node_deg + la);
-        double* dst = va + i * sa + 3 * (int)__ldg(A.slot + ((size_t)el * NEN + a) * NEN + b);
-        atomicAdd(dst, K0);
-        atomicAdd(dst + 1, K1);
-        atomicAdd(dst + 2, K2);
+        const int64_t dst = __ldg(A.node_rs + la) + i * sa + 3 * (int)__ldg(A.slot + ((size_t)el * NEN + a) * NEN + b);
+        atomicAdd(vout(A, la, dst), K0);
+        atomicAdd(vout(A, la, dst + 1), K1);
+        atomicAdd(vout(A, la, dst + 2), K2);
         if (b == a) {
-          double* rb = owna ? A.r_own : A.r_halo;
-          atomicAdd(rb + 3 * (owna ? la : la - A.n_owned) + i, rr);
+          atomicAdd(rout(A, la, i), rr);
         } else {
-          double* vbb = (ownb ? A.v_own : A.v_halo) + __ldg(A.node_rs + lb);
           const int sb3 = 3 * __ldg(A.node_deg + lb);
-          double* mir = vbb + 3 * (int)__ldg(A.slot + ((size_t)el * NEN + b) * NEN + a) + i;
-          atomicAdd(mir, K0);
-          atomicAdd(mir + sb3, K1);
-          atomicAdd(mir + 2 * sb3, K2);
+          const int64_t mir = __ldg(A.node_rs + lb) + 3 * (int)__ldg(A.slot + ((size_t)el * NEN + b) * NEN + a) + i;
+          atomicAdd(vout(A, lb, mir), K0);
+          atomicAdd(vout(A, lb, mir + sb3), K1);
+          atomicAdd(vout(A, lb, mir + 2 * sb3), K2);
         }
       }
     }

@@ -181,6 +181,42 @@ def test_slabs_on_one_device(name, n, P):
     assert rel(r_all, gr) <= TOL and rel(v_all, gv) <= TOL, (rel(r_all, gr), rel(v_all, gv))
 
 
+@pytest.mark.parametrize("name,n,P", [("c1", 4, 2), ("c2", 8, 4), ("c4", 3, 3)])
+def test_slabs_peer_mode_on_one_device(name, n, P):
+    """Peer mode (the fused interface reduction): each rank's kernels add their halo rows
+    straight into the owner's output buffers through the owner's receive maps -- no halo
+    buffers, no unpack.  P contexts on one device, outputs zeroed first, assembled one after
+    the other (no kernel waits on another); the concatenated rows equal the global oracle."""
+    torch = _torch()
+    import paper_2510_00884_b200 as pc
+    g = gen.make_config(name, n=n)
+    grp, gci = oracle.pattern(g["n_nodes"], g["conn"])
+    gr, gv, _ = oracle.assemble(g["ncm"], g["n_nodes"], g["conn"], g["gradN"], g["qp_w"], g["u"], grp, gci)
+    u = torch.from_numpy(g["u"]).cuda()
+    libs = [pc.Commet(c, c["ncm"]) for c in (gen.slab_partition(name, P, r, n=n) for r in range(P))]
+    outs = [lib.alloc_outputs() for lib in libs]
+    for r, lib in enumerate(libs):
+        for k in range(lib.halo_info()[0]):
+            owner = lib.halo_send(k)[0]
+            maps = {}
+            for kr in range(libs[owner].halo_info()[1]):
+                sender, vm, rm = libs[owner].halo_recv_maps(kr)
+                maps[sender] = (vm, rm)
+            vm, rm = maps[r]
+            lib.set_peer(k, outs[owner][0].data_ptr(), outs[owner][1].data_ptr(), vm, rm)
+        lib.set_peer_mode(True)
+    for lib, (res, val) in zip(libs, outs):
+        lib.zero_outputs(res, val)
+    for lib, (res, val) in zip(libs, outs):
+        lib.assemble(u, res, val)
+    torch.cuda.synchronize()
+    r_all = np.concatenate([o[0].cpu().numpy() for o in outs])
+    v_all = np.concatenate([o[1].cpu().numpy() for o in outs])
+    ci_all = np.concatenate([lib.pattern()[1] for lib in libs])
+    assert np.array_equal(ci_all, gci)
+    assert rel(r_all, gr) <= TOL and rel(v_all, gv) <= TOL, (rel(r_all, gr), rel(v_all, gv))
+
+
 def _elements_of(conn, a):
     return np.nonzero((conn == a).any(axis=1))[0]
 
