@@ -46,6 +46,9 @@
 #ifndef COMMET_PD_J
 #define COMMET_PD_J 2
 #endif
+#ifndef COMMET_ANALYTIC_MINB
+#define COMMET_ANALYTIC_MINB 4  // CTAs per SM of the analytic-network (NET = 1) kernels (measured: GT +7 %, CANN +4 % over 3)
+#endif
 #ifndef COMMET_PINGPONG
 #define COMMET_PINGPONG 0  // measured neutral (c3 10.31 vs 10.26 ms): barriers kept
 #endif
@@ -1164,7 +1167,7 @@ static void occ_cfg(int L, int* smem_bytes, int* ctas_per_sm, int* regs) {
 
 template <int NEN, int NQ>
 static void occ_et(int w, int L, int* a, int* b, int* c) {
-  if (w == 0) return occ_cfg<Cfg<16, 16, NEN, NQ, 3, 1>>(1, a, b, c);  // analytic networks
+  if (w == 0) return occ_cfg<Cfg<16, 16, NEN, NQ, COMMET_ANALYTIC_MINB, 1>>(1, a, b, c);  // analytic networks
   switch (w) {
     case 8: occ_cfg<Cfg<8, 32, NEN, NQ>>(L, a, b, c); break;
     case 16: occ_cfg<Cfg<16, 16, NEN, NQ>>(L, a, b, c); break;
@@ -1181,7 +1184,9 @@ void fused_occupancy(int n_en, int w, int L, int* smem_bytes, int* ctas_per_sm, 
 
 template <int NEN, int NQ, int K>
 static int launch_k(const AsmArgs& a, cudaStream_t st, int* launches) {
-  if (a.ncm.net != 0 || K == 2) return launch_cfg<Cfg<16, 16, NEN, NQ, 3, 1, K>>(a, st, launches);
+  if (a.ncm.net == 3)  // ICKAN: its per-qp forward mode needs the registers of 3 CTAs/SM (4: spills, -14 %)
+    return launch_cfg<Cfg<16, 16, NEN, NQ, 3, 1, K>>(a, st, launches);
+  if (a.ncm.net != 0 || K == 2) return launch_cfg<Cfg<16, 16, NEN, NQ, COMMET_ANALYTIC_MINB, 1, K>>(a, st, launches);
   if constexpr (K != 2)
   switch (a.ncm.w) {
     case 8: return launch_cfg<Cfg<8, 32, NEN, NQ, 3, 0, K>>(a, st, launches);

@@ -21,8 +21,15 @@ def run(path, cfg, steps=20):
                   cfg["qp_w"].ctypes.data, 0, cfg["n_nodes"], 1, 0, None, 0, None, None,
                   int(os.environ.get("AB_ORDER", "0")))
     m = cfg["ncm"]
-    keep = [np.ascontiguousarray(m[k]) for k in ("W1", "W", "b", "a")]
-    nd = NcmDesc(m["n_hidden"], m["width"], *[k.ctypes.data for k in keep], None, None, m["kappa"], 0.0)
+    net = os.environ.get("AB_NET")  # variants: gt | cann | ickan
+    if net == "gt":
+        m = gen.gent_thomas_params()
+    elif net == "cann":
+        m = gen.cann_params(4)
+    elif net == "ickan":
+        m = gen.ickan_params()
+    import paper_2510_00884_b200 as pc
+    nd, keep = pc.ncm_desc(m)
     ctx = C.c_void_p()
     st = torch.cuda.current_stream().cuda_stream
     assert lib.commet_setup(C.byref(md), C.byref(nd), 0, C.c_void_p(st), None, C.byref(ctx)) == 0
