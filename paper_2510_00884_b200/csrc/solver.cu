@@ -191,7 +191,47 @@ __global__ void cg_update_p_kernel(double* __restrict__ p, const double* __restr
     p[i] = fma(beta, p[i], z[i]);
 }
 
-// q = K p, partials of p.q.  A contiguous node range per block (neighbouring nodes share most of
+// q = K p by node blocks: the row triple of node a is deg(a) 3x3 blocks, block s at
+// node_rs[a] + 3 s (+ 3 deg(a) per row), its column node from the node adjacency (one int32 per
+// block instead of nine col_idx entries: 8 + 4/9 bytes per nonzero); a lane per neighbour node
+// reads 3 consecutive values of each row and 3 consecutive entries of p.  Single GPU: node_rs[a]
+// = 9 x (the adjacency offset of a).
+__global__ void cg_spmv_dot_nb_kernel(const int64_t* __restrict__ node_rs, const int32_t* __restrict__ node_deg,
+                                      const int32_t* __restrict__ adj, const double* __restrict__ vals,
+                                      const double* __restrict__ p, double* __restrict__ q, int64_t n_nodes,
+                                      double* part, const CgScal* s) {
+  if (s->done) return;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwb = blockDim.x >> 5;
+  const int64_t chunk = (n_nodes + gridDim.x - 1) / gridDim.x;
+  const int64_t a_end = min(n_nodes, (int64_t)(blockIdx.x + 1) * chunk);
+  double v[1] = {0.0};
+  for (int64_t a = (int64_t)blockIdx.x * chunk + wid; a < a_end; a += nwb) {
+    const int64_t rs = __ldg(node_rs + a);
+    const int deg = __ldg(node_deg + a), st = 3 * deg;
+    const int32_t* nb = adj + rs / 9;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+    for (int sl = lane; sl < deg; sl += 32) {
+      const int64_t b = __ldcs(nb + sl);
+      const double p0 = __ldg(p + 3 * b), p1 = __ldg(p + 3 * b + 1), p2 = __ldg(p + 3 * b + 2);
+      const double* v0 = vals + rs + 3 * sl;
+      s0 = fma(__ldcs(v0), p0, fma(__ldcs(v0 + 1), p1, fma(__ldcs(v0 + 2), p2, s0)));
+      s1 = fma(__ldcs(v0 + st), p0, fma(__ldcs(v0 + st + 1), p1, fma(__ldcs(v0 + st + 2), p2, s1)));
+      s2 = fma(__ldcs(v0 + 2 * st), p0, fma(__ldcs(v0 + 2 * st + 1), p1, fma(__ldcs(v0 + 2 * st + 2), p2, s2)));
+    }
+    s0 = warp_sum(s0);
+    s1 = warp_sum(s1);
+    s2 = warp_sum(s2);
+    if (lane == 0) {
+      q[3 * a] = s0;
+      q[3 * a + 1] = s1;
+      q[3 * a + 2] = s2;
+      v[0] += p[3 * a] * s0 + p[3 * a + 1] * s1 + p[3 * a + 2] * s2;
+    }
+  }
+  block_partials<1>(v, part);
+}
+
+// q = K p, partials of p.q (scalar CSR: the column list, kept for reference).  A contiguous node range per block (neighbouring nodes share most of
 // their stencil columns: the p gathers hit L1); the matrix streams with evict-first loads, all
 // lane loads of a row triple issued before the FMAs
 __global__ void cg_spmv_dot_kernel(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col_idx,
@@ -321,6 +361,7 @@ struct SolverWork {
   DevBuf<uint8_t> mask;
   DevBuf<double> bc_vals;
   DevBuf<double> r, vals, dinv, x, cr, z, p, q, part, part2, dotv;
+  DevBuf<int32_t> adj;  // node adjacency (column node of every 3x3 block), node order
   DevBuf<CgScal> scal;
   DevBuf<unsigned long long> bad;
   int nb = 0;
@@ -350,6 +391,12 @@ static commet_status work(commet_ctx c, SolverWork** out) {
     CUDA_TRY(c, w->cr.alloc(n));
     CUDA_TRY(c, w->z.alloc(n));
     CUDA_TRY(c, w->p.alloc(n));
+    {
+      std::vector<int32_t> adj(p.adj.nbr.size());
+      for (size_t x = 0; x < adj.size(); x++) adj[x] = (int32_t)p.adj.nbr[x];
+      CUDA_TRY(c, w->adj.alloc(std::max<size_t>(adj.size(), 1)));
+      if (!adj.empty()) CUDA_TRY(c, cudaMemcpy(w->adj.p, adj.data(), adj.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+    }
     CUDA_TRY(c, w->q.alloc(n));
     CUDA_TRY(c, w->part.alloc(2 * (size_t)w->nb));
     CUDA_TRY(c, w->part2.alloc(2 * (size_t)w->nb));
@@ -434,8 +481,8 @@ static commet_status cg(commet_ctx c, SolverWork* w, const double* vals, const d
     for (int kk = 0; kk < nk; kk++) {
       const int k = it0 + kk;
       cg_update_p_kernel<<<nb, kThreads, 0, st>>>(w->p.p, w->z.p, n, w->part2.p, nb, w->scal.p, k, max_iter);
-      cg_spmv_dot_kernel<<<nb, kThreads, 0, st>>>(c->row_ptr.p, c->col_idx.p, vals, w->p.p, w->q.p, n_nodes,
-                                                  w->part.p, w->scal.p);
+      cg_spmv_dot_nb_kernel<<<nb, kThreads, 0, st>>>(c->node_rs.p, c->node_deg.p, w->adj.p, vals, w->p.p, w->q.p,
+                                                     n_nodes, w->part.p, w->scal.p);
       cg_update_xr_kernel<<<nb, kThreads, 0, st>>>(x, w->cr.p, w->z.p, w->p.p, w->q.p, w->dinv.p, n, w->part.p, nb,
                                                    w->part2.p, w->scal.p, k);
     }
