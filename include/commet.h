@@ -93,18 +93,19 @@ typedef struct {
 enum { COMMET_ORDER_COLOURED = 0, COMMET_ORDER_ELEMENT = 1 };
 
 /* (M)ICNN inner network of Eq. icnn with softplus
- * activation, on the kinematic inputs k = (I1-3, I2-3, J-1):
+ * activation, on the kinematic inputs k = (I1-3, I2-3, J-1) (nk = 3; anisotropic: nk = 5, see a0):
  *   y1 = W1 k + b1;  y_l = W_l z_{l-1} + B_l k + b_l (l = 2..L);  z_l = softplus(y_l)
  *   N  = a . z_L + skip_out . k                                                 */
 typedef struct {
   int32_t n_hidden;            /* L >= 1 */
   int32_t width;               /* w; multiple of 8, 8 <= w <= 128 */
-  const double* W1;            /* host [w][3] */
+  const double* W1;            /* host [w][nk] */
   const double* W;             /* host [L-1][w][w] row-major (out, in); may be NULL if L == 1 */
   const double* b;             /* host [L][w] */
   const double* a;             /* host [w] output weights (no output bias: no effect on S, CC) */
-  const double* skip_out;      /* host [3] or NULL (= 0): output skip B^(n) */
-  const double* skip_hidden;   /* host [L-1][w][3] or NULL (= 0): hidden skips B^(l), l >= 2 */
+  const double* skip_out;      /* host [3] or NULL (= 0): output skip B^(n) on k1..k3 */
+  const double* skip_hidden;   /* host [L-1][w][3] or NULL (= 0): hidden skips B^(l), l >= 2, on k1..k3;
+                                  must be NULL for nk = 5 (COMMET_ERR_ARG) */
   double kappa;                /* volumetric penalty kappa (J-1)^2 */
   double ref_shift;            /* s0: adds -s0 (J-1) to W; 0 = off (reading R11) */
   /* ---- variants; a zero-initialised tail = the ICNN on k above ---- */
@@ -133,7 +134,8 @@ typedef struct {
   const double* kan_c;         /* host [edges][kan_nb]: control points */
   /* COMMET_KIN_ANISOTROPIC: one structural vector A0 (reference configuration); the network
    * inputs are k = (I1-3, I2-3, J-1, I4-1, I5-1), I4 = A0.C A0, I5 = A0.C^2 A0 (App. A.2.1,
-   * PAPER.md:810-826) -- CANN (cann_* arrays over 5 inputs) or ICKAN (kan_width[0] = 5) only. */
+   * PAPER.md:810-826) -- ICNN (W1 [w][5]), CANN (cann_* arrays over 5 inputs) or ICKAN
+   * (kan_width[0] = 5); not Gent-Thomas (COMMET_ERR_ARG). */
   double a0[3];
 } commet_ncm_desc;
 

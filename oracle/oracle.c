@@ -75,23 +75,25 @@ static double sigmoid(double y) {
  * k >= 2 use A^(k) = W[k-2], B^(k) = skip_hidden[k-2] (reading 6: B is the
  * current layer's B^(k)).
  */
-static int icnn_eval(const oracle_ncm* m, const double K[3], double* N_out, double g_out[3],
-                     double H_out[9]) {
-  const int w = m->width, L = m->n_hidden;
-  if (w < 1 || L < 1) return 1;
-  const int nmax = w > 3 ? w : 3;
+static int icnn_eval(const oracle_ncm* m, int nk, const double* K, double* N_out, double* g_out,
+                     double* H_out) {
+  /* nk inputs (3; 5 for anisotropic kinematics): W1 is [w][nk]; hidden skips B^(k) [w][3] act on
+   * the first three inputs only and are refused for nk != 3 */
+  const int w = m->width, L = m->n_hidden, n2 = nk * nk;
+  if (w < 1 || L < 1 || (nk != 3 && m->skip_hidden)) return 1;
+  const int nmax = w > nk ? w : nk;
   double* z = (double*)calloc(nmax, sizeof(double));
-  double* dz = (double*)calloc((size_t)nmax * 3, sizeof(double));
-  double* d2z = (double*)calloc((size_t)nmax * 9, sizeof(double));
+  double* dz = (double*)calloc((size_t)nmax * nk, sizeof(double));
+  double* d2z = (double*)calloc((size_t)nmax * n2, sizeof(double));
   double* y = (double*)calloc(nmax, sizeof(double));
-  double* dy = (double*)calloc((size_t)nmax * 3, sizeof(double));
-  double* d2y = (double*)calloc((size_t)nmax * 9, sizeof(double));
+  double* dy = (double*)calloc((size_t)nmax * nk, sizeof(double));
+  double* d2y = (double*)calloc((size_t)nmax * n2, sizeof(double));
   if (!z || !dz || !d2z || !y || !dy || !d2y) return 2;
-  int nin = 3;
-  for (int i = 0; i < 3; i++) {
+  int nin = nk;
+  for (int i = 0; i < nk; i++) {
     z[i] = K[i];
-    for (int j = 0; j < 3; j++) dz[i * 3 + j] = (i == j) ? 1.0 : 0.0;
-    for (int j = 0; j < 9; j++) d2z[i * 9 + j] = 0.0;
+    for (int j = 0; j < nk; j++) dz[i * nk + j] = (i == j) ? 1.0 : 0.0;
+    for (int j = 0; j < n2; j++) d2z[i * n2 + j] = 0.0;
   }
   for (int k = 1; k <= L; k++) {
     const double* A = (k == 1) ? m->W1 : m->W + (size_t)(k - 2) * w * w;
@@ -103,43 +105,43 @@ static int icnn_eval(const oracle_ncm* m, const double K[3], double* N_out, doub
       if (B)
         for (int i = 0; i < 3; i++) s += B[j * 3 + i] * K[i];
       y[j] = s;
-      for (int p = 0; p < 3; p++) {
+      for (int p = 0; p < nk; p++) {
         double t = 0.0;
-        for (int i = 0; i < nin; i++) t += A[(size_t)j * nin + i] * dz[i * 3 + p];
+        for (int i = 0; i < nin; i++) t += A[(size_t)j * nin + i] * dz[i * nk + p];
         if (B) t += B[j * 3 + p];
-        dy[j * 3 + p] = t;
+        dy[j * nk + p] = t;
       }
-      for (int pq = 0; pq < 9; pq++) {
+      for (int pq = 0; pq < n2; pq++) {
         double t = 0.0;
-        for (int i = 0; i < nin; i++) t += A[(size_t)j * nin + i] * d2z[i * 9 + pq];
-        d2y[j * 9 + pq] = t;
+        for (int i = 0; i < nin; i++) t += A[(size_t)j * nin + i] * d2z[i * n2 + pq];
+        d2y[j * n2 + pq] = t;
       }
     }
     for (int j = 0; j < w; j++) {
       double f1 = sigmoid(y[j]);
       double f2 = f1 * (1.0 - f1);
-      for (int p = 0; p < 3; p++)
-        for (int q = 0; q < 3; q++)
-          d2z[j * 9 + p * 3 + q] = f1 * d2y[j * 9 + p * 3 + q] + f2 * dy[j * 3 + p] * dy[j * 3 + q];
-      for (int p = 0; p < 3; p++) dz[j * 3 + p] = f1 * dy[j * 3 + p];
+      for (int p = 0; p < nk; p++)
+        for (int q = 0; q < nk; q++)
+          d2z[j * n2 + p * nk + q] = f1 * d2y[j * n2 + p * nk + q] + f2 * dy[j * nk + p] * dy[j * nk + q];
+      for (int p = 0; p < nk; p++) dz[j * nk + p] = f1 * dy[j * nk + p];
       z[j] = softplus(y[j]);
     }
     nin = w;
   }
-  double N = 0.0, g[3] = {0, 0, 0}, H[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  double N = 0.0;
+  for (int p = 0; p < nk; p++) g_out[p] = 0.0;
+  for (int pq = 0; pq < n2; pq++) H_out[pq] = 0.0;
   for (int j = 0; j < w; j++) {
     N += m->a[j] * z[j];
-    for (int p = 0; p < 3; p++) g[p] += m->a[j] * dz[j * 3 + p];
-    for (int pq = 0; pq < 9; pq++) H[pq] += m->a[j] * d2z[j * 9 + pq];
+    for (int p = 0; p < nk; p++) g_out[p] += m->a[j] * dz[j * nk + p];
+    for (int pq = 0; pq < n2; pq++) H_out[pq] += m->a[j] * d2z[j * n2 + pq];
   }
   if (m->skip_out)
     for (int p = 0; p < 3; p++) {
       N += m->skip_out[p] * K[p];
-      g[p] += m->skip_out[p];
+      g_out[p] += m->skip_out[p];
     }
   *N_out = N;
-  for (int p = 0; p < 3; p++) g_out[p] = g[p];
-  for (int pq = 0; pq < 9; pq++) H_out[pq] = H[pq];
   free(z); free(dz); free(d2z); free(y); free(dy); free(d2y);
   return 0;
 }
@@ -315,9 +317,9 @@ static int ickan_eval(const oracle_ncm* m, int nk, const double* K, double* N_ou
 int oracle_ncm_eval_n(const oracle_ncm* m, int nin, const double* K, double* N_out, double* g_out, double* H_out) {
   if (m->network == 1) return cann_eval(m, nin, K, N_out, g_out, H_out);
   if (m->network == 3) return ickan_eval(m, nin, K, N_out, g_out, H_out);
+  if (m->network == 0) return icnn_eval(m, nin, K, N_out, g_out, H_out);
   if (nin != 3) return 4;
-  if (m->network == 2) return gt_eval(m, K, N_out, g_out, H_out);
-  return icnn_eval(m, K, N_out, g_out, H_out);
+  return gt_eval(m, K, N_out, g_out, H_out);
 }
 
 int oracle_ncm_eval(const oracle_ncm* m, const double K[3], double* N_out, double g_out[3],

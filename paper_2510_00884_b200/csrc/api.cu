@@ -40,8 +40,8 @@ extern "C" commet_status commet_setup(const commet_mesh_desc* mesh, const commet
   if (kin != COMMET_KIN_STANDARD && kin != COMMET_KIN_ISOCHORIC && kin != COMMET_KIN_ANISOTROPIC)
     return fail(C, COMMET_ERR_ARG, "kinematics %d unknown", kin);
   const int nk = kin == COMMET_KIN_ANISOTROPIC ? 5 : 3;  // network inputs
-  if (nk == 5 && net != COMMET_NET_CANN && net != COMMET_NET_ICKAN)
-    return fail(C, COMMET_ERR_ARG, "anisotropic kinematics need a CANN or ICKAN inner network (5 inputs)");
+  if (nk == 5 && net == COMMET_NET_GENT_THOMAS)
+    return fail(C, COMMET_ERR_ARG, "anisotropic kinematics need an ICNN, CANN or ICKAN inner network (5 inputs)");
   if (net != COMMET_NET_ICNN && net != COMMET_NET_CANN && net != COMMET_NET_GENT_THOMAS && net != COMMET_NET_ICKAN)
     return fail(C, COMMET_ERR_ARG, "network %d unknown", net);
   // analytic networks use no hidden layers (the ICNN fields are ignored)
@@ -53,6 +53,8 @@ extern "C" commet_status commet_setup(const commet_mesh_desc* mesh, const commet
       return fail(C, COMMET_ERR_ARG, "width %d unsupported (8, 16, 32, 64 or 128)", w);
     if (!ncm->W1 || !ncm->b || !ncm->a || (L > 1 && !ncm->W))
       return fail(C, COMMET_ERR_ARG, "NCM weight pointer NULL (W1, b, a or W)");
+    if (nk != 3 && ncm->skip_hidden)
+      return fail(C, COMMET_ERR_ARG, "hidden skips B^(k) act on (K1, K2, K3) only: skip_hidden must be NULL for 5 inputs");
   }
   int64_t kan_edges = 0;
   if (net == COMMET_NET_ICKAN) {
@@ -156,9 +158,9 @@ extern "C" commet_status commet_setup(const commet_mesh_desc* mesh, const commet
 
   // ---- NCM ---------------------------------------------------------------------------------
   commet_status s;
-  std::vector<double> zeros3(3, 0.0), zw((size_t)L * w * 3 + 3, 0.0);
+  std::vector<double> zeros3(3, 0.0), zw((size_t)L * w * 5 + 5, 0.0);
   const bool icnn = net == COMMET_NET_ICNN;
-  if ((s = upload(C, c->W1, icnn ? ncm->W1 : zw.data(), (size_t)w * 3, st))) return s;
+  if ((s = upload(C, c->W1, icnn ? ncm->W1 : zw.data(), (size_t)w * nk, st))) return s;
   if ((s = upload(C, c->b, icnn ? ncm->b : zw.data(), (size_t)L * w, st))) return s;
   if ((s = upload(C, c->a, icnn ? ncm->a : zw.data(), (size_t)w, st))) return s;
   if (net == COMMET_NET_ICKAN) {
@@ -184,11 +186,8 @@ extern "C" commet_status commet_setup(const commet_mesh_desc* mesh, const commet
   std::vector<double> tab(kActTabSize);
   fill_act_table(tab.data());
   if ((s = upload(C, c->act_tab, tab.data(), tab.size(), st))) return s;
-  std::vector<double> gf((size_t)2 * 16 * w);
-  fused_gfrag_fill(w, icnn ? ncm->W1 : zw.data(), gf.data());
-  if ((s = upload(C, c->gfrag, gf.data(), gf.size(), st))) return s;
   c->ncm = NcmDev{L, w, c->W1.p, c->b.p, c->a.p, c->skip_out.p, c->skip_h.p, c->Wrow.p, c->Wfrag.p,
-                  c->act_tab.p, c->gfrag.p, ncm->kappa, ncm->ref_shift, kin, net,
+                  c->act_tab.p, ncm->kappa, ncm->ref_shift, kin, net,
                   net == COMMET_NET_CANN ? ncm->cann_n : 0, c->cann_f.p, c->cann_w1.p, c->cann_w2.p,
                   {ncm->gt[0], ncm->gt[1], ncm->gt[2]},
                   net == COMMET_NET_ICKAN ? ncm->kan_layers : 0, net == COMMET_NET_ICKAN ? ncm->kan_nb : 0,
@@ -426,11 +425,19 @@ extern "C" commet_status commet_kernel_info(commet_ctx c, int32_t* smem_bytes, i
                                             int32_t* regs_per_thread) {
   if (!c) return fail(nullptr, COMMET_ERR_ARG, "ctx is NULL");
   CUDA_TRY(c, cudaSetDevice(c->device));
-  int a = 0, b = 0, r = 0;
-  fused_occupancy(c->plan.n_en, c->ncm.net ? 0 : c->ncm.w, c->ncm.L, &a, &b, &r);
-  if (smem_bytes) *smem_bytes = a;
-  if (ctas_per_sm) *ctas_per_sm = b;
-  if (regs_per_thread) *regs_per_thread = r;
+  // the instantiation the assembly (or material-point) dispatch launches for this ctx
+  int q[3] = {0, 0, 0};
+  AsmArgs a{};
+  a.n_en = c->material_only ? 1 : c->plan.n_en;
+  a.n_q = c->material_only ? 1 : c->plan.n_q;
+  a.el_count = 1;
+  a.ncm = c->ncm;
+  a.query = q;
+  const int e = c->material_only ? launch_material(a, nullptr) : launch_fused(a, nullptr, nullptr);
+  if (e) return fail(c, COMMET_ERR_CUDA, "kernel query: %s", cudaGetErrorString((cudaError_t)e));
+  if (smem_bytes) *smem_bytes = q[0];
+  if (ctas_per_sm) *ctas_per_sm = q[1];
+  if (regs_per_thread) *regs_per_thread = q[2];
   return COMMET_OK;
 }
 

@@ -30,7 +30,6 @@ struct NcmDev {
   const double* Wrow;     // [L-1][w][w] row-major (simple kernel)
   const double* Wfrag;    // [L-1][2][frag] fragment-ordered W and W^T (fused kernel)
   const double* act_tab;  // [kActTabSize] softplus tables (qp_math.cuh)
-  const double* gfrag;    // [2][16 x w] fragments of [W1^T | 0] and [0 | V] (stage 5)
   double kappa, ref_shift;
   int kin, net, cann_n;   // variants (commet.h COMMET_KIN_* / COMMET_NET_*)
   const int32_t* cann_f;  // [3][n][3]
@@ -77,6 +76,9 @@ struct AsmArgs {
   double* tau_out;
   double* c_out;
   NcmDev ncm;
+  // launch query: when set, the dispatcher writes the chosen instantiation's {smem bytes,
+  // CTAs per SM, registers per thread} here and launches nothing (commet_kernel_info)
+  int* query;
 };
 
 // launchers (kernel_simple.cu / kernel_fused.cu); return cudaError_t as int
@@ -87,11 +89,9 @@ int launch_activation(const double* y, double* z, double* s, int64_t n, const do
 int launch_fused(const AsmArgs& a, void* stream, int* launches);
 int launch_material(const AsmArgs& a, void* stream);
 int fused_supported(int n_en, int n_q, int w, int L);
-void fused_occupancy(int n_en, int w, int L, int* smem_bytes, int* ctas_per_sm, int* regs);
 // prepares the fragment-ordered weight array on the host (size in doubles)
 int64_t fused_weight_frag_size(int w, int L);
 void fused_weight_frag_fill(int w, int L, const double* Wrow, double* out);
 // stage-5 fragments: 2 matrices of 16 x w (rows 0-2 W1^T; rows 3-8 W1_jm W1_jn)
-void fused_gfrag_fill(int w, const double* W1, double* out);
 
 }  // namespace commet

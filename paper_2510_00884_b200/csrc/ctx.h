@@ -51,7 +51,7 @@ struct commet_ctx_s {
   DevBuf<uint8_t> slot;
   DevBuf<int64_t> orig, node_rs, row_ptr;
   DevBuf<int32_t> node_deg;
-  DevBuf<double> W1, b, a, skip_out, skip_h, Wrow, Wfrag, act_tab, gfrag;
+  DevBuf<double> W1, b, a, skip_out, skip_h, Wrow, Wfrag, act_tab;
   DevBuf<int32_t> cann_f;
   DevBuf<double> cann_w1, cann_w2, kan_grid, kan_w, kan_c;
   DevBuf<double> r_halo, v_halo, r_recv, v_recv;

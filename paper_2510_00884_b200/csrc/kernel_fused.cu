@@ -46,6 +46,14 @@
 #ifndef COMMET_PD_J
 #define COMMET_PD_J 2
 #endif
+// analytic-network (NET = 1) instantiations, measured on c3 (tools/ab_bench.py AB_NET=...):
+// ICKAN and the 5-input networks run 32 qps per CTA iteration (one full warp in the per-qp
+// stage 7a; 16: ICKAN -19 %, CANN-5 -21 %) at 2 CTAs/SM (no spills at 254 registers;
+// 4 CTAs: ICKAN-5 -21 %, CANN-5 -20 %; ICKAN at 3: -2 %); Gent-Thomas / CANN keep
+// 16 qps (32: -15 % / -6 %)
+#ifndef COMMET_ICKAN_MINB
+#define COMMET_ICKAN_MINB 2
+#endif
 #ifndef COMMET_ANALYTIC_MINB
 #define COMMET_ANALYTIC_MINB 4  // CTAs per SM of the analytic-network (NET = 1) kernels (measured: GT +7 %, CANN +4 % over 3)
 #endif
@@ -123,7 +131,7 @@ struct Cfg {
   static constexpr int W = W_, Q = Q_, NEN = NEN_, NQ = NQ_, NET = NET_, KIN = KIN_, MODE = MODE_;
   // network inputs per qp: 3 (standard / isochoric invariants) or 5 (anisotropic: + I4, I5)
   static constexpr int NK = KIN == 2 ? 5 : 3, NH = NK * (NK + 1) / 2;
-  static_assert(KIN != 2 || NET == 1, "anisotropic inputs: analytic networks only");
+  static constexpr int NP = NK + NH;  // adjoint-pass partials per qp: g (NK) and H_1 (NH)
   static constexpr int NWARP = NW_, NTHR = 32 * NW_;
   static constexpr int MINB = MINB_;               // CTAs per SM the register budget targets (3: <= 168 regs)
   static constexpr bool DMMA_ELEM = MODE == 0 && (COMMET_DMMA_ELEM == 2 || (COMMET_DMMA_ELEM == 1 && NEN == 8));
@@ -140,7 +148,7 @@ struct Cfg {
   static constexpr int JMG = NWARP / QB, MT_J = MTILES / JMG;
   // A-fragment register ring depth (k-steps) of the value/adjoint and Jacobian GEMMs
   static constexpr int PD_V = COMMET_PD_V, PD_J = COMMET_PD_J;
-  static constexpr int LDA = 3 * Q + 4;            // act row stride (= 4 mod 16: conflict-free B frags)
+  static constexpr int LDA = NK * Q + 4;           // act row stride (= 4 mod 16: conflict-free B frags)
   static constexpr int LDS = Q + 2;                // s/c row stride (2-way conflicts at most)
   static_assert(W % 8 == 0 && Q % 8 == 0 && Q % NQ == 0, "tile");
   static_assert(Q <= 32, "stage-1 threads (one per qp) must sit in warp 0");
@@ -148,8 +156,8 @@ struct Cfg {
   static_assert(JMG >= 1 && JMG * QB == NWARP && MT_J * JMG == MTILES, "jacobian tiling");
   // ping-pong of the value / adjoint passes between act column blocks [0, Q) and [Q, 2Q), the
   // adjoint-pass g/H_1 partials in rows 9 vm + x of the free block [2Q, 3Q) (needs VMG*9 <= W)
-  static constexpr bool PP = COMMET_PINGPONG && VMG * 9 <= W;
-  static_assert(PP || VMG * Q * 9 <= W * LDA, "adjoint partials must fit in act");
+  static constexpr bool PP = COMMET_PINGPONG && NK == 3 && VMG * 9 <= W;
+  static_assert(PP || VMG * Q * NP <= W * LDA, "adjoint partials must fit in act");
 };
 
 // shared-memory carve-up (doubles); L is a runtime value.  The post-NCM
@@ -161,17 +169,19 @@ struct Smem {
   int act, sb, cb, qF, qk, qg, qH, hred, gsk, gN, ue, wq, qN, tab, qP, post, X, qA, total;
   __host__ __device__ Smem(int L) {
     int o = 0;
-    act = o; o += C::W * C::LDA;
-    sb = o;  o += (L > 1 ? L - 1 : 0) * C::W * C::LDS;   // s_l, l = 1..L-1
-    cb = o;  o += (L > 1 ? L - 1 : 1) * C::W * C::LDS;   // c_l, l = 2..L (L == 1: c_1)
+    // the network buffers: ICNN only (the analytic networks run per qp in registers)
+    const bool icnn = C::NET == 0;
+    act = o; o += icnn ? C::W * C::LDA : 0;
+    sb = o;  o += icnn ? (L > 1 ? L - 1 : 0) * C::W * C::LDS : 0;   // s_l, l = 1..L-1
+    cb = o;  o += icnn ? (L > 1 ? L - 1 : 1) * C::W * C::LDS : 0;   // c_l, l = 2..L (L == 1: c_1)
     const int dead = o;
     qF = o;  o += C::Q * 9;
     qk = o;  o += C::Q * C::NK;
-    qg = o;  o += C::Q * 3;
-    qH = o;  o += C::Q * 6;
-    hred = o; o += C::JMG * C::Q * 6;  // Jacobian-pass H partials per warp row group
+    qg = o;  o += C::Q * C::NK;
+    qH = o;  o += C::Q * C::NH;
+    hred = o; o += C::JMG * C::Q * C::NH;  // Jacobian-pass H partials per warp row group
     // (the adjoint-pass g/H_1 partials, VMG x Q x 9, live in act: dead at that point)
-    gsk = o; o += C::Q * 3;
+    gsk = o; o += C::Q * C::NK;
     gN = o;  o += C::Q * C::NEN * 3;
     ue = o;  o += C::E * C::NEN * 3;
     wq = o;  o += C::Q;
@@ -252,13 +262,13 @@ __device__ __forceinline__ void material_outputs(const AsmArgs& A, const NcmDev&
     const double* kq = qk + q * C::NK;
     if constexpr (C::NET == 0) {
 #pragma unroll
-      for (int x = 0; x < 3; x++) gq[x] = qg[q * 3 + x];
+      for (int x = 0; x < C::NK; x++) gq[x] = qg[q * C::NK + x];
 #pragma unroll
-      for (int x = 0; x < 6; x++) {
-        double s = qH[q * 6 + x];
+      for (int x = 0; x < C::NH; x++) {
+        double s = qH[q * C::NH + x];
         if (L > 1)
 #pragma unroll
-          for (int r = 0; r < C::JMG; r++) s += hred[(r * Q + q) * 6 + x];
+          for (int r = 0; r < C::JMG; r++) s += hred[(r * Q + q) * C::NH + x];
         H6[x] = s;
       }
       const int rows = L > 1 ? C::VMG : C::NTHR / Q;
@@ -412,7 +422,9 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
 
   // adjoint-pass g/H_1 partial (row group r, qp q, entry x): with ping-pong in the block
   // [2Q, 3Q) of act, free during the value and adjoint passes; otherwise packed at the start
-  auto part_at = [&](int r, int q, int x) { return C::PP ? (r * 9 + x) * LDA + 2 * Q + q : (r * Q + q) * 9 + x; };
+  auto part_at = [&](int r, int q, int x) {
+    return C::PP ? (r * 9 + x) * LDA + 2 * Q + q : (r * Q + q) * C::NP + x;
+  };
 
   for (int64_t batch = blockIdx.x; batch < n_batches; batch += gridDim.x) {
     const int64_t e0 = A.el_begin + batch * E;
@@ -498,7 +510,8 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
         qk[q * 3 + 1] = kin.I2 - 3.0;
         qk[q * 3 + 2] = kin.J - 1.0;
       }
-      gsk[q * 3 + 0] = gsk[q * 3 + 1] = gsk[q * 3 + 2] = 0.0;
+#pragma unroll
+      for (int x = 0; x < C::NK; x++) gsk[q * C::NK + x] = 0.0;
     }
     __syncthreads();
     STAGE_MARK(1)
@@ -515,13 +528,17 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
       constexpr int NIT = W * Q / C::NTHR, JS = C::NTHR / Q;
       static_assert(W * Q % C::NTHR == 0 && C::NTHR % Q == 0, "layer-1 split");
       const int q = tid % Q, j0 = tid / Q;
-      const double k0 = qk[q * 3 + 0], k1 = qk[q * 3 + 1], k2 = qk[q * 3 + 2];
+      double kq[C::NK];
+#pragma unroll
+      for (int x = 0; x < C::NK; x++) kq[x] = qk[q * C::NK + x];
       double yv[NIT];
 #pragma unroll
       for (int i = 0; i < NIT; i++) {
         const int j = j0 + i * JS;
-        yv[i] = __ldg(m.b + j) + __ldg(m.W1 + j * 3 + 0) * k0 + __ldg(m.W1 + j * 3 + 1) * k1 +
-                __ldg(m.W1 + j * 3 + 2) * k2;
+        double y = __ldg(m.b + j);
+#pragma unroll
+        for (int x = 0; x < C::NK; x++) y += __ldg(m.W1 + j * C::NK + x) * kq[x];
+        yv[i] = y;
       }
       double nv = 0.0;  // material mode, L == 1: partial a . z_1 of this thread's neurons
 #pragma unroll
@@ -584,7 +601,7 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
             for (int h = 0; h < 2; h++) {
               const int q = ncol[jj] + 2 * t + h;
               double y = acc[i][jj][h] + bj;
-              if (skips) y += B3[0] * qk[q * 3] + B3[1] * qk[q * 3 + 1] + B3[2] * qk[q * 3 + 2];
+              if (skips) y += B3[0] * qk[q * C::NK] + B3[1] * qk[q * C::NK + 1] + B3[2] * qk[q * C::NK + 2];
               if constexpr (C::MODE == 1) {  // material points need the value: z_L too
                 if (l == L) {
                   double z, s;
@@ -642,7 +659,7 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
             const double mu = act[j * LDA + cur * Q + tid];
             s0 += __ldg(Bl + j * 3) * mu; s1 += __ldg(Bl + j * 3 + 1) * mu; s2 += __ldg(Bl + j * 3 + 2) * mu;
           }
-          gsk[tid * 3] += s0; gsk[tid * 3 + 1] += s1; gsk[tid * 3 + 2] += s2;
+          gsk[tid * C::NK] += s0; gsk[tid * C::NK + 1] += s1; gsk[tid * C::NK + 2] += s2;
         }
         double acc[C::MT_V][C::NT_V][2];
         int ncr[C::NT_V];
@@ -675,17 +692,20 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
         } else {
           // l == 2: lambda_1 -> mu_1, c_1 consumed here: g = W1^T mu_1, H_1 = W1^T diag(c_1) W1,
           // partial over this thread's rows, reduced over the warp's row groups g
-          double pg[C::NT_V][2][9];
+          constexpr int NK = C::NK, NP = C::NP;
+          double pg[C::NT_V][2][NP];
 #pragma unroll
           for (int jj = 0; jj < C::NT_V; jj++)
 #pragma unroll
             for (int h = 0; h < 2; h++)
 #pragma unroll
-              for (int x = 0; x < 9; x++) pg[jj][h][x] = 0.0;
+              for (int x = 0; x < NP; x++) pg[jj][h][x] = 0.0;
 #pragma unroll
           for (int i = 0; i < C::MT_V; i++) {
             const int j = (mt0 + i) * 8 + g;
-            const double w0 = __ldg(m.W1 + j * 3), w1 = __ldg(m.W1 + j * 3 + 1), w2 = __ldg(m.W1 + j * 3 + 2);
+            double wv[NK];
+#pragma unroll
+            for (int x = 0; x < NK; x++) wv[x] = __ldg(m.W1 + j * NK + x);
 #pragma unroll
             for (int jj = 0; jj < C::NT_V; jj++)
 #pragma unroll
@@ -695,10 +715,23 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
                 const double s = sb[j * LDS + q];
                 const double mu = lam * s, c = mu * (1.0 - s);
                 double* P9 = pg[jj][h];
-                P9[0] += w0 * mu; P9[1] += w1 * mu; P9[2] += w2 * mu;
-                const double c0 = c * w0, c1 = c * w1;
-                P9[3] += c0 * w0; P9[4] += c0 * w1; P9[5] += c0 * w2;
-                P9[6] += c1 * w1; P9[7] += c1 * w2; P9[8] += c * w2 * w2;
+                if constexpr (NK == 3) {  // (the generic form below costs ~1 % on c3: kept explicit)
+                  const double w0 = wv[0], w1 = wv[1], w2 = wv[2];
+                  P9[0] += w0 * mu; P9[1] += w1 * mu; P9[2] += w2 * mu;
+                  const double c0 = c * w0, c1 = c * w1;
+                  P9[3] += c0 * w0; P9[4] += c0 * w1; P9[5] += c0 * w2;
+                  P9[6] += c1 * w1; P9[7] += c1 * w2; P9[8] += c * w2 * w2;
+                } else {
+#pragma unroll
+                  for (int x = 0; x < NK; x++) P9[x] += wv[x] * mu;
+                  int o = NK;
+#pragma unroll
+                  for (int a1 = 0; a1 < NK; a1++) {
+                    const double ca = c * wv[a1];
+#pragma unroll
+                    for (int a2 = a1; a2 < NK; a2++) P9[o++] += ca * wv[a2];
+                  }
+                }
               }
           }
 #pragma unroll
@@ -706,7 +739,7 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
 #pragma unroll
             for (int h = 0; h < 2; h++)
 #pragma unroll
-              for (int x = 0; x < 9; x++) {
+              for (int x = 0; x < NP; x++) {
                 double v = pg[jj][h][x];
                 v += __shfl_xor_sync(0xffffffffu, v, 4);
                 v += __shfl_xor_sync(0xffffffffu, v, 8);
@@ -719,7 +752,7 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
 #pragma unroll
               for (int h = 0; h < 2; h++)
 #pragma unroll
-                for (int x = 0; x < 9; x++) act[part_at(vm, ncol[jj] + 2 * t + h, x)] = pg[jj][h][x];
+                for (int x = 0; x < C::NP; x++) act[part_at(vm, ncol[jj] + 2 * t + h, x)] = pg[jj][h][x];
           }
         }
         __syncthreads();
@@ -732,41 +765,61 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
     if (L > 1) {
       if (tid < Q) {
         const int q = tid;
-        double v[9];
+        double v[C::NP];
 #pragma unroll
-        for (int x = 0; x < 9; x++) v[x] = 0.0;
+        for (int x = 0; x < C::NP; x++) v[x] = 0.0;
 #pragma unroll
         for (int r = 0; r < C::VMG; r++)
 #pragma unroll
-          for (int x = 0; x < 9; x++) v[x] += act[part_at(r, q, x)];
+          for (int x = 0; x < C::NP; x++) v[x] += act[part_at(r, q, x)];
 #pragma unroll
-        for (int x = 0; x < 3; x++) qg[q * 3 + x] = v[x] + gsk[q * 3 + x] + __ldg(m.skip_out + x);
+        for (int x = 0; x < C::NK; x++)
+          qg[q * C::NK + x] = v[x] + gsk[q * C::NK + x] + (x < 3 ? __ldg(m.skip_out + x) : 0.0);
 #pragma unroll
-        for (int x = 0; x < 6; x++) qH[q * 6 + x] = v[3 + x];
+        for (int x = 0; x < C::NH; x++) qH[q * C::NH + x] = v[C::NK + x];
       }
     } else {
       constexpr int P = C::NTHR / Q;  // threads per qp (lanes q*P .. q*P+P-1 share a warp)
       const int q = tid / P, part = tid % P;
-      double gs[3] = {0, 0, 0}, hs[6] = {0, 0, 0, 0, 0, 0};
+      double gs[C::NK], hs[C::NH];
+#pragma unroll
+      for (int x = 0; x < C::NK; x++) gs[x] = 0.0;
+#pragma unroll
+      for (int x = 0; x < C::NH; x++) hs[x] = 0.0;
       for (int j = part; j < W; j += P) {
-        const double w0 = __ldg(m.W1 + j * 3), w1 = __ldg(m.W1 + j * 3 + 1), w2 = __ldg(m.W1 + j * 3 + 2);
-        const double mu = act[j * LDA + q], c = cb[j * LDS + q];
-        gs[0] += w0 * mu; gs[1] += w1 * mu; gs[2] += w2 * mu;
-        hs[0] += c * w0 * w0; hs[1] += c * w0 * w1; hs[2] += c * w0 * w2;
-        hs[3] += c * w1 * w1; hs[4] += c * w1 * w2; hs[5] += c * w2 * w2;
+        if constexpr (C::NK == 3) {
+          const double w0 = __ldg(m.W1 + j * 3), w1 = __ldg(m.W1 + j * 3 + 1), w2 = __ldg(m.W1 + j * 3 + 2);
+          const double mu = act[j * LDA + q], c = cb[j * LDS + q];
+          gs[0] += w0 * mu; gs[1] += w1 * mu; gs[2] += w2 * mu;
+          hs[0] += c * w0 * w0; hs[1] += c * w0 * w1; hs[2] += c * w0 * w2;
+          hs[3] += c * w1 * w1; hs[4] += c * w1 * w2; hs[5] += c * w2 * w2;
+        } else {
+          double wv[C::NK];
+#pragma unroll
+          for (int x = 0; x < C::NK; x++) wv[x] = __ldg(m.W1 + j * C::NK + x);
+          const double mu = act[j * LDA + q], c = cb[j * LDS + q];
+#pragma unroll
+          for (int x = 0; x < C::NK; x++) gs[x] += wv[x] * mu;
+          int o = 0;
+#pragma unroll
+          for (int a1 = 0; a1 < C::NK; a1++)
+#pragma unroll
+            for (int a2 = a1; a2 < C::NK; a2++) hs[o++] += c * wv[a1] * wv[a2];
+        }
       }
 #pragma unroll
       for (int o = 1; o < P; o <<= 1) {
 #pragma unroll
-        for (int x = 0; x < 3; x++) gs[x] += __shfl_xor_sync(0xffffffffu, gs[x], o);
+        for (int x = 0; x < C::NK; x++) gs[x] += __shfl_xor_sync(0xffffffffu, gs[x], o);
 #pragma unroll
-        for (int x = 0; x < 6; x++) hs[x] += __shfl_xor_sync(0xffffffffu, hs[x], o);
+        for (int x = 0; x < C::NH; x++) hs[x] += __shfl_xor_sync(0xffffffffu, hs[x], o);
       }
       if (part == 0) {
 #pragma unroll
-        for (int x = 0; x < 3; x++) qg[q * 3 + x] = gs[x] + gsk[q * 3 + x] + __ldg(m.skip_out + x);
+        for (int x = 0; x < C::NK; x++)
+          qg[q * C::NK + x] = gs[x] + gsk[q * C::NK + x] + (x < 3 ? __ldg(m.skip_out + x) : 0.0);
 #pragma unroll
-        for (int x = 0; x < 6; x++) qH[q * 6 + x] = hs[x];
+        for (int x = 0; x < C::NH; x++) qH[q * C::NH + x] = hs[x];
       }
     }
     __syncthreads();
@@ -777,56 +830,77 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
       {  // D_1 = s_1 (.) W1: one qp per thread, weights loaded up front
         constexpr int NIT = W * Q / C::NTHR, JS = C::NTHR / Q;
         const int q = tid % Q, j0 = tid / Q;
-        double w1v[NIT][3];
+        double w1v[NIT][C::NK];
 #pragma unroll
         for (int i = 0; i < NIT; i++)
 #pragma unroll
-          for (int c = 0; c < 3; c++) w1v[i][c] = __ldg(m.W1 + (j0 + i * JS) * 3 + c);
+          for (int c = 0; c < C::NK; c++) w1v[i][c] = __ldg(m.W1 + (j0 + i * JS) * C::NK + c);
 #pragma unroll
         for (int i = 0; i < NIT; i++) {
           const int j = j0 + i * JS;
           const double s = sb[j * LDS + q];
 #pragma unroll
-          for (int c = 0; c < 3; c++) act[j * LDA + c * Q + q] = s * w1v[i][c];
+          for (int c = 0; c < C::NK; c++) act[j * LDA + c * Q + q] = s * w1v[i][c];
         }
       }
       __syncthreads();
       const int jm = warp / C::QB, qb = warp % C::QB;
       const int mt0 = jm * C::MT_J;
-      int ncol[3];
+      constexpr int NK = C::NK, NH = C::NH;
+      int ncol[NK];
 #pragma unroll
-      for (int c = 0; c < 3; c++) ncol[c] = c * Q + qb * 8;
-      double hp[2][6];
+      for (int c = 0; c < NK; c++) ncol[c] = c * Q + qb * 8;
+      double hp[2][NH];
 #pragma unroll
       for (int h = 0; h < 2; h++)
 #pragma unroll
-        for (int x = 0; x < 6; x++) hp[h][x] = 0.0;
+        for (int x = 0; x < NH; x++) hp[h][x] = 0.0;
       for (int l = 2; l <= L; l++) {
-        double acc[C::MT_J][3][2];
-        warp_gemm<C::MT_J, 3, KT2, C::PD_J>(m.Wfrag + (l - 2) * frag_layer, mt0, act, LDA, ncol, acc);
+        double acc[C::MT_J][NK][2];
+        warp_gemm<C::MT_J, NK, KT2, C::PD_J>(m.Wfrag + (l - 2) * frag_layer, mt0, act, LDA, ncol, acc);
         __syncthreads();
         if (l < L) frag_prefetch<C::MT_J, KT2, (COMMET_FRAG_PF + 1) / 2>(m.Wfrag + (l - 1) * frag_layer, mt0);
 #pragma unroll
         for (int i = 0; i < C::MT_J; i++) {
           const int j = (mt0 + i) * 8 + g;
-          double B3[3] = {0, 0, 0};
-          if (skips) {
+          double B3[NK];
+#pragma unroll
+          for (int x = 0; x < NK; x++) B3[x] = 0.0;
+          if (skips) {  // hidden skips act on the first three inputs only (API: NK == 3)
             const double* Bl = m.skip_h + ((size_t)(l - 2) * W + j) * 3;
             B3[0] = __ldg(Bl); B3[1] = __ldg(Bl + 1); B3[2] = __ldg(Bl + 2);
           }
 #pragma unroll
           for (int h = 0; h < 2; h++) {
             const int q = qb * 8 + 2 * t + h;
-            const double J0 = acc[i][0][h] + B3[0], J1 = acc[i][1][h] + B3[1], J2 = acc[i][2][h] + B3[2];
             const double c = cb[((l - 2) * W + j) * LDS + q];
-            const double c0 = c * J0, c1 = c * J1, c2 = c * J2;
-            hp[h][0] += c0 * J0; hp[h][1] += c0 * J1; hp[h][2] += c0 * J2;
-            hp[h][3] += c1 * J1; hp[h][4] += c1 * J2; hp[h][5] += c2 * J2;
-            if (l < L) {
-              const double s = sb[((l - 1) * W + j) * LDS + q];
-              act[j * LDA + q] = s * J0;
-              act[j * LDA + Q + q] = s * J1;
-              act[j * LDA + 2 * Q + q] = s * J2;
+            if constexpr (NK == 3) {  // (explicit: the generic form costs ~1 % on c3)
+              const double J0 = acc[i][0][h] + B3[0], J1 = acc[i][1][h] + B3[1], J2 = acc[i][2][h] + B3[2];
+              const double c0 = c * J0, c1 = c * J1, c2 = c * J2;
+              hp[h][0] += c0 * J0; hp[h][1] += c0 * J1; hp[h][2] += c0 * J2;
+              hp[h][3] += c1 * J1; hp[h][4] += c1 * J2; hp[h][5] += c2 * J2;
+              if (l < L) {
+                const double s = sb[((l - 1) * W + j) * LDS + q];
+                act[j * LDA + q] = s * J0;
+                act[j * LDA + Q + q] = s * J1;
+                act[j * LDA + 2 * Q + q] = s * J2;
+              }
+            } else {
+              double Jv[NK];
+#pragma unroll
+              for (int x = 0; x < NK; x++) Jv[x] = acc[i][x][h] + B3[x];
+              int o = 0;
+#pragma unroll
+              for (int a1 = 0; a1 < NK; a1++) {
+                const double ca = c * Jv[a1];
+#pragma unroll
+                for (int a2 = a1; a2 < NK; a2++) hp[h][o++] += ca * Jv[a2];
+              }
+              if (l < L) {
+                const double s = sb[((l - 1) * W + j) * LDS + q];
+#pragma unroll
+                for (int x = 0; x < NK; x++) act[j * LDA + x * Q + q] = s * Jv[x];
+              }
             }
           }
         }
@@ -836,7 +910,7 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
 #pragma unroll
       for (int h = 0; h < 2; h++)
 #pragma unroll
-        for (int x = 0; x < 6; x++) {
+        for (int x = 0; x < NH; x++) {
           double v = hp[h][x];
           v += __shfl_xor_sync(0xffffffffu, v, 4);
           v += __shfl_xor_sync(0xffffffffu, v, 8);
@@ -847,7 +921,7 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
 #pragma unroll
         for (int h = 0; h < 2; h++)
 #pragma unroll
-          for (int x = 0; x < 6; x++) hred[(jm * Q + qb * 8 + 2 * t + h) * 6 + x] = hp[h][x];
+          for (int x = 0; x < NH; x++) hred[(jm * Q + qb * 8 + 2 * t + h) * NH + x] = hp[h][x];
       }
       __syncthreads();
     }
@@ -872,13 +946,13 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
       double gq[C::NK], H6[C::NH];
       if constexpr (C::NET == 0) {
 #pragma unroll
-        for (int x = 0; x < 3; x++) gq[x] = qg[q * 3 + x];
+        for (int x = 0; x < C::NK; x++) gq[x] = qg[q * C::NK + x];
 #pragma unroll
-        for (int x = 0; x < 6; x++) {
-          double s = qH[q * 6 + x];
+        for (int x = 0; x < C::NH; x++) {
+          double s = qH[q * C::NH + x];
           if (L > 1)
 #pragma unroll
-            for (int r = 0; r < C::JMG; r++) s += hred[(r * Q + q) * 6 + x];
+            for (int r = 0; r < C::JMG; r++) s += hred[(r * Q + q) * C::NH + x];
           H6[x] = s;
         }
       } else {
@@ -1093,27 +1167,6 @@ void fused_weight_frag_fill(int w, int L, const double* Wrow, double* out) {
   }
 }
 
-void fused_gfrag_fill(int w, const double* W1, double* out) {
-  const int KT2 = w / 8;
-  for (int which = 0; which < 2; which++) {
-    double* f = out + (size_t)which * 16 * w;
-    for (int mt = 0; mt < 2; mt++)
-      for (int kt2 = 0; kt2 < KT2; kt2++)
-        for (int lane = 0; lane < 32; lane++)
-          for (int h = 0; h < 2; h++) {
-            const int g = lane >> 2, t = lane & 3;
-            const int r = 8 * mt + g, j = 8 * kt2 + 4 * h + t;
-            double v = 0.0;
-            if (which == 0 && r < 3) v = W1[j * 3 + r];
-            if (which == 1 && r >= 3 && r < 9) {
-              static const int pm[6] = {0, 0, 0, 1, 1, 2}, pn[6] = {0, 1, 2, 1, 2, 2};
-              v = W1[j * 3 + pm[r - 3]] * W1[j * 3 + pn[r - 3]];
-            }
-            f[((size_t)(mt * KT2 + kt2) * 32 + lane) * 2 + h] = v;
-          }
-  }
-}
-
 template <class C>
 static int launch_cfg(const AsmArgs& a, cudaStream_t st, int* launches) {
   const Smem<C> sm(a.ncm.L);
@@ -1143,6 +1196,14 @@ static int launch_cfg(const AsmArgs& a, cudaStream_t st, int* launches) {
     per_sm_c[dev] = per_sm < 1 ? 1 : per_sm;
     occ_bytes[dev] = bytes;
   }
+  if (a.query) {
+    cudaFuncAttributes fa{};
+    cudaFuncGetAttributes(&fa, fused_kernel<C>);
+    a.query[0] = (int)bytes;
+    a.query[1] = per_sm_c[dev];
+    a.query[2] = fa.numRegs;
+    return 0;
+  }
   const int64_t nb = (a.el_count + C::E - 1) / C::E;
   const int64_t grid = std::min<int64_t>(nb, (int64_t)sms_c[dev] * per_sm_c[dev]);
   if (grid <= 0) return 0;
@@ -1151,49 +1212,23 @@ static int launch_cfg(const AsmArgs& a, cudaStream_t st, int* launches) {
   return (int)cudaGetLastError();
 }
 
-template <class C>
-static void occ_cfg(int L, int* smem_bytes, int* ctas_per_sm, int* regs) {
-  const Smem<C> sm(L);
-  const size_t bytes = (size_t)sm.total * sizeof(double);
-  cudaFuncSetAttribute(fused_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fused_kernel<C>, C::NTHR, bytes);
-  cudaFuncAttributes fa{};
-  cudaFuncGetAttributes(&fa, fused_kernel<C>);
-  *smem_bytes = (int)bytes;
-  *ctas_per_sm = per_sm;
-  *regs = fa.numRegs;
-}
-
-template <int NEN, int NQ>
-static void occ_et(int w, int L, int* a, int* b, int* c) {
-  if (w == 0) return occ_cfg<Cfg<16, 16, NEN, NQ, COMMET_ANALYTIC_MINB, 1>>(1, a, b, c);  // analytic networks
-  switch (w) {
-    case 8: occ_cfg<Cfg<8, 32, NEN, NQ>>(L, a, b, c); break;
-    case 16: occ_cfg<Cfg<16, 16, NEN, NQ>>(L, a, b, c); break;
-    case 32: occ_cfg<Cfg<32, 16, NEN, NQ>>(L, a, b, c); break;
-    case 64: occ_cfg<Cfg<64, 16, NEN, NQ>>(L, a, b, c); break;
-    case 128: occ_cfg<Cfg<128, 8, NEN, NQ>>(L, a, b, c); break;
-  }
-}
-
-void fused_occupancy(int n_en, int w, int L, int* smem_bytes, int* ctas_per_sm, int* regs) {
-  if (n_en == 8) occ_et<8, 8>(w, L, smem_bytes, ctas_per_sm, regs);
-  else occ_et<10, 4>(w, L, smem_bytes, ctas_per_sm, regs);
-}
-
 template <int NEN, int NQ, int K>
 static int launch_k(const AsmArgs& a, cudaStream_t st, int* launches) {
-  if (a.ncm.net == 3)  // ICKAN: its per-qp forward mode needs the registers of 3 CTAs/SM (4: spills, -14 %)
-    return launch_cfg<Cfg<16, 16, NEN, NQ, 3, 1, K>>(a, st, launches);
-  if (a.ncm.net != 0 || K == 2) return launch_cfg<Cfg<16, 16, NEN, NQ, COMMET_ANALYTIC_MINB, 1, K>>(a, st, launches);
-  if constexpr (K != 2)
+  if constexpr (K == 2) {  // 5 inputs: packed 5x5 Hessians and the extended F-space factors
+    if (a.ncm.net != 0) return launch_cfg<Cfg<16, 32, NEN, NQ, 2, 1, K>>(a, st, launches);
+  } else {
+    if (a.ncm.net == 3)  // ICKAN: its per-qp forward mode needs the registers (4 CTAs/SM: spills, -14 %)
+      return launch_cfg<Cfg<16, 32, NEN, NQ, COMMET_ICKAN_MINB, 1, K>>(a, st, launches);
+    if (a.ncm.net != 0) return launch_cfg<Cfg<16, 16, NEN, NQ, COMMET_ANALYTIC_MINB, 1, K>>(a, st, launches);
+  }
+  // 5-input ICNN: the Jacobian pass carries 5 columns and 15 Hessian partials -> 2 CTAs/SM
+  constexpr int MB = K == 2 ? 2 : 3;
   switch (a.ncm.w) {
-    case 8: return launch_cfg<Cfg<8, 32, NEN, NQ, 3, 0, K>>(a, st, launches);
-    case 16: return launch_cfg<Cfg<16, 16, NEN, NQ, 3, 0, K>>(a, st, launches);
-    case 32: return launch_cfg<Cfg<32, 16, NEN, NQ, 3, 0, K>>(a, st, launches);
-    case 64: return launch_cfg<Cfg<64, 16, NEN, NQ, 3, 0, K>>(a, st, launches);
-    case 128: return launch_cfg<Cfg<128, 8, NEN, NQ, 3, 0, K>>(a, st, launches);
+    case 8: return launch_cfg<Cfg<8, 32, NEN, NQ, MB, 0, K>>(a, st, launches);
+    case 16: return launch_cfg<Cfg<16, 16, NEN, NQ, MB, 0, K>>(a, st, launches);
+    case 32: return launch_cfg<Cfg<32, 16, NEN, NQ, MB, 0, K>>(a, st, launches);
+    case 64: return launch_cfg<Cfg<64, 16, NEN, NQ, MB, 0, K>>(a, st, launches);
+    case 128: return launch_cfg<Cfg<128, 8, NEN, NQ, MB, 0, K>>(a, st, launches);
   }
   return (int)cudaErrorInvalidValue;
 }
@@ -1201,14 +1236,14 @@ static int launch_k(const AsmArgs& a, cudaStream_t st, int* launches) {
 // material points: NEN = NQ = 1, one "element" per point
 template <int K>
 static int launch_mat_k(const AsmArgs& a, cudaStream_t st) {
-  if (a.ncm.net != 0 || K == 2) return launch_cfg<Cfg<16, 16, 1, 1, 3, 1, K, 1>>(a, st, nullptr);
-  if constexpr (K != 2)
+  if (a.ncm.net != 0) return launch_cfg<Cfg<16, 16, 1, 1, 3, 1, K, 1>>(a, st, nullptr);
+  constexpr int MB = K == 2 ? 2 : 3;
   switch (a.ncm.w) {
-    case 8: return launch_cfg<Cfg<8, 32, 1, 1, 3, 0, K, 1>>(a, st, nullptr);
-    case 16: return launch_cfg<Cfg<16, 16, 1, 1, 3, 0, K, 1>>(a, st, nullptr);
-    case 32: return launch_cfg<Cfg<32, 16, 1, 1, 3, 0, K, 1>>(a, st, nullptr);
-    case 64: return launch_cfg<Cfg<64, 16, 1, 1, 3, 0, K, 1>>(a, st, nullptr);
-    case 128: return launch_cfg<Cfg<128, 8, 1, 1, 3, 0, K, 1>>(a, st, nullptr);
+    case 8: return launch_cfg<Cfg<8, 32, 1, 1, MB, 0, K, 1>>(a, st, nullptr);
+    case 16: return launch_cfg<Cfg<16, 16, 1, 1, MB, 0, K, 1>>(a, st, nullptr);
+    case 32: return launch_cfg<Cfg<32, 16, 1, 1, MB, 0, K, 1>>(a, st, nullptr);
+    case 64: return launch_cfg<Cfg<64, 16, 1, 1, MB, 0, K, 1>>(a, st, nullptr);
+    case 128: return launch_cfg<Cfg<128, 8, 1, 1, MB, 0, K, 1>>(a, st, nullptr);
   }
   return (int)cudaErrorInvalidValue;
 }

@@ -230,13 +230,14 @@ def shape_gradients(X: np.ndarray, conn: np.ndarray, elem_type: int, chunk: int 
 # --------------------------------------------------------------------------
 # NCM weights and displacements
 # --------------------------------------------------------------------------
-def ncm_weights(width: int, n_hidden: int, std: float = 0.3, seed: int = SEED_W, kappa: float = 10.0):
+def ncm_weights(width: int, n_hidden: int, std: float = 0.3, seed: int = SEED_W, kappa: float = 10.0,
+                n_in: int = 3):
     """ICNN/MLP parameters drawn N(0, std^2) in the order W1, b1, W2, b2, ...,
     a (SURVEY s8(c) reading 8).  W1: (w,3); W: (L-1,w,w) row-major (out,in);
     b: (L,w); a: (w,)."""
     rng = np.random.default_rng(seed)
     w, L = width, n_hidden
-    W1 = rng.normal(0.0, std, size=(w, 3))
+    W1 = rng.normal(0.0, std, size=(w, n_in))
     b = np.empty((L, w))
     W = np.empty((max(L - 1, 0), w, w))
     b[0] = rng.normal(0.0, std, size=w)

@@ -187,7 +187,7 @@ def energy_hd(F: list, ncm: dict):
     L, w = ncm["n_hidden"], ncm["width"]
     Wh = ncm.get("W")
     Bh = ncm.get("skip_hidden")
-    z = [sum((W1[j, i] * k[i] for i in range(3)), HD(0.0)) + b[0, j] for j in range(w)]
+    z = [sum((W1[j, i] * k[i] for i in range(len(k))), HD(0.0)) + b[0, j] for j in range(w)]
     z = [softplus(v) for v in z]
     for l in range(1, L):
         y = []

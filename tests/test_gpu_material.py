@@ -42,6 +42,7 @@ MODELS = {
     "gent_thomas": gent_thomas_params,
     "ickan": lambda: ickan_params(),
     "cann_anisotropic": lambda: anisotropic(cann_params(4, seed=6, n_in=5)),
+    "icnn_anisotropic_32x2": lambda: anisotropic(ncm_weights(32, 2, 0.3, 15, 10.0, n_in=5)),
 }
 
 

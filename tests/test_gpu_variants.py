@@ -40,6 +40,8 @@ VARIANTS = {
     "ickan_isochoric": lambda: ickan_params((3, 5, 1), nb=7, seed=5, kinematics="isochoric"),
     "cann_anisotropic": lambda: anisotropic(cann_params(4, seed=6, n_in=5)),
     "ickan_anisotropic": lambda: anisotropic(ickan_params((5, 4, 1), nb=7, seed=7)),
+    "icnn_anisotropic_16x2": lambda: anisotropic(ncm_weights(16, 2, 0.3, 13, 10.0, n_in=5)),
+    "icnn_anisotropic_64x3": lambda: anisotropic(ncm_weights(64, 3, 0.3, 14, 10.0, n_in=5)),
 }
 
 
@@ -88,6 +90,32 @@ def test_analytic_ncm_eval_matches_oracle(pc, name):
         _, go, Ho = oracle.ncm_eval_n(dict(ncm, kappa=0.0), k[i])
         assert np.abs(g[i] - go).max() <= 1e-14 * max(1.0, np.abs(go).max())
         assert np.abs(H[i] - Ho[np.triu_indices(nk)]).max() <= 1e-14 * max(1.0, np.abs(Ho).max())
+
+
+@pytest.mark.parametrize("name", ["icnn_anisotropic_16x2", "icnn_anisotropic_64x3"])
+def test_icnn5_ncm_eval_matches_oracle(pc, name):
+    """Alg. 4 with five inputs (W1 is [w][5]) against the oracle's icnn_eval at nk = 5;
+    the softplus / sigmoid tables carry the 1e-13 of the three-input ICNN check."""
+    ncm = VARIANTS[name]()
+    mesh, _ = _mesh(HEX8, 1)
+    lib = pc.Commet(mesh, ncm)
+    rng = np.random.default_rng(13)
+    k = rng.uniform(-0.4, 0.4, size=(25, 5))
+    g, H = lib.ncm_eval(torch.from_numpy(k).cuda())
+    g, H = g.cpu().numpy(), H.cpu().numpy()
+    for i in range(k.shape[0]):
+        _, go, Ho = oracle.ncm_eval_n(dict(ncm, kappa=0.0), k[i])
+        assert np.abs(g[i] - go).max() <= 1e-13 * np.abs(go).max()
+        Hu = Ho[np.triu_indices(5)]
+        assert np.abs(H[i] - Hu).max() <= 1e-13 * np.abs(Hu).max()
+
+
+def test_icnn5_rejects_hidden_skips(pc):
+    ncm = VARIANTS["icnn_anisotropic_16x2"]()
+    ncm["skip_hidden"] = np.zeros((1, 16, 3))
+    mesh, _ = _mesh(HEX8, 1)
+    with pytest.raises(pc.CommetError):
+        pc.Commet(mesh, ncm)
 
 
 def test_normalize_reference_rejects_anisotropic(pc):

@@ -30,6 +30,7 @@ VARIANTS = {
     "ickan_isochoric": lambda: ickan_params((3, 5, 1), nb=7, seed=5, kinematics="isochoric"),
     "cann_anisotropic": lambda: anisotropic(cann_params(4, seed=6, n_in=5)),
     "ickan_anisotropic": lambda: anisotropic(ickan_params((5, 4, 1), nb=7, seed=7)),
+    "icnn_anisotropic": lambda: anisotropic(ncm_weights(8, 2, 0.3, 13, 10.0, n_in=5)),
 }
 
 

@@ -21,13 +21,19 @@ def run(path, cfg, steps=20):
                   cfg["qp_w"].ctypes.data, 0, cfg["n_nodes"], 1, 0, None, 0, None, None,
                   int(os.environ.get("AB_ORDER", "0")))
     m = cfg["ncm"]
-    net = os.environ.get("AB_NET")  # variants: gt | cann | ickan
+    net = os.environ.get("AB_NET")  # variants: gt | cann | ickan | cann5 | ickan5 | icnn5
     if net == "gt":
         m = gen.gent_thomas_params()
     elif net == "cann":
         m = gen.cann_params(4)
     elif net == "ickan":
         m = gen.ickan_params()
+    elif net == "cann5":
+        m = gen.anisotropic(gen.cann_params(4, n_in=5))
+    elif net == "ickan5":
+        m = gen.anisotropic(gen.ickan_params((5, 4, 1), nb=7, seed=7))
+    elif net == "icnn5":
+        m = gen.anisotropic(gen.ncm_weights(64, 3, 0.3, 14, 10.0, n_in=5))
     import paper_2510_00884_b200 as pc
     nd, keep = pc.ncm_desc(m)
     ctx = C.c_void_p()

@@ -27,6 +27,7 @@ def main():
         "cann anisotropic": gen.anisotropic(gen.cann_params(4, n_in=5)),
         "ickan 3-6-6-1": gen.ickan_params(),
         "ickan anisotropic 5-4-1": gen.anisotropic(gen.ickan_params((5, 4, 1), nb=7, seed=7)),
+        "icnn 64x3 anisotropic": gen.anisotropic(gen.ncm_weights(64, 3, 0.3, 14, 10.0, n_in=5)),
     }
     u = torch.from_numpy(cfg["u"]).cuda()
     nq = cfg["conn"].shape[0] * 8
