@@ -14,7 +14,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libcommet.so")
+# COMMET_LIB: another build of the library (A/B tuning tools); default: the in-tree build
+LIB_PATH = os.environ.get("COMMET_LIB") or os.path.join(_HERE, "libcommet.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} not built: run `make -C {os.path.join(_HERE, 'csrc')}` "
