@@ -311,11 +311,18 @@ commet_status commet_set_dirichlet(commet_ctx ctx, const int64_t* dofs /* host [
 /* Eliminate in place: csr_values device [nnz] (this ctx's pattern), residual device
  * [n_rows] or NULL.  Asynchronous on cuda_stream. */
 commet_status commet_apply_dirichlet(commet_ctx ctx, double* residual, double* csr_values, void* cuda_stream);
+/* Preconditioner of the CG solves of this ctx (commet_cg_jacobi, commet_newton_step):
+ * COMMET_PC_JACOBI (default; the paper's "conjugate gradient ... with Jacobi relaxation
+ * as the preconditioner") or COMMET_PC_BLOCK_JACOBI (the inverses of the
+ * 3x3 nodal diagonal blocks of K).  COMMET_ERR_ARG for another kind. */
+enum { COMMET_PC_JACOBI = 0, COMMET_PC_BLOCK_JACOBI = 1 };
+commet_status commet_set_preconditioner(commet_ctx ctx, int32_t kind);
 /* Solve K x = b (K: csr_values on this ctx's pattern, device; b, x device [n_rows])
- * from x = 0 with Jacobi-preconditioned CG until ||b - K x||_2 <= rtol ||b||_2.
+ * from x = 0 with (block-)Jacobi-preconditioned CG until ||b - K x||_2 <= rtol ||b||_2.
  * Synchronous.  *iters, *rel_res (may be NULL) report the outcome.  Errors:
- * COMMET_ERR_DOMAIN if a diagonal entry is <= 0 (message names the row) or the
- * tolerance is not met in max_iter iterations (x holds the last iterate). */
+ * COMMET_ERR_DOMAIN if a diagonal entry is <= 0 / a 3x3 diagonal block is not positive
+ * definite (message names the row) or the tolerance is not met in max_iter iterations
+ * (x holds the last iterate). */
 commet_status commet_cg_jacobi(commet_ctx ctx, const double* csr_values, const double* b, double* x,
                                double rtol, int32_t max_iter, int32_t* iters, double* rel_res,
                                void* cuda_stream);

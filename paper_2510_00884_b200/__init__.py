@@ -37,7 +37,7 @@ SYMBOLS = ("commet_setup", "commet_csr_pattern", "commet_csr_pattern_copy", "com
            "commet_kernel_info", "commet_max_trace_C", "commet_set_dirichlet", "commet_apply_dirichlet",
            "commet_cg_jacobi", "commet_newton_step", "commet_ncm_eval", "commet_normalize_reference",
            "commet_material_eval", "commet_halo_recv_maps", "commet_set_peer", "commet_set_peer_mode",
-           "commet_zero_outputs")
+           "commet_zero_outputs", "commet_set_preconditioner")
 NEWTON_MAX_LOG = 64
 
 
@@ -161,7 +161,9 @@ _lib.commet_halo_recv_maps.argtypes = [_vp, _i32, _P(_vp), _P(_vp)]
 _lib.commet_set_peer.argtypes = [_vp, _i32, _vp, _vp, _vp, _i64, _vp, _i64]
 _lib.commet_set_peer_mode.argtypes = [_vp, _i32]
 _lib.commet_zero_outputs.argtypes = [_vp, _vp, _vp, _vp]
-for _f in ("commet_halo_recv_maps", "commet_set_peer", "commet_set_peer_mode", "commet_zero_outputs"):
+_lib.commet_set_preconditioner.argtypes = [_vp, _i32]
+for _f in ("commet_halo_recv_maps", "commet_set_peer", "commet_set_peer_mode", "commet_zero_outputs",
+           "commet_set_preconditioner"):
     getattr(_lib, _f).restype = C.c_int
 for _f in ("commet_ncm_eval", "commet_normalize_reference", "commet_max_trace_C", "commet_set_dirichlet", "commet_apply_dirichlet", "commet_cg_jacobi",
            "commet_newton_step"):
@@ -394,6 +396,13 @@ class Commet:
         st = stream if stream is not None else t.cuda.current_stream(self.device)
         _check(_lib.commet_apply_dirichlet(self.ctx, None if residual is None else residual.data_ptr(),
                                            values.data_ptr(), st.cuda_stream), self.ctx)
+
+    PRECONDITIONERS = {"jacobi": 0, "block_jacobi": 1}
+
+    def set_preconditioner(self, kind="jacobi"):
+        """CG preconditioner of cg_jacobi / newton_step: "jacobi" (the paper's) or "block_jacobi"
+        (3x3 nodal diagonal blocks)."""
+        _check(_lib.commet_set_preconditioner(self.ctx, self.PRECONDITIONERS[kind]), self.ctx)
 
     def cg_jacobi(self, values, b, rtol=1e-10, max_iter=100000, x=None, stream=None):
         """Solve K x = b on this ctx's pattern (device tensors). -> (x, iters, rel_res)."""

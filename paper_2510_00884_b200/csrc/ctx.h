@@ -41,6 +41,7 @@ struct commet_ctx_s {
   int device = 0;
   Plan plan;  // host copy (pattern, maps); element-order arrays are dropped after upload
   int kernel = COMMET_KERNEL_FUSED;
+  int precond = 0;              // COMMET_PC_JACOBI (the paper's) or COMMET_PC_BLOCK_JACOBI
   bool material_only = false;  // commet_setup(mesh = NULL): material-point calls only
   std::string err;
   cudaStream_t last_stream = nullptr;

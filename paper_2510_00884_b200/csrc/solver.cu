@@ -142,6 +142,54 @@ __global__ void jacobi_diag_kernel(const int64_t* __restrict__ row_ptr, const in
   }
 }
 
+// Block Jacobi: the inverse of the 3x3 diagonal block of every node (its own slot in the node
+// adjacency), by cofactors; a block that is not SPD (a leading minor <= 0) records the node's
+// first row in *bad (atomicMin)
+__global__ void block_jacobi_kernel(const int64_t* __restrict__ node_rs, const int32_t* __restrict__ node_deg,
+                                    const int32_t* __restrict__ adj, const double* __restrict__ vals,
+                                    double* __restrict__ binv, int64_t n_nodes, unsigned long long* bad) {
+  for (int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; a < n_nodes;
+       a += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t rs = node_rs[a];
+    const int deg = node_deg[a], st = 3 * deg;
+    const int32_t* nb = adj + rs / 9;
+    int sl = -1;
+    for (int t = 0; t < deg; t++)
+      if (nb[t] == (int32_t)a) { sl = t; break; }
+    double B[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    if (sl >= 0)
+#pragma unroll
+      for (int i = 0; i < 3; i++)
+#pragma unroll
+        for (int k = 0; k < 3; k++) B[i * 3 + k] = vals[rs + i * st + 3 * sl + k];
+    double cof[9];
+    cof[0] = B[4] * B[8] - B[5] * B[7];
+    cof[1] = B[5] * B[6] - B[3] * B[8];
+    cof[2] = B[3] * B[7] - B[4] * B[6];
+    cof[3] = B[2] * B[7] - B[1] * B[8];
+    cof[4] = B[0] * B[8] - B[2] * B[6];
+    cof[5] = B[1] * B[6] - B[0] * B[7];
+    cof[6] = B[1] * B[5] - B[2] * B[4];
+    cof[7] = B[2] * B[3] - B[0] * B[5];
+    cof[8] = B[0] * B[4] - B[1] * B[3];
+    const double det = B[0] * cof[0] + B[1] * cof[1] + B[2] * cof[2];
+    if (!(B[0] > 0.0 && cof[8] > 0.0 && det > 0.0)) atomicMin(bad, (unsigned long long)(3 * a));
+    const double id = 1.0 / det;
+    // (B^-1)_ik = cof_ki / det
+#pragma unroll
+    for (int i = 0; i < 3; i++)
+#pragma unroll
+      for (int k = 0; k < 3; k++) binv[9 * a + i * 3 + k] = cof[k * 3 + i] * id;
+  }
+}
+
+__device__ __forceinline__ void bj_apply(const double* __restrict__ binv, int64_t a, const double (&r)[3],
+                                         double (&z)[3]) {
+  const double* Bi = binv + 9 * a;
+#pragma unroll
+  for (int i = 0; i < 3; i++) z[i] = Bi[3 * i] * r[0] + Bi[3 * i + 1] * r[1] + Bi[3 * i + 2] * r[2];
+}
+
 // ---- CG ------------------------------------------------------------------------------------
 // init: x = 0, r = b, z = D^-1 b, p = z; partials (r.z, b.b)
 __global__ void cg_init_kernel(const double* __restrict__ b, const double* __restrict__ dinv, double* __restrict__ x,
@@ -156,6 +204,30 @@ __global__ void cg_init_kernel(const double* __restrict__ b, const double* __res
     p[i] = zi;
     v[0] += bi * zi;
     v[1] += bi * bi;
+  }
+  block_partials<2>(v, part);
+}
+
+// block-Jacobi init: per node, z = B^-1 b
+__global__ void cg_init_bj_kernel(const double* __restrict__ b, const double* __restrict__ binv, double* __restrict__ x,
+                                  double* __restrict__ r, double* __restrict__ z, double* __restrict__ p,
+                                  int64_t n_nodes, double* part) {
+  double v[2] = {0.0, 0.0};
+  for (int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; a < n_nodes;
+       a += (int64_t)gridDim.x * blockDim.x) {
+    double bv[3], zv[3];
+#pragma unroll
+    for (int i = 0; i < 3; i++) bv[i] = b[3 * a + i];
+    bj_apply(binv, a, bv, zv);
+#pragma unroll
+    for (int i = 0; i < 3; i++) {
+      x[3 * a + i] = 0.0;
+      r[3 * a + i] = bv[i];
+      z[3 * a + i] = zv[i];
+      p[3 * a + i] = zv[i];
+      v[0] += bv[i] * zv[i];
+      v[1] += bv[i] * bv[i];
+    }
   }
   block_partials<2>(v, part);
 }
@@ -344,6 +416,37 @@ __global__ void cg_update_xr_kernel(double* __restrict__ x, double* __restrict__
   block_partials<2>(v, part);
 }
 
+// block-Jacobi update: per node, x += alpha p, r -= alpha q, z = B^-1 r; partials (r.z, r.r)
+__global__ void cg_update_xr_bj_kernel(double* __restrict__ x, double* __restrict__ r, double* __restrict__ z,
+                                       const double* __restrict__ p, const double* __restrict__ q,
+                                       const double* __restrict__ binv, int64_t n_nodes, const double* part_pq,
+                                       int nb, double* part, const CgScal* s, int it) {
+  if (s->done) return;
+  double pq[1];
+  sum_partials<1>(part_pq, nb, pq);
+  const double alpha = s->rz[it & 1] / pq[0];
+  double v[2] = {0.0, 0.0};
+  for (int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; a < n_nodes;
+       a += (int64_t)gridDim.x * blockDim.x) {
+    double rv[3], zv[3];
+#pragma unroll
+    for (int i = 0; i < 3; i++) {
+      const int64_t j = 3 * a + i;
+      x[j] = fma(alpha, p[j], x[j]);
+      rv[i] = fma(-alpha, q[j], r[j]);
+      r[j] = rv[i];
+    }
+    bj_apply(binv, a, rv, zv);
+#pragma unroll
+    for (int i = 0; i < 3; i++) {
+      z[3 * a + i] = zv[i];
+      v[0] += rv[i] * zv[i];
+      v[1] += rv[i] * rv[i];
+    }
+  }
+  block_partials<2>(v, part);
+}
+
 // increment of the constrained dofs: d = 0, d[dofs] = v - u[dofs]
 __global__ void bc_increment_kernel(double* __restrict__ d, const double* __restrict__ u,
                                     const int64_t* __restrict__ dofs, const double* __restrict__ v, int64_t n) {
@@ -405,6 +508,7 @@ struct SolverWork {
   DevBuf<uint8_t> mask;
   DevBuf<double> bc_vals;
   DevBuf<double> r, vals, dinv, x, cr, z, p, q, part, part2, dotv;
+  DevBuf<double> binv;  // block Jacobi: [n_nodes][3][3]
   DevBuf<int32_t> adj;  // node adjacency (column node of every 3x3 block), node order
   DevBuf<CgScal> scal;
   DevBuf<unsigned long long> bad;
@@ -510,15 +614,25 @@ static commet_status cg(commet_ctx c, SolverWork* w, const double* vals, const d
   const Plan& p = c->plan;
   const int64_t n = 3 * p.n_owned, n_nodes = p.n_owned;
   const int nb = w->nb;
+  const bool bj = c->precond == COMMET_PC_BLOCK_JACOBI;
+  if (bj && !w->binv.p) CUDA_TRY(c, w->binv.alloc(9 * (size_t)std::max<int64_t>(n_nodes, 1)));
   CUDA_TRY(c, cudaMemsetAsync(w->bad.p, 0xff, sizeof(unsigned long long), st));
-  jacobi_diag_kernel<<<nb, kThreads, 0, st>>>(c->row_ptr.p, c->col_idx.p, vals, w->dinv.p, n, w->bad.p);
-  cg_init_kernel<<<nb, kThreads, 0, st>>>(b, w->dinv.p, x, w->cr.p, w->z.p, w->p.p, n, w->part2.p);
+  if (bj) {
+    block_jacobi_kernel<<<nb, kThreads, 0, st>>>(c->node_rs.p, c->node_deg.p, w->adj.p, vals, w->binv.p, n_nodes,
+                                                 w->bad.p);
+    cg_init_bj_kernel<<<nb, kThreads, 0, st>>>(b, w->binv.p, x, w->cr.p, w->z.p, w->p.p, n_nodes, w->part2.p);
+  } else {
+    jacobi_diag_kernel<<<nb, kThreads, 0, st>>>(c->row_ptr.p, c->col_idx.p, vals, w->dinv.p, n, w->bad.p);
+    cg_init_kernel<<<nb, kThreads, 0, st>>>(b, w->dinv.p, x, w->cr.p, w->z.p, w->p.p, n, w->part2.p);
+  }
   cg_init_scal_kernel<<<1, kThreads, 0, st>>>(w->part2.p, nb, rtol, w->scal.p);
   CUDA_TRY(c, cudaGetLastError());
   unsigned long long bad = ~0ULL;
   CUDA_TRY(c, cudaMemcpyAsync(&bad, w->bad.p, sizeof bad, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(c, cudaStreamSynchronize(st));
-  if (bad != ~0ULL) return fail(c, COMMET_ERR_DOMAIN, "CG-Jacobi: diagonal entry of row %llu is not positive", bad);
+  if (bad != ~0ULL)
+    return fail(c, COMMET_ERR_DOMAIN, bj ? "CG-Jacobi: the 3x3 diagonal block at row %llu is not positive definite"
+                                         : "CG-Jacobi: diagonal entry of row %llu is not positive", bad);
   CgScal hs{};
   for (int it0 = 0; it0 <= max_iter; it0 += kCheck) {
     const int nk = std::min(kCheck, max_iter + 1 - it0);
@@ -532,8 +646,12 @@ static commet_status cg(commet_ctx c, SolverWork* w, const double* vals, const d
       cg_spmv_dot_nb_kernel<<<nb, kThreads, 0, st>>>(c->node_rs.p, c->node_deg.p, w->adj.p, vals, w->p.p, w->q.p,
                                                      n_nodes, w->part.p, w->scal.p);
 #endif
-      cg_update_xr_kernel<<<nb, kThreads, 0, st>>>(x, w->cr.p, w->z.p, w->p.p, w->q.p, w->dinv.p, n, w->part.p, nb,
-                                                   w->part2.p, w->scal.p, k);
+      if (bj)
+        cg_update_xr_bj_kernel<<<nb, kThreads, 0, st>>>(x, w->cr.p, w->z.p, w->p.p, w->q.p, w->binv.p, n_nodes,
+                                                        w->part.p, nb, w->part2.p, w->scal.p, k);
+      else
+        cg_update_xr_kernel<<<nb, kThreads, 0, st>>>(x, w->cr.p, w->z.p, w->p.p, w->q.p, w->dinv.p, n, w->part.p, nb,
+                                                     w->part2.p, w->scal.p, k);
     }
     CUDA_TRY(c, cudaGetLastError());
     CUDA_TRY(c, cudaMemcpyAsync(&hs, w->scal.p, sizeof hs, cudaMemcpyDeviceToHost, st));
@@ -546,6 +664,14 @@ static commet_status cg(commet_ctx c, SolverWork* w, const double* vals, const d
   if (!(rr <= hs.tol2))
     return fail(c, COMMET_ERR_DOMAIN, "CG-Jacobi did not reach rtol %.3g in %d iterations (rel. residual %.3g)", rtol,
                 max_iter, hs.bb > 0 ? std::sqrt(rr / hs.bb) : 0.0);
+  return COMMET_OK;
+}
+
+extern "C" commet_status commet_set_preconditioner(commet_ctx c, int32_t kind) {
+  if (!c) return fail(nullptr, COMMET_ERR_ARG, "ctx is NULL");
+  if (kind != COMMET_PC_JACOBI && kind != COMMET_PC_BLOCK_JACOBI)
+    return fail(c, COMMET_ERR_ARG, "preconditioner %d unknown", kind);
+  c->precond = kind;
   return COMMET_OK;
 }
 

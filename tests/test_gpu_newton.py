@@ -104,6 +104,48 @@ def test_cg_jacobi_matches_direct_solve(pc):
     assert abs(it - it_o) <= 3, (it, it_o)
 
 
+def test_block_jacobi_cg_matches_direct_solve(pc):
+    """3x3 block-Jacobi PCG on an eliminated twist tangent: the direct solution, and the
+    oracle's block PCG iteration count (fewer iterations than scalar Jacobi)."""
+    mesh, ncm, lib, dofs, _ = _twist_setup(pc, 5)
+    rp, ci = oracle.pattern(mesh["n_nodes"], mesh["conn"])
+    u = np.zeros(3 * mesh["n_nodes"])
+    for s in (1, 2):
+        u, _, ok = on.newton_step(ncm, mesh, rp, ci, u, dofs, twist.twist_values(mesh["X"], dofs, s / 10))
+        assert ok
+    r, v = lib.assemble(torch.from_numpy(u).cuda())
+    lib.apply_dirichlet(r, v)
+    _, it_j, _ = lib.cg_jacobi(v, r, rtol=1e-12)
+    lib.set_preconditioner("block_jacobi")
+    x, it, rel = lib.cg_jacobi(v, r, rtol=1e-12)
+    n = r.numel()
+    K = sp.csr_matrix((v.cpu().numpy(), ci, rp), shape=(n, n))
+    xd = spla.spsolve(K.tocsc(), r.cpu().numpy())
+    assert rel <= 1e-12
+    assert np.linalg.norm(x.cpu().numpy() - xd) <= 1e-9 * np.linalg.norm(xd)
+    _, it_o = on.cg_jacobi(K, r.cpu().numpy(), rtol=1e-12, block=True)
+    assert abs(it - it_o) <= 3, (it, it_o)
+    assert it < it_j, (it, it_j)
+    with pytest.raises(pc.CommetError):  # the C ABI refuses an unknown kind
+        pc._check(pc._lib.commet_set_preconditioner(lib.ctx, 7), lib.ctx)
+
+
+def test_block_jacobi_newton_twist_matches_oracle(pc):
+    n, steps = 3, 5
+    mesh, ncm, lib, dofs, _ = _twist_setup(pc, n)
+    lib.set_preconditioner("block_jacobi")
+    rp, ci = oracle.pattern(mesh["n_nodes"], mesh["conn"])
+    uo = np.zeros(3 * mesh["n_nodes"])
+    ug = torch.zeros(3 * mesh["n_nodes"], dtype=torch.float64, device="cuda")
+    for s in range(1, steps + 1):
+        vals = twist.twist_values(mesh["X"], dofs, s / steps)
+        uo, norms, ok = on.newton_step(ncm, mesh, rp, ci, uo, dofs, vals, atol=1e-11, rtol=1e-12)
+        rep = lib.newton_step(ug, vals, atol=1e-11, rtol=1e-12, cg_rtol=1e-13)
+        assert ok and rep["converged"], (s, norms, rep["res_norm"])
+        d = np.abs(ug.cpu().numpy() - uo).max() / np.abs(uo).max()
+        assert d <= 1e-9, (s, d)
+
+
 def test_newton_zero_load(pc):
     mesh, ncm, lib, dofs, _ = _twist_setup(pc, 3)
     u = torch.zeros(3 * mesh["n_nodes"], dtype=torch.float64, device="cuda")

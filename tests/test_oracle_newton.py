@@ -39,6 +39,32 @@ def test_cg_random_spd_matches_dense_solve():
     assert it <= 50
 
 
+def test_block_cg_block_diagonal_one_iteration():
+    """A block-diagonal SPD matrix of 3x3 blocks is its own block-Jacobi preconditioner:
+    PCG converges in one iteration to the exact solution."""
+    rng = np.random.default_rng(7)
+    blocks = []
+    for _ in range(4):
+        M = rng.normal(size=(3, 3))
+        blocks.append(M @ M.T + 3 * np.eye(3))
+    A = sp.block_diag(blocks, format="csr")
+    b = rng.normal(size=12)
+    x, it = on.cg_jacobi(A, b, rtol=1e-14, block=True)
+    assert it == 1 and np.allclose(x, np.linalg.solve(A.toarray(), b), rtol=0, atol=1e-13)
+    _, it_j = on.cg_jacobi(A, b, rtol=1e-14)
+    assert it_j > 1  # the scalar Jacobi preconditioner does not invert the blocks
+
+
+def test_block_cg_random_spd_matches_dense_solve():
+    rng = np.random.default_rng(6)
+    M = rng.normal(size=(48, 48))
+    A = M @ M.T + 48 * np.eye(48)
+    b = rng.normal(size=48)
+    x, it = on.cg_jacobi(sp.csr_matrix(A), b, rtol=1e-13, block=True)
+    xd = np.linalg.solve(A, b)
+    assert np.linalg.norm(x - xd) <= 1e-8 * np.linalg.norm(xd) and it <= 48
+
+
 # ---- symmetric elimination -------------------------------------------------------
 def test_eliminate_definition():
     rng = np.random.default_rng(3)

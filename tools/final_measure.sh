@@ -6,17 +6,18 @@
 set -u
 O=gpurun_out/final
 mkdir -p $O
-run() { echo "== $*" >> $O/log.txt; timeout "$@" >> $O/log.txt 2>&1; echo "rc=$?" >> $O/log.txt; }
-run 900 python bench.py > $O/bench_c5.json
-run 600 python bench.py --config c3 --steps 20 --warmup 5 > $O/bench_c3.json
-run 600 python bench.py --config c4 --steps 10 --warmup 3 > $O/bench_c4.json
-for n in 16 32 64; do run 600 python tools/newton_bench.py --n $n >> $O/newton_twist.jsonl; done
-if [ "${FINAL_N128:-1}" = 1 ]; then run 1200 python tools/newton_bench.py --n 128 >> $O/newton_twist.jsonl; fi
-run 600 python tools/material_sweep.py > $O/material_sweep.jsonl
+# run OUT SECONDS CMD...: stdout appended to $O/OUT, stderr and the exit code to $O/log.txt
+run() { local out=$1; shift; echo "== $*" >> $O/log.txt; timeout "$@" >> $O/$out 2>> $O/log.txt; echo "rc=$?" >> $O/log.txt; }
+run bench_c5.json 900 python bench.py
+run bench_c3.json 600 python bench.py --config c3 --steps 20 --warmup 5
+run bench_c4.json 600 python bench.py --config c4 --steps 10 --warmup 3
+for n in 16 32 64; do run newton_twist.jsonl 600 python tools/newton_bench.py --n $n; done
+if [ "${FINAL_N128:-1}" = 1 ]; then run newton_twist.jsonl 1200 python tools/newton_bench.py --n 128; fi
+run material_sweep.jsonl 600 python tools/material_sweep.py
 # launch list of the default bench command (cold-cache, serialised: shares, not absolutes)
-run 1200 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_c5.csv \
+run ncu.log 1200 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_c5.csv \
     python bench.py --steps 2 --warmup 1 --no-cpu --no-e2e
 # the fused kernel, full set, 1 launch after 8 warm-up launches (c3, colour launches)
-run 1200 ncu --set full --clock-control none --import-source on -k regex:fused_kernel -s 8 -c 1 \
+run ncu.log 1200 ncu --set full --clock-control none --import-source on -k regex:fused_kernel -s 8 -c 1 \
     -o $O/prof_c3 python bench.py --config c3 --steps 1 --warmup 1 --no-cpu --no-e2e
 tail -c 3000 $O/log.txt
