@@ -28,10 +28,6 @@
 
 #include "ctx.h"
 
-#ifndef COMMET_SPMV_V
-#define COMMET_SPMV_V 1  // value-major node-block SpMV (cg_spmv_dot_nbv_kernel)
-#endif
-
 namespace {
 
 constexpr int kThreads = 256;
@@ -293,46 +289,6 @@ __global__ void cg_spmv_dot_nb_kernel(const int64_t* __restrict__ node_rs, const
       s0 = fma(__ldcs(v0), p0, fma(__ldcs(v0 + 1), p1, fma(__ldcs(v0 + 2), p2, s0)));
       s1 = fma(__ldcs(v0 + st), p0, fma(__ldcs(v0 + st + 1), p1, fma(__ldcs(v0 + st + 2), p2, s1)));
       s2 = fma(__ldcs(v0 + 2 * st), p0, fma(__ldcs(v0 + 2 * st + 1), p1, fma(__ldcs(v0 + 2 * st + 2), p2, s2)));
-    }
-    s0 = warp_sum(s0);
-    s1 = warp_sum(s1);
-    s2 = warp_sum(s2);
-    if (lane == 0) {
-      q[3 * a] = s0;
-      q[3 * a + 1] = s1;
-      q[3 * a + 2] = s2;
-      v[0] += p[3 * a] * s0 + p[3 * a + 1] * s1 + p[3 * a + 2] * s2;
-    }
-  }
-  block_partials<1>(v, part);
-}
-
-// Same product, the lanes on consecutive values of each row (x = 3 s + k: neighbour slot s,
-// component k): every value load instruction is one coalesced 256-byte segment of the row
-// triple (the slot-major form above reads 3 doubles at a 24-byte lane stride per instruction);
-// p[3 b + k] is gathered once per value position and serves the node's three rows.
-__global__ void cg_spmv_dot_nbv_kernel(const int64_t* __restrict__ node_rs, const int32_t* __restrict__ node_deg,
-                                       const int32_t* __restrict__ adj, const double* __restrict__ vals,
-                                       const double* __restrict__ p, double* __restrict__ q, int64_t n_nodes,
-                                       double* part, const CgScal* s) {
-  if (s->done) return;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwb = blockDim.x >> 5;
-  const int64_t chunk = (n_nodes + gridDim.x - 1) / gridDim.x;
-  const int64_t a_end = min(n_nodes, (int64_t)(blockIdx.x + 1) * chunk);
-  double v[1] = {0.0};
-  for (int64_t a = (int64_t)blockIdx.x * chunk + wid; a < a_end; a += nwb) {
-    const int64_t rs = __ldg(node_rs + a);
-    const int st = 3 * __ldg(node_deg + a);
-    const int32_t* nb = adj + rs / 9;
-    const double* v0 = vals + rs;
-    double s0 = 0.0, s1 = 0.0, s2 = 0.0;
-#pragma unroll 4
-    for (int x = lane; x < st; x += 32) {
-      const int sl = x / 3, k = x - 3 * sl;
-      const double pv = __ldg(p + 3 * (int64_t)__ldg(nb + sl) + k);
-      s0 = fma(__ldcs(v0 + x), pv, s0);
-      s1 = fma(__ldcs(v0 + st + x), pv, s1);
-      s2 = fma(__ldcs(v0 + 2 * st + x), pv, s2);
     }
     s0 = warp_sum(s0);
     s1 = warp_sum(s1);
@@ -639,13 +595,8 @@ static commet_status cg(commet_ctx c, SolverWork* w, const double* vals, const d
     for (int kk = 0; kk < nk; kk++) {
       const int k = it0 + kk;
       cg_update_p_kernel<<<nb, kThreads, 0, st>>>(w->p.p, w->z.p, n, w->part2.p, nb, w->scal.p, k, max_iter);
-#if COMMET_SPMV_V
-      cg_spmv_dot_nbv_kernel<<<nb, kThreads, 0, st>>>(c->node_rs.p, c->node_deg.p, w->adj.p, vals, w->p.p, w->q.p,
-                                                      n_nodes, w->part.p, w->scal.p);
-#else
       cg_spmv_dot_nb_kernel<<<nb, kThreads, 0, st>>>(c->node_rs.p, c->node_deg.p, w->adj.p, vals, w->p.p, w->q.p,
                                                      n_nodes, w->part.p, w->scal.p);
-#endif
       if (bj)
         cg_update_xr_bj_kernel<<<nb, kThreads, 0, st>>>(x, w->cr.p, w->z.p, w->p.p, w->q.p, w->binv.p, n_nodes,
                                                         w->part.p, nb, w->part2.p, w->scal.p, k);

@@ -39,6 +39,7 @@ def main():
     ap.add_argument("--layers", type=int, default=2)
     ap.add_argument("--cg-rtol", type=float, default=1e-8)
     ap.add_argument("--rtol", type=float, default=1e-8)
+    ap.add_argument("--precond", default="jacobi", choices=["jacobi", "block_jacobi"])
     args = ap.parse_args()
     import torch
     import paper_2510_00884_b200 as pc
@@ -48,6 +49,7 @@ def main():
     ncm = twist.stable_ncm(args.width, args.layers)
     lib = pc.Commet(dict(elem_type=mesh["elem_type"], n_nodes=mesh["n_nodes"], conn=mesh["conn"],
                          gradN=mesh["gradN"], qp_w=mesh["qp_w"]), ncm)
+    lib.set_preconditioner(args.precond)
     s0 = lib.normalize_reference()
     dofs, _, _ = twist.twist_bc(mesh["X"])
     lib.set_dirichlet(dofs)
@@ -86,7 +88,7 @@ def main():
     gbs = cg_bytes_per_iter(lib.n_rows, lib.nnz) / (per_it * 1e-3) / 1e9
     line = dict(what="twist-cube Newton (GPU assembly + GPU CG-Jacobi)", n=args.n, dofs=lib.n_rows, nnz=lib.nnz,
                 elements=int(mesh["conn"].shape[0]), ncm=f"{args.width}x{args.layers} convex ICNN, s0={s0:.6f}",
-                load_steps=args.steps, steps_taken=len(steps),
+                precond=args.precond, load_steps=args.steps, steps_taken=len(steps),
                 newton_iters=sum(x.get("iters", 0) for x in steps), cg_iters_total=int(cg_total),
                 converged=bool(steps) and abs(steps[-1]["t"] - 1.0) < 1e-12 and steps[-1].get("converged", False),
                 max_trC=max_trc,
