@@ -268,6 +268,11 @@ def main():
         NCS = int(os.environ.get("COMMET_E2E_STREAMS", "2"))
         copy_streams = [torch.cuda.Stream(dev) for _ in range(NCS)]
         done_c = [torch.cuda.Event(), torch.cuda.Event()]
+        # the H2D of step s's u runs on its own stream into one of two device copies, so it
+        # overlaps the assembly of step s-1 (the copy of step s waits for step s-2's assembly)
+        u_sets = [u, torch.empty_like(u)]
+        h2d = torch.cuda.Stream(dev)
+        done_h = [torch.cuda.Event(), torch.cuda.Event()]
         done_d = [[torch.cuda.Event() for _ in range(NCS)] for _ in range(2)]
         nchunk = 4 * NCS
         vchunks = [(i * v.numel() // nchunk, (i + 1) * v.numel() // nchunk) for i in range(nchunk)]
@@ -284,8 +289,13 @@ def main():
             if peer and s_ >= 1:  # single output set: the previous read-back must be done
                 for ev in done_d[1 - k]:
                     stream.wait_event(ev)
-            u.copy_(u_host, non_blocking=True)
-            lib.assemble(u, *sets[k])
+            if s_ >= 2:
+                h2d.wait_event(done_c[k])
+            with torch.cuda.stream(h2d):
+                u_sets[k].copy_(u_host, non_blocking=True)
+            done_h[k].record(h2d)
+            stream.wait_event(done_h[k])
+            lib.assemble(u_sets[k], *sets[k])
             done_c[k].record(stream)
             for cs in copy_streams:
                 cs.wait_event(done_c[k])
@@ -308,9 +318,9 @@ def main():
         e2e = dict(value=spec_total_qp(args.config, n_el, n_q, ws) / (ms_e2e * 1e-3), unit="qp/s",
                    h2d_bytes_per_step=u_host.numel() * 8, d2h_bytes_per_step=(r.numel() + v.numel()) * 8,
                    ms_per_step=ms_e2e,
-                   note=f"pinned host buffers; D2H of step s overlaps the assembly of step s+1 "
-                        f"(two device output sets, {NCS} copy streams)")
-        del sets
+                   note=f"pinned host buffers; H2D of step s+1 and D2H of step s overlap the assembly "
+                        f"of step s+1 (two device input and output sets, 1 + {NCS} copy streams)")
+        del sets, u_sets
 
     total_qp = spec_total_qp(args.config, n_el, n_q, ws)
     total_el = total_qp // n_q
