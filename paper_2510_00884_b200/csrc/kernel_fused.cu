@@ -248,6 +248,19 @@ __constant__ int kVoigt[6][2] = {{0, 0}, {1, 1}, {2, 2}, {1, 2}, {0, 2}, {0, 1}}
 __constant__ int kVoigtPair[21][2] = {{0, 0}, {0, 1}, {0, 2}, {0, 3}, {0, 4}, {0, 5}, {1, 1}, {1, 2}, {1, 3},
                                       {1, 4}, {1, 5}, {2, 2}, {2, 3}, {2, 4}, {2, 5}, {3, 3}, {3, 4}, {3, 5},
                                       {4, 4}, {4, 5}, {5, 5}};
+// kVoigtPair -> (i, j, k, l), 2 bits each (i | j << 2 | k << 4 | l << 6), 8 entries per word
+constexpr unsigned long long voigt_code_word(int w) {
+  constexpr int V[6][2] = {{0, 0}, {1, 1}, {2, 2}, {1, 2}, {0, 2}, {0, 1}};
+  unsigned long long c = 0;
+  int vw = 0;
+  for (int p = 0; p < 6; p++)
+    for (int q = p; q < 6; q++, vw++)
+      if (vw >> 3 == w)
+        c |= (unsigned long long)(V[p][0] | V[p][1] << 2 | V[q][0] << 4 | V[q][1] << 6) << (8 * (vw & 7));
+  return c;
+}
+constexpr unsigned long long kVoigtCode0 = voigt_code_word(0), kVoigtCode1 = voigt_code_word(1),
+                             kVoigtCode2 = voigt_code_word(2);
 
 template <class C>
 __device__ __forceinline__ void material_outputs(const AsmArgs& A, const NcmDev& m, int L, int64_t e0, int ne,
@@ -317,8 +330,11 @@ __device__ __forceinline__ void material_outputs(const AsmArgs& A, const NcmDev&
   for (int it = tid; it < Q * 21; it += C::NTHR) {
     const int q = it / 21, vw = it % 21;
     if (q >= ne) continue;
-    const int i = kVoigt[kVoigtPair[vw][0]][0], j = kVoigt[kVoigtPair[vw][0]][1];
-    const int k = kVoigt[kVoigtPair[vw][1]][0], l = kVoigt[kVoigtPair[vw][1]][1];
+    // (i, j, k, l) of entry vw from a packed immediate (the per-thread index into the
+    // __constant__ tables would serialise the constant cache)
+    const unsigned long long cw = vw < 8 ? kVoigtCode0 : (vw < 16 ? kVoigtCode1 : kVoigtCode2);
+    const unsigned code = (unsigned)(cw >> (8 * (vw & 7))) & 0xffu;
+    const int i = code & 3, j = (code >> 2) & 3, k = (code >> 4) & 3, l = code >> 6;
     const double* F = qF + q * 9;
     const double* Aq = qA + q * 81;
     double c = (i == k) ? -qP[q * 9 + j * 3 + l] : 0.0;
