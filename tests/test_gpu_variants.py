@@ -118,6 +118,29 @@ def test_icnn5_rejects_hidden_skips(pc):
         pc.Commet(mesh, ncm)
 
 
+def test_kernel_info_reports_launched_instantiation(pc):
+    """commet_kernel_info queries the same dispatch the assembly launches: the 5-input
+    networks run 2 CTAs/SM without spills (> 168 registers), the 3-input ICNN 3 CTAs/SM at
+    <= 168; the analytic networks allocate no ICNN buffers (less shared memory than the
+    ICNN of the same qp count); the query launches nothing (outputs untouched)."""
+    mesh, u = _mesh(HEX8, 2)
+    info = {}
+    for name, ncm in (("icnn", ncm_weights(64, 3, 0.3, 1, 10.0)), ("cann", VARIANTS["cann_standard"]()),
+                      ("cann5", VARIANTS["cann_anisotropic"]()), ("icnn5", VARIANTS["icnn_anisotropic_64x3"]())):
+        lib = pc.Commet(mesh, ncm)
+        r, v = lib.alloc_outputs()
+        r.fill_(7.0)
+        info[name] = lib.kernel_info()
+        torch.cuda.synchronize()
+        assert (r == 7.0).all()
+        lib.assemble(torch.from_numpy(u).cuda(), r, v)
+        assert lib.check() == -1
+    assert info["icnn"]["ctas_per_sm"] == 3 and info["icnn"]["regs_per_thread"] <= 168
+    assert info["icnn5"]["ctas_per_sm"] == 2 and info["icnn5"]["regs_per_thread"] > 168
+    assert info["cann5"]["ctas_per_sm"] == 2 and info["cann5"]["regs_per_thread"] > 168
+    assert info["cann"]["ctas_per_sm"] >= 3 and info["cann"]["smem_bytes"] < info["icnn"]["smem_bytes"]
+
+
 def test_normalize_reference_rejects_anisotropic(pc):
     mesh, _ = _mesh(HEX8, 1)
     lib = pc.Commet(mesh, VARIANTS["cann_anisotropic"]())
