@@ -130,6 +130,22 @@ def test_block_jacobi_cg_matches_direct_solve(pc):
         pc._check(pc._lib.commet_set_preconditioner(lib.ctx, 7), lib.ctx)
 
 
+@pytest.mark.parametrize("kind", ["jacobi", "block_jacobi"])
+def test_cg_refuses_indefinite_preconditioner(pc, kind):
+    """A non-positive diagonal entry (Jacobi) / a 3x3 diagonal block that is not positive
+    definite (block Jacobi) is a domain error naming the first offending row."""
+    cfg = make_config("c2", n=3)
+    lib = pc.from_config(cfg)
+    r, v = lib.assemble(torch.from_numpy(cfg["u"]).cuda())
+    rp, ci = lib.pattern()
+    row = 3 * 5 + 1  # node 5, component 1
+    d = rp[row] + int(np.nonzero(ci[rp[row]:rp[row + 1]] == row)[0][0])
+    v[d] = -abs(float(v[d]))
+    lib.set_preconditioner(kind)
+    with pytest.raises(pc.CommetError, match=str(row if kind == "jacobi" else 15)):
+        lib.cg_jacobi(v, r, rtol=1e-8)
+
+
 def test_block_jacobi_newton_twist_matches_oracle(pc):
     n, steps = 3, 5
     mesh, ncm, lib, dofs, _ = _twist_setup(pc, n)
