@@ -24,7 +24,7 @@ PY
 }
 mut "0.25 * Jd * Ci" "0.26 * Jd * Ci"
 mut "double s = (i == kk) ? S[J * 3 + L] : 0.0;" "double s = 0.0;"
-mut "f2 * dy[j * 3 + p] * dy[j * 3 + q]" "f2 * dy[j * 3 + p] * dy[j * 3 + p]"
+mut "f2 * dy[j * nk + p] * dy[j * nk + q]" "f2 * dy[j * nk + p] * dy[j * nk + p]"
 mut "h[1][I * 3 + J] = I1 * d - C[I * 3 + J];" "h[1][I * 3 + J] = I1 * d - C[J * 3 + I] * 1.0000001;"
 mut "H[8] += 2.0 * m->kappa;" "H[8] += 1.0 * m->kappa;"
 mut "s += F[i * 3 + I] * CC[I4(I, J, K, L)] * F[kk * 3 + K];" "s += F[i * 3 + I] * CC[I4(I, J, K, L)] * F[K * 3 + kk];"
@@ -32,6 +32,8 @@ mut "if (B) t += B[j * 3 + p];" ""
 mut "F[i * 3 + J] += u[3 * node + i] * gN[a * 3 + J];" "F[i * 3 + J] += u[3 * node + J] * gN[a * 3 + i];"
 mut "r[3 * (node - node_begin) + i] += wq * s;" "r[3 * (node - node_begin) + i] += s;"
 mut "double I2 = 0.5 * (I1 * I1 - trC2);" "double I2 = 0.5 * (I1 * I1 + trC2);"
+# the ICNN on 5 (anisotropic) inputs: W1 is [w][nk]
+mut "for (int i = 0; i < nin; i++) s += A[(size_t)j * nin + i] * z[i];" "for (int i = 0; i < nin; i++) s += A[(size_t)j * (k == 1 ? 3 : nin) + i] * z[i];"
 # the s8(f) variants: isochoric G-tensor table, CANN chain rule, Gent-Thomas
 mut "const double Ib[2] = {Ib1, Ib2}, e[2] = {-1.0 / 3.0, -2.0 / 3.0};" "const double Ib[2] = {Ib1, Ib2}, e[2] = {-1.0 / 3.0, -1.0 / 3.0};"
 mut "GGb[1][I4(i, j, k, l)] = Bb[i * 3 + j] * Bb[k * 3 + l] -" "GGb[1][I4(i, j, k, l)] = Bb[i * 3 + j] * Bb[k * 3 + l] +"
