@@ -170,11 +170,15 @@ def test_newton_zero_load(pc):
     assert not u.any()
 
 
-def test_newton_uniaxial_closed_form(pc):
+@pytest.mark.parametrize("precond", ["jacobi", "block_jacobi"])
+def test_newton_uniaxial_closed_form(pc, precond):
+    """Partially constrained nodes (one or two components fixed): the block-Jacobi blocks mix
+    eliminated unit rows with free ones and must stay SPD."""
     from tests.test_oracle_newton import mooney_rivlin_ncm, mr_lateral_stress
     c1, c2, kappa, lam = 0.7, 0.2, 3.0, 1.6
     mesh, dofs, vals = twist.uniaxial_problem(lam)
     lib = _ctx(pc, mesh, mooney_rivlin_ncm(c1, c2, kappa))
+    lib.set_preconditioner(precond)
     lib.set_dirichlet(dofs)
     u = torch.zeros(3 * mesh["n_nodes"], dtype=torch.float64, device="cuda")
     rep = lib.newton_step(u, vals, atol=1e-13, rtol=1e-14, cg_rtol=1e-14)
