@@ -221,13 +221,16 @@ def _elements_of(conn, a):
     return np.nonzero((conn == a).any(axis=1))[0]
 
 
-def sampled_rows_check(name, n_samples=12, seed=0):
+def sampled_rows_check(name, n_samples=12, seed=0, ncm=None):
     """Full BASELINE size, the bench's launch configuration: the GPU's CSR rows of
     sampled nodes (interior, faces, edges, corners) against the oracle assembling
-    only the elements that touch each node (those rows are then complete)."""
+    only the elements that touch each node (those rows are then complete).
+    ncm: another NCM on the config's mesh and displacement (the variants)."""
     torch = _torch()
     import paper_2510_00884_b200 as pc
     cfg = gen.make_config(name)
+    if ncm is not None:
+        cfg["ncm"] = ncm
     lib = pc.from_config(cfg)
     u = torch.from_numpy(cfg["u"]).cuda()
     r, v = lib.assemble(u)
@@ -266,3 +269,14 @@ def test_parity_c5_sampled():
     """c5: 4.09e9 nonzeros (> 2^31: int64 row starts), 256^3 hex8 -- sampled rows."""
     ev, er = sampled_rows_check("c5", n_samples=10)
     print(f"c5 sampled rows: values rel err {ev:.2e}, residual rel err {er:.2e}")
+
+
+@pytest.mark.parametrize("variant", ["icnn_isochoric", "icnn_anisotropic", "cann_anisotropic", "ickan"])
+def test_parity_full_size_sampled_variants(variant):
+    """The variants' instantiations at the c3 size (2.1M qp, the persistent grid of the bench):
+    sampled complete rows against the oracle."""
+    ncm = {"icnn_isochoric": lambda: dict(gen.ncm_weights(64, 3, 0.3, 11, 10.0), kinematics="isochoric"),
+           "icnn_anisotropic": lambda: gen.anisotropic(gen.ncm_weights(64, 3, 0.3, 14, 10.0, n_in=5)),
+           "cann_anisotropic": lambda: gen.anisotropic(gen.cann_params(4, seed=6, n_in=5)),
+           "ickan": lambda: gen.ickan_params()}[variant]()
+    sampled_rows_check("c3", n_samples=8, ncm=ncm)
