@@ -57,6 +57,9 @@
 #ifndef COMMET_ANALYTIC_MINB
 #define COMMET_ANALYTIC_MINB 4  // CTAs per SM of the analytic-network (NET = 1) kernels (measured: GT +7 %, CANN +4 % over 3)
 #endif
+#ifndef COMMET_FWD
+#define COMMET_FWD 1  // forward value+Jacobian sweep, Hessian terms in the backward pass (L <= 3, no skips)
+#endif
 #ifndef COMMET_PINGPONG
 #define COMMET_PINGPONG 0  // measured neutral (c3 10.31 vs 10.26 ms): barriers kept
 #endif
@@ -148,7 +151,13 @@ struct Cfg {
   static constexpr int JMG = NWARP / QB, MT_J = MTILES / JMG;
   // A-fragment register ring depth (k-steps) of the value/adjoint and Jacobian GEMMs
   static constexpr int PD_V = COMMET_PD_V, PD_J = COMMET_PD_J;
-  static constexpr int LDA = NK * Q + 4;           // act row stride (= 4 mod 16: conflict-free B frags)
+  // one forward sweep for the value and the Jacobian (3-input ICNN assembly, L = 2 or 3): act
+  // holds z | s (.) J (4 column groups per qp) and keeps s_2 (.) J_2 for the backward pass.
+  // Measured (tools/ab_bench.py): w = 128 (c4) 41.10 -> 39.94 ms; w = 64 (c3) 10.29 -> 10.64 ms
+  // (the 16-tile forward GEMM spills at 168 registers and the inner layer's Hessian term needs
+  // a division per neuron), so w >= 128 only.
+  static constexpr bool FWDC = COMMET_FWD && W >= 128 && NET == 0 && NK == 3 && MODE == 0 && !COMMET_PINGPONG;
+  static constexpr int LDA = (FWDC ? 4 : NK) * Q + 4;  // act row stride (= 4 mod 16: conflict-free B frags)
   static constexpr int LDS = Q + 2;                // s/c row stride (2-way conflicts at most)
   static_assert(W % 8 == 0 && Q % 8 == 0 && Q % NQ == 0, "tile");
   static_assert(Q <= 32, "stage-1 threads (one per qp) must sit in warp 0");
@@ -167,19 +176,22 @@ struct Smem {
   // per-qp stride of the stage-7a outputs (odd: bank spread); anisotropic: 5 factor pairs
   static constexpr int PS = C::KIN == 2 ? kPostAniso : 101;
   int act, sb, cb, qF, qk, qg, qH, hred, gsk, gN, ue, wq, qN, tab, qP, post, X, qA, total;
-  __host__ __device__ Smem(int L) {
+  // fwd: the forward-sweep path runs (C::FWDC, 2 <= L <= 3, no hidden skips): no c buffers
+  __host__ __device__ static bool fwd_path(int L, bool skips) { return C::FWDC && L >= 2 && L <= 3 && !skips; }
+  __host__ __device__ Smem(int L, bool skips = false) {
+    const bool fwd = fwd_path(L, skips);
     int o = 0;
     // the network buffers: ICNN only (the analytic networks run per qp in registers)
     const bool icnn = C::NET == 0;
     act = o; o += icnn ? C::W * C::LDA : 0;
     sb = o;  o += icnn ? (L > 1 ? L - 1 : 0) * C::W * C::LDS : 0;   // s_l, l = 1..L-1
-    cb = o;  o += icnn ? (L > 1 ? L - 1 : 1) * C::W * C::LDS : 0;   // c_l, l = 2..L (L == 1: c_1)
+    cb = o;  o += icnn && !fwd ? (L > 1 ? L - 1 : 1) * C::W * C::LDS : 0;   // c_l, l = 2..L (L == 1: c_1)
     const int dead = o;
     qF = o;  o += C::Q * 9;
     qk = o;  o += C::Q * C::NK;
     qg = o;  o += C::Q * C::NK;
     qH = o;  o += C::Q * C::NH;
-    hred = o; o += C::JMG * C::Q * C::NH;  // Jacobian-pass H partials per warp row group
+    hred = o; o += (C::JMG + (C::FWDC ? C::VMG : 0)) * C::Q * C::NH;  // H partials per warp row group
     // (the adjoint-pass g/H_1 partials, VMG x Q x 9, live in act: dead at that point)
     gsk = o; o += C::Q * C::NK;
     gN = o;  o += C::Q * C::NEN * 3;
@@ -346,13 +358,222 @@ __device__ __forceinline__ void material_outputs(const AsmArgs& A, const NcmDev&
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Forward sweep (3-input ICNN, L = 2 or 3, no hidden skips): the value and the input Jacobian
+// in one GEMM per layer -- y_l = W_l z_{l-1} and J_l = W_l (s_{l-1} (.) J_{l-1}) share their A
+// operand -- so each hidden weight matrix is read once on the way forward.  The last layer's
+// Hessian term is final at once (c_L = a s_L (1 - s_L)); the inner layer's (L = 3: layer 2)
+// waits in act as s_2 (.) J_2 for lambda_2 from the backward pass:
+//   c_2 J_2 J_2^T = lambda_2 (1 - s_2) / s_2 (s_2 J_2)(s_2 J_2)^T.
+// The backward pass then gives g and H_1 as before (stage 4's l = 2 epilogue, stage 5).
+// act: columns [0, Q) z_l / mu_l, [Q, 4Q) s_l (.) J_l; on entry z_1 | D_1 (stage 2).
+// ---------------------------------------------------------------------------
+template <class C>
+__device__ __forceinline__ void fwd_sweep(const NcmDev& m, int L, double* act, double* sb, double* hred, double* qg,
+                                          double* qH, const double* gsk, const double* stab) {
+  constexpr int W = C::W, Q = C::Q, LDA = C::LDA, LDS = C::LDS, KT2 = C::KT2;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+  const size_t frag_layer = (size_t)2 * W * W;
+  // ---- forward: layers 2..L, warp tile = MT_J m-tiles x 4 column groups of one qp block ----
+  {
+    const int jm = warp / C::QB, qb = warp % C::QB;
+    const int mt0 = jm * C::MT_J;
+    int ncol[4];
+#pragma unroll
+    for (int c = 0; c < 4; c++) ncol[c] = c * Q + qb * 8;
+    double hp[2][6];
+#pragma unroll
+    for (int h = 0; h < 2; h++)
+#pragma unroll
+      for (int x = 0; x < 6; x++) hp[h][x] = 0.0;
+    for (int l = 2; l <= L; l++) {
+      double acc[C::MT_J][4][2];
+      warp_gemm<C::MT_J, 4, KT2, C::PD_J>(m.Wfrag + (l - 2) * frag_layer, mt0, act, LDA, ncol, acc);
+      __syncthreads();
+#pragma unroll
+      for (int i = 0; i < C::MT_J; i++) {
+        const int j = (mt0 + i) * 8 + g;
+        const double bj = __ldg(m.b + (l - 1) * W + j);
+        const double aj = __ldg(m.a + j);
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+          const int q = qb * 8 + 2 * t + h;
+          const double y = acc[i][0][h] + bj;
+          const double J0 = acc[i][1][h], J1 = acc[i][2][h], J2 = acc[i][3][h];
+          if (l < L) {
+            double z, s;
+            softplus_sig(y, stab, z, s);
+            sb[((l - 1) * W + j) * LDS + q] = s;
+            act[j * LDA + q] = z;
+            act[j * LDA + Q + q] = s * J0;
+            act[j * LDA + 2 * Q + q] = s * J1;
+            act[j * LDA + 3 * Q + q] = s * J2;
+          } else {  // last layer: mu_L = a s_L for the backward pass, c_L final
+            const double s = sigmoid_tab(y, stab);
+            const double c = aj * s * (1.0 - s);
+            const double c0 = c * J0, c1 = c * J1, c2 = c * J2;
+            hp[h][0] += c0 * J0; hp[h][1] += c0 * J1; hp[h][2] += c0 * J2;
+            hp[h][3] += c1 * J1; hp[h][4] += c1 * J2; hp[h][5] += c2 * J2;
+            act[j * LDA + q] = aj * s;
+          }
+        }
+      }
+      __syncthreads();
+    }
+#pragma unroll
+    for (int h = 0; h < 2; h++)
+#pragma unroll
+      for (int x = 0; x < 6; x++) {
+        double v = hp[h][x];
+        v += __shfl_xor_sync(0xffffffffu, v, 4);
+        v += __shfl_xor_sync(0xffffffffu, v, 8);
+        v += __shfl_xor_sync(0xffffffffu, v, 16);
+        hp[h][x] = v;
+      }
+    if (g == 0) {
+#pragma unroll
+      for (int h = 0; h < 2; h++)
+#pragma unroll
+        for (int x = 0; x < 6; x++) hred[(jm * Q + qb * 8 + 2 * t + h) * 6 + x] = hp[h][x];
+    }
+  }
+  // ---- backward: mu_{l-1} = (W_l^T mu_l) (.) s_{l-1}; layer 1 -> g, H_1 partials -------------
+  {
+    const int vm = warp / C::VNG, vn = warp % C::VNG;
+    const int mt0 = vm * C::MT_V;
+    int ncol[C::NT_V];
+#pragma unroll
+    for (int j = 0; j < C::NT_V; j++) ncol[j] = (vn * C::NT_V + j) * 8;
+    for (int l = L; l >= 2; l--) {
+      double acc[C::MT_V][C::NT_V][2];
+      warp_gemm<C::MT_V, C::NT_V, KT2, C::PD_V>(m.Wfrag + (l - 2) * frag_layer + (size_t)W * W, mt0, act, LDA, ncol,
+                                               acc);
+      __syncthreads();
+      if (l > 2) {  // l = 3: lambda_2 -> mu_2, and layer 2's Hessian term from s_2 (.) J_2
+        double hb[C::NT_V][2][6];
+#pragma unroll
+        for (int jj = 0; jj < C::NT_V; jj++)
+#pragma unroll
+          for (int h = 0; h < 2; h++)
+#pragma unroll
+            for (int x = 0; x < 6; x++) hb[jj][h][x] = 0.0;
+#pragma unroll
+        for (int i = 0; i < C::MT_V; i++) {
+          const int j = (mt0 + i) * 8 + g;
+#pragma unroll
+          for (int jj = 0; jj < C::NT_V; jj++)
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+              const int q = ncol[jj] + 2 * t + h;
+              const double lam = acc[i][jj][h];
+              const double s = sb[((l - 2) * W + j) * LDS + q];
+              const double k2 = lam * (1.0 - s) / s;
+              const double P0 = act[j * LDA + Q + q], P1 = act[j * LDA + 2 * Q + q], P2 = act[j * LDA + 3 * Q + q];
+              const double c0 = k2 * P0, c1 = k2 * P1, c2 = k2 * P2;
+              double* hh = hb[jj][h];
+              hh[0] += c0 * P0; hh[1] += c0 * P1; hh[2] += c0 * P2;
+              hh[3] += c1 * P1; hh[4] += c1 * P2; hh[5] += c2 * P2;
+              act[j * LDA + q] = lam * s;  // mu_2
+            }
+        }
+#pragma unroll
+        for (int jj = 0; jj < C::NT_V; jj++)
+#pragma unroll
+          for (int h = 0; h < 2; h++)
+#pragma unroll
+            for (int x = 0; x < 6; x++) {
+              double v = hb[jj][h][x];
+              v += __shfl_xor_sync(0xffffffffu, v, 4);
+              v += __shfl_xor_sync(0xffffffffu, v, 8);
+              v += __shfl_xor_sync(0xffffffffu, v, 16);
+              hb[jj][h][x] = v;
+            }
+        if (g == 0) {
+#pragma unroll
+          for (int jj = 0; jj < C::NT_V; jj++)
+#pragma unroll
+            for (int h = 0; h < 2; h++)
+#pragma unroll
+              for (int x = 0; x < 6; x++)
+                hred[((C::JMG + vm) * Q + ncol[jj] + 2 * t + h) * 6 + x] = hb[jj][h][x];
+        }
+      } else {  // l == 2: mu_1, c_1 -> partials of g = W1^T mu_1 and H_1 = W1^T diag(c_1) W1
+        double pg[C::NT_V][2][9];
+#pragma unroll
+        for (int jj = 0; jj < C::NT_V; jj++)
+#pragma unroll
+          for (int h = 0; h < 2; h++)
+#pragma unroll
+            for (int x = 0; x < 9; x++) pg[jj][h][x] = 0.0;
+#pragma unroll
+        for (int i = 0; i < C::MT_V; i++) {
+          const int j = (mt0 + i) * 8 + g;
+          const double w0 = __ldg(m.W1 + j * 3), w1 = __ldg(m.W1 + j * 3 + 1), w2 = __ldg(m.W1 + j * 3 + 2);
+#pragma unroll
+          for (int jj = 0; jj < C::NT_V; jj++)
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+              const int q = ncol[jj] + 2 * t + h;
+              const double lam = acc[i][jj][h];
+              const double s = sb[j * LDS + q];
+              const double mu = lam * s, c = mu * (1.0 - s);
+              double* P9 = pg[jj][h];
+              P9[0] += w0 * mu; P9[1] += w1 * mu; P9[2] += w2 * mu;
+              const double c0 = c * w0, c1 = c * w1;
+              P9[3] += c0 * w0; P9[4] += c0 * w1; P9[5] += c0 * w2;
+              P9[6] += c1 * w1; P9[7] += c1 * w2; P9[8] += c * w2 * w2;
+            }
+        }
+#pragma unroll
+        for (int jj = 0; jj < C::NT_V; jj++)
+#pragma unroll
+          for (int h = 0; h < 2; h++)
+#pragma unroll
+            for (int x = 0; x < 9; x++) {
+              double v = pg[jj][h][x];
+              v += __shfl_xor_sync(0xffffffffu, v, 4);
+              v += __shfl_xor_sync(0xffffffffu, v, 8);
+              v += __shfl_xor_sync(0xffffffffu, v, 16);
+              pg[jj][h][x] = v;
+            }
+        if (g == 0) {  // act is dead now: partials at (vm, q)
+#pragma unroll
+          for (int jj = 0; jj < C::NT_V; jj++)
+#pragma unroll
+            for (int h = 0; h < 2; h++)
+#pragma unroll
+              for (int x = 0; x < 9; x++) act[(vm * Q + ncol[jj] + 2 * t + h) * 9 + x] = pg[jj][h][x];
+        }
+      }
+      __syncthreads();
+    }
+  }
+  // ---- g = W1^T mu_1 + skip_out, H_1 -----------------------------------------------------
+  if (tid < Q) {
+    const int q = tid;
+    double v[9];
+#pragma unroll
+    for (int x = 0; x < 9; x++) v[x] = 0.0;
+#pragma unroll
+    for (int r = 0; r < C::VMG; r++)
+#pragma unroll
+      for (int x = 0; x < 9; x++) v[x] += act[(r * Q + q) * 9 + x];
+#pragma unroll
+    for (int x = 0; x < 3; x++) qg[q * 3 + x] = v[x] + gsk[q * 3 + x] + __ldg(m.skip_out + x);
+#pragma unroll
+    for (int x = 0; x < 6; x++) qH[q * 6 + x] = v[3 + x];
+  }
+  __syncthreads();
+}
+
 template <class C>
 __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
   constexpr int W = C::W, Q = C::Q, NEN = C::NEN, NQ = C::NQ, E = C::E;
   constexpr int LDA = C::LDA, LDS = C::LDS, KT2 = C::KT2;
   extern __shared__ __align__(16) double smem[];
   const int L = A.ncm.L;
-  const Smem<C> sm(L);
+  const Smem<C> sm(L, A.ncm.skip_h != nullptr);
   double* act = smem + sm.act;
   double* sb = smem + sm.sb;
   double* cb = smem + sm.cb;
@@ -376,6 +597,7 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
   const NcmDev& m = A.ncm;
   const bool skips = m.skip_h != nullptr;
+  const bool fwd = Smem<C>::fwd_path(L, skips);
   const int64_t n_batches = (A.el_count + E - 1) / E;
   const size_t frag_layer = (size_t)2 * W * W;  // W and W^T fragments per hidden layer
   for (int x = threadIdx.x; x < kActTabSize; x += C::NTHR) stab[x] = __ldg(A.ncm.act_tab + x);
@@ -565,6 +787,11 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
         if (L > 1) {
           sb[j * LDS + q] = s;
           act[j * LDA + q] = z;
+          if constexpr (C::FWDC)
+            if (fwd) {  // D_1 = s_1 (.) W1: the Jacobian columns of the forward sweep
+#pragma unroll
+              for (int c = 0; c < 3; c++) act[j * LDA + (c + 1) * Q + q] = s * __ldg(m.W1 + j * 3 + c);
+            }
         } else {
           const double aj = __ldg(m.a + j);
           act[j * LDA + q] = aj * s;
@@ -578,6 +805,10 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
     __syncthreads();
     STAGE_MARK(2)
 
+    if constexpr (C::FWDC) {
+      if (fwd) fwd_sweep<C>(m, L, act, sb, hred, qg, qH, gsk, stab);
+    }
+    if (!fwd) {
     // ---- stage 3: value pass, layers 2..L --------------------------------------------
     {
       const int vm = warp / C::VNG, vn = warp % C::VNG;
@@ -942,6 +1173,7 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
       __syncthreads();
     }
 
+    }  // !fwd
     }  // NET == 0
     STAGE_MARK(6)
 #ifdef COMMET_EXP_SKIP_NCM
@@ -969,6 +1201,10 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
           if (L > 1)
 #pragma unroll
             for (int r = 0; r < C::JMG; r++) s += hred[(r * Q + q) * C::NH + x];
+          if constexpr (C::FWDC)
+            if (fwd && L == 3)  // the inner layer's Hessian term, from the backward pass
+#pragma unroll
+              for (int r = 0; r < C::VMG; r++) s += hred[((C::JMG + r) * Q + q) * C::NH + x];
           H6[x] = s;
         }
       } else {
@@ -1185,7 +1421,7 @@ void fused_weight_frag_fill(int w, int L, const double* Wrow, double* out) {
 
 template <class C>
 static int launch_cfg(const AsmArgs& a, cudaStream_t st, int* launches) {
-  const Smem<C> sm(a.ncm.L);
+  const Smem<C> sm(a.ncm.L, a.ncm.skip_h != nullptr);
   size_t bytes = (size_t)sm.total * sizeof(double);
 #ifdef COMMET_EXP_SMEM_PAD
   bytes += COMMET_EXP_SMEM_PAD;  // experiments only: limit resident CTAs per SM
