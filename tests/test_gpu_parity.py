@@ -70,6 +70,11 @@ CASES = [
     ("tet", 3, 64, 3, False, False),
     ("tet", 2, 128, 3, True, False),
     ("tet", 2, 32, 3, False, True),
+    # w = 128: the forward sweep with L = 2 (the last layer right after layer 1), the three-pass
+    # fallback at L = 4 and L = 1
+    ("hex", 3, 128, 2, False, True),
+    ("tet", 2, 128, 4, False, False),
+    ("hex", 2, 128, 1, False, False),
 ]
 
 
