@@ -36,6 +36,7 @@ VARIANTS = {
     "cann_isochoric": lambda: cann_params(5, seed=4, kinematics="isochoric"),
     "icnn_isochoric_16x2": lambda: _iso_icnn(16, 2),
     "icnn_isochoric_64x3": lambda: _iso_icnn(64, 3),
+    "icnn_isochoric_128x3": lambda: _iso_icnn(128, 3),  # the forward-sweep instantiation
     "ickan": lambda: ickan_params(),
     "ickan_isochoric": lambda: ickan_params((3, 5, 1), nb=7, seed=5, kinematics="isochoric"),
     "cann_anisotropic": lambda: anisotropic(cann_params(4, seed=6, n_in=5)),
