@@ -145,18 +145,20 @@ struct Cfg {
   static constexpr int NT_V = (QB >= 2 && TPW % 2 == 0 && TPW >= 4) ? 2 : 1;
   static constexpr int MT_V = TPW / NT_V;
   static constexpr int VNG = QB / NT_V, VMG = MTILES / MT_V;
-  // material mode: rows of per-qp partial sums of the network value a . z_L
-  static constexpr int NPR = MODE == 0 ? 0 : (VMG > NTHR / Q ? VMG : NTHR / Q);
   // Jacobian warp tiles: JMG m-groups x QB qp blocks, each MT_J x 3 tiles
   static constexpr int JMG = NWARP / QB, MT_J = MTILES / JMG;
+  // material mode: rows of per-qp partial sums of the network value a . z_L (value tiling: VMG
+  // rows; forward sweep: JMG rows; L = 1: NTHR / Q rows)
+  static constexpr int NPR0 = VMG > NTHR / Q ? VMG : NTHR / Q;
+  static constexpr int NPR = MODE == 0 ? 0 : (JMG > NPR0 ? JMG : NPR0);
   // A-fragment register ring depth (k-steps) of the value/adjoint and Jacobian GEMMs
   static constexpr int PD_V = COMMET_PD_V, PD_J = COMMET_PD_J;
-  // one forward sweep for the value and the Jacobian (3-input ICNN assembly, L = 2 or 3): act
+  // one forward sweep for the value and the Jacobian (3-input ICNN, L = 2 or 3): act
   // holds z | s (.) J (4 column groups per qp) and keeps s_2 (.) J_2 for the backward pass.
   // Measured (tools/ab_bench.py): w = 128 (c4) 41.10 -> 39.94 ms; w = 64 (c3) 10.29 -> 10.64 ms
   // (the 16-tile forward GEMM spills at 168 registers and the inner layer's Hessian term needs
   // a division per neuron), so w >= 128 only.
-  static constexpr bool FWDC = COMMET_FWD && W >= 128 && NET == 0 && NK == 3 && MODE == 0 && !COMMET_PINGPONG;
+  static constexpr bool FWDC = COMMET_FWD && W >= 128 && NET == 0 && NK == 3 && !COMMET_PINGPONG;
   static constexpr int LDA = (FWDC ? 4 : NK) * Q + 4;  // act row stride (= 4 mod 16: conflict-free B frags)
   static constexpr int LDS = Q + 2;                // s/c row stride (2-way conflicts at most)
   static_assert(W % 8 == 0 && Q % 8 == 0 && Q % NQ == 0, "tile");
@@ -294,9 +296,14 @@ __device__ __forceinline__ void material_outputs(const AsmArgs& A, const NcmDev&
         if (L > 1)
 #pragma unroll
           for (int r = 0; r < C::JMG; r++) s += hred[(r * Q + q) * C::NH + x];
+        if constexpr (C::FWDC)
+          if (Smem<C>::fwd_path(L, m.skip_h != nullptr) && L == 3)
+#pragma unroll
+            for (int r = 0; r < C::VMG; r++) s += hred[((C::JMG + r) * Q + q) * C::NH + x];
         H6[x] = s;
       }
-      const int rows = L > 1 ? C::VMG : C::NTHR / Q;
+      // partial sums of a . z_L: one row per value-tiling row group (forward sweep: per jm group)
+      const int rows = L > 1 ? (C::FWDC && Smem<C>::fwd_path(L, m.skip_h != nullptr) ? C::JMG : C::VMG) : C::NTHR / Q;
       for (int r = 0; r < rows; r++) N += qNp[r * Q + q];
       N += __ldg(m.skip_out) * kq[0] + __ldg(m.skip_out + 1) * kq[1] + __ldg(m.skip_out + 2) * kq[2];
     } else {
@@ -371,7 +378,7 @@ __device__ __forceinline__ void material_outputs(const AsmArgs& A, const NcmDev&
 // ---------------------------------------------------------------------------
 template <class C>
 __device__ __forceinline__ void fwd_sweep(const NcmDev& m, int L, double* act, double* sb, double* hred, double* qg,
-                                          double* qH, const double* gsk, const double* stab) {
+                                          double* qH, const double* gsk, const double* stab, double* qNp) {
   constexpr int W = C::W, Q = C::Q, LDA = C::LDA, LDS = C::LDS, KT2 = C::KT2;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
   const size_t frag_layer = (size_t)2 * W * W;
@@ -382,7 +389,7 @@ __device__ __forceinline__ void fwd_sweep(const NcmDev& m, int L, double* act, d
     int ncol[4];
 #pragma unroll
     for (int c = 0; c < 4; c++) ncol[c] = c * Q + qb * 8;
-    double hp[2][6];
+    double hp[2][6], nacc[2] = {0.0, 0.0};  // nacc: material points, partial a . z_L
 #pragma unroll
     for (int h = 0; h < 2; h++)
 #pragma unroll
@@ -410,7 +417,14 @@ __device__ __forceinline__ void fwd_sweep(const NcmDev& m, int L, double* act, d
             act[j * LDA + 2 * Q + q] = s * J1;
             act[j * LDA + 3 * Q + q] = s * J2;
           } else {  // last layer: mu_L = a s_L for the backward pass, c_L final
-            const double s = sigmoid_tab(y, stab);
+            double s;
+            if constexpr (C::MODE == 1) {  // material points need the value: z_L too
+              double z;
+              softplus_sig(y, stab, z, s);
+              nacc[h] += aj * z;
+            } else {
+              s = sigmoid_tab(y, stab);
+            }
             const double c = aj * s * (1.0 - s);
             const double c0 = c * J0, c1 = c * J1, c2 = c * J2;
             hp[h][0] += c0 * J0; hp[h][1] += c0 * J1; hp[h][2] += c0 * J2;
@@ -436,6 +450,16 @@ __device__ __forceinline__ void fwd_sweep(const NcmDev& m, int L, double* act, d
       for (int h = 0; h < 2; h++)
 #pragma unroll
         for (int x = 0; x < 6; x++) hred[(jm * Q + qb * 8 + 2 * t + h) * 6 + x] = hp[h][x];
+    }
+    if constexpr (C::MODE == 1) {
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        double v = nacc[h];
+        v += __shfl_xor_sync(0xffffffffu, v, 4);
+        v += __shfl_xor_sync(0xffffffffu, v, 8);
+        v += __shfl_xor_sync(0xffffffffu, v, 16);
+        if (g == 0) qNp[jm * Q + qb * 8 + 2 * t + h] = v;
+      }
     }
   }
   // ---- backward: mu_{l-1} = (W_l^T mu_l) (.) s_{l-1}; layer 1 -> g, H_1 partials -------------
@@ -806,7 +830,7 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
     STAGE_MARK(2)
 
     if constexpr (C::FWDC) {
-      if (fwd) fwd_sweep<C>(m, L, act, sb, hred, qg, qH, gsk, stab);
+      if (fwd) fwd_sweep<C>(m, L, act, sb, hred, qg, qH, gsk, stab, qNp);
     }
     if (!fwd) {
     // ---- stage 3: value pass, layers 2..L --------------------------------------------

@@ -37,6 +37,8 @@ def pc():
 MODELS = {
     "icnn_64x3": lambda: ncm_weights(64, 3, 0.3, 1, 10.0),
     "icnn_16x1": lambda: ncm_weights(16, 1, 0.3, 2, 10.0),
+    "icnn_128x3": lambda: ncm_weights(128, 3, 0.3, 5, 10.0),  # forward sweep, L = 3
+    "icnn_128x2": lambda: ncm_weights(128, 2, 0.3, 6, 10.0),  # forward sweep, L = 2
     "icnn_iso_16x2": isochoric_icnn,
     "cann": lambda: cann_params(4, seed=3),
     "gent_thomas": gent_thomas_params,
