@@ -182,3 +182,29 @@ def test_anisotropic_invariants_values():
     Q *= np.sign(np.linalg.det(Q))
     o = oracle.material_point(dict(m, kappa=0.0), Q)
     assert np.abs(o["k"]).max() < 1e-14
+
+
+@pytest.mark.parametrize("bad", ["gt_on_5_inputs", "icnn_skips_on_5_inputs", "unknown_network"])
+def test_unsupported_network_kinematics_raise(bad):
+    """The checker fails loudly: a network / kinematics combination the inner network cannot
+    evaluate raises (material point, energy and assembly) instead of using uninitialised
+    derivatives."""
+    if bad == "gt_on_5_inputs":
+        m = anisotropic(gent_thomas_params())
+    elif bad == "icnn_skips_on_5_inputs":
+        m = anisotropic(ncm_weights(8, 2, n_in=5))
+        m["skip_hidden"] = np.zeros((1, 8, 3))
+    else:
+        m = dict(gent_thomas_params(), network=7)
+    F = I3 + 0.05 * np.arange(9).reshape(3, 3) / 9
+    with pytest.raises(oracle.OracleError):
+        oracle.material_point(m, F)
+    X, conn = hex_mesh(1)
+    gN, w = shape_gradients(X, conn, 0)
+    u = np.zeros(X.size)
+    with pytest.raises(oracle.OracleError):
+        oracle.energy(m, conn, gN, w, u)
+    rp, ci = oracle.pattern(X.shape[0], conn)
+    for mode in (0, 1):
+        with pytest.raises(oracle.OracleError, match="inner network"):
+            oracle.assemble(m, X.shape[0], conn, gN, w, u, rp, ci, mode=mode)
