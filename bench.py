@@ -71,6 +71,39 @@ def dist_env():
     return ws, rank, local
 
 
+def launch_plan(gpus: int, env: dict, device_count: int, needs_gpus: bool = True):
+    """What `bench.py --gpus N` does in this process: ("run", None) -- this process is one
+    of the N ranks (or N = 1); ("relaunch", None) -- re-run itself under torch.distributed.run
+    with N ranks (WORLD_SIZE unset, N > 1); ("refuse", why) -- --gpus disagrees with the
+    launcher's WORLD_SIZE, or fewer than N devices are visible (a silent 1-GPU line labelled
+    N GPUs would be wrong)."""
+    if gpus < 1:
+        return "refuse", f"--gpus {gpus} < 1"
+    ws = env.get("WORLD_SIZE")
+    if ws is not None and int(ws) != gpus:
+        return "refuse", f"--gpus {gpus} but the launcher started WORLD_SIZE={ws} ranks"
+    if needs_gpus and device_count < gpus:
+        return "refuse", f"--gpus {gpus} but only {device_count} CUDA device(s) are visible"
+    if ws is None and gpus > 1:
+        return ("relaunch", None) if needs_gpus else ("run", None)
+    return "run", None
+
+
+def relaunch_cmd(gpus: int, argv: list, port: int):
+    """torch.distributed.run command line that re-runs this script with `gpus` ranks on this node."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+            "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + list(argv)
+
+
+def _free_port():
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
 class Clocks:
     """nvidia-smi sampler running during the timed region."""
 
@@ -164,7 +197,7 @@ def run_reference(args):
             times.append(time.perf_counter() - t0)
     t = float(np.mean(times))
     value = ns * n_q / t
-    line = dict(impl="reference", metric=METRIC, value=value, unit="qp/s", n_gpus=ws, steps=args.steps,
+    line = dict(impl="reference", metric=METRIC, value=value, unit="qp/s", n_gpus=args.gpus, steps=args.steps,
                 warmup=args.warmup, ms_per_step=t * 1e3, higher_is_better=True, scaling="strong",
                 vs_baseline=None, dtype="f64", data="synthetic",
                 config=dict(workload=WORKLOAD[args.config], sample_elements=ns),
@@ -194,6 +227,16 @@ def main():
                     help="N > 1: interface rows over NCCL send/recv + unpack (default), or added straight "
                          "into the owner's buffers by the kernels over NVLink P2P (CUDA IPC)")
     args = ap.parse_args()
+    ndev = 0
+    if args.impl != "reference" or "WORLD_SIZE" in os.environ:
+        import torch
+        ndev = torch.cuda.device_count() if args.impl != "reference" else 0
+    action, why = launch_plan(args.gpus, dict(os.environ), ndev, needs_gpus=args.impl != "reference")
+    if action == "refuse":
+        print(f"bench.py: {why}", file=sys.stderr, flush=True)
+        return 2
+    if action == "relaunch":
+        return subprocess.call(relaunch_cmd(args.gpus, sys.argv[1:], _free_port()))
     if args.impl == "reference":
         return run_reference(args)
 

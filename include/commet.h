@@ -169,14 +169,29 @@ commet_status commet_csr_pattern_copy(commet_ctx ctx, int64_t* row_ptr, int32_t*
 
 /* Assemble: u device fp64 [3*n_nodes] (global, every rank passes the full
  * vector); residual device fp64 [n_rows]; csr_values device fp64 [nnz].
- * Asynchronous on cuda_stream. */
+ * Asynchronous on cuda_stream.  With an NCCL communicator and a partition
+ * (n_ranks > 1, NCCL mode): every colour's interface elements (those touching a
+ * halo row) are launched first, the halo send/recv group then runs on an
+ * internal stream while the interior elements are launched, and the unpack of
+ * the received rows follows both on cuda_stream.  NCCL
+ * asynchronous errors are checked after the group (COMMET_ERR_NCCL). */
 commet_status commet_assemble(commet_ctx ctx, const double* u, double* residual,
                               double* csr_values, void* cuda_stream);
 
-/* Synchronises the ctx's last assemble stream; returns COMMET_ERR_DOMAIN and
- * *first_bad_qp = e*n_q+q (local element index) if some det F <= 0, else
- * COMMET_OK and -1. */
+/* Synchronises the ctx's last assemble stream; *first_bad_qp = this rank's
+ * lowest e*n_q+q (local element index) with det F <= 0, else -1.  Returns
+ * COMMET_ERR_DOMAIN if some det F <= 0 (R10), else COMMET_OK.
+ * With an NCCL communicator and n_ranks > 1 the call is COLLECTIVE (every rank
+ * must call it): one MIN all-reduce of (rank, first bad qp) over the
+ * communicator, so every rank returns COMMET_ERR_DOMAIN when any rank saw a
+ * bad point (the message names the lowest such rank and its index); an NCCL
+ * asynchronous error (ncclCommGetAsyncError) returns COMMET_ERR_NCCL. */
 commet_status commet_check(commet_ctx ctx, int64_t* first_bad_qp);
+
+/* As commet_check, but reports the cross-rank result: *bad_rank = the lowest
+ * rank with a det F <= 0 point and *first_bad_qp = its lowest local flat index
+ * (-1, -1 if none).  Collective under the same conditions. */
+commet_status commet_check_ranks(commet_ctx ctx, int32_t* bad_rank, int64_t* first_bad_qp);
 
 /* Select the kernel variant used by subsequent commet_assemble calls. */
 commet_status commet_set_kernel(commet_ctx ctx, int32_t variant);
@@ -264,6 +279,10 @@ commet_status commet_plan_send(commet_plan p, int32_t k, int32_t* peer, int64_t*
 commet_status commet_plan_recv(commet_plan p, int32_t k, int32_t* peer, int64_t* n_vals,
                                const int64_t** val_map, int64_t* n_res, const int64_t** res_map);
 commet_status commet_plan_colours(commet_plan p, const int64_t** colour_start, const int64_t** perm);
+/* [n_colours]: colour k's first colour_iface[k] elements (perm[colour_start[k] ..]) are its
+ * interface elements -- those with a node outside the owned range; 0 without a partition.
+ * commet_assemble launches them before the interiors so the NCCL exchange overlaps the latter. */
+commet_status commet_plan_colour_iface(commet_plan p, const int64_t** colour_iface);
 void commet_plan_destroy(commet_plan p);
 
 /* Max over all quadrature points of tr C = I1 at the last commet_assemble

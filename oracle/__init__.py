@@ -45,6 +45,10 @@ NET = {"icnn": 0, "cann": 1, "gent_thomas": 2, "ickan": 3}
 _lib = None
 
 
+class OracleError(RuntimeError):
+    """The checker could not compute a trustworthy result (it fails loudly, never silently)."""
+
+
 def lib():
     global _lib
     if _lib is None:
@@ -110,7 +114,8 @@ def ncm_eval(ncm: dict, k):
     k = np.ascontiguousarray(k, dtype=np.float64)
     N, g, H = np.zeros(1), np.zeros(3), np.zeros(9)
     rc = lib().oracle_ncm_eval(m.ptr, _p(k), _p(N), _p(g), _p(H))
-    assert rc == 0
+    if rc != 0:
+        raise OracleError(f"oracle: inner network evaluation failed (status {rc})")
     return N[0], g, H.reshape(3, 3)
 
 
@@ -121,7 +126,8 @@ def ncm_eval_n(ncm: dict, k):
     n = k.size
     N, g, H = np.zeros(1), np.zeros(n), np.zeros(n * n)
     rc = lib().oracle_ncm_eval_n(m.ptr, n, _p(k), _p(N), _p(g), _p(H))
-    assert rc == 0, rc
+    if rc != 0:
+        raise OracleError(f"oracle: inner network evaluation on {n} inputs failed (status {rc})")
     return N[0], g, H.reshape(n, n)
 
 
@@ -133,6 +139,9 @@ def material_point(ncm: dict, F):
     S, CC, P, A = np.zeros(9), np.zeros(81), np.zeros(9), np.zeros(81)
     J = lib().oracle_material_point(m.ptr, _p(F), _p(k), _p(W), _p(g), _p(H), _p(S), _p(CC),
                                     _p(P), _p(A))
+    if np.isnan(J):
+        raise OracleError("oracle: the inner network rejected this network / kinematics combination (or F is "
+                          "not finite)")
     return dict(J=J, k=k, W=W[0], g=g, H=H.reshape(3, 3), S=S.reshape(3, 3),
                 CC=CC.reshape(3, 3, 3, 3), P=P.reshape(3, 3), A=A.reshape(3, 3, 3, 3))
 
@@ -149,10 +158,13 @@ def qp_F(conn, gradN, u):
 def energy(ncm: dict, conn, gradN, qp_w, u):
     m = Ncm(ncm)
     n_el, n_en = conn.shape
-    return lib().oracle_energy(m.ptr, n_el, n_en, gradN.shape[1],
-                               _p(np.ascontiguousarray(conn, np.int32)),
-                               _p(np.ascontiguousarray(gradN)), _p(np.ascontiguousarray(qp_w)),
-                               _p(np.ascontiguousarray(u, np.float64)))
+    Pi = lib().oracle_energy(m.ptr, n_el, n_en, gradN.shape[1],
+                             _p(np.ascontiguousarray(conn, np.int32)),
+                             _p(np.ascontiguousarray(gradN)), _p(np.ascontiguousarray(qp_w)),
+                             _p(np.ascontiguousarray(u, np.float64)))
+    if np.isnan(Pi):
+        raise OracleError("oracle: energy is NaN (inner network evaluation failed or non-finite input)")
+    return Pi
 
 
 def pattern(n_nodes, conn, node_begin=0, node_end=None):
@@ -186,8 +198,13 @@ def assemble(ncm: dict, n_nodes, conn, gradN, qp_w, u, row_ptr, col_idx, node_be
                                  _p(np.ascontiguousarray(u, np.float64)), node_begin, node_end,
                                  _p(row_ptr), _p(col_idx), _p(r), _p(vals), _p(bad), mode,
                                  n_threads)
+    if miss == -2:
+        raise OracleError("oracle: inner network evaluation failed (unsupported network / kinematics "
+                          "combination)")
+    if miss == -1:
+        raise OracleError("oracle: element colouring needs more than 64 colours")
     if miss != 0:
-        raise RuntimeError("oracle: %d stiffness entries outside the pattern" % miss)
+        raise OracleError("oracle: %d stiffness entries outside the pattern" % miss)
     return r, vals, int(bad[0])
 
 

@@ -88,7 +88,10 @@ static int icnn_eval(const oracle_ncm* m, int nk, const double* K, double* N_out
   double* y = (double*)calloc(nmax, sizeof(double));
   double* dy = (double*)calloc((size_t)nmax * nk, sizeof(double));
   double* d2y = (double*)calloc((size_t)nmax * n2, sizeof(double));
-  if (!z || !dz || !d2z || !y || !dy || !d2y) return 2;
+  if (!z || !dz || !d2z || !y || !dy || !d2y) {
+    free(z); free(dz); free(d2z); free(y); free(dy); free(d2y);
+    return 2;
+  }
   int nin = nk;
   for (int i = 0; i < nk; i++) {
     z[i] = K[i];
@@ -313,11 +316,14 @@ static int ickan_eval(const oracle_ncm* m, int nk, const double* K, double* N_ou
 }
 
 /* the inner network on nin = 3 inputs (standard / isochoric kinematics) or 5 (anisotropic:
- * CANN and ICKAN only); g [nin], H [nin][nin] */
+ * ICNN, CANN and ICKAN); g [nin], H [nin][nin].  Returns 0, or a non-zero status for a
+ * configuration the network cannot evaluate: 1 bad ICNN shape / skips on 5 inputs, 2 out of
+ * memory, 3 ICKAN input count, 4 Gent-Thomas on 5 inputs, 5 unknown network. */
 int oracle_ncm_eval_n(const oracle_ncm* m, int nin, const double* K, double* N_out, double* g_out, double* H_out) {
   if (m->network == 1) return cann_eval(m, nin, K, N_out, g_out, H_out);
   if (m->network == 3) return ickan_eval(m, nin, K, N_out, g_out, H_out);
   if (m->network == 0) return icnn_eval(m, nin, K, N_out, g_out, H_out);
+  if (m->network != 2) return 5;
   if (nin != 3) return 4;
   return gt_eval(m, K, N_out, g_out, H_out);
 }
@@ -512,8 +518,20 @@ static void anisotropic_S_CC(const double F[9], double Jd, const double a0[3], c
  * S = 2 sum_m g_m h_m;  CC = 4 sum_mn H_mn h_m (x) h_n + 4 sum_m g_m HH_m
  *   (Eq. stress-cgo / stiffnes-cgo, pulled back; reading 4)
  * P = F S;  A_iJkL = d_ik S_JL + F_iI CC_IJKL F_kK  (Eq. p-stiffness)
- * Returns J.
+ * Returns J, or NaN (every output NaN) when the inner network rejects the configuration
+ * (oracle_ncm_eval_n status != 0): the checker fails loudly instead of using garbage.
  */
+static double ncm_failed(double* k_out, double* W_out, double* g_out, double* H_out, double S[9], double CC[81],
+                         double P[9], double A[81]) {
+  const double nan = NAN;
+  if (k_out) for (int p = 0; p < 3; p++) k_out[p] = nan;
+  if (W_out) *W_out = nan;
+  if (g_out) for (int p = 0; p < 3; p++) g_out[p] = nan;
+  if (H_out) for (int p = 0; p < 9; p++) H_out[p] = nan;
+  for (int p = 0; p < 9; p++) S[p] = P[p] = nan;
+  for (int p = 0; p < 81; p++) CC[p] = A[p] = nan;
+  return nan;
+}
 double oracle_material_point(const oracle_ncm* m, const double F[9], double k_out[3],
                              double* W_out, double g_out[3], double H_out[9], double S[9],
                              double CC[81], double P[9], double A[81]) {
@@ -540,7 +558,7 @@ double oracle_material_point(const oracle_ncm* m, const double F[9], double k_ou
     }
     const double k5[5] = {I1 - 3.0, I2 - 3.0, Jd - 1.0, I4v - 1.0, C2A - 1.0};
     double N5, g5[5], H5[25];
-    oracle_ncm_eval_n(m, 5, k5, &N5, g5, H5);
+    if (oracle_ncm_eval_n(m, 5, k5, &N5, g5, H5) != 0) return ncm_failed(k_out, W_out, g_out, H_out, S, CC, P, A);
     const double W5 = N5 + m->kappa * (Jd - 1.0) * (Jd - 1.0) - m->ref_shift * (Jd - 1.0);
     g5[2] += 2.0 * m->kappa * (Jd - 1.0) - m->ref_shift;
     H5[12] += 2.0 * m->kappa;
@@ -577,7 +595,7 @@ double oracle_material_point(const oracle_ncm* m, const double F[9], double k_ou
     k[1] = a * a * I2 - 3.0;
   }
   double N, g[3], H[9];
-  oracle_ncm_eval(m, k, &N, g, H);
+  if (oracle_ncm_eval(m, k, &N, g, H) != 0) return ncm_failed(k_out, W_out, g_out, H_out, S, CC, P, A);
   /* volumetric penalty (a5) and optional reference shift (reading 11) */
   double W = N + m->kappa * (Jd - 1.0) * (Jd - 1.0) - m->ref_shift * (Jd - 1.0);
   g[2] += 2.0 * m->kappa * (Jd - 1.0) - m->ref_shift;
@@ -792,7 +810,7 @@ static void assemble_element(const oracle_ncm* m, int64_t e, int n_en, int n_q,
                              const int32_t* conn, const double* gradN, const double* qp_w,
                              const double* u, int64_t node_begin, int64_t node_end,
                              const int64_t* row_ptr, const int32_t* col_idx, double* r,
-                             double* vals, int64_t* bad, int64_t* missing) {
+                             double* vals, int64_t* bad, int64_t* missing, int64_t* ncm_err) {
   const int nd = 3 * n_en;
   double* Ke = (double*)calloc((size_t)nd * nd, sizeof(double));
   const int32_t* ce = conn + e * n_en;
@@ -802,6 +820,7 @@ static void assemble_element(const oracle_ncm* m, int64_t e, int n_en, int n_q,
     double F[9], S[9], CC[81], P[9], A[81];
     qp_F(n_en, ce, gN, u, F);
     double Jd = oracle_material_point(m, F, NULL, NULL, NULL, NULL, S, CC, P, A);
+    if (isnan(Jd)) (*ncm_err)++;
     if (Jd <= 0.0) {
       int64_t flat = e * n_q + q;
 #pragma omp critical(oracle_bad)
@@ -864,7 +883,9 @@ static int colour_elements(int64_t n_nodes, int64_t n_el, int n_en, const int32_
 /* r and vals are OVERWRITTEN.  mode 0: serial, element order (Alg. 1 as
  * written).  mode 1: OpenMP over the elements of one colour at a time
  * (deterministic for any thread count).  Returns #missing pattern entries
- * (0 expected), or -1 on colouring failure. */
+ * (0 expected), -1 on colouring failure, or -2 if the inner network could not
+ * be evaluated (unsupported network / kinematics combination: the outputs are
+ * then meaningless and the caller must fail). */
 int64_t oracle_assemble(const oracle_ncm* m, int64_t n_nodes, int64_t n_el, int n_en, int n_q,
                         const int32_t* conn, const double* gradN, const double* qp_w,
                         const double* u, int64_t node_begin, int64_t node_end,
@@ -874,12 +895,12 @@ int64_t oracle_assemble(const oracle_ncm* m, int64_t n_nodes, int64_t n_el, int 
   memset(r, 0, sizeof(double) * nr);
   memset(vals, 0, sizeof(double) * row_ptr[nr]);
   *bad = -1;
-  int64_t missing = 0;
+  int64_t missing = 0, ncm_err = 0;
   if (mode == 0) {
     for (int64_t e = 0; e < n_el; e++)
       assemble_element(m, e, n_en, n_q, conn, gradN, qp_w, u, node_begin, node_end, row_ptr,
-                       col_idx, r, vals, bad, &missing);
-    return missing;
+                       col_idx, r, vals, bad, &missing, &ncm_err);
+    return ncm_err ? -2 : missing;
   }
   int32_t* colour = (int32_t*)malloc(sizeof(int32_t) * (n_el + 1));
   int ncol = colour_elements(n_nodes, n_el, n_en, conn, colour);
@@ -888,16 +909,17 @@ int64_t oracle_assemble(const oracle_ncm* m, int64_t n_nodes, int64_t n_el, int 
   if (n_threads > 0) omp_set_num_threads(n_threads);
 #endif
   for (int c = 0; c < ncol; c++) {
-    int64_t miss_c = 0;
-#pragma omp parallel for schedule(dynamic, 16) reduction(+ : miss_c)
+    int64_t miss_c = 0, err_c = 0;
+#pragma omp parallel for schedule(dynamic, 16) reduction(+ : miss_c, err_c)
     for (int64_t e = 0; e < n_el; e++)
       if (colour[e] == c)
         assemble_element(m, e, n_en, n_q, conn, gradN, qp_w, u, node_begin, node_end, row_ptr,
-                         col_idx, r, vals, bad, &miss_c);
+                         col_idx, r, vals, bad, &miss_c, &err_c);
     missing += miss_c;
+    ncm_err += err_c;
   }
   free(colour);
-  return missing;
+  return ncm_err ? -2 : missing;
 }
 
 int oracle_max_threads(void) {

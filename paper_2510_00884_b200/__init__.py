@@ -37,7 +37,7 @@ SYMBOLS = ("commet_setup", "commet_csr_pattern", "commet_csr_pattern_copy", "com
            "commet_kernel_info", "commet_max_trace_C", "commet_set_dirichlet", "commet_apply_dirichlet",
            "commet_cg_jacobi", "commet_newton_step", "commet_ncm_eval", "commet_normalize_reference",
            "commet_material_eval", "commet_halo_recv_maps", "commet_set_peer", "commet_set_peer_mode",
-           "commet_zero_outputs", "commet_set_preconditioner")
+           "commet_zero_outputs", "commet_set_preconditioner", "commet_check_ranks", "commet_plan_colour_iface")
 NEWTON_MAX_LOG = 64
 
 
@@ -114,6 +114,8 @@ _lib.commet_assemble.argtypes = [_vp, _vp, _vp, _vp, _vp]
 _lib.commet_assemble.restype = C.c_int
 _lib.commet_check.argtypes = [_vp, C.POINTER(_i64)]
 _lib.commet_check.restype = C.c_int
+_lib.commet_check_ranks.argtypes = [_vp, C.POINTER(_i32), C.POINTER(_i64)]
+_lib.commet_check_ranks.restype = C.c_int
 _lib.commet_set_kernel.argtypes = [_vp, _i32]
 _lib.commet_set_kernel.restype = C.c_int
 _lib.commet_info.argtypes = [_vp] + [C.POINTER(_i32)] * 4
@@ -139,12 +141,13 @@ _lib.commet_plan_halo.argtypes = [_vp, _P(_vp), _P(_vp), _P(_vp)]
 _lib.commet_plan_send.argtypes = [_vp, _i32, _P(_i32), _P(_i64), _P(_i64), _P(_i64), _P(_i64)]
 _lib.commet_plan_recv.argtypes = [_vp, _i32, _P(_i32), _P(_i64), _P(_vp), _P(_i64), _P(_vp)]
 _lib.commet_plan_colours.argtypes = [_vp, _P(_vp), _P(_vp)]
+_lib.commet_plan_colour_iface.argtypes = [_vp, _P(_vp)]
 _lib.commet_plan_destroy.argtypes = [_vp]
 _lib.commet_plan_destroy.restype = None
 for _f in ("commet_nccl_unique_id", "commet_nccl_comm_init", "commet_nccl_comm_destroy", "commet_halo_info",
            "commet_halo_send", "commet_halo_recv", "commet_halo_unpack", "commet_plan_create",
            "commet_plan_info", "commet_plan_csr", "commet_plan_halo", "commet_plan_send", "commet_plan_recv",
-           "commet_plan_colours"):
+           "commet_plan_colours", "commet_plan_colour_iface"):
     getattr(_lib, _f).restype = C.c_int
 _lib.commet_kernel_info.argtypes = [_vp, _P(_i32), _P(_i32), _P(_i32)]
 _lib.commet_kernel_info.restype = C.c_int
@@ -460,12 +463,22 @@ class Commet:
         return reports
 
     def check(self) -> int:
-        """-1 if every det F > 0, else the lowest flat e*n_q+q with det F <= 0."""
+        """-1 if every det F > 0 on this rank, else its lowest flat e*n_q+q with det F <= 0
+        (collective with an NCCL partition: see check_ranks)."""
         bad = _i64()
         s = _lib.commet_check(self.ctx, C.byref(bad))
         if s not in (COMMET_OK, COMMET_ERR_DOMAIN):
             _check(s, self.ctx)
         return bad.value
+
+    def check_ranks(self):
+        """(rank, qp) of the lowest rank with a det F <= 0 point and its lowest local flat index,
+        (-1, -1) if none; one MIN all-reduce over the NCCL communicator (every rank calls it)."""
+        rk, q = _i32(), _i64()
+        s = _lib.commet_check_ranks(self.ctx, C.byref(rk), C.byref(q))
+        if s not in (COMMET_OK, COMMET_ERR_DOMAIN):
+            _check(s, self.ctx)
+        return rk.value, q.value
 
     def close(self):
         if getattr(self, "ctx", None):
@@ -529,6 +542,12 @@ class Plan:
         cs, pm = _vp(), _vp()
         _check(_lib.commet_plan_colours(self.h, C.byref(cs), C.byref(pm)))
         return self._arr(cs, self.n_colours + 1, np.int64), self._arr(pm, n_el, np.int64)
+
+    def colour_iface(self):
+        """[n_colours]: the interface elements at the start of each colour (launched first)."""
+        ci = _vp()
+        _check(_lib.commet_plan_colour_iface(self.h, C.byref(ci)))
+        return self._arr(ci, self.n_colours, np.int64)
 
     def __del__(self):
         try:

@@ -238,6 +238,12 @@ extern "C" commet_status commet_setup(const commet_mesh_desc* mesh, const commet
                     (long long)nrr);
     }
   }
+  if (c->comm && p.n_ranks > 1) {
+    CUDA_TRY(C, cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking));
+    CUDA_TRY(C, cudaEventCreateWithFlags(&c->ev_iface, cudaEventDisableTiming));
+    CUDA_TRY(C, cudaEventCreateWithFlags(&c->ev_comm, cudaEventDisableTiming));
+    CUDA_TRY(C, c->check_buf.alloc(1));
+  }
   // element-order arrays live on the device now
   std::vector<int32_t>().swap(p.lrow);
   std::vector<uint8_t>().swap(p.slot);
@@ -336,34 +342,53 @@ extern "C" commet_status commet_assemble(commet_ctx c, const double* u, double* 
   a.ncm = c->ncm;
   const int slot = c->ev0.empty() ? -1 : (int)(c->n_assembled % (int64_t)c->ev0.size());
   if (slot >= 0) CUDA_TRY(c, cudaEventRecord(c->ev0[slot], st));
-  for (int k = 0; k < p.n_colours; k++) {
-    a.el_begin = p.colour_start[k];
-    a.el_count = p.colour_start[k + 1] - p.colour_start[k];
-    int rc = c->kernel == COMMET_KERNEL_SIMPLE ? launch_simple(a, st) : launch_fused(a, st, nullptr);
-    if (rc) return fail(c, COMMET_ERR_CUDA, "kernel launch (colour %d): %s", k, cudaGetErrorString((cudaError_t)rc));
+  // NCCL exchange with a partition: phase 0 launches every colour's interface elements (the only
+  // writers of halo rows), then the exchange starts on the comm stream while phase 1 launches the
+  // interiors; the unpack follows both.  Otherwise one phase of whole colours.
+  const bool exch = !c->peer && c->comm && p.n_ranks > 1 && (!p.send_rank.empty() || !p.recv_rank.empty());
+  for (int phase = 0; phase < (exch ? 2 : 1); phase++) {
+    for (int k = 0; k < p.n_colours; k++) {
+      const int64_t b0 = p.colour_start[k], b1 = p.colour_start[k + 1], bi = b0 + p.colour_iface[k];
+      a.el_begin = !exch ? b0 : (phase == 0 ? b0 : bi);
+      a.el_count = !exch ? b1 - b0 : (phase == 0 ? bi - b0 : b1 - bi);
+      if (a.el_count == 0) continue;
+      int rc = c->kernel == COMMET_KERNEL_SIMPLE ? launch_simple(a, st) : launch_fused(a, st, nullptr);
+      if (rc) return fail(c, COMMET_ERR_CUDA, "kernel launch (colour %d): %s", k, cudaGetErrorString((cudaError_t)rc));
+    }
+    if (exch && phase == 0) {
+      // ---- halo exchange over NCCL on the comm stream: one group of point-to-point transfers --
+      CUDA_TRY(c, cudaEventRecord(c->ev_iface, st));
+      CUDA_TRY(c, cudaStreamWaitEvent(c->comm_stream, c->ev_iface, 0));
+      cudaStream_t cs = c->comm_stream;
+      NCCL_TRY(c, ncclGroupStart());
+      for (size_t k = 0; k < p.send_rank.size(); k++) {
+        const int64_t v0 = p.send_val_off[k], v1 = p.send_val_off[k + 1];
+        const int64_t r0 = p.send_row_off[k], r1 = p.send_row_off[k + 1];
+        NCCL_TRY(c, ncclSend(c->v_halo.p + v0, v1 - v0, ncclDouble, p.send_rank[k], c->comm, cs));
+        NCCL_TRY(c, ncclSend(c->r_halo.p + r0, r1 - r0, ncclDouble, p.send_rank[k], c->comm, cs));
+      }
+      for (size_t k = 0; k < p.recv_rank.size(); k++) {
+        const int64_t v0 = p.recv_val_off[k], v1 = p.recv_val_off[k + 1];
+        const int64_t r0 = p.recv_row_off[k], r1 = p.recv_row_off[k + 1];
+        NCCL_TRY(c, ncclRecv(c->v_recv.p + v0, v1 - v0, ncclDouble, p.recv_rank[k], c->comm, cs));
+        NCCL_TRY(c, ncclRecv(c->r_recv.p + r0, r1 - r0, ncclDouble, p.recv_rank[k], c->comm, cs));
+      }
+      NCCL_TRY(c, ncclGroupEnd());
+      NCCL_ASYNC_CHECK(c, c->comm);
+      CUDA_TRY(c, cudaEventRecord(c->ev_comm, cs));
+    }
   }
   if (slot >= 0) CUDA_TRY(c, cudaEventRecord(c->ev1[slot], st));
   c->n_assembled++;
   if (c->peer) {  // halo rows went straight to their owners: only the closing barrier
-    if (c->comm) NCCL_TRY(c, ncclAllReduce(c->barrier_buf.p, c->barrier_buf.p, 1, ncclFloat, ncclSum, c->comm, st));
+    if (c->comm) {
+      NCCL_TRY(c, ncclAllReduce(c->barrier_buf.p, c->barrier_buf.p, 1, ncclFloat, ncclSum, c->comm, st));
+      NCCL_ASYNC_CHECK(c, c->comm);
+    }
     return COMMET_OK;
   }
-  // ---- halo exchange over NCCL: one group of point-to-point transfers, then unpack ----------
-  if (c->comm && p.n_ranks > 1 && (!p.send_rank.empty() || !p.recv_rank.empty())) {
-    NCCL_TRY(c, ncclGroupStart());
-    for (size_t k = 0; k < p.send_rank.size(); k++) {
-      const int64_t v0 = p.send_val_off[k], v1 = p.send_val_off[k + 1];
-      const int64_t r0 = p.send_row_off[k], r1 = p.send_row_off[k + 1];
-      NCCL_TRY(c, ncclSend(c->v_halo.p + v0, v1 - v0, ncclDouble, p.send_rank[k], c->comm, st));
-      NCCL_TRY(c, ncclSend(c->r_halo.p + r0, r1 - r0, ncclDouble, p.send_rank[k], c->comm, st));
-    }
-    for (size_t k = 0; k < p.recv_rank.size(); k++) {
-      const int64_t v0 = p.recv_val_off[k], v1 = p.recv_val_off[k + 1];
-      const int64_t r0 = p.recv_row_off[k], r1 = p.recv_row_off[k + 1];
-      NCCL_TRY(c, ncclRecv(c->v_recv.p + v0, v1 - v0, ncclDouble, p.recv_rank[k], c->comm, st));
-      NCCL_TRY(c, ncclRecv(c->r_recv.p + r0, r1 - r0, ncclDouble, p.recv_rank[k], c->comm, st));
-    }
-    NCCL_TRY(c, ncclGroupEnd());
+  if (exch) {  // unpack in sender order (deterministic) once the exchange and the interior are done
+    CUDA_TRY(c, cudaStreamWaitEvent(st, c->ev_comm, 0));
     for (size_t k = 0; k < p.recv_rank.size(); k++) {
       commet_status s = unpack(c, (int)k, c->v_recv.p + p.recv_val_off[k], c->r_recv.p + p.recv_row_off[k],
                                residual, csr_values, st);
@@ -373,16 +398,50 @@ extern "C" commet_status commet_assemble(commet_ctx c, const double* u, double* 
   return COMMET_OK;
 }
 
-extern "C" commet_status commet_check(commet_ctx c, int64_t* first_bad_qp) {
-  if (!c) return fail(nullptr, COMMET_ERR_ARG, "ctx is NULL");
+// cross-rank key of a rank's first bad qp: (rank, flat index) in one word, ordered by rank first
+static constexpr int kBadIdxBits = 44;
+
+// det F <= 0 status of the last assemble.  local: this rank's lowest bad flat index (-1: none);
+// with an NCCL partition, (rank, qp) = the lowest rank that has one and its index (collective)
+static commet_status check_impl(commet_ctx c, int64_t* local, int32_t* bad_rank, int64_t* first_bad_qp) {
   CUDA_TRY(c, cudaSetDevice(c->device));
   CUDA_TRY(c, cudaStreamSynchronize(c->last_stream));
   unsigned long long v = ~0ULL;
   CUDA_TRY(c, cudaMemcpy(&v, c->bad.p, sizeof v, cudaMemcpyDeviceToHost));
-  const int64_t r = v == ~0ULL ? -1 : (int64_t)v;
-  if (first_bad_qp) *first_bad_qp = r;
-  if (r >= 0) return fail(c, COMMET_ERR_DOMAIN, "det F <= 0 at flat quadrature point %lld", (long long)r);
+  *local = v == ~0ULL ? -1 : (int64_t)v;
+  int32_t rk = v == ~0ULL ? -1 : c->plan.rank;
+  int64_t q = *local;
+  if (c->comm && c->plan.n_ranks > 1) {  // collective: MIN over the ranks of (rank, first bad qp)
+    unsigned long long key = ~0ULL;
+    if (q >= 0) key = ((unsigned long long)c->plan.rank << kBadIdxBits) | ((unsigned long long)q & ((1ULL << kBadIdxBits) - 1));
+    cudaStream_t st = c->comm_stream;
+    CUDA_TRY(c, cudaMemcpyAsync(c->check_buf.p, &key, sizeof key, cudaMemcpyHostToDevice, st));
+    NCCL_TRY(c, ncclAllReduce(c->check_buf.p, c->check_buf.p, 1, ncclUint64, ncclMin, c->comm, st));
+    CUDA_TRY(c, cudaMemcpyAsync(&key, c->check_buf.p, sizeof key, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(c, cudaStreamSynchronize(st));
+    NCCL_ASYNC_CHECK(c, c->comm);
+    rk = key == ~0ULL ? -1 : (int32_t)(key >> kBadIdxBits);
+    q = key == ~0ULL ? -1 : (int64_t)(key & ((1ULL << kBadIdxBits) - 1));
+  }
+  if (bad_rank) *bad_rank = rk;
+  if (first_bad_qp) *first_bad_qp = q;
+  if (q >= 0)
+    return fail(c, COMMET_ERR_DOMAIN, "det F <= 0 at flat quadrature point %lld of rank %d", (long long)q, rk);
   return COMMET_OK;
+}
+
+extern "C" commet_status commet_check_ranks(commet_ctx c, int32_t* bad_rank, int64_t* first_bad_qp) {
+  if (!c) return fail(nullptr, COMMET_ERR_ARG, "ctx is NULL");
+  int64_t local = -1;
+  return check_impl(c, &local, bad_rank, first_bad_qp);
+}
+
+extern "C" commet_status commet_check(commet_ctx c, int64_t* first_bad_qp) {
+  if (!c) return fail(nullptr, COMMET_ERR_ARG, "ctx is NULL");
+  int64_t local = -1;
+  const commet_status s = check_impl(c, &local, nullptr, nullptr);
+  if (first_bad_qp) *first_bad_qp = local;
+  return s;
 }
 
 extern "C" commet_status commet_max_trace_C(commet_ctx c, double* max_trC) {
@@ -413,9 +472,13 @@ extern "C" commet_status commet_info(commet_ctx c, int32_t* n_colours, int32_t* 
   if (n_q) *n_q = p.n_q;
   if (n_en) *n_en = p.n_en;
   if (launches) {
+    const bool exch = !c->peer && c->comm && p.n_ranks > 1 && (!p.send_rank.empty() || !p.recv_rank.empty());
     int nonempty = 0;
-    for (int k = 0; k < p.n_colours; k++) nonempty += p.colour_start[k + 1] > p.colour_start[k];
-    const int unpacks = c->comm ? (int)p.recv_rank.size() : 0;
+    for (int k = 0; k < p.n_colours; k++) {
+      const int64_t n = p.colour_start[k + 1] - p.colour_start[k], ni = p.colour_iface[k];
+      nonempty += exch ? (ni > 0) + (n - ni > 0) : n > 0;
+    }
+    const int unpacks = exch ? (int)p.recv_rank.size() : 0;
     *launches = nonempty + unpacks;
   }
   return COMMET_OK;
@@ -690,6 +753,12 @@ extern "C" commet_status commet_plan_colours(commet_plan pl, const int64_t** col
   if (!pl) return fail(nullptr, COMMET_ERR_ARG, "plan is NULL");
   if (colour_start) *colour_start = pl->p.colour_start.data();
   if (perm) *perm = pl->p.perm.data();
+  return COMMET_OK;
+}
+
+extern "C" commet_status commet_plan_colour_iface(commet_plan pl, const int64_t** colour_iface) {
+  if (!pl) return fail(nullptr, COMMET_ERR_ARG, "plan is NULL");
+  if (colour_iface) *colour_iface = pl->p.colour_iface.data();
   return COMMET_OK;
 }
 

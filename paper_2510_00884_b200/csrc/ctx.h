@@ -46,6 +46,11 @@ struct commet_ctx_s {
   std::string err;
   cudaStream_t last_stream = nullptr;
   ncclComm_t comm = nullptr;
+  // NCCL mode with a partition: the halo exchange runs on its own stream, after the interface
+  // elements' launches (ev_iface) and beside the interior's; the unpack waits for ev_comm
+  cudaStream_t comm_stream = nullptr;
+  cudaEvent_t ev_iface = nullptr, ev_comm = nullptr;
+  DevBuf<unsigned long long> check_buf;  // cross-rank MIN of (rank, first bad qp)
   // device data
   DevBuf<int32_t> conn, lrow, col_idx;
   DevBuf<double> gradN, qp_w;
@@ -72,6 +77,9 @@ struct commet_ctx_s {
   int64_t n_assembled = 0;
   ~commet_ctx_s() {
     solver_work_free(solver);
+    if (ev_iface) cudaEventDestroy(ev_iface);
+    if (ev_comm) cudaEventDestroy(ev_comm);
+    if (comm_stream) cudaStreamDestroy(comm_stream);
     for (auto e : ev0) cudaEventDestroy(e);
     for (auto e : ev1) cudaEventDestroy(e);
   }
@@ -106,6 +114,18 @@ inline commet_status fail(commet_ctx c, commet_status s, const char* fmt, ...) {
     if (r_ != ncclSuccess)                                                                         \
       return fail(ctx, COMMET_ERR_NCCL, "NCCL error %s at %s:%d (%s)", ncclGetErrorString(r_), __FILE__, \
                   __LINE__, #x);                                                                   \
+  } while (0)
+
+// NCCL reports errors of operations already enqueued (a peer died, a network error) only
+// through the communicator's asynchronous error state
+#define NCCL_ASYNC_CHECK(ctx, comm)                                                                \
+  do {                                                                                             \
+    ncclResult_t a_ = ncclSuccess;                                                                 \
+    ncclResult_t q_ = ncclCommGetAsyncError((comm), &a_);                                           \
+    if (q_ != ncclSuccess) a_ = q_;                                                                \
+    if (a_ != ncclSuccess && a_ != ncclInProgress)                                                 \
+      return fail(ctx, COMMET_ERR_NCCL, "NCCL asynchronous error %s at %s:%d", ncclGetErrorString(a_), \
+                  __FILE__, __LINE__);                                                             \
   } while (0)
 
 template <class T>

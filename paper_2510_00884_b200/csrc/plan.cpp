@@ -210,9 +210,21 @@ commet_status plan_build(const commet_mesh_desc* mesh, Plan& p, std::string& err
   for (int64_t e = 0; e < n_el; e++) p.colour_start[colour[e] + 1]++;
   for (int k = 0; k < p.n_colours; k++) p.colour_start[k + 1] += p.colour_start[k];
   p.perm.resize(n_el);
+  p.colour_iface.assign(p.n_colours, 0);
   {
+    // within a colour: interface elements (a node in the halo) first, then the interior, each in
+    // input order -- the colour's update set, hence the summation order, is unchanged
+    std::vector<char> iface(n_el, 0);
+    if (p.n_halo)
+      for (int64_t e = 0; e < n_el; e++)
+        for (int a = 0; a < n_en; a++) iface[e] |= p.lrow[e * n_en + a] >= p.n_owned;
     std::vector<int64_t> pos(p.colour_start.begin(), p.colour_start.end() - 1);
-    for (int64_t e = 0; e < n_el; e++) p.perm[pos[colour[e]]++] = e;
+    for (int pass = 1; pass >= 0; pass--)
+      for (int64_t e = 0; e < n_el; e++)
+        if (iface[e] == pass) {
+          p.perm[pos[colour[e]]++] = e;
+          if (pass) p.colour_iface[colour[e]]++;
+        }
   }
   p.slot.resize((size_t)n_el * n_en * n_en);
 #pragma omp parallel for schedule(static)

@@ -33,6 +33,9 @@ struct Plan {
   // colouring
   int n_colours = 0;
   std::vector<int64_t> colour_start;  // [n_colours+1] into perm
+  // multi-rank: interface elements (touching a halo row) first within each colour, so the
+  // assembly can launch them first and overlap the halo exchange with the interior
+  std::vector<int64_t> colour_iface;  // [n_colours] interface elements at the start of colour k
   std::vector<int64_t> perm;          // sorted position -> original element
   std::vector<uint8_t> slot;          // [n_el][n_en][n_en] in SORTED order
   // interface: this rank sends halo rows to their owners, receives from ranks whose
