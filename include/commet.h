@@ -379,7 +379,12 @@ commet_status commet_newton_step(commet_ctx ctx, const double* bc_values, const 
 /* Diagnostic: evaluates the kernels' activation on n device values y:
  * z = softplus(y) = log(1+e^y), s = sigmoid(y) (device fp64 arrays).
  * Asynchronous on cuda_stream.  Used by the tests to pin the table-driven
- * softplus/sigmoid of the fused kernel on its own. */
+ * softplus/sigmoid of the fused kernel on its own.  commet_selftest_activation
+ * uses the 64-entry tables (3-pass kernels); the _tab form takes table_bits 6
+ * or 8 (the 256-entry tables of the forward-sweep kernels).  s is NaN where the
+ * sigmoid-only form (last hidden layer) differs from the softplus+sigmoid one. */
+commet_status commet_selftest_activation_tab(const double* y, double* z, double* s, int64_t n,
+                                             int32_t table_bits, void* cuda_stream);
 commet_status commet_selftest_activation(const double* y, double* z, double* s, int64_t n,
                                          void* cuda_stream);
 

@@ -37,7 +37,8 @@ SYMBOLS = ("commet_setup", "commet_csr_pattern", "commet_csr_pattern_copy", "com
            "commet_kernel_info", "commet_max_trace_C", "commet_set_dirichlet", "commet_apply_dirichlet",
            "commet_cg_jacobi", "commet_newton_step", "commet_ncm_eval", "commet_normalize_reference",
            "commet_material_eval", "commet_halo_recv_maps", "commet_set_peer", "commet_set_peer_mode",
-           "commet_zero_outputs", "commet_set_preconditioner", "commet_check_ranks", "commet_plan_colour_iface")
+           "commet_zero_outputs", "commet_set_preconditioner", "commet_check_ranks", "commet_plan_colour_iface",
+           "commet_selftest_activation_tab")
 NEWTON_MAX_LOG = 64
 
 
@@ -126,6 +127,8 @@ _lib.commet_kernel_times.argtypes = [_vp, _vp, _i32]
 _lib.commet_kernel_times.restype = C.c_int
 _lib.commet_selftest_activation.argtypes = [_vp, _vp, _vp, _i64, _vp]
 _lib.commet_selftest_activation.restype = C.c_int
+_lib.commet_selftest_activation_tab.argtypes = [_vp, _vp, _vp, _i64, _i32, _vp]
+_lib.commet_selftest_activation_tab.restype = C.c_int
 _P = C.POINTER
 _lib.commet_nccl_unique_id.argtypes = [_vp]
 _lib.commet_nccl_comm_init.argtypes = [_vp, _i32, _i32, C.c_int, _P(_vp)]
@@ -281,15 +284,24 @@ class Commet:
         return (t.empty(self.n_rows, dtype=t.float64, device=self.device),
                 t.empty(self.nnz, dtype=t.float64, device=self.device))
 
+    def _dev_f64(self, x, n, name):
+        """The library reads / writes n doubles at x on this ctx's device: refuse anything else."""
+        t = self.torch
+        if not (isinstance(x, t.Tensor) and x.is_cuda and x.dtype == t.float64 and x.is_contiguous()):
+            raise TypeError(f"{name} must be a contiguous cuda float64 tensor")
+        if x.device != self.device:
+            raise ValueError(f"{name} is on {x.device}, the ctx on {self.device}")
+        if x.numel() != n:
+            raise ValueError(f"{name} has {x.numel()} entries, expected {n}")
+
     def assemble(self, u, residual=None, values=None, stream=None):
         """u: cuda fp64 tensor [3 n_nodes]. Returns (residual, values) (asynchronous)."""
         t = self.torch
-        if not (isinstance(u, t.Tensor) and u.is_cuda and u.dtype == t.float64 and u.is_contiguous()):
-            raise TypeError("u must be a contiguous cuda float64 tensor")
-        if u.numel() != 3 * self.n_nodes:
-            raise ValueError(f"u has {u.numel()} entries, expected {3 * self.n_nodes}")
+        self._dev_f64(u, 3 * self.n_nodes, "u")
         if residual is None or values is None:
             residual, values = self.alloc_outputs()
+        self._dev_f64(residual, self.n_rows, "residual")
+        self._dev_f64(values, self.nnz, "values")
         st = stream if stream is not None else t.cuda.current_stream(self.device)
         _check(_lib.commet_assemble(self.ctx, u.data_ptr(), residual.data_ptr(), values.data_ptr(),
                                     st.cuda_stream), self.ctx)
@@ -396,6 +408,9 @@ class Commet:
 
     def apply_dirichlet(self, residual, values, stream=None):
         t = self.torch
+        self._dev_f64(values, self.nnz, "values")
+        if residual is not None:
+            self._dev_f64(residual, self.n_rows, "residual")
         st = stream if stream is not None else t.cuda.current_stream(self.device)
         _check(_lib.commet_apply_dirichlet(self.ctx, None if residual is None else residual.data_ptr(),
                                            values.data_ptr(), st.cuda_stream), self.ctx)
@@ -412,6 +427,9 @@ class Commet:
         t = self.torch
         if x is None:
             x = t.empty_like(b)
+        self._dev_f64(values, self.nnz, "values")
+        self._dev_f64(b, self.n_rows, "b")
+        self._dev_f64(x, self.n_rows, "x")
         st = stream if stream is not None else t.cuda.current_stream(self.device)
         it, rel = _i32(), C.c_double()
         _check(_lib.commet_cg_jacobi(self.ctx, values.data_ptr(), b.data_ptr(), x.data_ptr(), rtol, max_iter,
@@ -423,7 +441,10 @@ class Commet:
         """One load step: u[dirichlet] = bc_values, Newton iterations until converged.
         u: cuda fp64 tensor [3 n_nodes] (in/out).  -> report dict."""
         t = self.torch
-        bv = np.ascontiguousarray(bc_values, dtype=np.float64)
+        bv = np.ascontiguousarray(bc_values, dtype=np.float64).reshape(-1)
+        if bv.size != getattr(self, "n_dirichlet", 0):
+            raise ValueError(f"bc_values has {bv.size} entries, set_dirichlet gave {getattr(self, 'n_dirichlet', 0)} dofs")
+        self._dev_f64(u, 3 * self.n_nodes, "u")
         cfg = NewtonCfg(atol, rtol, max_iter, cg_rtol, cg_max_iter)
         rep = NewtonReport()
         st = stream if stream is not None else t.cuda.current_stream(self.device)
@@ -607,13 +628,14 @@ def nccl_comm_destroy(comm):
         _check(_lib.commet_nccl_comm_destroy(comm))
 
 
-def activation(y):
-    """The fused kernel's softplus and sigmoid on a cuda fp64 tensor (diagnostic)."""
+def activation(y, table_bits: int = 6):
+    """The fused kernel's softplus and sigmoid on a cuda fp64 tensor (diagnostic); table_bits 6
+    (64-entry tables, 3-pass kernels) or 8 (256 entries, forward-sweep kernels)."""
     import torch
     y = y.contiguous()
     z, s = torch.empty_like(y), torch.empty_like(y)
-    _check(_lib.commet_selftest_activation(y.data_ptr(), z.data_ptr(), s.data_ptr(), y.numel(),
-                                           torch.cuda.current_stream(y.device).cuda_stream))
+    _check(_lib.commet_selftest_activation_tab(y.data_ptr(), z.data_ptr(), s.data_ptr(), y.numel(), table_bits,
+                                               torch.cuda.current_stream(y.device).cuda_stream))
     return z, s
 
 

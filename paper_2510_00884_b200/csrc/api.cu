@@ -11,6 +11,7 @@
 #include <cstdio>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <new>
 #include <string>
 #include <vector>
@@ -764,20 +765,30 @@ extern "C" commet_status commet_plan_colour_iface(commet_plan pl, const int64_t*
 
 extern "C" void commet_plan_destroy(commet_plan pl) { delete pl; }
 
-extern "C" commet_status commet_selftest_activation(const double* y, double* z, double* s, int64_t n,
-                                                    void* cuda_stream) {
+extern "C" commet_status commet_selftest_activation_tab(const double* y, double* z, double* s, int64_t n,
+                                                        int32_t table_bits, void* cuda_stream) {
   if (n < 0 || (n && (!y || !z || !s)))
     return fail(nullptr, COMMET_ERR_ARG, "bad arguments (n = %lld)", (long long)n);
+  if (table_bits != 6 && table_bits != 8) return fail(nullptr, COMMET_ERR_ARG, "table_bits %d not 6 or 8", table_bits);
+  static std::mutex mu;
   static double* d_tab = nullptr;
-  if (!d_tab) {
-    double tab[kActTabSize];
-    fill_act_table(tab);
-    CUDA_TRY(nullptr, cudaMalloc(&d_tab, sizeof tab));
-    CUDA_TRY(nullptr, cudaMemcpy(d_tab, tab, sizeof tab, cudaMemcpyHostToDevice));
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    if (!d_tab) {
+      std::vector<double> tab(kActTabSize);
+      fill_act_table(tab.data());
+      CUDA_TRY(nullptr, cudaMalloc(&d_tab, tab.size() * sizeof(double)));
+      CUDA_TRY(nullptr, cudaMemcpy(d_tab, tab.data(), tab.size() * sizeof(double), cudaMemcpyHostToDevice));
+    }
   }
-  int rc = launch_activation(y, z, s, n, d_tab, cuda_stream);
+  int rc = launch_activation(y, z, s, n, d_tab, table_bits, cuda_stream);
   if (rc) return fail(nullptr, COMMET_ERR_CUDA, "activation kernel: %s", cudaGetErrorString((cudaError_t)rc));
   return COMMET_OK;
+}
+
+extern "C" commet_status commet_selftest_activation(const double* y, double* z, double* s, int64_t n,
+                                                    void* cuda_stream) {
+  return commet_selftest_activation_tab(y, z, s, n, 6, cuda_stream);
 }
 
 extern "C" const char* commet_last_error(commet_ctx c) {

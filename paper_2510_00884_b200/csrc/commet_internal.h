@@ -85,7 +85,8 @@ struct AsmArgs {
 int launch_simple(const AsmArgs& a, void* stream);
 int launch_unpack(const double* vals, const int64_t* vmap, int64_t nv, double* csr, const double* res,
                   const int64_t* rmap, int64_t nr, double* r, void* stream);
-int launch_activation(const double* y, double* z, double* s, int64_t n, const double* tab, void* stream);
+int launch_activation(const double* y, double* z, double* s, int64_t n, const double* tab, int table_bits,
+                      void* stream);
 int launch_fused(const AsmArgs& a, void* stream, int* launches);
 int launch_material(const AsmArgs& a, void* stream);
 int fused_supported(int n_en, int n_q, int w, int L);

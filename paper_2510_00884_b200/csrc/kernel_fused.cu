@@ -25,6 +25,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <mutex>
 
 #include "commet_internal.h"
 #include "qp_math.cuh"
@@ -59,6 +60,15 @@
 #endif
 #ifndef COMMET_FWD
 #define COMMET_FWD 1  // forward value+Jacobian sweep, Hessian terms in the backward pass (L <= 3, no skips)
+#endif
+#ifndef COMMET_FWD_MINW
+#define COMMET_FWD_MINW 64  // narrowest width that takes the forward sweep (w = 64: measured -4.8 % c3 time, round 2)
+#endif
+#ifndef COMMET_ACT_TB
+#define COMMET_ACT_TB 8  // forward-sweep activations on 256-entry tables (lower polynomial degrees)
+#endif
+#ifndef COMMET_POST_PAR
+#define COMMET_POST_PAR 0  // stage 7a split over the four warps (post_qp_part): measured no gain (c3 +0.3 %, c4 +3 %: spills)
 #endif
 #ifndef COMMET_PINGPONG
 #define COMMET_PINGPONG 0  // measured neutral (c3 10.31 vs 10.26 ms): barriers kept
@@ -155,10 +165,11 @@ struct Cfg {
   static constexpr int PD_V = COMMET_PD_V, PD_J = COMMET_PD_J;
   // one forward sweep for the value and the Jacobian (3-input ICNN, L = 2 or 3): act
   // holds z | s (.) J (4 column groups per qp) and keeps s_2 (.) J_2 for the backward pass.
-  // Measured (tools/ab_bench.py): w = 128 (c4) 41.10 -> 39.94 ms; w = 64 (c3) 10.29 -> 10.64 ms
-  // (the 16-tile forward GEMM spills at 168 registers and the inner layer's Hessian term needs
-  // a division per neuron), so w >= 128 only.
-  static constexpr bool FWDC = COMMET_FWD && W >= 128 && NET == 0 && NK == 3 && !COMMET_PINGPONG;
+  // Measured (tools/ab_bench.py): round 1, w = 128 (c4) 41.10 -> 39.94 ms, w = 64 (c3) 10.29 ->
+  // 10.64 ms; round 2 with the layer count a template parameter (unrolled, short live ranges)
+  // and 1/s by rcp + Newton instead of an IEEE division: c3 10.34 -> 9.84 ms, c4 39.86 -> 37.85.
+  static constexpr bool FWDC = COMMET_FWD && W >= COMMET_FWD_MINW && NET == 0 && NK == 3 && !COMMET_PINGPONG;
+  static constexpr int TB_FWD = COMMET_ACT_TB;     // activation table bits on the forward-sweep path
   static constexpr int LDA = (FWDC ? 4 : NK) * Q + 4;  // act row stride (= 4 mod 16: conflict-free B frags)
   static constexpr int LDS = Q + 2;                // s/c row stride (2-way conflicts at most)
   static_assert(W % 8 == 0 && Q % 8 == 0 && Q % NQ == 0, "tile");
@@ -200,7 +211,7 @@ struct Smem {
     ue = o;  o += C::E * C::NEN * 3;
     wq = o;  o += C::Q;
     qN = o;  o += C::NPR * C::Q;
-    tab = o; o += kActTabSize;
+    tab = o; o += fwd ? ActTab<C::TB_FWD>::SIZE : ActTab<6>::SIZE;
     o = (o + 1) & ~1;
     const int xs = C::DMMA_ELEM ? 0 : C::Q * C::NEN * 27;  // X only for the scalar element path
     const int px = C::Q * PS > xs ? C::Q * PS : xs;
@@ -376,8 +387,17 @@ __device__ __forceinline__ void material_outputs(const AsmArgs& A, const NcmDev&
 // The backward pass then gives g and H_1 as before (stage 4's l = 2 epilogue, stage 5).
 // act: columns [0, Q) z_l / mu_l, [Q, 4Q) s_l (.) J_l; on entry z_1 | D_1 (stage 2).
 // ---------------------------------------------------------------------------
-template <class C>
-__device__ __forceinline__ void fwd_sweep(const NcmDev& m, int L, double* act, double* sb, double* hred, double* qg,
+// 1/x for x in [2^-500, 1]: MUFU seed (rcp.approx.ftz.f64, ~2^-23) + two Newton steps -- full
+// precision, no IEEE-division slow path
+__device__ __forceinline__ double rcp_nr(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  r = r * fma(-x, r, 2.0);
+  return r * fma(-x, r, 2.0);
+}
+
+template <class C, int L>
+__device__ __forceinline__ void fwd_sweep(const NcmDev& m, double* act, double* sb, double* hred, double* qg,
                                           double* qH, const double* gsk, const double* stab, double* qNp) {
   constexpr int W = C::W, Q = C::Q, LDA = C::LDA, LDS = C::LDS, KT2 = C::KT2;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
@@ -394,6 +414,7 @@ __device__ __forceinline__ void fwd_sweep(const NcmDev& m, int L, double* act, d
     for (int h = 0; h < 2; h++)
 #pragma unroll
       for (int x = 0; x < 6; x++) hp[h][x] = 0.0;
+#pragma unroll
     for (int l = 2; l <= L; l++) {
       double acc[C::MT_J][4][2];
       warp_gemm<C::MT_J, 4, KT2, C::PD_J>(m.Wfrag + (l - 2) * frag_layer, mt0, act, LDA, ncol, acc);
@@ -410,7 +431,7 @@ __device__ __forceinline__ void fwd_sweep(const NcmDev& m, int L, double* act, d
           const double J0 = acc[i][1][h], J1 = acc[i][2][h], J2 = acc[i][3][h];
           if (l < L) {
             double z, s;
-            softplus_sig(y, stab, z, s);
+            softplus_sig_t<C::TB_FWD>(y, stab, z, s);
             sb[((l - 1) * W + j) * LDS + q] = s;
             act[j * LDA + q] = z;
             act[j * LDA + Q + q] = s * J0;
@@ -420,10 +441,10 @@ __device__ __forceinline__ void fwd_sweep(const NcmDev& m, int L, double* act, d
             double s;
             if constexpr (C::MODE == 1) {  // material points need the value: z_L too
               double z;
-              softplus_sig(y, stab, z, s);
+              softplus_sig_t<C::TB_FWD>(y, stab, z, s);
               nacc[h] += aj * z;
             } else {
-              s = sigmoid_tab(y, stab);
+              s = sigmoid_t<C::TB_FWD>(y, stab);
             }
             const double c = aj * s * (1.0 - s);
             const double c0 = c * J0, c1 = c * J1, c2 = c * J2;
@@ -469,6 +490,7 @@ __device__ __forceinline__ void fwd_sweep(const NcmDev& m, int L, double* act, d
     int ncol[C::NT_V];
 #pragma unroll
     for (int j = 0; j < C::NT_V; j++) ncol[j] = (vn * C::NT_V + j) * 8;
+#pragma unroll
     for (int l = L; l >= 2; l--) {
       double acc[C::MT_V][C::NT_V][2];
       warp_gemm<C::MT_V, C::NT_V, KT2, C::PD_V>(m.Wfrag + (l - 2) * frag_layer + (size_t)W * W, mt0, act, LDA, ncol,
@@ -492,7 +514,9 @@ __device__ __forceinline__ void fwd_sweep(const NcmDev& m, int L, double* act, d
               const int q = ncol[jj] + 2 * t + h;
               const double lam = acc[i][jj][h];
               const double s = sb[((l - 2) * W + j) * LDS + q];
-              const double k2 = lam * (1.0 - s) / s;
+              // c_2 J_2 J_2^T = lam (1 - s)/s P P^T.  1/s of s clamped at 2^-500: finite for any lam
+              // the weights can produce (a neuron with s < 2^-500 contributes < 1e-150 either way)
+              const double k2 = lam * (1.0 - s) * rcp_nr(fmax(s, 0x1p-500));
               const double P0 = act[j * LDA + Q + q], P1 = act[j * LDA + 2 * Q + q], P2 = act[j * LDA + 3 * Q + q];
               const double c0 = k2 * P0, c1 = k2 * P1, c2 = k2 * P2;
               double* hh = hb[jj][h];
@@ -591,6 +615,54 @@ __device__ __forceinline__ void fwd_sweep(const NcmDev& m, int L, double* act, d
   __syncthreads();
 }
 
+// ---- stage 2: layer 1 (3 -> W), elementwise.  Each thread: one qp, neurons j0, j0 + NTHR/Q, ...
+// -- all loads issued up front and the NIT activations interleaved (independent chains).
+// TB: activation table bits (8 on the forward-sweep path, 6 otherwise)
+template <class C, int TB>
+__device__ __forceinline__ void layer1(const NcmDev& m, int L, bool fwd, const double* qk, double* act, double* sb,
+                                   double* cb, double* qNp, const double* stab) {
+  constexpr int W = C::W, Q = C::Q, LDA = C::LDA, LDS = C::LDS;
+  const int tid = threadIdx.x;
+  constexpr int NIT = W * Q / C::NTHR, JS = C::NTHR / Q;
+  static_assert(W * Q % C::NTHR == 0 && C::NTHR % Q == 0, "layer-1 split");
+  const int q = tid % Q, j0 = tid / Q;
+  double kq[C::NK];
+#pragma unroll
+  for (int x = 0; x < C::NK; x++) kq[x] = qk[q * C::NK + x];
+  double yv[NIT];
+#pragma unroll
+  for (int i = 0; i < NIT; i++) {
+    const int j = j0 + i * JS;
+    double y = __ldg(m.b + j);
+#pragma unroll
+    for (int x = 0; x < C::NK; x++) y += __ldg(m.W1 + j * C::NK + x) * kq[x];
+    yv[i] = y;
+  }
+  double nv = 0.0;  // material mode, L == 1: partial a . z_1 of this thread's neurons
+#pragma unroll
+  for (int i = 0; i < NIT; i++) {
+    const int j = j0 + i * JS;
+    double z, s;
+    softplus_sig_t<TB>(yv[i], stab, z, s);
+    if (L > 1) {
+      sb[j * LDS + q] = s;
+      act[j * LDA + q] = z;
+      if constexpr (C::FWDC)
+        if (fwd) {  // D_1 = s_1 (.) W1: the Jacobian columns of the forward sweep
+#pragma unroll
+          for (int c = 0; c < 3; c++) act[j * LDA + (c + 1) * Q + q] = s * __ldg(m.W1 + j * 3 + c);
+        }
+    } else {
+      const double aj = __ldg(m.a + j);
+      act[j * LDA + q] = aj * s;
+      cb[j * LDS + q] = aj * s * (1.0 - s);
+      nv += aj * z;
+    }
+  }
+  if constexpr (C::MODE == 1)
+    if (L == 1) qNp[j0 * Q + q] = nv;
+}
+
 template <class C>
 __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
   constexpr int W = C::W, Q = C::Q, NEN = C::NEN, NQ = C::NQ, E = C::E;
@@ -624,7 +696,10 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
   const bool fwd = Smem<C>::fwd_path(L, skips);
   const int64_t n_batches = (A.el_count + E - 1) / E;
   const size_t frag_layer = (size_t)2 * W * W;  // W and W^T fragments per hidden layer
-  for (int x = threadIdx.x; x < kActTabSize; x += C::NTHR) stab[x] = __ldg(A.ncm.act_tab + x);
+  {  // the activation table of this path (256 entries on the forward sweep, 64 otherwise)
+    const int tb0 = fwd ? act_tab_offset<C::TB_FWD>() : 0, tbn = fwd ? ActTab<C::TB_FWD>::SIZE : ActTab<6>::SIZE;
+    for (int x = threadIdx.x; x < tbn; x += C::NTHR) stab[x] = __ldg(A.ncm.act_tab + tb0 + x);
+  }
   // (made visible by the first __syncthreads of the batch loop)
 #ifdef COMMET_STAGE_PROF
   __shared__ long long st_acc[16];  // thread 0 only; [15] = previous mark
@@ -642,6 +717,7 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
   double2 pf_g[PG];
   double pf_u[PU], pf_w = 0.0;
   int pf_c[PU];
+
   auto pf_load_a = [&](int64_t b) {
     const int64_t f0 = A.el_begin + b * E;
     const int64_t frem = A.el_begin + A.el_count - f0;
@@ -784,53 +860,16 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
     if constexpr (C::NET == 0) {
     // ---- stage 2: layer 1 (3 -> W), elementwise -------------------------------------
     if (L > 1) frag_prefetch<C::MT_V, KT2, COMMET_FRAG_PF + (COMMET_FRAG_PF == 0)>(m.Wfrag, (warp / C::VNG) * C::MT_V);
-    // each thread: one qp, neurons j0, j0 + NTHR/Q, ... -- all loads issued up front and the
-    // NIT activations interleaved (independent chains)
-    {
-      constexpr int NIT = W * Q / C::NTHR, JS = C::NTHR / Q;
-      static_assert(W * Q % C::NTHR == 0 && C::NTHR % Q == 0, "layer-1 split");
-      const int q = tid % Q, j0 = tid / Q;
-      double kq[C::NK];
-#pragma unroll
-      for (int x = 0; x < C::NK; x++) kq[x] = qk[q * C::NK + x];
-      double yv[NIT];
-#pragma unroll
-      for (int i = 0; i < NIT; i++) {
-        const int j = j0 + i * JS;
-        double y = __ldg(m.b + j);
-#pragma unroll
-        for (int x = 0; x < C::NK; x++) y += __ldg(m.W1 + j * C::NK + x) * kq[x];
-        yv[i] = y;
-      }
-      double nv = 0.0;  // material mode, L == 1: partial a . z_1 of this thread's neurons
-#pragma unroll
-      for (int i = 0; i < NIT; i++) {
-        const int j = j0 + i * JS;
-        double z, s;
-        softplus_sig(yv[i], stab, z, s);
-        if (L > 1) {
-          sb[j * LDS + q] = s;
-          act[j * LDA + q] = z;
-          if constexpr (C::FWDC)
-            if (fwd) {  // D_1 = s_1 (.) W1: the Jacobian columns of the forward sweep
-#pragma unroll
-              for (int c = 0; c < 3; c++) act[j * LDA + (c + 1) * Q + q] = s * __ldg(m.W1 + j * 3 + c);
-            }
-        } else {
-          const double aj = __ldg(m.a + j);
-          act[j * LDA + q] = aj * s;
-          cb[j * LDS + q] = aj * s * (1.0 - s);
-          nv += aj * z;
-        }
-      }
-      if constexpr (C::MODE == 1)
-        if (L == 1) qNp[j0 * Q + q] = nv;
-    }
+    if (C::FWDC && fwd) layer1<C, C::TB_FWD>(m, L, true, qk, act, sb, cb, qNp, stab);
+    else layer1<C, 6>(m, L, false, qk, act, sb, cb, qNp, stab);
     __syncthreads();
     STAGE_MARK(2)
 
     if constexpr (C::FWDC) {
-      if (fwd) fwd_sweep<C>(m, L, act, sb, hred, qg, qH, gsk, stab, qNp);
+      if (fwd) {
+        if (L == 3) fwd_sweep<C, 3>(m, act, sb, hred, qg, qH, gsk, stab, qNp);
+        else fwd_sweep<C, 2>(m, act, sb, hred, qg, qH, gsk, stab, qNp);
+      }
     }
     if (!fwd) {
     // ---- stage 3: value pass, layers 2..L --------------------------------------------
@@ -1213,8 +1252,11 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
 #if COMMET_PREFETCH
     if (batch + gridDim.x < n_batches) pf_load_a(batch + gridDim.x);
 #endif
-    if (tid < Q) {
-      const int q = tid;
+    // ICNN, 3 inputs: four warps cooperate (warp = part of post_qp, lane = qp); otherwise one
+    // thread per qp
+    constexpr bool PAR7 = COMMET_POST_PAR && C::NET == 0 && C::KIN != 2 && C::NWARP == 4;
+    if (PAR7 ? lane < Q : tid < Q) {
+      const int q = PAR7 ? lane : tid;
       double gq[C::NK], H6[C::NH];
       if constexpr (C::NET == 0) {
 #pragma unroll
@@ -1241,6 +1283,8 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
       H6[packed_index(C::NK, 2, 2)] += 2.0 * m.kappa;
       if constexpr (C::KIN == 2)
         post_qp_aniso(kin, m.a0, gq, H6, swq[q], post + q * PS, qP + q * 9);
+      else if constexpr (PAR7)
+        post_qp_part(kin, gq, H6, swq[q], post + q * PS, qP + q * 9, warp);
       else
         post_qp(kin, gq, H6, swq[q], post + q * PS, qP + q * 9);
     }
@@ -1452,44 +1496,64 @@ static int launch_cfg(const AsmArgs& a, cudaStream_t st, int* launches) {
 #endif
   // per device: the shared-memory attribute, SM count and occupancy are queried once per
   // (device, smem size) -- the host-side launch cost matters for small batches
+  // (several contexts on one device may launch from different host threads: the cache is
+  // read and updated under a lock, and a launch uses one consistent snapshot of it)
   constexpr int kDev = 16;
+  static std::mutex mu;
   static size_t attr_bytes[kDev] = {0};
   static int sms_c[kDev] = {0}, per_sm_c[kDev] = {0};
   static size_t occ_bytes[kDev] = {0};
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 0 || dev >= kDev) return (int)cudaErrorInvalidDevice;
-  if (attr_bytes[dev] < bytes) {
-    cudaError_t e = cudaFuncSetAttribute(fused_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-    if (e != cudaSuccess) return (int)e;
-    attr_bytes[dev] = bytes;
-  }
-  if (occ_bytes[dev] != bytes) {
-    int sms = 148, per_sm = 1;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fused_kernel<C>, C::NTHR, bytes);
-    sms_c[dev] = sms;
-    per_sm_c[dev] = per_sm < 1 ? 1 : per_sm;
-    occ_bytes[dev] = bytes;
+  int sms = 0, per_sm = 0;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    if (attr_bytes[dev] < bytes) {
+      cudaError_t e = cudaFuncSetAttribute(fused_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+      if (e != cudaSuccess) return (int)e;
+      attr_bytes[dev] = bytes;
+    }
+    if (occ_bytes[dev] != bytes) {
+      int s = 0, ps = 0;
+      cudaError_t e = cudaDeviceGetAttribute(&s, cudaDevAttrMultiProcessorCount, dev);
+      if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, fused_kernel<C>, C::NTHR, bytes);
+      if (e != cudaSuccess) return (int)e;
+      sms_c[dev] = s;
+      per_sm_c[dev] = ps < 1 ? 1 : ps;
+      occ_bytes[dev] = bytes;
+    }
+    sms = sms_c[dev];
+    per_sm = per_sm_c[dev];
   }
   if (a.query) {
     cudaFuncAttributes fa{};
     cudaFuncGetAttributes(&fa, fused_kernel<C>);
     a.query[0] = (int)bytes;
-    a.query[1] = per_sm_c[dev];
+    a.query[1] = per_sm;
     a.query[2] = fa.numRegs;
     return 0;
   }
   const int64_t nb = (a.el_count + C::E - 1) / C::E;
-  const int64_t grid = std::min<int64_t>(nb, (int64_t)sms_c[dev] * per_sm_c[dev]);
-  if (grid <= 0) return 0;
+  const int64_t grid = std::min<int64_t>(nb, (int64_t)sms * per_sm);
+  if (nb <= 0) return 0;
+  if (grid <= 0) return (int)cudaErrorInvalidConfiguration;  // never a silent no-op with work to do
   fused_kernel<C><<<(unsigned)grid, C::NTHR, bytes, st>>>(a);
   if (launches) (*launches)++;
   return (int)cudaGetLastError();
 }
 
+// COMMET_AB_MIN: tuning builds of the benchmark instantiations only (ICNN, standard inputs,
+// w = 64 / 128) -- a fraction of the compile time; never the product library
 template <int NEN, int NQ, int K>
 static int launch_k(const AsmArgs& a, cudaStream_t st, int* launches) {
+#ifdef COMMET_AB_MIN
+  if constexpr (K == 0) {
+    if (a.ncm.net == 0 && a.ncm.w == 64) return launch_cfg<Cfg<64, 16, NEN, NQ, 3, 0, 0>>(a, st, launches);
+    if (a.ncm.net == 0 && a.ncm.w == 128) return launch_cfg<Cfg<128, 8, NEN, NQ, 3, 0, 0>>(a, st, launches);
+  }
+  return (int)cudaErrorInvalidValue;
+#else
   if constexpr (K == 2) {  // 5 inputs: packed 5x5 Hessians and the extended F-space factors
     if (a.ncm.net != 0) return launch_cfg<Cfg<16, 32, NEN, NQ, 2, 1, K>>(a, st, launches);
   } else {
@@ -1507,11 +1571,15 @@ static int launch_k(const AsmArgs& a, cudaStream_t st, int* launches) {
     case 128: return launch_cfg<Cfg<128, 8, NEN, NQ, MB, 0, K>>(a, st, launches);
   }
   return (int)cudaErrorInvalidValue;
+#endif
 }
 
 // material points: NEN = NQ = 1, one "element" per point
 template <int K>
 static int launch_mat_k(const AsmArgs& a, cudaStream_t st) {
+#ifdef COMMET_AB_MIN
+  return (int)cudaErrorInvalidValue;
+#else
   if (a.ncm.net != 0) return launch_cfg<Cfg<16, 16, 1, 1, 3, 1, K, 1>>(a, st, nullptr);
   constexpr int MB = K == 2 ? 2 : 3;
   switch (a.ncm.w) {
@@ -1522,6 +1590,7 @@ static int launch_mat_k(const AsmArgs& a, cudaStream_t st) {
     case 128: return launch_cfg<Cfg<128, 8, 1, 1, MB, 0, K, 1>>(a, st, nullptr);
   }
   return (int)cudaErrorInvalidValue;
+#endif
 }
 
 int launch_material(const AsmArgs& a, void* stream) {
@@ -1532,8 +1601,12 @@ int launch_material(const AsmArgs& a, void* stream) {
 
 template <int NEN, int NQ>
 static int launch_et(const AsmArgs& a, cudaStream_t st, int* launches) {
+#ifdef COMMET_AB_MIN
+  return launch_k<NEN, NQ, 0>(a, st, launches);
+#else
   if (a.ncm.kin == 2) return launch_k<NEN, NQ, 2>(a, st, launches);
   return a.ncm.kin == 1 ? launch_k<NEN, NQ, 1>(a, st, launches) : launch_k<NEN, NQ, 0>(a, st, launches);
+#endif
 }
 
 int launch_fused(const AsmArgs& a, void* stream, int* launches) {

@@ -90,15 +90,29 @@ __global__ void __launch_bounds__(64) simple_kernel(AsmArgs A) {
   }
 }
 
+// the fused kernels' activation on its own: softplus and sigmoid (both forms: the sigmoid-only
+// function of the last hidden layer must give the same s)
+template <int TB>
 __global__ void activation_kernel(const double* __restrict__ y, double* __restrict__ z, double* __restrict__ s,
                                   int64_t n, const double* __restrict__ tab) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i < n) softplus_sig(y[i], tab, z[i], s[i]);
+  if (i < n) {
+    double zz, ss;
+    softplus_sig_t<TB>(y[i], tab, zz, ss);
+    const double s2 = sigmoid_t<TB>(y[i], tab);
+    z[i] = zz;
+    s[i] = ss == s2 ? ss : __longlong_as_double(0x7ff8000000000bad);  // NaN if the two forms differ
+  }
 }
 
-int launch_activation(const double* y, double* z, double* s, int64_t n, const double* tab, void* stream) {
+int launch_activation(const double* y, double* z, double* s, int64_t n, const double* tab, int table_bits,
+                      void* stream) {
   if (n <= 0) return 0;
-  activation_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(y, z, s, n, tab);
+  const unsigned g = (unsigned)((n + 255) / 256);
+  if (table_bits == 8)
+    activation_kernel<8><<<g, 256, 0, (cudaStream_t)stream>>>(y, z, s, n, tab + act_tab_offset<8>());
+  else
+    activation_kernel<6><<<g, 256, 0, (cudaStream_t)stream>>>(y, z, s, n, tab);
   return (int)cudaGetLastError();
 }
 

@@ -122,6 +122,75 @@ __device__ __forceinline__ void post_qp(const Kin& k, const double* __restrict__
       P[i * 3 + J] = w * (F[i * 3 + 0] * S[0 * 3 + J] + F[i * 3 + 1] * S[1 * 3 + J] + F[i * 3 + 2] * S[2 * 3 + J]);
 }
 
+// post_qp split over four cooperating warps (part = warp index, one lane per qp): the same
+// outputs, each part a quarter of the work after its own copy of the kinematics --
+//   part 0: F, F^-T, b, c2, c3 and P = w F S;  part 1: T = w (S - g3 J C^-1), Phi_m, Psi_0;
+//   part 2: Psi_1;  part 3: Psi_2
+__device__ __forceinline__ void post_qp_part(const Kin& k, const double* __restrict__ g,
+                                             const double* __restrict__ H6, double w, double* __restrict__ post,
+                                             double* __restrict__ P, int part) {
+  const double* F = k.F;
+  const double hJ = 0.5 * k.J;
+  if (part <= 1) {
+    double S[9];
+#pragma unroll
+    for (int I = 0; I < 3; I++)
+#pragma unroll
+      for (int J = 0; J < 3; J++) {
+        const double d = (I == J) ? 1.0 : 0.0;
+        S[I * 3 + J] = 2.0 * (g[0] * d + g[1] * (k.I1 * d - k.C[I * 3 + J]) + g[2] * hJ * k.Ci[I * 3 + J]);
+      }
+    if (part == 0) {
+#pragma unroll
+      for (int x = 0; x < 9; x++) {
+        post[x] = F[x];
+        post[9 + x] = k.FiT[x];
+      }
+#pragma unroll
+      for (int i = 0; i < 3; i++)
+#pragma unroll
+        for (int kk = 0; kk < 3; kk++)
+          post[81 + i * 3 + kk] = F[i * 3 + 0] * F[kk * 3 + 0] + F[i * 3 + 1] * F[kk * 3 + 1] + F[i * 3 + 2] * F[kk * 3 + 2];
+      post[90] = -2.0 * g[1] * w;
+      post[91] = -g[2] * k.J * w;
+#pragma unroll
+      for (int i = 0; i < 3; i++)
+#pragma unroll
+        for (int J = 0; J < 3; J++)
+          P[i * 3 + J] = w * (F[i * 3 + 0] * S[0 * 3 + J] + F[i * 3 + 1] * S[1 * 3 + J] + F[i * 3 + 2] * S[2 * 3 + J]);
+      return;
+    }
+#pragma unroll
+    for (int x = 0; x < 9; x++) post[18 + x] = w * (S[x] - g[2] * k.J * k.Ci[x]);
+  }
+  double Phi[3][9];
+#pragma unroll
+  for (int i = 0; i < 3; i++)
+#pragma unroll
+    for (int J = 0; J < 3; J++) {
+      const double FC = F[i * 3 + 0] * k.C[0 * 3 + J] + F[i * 3 + 1] * k.C[1 * 3 + J] + F[i * 3 + 2] * k.C[2 * 3 + J];
+      Phi[0][i * 3 + J] = F[i * 3 + J];
+      Phi[1][i * 3 + J] = k.I1 * F[i * 3 + J] - FC;
+      Phi[2][i * 3 + J] = hJ * k.FiT[i * 3 + J];
+    }
+  // row m of H' = H + diag(g2, 0, g3/J)
+  const int m = part == 1 ? 0 : part - 1;
+  double hp[3];
+  if (m == 0) { hp[0] = H6[0] + g[1]; hp[1] = H6[1]; hp[2] = H6[2]; }
+  else if (m == 1) { hp[0] = H6[1]; hp[1] = H6[3]; hp[2] = H6[4]; }
+  else { hp[0] = H6[2]; hp[1] = H6[4]; hp[2] = H6[5] + g[2] / k.J; }
+  const double w4 = 4.0 * w;
+#pragma unroll
+  for (int x = 0; x < 9; x++) {
+    if (part == 1) {
+      post[27 + x] = Phi[0][x];
+      post[36 + x] = Phi[1][x];
+      post[45 + x] = Phi[2][x];
+    }
+    post[54 + m * 9 + x] = w4 * (hp[0] * Phi[0][x] + hp[1] * Phi[1][x] + hp[2] * Phi[2][x]);
+  }
+}
+
 // Row iJ of w A:  A_iJkL = 4 sum_m Phi_m,iJ Psi_m,kL / (4w) ... (see header), kL = 0..8
 __device__ __forceinline__ void tangent_row(const double* __restrict__ post, int iJ, double* __restrict__ out) {
   const int i = iJ / 3, J = iJ % 3;
@@ -405,80 +474,126 @@ __device__ __forceinline__ double analytic_value(int net, int n, const int32_t* 
 // ---------------------------------------------------------------------------
 // softplus z = log(1 + e^y) and sigmoid s = softplus' (SURVEY s7 hard part 3),
 // branch-free, fp64 FMA + integer ops only (no MUFU, no F2I, no libdevice slow
-// paths).  e = exp(-|y|) by table (2^(j/64)) + degree-5 polynomial on
-// |r| <= ln2/128; log1p(e) by table (1/c_j, log c_j, c_j = 1 + j/64) + degree-7
-// log1p polynomial on |r2| <= 1/128 with the rounding of u = 1 + e corrected;
-// 1/u = invc / (1 + r2) by its 8-term series.  Relative error ~1e-16.
-// tab layout (kActTabSize doubles): [0,64) 2^(j/64); [64,129) invc_j; [129,194) -log(invc_j)
-constexpr int kActTabSize = 194;
+// paths), on tables of N = 2^TB entries:
+//   e = exp(-|y|) = 2^(k/N) * p(r), r = -|y| - k ln2/N, |r| <= ln2/(2N), p the Taylor
+//       polynomial of degree 5 (N = 64) / 4 (N = 256);
+//   log1p(e) = log c_j + log1p(r2), c_j = 1 + j/N nearest to u = 1 + e, r2 = u/c_j - 1,
+//       |r2| <= 1/(2N), log1p by its series to degree 7 / 6, the rounding of u corrected;
+//   1/u = (1/c_j) / (1 + r2) by the series 1 - r2 + ... - r2^7 / - r2^5.
+// Truncation errors, relative: 6e-18 / 3.7e-17 (exp), 2.2e-16 / 1.2e-17 (log1p: r2^(d+1)/(d+1)
+// relative to log1p(r2) ~ r2 when j = 0), 2e-17 / 5.7e-17 (1/u).  The fused kernels whose shared memory allows it use N = 256
+// (4 fp64 ops per neuron fewer, measured on the round-2 A/B); the rest N = 64.
+// tab layout: [0, N) 2^(j/N); [N, 2N+1) 1/c_j; [2N+1, 3N+2) log c_j.  Both tables sit back to
+// back in one device array: N = 64 at offset 0, N = 256 at kActTab6 (kActTabSize doubles).
+template <int TB>
+struct ActTab {
+  static constexpr int N = 1 << TB, SIZE = 3 * N + 2;
+};
+constexpr int kActTab6 = ActTab<6>::SIZE;                   // 194
+constexpr int kActTabSize = ActTab<6>::SIZE + ActTab<8>::SIZE;  // both tables
+template <int TB>
+__host__ __device__ constexpr int act_tab_offset() { return TB == 6 ? 0 : kActTab6; }
 
-__device__ __forceinline__ void softplus_sig(double y, const double* __restrict__ tab, double& z, double& s) {
+template <int TB>
+__device__ __forceinline__ double exp_neg_abs(double y, const double* __restrict__ tab, int& k_out) {
+  constexpr int N = ActTab<TB>::N;
   const double MAGIC = 6755399441055744.0;  // 1.5 * 2^52: round-to-integer by addition
   const double x = fmax(-fabs(y), -708.0);
-  double kd = fma(x, 92.33248261689366, MAGIC);  // 64 / ln2
+  double kd = fma(x, (double)N / 0.6931471805599453, MAGIC);
   const int k = __double2loint(kd);
   kd -= MAGIC;
-  double r = fma(kd, -0.010830424696249145, x);  // ln2/64 hi
-  r = fma(kd, -3.623510646634843e-19, r);        // ln2/64 lo
-  double p = fma(r, 1.0 / 120.0, 1.0 / 24.0);
-  p = fma(p, r, 1.0 / 6.0);
+  double r, p;
+  if constexpr (TB == 6) {
+    r = fma(kd, -0.010830424696249145, x);  // ln2/64 hi
+    r = fma(kd, -3.623510646634843e-19, r); // ln2/64 lo
+    p = fma(r, 1.0 / 120.0, 1.0 / 24.0);
+    p = fma(p, r, 1.0 / 6.0);
+  } else {
+    r = fma(kd, -0.0027076061740622863, x);  // ln2/256 hi
+    r = fma(kd, -9.058776616587108e-20, r);  // ln2/256 lo
+    p = fma(r, 1.0 / 24.0, 1.0 / 6.0);
+  }
   p = fma(p, r, 0.5);
   p = fma(p, r, 1.0);
   p = fma(p, r, 1.0);
-  double e = tab[k & 63] * p;
-  e = __hiloint2double(__double2hiint(e) + (k >> 6) * 1048576, __double2loint(e));  // * 2^(k >> 6)
+  const double e = tab[k & (N - 1)] * p;
+  k_out = k;
+  return __hiloint2double(__double2hiint(e) + (k >> TB) * 1048576, __double2loint(e));  // * 2^(k >> TB)
+}
+
+template <int TB>
+__device__ __forceinline__ void softplus_sig_t(double y, const double* __restrict__ tab, double& z, double& s) {
+  constexpr int N = ActTab<TB>::N;
+  const double MAGIC = 6755399441055744.0;
+  int k;
+  const double e = exp_neg_abs<TB>(y, tab, k);
   const double u = 1.0 + e;
-  const int j = __double2loint(fma(e, 64.0, MAGIC));  // round(64 e) in [0, 64]
-  const double invc = tab[64 + j], logc = tab[129 + j];
+  const int j = __double2loint(fma(e, (double)N, MAGIC));  // round(N e) in [0, N]
+  const double invc = tab[N + j], logc = tab[2 * N + 1 + j];
   const double r2 = fma(u, invc, -1.0);
-  double q = fma(r2, 1.0 / 7.0, -1.0 / 6.0);
-  q = fma(q, r2, 0.2);
-  q = fma(q, r2, -0.25);
-  q = fma(q, r2, 1.0 / 3.0);
-  q = fma(q, r2, -0.5);
   const double r2s = r2 * r2;
+  double q, v;
+  if constexpr (TB == 6) {
+    q = fma(r2, 1.0 / 7.0, -1.0 / 6.0);
+    q = fma(q, r2, 0.2);
+    q = fma(q, r2, -0.25);
+    q = fma(q, r2, 1.0 / 3.0);
+    q = fma(q, r2, -0.5);
+    const double r4 = r2s * r2s;
+    v = (1.0 - r2) * (1.0 + r2s) * (1.0 + r4);  // 1/(1 + r2), error r2^8
+  } else {  // degree 6: at j = 0 (e < 1/512) z = log1p(r2) ~ r2, so the RELATIVE error is r2^6/7
+    q = fma(r2, -1.0 / 6.0, 0.2);
+    q = fma(q, r2, -0.25);
+    q = fma(q, r2, 1.0 / 3.0);
+    q = fma(q, r2, -0.5);
+    v = (1.0 - r2) * (fma(r2s, r2s, r2s) + 1.0);  // 1/(1 + r2), error r2^6
+  }
   const double lp = fma(q, r2s, r2);                 // log1p(r2)
   const double d = e - (u - 1.0);                    // rounding error of u (exact)
   z = fmax(y, 0.0) + (logc + fma(d, invc, lp));      // max(y,0) + log1p(e)
-  const double r4 = r2s * r2s;
-  const double v = (1.0 - r2) * (1.0 + r2s) * (1.0 + r4);  // 1/(1 + r2), error r2^8
-  const double iu = invc * v;                        // 1 / u
-  s = (y >= 0.0 ? 1.0 : e) * iu;
+  s = (y >= 0.0 ? 1.0 : e) * (invc * v);
 }
 
 // sigmoid only (the last hidden layer needs s, not z): e = exp(-|y|) and 1/(1+e) as above
-__device__ __forceinline__ double sigmoid_tab(double y, const double* __restrict__ tab) {
+template <int TB>
+__device__ __forceinline__ double sigmoid_t(double y, const double* __restrict__ tab) {
+  constexpr int N = ActTab<TB>::N;
   const double MAGIC = 6755399441055744.0;
-  const double x = fmax(-fabs(y), -708.0);
-  double kd = fma(x, 92.33248261689366, MAGIC);
-  const int k = __double2loint(kd);
-  kd -= MAGIC;
-  double r = fma(kd, -0.010830424696249145, x);
-  r = fma(kd, -3.623510646634843e-19, r);
-  double p = fma(r, 1.0 / 120.0, 1.0 / 24.0);
-  p = fma(p, r, 1.0 / 6.0);
-  p = fma(p, r, 0.5);
-  p = fma(p, r, 1.0);
-  p = fma(p, r, 1.0);
-  double e = tab[k & 63] * p;
-  e = __hiloint2double(__double2hiint(e) + (k >> 6) * 1048576, __double2loint(e));
+  int k;
+  const double e = exp_neg_abs<TB>(y, tab, k);
   const double u = 1.0 + e;
-  const int j = __double2loint(fma(e, 64.0, MAGIC));
-  const double invc = tab[64 + j];
+  const int j = __double2loint(fma(e, (double)N, MAGIC));
+  const double invc = tab[N + j];
   const double r2 = fma(u, invc, -1.0);
   const double r2s = r2 * r2;
-  const double v = (1.0 - r2) * (1.0 + r2s) * (1.0 + r2s * r2s);
+  double v;
+  if constexpr (TB == 6)
+    v = (1.0 - r2) * (1.0 + r2s) * (1.0 + r2s * r2s);
+  else
+    v = (1.0 - r2) * (fma(r2s, r2s, r2s) + 1.0);
   return (y >= 0.0 ? 1.0 : e) * (invc * v);
 }
 
-// host: fill the table (long double for the reference values)
-inline void fill_act_table(double* tab) {
-  for (int j = 0; j < 64; j++) tab[j] = (double)exp2l((long double)j / 64.0L);
-  for (int j = 0; j <= 64; j++) {
-    const double invc = (double)(1.0L / (1.0L + (long double)j / 64.0L));
-    tab[64 + j] = invc;
-    tab[129 + j] = (double)(-logl((long double)invc));
+// the N = 64 forms (kernels that keep the small table: simple kernel, Alg. 4 helper, 3-pass)
+__device__ __forceinline__ void softplus_sig(double y, const double* __restrict__ tab, double& z, double& s) {
+  softplus_sig_t<6>(y, tab, z, s);
+}
+__device__ __forceinline__ double sigmoid_tab(double y, const double* __restrict__ tab) { return sigmoid_t<6>(y, tab); }
+
+// host: fill both tables (long double for the reference values)
+template <int TB>
+inline void fill_act_table_t(double* tab) {
+  constexpr int N = ActTab<TB>::N;
+  for (int j = 0; j < N; j++) tab[j] = (double)exp2l((long double)j / N);
+  for (int j = 0; j <= N; j++) {
+    const double invc = (double)(1.0L / (1.0L + (long double)j / N));
+    tab[N + j] = invc;
+    tab[2 * N + 1 + j] = (double)(-logl((long double)invc));
   }
+}
+inline void fill_act_table(double* tab) {
+  fill_act_table_t<6>(tab);
+  fill_act_table_t<8>(tab + kActTab6);
 }
 
 }  // namespace commet

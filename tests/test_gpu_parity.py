@@ -136,15 +136,17 @@ def test_deterministic():
     assert np.array_equal(r1, r2) and np.array_equal(v1, v2)
 
 
-def test_activation_table_accuracy():
+@pytest.mark.parametrize("table_bits", [6, 8])
+def test_activation_table_accuracy(table_bits):
     """The fused kernel's branch-free softplus/sigmoid (qp_math.cuh) against
-    numpy's logaddexp / exp on a sweep of y, incl. the extremes."""
+    numpy's logaddexp / exp on a sweep of y, incl. the extremes -- both table sizes;
+    the sigmoid-only form must equal the softplus+sigmoid one bit for bit."""
     torch = _torch()
     import paper_2510_00884_b200 as pc
     rng = np.random.default_rng(0)
     y = np.concatenate([np.linspace(-40, 40, 200001), rng.normal(0, 3, 100000), rng.uniform(-800, 800, 10000),
                         np.array([0.0, -0.0, 1e-300, -1e-300, 708.0, -708.0, 750.0, -750.0, 1e-8, -1e-8])])
-    z, s = pc.activation(torch.from_numpy(y).cuda())
+    z, s = pc.activation(torch.from_numpy(y).cuda(), table_bits)
     z, s = z.cpu().numpy(), s.cpu().numpy()
     zr = np.logaddexp(0.0, y)
     sr = np.where(y >= 0, 1.0 / (1.0 + np.exp(-np.abs(y))), np.exp(-np.abs(y)) / (1.0 + np.exp(-np.abs(y))))

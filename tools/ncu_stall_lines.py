@@ -17,7 +17,7 @@ import sys
 import tempfile
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-LIB = os.path.join(ROOT, "paper_2510_00884_b200", "libcommet.so")
+LIB = os.environ.get("COMMET_LIB") or os.path.join(ROOT, "paper_2510_00884_b200", "libcommet.so")
 CSRC = os.path.join(ROOT, "paper_2510_00884_b200", "csrc")
 DEFAULT_K = "_ZN6commet12fused_kernelINS_3CfgILi64ELi16ELi8ELi8ELi3ELi0ELi0ELi0ELi4EEEEEvNS_7AsmArgsE"
 
