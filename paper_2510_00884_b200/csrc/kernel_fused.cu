@@ -1255,7 +1255,11 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
     // ICNN, 3 inputs: four warps cooperate (warp = part of post_qp, lane = qp); otherwise one
     // thread per qp
     constexpr bool PAR7 = COMMET_POST_PAR && C::NET == 0 && C::KIN != 2 && C::NWARP == 4;
+#ifdef COMMET_EXP_SKIP_7A  // timing experiments only
+    if (false) {
+#else
     if (PAR7 ? lane < Q : tid < Q) {
+#endif
       const int q = PAR7 ? lane : tid;
       double gq[C::NK], H6[C::NH];
       if constexpr (C::NET == 0) {
@@ -1292,7 +1296,11 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
 
     STAGE_MARK(7)
     // ---- stage 7b: A_q (81 entries, scaled by w), one (q, iJ) row per item ------------------
+#ifdef COMMET_EXP_SKIP_7B  // timing experiments only
+    for (int it = tid; it < 0; it += C::NTHR) {
+#else
     for (int it = tid; it < Q * 9; it += C::NTHR) {
+#endif
       const int q = it / 9, iJ = it % 9;
       if constexpr (C::KIN == 2)
         tangent_row_aniso(post + q * PS, iJ, qA + q * 81 + iJ * 9);
@@ -1320,8 +1328,14 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
         const int k = ik < 3 ? ik : (ik < 5 ? ik - 2 : 2);
         double c[2] = {0.0, 0.0};
         const int a = 8 * mt + g, bq = 8 * nt + g;
+#ifdef COMMET_EXP_SKIP_KE  // timing experiments only
+        c[0] = qA[tid]; c[1] = qA[tid + 1];
+#pragma unroll
+        for (int kt = 0; kt < 0; kt++) {
+#else
 #pragma unroll
         for (int kt = 0; kt < KS; kt++) {
+#endif
           const int kk = 4 * kt + t, q = e * NQ + kk / 3, J = kk % 3;
           const double av = a < NEN ? sgN[(q * NEN + a) * 3 + J] : 0.0;
           double bv = 0.0;
@@ -1333,7 +1347,12 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
           dmma(c, av, bv);
         }
         const int64_t el = e0 + e;
+#ifdef COMMET_EXP_SKIP_SCATTER  // timing experiments only: keep the values alive, no addresses
+        if (c[0] == 1234.5678 && c[1] == 8765.4321) A.v_own[0] = c[0] + c[1];
+        if (false) {
+#else
         if (a < NEN) {
+#endif
           const int64_t la = __ldg(A.lrow + el * NEN + a);
           const int64_t rsa = __ldg(A.node_rs + la);
           const int sa = 3 * __ldg(A.node_deg + la);
