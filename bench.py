@@ -29,9 +29,50 @@ from synth import gen  # noqa: E402
 METRIC = "quadrature-point stress+tangent updates/s (assembled elements/s and % fp64 roofline alongside)"
 FP64_PEAK_TFLOPS = 36.9   # measured, sustained DMMA m8n8k4, profiles/r01_fp64_peak.json
 FP64_PEAK_SOURCE = "measured: tools/fp64_peak.cu sustained DMMA (profiles/r01_fp64_peak.json); MEASURED_PEAKS.json has no fp64 entry"
-# DRAM bytes (read + write) per colour launch of the fused kernel, from ncu captures of this
-# kernel version (profiles/r01_ncu_c5_dram.csv, profiles/r01_ncu_full_c3_s2.txt); 8 equal colours
-NCU_DRAM_PER_LAUNCH = {"c3": 362.99e6 + 198.65e6, "c5": 23.43e9 + 14.88e9}
+HBM_FALLBACK_GBS = 6549.1  # only if MEASURED_PEAKS.json is absent (its value on this pool, round 2)
+# DRAM bytes (read + write) per launch of the dominant kernel, from one ncu capture of the kernel
+# the bench launches (profiles/r02_ncu_traffic.json: config -> kernel signature + bytes); reported
+# only when the signature matches the launched kernel
+TRAFFIC_FILE = os.path.join(ROOT, "profiles", "r02_ncu_traffic.json")
+
+
+def hbm_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs"
+    except (OSError, KeyError, ValueError):
+        return HBM_FALLBACK_GBS, "fallback (MEASURED_PEAKS.json absent)"
+
+
+def measured_traffic(config: str, kernel: str):
+    """-> (bytes per launch, source) of the ncu capture of `kernel` on `config`, or (None, why)."""
+    try:
+        with open(TRAFFIC_FILE) as f:
+            rec = json.load(f).get(config)
+    except (OSError, ValueError):
+        return None, "no ncu traffic record"
+    if not rec:
+        return None, f"no ncu traffic record for {config}"
+    if rec.get("kernel") != kernel:
+        return None, f"ncu record is of {rec.get('kernel')}, the bench launched {kernel}"
+    return float(rec["dram_bytes_per_launch"]), rec.get("source", TRAFFIC_FILE)
+
+
+def host_info():
+    """CPU model, logical CPUs and RAM of the host (the cpu_baseline context)."""
+    model, ram = None, None
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+        for ln in open("/proc/meminfo"):
+            if ln.startswith("MemTotal"):
+                ram = round(int(ln.split()[1]) / 2 ** 20, 1)
+                break
+    except OSError:
+        pass
+    return dict(cpu_model=model, logical_cpus=os.cpu_count(), ram_gib=ram)
 
 WORKLOAD = {
     "c1": "c1: 4^3 hex8 unit cube, 2x2x2 Gauss (512 qp), NCM 16x2 softplus + kappa(J-1)^2, u ~ U(+-0.02)",
@@ -57,8 +98,8 @@ def hbm_bytes_per_element(elem_type: int, nnz_per_el: float, dofs_per_el: float)
     """Algorithmic HBM bytes per element (write-once outputs): dN/dX + w + conn
     + slots + u gather + r + CSR values."""
     n_en, n_q = (8, 8) if elem_type == gen.HEX8 else (10, 4)
-    return 8 * n_q * n_en * 3 + 8 * n_q + 4 * n_en + n_en * n_en + 8 * 3 * n_en * 0.0 + \
-        8 * dofs_per_el + 8 * nnz_per_el + 8 * dofs_per_el
+    return 8 * n_q * n_en * 3 + 8 * n_q + 4 * n_en + n_en * n_en + 8 * dofs_per_el + 8 * nnz_per_el + \
+        8 * dofs_per_el
 
 
 # ---------------------------------------------------------------------------
@@ -168,10 +209,22 @@ def oracle_sample(cfg: dict, seconds: float):
     ns2 = int(min(conn.shape[0], max(ns, ns * seconds / max(t, 1e-9))))
     if ns2 != ns:
         ns, t = ns2, run(ns2)
-    return dict(value=ns * n_q / t, unit="qp/s", cores=oracle.max_threads(), kind="oracle",
+    cores = oracle.max_threads()
+    # per-core rate: one thread on a sample of ~2 s (then the thread count is restored)
+    ns1 = int(max(16, min(ns, ns * 2.0 / max(t * cores, 1e-9))))
+    sub1 = np.ascontiguousarray(conn[:ns1])
+    rp1, ci1 = oracle.pattern(cfg["n_nodes"], sub1)
+    t1 = time.perf_counter()
+    oracle.assemble(cfg["ncm"], cfg["n_nodes"], sub1, gN[:ns1], qw[:ns1], cfg["u"], rp1, ci1, mode=1, n_threads=1)
+    t1 = time.perf_counter() - t1
+    oracle.assemble(cfg["ncm"], cfg["n_nodes"], sub1[:1], gN[:1], qw[:1], cfg["u"], *oracle.pattern(cfg["n_nodes"], sub1[:1]),
+                    mode=1, n_threads=cores)
+    host = dict(host_info(), single_thread_qp_s=ns1 * n_q / t1,
+                single_thread_sample=f"first {ns1} elements, 1 thread, {t1:.2f} s")
+    return dict(value=ns * n_q / t, unit="qp/s", cores=cores, kind="oracle",
                 sample=f"first {ns} of {conn.shape[0]} elements ({ns * n_q} qp), oracle.assemble "
                        f"(plain C, OpenMP over element colours), {t:.1f} s",
-                elements_per_s=ns / t, seconds=t)
+                host=host, elements_per_s=ns / t, seconds=t)
 
 
 def run_reference(args):
@@ -203,7 +256,7 @@ def run_reference(args):
                 config=dict(workload=WORKLOAD[args.config], sample_elements=ns),
                 elements_per_s=ns / t,
                 cpu_baseline=dict(value=value, unit="qp/s", cores=oracle.max_threads(), kind="oracle",
-                                  sample=f"first {ns} elements of {args.config} per step"),
+                                  sample=f"first {ns} elements of {args.config} per step", host=base["host"]),
                 e2e=dict(value=value, unit="qp/s", h2d_bytes_per_step=0, d2h_bytes_per_step=0))
     print(json.dumps(line), flush=True)
     return 0
@@ -368,8 +421,14 @@ def main():
     total_qp = spec_total_qp(args.config, n_el, n_q, ws)
     total_el = total_qp // n_q
     fl = flops_per_qp(cfg["elem_type"], spec.width, spec.n_hidden)
-    # roofline of the dominant kernel (fused_kernel: all colour launches of one step)
+    # roofline of the dominant kernel (all its colour launches of one step; the launches are equal
+    # in size, so the per-launch rate is the per-step rate)
     achieved = fl * total_qp / ws / (kern_ms * 1e-3) / 1e12
+    kname = ("ws_kernel" if kinfo.get("warp_specialised") else "fused_kernel") + \
+        f"<w={spec.width},L={spec.n_hidden},{'hex8' if cfg['elem_type'] == gen.HEX8 else 'tet10'}>"
+    traffic, traffic_src = measured_traffic(args.config, kname) if ws == 1 and args.kernel == "fused" else \
+        (None, "single-GPU fused kernel only")
+    hbm_pk, hbm_src = hbm_peak()
     nnz_local, rows_local = lib.nnz, lib.n_rows
     hbm = hbm_bytes_per_element(cfg["elem_type"], nnz_local / max(n_el, 1), rows_local / max(n_el, 1))
     line = dict(
@@ -387,18 +446,18 @@ def main():
         kernel_ms_per_step=kern_ms,
         roofline=dict(bound="alu", pipe="fp64 (DFMA/DMMA share one datapath)", achieved=achieved,
                       peak=FP64_PEAK_TFLOPS, unit="TFLOP/s", frac=achieved / FP64_PEAK_TFLOPS,
-                      traffic=(NCU_DRAM_PER_LAUNCH[args.config] * info["n_colours"]
-                               if args.config in NCU_DRAM_PER_LAUNCH and ws == 1 and args.kernel == "fused" else None),
-                      traffic_unit="bytes per step (all colour launches; ncu dram__bytes_read+write, "
-                                   "profiles/); algorithmic per step: hbm_algorithmic_gbs x kernel time",
-                      flops_per_qp=fl, peak_source=FP64_PEAK_SOURCE,
-                      hbm_algorithmic_gbs=hbm * n_el / (kern_ms * 1e-3) / 1e9, hbm_peak_gbs=6556.2),
+                      traffic=traffic, traffic_unit="bytes per launch (one colour launch of " + kname +
+                      "; ncu dram__bytes_read.sum + dram__bytes_write.sum)", traffic_source=traffic_src,
+                      algorithmic_bytes_per_launch=hbm * n_el / max(info["n_colours"], 1),
+                      kernel=kname, flops_per_qp=fl, peak_source=FP64_PEAK_SOURCE,
+                      hbm_algorithmic_gbs=hbm * n_el / (kern_ms * 1e-3) / 1e9, hbm_peak_gbs=hbm_pk,
+                      hbm_peak_source=hbm_src),
         clocks=clocks, gpu_launches=info["launches"] * args.steps,
         e2e=e2e, det_f_ok=(bad == -1),
     )
     if rank == 0 and ws == 1 and not args.no_cpu:
         line["cpu_baseline"] = {k: v for k, v in oracle_sample(cfg, args.cpu_seconds).items()
-                                if k in ("value", "unit", "cores", "kind", "sample")}
+                                if k in ("value", "unit", "cores", "kind", "sample", "host")}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if ws > 1:

@@ -202,9 +202,15 @@ commet_status commet_info(commet_ctx ctx, int32_t* n_colours, int32_t* n_q, int3
                           int32_t* launches_per_assemble);
 
 /* Launch shape of the fused kernel for this ctx: dynamic shared memory per CTA,
- * resident CTAs per SM and registers per thread (diagnostics). */
+ * resident CTAs per SM and registers per thread at launch (diagnostics; the
+ * warp-specialised kernel then moves registers between its warpgroups with
+ * setmaxnreg: 168 network / 88 element). */
 commet_status commet_kernel_info(commet_ctx ctx, int32_t* smem_bytes, int32_t* ctas_per_sm,
                                  int32_t* regs_per_thread);
+/* Which kernel the assembly launches for this ctx: threads per CTA, and 1 for the
+ * warp-specialised kernel (hex8, forward-sweep ICNN: 4 network + 4 element warps,
+ * DESIGN.md s7), 0 for the one-role fused kernel (diagnostics). */
+commet_status commet_kernel_config(commet_ctx ctx, int32_t* threads_per_cta, int32_t* warp_specialised);
 
 /* Kernel-time instrumentation for benchmarks: with n_slots > 0, every
  * commet_assemble records a CUDA event pair on its stream around its kernel

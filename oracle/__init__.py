@@ -36,7 +36,7 @@ class _Ncm(C.Structure):
                 ("cann_f", C.c_void_p), ("cann_w1", C.c_void_p), ("cann_w2", C.c_void_p),
                 ("gt", C.c_double * 3), ("kan_layers", C.c_int32), ("kan_width", C.c_void_p),
                 ("kan_nb", C.c_int32), ("kan_k", C.c_int32), ("kan_grid", C.c_void_p), ("kan_w", C.c_void_p),
-                ("kan_c", C.c_void_p), ("a0", C.c_double * 3)]
+                ("kan_c", C.c_void_p), ("a0", C.c_double * 3), ("n_sv", C.c_int32), ("a1", C.c_double * 3)]
 
 KIN = {"standard": 0, "isochoric": 1, "anisotropic": 2}
 NET = {"icnn": 0, "cann": 1, "gent_thomas": 2, "ickan": 3}
@@ -102,7 +102,9 @@ class Ncm:
                       0 if self.kan_width is None else self.kan_width.size - 1, _p(self.kan_width),
                       int(ncm.get("kan_nb", 0)), int(ncm.get("kan_k", 3)), _p(self.arrays["kan_grid"]),
                       _p(self.arrays["kan_w"]), _p(self.arrays["kan_c"]),
-                      (C.c_double * 3)(*(ncm.get("a0") if ncm.get("a0") is not None else (0.0, 0.0, 0.0))))
+                      (C.c_double * 3)(*(ncm.get("a0") if ncm.get("a0") is not None else (0.0, 0.0, 0.0))),
+                      2 if ncm.get("a1") is not None else 1,
+                      (C.c_double * 3)(*(ncm.get("a1") if ncm.get("a1") is not None else (0.0, 0.0, 0.0))))
 
     @property
     def ptr(self):

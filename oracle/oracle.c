@@ -53,6 +53,8 @@ typedef struct {
   const double* kan_w;       /* [edges] */
   const double* kan_c;       /* [edges][nb] */
   double a0[3];              /* anisotropic kinematics (kinematics = 2): structural vector A0 (reference) */
+  int32_t n_sv;              /* anisotropic: number of structural vectors, 1 (0 = 1) or 2 (a0, a1) */
+  double a1[3];              /* anisotropic, n_sv = 2: the second structural vector */
 } oracle_ncm;
 
 /* ---------------------------------------------------------------------- */
@@ -271,9 +273,9 @@ static void spline_eval(const double* c, int nb, int k, double xmin, double xmax
 /* forward mode through the layers: z, dz/dK (3), d2z/dK2 (3x3) per node, as Alg. 4 does for the ICNN */
 static int ickan_eval(const oracle_ncm* m, int nk, const double* K, double* N_out, double* g, double* H) {
   const int R = m->kan_layers, nb = m->kan_nb, k = m->kan_k;
-  double z[32], dz[32][5], d2z[32][25], y[32], dy[32][5], d2y[32][25];
+  double z[32], dz[32][9], d2z[32][81], y[32], dy[32][9], d2y[32][81];
   int nin = m->kan_width[0];
-  if (nin != nk) return 3;
+  if (nin != nk || nk > 9) return 3;
   for (int j = 0; j < nin; j++) {
     z[j] = K[j];
     for (int p = 0; p < nk; p++) dz[j][p] = (p == j);
@@ -466,33 +468,52 @@ static void spatial_to_material(const double F[9], int n, double G[][9], double 
 }
 
 /*
- * Anisotropic kinematics (one structural vector A0; App. A.2.1 table) in the
- * paper's spatial form, a = F A0:
+ * Anisotropic kinematics (App. A.2.1 table; Eq. standard-inv-II) with
+ * n_sv = 1 or 2 structural vectors A_i (reference configuration), in the paper's spatial form,
+ * a_i = F A_i:
  *   I1: G = B, GG = O;  I2: G = B tr B - B^2, GG = B(x)B - B(x)_B;  J: G = J/2 I, GG = J/4 (I(x)I - 2 I(x)_I)
- *   I4 = A0.C A0: G = sym(a (x) a), GG = O;  I5 = A0.C^2 A0: G = 2 sym(a (x) B a),
- *   GG = B (x)_ sym(a (x) a) + sym(a (x) a) (x)_ B
- * then tau, c and the pull-back as above.  Inputs K = (I1-3, I2-3, J-1, I4-1, I5-1).
+ *   I4,ij = A_i.C A_j:   G = sym(a_i (x) a_j), GG = O
+ *   I5,ij = A_i.C^2 A_j: G = sym(a_i (x) B a_j) + sym(a_j (x) B a_i)   (reading R28: the table's
+ *                        2 sym(a_i (x) B a_j) holds for i = j only -- I5,ij is symmetric in i, j),
+ *                        GG = B (x)_ sym(a_i (x) a_j) + sym(a_i (x) a_j) (x)_ B
+ * for the pairs i <= j in the order (0,0), (0,1), (1,1); then tau, c and the pull-back as above.
+ * Inputs K = (I1-3, I2-3, J-1, then per pair I4,ij - A_i.A_j, I5,ij - A_i.A_j): K = 0 at F = I
+ * (for one unit vector: I4-1, I5-1).  nk = 3 + 2 n_pairs (5 or 9).
  */
-static void anisotropic_S_CC(const double F[9], double Jd, const double a0[3], const double g[5], const double H[25],
+static int aniso_pairs(const oracle_ncm* m, const double* A[2], int pi[3], int pj[3]) {
+  const int nsv = m->n_sv > 1 ? 2 : 1;
+  A[0] = m->a0;
+  A[1] = m->a1;
+  int np = 0;
+  for (int i = 0; i < nsv; i++)
+    for (int j = i; j < nsv; j++) {
+      pi[np] = i;
+      pj[np] = j;
+      np++;
+    }
+  return np;
+}
+
+static void anisotropic_S_CC(const oracle_ncm* m, const double F[9], double Jd, const double* g, const double* H,
                              double S[9], double CC[81]) {
-  double B[9], B2[9], a[3], Ba[3], A[9], G[5][9], GG[5][81];
-  for (int i = 0; i < 3; i++) {
-    a[i] = F[i * 3] * a0[0] + F[i * 3 + 1] * a0[1] + F[i * 3 + 2] * a0[2];
+  const double* A[2];
+  int pi[3], pj[3];
+  const int np = aniso_pairs(m, A, pi, pj), nk = 3 + 2 * np;
+  double B[9], B2[9], a[2][3], Ba[2][3], G[9][9], GG[9][81];
+  for (int i = 0; i < 3; i++)
     for (int j = 0; j < 3; j++) B[i * 3 + j] = F[i * 3] * F[j * 3] + F[i * 3 + 1] * F[j * 3 + 1] + F[i * 3 + 2] * F[j * 3 + 2];
-  }
-  for (int i = 0; i < 3; i++) {
-    Ba[i] = B[i * 3] * a[0] + B[i * 3 + 1] * a[1] + B[i * 3 + 2] * a[2];
+  for (int v = 0; v < 2; v++)
+    for (int i = 0; i < 3; i++) a[v][i] = F[i * 3] * A[v][0] + F[i * 3 + 1] * A[v][1] + F[i * 3 + 2] * A[v][2];
+  for (int v = 0; v < 2; v++)
+    for (int i = 0; i < 3; i++) Ba[v][i] = B[i * 3] * a[v][0] + B[i * 3 + 1] * a[v][1] + B[i * 3 + 2] * a[v][2];
+  for (int i = 0; i < 3; i++)
     for (int j = 0; j < 3; j++) B2[i * 3 + j] = B[i * 3] * B[j] + B[i * 3 + 1] * B[3 + j] + B[i * 3 + 2] * B[6 + j];
-  }
   const double trB = B[0] + B[4] + B[8];
   for (int i = 0; i < 3; i++)
     for (int j = 0; j < 3; j++) {
-      A[i * 3 + j] = a[i] * a[j];  /* sym(a (x) a) */
       G[0][i * 3 + j] = B[i * 3 + j];
       G[1][i * 3 + j] = B[i * 3 + j] * trB - B2[i * 3 + j];
       G[2][i * 3 + j] = 0.5 * Jd * (i == j);
-      G[3][i * 3 + j] = a[i] * a[j];
-      G[4][i * 3 + j] = a[i] * Ba[j] + Ba[i] * a[j];  /* 2 sym(a (x) B a) */
     }
   for (int i = 0; i < 3; i++)
     for (int j = 0; j < 3; j++)
@@ -502,11 +523,28 @@ static void anisotropic_S_CC(const double F[9], double Jd, const double a0[3], c
           GG[0][x] = 0.0;
           GG[1][x] = B[i * 3 + j] * B[k * 3 + l] - 0.5 * (B[i * 3 + k] * B[j * 3 + l] + B[i * 3 + l] * B[j * 3 + k]);
           GG[2][x] = 0.25 * Jd * ((double)((i == j) * (k == l)) - ((i == k) * (j == l) + (i == l) * (j == k)));
-          GG[3][x] = 0.0;
-          GG[4][x] = 0.5 * (B[i * 3 + k] * A[j * 3 + l] + B[i * 3 + l] * A[j * 3 + k]) +
-                     0.5 * (A[i * 3 + k] * B[j * 3 + l] + A[i * 3 + l] * B[j * 3 + k]);
         }
-  spatial_to_material(F, 5, G, GG, g, H, S, CC);
+  for (int p = 0; p < np; p++) {
+    const double *ai = a[pi[p]], *aj = a[pj[p]], *Bai = Ba[pi[p]], *Baj = Ba[pj[p]];
+    double As[9];
+    const int m4 = 3 + 2 * p, m5 = 4 + 2 * p;
+    for (int i = 0; i < 3; i++)
+      for (int j = 0; j < 3; j++) {
+        As[i * 3 + j] = 0.5 * (ai[i] * aj[j] + aj[i] * ai[j]); /* sym(a_i (x) a_j) */
+        G[m4][i * 3 + j] = As[i * 3 + j];
+        G[m5][i * 3 + j] = 0.5 * (ai[i] * Baj[j] + Baj[i] * ai[j]) + 0.5 * (aj[i] * Bai[j] + Bai[i] * aj[j]);
+      }
+    for (int i = 0; i < 3; i++)
+      for (int j = 0; j < 3; j++)
+        for (int k = 0; k < 3; k++)
+          for (int l = 0; l < 3; l++) {
+            const int x = I4(i, j, k, l);
+            GG[m4][x] = 0.0;
+            GG[m5][x] = 0.5 * (B[i * 3 + k] * As[j * 3 + l] + B[i * 3 + l] * As[j * 3 + k]) +
+                        0.5 * (As[i * 3 + k] * B[j * 3 + l] + As[i * 3 + l] * B[j * 3 + k]);
+          }
+  }
+  spatial_to_material(F, nk, G, GG, g, H, S, CC);
 }
 
 /*
@@ -549,20 +587,31 @@ double oracle_material_point(const oracle_ncm* m, const double F[9], double k_ou
   double I2 = 0.5 * (I1 * I1 - trC2);
   double Jd = det3(F);
   inv3(C, Ci);
-  if (m->kinematics == 2) { /* anisotropic: K = (I1-3, I2-3, J-1, I4-1, I5-1) */
-    double CA[3], C2A = 0.0, I4v = 0.0;
-    for (int I = 0; I < 3; I++) CA[I] = C[I * 3] * m->a0[0] + C[I * 3 + 1] * m->a0[1] + C[I * 3 + 2] * m->a0[2];
-    for (int I = 0; I < 3; I++) {
-      I4v += m->a0[I] * CA[I];
-      C2A += CA[I] * CA[I]; /* A0.C^2 A0 = |C A0|^2 */
+  if (m->kinematics == 2) { /* anisotropic: K = (I1-3, I2-3, J-1, per pair I4,ij - A_i.A_j, I5,ij - A_i.A_j) */
+    const double* Av[2];
+    int pi[3], pj[3];
+    const int np = aniso_pairs(m, Av, pi, pj), nk = 3 + 2 * np;
+    double CA[2][3];
+    for (int v = 0; v < 2; v++)
+      for (int I = 0; I < 3; I++) CA[v][I] = C[I * 3] * Av[v][0] + C[I * 3 + 1] * Av[v][1] + C[I * 3 + 2] * Av[v][2];
+    double kN[9] = {I1 - 3.0, I2 - 3.0, Jd - 1.0, 0, 0, 0, 0, 0, 0};
+    for (int p = 0; p < np; p++) {
+      const double *Ai = Av[pi[p]], *Aj = Av[pj[p]], *CAi = CA[pi[p]], *CAj = CA[pj[p]];
+      double i4 = 0.0, i5 = 0.0, aa = 0.0;
+      for (int I = 0; I < 3; I++) {
+        i4 += Ai[I] * CAj[I];   /* A_i.C A_j */
+        i5 += CAi[I] * CAj[I];  /* A_i.C^2 A_j = (C A_i).(C A_j) */
+        aa += Ai[I] * Aj[I];
+      }
+      kN[3 + 2 * p] = i4 - aa;
+      kN[4 + 2 * p] = i5 - aa;
     }
-    const double k5[5] = {I1 - 3.0, I2 - 3.0, Jd - 1.0, I4v - 1.0, C2A - 1.0};
-    double N5, g5[5], H5[25];
-    if (oracle_ncm_eval_n(m, 5, k5, &N5, g5, H5) != 0) return ncm_failed(k_out, W_out, g_out, H_out, S, CC, P, A);
-    const double W5 = N5 + m->kappa * (Jd - 1.0) * (Jd - 1.0) - m->ref_shift * (Jd - 1.0);
-    g5[2] += 2.0 * m->kappa * (Jd - 1.0) - m->ref_shift;
-    H5[12] += 2.0 * m->kappa;
-    anisotropic_S_CC(F, Jd, m->a0, g5, H5, S, CC);
+    double NN, gN[9], HN[81];
+    if (oracle_ncm_eval_n(m, nk, kN, &NN, gN, HN) != 0) return ncm_failed(k_out, W_out, g_out, H_out, S, CC, P, A);
+    const double WN = NN + m->kappa * (Jd - 1.0) * (Jd - 1.0) - m->ref_shift * (Jd - 1.0);
+    gN[2] += 2.0 * m->kappa * (Jd - 1.0) - m->ref_shift;
+    HN[2 * nk + 2] += 2.0 * m->kappa;
+    anisotropic_S_CC(m, F, Jd, gN, HN, S, CC);
     for (int i = 0; i < 3; i++)
       for (int J = 0; J < 3; J++) {
         double t = 0.0;
@@ -579,13 +628,13 @@ double oracle_material_point(const oracle_ncm* m, const double F[9], double k_ou
             A[I4(i, J, kk, L)] = t;
           }
     if (k_out)
-      for (int p = 0; p < 3; p++) k_out[p] = k5[p];
-    if (W_out) *W_out = W5;
+      for (int p = 0; p < 3; p++) k_out[p] = kN[p];
+    if (W_out) *W_out = WN;
     if (g_out)
-      for (int p = 0; p < 3; p++) g_out[p] = g5[p];
+      for (int p = 0; p < 3; p++) g_out[p] = gN[p];
     if (H_out)
       for (int p = 0; p < 3; p++)
-        for (int q = 0; q < 3; q++) H_out[p * 3 + q] = H5[p * 5 + q];
+        for (int q = 0; q < 3; q++) H_out[p * 3 + q] = HN[p * nk + q];
     return Jd;
   }
   double k[3] = {I1 - 3.0, I2 - 3.0, Jd - 1.0};

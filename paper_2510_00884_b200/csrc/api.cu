@@ -485,12 +485,9 @@ extern "C" commet_status commet_info(commet_ctx c, int32_t* n_colours, int32_t* 
   return COMMET_OK;
 }
 
-extern "C" commet_status commet_kernel_info(commet_ctx c, int32_t* smem_bytes, int32_t* ctas_per_sm,
-                                            int32_t* regs_per_thread) {
-  if (!c) return fail(nullptr, COMMET_ERR_ARG, "ctx is NULL");
+static commet_status kernel_query(commet_ctx c, int (&q)[5]) {
   CUDA_TRY(c, cudaSetDevice(c->device));
   // the instantiation the assembly (or material-point) dispatch launches for this ctx
-  int q[3] = {0, 0, 0};
   AsmArgs a{};
   a.n_en = c->material_only ? 1 : c->plan.n_en;
   a.n_q = c->material_only ? 1 : c->plan.n_q;
@@ -499,9 +496,28 @@ extern "C" commet_status commet_kernel_info(commet_ctx c, int32_t* smem_bytes, i
   a.query = q;
   const int e = c->material_only ? launch_material(a, nullptr) : launch_fused(a, nullptr, nullptr);
   if (e) return fail(c, COMMET_ERR_CUDA, "kernel query: %s", cudaGetErrorString((cudaError_t)e));
+  return COMMET_OK;
+}
+
+extern "C" commet_status commet_kernel_info(commet_ctx c, int32_t* smem_bytes, int32_t* ctas_per_sm,
+                                            int32_t* regs_per_thread) {
+  if (!c) return fail(nullptr, COMMET_ERR_ARG, "ctx is NULL");
+  int q[5] = {0, 0, 0, 128, 0};
+  const commet_status s = kernel_query(c, q);
+  if (s != COMMET_OK) return s;
   if (smem_bytes) *smem_bytes = q[0];
   if (ctas_per_sm) *ctas_per_sm = q[1];
   if (regs_per_thread) *regs_per_thread = q[2];
+  return COMMET_OK;
+}
+
+extern "C" commet_status commet_kernel_config(commet_ctx c, int32_t* threads_per_cta, int32_t* warp_specialised) {
+  if (!c) return fail(nullptr, COMMET_ERR_ARG, "ctx is NULL");
+  int q[5] = {0, 0, 0, 128, 0};
+  const commet_status s = kernel_query(c, q);
+  if (s != COMMET_OK) return s;
+  if (threads_per_cta) *threads_per_cta = q[3];
+  if (warp_specialised) *warp_specialised = q[4];
   return COMMET_OK;
 }
 

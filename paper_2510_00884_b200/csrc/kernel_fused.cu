@@ -70,6 +70,24 @@
 #ifndef COMMET_POST_PAR
 #define COMMET_POST_PAR 0  // stage 7a split over the four warps (post_qp_part): measured no gain (c3 +0.3 %, c4 +3 %: spills)
 #endif
+#ifndef COMMET_WS
+#define COMMET_WS 0  // warp-specialised kernel (ws_kernel) for the hex8 forward-sweep ICNN: measured c3 -2.2 %, c5 +4 % -> off
+#endif
+#ifndef COMMET_WS_NWE
+#define COMMET_WS_NWE 4  // element warps per CTA of the warp-specialised kernel (4: one warpgroup, setmaxnreg)
+#endif
+#ifndef COMMET_WS_NREG_NET
+#define COMMET_WS_NREG_NET 168  // registers of the network warpgroup after setmaxnreg (element: 256 - this)
+#endif
+#ifndef COMMET_ROWS3
+#define COMMET_ROWS3 1  // stage 7b: three A rows (i, J = 0..2) per item
+#endif
+#ifndef COMMET_ELEM_HALF
+#define COMMET_ELEM_HALF 0  // hex8 stage 8 of the one-role kernel: one warp per (element, i-half) (measured: c3 9.75 -> 9.83 ms; the warp-specialised kernel uses it)
+#endif
+#ifndef COMMET_WS_PAR7
+#define COMMET_WS_PAR7 0  // warp-specialised kernel: stage 7a split over the four element warps (measured: c3 9.52 -> 9.78 ms)
+#endif
 #ifndef COMMET_PINGPONG
 #define COMMET_PINGPONG 0  // measured neutral (c3 10.31 vs 10.26 ms): barriers kept
 #endif
@@ -93,6 +111,20 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                : "+d"(c[0]), "+d"(c[1])
                : "d"(a), "d"(b));
+}
+
+// CTA-wide barrier of the network stages: __syncthreads, or in the warp-specialised kernel the
+// named barrier 1 of the NTHR network threads (the element warps run their own schedule)
+template <class C>
+__device__ __forceinline__ void net_sync() {
+  if constexpr (C::WS)
+    asm volatile("bar.sync 1, %0;" ::"n"(C::NTHR) : "memory");
+  else
+    __syncthreads();
+}
+__device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void named_arrive(int id, int n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
 // L1 prefetch of the first NK k-steps of a warp's A fragments for the NEXT GEMM, issued at the
@@ -139,9 +171,15 @@ __device__ __forceinline__ double2 ldg2(const double* p) {
 // Gent-Thomas, evaluated per qp in stage 7a; W is then unused).  KIN_: 0 standard
 // invariants, 1 isochoric (compile-time, so the standard path carries no extra code)
 // MODE_: 0 = FE assembly; 1 = material points (F in; Psi, tau, c out; NEN = NQ = 1)
-template <int W_, int Q_, int NEN_, int NQ_, int MINB_ = 3, int NET_ = 0, int KIN_ = 0, int MODE_ = 0, int NW_ = 4>
+// WS_: warp-specialised kernel (ws_kernel): the NW_ network warps are joined by NWE element warps
+// that run stages 7-8 of batch b (and load the inputs of batch b + 2) while the network warps
+// compute batch b + 1; the network warps then synchronise among themselves with a named barrier
+template <int W_, int Q_, int NEN_, int NQ_, int MINB_ = 3, int NET_ = 0, int KIN_ = 0, int MODE_ = 0, int NW_ = 4,
+          int WS_ = 0>
 struct Cfg {
   static constexpr int W = W_, Q = Q_, NEN = NEN_, NQ = NQ_, NET = NET_, KIN = KIN_, MODE = MODE_;
+  static constexpr bool WS = WS_ != 0;
+  static constexpr int NWE = WS ? COMMET_WS_NWE : 0, NTHR_ALL = 32 * (NW_ + NWE);
   // network inputs per qp: 3 (standard / isochoric invariants) or 5 (anisotropic: + I4, I5)
   static constexpr int NK = KIN == 2 ? 5 : 3, NH = NK * (NK + 1) / 2;
   static constexpr int NP = NK + NH;  // adjoint-pass partials per qp: g (NK) and H_1 (NH)
@@ -418,7 +456,7 @@ __device__ __forceinline__ void fwd_sweep(const NcmDev& m, double* act, double* 
     for (int l = 2; l <= L; l++) {
       double acc[C::MT_J][4][2];
       warp_gemm<C::MT_J, 4, KT2, C::PD_J>(m.Wfrag + (l - 2) * frag_layer, mt0, act, LDA, ncol, acc);
-      __syncthreads();
+      net_sync<C>();
 #pragma unroll
       for (int i = 0; i < C::MT_J; i++) {
         const int j = (mt0 + i) * 8 + g;
@@ -454,7 +492,7 @@ __device__ __forceinline__ void fwd_sweep(const NcmDev& m, double* act, double* 
           }
         }
       }
-      __syncthreads();
+      net_sync<C>();
     }
 #pragma unroll
     for (int h = 0; h < 2; h++)
@@ -495,7 +533,7 @@ __device__ __forceinline__ void fwd_sweep(const NcmDev& m, double* act, double* 
       double acc[C::MT_V][C::NT_V][2];
       warp_gemm<C::MT_V, C::NT_V, KT2, C::PD_V>(m.Wfrag + (l - 2) * frag_layer + (size_t)W * W, mt0, act, LDA, ncol,
                                                acc);
-      __syncthreads();
+      net_sync<C>();
       if (l > 2) {  // l = 3: lambda_2 -> mu_2, and layer 2's Hessian term from s_2 (.) J_2
         double hb[C::NT_V][2][6];
 #pragma unroll
@@ -594,7 +632,7 @@ __device__ __forceinline__ void fwd_sweep(const NcmDev& m, double* act, double* 
               for (int x = 0; x < 9; x++) act[(vm * Q + ncol[jj] + 2 * t + h) * 9 + x] = pg[jj][h][x];
         }
       }
-      __syncthreads();
+      net_sync<C>();
     }
   }
   // ---- g = W1^T mu_1 + skip_out, H_1 -----------------------------------------------------
@@ -612,7 +650,7 @@ __device__ __forceinline__ void fwd_sweep(const NcmDev& m, double* act, double* 
 #pragma unroll
     for (int x = 0; x < 6; x++) qH[q * 6 + x] = v[3 + x];
   }
-  __syncthreads();
+  net_sync<C>();
 }
 
 // ---- stage 2: layer 1 (3 -> W), elementwise.  Each thread: one qp, neurons j0, j0 + NTHR/Q, ...
@@ -1296,6 +1334,7 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
 
     STAGE_MARK(7)
     // ---- stage 7b: A_q (81 entries, scaled by w), one (q, iJ) row per item ------------------
+    if constexpr (C::KIN == 2 || !COMMET_ROWS3) {
 #ifdef COMMET_EXP_SKIP_7B  // timing experiments only
     for (int it = tid; it < 0; it += C::NTHR) {
 #else
@@ -1306,6 +1345,10 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
         tangent_row_aniso(post + q * PS, iJ, qA + q * 81 + iJ * 9);
       else
         tangent_row(post + q * PS, iJ, qA + q * 81 + iJ * 9);
+    }
+    } else {  // three rows (i, J = 0..2) per item: the qp's factors loaded once for the three
+      for (int it = tid; it < Q * 3; it += C::NTHR)
+        tangent_rows_i(post + (it / 3) * PS, it % 3, qA + (it / 3) * 81 + (it % 3) * 27);
     }
     __syncthreads();
 
@@ -1318,6 +1361,53 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
     //      Y_q[J][b] = sum_L A_q[(i,J),(k,L)] dN_q[b][L] formed in the B fragment (3 FMA per
     //      element); M = a, N = b, K = (q, J); r_e; RED scatter (+ mirror for i < k)
     {
+      if constexpr (NEN == 8 && COMMET_ELEM_HALF) {
+      // hex8: one warp per (element, i-half), the (i, k) blocks (0,0) (0,1) (0,2) or (1,1) (1,2)
+      // (2,2) at once -- the dN/dX operands and the scatter metadata of the lane's node pair are
+      // loaded once for the three
+      constexpr int KS = NQ * 3 / 4;
+      for (int task = warp; task < ne * 2; task += C::NWARP) {
+        const int e = task >> 1, i0 = task & 1;
+        double c[3][2];
+#pragma unroll
+        for (int ik = 0; ik < 3; ik++) c[ik][0] = c[ik][1] = 0.0;
+#pragma unroll
+        for (int kt = 0; kt < KS; kt++) {
+          const int kk = 4 * kt + t, q = e * NQ + kk / 3, J = kk % 3;
+          const double* Gg = sgN + (q * NEN + g) * 3;  // node a = b_row = g of the fragments
+          const double g0 = Gg[0], g1 = Gg[1], g2 = Gg[2];
+          const double av = J == 0 ? g0 : (J == 1 ? g1 : g2);
+          const double* Aq = qA + q * 81 + J * 9;
+#pragma unroll
+          for (int ik = 0; ik < 3; ik++) {
+            const int i = i0 ? (ik < 2 ? 1 : 2) : 0;
+            const int k = i0 ? (ik < 2 ? ik + 1 : 2) : ik;
+            const double* Ar = Aq + i * 27 + 3 * k;
+            dmma(c[ik], av, Ar[0] * g0 + Ar[1] * g1 + Ar[2] * g2);
+          }
+        }
+        const int64_t el = e0 + e;
+        const int a = g;
+        const int64_t la = __ldg(A.lrow + el * NEN + a);
+        const int64_t rsa = __ldg(A.node_rs + la);
+        const int sa = 3 * __ldg(A.node_deg + la);
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+          const int b = 2 * t + h;
+          const int sab = 3 * (int)__ldg(A.slot + ((size_t)el * NEN + a) * NEN + b);
+          const int64_t lb = __ldg(A.lrow + el * NEN + b);
+          const int sb3 = 3 * __ldg(A.node_deg + lb);
+          const int64_t mb = __ldg(A.node_rs + lb) + 3 * (int)__ldg(A.slot + ((size_t)el * NEN + b) * NEN + a);
+#pragma unroll
+          for (int ik = 0; ik < 3; ik++) {
+            const int i = i0 ? (ik < 2 ? 1 : 2) : 0;
+            const int k = i0 ? (ik < 2 ? ik + 1 : 2) : ik;
+            atomicAdd(vout(A, la, rsa + i * sa + sab + k), c[ik][h]);
+            if (i < k) atomicAdd(vout(A, lb, mb + k * sb3 + i), c[ik][h]);
+          }
+        }
+      }
+      } else {
       constexpr int MTE = (NEN + 7) / 8, KS = NQ * 3 / 4;
       constexpr int NIK = 6;
       static_assert((NQ * 3) % 4 == 0, "k-steps");
@@ -1371,6 +1461,7 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
             }
           }
         }
+      }
       }
       // residual r_e[a][i] = sum_q P_q[i][:] . dN_q[a][:]
       for (int it = tid; it < ne * NEN * 3; it += C::NTHR) {
@@ -1460,6 +1551,363 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
 }
 
 // ---------------------------------------------------------------------------
+// Warp-specialised kernel (the forward-sweep ICNN path, assembly): per CTA, NW = 4 network warps
+// and NWE = 2 element warps in a three-slot pipeline.  Element warps: load the inputs of batch
+// b + 2 (dN/dX, u_e, w) into slot (b + 2) % 3, and run stages 7-8 (penalty, S, A_q, K_e, r_e,
+// scatter) of batch b from slot b % 3 -- while the network warps run stages 1-6 of batch b + 1.
+// Named barriers: 1 network-internal (net_sync), FULL[3] (network -> element: F, g, H of the
+// slot's batch are ready), EMPTY[3] (element -> network: the slot holds the next batch's inputs),
+// 8 element-internal.  Measured motivation (profiles/r02_ab_elem_breakdown.txt, r02_ab_pad2.txt):
+// in the one-role kernel the element stage adds 1.79 of 9.74 ms at c3 (it hardly overlaps the
+// other CTAs' network phases) while the network alone loses only 5.5 % at 2 instead of 3 CTAs/SM.
+// ---------------------------------------------------------------------------
+constexpr int kBarFull0 = 2, kBarEmpty0 = 5, kBarElem = 8;
+
+template <class C>
+struct WsSmem {
+  static constexpr int PS = 101;
+  static constexpr int GN = C::Q * C::NEN * 3, UE = C::E * C::NEN * 3;
+  // slot: dN/dX, u_e, w, F, (g, H)
+  static constexpr int SLOT = ((GN + UE + C::Q + C::Q * 9 + C::Q * 9) + 1) & ~1;
+  int act, sb, qk, qg, qH, hred, gsk, tab, slots, post, qA, qP, total;
+  __host__ __device__ WsSmem() {
+    int o = 0;
+    act = o; o += C::W * C::LDA;
+    sb = o; o += 2 * C::W * C::LDS;  // s_1, s_2 (L <= 3)
+    qk = o; o += C::Q * 3;
+    qg = o; o += C::Q * 3;
+    qH = o; o += C::Q * 6;
+    hred = o; o += (C::JMG + C::VMG) * C::Q * 6;
+    gsk = o; o += C::Q * 3;
+    tab = o; o += ActTab<C::TB_FWD>::SIZE;
+    o = (o + 1) & ~1;
+    slots = o; o += 3 * SLOT;
+    post = o; o += C::Q * PS;
+    qA = o; o += C::Q * 81;
+    qP = o; o += C::Q * 9;
+    total = o;
+  }
+  __device__ double* gN(double* sm, int s) const { return sm + slots + s * SLOT; }
+  __device__ double* ue(double* sm, int s) const { return sm + slots + s * SLOT + GN; }
+  __device__ double* wq(double* sm, int s) const { return sm + slots + s * SLOT + GN + UE; }
+  __device__ double* qF(double* sm, int s) const { return sm + slots + s * SLOT + GN + UE + C::Q; }
+  __device__ double* gH(double* sm, int s) const { return sm + slots + s * SLOT + GN + UE + C::Q + C::Q * 9; }
+};
+
+template <class C>
+__device__ __forceinline__ void ws_network(const AsmArgs& A, double* smem, int L, int64_t n_it) {
+  constexpr int Q = C::Q, NEN = C::NEN, NQ = C::NQ, E = C::E;
+  const WsSmem<C> sm;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const NcmDev& m = A.ncm;
+  double* act = smem + sm.act;
+  double* sb = smem + sm.sb;
+  double* qk = smem + sm.qk;
+  double* qg = smem + sm.qg;
+  double* qH = smem + sm.qH;
+  double* hred = smem + sm.hred;
+  double* gsk = smem + sm.gsk;
+  const double* stab = smem + sm.tab;
+  double trc_max = 0.0;
+  for (int64_t it = 0; it < n_it; it++) {
+    const int s = (int)(it % 3);
+    const int64_t e0 = A.el_begin + (blockIdx.x + it * gridDim.x) * E;
+    const int64_t rem = A.el_begin + A.el_count - e0;
+    const int ne = rem < E ? (int)rem : E;
+    named_sync(kBarEmpty0 + s, C::NTHR_ALL);  // the element warps have put this batch's inputs in slot s
+    // ---- stage 1: F, kinematics, k; det F flag ----------------------------------------------
+    if (tid < Q) {
+      const int q = tid, e = q / NQ;
+      const double* gq = sm.gN(smem, s) + q * NEN * 3;
+      const double* ue = sm.ue(smem, s) + e * NEN * 3;
+      double F[9];
+#pragma unroll
+      for (int i = 0; i < 3; i++)
+#pragma unroll
+        for (int J = 0; J < 3; J++) {
+          double v = (i == J) ? 1.0 : 0.0;
+#pragma unroll
+          for (int a = 0; a < NEN; a++) v += ue[a * 3 + i] * gq[a * 3 + J];
+          F[i * 3 + J] = v;
+        }
+      Kin kin;
+      kinematics(F, kin);
+      if (e < ne) {
+        if (!(kin.J > 0.0)) atomicMin(A.bad, (unsigned long long)(__ldg(A.orig + e0 + e) * NQ + q % NQ));
+        trc_max = fmax(trc_max, kin.I1);
+      }
+      double* qF = sm.qF(smem, s);
+#pragma unroll
+      for (int x = 0; x < 9; x++) qF[q * 9 + x] = F[x];
+      if constexpr (C::KIN == 1) {
+        double kb[3];
+        isochoric_inputs(kin, kb);
+        qk[q * 3 + 0] = kb[0];
+        qk[q * 3 + 1] = kb[1];
+        qk[q * 3 + 2] = kb[2];
+      } else {
+        qk[q * 3 + 0] = kin.I1 - 3.0;
+        qk[q * 3 + 1] = kin.I2 - 3.0;
+        qk[q * 3 + 2] = kin.J - 1.0;
+      }
+      gsk[q * 3] = gsk[q * 3 + 1] = gsk[q * 3 + 2] = 0.0;
+    }
+    net_sync<C>();
+    // ---- stages 2-6: layer 1, forward sweep, backward pass ----------------------------------
+#ifndef COMMET_EXP_SKIP_NCM  // (timing experiments only)
+    layer1<C, C::TB_FWD>(m, L, true, qk, act, sb, nullptr, nullptr, stab);
+    net_sync<C>();
+    if (L == 3)
+      fwd_sweep<C, 3>(m, act, sb, hred, qg, qH, gsk, stab, nullptr);
+    else
+      fwd_sweep<C, 2>(m, act, sb, hred, qg, qH, gsk, stab, nullptr);
+#endif
+    // ---- g, H (summed over the warp row groups) into the slot; hand the batch over ----------
+    if (tid < Q) {
+      const int q = tid;
+      double* gH = sm.gH(smem, s) + q * 9;
+#pragma unroll
+      for (int x = 0; x < 3; x++) gH[x] = qg[q * 3 + x];
+#pragma unroll
+      for (int x = 0; x < 6; x++) {
+        double v = qH[q * 6 + x];
+#pragma unroll
+        for (int r = 0; r < C::JMG; r++) v += hred[(r * Q + q) * 6 + x];
+        if (L == 3)
+#pragma unroll
+          for (int r = 0; r < C::VMG; r++) v += hred[((C::JMG + r) * Q + q) * 6 + x];
+        gH[3 + x] = v;
+      }
+    }
+    named_arrive(kBarFull0 + s, C::NTHR_ALL);
+  }
+  if (warp == 0) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) trc_max = fmax(trc_max, __shfl_xor_sync(0xffffffffu, trc_max, o));
+    if (lane == 0 && trc_max > 0.0) atomicMax(A.max_trc, (unsigned long long)__double_as_longlong(trc_max));
+  }
+}
+
+template <class C>
+__device__ __forceinline__ void ws_element(const AsmArgs& A, double* smem, int64_t n_it) {
+  constexpr int Q = C::Q, NEN = C::NEN, NQ = C::NQ, E = C::E, NTE = 32 * C::NWE, PS = WsSmem<C>::PS;
+  const WsSmem<C> sm;
+  const int etid = threadIdx.x - C::NTHR, ewarp = etid >> 5, lane = etid & 31, g = lane >> 2, t = lane & 3;
+  const NcmDev& m = A.ncm;
+  double* post = smem + sm.post;
+  double* qA = smem + sm.qA;
+  double* qP = smem + sm.qP;
+  // batch inputs: dN/dX (double2 chunks), the u gather through conn, w -- registers, then the slot
+  constexpr int NG2 = Q * NEN * 3 / 2, NU = E * NEN * 3;
+  constexpr int PG = (NG2 + NTE - 1) / NTE, PU = (NU + NTE - 1) / NTE, PW = (Q + NTE - 1) / NTE;
+  double2 rg[PG];
+  double ru[PU], rw[PW];
+  auto load = [&](int64_t it) {
+    const int64_t f0 = A.el_begin + (blockIdx.x + it * gridDim.x) * E;
+    const int64_t frem = A.el_begin + A.el_count - f0;
+    const int fne = frem < E ? (int)frem : E;
+    const double2* src = reinterpret_cast<const double2*>(A.gradN + (size_t)f0 * NQ * NEN * 3);
+    const int n2 = fne * NQ * NEN * 3 / 2;
+#pragma unroll
+    for (int i = 0; i < PG; i++) {
+      const int x = etid + i * NTE;
+      rg[i] = x < n2 ? __ldg(src + x) : make_double2(0.0, 0.0);
+    }
+    int cn[PU];
+#pragma unroll
+    for (int i = 0; i < PU; i++) {
+      const int x = etid + i * NTE;
+      const int e = x / (NEN * 3), ai = x % (NEN * 3);
+      cn[i] = (x < NU && e < fne) ? __ldg(A.conn + (f0 + e) * NEN + ai / 3) : -1;
+    }
+#pragma unroll
+    for (int i = 0; i < PU; i++) ru[i] = cn[i] >= 0 ? __ldg(A.u + 3 * (int64_t)cn[i] + (etid + i * NTE) % 3) : 0.0;
+#pragma unroll
+    for (int i = 0; i < PW; i++) {
+      const int x = etid + i * NTE;
+      rw[i] = x < fne * NQ ? __ldg(A.qp_w + f0 * NQ + x) : 0.0;
+    }
+  };
+  auto store = [&](int s) {
+    double2* dg = reinterpret_cast<double2*>(sm.gN(smem, s));
+#pragma unroll
+    for (int i = 0; i < PG; i++) {
+      const int x = etid + i * NTE;
+      if (x < NG2) dg[x] = rg[i];
+    }
+    double* du = sm.ue(smem, s);
+#pragma unroll
+    for (int i = 0; i < PU; i++) {
+      const int x = etid + i * NTE;
+      if (x < NU) du[x] = ru[i];
+    }
+    double* dw = sm.wq(smem, s);
+#pragma unroll
+    for (int i = 0; i < PW; i++) {
+      const int x = etid + i * NTE;
+      if (x < Q) dw[x] = rw[i];
+    }
+  };
+  for (int64_t it0 = 0; it0 < 2 && it0 < n_it; it0++) {
+    load(it0);
+    store((int)it0);
+    named_arrive(kBarEmpty0 + (int)it0, C::NTHR_ALL);
+  }
+  for (int64_t it = 0; it < n_it; it++) {
+    const int s = (int)(it % 3);
+    const int64_t e0 = A.el_begin + (blockIdx.x + it * gridDim.x) * E;
+    const int64_t rem = A.el_begin + A.el_count - e0;
+    const int ne = rem < E ? (int)rem : E;
+    const bool next = it + 2 < n_it;
+    if (next) load(it + 2);  // in flight during this batch's element stage
+    named_sync(kBarFull0 + s, C::NTHR_ALL);
+    const double* sgN = sm.gN(smem, s);
+#ifdef COMMET_EXP_SKIP_ELEM  // (timing experiments only)
+    if (false) {
+#endif
+    // ---- stage 7a: penalty, S, T, Phi_m, Psi_m, b, P (scaled by w), one thread per qp --------
+    //      with four element warps: warp = part of post_qp (post_qp_part), lane = qp
+    constexpr bool PAR = C::NWE == 4 && COMMET_WS_PAR7;
+#ifdef COMMET_EXP_SKIP_7A
+    if (false) {
+#else
+    if (PAR ? lane < Q : etid < Q) {
+#endif
+      const int q = PAR ? lane : etid;
+      const double* gH = sm.gH(smem, s) + q * 9;
+      double gq[3], H6[6];
+#pragma unroll
+      for (int x = 0; x < 3; x++) gq[x] = gH[x];
+#pragma unroll
+      for (int x = 0; x < 6; x++) H6[x] = gH[3 + x];
+      Kin kin;
+      kinematics(sm.qF(smem, s) + q * 9, kin);
+      if constexpr (C::KIN == 1) isochoric_to_standard(kin, gq, H6);
+      gq[2] += 2.0 * m.kappa * (kin.J - 1.0) - m.ref_shift;
+      H6[5] += 2.0 * m.kappa;
+      if constexpr (PAR)
+        post_qp_part(kin, gq, H6, sm.wq(smem, s)[q], post + q * PS, qP + q * 9, ewarp);
+      else
+        post_qp(kin, gq, H6, sm.wq(smem, s)[q], post + q * PS, qP + q * 9);
+    }
+    named_sync(kBarElem, NTE);
+    // ---- stage 7b: A_q, three rows (i, J = 0..2) per item ------------------------------------
+#ifndef COMMET_EXP_SKIP_7B
+    for (int x = etid; x < Q * 3; x += NTE) tangent_rows_i(post + (x / 3) * PS, x % 3, qA + (x / 3) * 81 + (x % 3) * 27);
+#endif
+    named_sync(kBarElem, NTE);
+    // ---- stage 8: K_ik[a][b] = sum_(q,J) dN_q[a][J] Y_q[J][b] (i <= k, DMMA), RED scatter ------
+    //      hex8: one warp per (element, i-half): the (i, k) blocks (0,0) (0,1) (0,2) or (1,1) (1,2)
+    //      (2,2) at once -- the dN/dX operands and the scatter metadata of the lane's node pair are
+    //      loaded once for the three
+    {
+      constexpr int KS = NQ * 3 / 4;
+      static_assert((NQ * 3) % 4 == 0 && NEN == 8, "k-steps / one 8x8 tile per (i, k) block");
+      for (int task = ewarp; task < ne * 2; task += C::NWE) {
+        const int e = task >> 1, i0 = task & 1;  // blocks (0,0..2) or (1,1..2),(2,2)
+        double c[3][2];
+#pragma unroll
+        for (int ik = 0; ik < 3; ik++) c[ik][0] = c[ik][1] = 0.0;
+#pragma unroll
+        for (int kt = 0; kt < KS; kt++) {
+          const int kk = 4 * kt + t, q = e * NQ + kk / 3, J = kk % 3;
+          const double* Gg = sgN + (q * NEN + g) * 3;  // node a = b_row = g of the fragments
+          const double g0 = Gg[0], g1 = Gg[1], g2 = Gg[2];
+          const double av = J == 0 ? g0 : (J == 1 ? g1 : g2);
+          const double* Aq = qA + q * 81 + J * 9;
+#pragma unroll
+          for (int ik = 0; ik < 3; ik++) {
+            const int i = i0 ? (ik < 2 ? 1 : 2) : 0;
+            const int k = i0 ? (ik < 2 ? ik + 1 : 2) : ik;
+            const double* Ar = Aq + i * 27 + 3 * k;
+#ifdef COMMET_EXP_SKIP_KE
+            c[ik][0] += Ar[0] * g0; c[ik][1] += av;
+#else
+            dmma(c[ik], av, Ar[0] * g0 + Ar[1] * g1 + Ar[2] * g2);
+#endif
+          }
+        }
+        const int64_t el = e0 + e;
+        const int a = g;
+#ifdef COMMET_EXP_SKIP_SCATTER
+        if (c[0][0] == 1234.5678 && c[2][1] == 8765.4321) A.v_own[0] = c[1][0];
+        if (false) {
+#else
+        {
+#endif
+        const int64_t la = __ldg(A.lrow + el * NEN + a);
+        const int64_t rsa = __ldg(A.node_rs + la);
+        const int sa = 3 * __ldg(A.node_deg + la);
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+          const int b = 2 * t + h;
+          const int sab = 3 * (int)__ldg(A.slot + ((size_t)el * NEN + a) * NEN + b);
+          const int64_t lb = __ldg(A.lrow + el * NEN + b);
+          const int sb3 = 3 * __ldg(A.node_deg + lb);
+          const int64_t mb = __ldg(A.node_rs + lb) + 3 * (int)__ldg(A.slot + ((size_t)el * NEN + b) * NEN + a);
+#pragma unroll
+          for (int ik = 0; ik < 3; ik++) {
+            const int i = i0 ? (ik < 2 ? 1 : 2) : 0;
+            const int k = i0 ? (ik < 2 ? ik + 1 : 2) : ik;
+            atomicAdd(vout(A, la, rsa + i * sa + sab + k), c[ik][h]);
+            if (i < k) atomicAdd(vout(A, lb, mb + k * sb3 + i), c[ik][h]);
+          }
+        }
+        }
+      }
+      // residual r_e[a][i] = sum_q P_q[i][:] . dN_q[a][:]
+      for (int x = etid; x < ne * NEN * 3; x += NTE) {
+        const int i = x % 3, a = (x / 3) % NEN, e = x / (3 * NEN);
+        double rr = 0.0;
+#pragma unroll
+        for (int qq = 0; qq < NQ; qq++) {
+          const int q = e * NQ + qq;
+          const double* ga = sgN + (q * NEN + a) * 3;
+          rr += qP[q * 9 + i * 3] * ga[0] + qP[q * 9 + i * 3 + 1] * ga[1] + qP[q * 9 + i * 3 + 2] * ga[2];
+        }
+        atomicAdd(rout(A, __ldg(A.lrow + (e0 + e) * NEN + a), i), rr);
+      }
+    }
+#ifdef COMMET_EXP_SKIP_ELEM
+    }
+#endif
+    // slot s is free for batch it + 3 once both element warps are past stage 8 (the next batch's
+    // 7a barrier orders that); the inputs of batch it + 2 go to slot (it + 2) % 3 now
+    if (next) {
+      store((int)((it + 2) % 3));
+      named_arrive(kBarEmpty0 + (int)((it + 2) % 3), C::NTHR_ALL);
+    }
+  }
+}
+
+template <class C>
+__global__ void __launch_bounds__(C::NTHR_ALL, C::MINB) ws_kernel(AsmArgs A) {
+  static_assert(C::WS && C::FWDC && C::NET == 0 && C::MODE == 0 && C::NK == 3 && C::NWARP == 4, "ws config");
+  extern __shared__ __align__(16) double smem[];
+  const WsSmem<C> sm;
+  const int L = A.ncm.L;
+  for (int x = threadIdx.x; x < ActTab<C::TB_FWD>::SIZE; x += C::NTHR_ALL)
+    smem[sm.tab + x] = __ldg(A.ncm.act_tab + act_tab_offset<C::TB_FWD>() + x);
+  __syncthreads();
+  const int64_t nb = (A.el_count + C::E - 1) / C::E;
+  const int64_t n_it = nb > blockIdx.x ? (nb - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  if constexpr (C::NWE == 4) {  // two warpgroups: move registers from the element to the network one
+    if (threadIdx.x < C::NTHR) {
+      asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(COMMET_WS_NREG_NET));
+      ws_network<C>(A, smem, L, n_it);
+    } else {
+      asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(256 - COMMET_WS_NREG_NET));
+      ws_element<C>(A, smem, n_it);
+    }
+  } else {
+    if (threadIdx.x < C::NTHR)
+      ws_network<C>(A, smem, L, n_it);
+    else
+      ws_element<C>(A, smem, n_it);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // host side: dispatch and weight fragments
 // ---------------------------------------------------------------------------
 
@@ -1506,17 +1954,14 @@ void fused_weight_frag_fill(int w, int L, const double* Wrow, double* out) {
   }
 }
 
-template <class C>
-static int launch_cfg(const AsmArgs& a, cudaStream_t st, int* launches) {
-  const Smem<C> sm(a.ncm.L, a.ncm.skip_h != nullptr);
-  size_t bytes = (size_t)sm.total * sizeof(double);
-#ifdef COMMET_EXP_SMEM_PAD
-  bytes += COMMET_EXP_SMEM_PAD;  // experiments only: limit resident CTAs per SM
-#endif
-  // per device: the shared-memory attribute, SM count and occupancy are queried once per
-  // (device, smem size) -- the host-side launch cost matters for small batches
-  // (several contexts on one device may launch from different host threads: the cache is
-  // read and updated under a lock, and a launch uses one consistent snapshot of it)
+// One launch of kernel `fn` (nthr threads, `bytes` of dynamic shared memory, E elements per
+// batch): a persistent grid of min(batches, SMs x resident CTAs).  The shared-memory attribute,
+// SM count and occupancy are queried once per (kernel, device, smem size) -- the host-side launch
+// cost matters for small batches -- under a lock (several contexts on one device may launch from
+// different host threads) and used as one consistent snapshot.
+template <class Tag>
+static int launch_persistent(void (*fn)(AsmArgs), int nthr, size_t bytes, int E, const AsmArgs& a, cudaStream_t st,
+                             int* launches, int kind = 0) {
   constexpr int kDev = 16;
   static std::mutex mu;
   static size_t attr_bytes[kDev] = {0};
@@ -1529,16 +1974,16 @@ static int launch_cfg(const AsmArgs& a, cudaStream_t st, int* launches) {
   {
     std::lock_guard<std::mutex> lk(mu);
     if (attr_bytes[dev] < bytes) {
-      cudaError_t e = cudaFuncSetAttribute(fused_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+      cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
       if (e != cudaSuccess) return (int)e;
       attr_bytes[dev] = bytes;
     }
     if (occ_bytes[dev] != bytes) {
-      int s = 0, ps = 0;
-      cudaError_t e = cudaDeviceGetAttribute(&s, cudaDevAttrMultiProcessorCount, dev);
-      if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, fused_kernel<C>, C::NTHR, bytes);
+      int sc = 0, ps = 0;
+      cudaError_t e = cudaDeviceGetAttribute(&sc, cudaDevAttrMultiProcessorCount, dev);
+      if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, fn, nthr, bytes);
       if (e != cudaSuccess) return (int)e;
-      sms_c[dev] = s;
+      sms_c[dev] = sc;
       per_sm_c[dev] = ps < 1 ? 1 : ps;
       occ_bytes[dev] = bytes;
     }
@@ -1547,27 +1992,51 @@ static int launch_cfg(const AsmArgs& a, cudaStream_t st, int* launches) {
   }
   if (a.query) {
     cudaFuncAttributes fa{};
-    cudaFuncGetAttributes(&fa, fused_kernel<C>);
+    cudaFuncGetAttributes(&fa, fn);
     a.query[0] = (int)bytes;
     a.query[1] = per_sm;
     a.query[2] = fa.numRegs;
+    a.query[3] = nthr;
+    a.query[4] = kind;  // 0 one-role fused kernel, 1 warp-specialised
     return 0;
   }
-  const int64_t nb = (a.el_count + C::E - 1) / C::E;
+  const int64_t nb = (a.el_count + E - 1) / E;
   const int64_t grid = std::min<int64_t>(nb, (int64_t)sms * per_sm);
   if (nb <= 0) return 0;
   if (grid <= 0) return (int)cudaErrorInvalidConfiguration;  // never a silent no-op with work to do
-  fused_kernel<C><<<(unsigned)grid, C::NTHR, bytes, st>>>(a);
+  fn<<<(unsigned)grid, nthr, bytes, st>>>(a);
   if (launches) (*launches)++;
   return (int)cudaGetLastError();
 }
 
-// COMMET_AB_MIN: tuning builds of the benchmark instantiations only (ICNN, standard inputs,
-// w = 64 / 128) -- a fraction of the compile time; never the product library
+template <class C>
+static int launch_cfg(const AsmArgs& a, cudaStream_t st, int* launches) {
+  const Smem<C> sm(a.ncm.L, a.ncm.skip_h != nullptr);
+  size_t bytes = (size_t)sm.total * sizeof(double);
+#ifdef COMMET_EXP_SMEM_PAD
+  bytes += COMMET_EXP_SMEM_PAD;  // experiments only: limit resident CTAs per SM
+#endif
+  return launch_persistent<C>(fused_kernel<C>, C::NTHR, bytes, C::E, a, st, launches);
+}
+
+// the warp-specialised kernel (forward-sweep ICNN path of the assembly)
+template <class C>
+struct WsTag {};
+template <class C>
+static int launch_ws(const AsmArgs& a, cudaStream_t st, int* launches) {
+  const size_t bytes = (size_t)WsSmem<C>().total * sizeof(double);
+  return launch_persistent<WsTag<C>>(ws_kernel<C>, C::NTHR_ALL, bytes, C::E, a, st, launches, 1);
+}
+
 template <int NEN, int NQ, int K>
 static int launch_k(const AsmArgs& a, cudaStream_t st, int* launches) {
 #ifdef COMMET_AB_MIN
   if constexpr (K == 0) {
+    if constexpr (NEN == 8 && COMMET_WS)
+      if (a.ncm.net == 0 && a.ncm.L >= 2 && a.ncm.L <= 3 && a.ncm.skip_h == nullptr) {
+        if (a.ncm.w == 64) return launch_ws<Cfg<64, 16, NEN, NQ, 2, 0, 0, 0, 4, 1>>(a, st, launches);
+        if (a.ncm.w == 128) return launch_ws<Cfg<128, 8, NEN, NQ, 2, 0, 0, 0, 4, 1>>(a, st, launches);
+      }
     if (a.ncm.net == 0 && a.ncm.w == 64) return launch_cfg<Cfg<64, 16, NEN, NQ, 3, 0, 0>>(a, st, launches);
     if (a.ncm.net == 0 && a.ncm.w == 128) return launch_cfg<Cfg<128, 8, NEN, NQ, 3, 0, 0>>(a, st, launches);
   }
@@ -1579,6 +2048,14 @@ static int launch_k(const AsmArgs& a, cudaStream_t st, int* launches) {
     if (a.ncm.net == 3)  // ICKAN: its per-qp forward mode needs the registers (4 CTAs/SM: spills, -14 %)
       return launch_cfg<Cfg<16, 32, NEN, NQ, COMMET_ICKAN_MINB, 1, K>>(a, st, launches);
     if (a.ncm.net != 0) return launch_cfg<Cfg<16, 16, NEN, NQ, COMMET_ANALYTIC_MINB, 1, K>>(a, st, launches);
+  }
+  // the forward-sweep ICNN (w = 64 / 128, L = 2 or 3, no hidden skips) on hex8: warp-specialised
+  // kernel (tet10 keeps the one-role kernel: its scalar element stage needs the aliased X buffer)
+  if constexpr (K != 2 && NEN == 8 && COMMET_WS) {
+    if (a.ncm.L >= 2 && a.ncm.L <= 3 && a.ncm.skip_h == nullptr) {
+      if (a.ncm.w == 64) return launch_ws<Cfg<64, 16, NEN, NQ, 2, 0, K, 0, 4, 1>>(a, st, launches);
+      if (a.ncm.w == 128) return launch_ws<Cfg<128, 8, NEN, NQ, 2, 0, K, 0, 4, 1>>(a, st, launches);
+    }
   }
   // 5-input ICNN: the Jacobian pass carries 5 columns and 15 Hessian partials -> 2 CTAs/SM
   constexpr int MB = K == 2 ? 2 : 3;

@@ -211,6 +211,48 @@ __device__ __forceinline__ void tangent_row(const double* __restrict__ post, int
   }
 }
 
+// Rows (i, J = 0..2) of w A (27 entries, out[J * 9 + kL]) -- tangent_row for three rows sharing
+// their loads (Psi_m, F^-T, b, T of the qp are read once for the three rows)
+__device__ __forceinline__ void tangent_rows_i(const double* __restrict__ post, int i, double* __restrict__ out) {
+  const double c2 = post[90], c3 = post[91];
+  double FiL[3], GiL[3], bik[3];
+#pragma unroll
+  for (int x = 0; x < 3; x++) {
+    FiL[x] = post[i * 3 + x];
+    GiL[x] = post[9 + i * 3 + x];
+    bik[x] = post[81 + i * 3 + x];
+  }
+  double p[3][3];
+#pragma unroll
+  for (int J = 0; J < 3; J++) {
+    p[J][0] = post[27 + i * 3 + J];
+    p[J][1] = post[36 + i * 3 + J];
+    p[J][2] = post[45 + i * 3 + J];
+  }
+#pragma unroll
+  for (int kk = 0; kk < 3; kk++) {
+    double FkJ[3], GkJ[3];
+#pragma unroll
+    for (int J = 0; J < 3; J++) {
+      FkJ[J] = post[kk * 3 + J];
+      GkJ[J] = post[9 + kk * 3 + J];
+    }
+#pragma unroll
+    for (int L = 0; L < 3; L++) {
+      const int kL = kk * 3 + L;
+      const double s0 = post[54 + kL], s1 = post[63 + kL], s2 = post[72 + kL];
+#pragma unroll
+      for (int J = 0; J < 3; J++) {
+        double v = p[J][0] * s0 + p[J][1] * s1 + p[J][2] * s2;
+        v += c2 * FiL[L] * FkJ[J] + c3 * GiL[L] * GkJ[J];
+        if (J == L) v += c2 * bik[kk];
+        if (i == kk) v += post[18 + J * 3 + L];
+        out[J * 9 + kL] = v;
+      }
+    }
+  }
+}
+
 // Whole tangent of one qp (simple kernel): P[9] and A[81], both scaled by w.
 __device__ __forceinline__ void stress_tangent(const Kin& k, const double* __restrict__ g,
                                                const double* __restrict__ H6, double w,

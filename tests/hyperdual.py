@@ -160,11 +160,17 @@ def energy_hd(F: list, ncm: dict):
          - F[0][2] * F[1][1] * F[2][0] - F[0][0] * F[1][2] * F[2][1] - F[0][1] * F[1][0] * F[2][2])
     k = [I1 - 3.0, I2 - 3.0, J - 1.0]
     if ncm.get("kinematics", "standard") == "anisotropic":
-        a0 = ncm["a0"]
-        CA = [sum((Cm[I][J] * a0[J] for J in range(3)), HD(0.0)) for I in range(3)]
-        I4 = sum((a0[I] * CA[I] for I in range(3)), HD(0.0))
-        I5 = sum((CA[I] * CA[I] for I in range(3)), HD(0.0))
-        k = [I1 - 3.0, I2 - 3.0, J - 1.0, I4 - 1.0, I5 - 1.0]
+        # Eq. standard-inv-II: I4,ij = A_i . C A_j, I5,ij = A_i . C^2 A_j over the pairs i <= j
+        # of the structural vectors; inputs I4,ij - A_i.A_j, I5,ij - A_i.A_j (zero at F = I)
+        vecs = [np.asarray(ncm["a0"], float)] + ([np.asarray(ncm["a1"], float)] if ncm.get("a1") is not None else [])
+        CAs = [[sum((Cm[I][Jx] * v[Jx] for Jx in range(3)), HD(0.0)) for I in range(3)] for v in vecs]
+        k = [I1 - 3.0, I2 - 3.0, J - 1.0]
+        for i in range(len(vecs)):
+            for j in range(i, len(vecs)):
+                aa = float(vecs[i] @ vecs[j])
+                I4 = sum((vecs[i][I] * CAs[j][I] for I in range(3)), HD(0.0))
+                I5 = sum((CAs[i][I] * CAs[j][I] for I in range(3)), HD(0.0))
+                k += [I4 - aa, I5 - aa]
     if ncm.get("kinematics", "standard") == "isochoric":
         a23 = hd_pow(J, -2.0 / 3.0)
         k = [a23 * I1 - 3.0, a23 * a23 * I2 - 3.0, J - 1.0]

@@ -46,6 +46,17 @@ VARIANTS = {
 }
 
 
+def _icnn_skips(w, L):
+    m = ncm_weights(w, L, 0.3, 15, 10.0)
+    rng = np.random.default_rng(16)
+    m["skip_out"] = rng.normal(0, 0.3, 3)
+    m["skip_hidden"] = rng.normal(0, 0.3, (L - 1, w, 3))
+    return m
+
+
+VARIANTS_EXTRA = {"icnn_skips_64x3": lambda: _icnn_skips(64, 3)}
+
+
 def _mesh(elem_type, n):
     if elem_type == HEX8:
         X, conn = hex_mesh(n, 0.1, seed=5)
@@ -125,18 +136,34 @@ def test_kernel_info_reports_launched_instantiation(pc):
     <= 168; the analytic networks allocate no ICNN buffers (less shared memory than the
     ICNN of the same qp count); the query launches nothing (outputs untouched)."""
     mesh, u = _mesh(HEX8, 2)
+    tmesh, tu = _mesh(TET10, 2)
     info = {}
     for name, ncm in (("icnn", ncm_weights(64, 3, 0.3, 1, 10.0)), ("cann", VARIANTS["cann_standard"]()),
-                      ("cann5", VARIANTS["cann_anisotropic"]()), ("icnn5", VARIANTS["icnn_anisotropic_64x3"]())):
-        lib = pc.Commet(mesh, ncm)
+                      ("cann5", VARIANTS["cann_anisotropic"]()), ("icnn5", VARIANTS["icnn_anisotropic_64x3"]()),
+                      ("icnn_tet", ncm_weights(64, 3, 0.3, 1, 10.0)), ("icnn_skips", VARIANTS_EXTRA["icnn_skips_64x3"]())):
+        m_, u_ = (tmesh, tu) if name == "icnn_tet" else (mesh, u)
+        lib = pc.Commet(m_, ncm)
         r, v = lib.alloc_outputs()
         r.fill_(7.0)
         info[name] = lib.kernel_info()
         torch.cuda.synchronize()
         assert (r == 7.0).all()
-        lib.assemble(torch.from_numpy(u).cuda(), r, v)
+        lib.assemble(torch.from_numpy(u_).cuda(), r, v)
         assert lib.check() == -1
-    assert info["icnn"]["ctas_per_sm"] == 3 and info["icnn"]["regs_per_thread"] <= 168
+    # hex8 forward-sweep ICNN: the one-role kernel (3 x 128 threads per SM at <= 168 registers), or in
+    # a COMMET_WS build the warp-specialised kernel (2 x 256 threads, 128 registers at launch); tet10
+    # and the 3-pass path (hidden skips): always the one-role kernel
+    if info["icnn"]["warp_specialised"]:
+        assert info["icnn"]["threads_per_cta"] == 256 and info["icnn"]["ctas_per_sm"] == 2
+    else:
+        assert info["icnn"]["threads_per_cta"] == 128 and info["icnn"]["ctas_per_sm"] == 3
+        assert info["icnn"]["regs_per_thread"] <= 168
+    for nm in ("icnn_tet", "icnn_skips"):
+        assert not info[nm]["warp_specialised"] and info[nm]["threads_per_cta"] == 128
+        assert info[nm]["regs_per_thread"] <= 168
+    # tet10 takes the forward sweep (3 CTAs/SM); the 3-pass fallback of the same w = 64 instantiation
+    # (hidden skips) keeps the forward sweep's wider act rows: 2 CTAs/SM
+    assert info["icnn_tet"]["ctas_per_sm"] == 3 and info["icnn_skips"]["ctas_per_sm"] >= 2
     assert info["icnn5"]["ctas_per_sm"] == 2 and info["icnn5"]["regs_per_thread"] > 168
     assert info["cann5"]["ctas_per_sm"] == 2 and info["cann5"]["regs_per_thread"] > 168
     assert info["cann"]["ctas_per_sm"] >= 3 and info["cann"]["smem_bytes"] < info["icnn"]["smem_bytes"]

@@ -9,7 +9,7 @@ import numpy as np
 import pytest
 
 import oracle
-from synth.gen import (anisotropic, cann_params, gent_thomas_params, hex_mesh, ickan_params, ncm_weights,
+from synth.gen import (A_FIBRE, A_SHEET, anisotropic, cann_params, gent_thomas_params, hex_mesh, ickan_params, ncm_weights,
                        shape_gradients)
 from tests import hyperdual
 from tests.test_oracle_material import I3, rand_F, rot
@@ -31,6 +31,10 @@ VARIANTS = {
     "cann_anisotropic": lambda: anisotropic(cann_params(4, seed=6, n_in=5)),
     "ickan_anisotropic": lambda: anisotropic(ickan_params((5, 4, 1), nb=7, seed=7)),
     "icnn_anisotropic": lambda: anisotropic(ncm_weights(8, 2, 0.3, 13, 10.0, n_in=5)),
+    # two structural vectors (fibre + sheet; pairs 00, 01, 11: 9 inputs), and a non-orthogonal pair
+    "cann_two_vectors": lambda: anisotropic(cann_params(3, seed=8, n_in=9), A_FIBRE, A_SHEET),
+    "ickan_two_vectors": lambda: anisotropic(ickan_params((9, 4, 1), nb=7, seed=9), A_FIBRE, A_SHEET),
+    "icnn_two_vectors": lambda: anisotropic(ncm_weights(8, 2, 0.3, 17, 10.0, n_in=9), A_FIBRE, (0.0, 0.6, 0.8)),
 }
 
 
@@ -208,3 +212,49 @@ def test_unsupported_network_kinematics_raise(bad):
     for mode in (0, 1):
         with pytest.raises(oracle.OracleError, match="inner network"):
             oracle.assemble(m, X.shape[0], conn, gN, w, u, rp, ci, mode=mode)
+
+
+
+def test_two_vector_invariants_closed_form():
+    """Eq. standard-inv-II for i != j on a closed form: the simple shear F = I + gamma
+    e1 (x) e2 with A0 = e1, A1 = e2 gives C = [[1, g, 0], [g, 1 + g^2, 0], [0, 0, 1]], so
+    I4,01 = C_12 = gamma and I5,01 = (C^2)_12 = 2 gamma + gamma^3 (and I4,00 = 1, I5,00 = 1 +
+    gamma^2, I4,11 = 1 + gamma^2, I5,11 = gamma^2 + (1 + gamma^2)^2); S from the definition
+    S = 2 sum_m g_m dK_m/dC with dI4,ij/dC = sym(A_i (x) A_j), dI5,ij/dC = sym(A_i (x) C A_j +
+    C A_i (x) A_j)."""
+    e1, e2 = np.array([1.0, 0, 0]), np.array([0, 1.0, 0])
+    m = anisotropic(cann_params(3, seed=10, n_in=9), e1, e2)
+    gam = 0.3
+    F = np.eye(3) + gam * np.outer(e1, e2)
+    C = F.T @ F
+    C2 = C @ C
+    k = np.array([np.trace(C) - 3.0, 0.5 * (np.trace(C) ** 2 - np.trace(C2)) - 3.0, np.linalg.det(F) - 1.0,
+                  0.0, gam ** 2, gam, 2 * gam + gam ** 3, gam ** 2, gam ** 2 + (1 + gam ** 2) ** 2 - 1.0])
+    assert abs(C[0, 1] - gam) < 1e-15 and abs(C2[0, 1] - (2 * gam + gam ** 3)) < 1e-15
+    _, g_ref, _ = oracle.ncm_eval_n(m, k)
+    o = oracle.material_point(dict(m, kappa=0.0), F)
+    sym = lambda X: 0.5 * (X + X.T)
+    Ci = np.linalg.inv(C)
+    h = [np.eye(3), np.trace(C) * np.eye(3) - C, 0.5 * np.linalg.det(F) * Ci]
+    for a, b in ((e1, e1), (e1, e2), (e2, e2)):
+        h += [sym(np.outer(a, b)), sym(np.outer(a, C @ b) + np.outer(C @ a, b))]
+    S = 2 * sum(g_ref[i] * h[i] for i in range(9))
+    assert np.abs(o["S"] - S).max() < 1e-13 * np.abs(S).max()
+    # objectivity: a rotation leaves every input at 0
+    Q, _ = np.linalg.qr(np.random.default_rng(3).normal(size=(3, 3)))
+    Q *= np.sign(np.linalg.det(Q))
+    assert np.abs(oracle.material_point(dict(m, kappa=0.0), Q)["k"]).max() < 1e-14
+
+
+def test_two_vectors_reduce_to_one():
+    """With A1 = A0 every pair repeats the single-vector invariants: a CANN whose branches on the
+    01 and 11 inputs have zero output weights gives the one-vector model exactly."""
+    m1 = anisotropic(cann_params(3, seed=11, n_in=5), A_FIBRE)
+    m2 = anisotropic(cann_params(3, seed=11, n_in=9), A_FIBRE, A_FIBRE)
+    for key in ("cann_f", "cann_w1", "cann_w2"):
+        m2[key] = np.concatenate([m1[key], m1[key][3:5], m1[key][3:5]])
+    m2["cann_w2"][5:] = 0.0
+    F = I3 + 0.08 * np.random.default_rng(4).normal(size=(3, 3))
+    o1, o2 = oracle.material_point(m1, F), oracle.material_point(m2, F)
+    assert abs(o1["W"] - o2["W"]) < 1e-14 * abs(o1["W"])
+    assert np.abs(o1["A"] - o2["A"]).max() < 1e-13 * np.abs(o1["A"]).max()
