@@ -132,11 +132,16 @@ typedef struct {
   const double* kan_grid;      /* host [R][2]: xmin, xmax of layer r's inputs */
   const double* kan_w;         /* host [edges]: spline weights, edges in (r, i, j) order */
   const double* kan_c;         /* host [edges][kan_nb]: control points */
-  /* COMMET_KIN_ANISOTROPIC: one structural vector A0 (reference configuration); the network
-   * inputs are k = (I1-3, I2-3, J-1, I4-1, I5-1), I4 = A0.C A0, I5 = A0.C^2 A0 (App. A.2.1,
-   * PAPER.md:810-826) -- ICNN (W1 [w][5]), CANN (cann_* arrays over 5 inputs) or ICKAN
-   * (kan_width[0] = 5); not Gent-Thomas (COMMET_ERR_ARG). */
+  /* COMMET_KIN_ANISOTROPIC: n_sv structural vectors A_v (reference configuration): a0, and a1
+   * when n_sv = 2 (n_sv 0 or 1: a0 only).  The network inputs are k = (I1-3, I2-3, J-1, then for
+   * each pair i <= j in the order (0,0), (0,1), (1,1): I4,ij - A_i.A_j, I5,ij - A_i.A_j) with
+   * I4,ij = A_i.C A_j, I5,ij = A_i.C^2 A_j (Eq. standard-inv-II; App. A.2.1 table,
+   * PAPER.md:810-826; readings R27, R28) -- 5 inputs for one vector (I4-1, I5-1 for a
+   * unit A0): ICNN (W1 [w][5]), CANN (cann_* arrays over 5 inputs) or ICKAN (kan_width[0] = 5);
+   * 9 inputs for two: CANN or ICKAN (an ICNN on 9 inputs: COMMET_ERR_ARG); never Gent-Thomas. */
   double a0[3];
+  int32_t n_sv;
+  double a1[3];
 } commet_ncm_desc;
 
 enum { COMMET_KIN_STANDARD = 0, COMMET_KIN_ISOCHORIC = 1, COMMET_KIN_ANISOTROPIC = 2 };

@@ -59,7 +59,7 @@ class NcmDesc(C.Structure):
                 ("cann_f", C.c_void_p), ("cann_w1", C.c_void_p), ("cann_w2", C.c_void_p),
                 ("gt", C.c_double * 3), ("kan_layers", C.c_int32), ("kan_width", C.c_void_p),
                 ("kan_nb", C.c_int32), ("kan_k", C.c_int32), ("kan_grid", C.c_void_p), ("kan_w", C.c_void_p),
-                ("kan_c", C.c_void_p), ("a0", C.c_double * 3)]
+                ("kan_c", C.c_void_p), ("a0", C.c_double * 3), ("n_sv", C.c_int32), ("a1", C.c_double * 3)]
 
 
 KIN_STANDARD, KIN_ISOCHORIC, KIN_ANISOTROPIC = 0, 1, 2
@@ -88,7 +88,9 @@ def ncm_desc(ncm: dict):
                  (C.c_double * 3)(*(gt if gt is not None else (0.0, 0.0, 0.0))),
                  0 if kw is None else kw.size - 1, _ptr(kw), int(ncm.get("kan_nb", 0)), int(ncm.get("kan_k", 3)),
                  _ptr(arrs["kan_grid"]), _ptr(arrs["kan_w"]), _ptr(arrs["kan_c"]),
-                 (C.c_double * 3)(*(ncm.get("a0") if ncm.get("a0") is not None else (0.0, 0.0, 0.0))))
+                 (C.c_double * 3)(*(ncm.get("a0") if ncm.get("a0") is not None else (0.0, 0.0, 0.0))),
+                 2 if ncm.get("a1") is not None else 1,
+                 (C.c_double * 3)(*(ncm.get("a1") if ncm.get("a1") is not None else (0.0, 0.0, 0.0))))
     return nd, [arrs, cf, kw]
 
 

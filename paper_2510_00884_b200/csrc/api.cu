@@ -40,9 +40,16 @@ extern "C" commet_status commet_setup(const commet_mesh_desc* mesh, const commet
   const int net = ncm->network, kin = ncm->kinematics;
   if (kin != COMMET_KIN_STANDARD && kin != COMMET_KIN_ISOCHORIC && kin != COMMET_KIN_ANISOTROPIC)
     return fail(C, COMMET_ERR_ARG, "kinematics %d unknown", kin);
-  const int nk = kin == COMMET_KIN_ANISOTROPIC ? 5 : 3;  // network inputs
-  if (nk == 5 && net == COMMET_NET_GENT_THOMAS)
-    return fail(C, COMMET_ERR_ARG, "anisotropic kinematics need an ICNN, CANN or ICKAN inner network (5 inputs)");
+  // anisotropic: one structural vector (a0; n_sv 0 or 1) -> 5 inputs, two (a0, a1) -> 9 inputs
+  const int n_sv = kin == COMMET_KIN_ANISOTROPIC ? (ncm->n_sv > 1 ? ncm->n_sv : 1) : 0;
+  if (kin == COMMET_KIN_ANISOTROPIC && (ncm->n_sv < 0 || ncm->n_sv > 2))
+    return fail(C, COMMET_ERR_ARG, "n_sv %d not in 0..2 (structural vectors)", ncm->n_sv);
+  const int nk = n_sv == 2 ? 9 : (n_sv == 1 ? 5 : 3);  // network inputs
+  if (nk > 3 && net == COMMET_NET_GENT_THOMAS)
+    return fail(C, COMMET_ERR_ARG, "anisotropic kinematics need an ICNN, CANN or ICKAN inner network (%d inputs)", nk);
+  if (nk == 9 && net == COMMET_NET_ICNN)
+    return fail(C, COMMET_ERR_ARG, "two structural vectors (9 inputs): CANN or ICKAN inner network (the ICNN kernels "
+                "take up to 5 inputs)");
   if (net != COMMET_NET_ICNN && net != COMMET_NET_CANN && net != COMMET_NET_GENT_THOMAS && net != COMMET_NET_ICKAN)
     return fail(C, COMMET_ERR_ARG, "network %d unknown", net);
   // analytic networks use no hidden layers (the ICNN fields are ignored)
@@ -192,7 +199,9 @@ extern "C" commet_status commet_setup(const commet_mesh_desc* mesh, const commet
                   net == COMMET_NET_CANN ? ncm->cann_n : 0, c->cann_f.p, c->cann_w1.p, c->cann_w2.p,
                   {ncm->gt[0], ncm->gt[1], ncm->gt[2]},
                   net == COMMET_NET_ICKAN ? ncm->kan_layers : 0, net == COMMET_NET_ICKAN ? ncm->kan_nb : 0,
-                  {0, 0, 0, 0, 0}, c->kan_grid.p, c->kan_w.p, c->kan_c.p, {ncm->a0[0], ncm->a0[1], ncm->a0[2]}};
+                  {0, 0, 0, 0, 0}, c->kan_grid.p, c->kan_w.p, c->kan_c.p, {ncm->a0[0], ncm->a0[1], ncm->a0[2]},
+                  {n_sv == 2 ? ncm->a1[0] : 0.0, n_sv == 2 ? ncm->a1[1] : 0.0, n_sv == 2 ? ncm->a1[2] : 0.0}};
+  if (n_sv == 2) c->ncm.kin = 3;  // internal: anisotropic with two structural vectors
   if (net == COMMET_NET_ICKAN)
     for (int r = 0; r <= ncm->kan_layers; r++) c->ncm.kan_width[r] = ncm->kan_width[r];
   CUDA_TRY(C, c->bad.alloc(1));
@@ -330,6 +339,9 @@ extern "C" commet_status commet_assemble(commet_ctx c, const double* u, double* 
   a.v_halo = c->v_halo.p;
   a.bad = c->bad.p;
   a.max_trc = c->max_trc.p;
+  a.dbg_nnz = p.nnz;
+  a.dbg_nnz_halo = p.nnz_halo;
+  a.dbg_n_halo = p.n_halo;
   if (c->peer) {
     a.peer = 1;
     a.halo_peer = c->halo_peer.p;

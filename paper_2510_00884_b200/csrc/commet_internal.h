@@ -42,6 +42,7 @@ struct NcmDev {
   const double* kan_w;     // [edges]
   const double* kan_c;     // [edges][nb]
   double a0[3];            // anisotropic kinematics: structural vector (reference configuration)
+  double a1[3];            // anisotropic kinematics, two vectors (kin 3): the second structural vector
 };
 
 struct AsmArgs {
@@ -79,6 +80,8 @@ struct AsmArgs {
   // launch query: when set, the dispatcher writes the chosen instantiation's {smem bytes,
   // CTAs per SM, registers per thread} here and launches nothing (commet_kernel_info)
   int* query;
+  // debug builds (COMMET_DEBUG_CHECKS): buffer sizes for the scatter bounds checks
+  int64_t dbg_nnz, dbg_nnz_halo, dbg_n_halo;
 };
 
 // launchers (kernel_simple.cu / kernel_fused.cu); return cudaError_t as int

@@ -149,11 +149,23 @@ __device__ __forceinline__ void frag_prefetch(const double* __restrict__ Af, int
 // P2P): halo rows go straight to the owning rank's buffers through the owner's receive maps,
 // replacing the NCCL exchange + unpack.
 __device__ __forceinline__ double* vout(const AsmArgs& A, int64_t la, int64_t off) {
+#ifdef COMMET_DEBUG_CHECKS  // debug builds: every scatter address inside its buffer
+  if (la < 0 || off < 0 || (la < A.n_owned ? off >= A.dbg_nnz : off >= A.dbg_nnz_halo)) {
+    printf("commet debug: CSR scatter out of range (row node %lld, offset %lld)\n", (long long)la, (long long)off);
+    __trap();
+  }
+#endif
   if (la < A.n_owned) return A.v_own + off;
   if (!A.peer) return A.v_halo + off;
   return A.peer_v[__ldg(A.halo_peer + (la - A.n_owned))] + __ldg(A.peer_vmap + off);
 }
 __device__ __forceinline__ double* rout(const AsmArgs& A, int64_t la, int i) {
+#ifdef COMMET_DEBUG_CHECKS
+  if (la < 0 || i < 0 || i > 2 || la >= A.n_owned + A.dbg_n_halo) {
+    printf("commet debug: residual scatter out of range (row node %lld)\n", (long long)la);
+    __trap();
+  }
+#endif
   if (la < A.n_owned) return A.r_own + 3 * la + i;
   const int64_t hr = 3 * (la - A.n_owned) + i;
   if (!A.peer) return A.r_halo + hr;
@@ -181,7 +193,9 @@ struct Cfg {
   static constexpr bool WS = WS_ != 0;
   static constexpr int NWE = WS ? COMMET_WS_NWE : 0, NTHR_ALL = 32 * (NW_ + NWE);
   // network inputs per qp: 3 (standard / isochoric invariants) or 5 (anisotropic: + I4, I5)
-  static constexpr int NK = KIN == 2 ? 5 : 3, NH = NK * (NK + 1) / 2;
+  // (KIN 2: one structural vector, 5 inputs; KIN 3: two vectors, 9 inputs -- App. A.2.1)
+  static constexpr int NSV = KIN == 3 ? 2 : 1;
+  static constexpr int NK = KIN == 2 ? 5 : (KIN == 3 ? 9 : 3), NH = NK * (NK + 1) / 2;
   static constexpr int NP = NK + NH;  // adjoint-pass partials per qp: g (NK) and H_1 (NH)
   static constexpr int NWARP = NW_, NTHR = 32 * NW_;
   static constexpr int MINB = MINB_;               // CTAs per SM the register budget targets (3: <= 168 regs)
@@ -225,7 +239,7 @@ struct Cfg {
 template <class C>
 struct Smem {
   // per-qp stride of the stage-7a outputs (odd: bank spread); anisotropic: 5 factor pairs
-  static constexpr int PS = C::KIN == 2 ? kPostAniso : 101;
+  static constexpr int PS = C::KIN == 3 ? kPostAniso2 : (C::KIN == 2 ? kPostAniso : 101);
   int act, sb, cb, qF, qk, qg, qH, hred, gsk, gN, ue, wq, qN, tab, qP, post, X, qA, total;
   // fwd: the forward-sweep path runs (C::FWDC, 2 <= L <= 3, no hidden skips): no c buffers
   __host__ __device__ static bool fwd_path(int L, bool skips) { return C::FWDC && L >= 2 && L <= 3 && !skips; }
@@ -365,8 +379,8 @@ __device__ __forceinline__ void material_outputs(const AsmArgs& A, const NcmDev&
     const double Wv = N + m.kappa * jm1 * jm1 - m.ref_shift * jm1;
     gq[2] += 2.0 * m.kappa * jm1 - m.ref_shift;
     H6[packed_index(C::NK, 2, 2)] += 2.0 * m.kappa;
-    if constexpr (C::KIN == 2)
-      post_qp_aniso(kin, m.a0, gq, H6, 1.0, post + q * PS, qP + q * 9);
+    if constexpr (C::KIN >= 2)
+      post_qp_aniso<C::NSV>(kin, m.a0, m.a1, gq, H6, 1.0, post + q * PS, qP + q * 9);
     else
       post_qp(kin, gq, H6, 1.0, post + q * PS, qP + q * 9);
     double tau[9];
@@ -389,8 +403,8 @@ __device__ __forceinline__ void material_outputs(const AsmArgs& A, const NcmDev&
   if (!A.c_out) return;
   for (int it = tid; it < Q * 9; it += C::NTHR) {
     const int q = it / 9, iJ = it % 9;
-    if constexpr (C::KIN == 2)
-      tangent_row_aniso(post + q * PS, iJ, qA + q * 81 + iJ * 9);
+    if constexpr (C::KIN >= 2)
+      tangent_row_aniso<C::NSV>(post + q * PS, iJ, qA + q * 81 + iJ * 9);
     else
       tangent_row(post + q * PS, iJ, qA + q * 81 + iJ * 9);
   }
@@ -807,6 +821,19 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
     const int64_t rem = A.el_begin + A.el_count - e0;
     const int ne = rem < E ? (int)rem : E;
     int cur = 0;  // act column block holding the current layer's input (value / adjoint passes)
+#ifdef COMMET_DEBUG_CHECKS
+    // race / stale-read check (debug builds, tools/race_check.py): every shared buffer except the
+    // activation tables is poisoned with NaN before each batch, so a read that is not ordered after
+    // this batch's write of the same word (a missing barrier, a wrong alias) returns NaN instead of
+    // a plausible stale value and shows in the outputs
+    {
+      const int t0 = sm.tab, t1 = sm.tab + (fwd ? ActTab<C::TB_FWD>::SIZE : ActTab<6>::SIZE);
+      __syncthreads();
+      for (int x = tid; x < sm.total; x += C::NTHR)
+        if (x < t0 || x >= t1) smem[x] = __longlong_as_double(0x7ff8deaddeadbeefLL);
+      __syncthreads();
+    }
+#endif
 
     // ---- stage 0: stage element inputs --------------------------------------------
     if constexpr (C::MODE == 1) {  // material points: F rows (tail points get F = I)
@@ -870,11 +897,11 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
       }
 #pragma unroll
       for (int x = 0; x < 9; x++) qF[q * 9 + x] = F[x];
-      if constexpr (C::KIN == 2) {  // anisotropic inputs (+ I4, I5)
-        double kb[5];
-        anisotropic_inputs(kin, m.a0, kb);
+      if constexpr (C::KIN >= 2) {  // anisotropic inputs (+ I4,ij, I5,ij per vector pair)
+        double kb[C::NK];
+        anisotropic_inputs<C::NSV>(kin, m.a0, m.a1, kb);
 #pragma unroll
-        for (int x = 0; x < 5; x++) qk[q * 5 + x] = kb[x];
+        for (int x = 0; x < C::NK; x++) qk[q * C::NK + x] = kb[x];
       } else if constexpr (C::KIN == 1) {  // isochoric inputs (App. A.2.2)
         double kb[3];
         isochoric_inputs(kin, kb);
@@ -889,7 +916,9 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
 #pragma unroll
       for (int x = 0; x < C::NK; x++) gsk[q * C::NK + x] = 0.0;
     }
+#if !defined(COMMET_DEBUG_DROP) || COMMET_DEBUG_DROP != 2  // (planted race: tools/race_check.py)
     __syncthreads();
+#endif
     STAGE_MARK(1)
 
 #ifdef COMMET_EXP_SKIP_NCM
@@ -1292,7 +1321,7 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
 #endif
     // ICNN, 3 inputs: four warps cooperate (warp = part of post_qp, lane = qp); otherwise one
     // thread per qp
-    constexpr bool PAR7 = COMMET_POST_PAR && C::NET == 0 && C::KIN != 2 && C::NWARP == 4;
+    constexpr bool PAR7 = COMMET_POST_PAR && C::NET == 0 && C::KIN < 2 && C::NWARP == 4;
 #ifdef COMMET_EXP_SKIP_7A  // timing experiments only
     if (false) {
 #else
@@ -1323,26 +1352,28 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
       if constexpr (C::KIN == 1) isochoric_to_standard(kin, gq, H6);
       gq[2] += 2.0 * m.kappa * (kin.J - 1.0) - m.ref_shift;
       H6[packed_index(C::NK, 2, 2)] += 2.0 * m.kappa;
-      if constexpr (C::KIN == 2)
-        post_qp_aniso(kin, m.a0, gq, H6, swq[q], post + q * PS, qP + q * 9);
+      if constexpr (C::KIN >= 2)
+        post_qp_aniso<C::NSV>(kin, m.a0, m.a1, gq, H6, swq[q], post + q * PS, qP + q * 9);
       else if constexpr (PAR7)
         post_qp_part(kin, gq, H6, swq[q], post + q * PS, qP + q * 9, warp);
       else
         post_qp(kin, gq, H6, swq[q], post + q * PS, qP + q * 9);
     }
+#if !defined(COMMET_DEBUG_DROP) || COMMET_DEBUG_DROP != 1  // (planted race: tools/race_check.py)
     __syncthreads();
+#endif
 
     STAGE_MARK(7)
     // ---- stage 7b: A_q (81 entries, scaled by w), one (q, iJ) row per item ------------------
-    if constexpr (C::KIN == 2 || !COMMET_ROWS3) {
+    if constexpr (C::KIN >= 2 || !COMMET_ROWS3) {
 #ifdef COMMET_EXP_SKIP_7B  // timing experiments only
     for (int it = tid; it < 0; it += C::NTHR) {
 #else
     for (int it = tid; it < Q * 9; it += C::NTHR) {
 #endif
       const int q = it / 9, iJ = it % 9;
-      if constexpr (C::KIN == 2)
-        tangent_row_aniso(post + q * PS, iJ, qA + q * 81 + iJ * 9);
+      if constexpr (C::KIN >= 2)
+        tangent_row_aniso<C::NSV>(post + q * PS, iJ, qA + q * 81 + iJ * 9);
       else
         tangent_row(post + q * PS, iJ, qA + q * 81 + iJ * 9);
     }
@@ -2042,6 +2073,10 @@ static int launch_k(const AsmArgs& a, cudaStream_t st, int* launches) {
   }
   return (int)cudaErrorInvalidValue;
 #else
+  if constexpr (K == 3) {  // two structural vectors, 9 inputs: the per-qp (analytic) networks only
+    if (a.ncm.net != 0) return launch_cfg<Cfg<16, 32, NEN, NQ, 2, 1, K>>(a, st, launches);
+    return (int)cudaErrorInvalidValue;  // (an ICNN on 9 inputs is refused at setup)
+  } else {
   if constexpr (K == 2) {  // 5 inputs: packed 5x5 Hessians and the extended F-space factors
     if (a.ncm.net != 0) return launch_cfg<Cfg<16, 32, NEN, NQ, 2, 1, K>>(a, st, launches);
   } else {
@@ -2067,6 +2102,7 @@ static int launch_k(const AsmArgs& a, cudaStream_t st, int* launches) {
     case 128: return launch_cfg<Cfg<128, 8, NEN, NQ, MB, 0, K>>(a, st, launches);
   }
   return (int)cudaErrorInvalidValue;
+  }
 #endif
 }
 
@@ -2076,6 +2112,10 @@ static int launch_mat_k(const AsmArgs& a, cudaStream_t st) {
 #ifdef COMMET_AB_MIN
   return (int)cudaErrorInvalidValue;
 #else
+  if constexpr (K == 3) {  // two structural vectors: analytic networks only
+    if (a.ncm.net != 0) return launch_cfg<Cfg<16, 16, 1, 1, 2, 1, K, 1>>(a, st, nullptr);
+    return (int)cudaErrorInvalidValue;
+  } else {
   if (a.ncm.net != 0) return launch_cfg<Cfg<16, 16, 1, 1, 3, 1, K, 1>>(a, st, nullptr);
   constexpr int MB = K == 2 ? 2 : 3;
   switch (a.ncm.w) {
@@ -2086,12 +2126,14 @@ static int launch_mat_k(const AsmArgs& a, cudaStream_t st) {
     case 128: return launch_cfg<Cfg<128, 8, 1, 1, MB, 0, K, 1>>(a, st, nullptr);
   }
   return (int)cudaErrorInvalidValue;
+  }
 #endif
 }
 
 int launch_material(const AsmArgs& a, void* stream) {
   if (a.el_count <= 0) return 0;
   cudaStream_t st = (cudaStream_t)stream;
+  if (a.ncm.kin == 3) return launch_mat_k<3>(a, st);
   return a.ncm.kin == 2 ? launch_mat_k<2>(a, st) : a.ncm.kin == 1 ? launch_mat_k<1>(a, st) : launch_mat_k<0>(a, st);
 }
 
@@ -2100,6 +2142,7 @@ static int launch_et(const AsmArgs& a, cudaStream_t st, int* launches) {
 #ifdef COMMET_AB_MIN
   return launch_k<NEN, NQ, 0>(a, st, launches);
 #else
+  if (a.ncm.kin == 3) return launch_k<NEN, NQ, 3>(a, st, launches);
   if (a.ncm.kin == 2) return launch_k<NEN, NQ, 2>(a, st, launches);
   return a.ncm.kin == 1 ? launch_k<NEN, NQ, 1>(a, st, launches) : launch_k<NEN, NQ, 0>(a, st, launches);
 #endif

@@ -42,18 +42,21 @@ __global__ void __launch_bounds__(64) simple_kernel(AsmArgs A) {
     kinematics(F, kin);
     if (!(kin.J > 0.0)) atomicMin(A.bad, (unsigned long long)(A.orig[e] * nq + q));
     trc = fmax(trc, kin.I1);
-    double kv[5] = {kin.I1 - 3.0, kin.I2 - 3.0, kin.J - 1.0, 0.0, 0.0};
+    double kv[9] = {kin.I1 - 3.0, kin.I2 - 3.0, kin.J - 1.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
     if (A.ncm.kin == 1) isochoric_inputs(kin, kv);
-    if (A.ncm.kin == 2) anisotropic_inputs(kin, A.ncm.a0, kv);
-    double g[5], H6[15];
+    if (A.ncm.kin == 2) anisotropic_inputs<1>(kin, A.ncm.a0, A.ncm.a1, kv);
+    if (A.ncm.kin == 3) anisotropic_inputs<2>(kin, A.ncm.a0, A.ncm.a1, kv);
+    double g[9], H6[45];
     ncm_point(A.ncm, kv, g, H6);
     if (A.ncm.kin == 1) isochoric_to_standard(kin, g, H6);
-    const int nk = A.ncm.kin == 2 ? 5 : 3;
+    const int nk = A.ncm.kin == 2 ? 5 : (A.ncm.kin == 3 ? 9 : 3);
     g[2] += 2.0 * A.ncm.kappa * (kin.J - 1.0) - A.ncm.ref_shift;
     H6[packed_index(nk, 2, 2)] += 2.0 * A.ncm.kappa;
     double P[9], Am[81];
     if (A.ncm.kin == 2)
-      stress_tangent_aniso(kin, A.ncm.a0, g, H6, w, P, Am);
+      stress_tangent_aniso<1>(kin, A.ncm.a0, A.ncm.a1, g, H6, w, P, Am);
+    else if (A.ncm.kin == 3)
+      stress_tangent_aniso<2>(kin, A.ncm.a0, A.ncm.a1, g, H6, w, P, Am);
     else
       stress_tangent(kin, g, H6, w, P, Am);
     for (int a = 0; a < nen; a++) {

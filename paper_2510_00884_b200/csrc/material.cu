@@ -13,9 +13,9 @@ namespace {
 
 __global__ void ncm_eval_kernel(NcmDev m, const double* __restrict__ k, double* __restrict__ g,
                                 double* __restrict__ H, int64_t n) {
-  const int nk = m.kin == 2 ? 5 : 3, nh = nk * (nk + 1) / 2;
+  const int nk = m.kin == 2 ? 5 : (m.kin == 3 ? 9 : 3), nh = nk * (nk + 1) / 2;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    double gi[5], Hi[15];
+    double gi[9], Hi[45];
     ncm_point(m, k + nk * i, gi, Hi);
     for (int p = 0; p < nk; p++) g[nk * i + p] = gi[p];
     for (int p = 0; p < nh; p++) H[nh * i + p] = Hi[p];
@@ -52,7 +52,7 @@ extern "C" commet_status commet_ncm_eval(commet_ctx c, const double* k, double* 
 
 extern "C" commet_status commet_normalize_reference(commet_ctx c, double* s0) {
   if (!c) return fail(nullptr, COMMET_ERR_ARG, "ctx is NULL");
-  if (c->ncm.kin == 2)
+  if (c->ncm.kin >= 2)
     return fail(c, COMMET_ERR_ARG, "anisotropic kinematics: S(I) has a structural part (2 g4 + 4 g5) A0 A0 that a "
                 "volumetric -s0 (J - 1) term cannot cancel");
   CUDA_TRY(c, cudaSetDevice(c->device));

@@ -83,6 +83,8 @@ __device__ __forceinline__ void ncm_point(const NcmDev& m, const double* kin, do
     ncm_alg4<5>(m, kin, g, H6);
   else if (m.net == 0)
     ncm_alg4<3>(m, kin, g, H6);
+  else if (m.kin == 3)
+    analytic_point<9>(m, kin, g, H6, nullptr);
   else if (m.kin == 2)
     analytic_point<5>(m, kin, g, H6, nullptr);
   else

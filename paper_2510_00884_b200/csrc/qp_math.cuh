@@ -263,42 +263,77 @@ __device__ __forceinline__ void stress_tangent(const Kin& k, const double* __res
 }
 
 // ---------------------------------------------------------------------------
-// anisotropic inputs (App. A.2.1): one structural vector A0,
-//   K = (I1-3, I2-3, J-1, I4-1, I5-1),  I4 = A0.C A0,  I5 = A0.C^2 A0 = |C A0|^2.
-// Tangent: the F-space factors above extended by Phi_4 = F h4 = a (x) A0 (a = F A0) and
-// Phi_5 = F h5 = a (x) C A0 + F C A0 (x) A0, plus the second-derivative term of I5,
-//   4 g5 F_iI HH5_IJKL F_kK = 2 g5 (a_i F_kJ A0_L + a_i a_k d_JL + b_ik A0_J A0_L + F_iL a_k A0_J)
-// (HH4 = 0).  H6 below is the packed upper triangle of the 5x5 Hessian (15 entries).
+// anisotropic inputs (App. A.2.1, Eq. standard-inv-II): NSV = 1 or 2
+// structural vectors A_v (reference configuration), the pairs p = (i <= j) in the order (0,0),
+// (0,1), (1,1), NK = 3 + 2 NP inputs
+//   K = (I1-3, I2-3, J-1, then per pair I4,ij - A_i.A_j, I5,ij - A_i.A_j),
+//   I4,ij = A_i.C A_j,  I5,ij = A_i.C^2 A_j = (C A_i).(C A_j)
+// (one unit vector: I4 - 1, I5 - 1).  Tangent: the F-space factors of the header extended by
+// (a_v = F A_v)
+//   Phi_4p = 1/2 (a_i (x) A_j + a_j (x) A_i),
+//   Phi_5p = 1/2 (F C A_j (x) A_i + a_i (x) C A_j + a_j (x) C A_i + F C A_i (x) A_j)
+// (dK/dF = 2 Phi), and the second-derivative term of I5,ij (I4's is d_ik (dI4/dC)_JL, inside T):
+//   g5p [F_kJ (a_i,i A_j,L + a_j,i A_i,L) + F_iL (A_i,J a_j,k + A_j,J a_i,k) + b_ik (A_i,J A_j,L +
+//        A_j,J A_i,L) + d_JL (a_i,i a_j,k + a_j,i a_i,k)]
+// (written from d2(u.v) with u = C A_i, v = C A_j; two i = j pairs reduce to the one-vector form).
+// H below is the packed upper triangle of the NK x NK Hessian.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void anisotropic_inputs(const Kin& k, const double* a0, double kk[5]) {
-  double CA[3];
+template <int NSV>
+struct Aniso {
+  static constexpr int NP = NSV * (NSV + 1) / 2, NK = 3 + 2 * NP, NH = NK * (NK + 1) / 2;
+  // post layout (per qp): [0..8] F, [9..17] F^-T, [18..26] w T, [27 .. 27+9NK) Phi_m,
+  // [PSI .. PSI+9NK) Psi_m = 4w sum_n H'_mn Phi_n, [B] b = F F^T, [C] c2 = -2 g2 w, c3 = -g3 J w,
+  // [AV] a_v = F A_v, [A0] A_v, [C5] c5_p = g5p w;  P[9] = w F S.
+  static constexpr int PSI = 27 + 9 * NK, B = PSI + 9 * NK, CC = B + 9, AV = CC + 2, A0 = AV + 3 * NSV,
+                       C5 = A0 + 3 * NSV, SIZE = C5 + NP;
+  __host__ __device__ static constexpr int pi(int p) { return NSV == 1 ? 0 : (p < 2 ? 0 : 1); }
+  __host__ __device__ static constexpr int pj(int p) { return NSV == 1 ? 0 : (p == 0 ? 0 : 1); }
+};
+constexpr int kPostAniso = Aniso<1>::SIZE;   // 135
+constexpr int kPostAniso2 = Aniso<2>::SIZE;  // 215
+
+template <int NSV>
+__device__ __forceinline__ void anisotropic_inputs(const Kin& k, const double* a0, const double* a1, double* kk) {
+  using AN = Aniso<NSV>;
+  const double* Av[2] = {a0, a1};
+  double CA[NSV][3];
 #pragma unroll
-  for (int I = 0; I < 3; I++) CA[I] = k.C[I * 3] * a0[0] + k.C[I * 3 + 1] * a0[1] + k.C[I * 3 + 2] * a0[2];
+  for (int v = 0; v < NSV; v++)
+#pragma unroll
+    for (int I = 0; I < 3; I++) CA[v][I] = k.C[I * 3] * Av[v][0] + k.C[I * 3 + 1] * Av[v][1] + k.C[I * 3 + 2] * Av[v][2];
   kk[0] = k.I1 - 3.0;
   kk[1] = k.I2 - 3.0;
   kk[2] = k.J - 1.0;
-  kk[3] = a0[0] * CA[0] + a0[1] * CA[1] + a0[2] * CA[2] - 1.0;
-  kk[4] = CA[0] * CA[0] + CA[1] * CA[1] + CA[2] * CA[2] - 1.0;
+#pragma unroll
+  for (int p = 0; p < AN::NP; p++) {
+    const int i = AN::pi(p), j = AN::pj(p);
+    const double aa = Av[i][0] * Av[j][0] + Av[i][1] * Av[j][1] + Av[i][2] * Av[j][2];
+    kk[3 + 2 * p] = Av[i][0] * CA[j][0] + Av[i][1] * CA[j][1] + Av[i][2] * CA[j][2] - aa;
+    kk[4 + 2 * p] = CA[i][0] * CA[j][0] + CA[i][1] * CA[j][1] + CA[i][2] * CA[j][2] - aa;
+  }
 }
 
 __host__ __device__ constexpr int packed_index(int n, int p, int q) { return p * n - p * (p - 1) / 2 + (q - p); }
 
-// post layout (per qp, PSA = 137): [0..8] F, [9..17] F^-T, [18..26] w T, [27..71] Phi_1..5,
-// [72..116] Psi_m = 4w sum_n H'_mn Phi_n, [117..125] b, [126] c2 = -2 g2 w, [127] c3 = -g3 J w,
-// [128..130] a = F A0, [131..133] A0, [134] c5 = 2 g5 w;  P[9] = w F S.
-constexpr int kPostAniso = 137;
-__device__ __forceinline__ void post_qp_aniso(const Kin& k, const double* a0, const double* __restrict__ g,
-                                              const double* __restrict__ H15, double w, double* __restrict__ post,
-                                              double* __restrict__ P) {
+template <int NSV>
+__device__ __forceinline__ void post_qp_aniso(const Kin& k, const double* a0, const double* a1,
+                                              const double* __restrict__ g, const double* __restrict__ Hpk, double w,
+                                              double* __restrict__ post, double* __restrict__ P) {
+  using AN = Aniso<NSV>;
+  constexpr int NK = AN::NK;
   const double* F = k.F;
   const double hJ = 0.5 * k.J;
-  double CA[3], a[3], FCA[3];
+  const double* Av[2] = {a0, a1};
+  double CA[NSV][3], a[NSV][3], FCA[NSV][3];
 #pragma unroll
-  for (int I = 0; I < 3; I++) CA[I] = k.C[I * 3] * a0[0] + k.C[I * 3 + 1] * a0[1] + k.C[I * 3 + 2] * a0[2];
+  for (int v = 0; v < NSV; v++) {
 #pragma unroll
-  for (int i = 0; i < 3; i++) {
-    a[i] = F[i * 3] * a0[0] + F[i * 3 + 1] * a0[1] + F[i * 3 + 2] * a0[2];
-    FCA[i] = F[i * 3] * CA[0] + F[i * 3 + 1] * CA[1] + F[i * 3 + 2] * CA[2];
+    for (int I = 0; I < 3; I++) CA[v][I] = k.C[I * 3] * Av[v][0] + k.C[I * 3 + 1] * Av[v][1] + k.C[I * 3 + 2] * Av[v][2];
+#pragma unroll
+    for (int i = 0; i < 3; i++) {
+      a[v][i] = F[i * 3] * Av[v][0] + F[i * 3 + 1] * Av[v][1] + F[i * 3 + 2] * Av[v][2];
+      FCA[v][i] = F[i * 3] * CA[v][0] + F[i * 3 + 1] * CA[v][1] + F[i * 3 + 2] * CA[v][2];
+    }
   }
   double S[9];
 #pragma unroll
@@ -306,11 +341,17 @@ __device__ __forceinline__ void post_qp_aniso(const Kin& k, const double* a0, co
 #pragma unroll
     for (int J = 0; J < 3; J++) {
       const double d = (I == J) ? 1.0 : 0.0;
-      S[I * 3 + J] = 2.0 * (g[0] * d + g[1] * (k.I1 * d - k.C[I * 3 + J]) + g[2] * hJ * k.Ci[I * 3 + J] +
-                            g[3] * a0[I] * a0[J] + g[4] * (a0[I] * CA[J] + CA[I] * a0[J]));
-      post[18 + I * 3 + J] = w * (S[I * 3 + J] - g[2] * k.J * k.Ci[I * 3 + J]);
+      double s = 2.0 * (g[0] * d + g[1] * (k.I1 * d - k.C[I * 3 + J]) + g[2] * hJ * k.Ci[I * 3 + J]);
+#pragma unroll
+      for (int p = 0; p < AN::NP; p++) {
+        const int vi = AN::pi(p), vj = AN::pj(p);
+        s += g[3 + 2 * p] * (Av[vi][I] * Av[vj][J] + Av[vj][I] * Av[vi][J]) +
+             g[4 + 2 * p] * (Av[vi][I] * CA[vj][J] + CA[vj][I] * Av[vi][J] + CA[vi][I] * Av[vj][J] + Av[vj][I] * CA[vi][J]);
+      }
+      S[I * 3 + J] = s;
+      post[18 + I * 3 + J] = w * (s - g[2] * k.J * k.Ci[I * 3 + J]);
     }
-  double Phi[5][9];
+  double Phi[NK][9];
 #pragma unroll
   for (int i = 0; i < 3; i++)
 #pragma unroll
@@ -319,43 +360,52 @@ __device__ __forceinline__ void post_qp_aniso(const Kin& k, const double* a0, co
       Phi[0][i * 3 + J] = F[i * 3 + J];
       Phi[1][i * 3 + J] = k.I1 * F[i * 3 + J] - FC;
       Phi[2][i * 3 + J] = hJ * k.FiT[i * 3 + J];
-      Phi[3][i * 3 + J] = a[i] * a0[J];
-      Phi[4][i * 3 + J] = a[i] * CA[J] + FCA[i] * a0[J];
+#pragma unroll
+      for (int p = 0; p < AN::NP; p++) {
+        const int vi = AN::pi(p), vj = AN::pj(p);
+        Phi[3 + 2 * p][i * 3 + J] = 0.5 * (a[vi][i] * Av[vj][J] + a[vj][i] * Av[vi][J]);
+        Phi[4 + 2 * p][i * 3 + J] = 0.5 * (FCA[vj][i] * Av[vi][J] + a[vi][i] * CA[vj][J] + a[vj][i] * CA[vi][J] +
+                                           FCA[vi][i] * Av[vj][J]);
+      }
     }
-  double Hp[25];
-#pragma unroll
-  for (int p = 0; p < 5; p++)
-#pragma unroll
-    for (int q = 0; q < 5; q++) Hp[p * 5 + q] = H15[p <= q ? packed_index(5, p, q) : packed_index(5, q, p)];
-  Hp[0] += g[1];
-  Hp[12] += g[2] / k.J;
   const double w4 = 4.0 * w;
 #pragma unroll
   for (int x = 0; x < 9; x++) {
     post[x] = F[x];
     post[9 + x] = k.FiT[x];
+  }
 #pragma unroll
-    for (int m = 0; m < 5; m++) {
+  for (int m = 0; m < NK; m++) {
+    double hr[NK];  // row m of H' = H + diag(g2, 0, g3/J, 0, ...)
+#pragma unroll
+    for (int n = 0; n < NK; n++) hr[n] = Hpk[m <= n ? packed_index(NK, m, n) : packed_index(NK, n, m)];
+    if (m == 0) hr[0] += g[1];
+    if (m == 2) hr[2] += g[2] / k.J;
+#pragma unroll
+    for (int x = 0; x < 9; x++) {
       post[27 + m * 9 + x] = Phi[m][x];
       double t = 0.0;
 #pragma unroll
-      for (int n = 0; n < 5; n++) t += Hp[m * 5 + n] * Phi[n][x];
-      post[72 + m * 9 + x] = w4 * t;
+      for (int n = 0; n < NK; n++) t += hr[n] * Phi[n][x];
+      post[AN::PSI + m * 9 + x] = w4 * t;
     }
   }
 #pragma unroll
   for (int i = 0; i < 3; i++)
 #pragma unroll
     for (int kk = 0; kk < 3; kk++)
-      post[117 + i * 3 + kk] = F[i * 3 + 0] * F[kk * 3 + 0] + F[i * 3 + 1] * F[kk * 3 + 1] + F[i * 3 + 2] * F[kk * 3 + 2];
-  post[126] = -2.0 * g[1] * w;
-  post[127] = -g[2] * k.J * w;
+      post[AN::B + i * 3 + kk] = F[i * 3 + 0] * F[kk * 3 + 0] + F[i * 3 + 1] * F[kk * 3 + 1] + F[i * 3 + 2] * F[kk * 3 + 2];
+  post[AN::CC] = -2.0 * g[1] * w;
+  post[AN::CC + 1] = -g[2] * k.J * w;
 #pragma unroll
-  for (int i = 0; i < 3; i++) {
-    post[128 + i] = a[i];
-    post[131 + i] = a0[i];
-  }
-  post[134] = 2.0 * g[4] * w;
+  for (int v = 0; v < NSV; v++)
+#pragma unroll
+    for (int i = 0; i < 3; i++) {
+      post[AN::AV + 3 * v + i] = a[v][i];
+      post[AN::A0 + 3 * v + i] = Av[v][i];
+    }
+#pragma unroll
+  for (int p = 0; p < AN::NP; p++) post[AN::C5 + p] = g[4 + 2 * p] * w;
 #pragma unroll
   for (int i = 0; i < 3; i++)
 #pragma unroll
@@ -363,37 +413,50 @@ __device__ __forceinline__ void post_qp_aniso(const Kin& k, const double* a0, co
       P[i * 3 + J] = w * (F[i * 3 + 0] * S[0 * 3 + J] + F[i * 3 + 1] * S[1 * 3 + J] + F[i * 3 + 2] * S[2 * 3 + J]);
 }
 
+template <int NSV>
 __device__ __forceinline__ void tangent_row_aniso(const double* __restrict__ post, int iJ, double* __restrict__ out) {
+  using AN = Aniso<NSV>;
+  constexpr int NK = AN::NK;
   const int i = iJ / 3, J = iJ % 3;
-  double p[5];
+  double p[NK];
 #pragma unroll
-  for (int m = 0; m < 5; m++) p[m] = post[27 + m * 9 + iJ];
-  const double c2 = post[126], c3 = post[127], c5 = post[134];
-  const double ai = post[128 + i], A0J = post[131 + J];
+  for (int m = 0; m < NK; m++) p[m] = post[27 + m * 9 + iJ];
+  const double c2 = post[AN::CC], c3 = post[AN::CC + 1];
 #pragma unroll
   for (int kk = 0; kk < 3; kk++) {
-    const double FkJ = post[kk * 3 + J], GkJ = post[9 + kk * 3 + J], ak = post[128 + kk], bik = post[117 + i * 3 + kk];
+    const double FkJ = post[kk * 3 + J], GkJ = post[9 + kk * 3 + J], bik = post[AN::B + i * 3 + kk];
 #pragma unroll
     for (int L = 0; L < 3; L++) {
       const int kL = kk * 3 + L;
       double v = 0.0;
 #pragma unroll
-      for (int m = 0; m < 5; m++) v += p[m] * post[72 + m * 9 + kL];
+      for (int m = 0; m < NK; m++) v += p[m] * post[AN::PSI + m * 9 + kL];
       v += c2 * post[i * 3 + L] * FkJ + c3 * post[9 + i * 3 + L] * GkJ;
-      const double A0L = post[131 + L];
-      v += c5 * (ai * FkJ * A0L + bik * A0J * A0L + post[i * 3 + L] * ak * A0J);
-      if (J == L) v += c2 * bik + c5 * ai * ak;
+      if (J == L) v += c2 * bik;
+#pragma unroll
+      for (int q = 0; q < AN::NP; q++) {
+        const int vi = AN::pi(q), vj = AN::pj(q);
+        const double* ai = post + AN::AV + 3 * vi;
+        const double* aj = post + AN::AV + 3 * vj;
+        const double* Ai = post + AN::A0 + 3 * vi;
+        const double* Aj = post + AN::A0 + 3 * vj;
+        double t = FkJ * (ai[i] * Aj[L] + aj[i] * Ai[L]) + post[i * 3 + L] * (Ai[J] * aj[kk] + Aj[J] * ai[kk]) +
+                   bik * (Ai[J] * Aj[L] + Aj[J] * Ai[L]);
+        if (J == L) t += ai[i] * aj[kk] + aj[i] * ai[kk];
+        v += post[AN::C5 + q] * t;
+      }
       if (i == kk) v += post[18 + J * 3 + L];
       out[kL] = v;
     }
   }
 }
 
-__device__ __forceinline__ void stress_tangent_aniso(const Kin& k, const double* a0, const double* g,
-                                                     const double* H15, double w, double* P, double* A) {
-  double post[kPostAniso];
-  post_qp_aniso(k, a0, g, H15, w, post, P);
-  for (int iJ = 0; iJ < 9; iJ++) tangent_row_aniso(post, iJ, A + iJ * 9);
+template <int NSV>
+__device__ __forceinline__ void stress_tangent_aniso(const Kin& k, const double* a0, const double* a1,
+                                                     const double* g, const double* H, double w, double* P, double* A) {
+  double post[Aniso<NSV>::SIZE];
+  post_qp_aniso<NSV>(k, a0, a1, g, H, w, post, P);
+  for (int iJ = 0; iJ < 9; iJ++) tangent_row_aniso<NSV>(post, iJ, A + iJ * 9);
 }
 
 // ---------------------------------------------------------------------------

@@ -7,7 +7,7 @@ import numpy as np
 import pytest
 
 import oracle
-from synth.gen import anisotropic, cann_params, gent_thomas_params, ickan_params, ncm_weights
+from synth.gen import A_FIBRE, A_SHEET, anisotropic, cann_params, gent_thomas_params, ickan_params, ncm_weights
 from tests.test_oracle_material import rand_F
 from tests.test_oracle_variants import isochoric_icnn
 
@@ -45,6 +45,7 @@ MODELS = {
     "ickan": lambda: ickan_params(),
     "cann_anisotropic": lambda: anisotropic(cann_params(4, seed=6, n_in=5)),
     "icnn_anisotropic_32x2": lambda: anisotropic(ncm_weights(32, 2, 0.3, 15, 10.0, n_in=5)),
+    "cann_two_vectors": lambda: anisotropic(cann_params(3, seed=8, n_in=9), A_FIBRE, A_SHEET),
 }
 
 

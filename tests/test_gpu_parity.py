@@ -315,12 +315,15 @@ def test_parity_c5_sampled():
     print(f"c5 sampled rows: values rel err {ev:.2e}, residual rel err {er:.2e}")
 
 
-@pytest.mark.parametrize("variant", ["icnn_isochoric", "icnn_anisotropic", "cann_anisotropic", "ickan"])
+@pytest.mark.parametrize("variant", ["icnn_isochoric", "icnn_anisotropic", "cann_anisotropic", "ickan",
+                                     "cann_two_vectors"])
 def test_parity_full_size_sampled_variants(variant):
     """The variants' instantiations at the c3 size (2.1M qp, the persistent grid of the bench):
     sampled complete rows against the oracle."""
     ncm = {"icnn_isochoric": lambda: dict(gen.ncm_weights(64, 3, 0.3, 11, 10.0), kinematics="isochoric"),
            "icnn_anisotropic": lambda: gen.anisotropic(gen.ncm_weights(64, 3, 0.3, 14, 10.0, n_in=5)),
            "cann_anisotropic": lambda: gen.anisotropic(gen.cann_params(4, seed=6, n_in=5)),
-           "ickan": lambda: gen.ickan_params()}[variant]()
+           "ickan": lambda: gen.ickan_params(),
+           "cann_two_vectors": lambda: gen.anisotropic(gen.cann_params(3, seed=8, n_in=9), gen.A_FIBRE,
+                                                       gen.A_SHEET)}[variant]()
     sampled_rows_check("c3", n_samples=8, ncm=ncm)

@@ -7,7 +7,7 @@ import pytest
 
 import oracle
 from oracle import newton as on
-from synth.gen import (HEX8, TET10, anisotropic, cann_params, gent_thomas_params, hex_mesh, ickan_params,
+from synth.gen import (A_FIBRE, A_SHEET, HEX8, TET10, anisotropic, cann_params, gent_thomas_params, hex_mesh, ickan_params,
                        ncm_weights, shape_gradients, smooth_field, tet10_mesh)
 
 pytestmark = pytest.mark.gpu
@@ -43,6 +43,9 @@ VARIANTS = {
     "ickan_anisotropic": lambda: anisotropic(ickan_params((5, 4, 1), nb=7, seed=7)),
     "icnn_anisotropic_16x2": lambda: anisotropic(ncm_weights(16, 2, 0.3, 13, 10.0, n_in=5)),
     "icnn_anisotropic_64x3": lambda: anisotropic(ncm_weights(64, 3, 0.3, 14, 10.0, n_in=5)),
+    # two structural vectors (pairs 00, 01, 11: 9 inputs, Eq. standard-inv-II), one pair not orthogonal
+    "cann_two_vectors": lambda: anisotropic(cann_params(3, seed=8, n_in=9), A_FIBRE, A_SHEET),
+    "ickan_two_vectors": lambda: anisotropic(ickan_params((9, 4, 1), nb=7, seed=9), A_FIBRE, (0.0, 0.6, 0.8)),
 }
 
 
@@ -88,10 +91,10 @@ def test_variant_assembly_matches_oracle(pc, name, elem_type, n, kernel):
 
 
 @pytest.mark.parametrize("name", ["gent_thomas", "cann_standard", "cann_isochoric", "ickan", "cann_anisotropic",
-                                  "ickan_anisotropic"])
+                                  "ickan_anisotropic", "cann_two_vectors", "ickan_two_vectors"])
 def test_analytic_ncm_eval_matches_oracle(pc, name):
     ncm = VARIANTS[name]()
-    nk = 5 if ncm.get("kinematics") == "anisotropic" else 3
+    nk = (9 if ncm.get("a1") is not None else 5) if ncm.get("kinematics") == "anisotropic" else 3
     mesh, _ = _mesh(HEX8, 1)
     lib = pc.Commet(mesh, ncm)
     rng = np.random.default_rng(12)
@@ -186,3 +189,11 @@ def test_normalize_reference_variants(pc, name):
     assert abs(s0 - ref) <= 1e-13 * max(1.0, abs(ref))
     if name == "gent_thomas":
         assert s0 == 0.0  # stress-free by construction (App. C)
+
+
+def test_two_vector_icnn_refused(pc):
+    """An ICNN on the nine inputs of two structural vectors is refused at setup (the ICNN kernels
+    take up to five inputs); CANN / ICKAN run them (test_variant_assembly_matches_oracle)."""
+    mesh, _ = _mesh(HEX8, 1)
+    with pytest.raises(pc.CommetError, match="two structural vectors"):
+        pc.Commet(mesh, anisotropic(ncm_weights(16, 2, 0.3, 3, 10.0, n_in=9), A_FIBRE, A_SHEET))
