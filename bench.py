@@ -276,6 +276,8 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--jitter", type=float, default=None,
+                    help="override the config's node jitter (fraction of h): every element then has its own dN/dX")
     ap.add_argument("--exchange", default="nccl", choices=["nccl", "peer"],
                     help="N > 1: interface rows over NCCL send/recv + unpack (default), or added straight "
                          "into the owner's buffers by the kernels over NVLink P2P (CUDA IPC)")
@@ -307,7 +309,7 @@ def main():
         cfg = gen.slab_partition(args.config, ws, rank)   # z-slab r of ws, with ghost layer
         comm = pc.nccl_comm_from_process_group(rank, ws, local)
     else:
-        cfg = gen.make_config(args.config)
+        cfg = gen.make_config(args.config, jitter=args.jitter)
     lib = pc.Commet(cfg, cfg["ncm"], device=local, nccl_comm=comm)
     if args.kernel == "simple":
         lib.set_kernel(pc.KERNEL_SIMPLE)
@@ -435,7 +437,8 @@ def main():
         metric=METRIC, value=total_qp / (ms * 1e-3), unit="qp/s", n_gpus=ws, steps=args.steps,
         warmup=args.warmup, ms_per_step=ms, higher_is_better=True, scaling="strong", vs_baseline=None,
         dtype="f64", data="synthetic (seeded mesh, NCM weights N(0,0.3^2), displacement; synth/gen.py)",
-        config=dict(workload=WORKLOAD[args.config], elements=total_el, qp=total_qp, nnz_rank0=nnz_local,
+        config=dict(workload=WORKLOAD[args.config] + (f", nodes jittered {args.jitter:g} h" if args.jitter else ""),
+                    elements=total_el, qp=total_qp, nnz_rank0=nnz_local,
                     width=spec.width, hidden_layers=spec.n_hidden, colours=info["n_colours"],
                     kernel=args.kernel, launch=kinfo,
                     parallelism=(f"z-slabs x{ws}, interface rows over " + ("NVLink P2P (peer mode)" if peer else "NCCL"))

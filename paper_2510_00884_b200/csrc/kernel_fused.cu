@@ -1365,7 +1365,9 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
 
     STAGE_MARK(7)
     // ---- stage 7b: A_q (81 entries, scaled by w), one (q, iJ) row per item ------------------
-    if constexpr (C::KIN >= 2 || !COMMET_ROWS3) {
+    // (three rows per item only with 16+ qps per batch: at Q = 8 the 24 items leave most threads
+    // idle -- measured c4 38.0 -> 40.3 ms -- while at Q = 16 it is 0.2 % faster)
+    if constexpr (C::KIN >= 2 || !COMMET_ROWS3 || C::Q < 16) {
 #ifdef COMMET_EXP_SKIP_7B  // timing experiments only
     for (int it = tid; it < 0; it += C::NTHR) {
 #else

@@ -348,10 +348,16 @@ def make_mesh(spec: ConfigSpec, n: int | None = None, z_range=None):
     return tet10_mesh(n, spec.jitter, SEED_MESH, z_range)
 
 
-def make_config(name: str, n: int | None = None, z_range=None, with_gradients: bool = True) -> dict:
+def make_config(name: str, n: int | None = None, z_range=None, with_gradients: bool = True,
+                jitter: float | None = None) -> dict:
     """Everything the boundary needs for config ``name`` (optionally resized to
-    ``n`` cells per edge, or restricted to element layers ``z_range``)."""
+    ``n`` cells per edge, or restricted to element layers ``z_range``; ``jitter``
+    overrides the config's node jitter, e.g. a jittered c3 / c5 to show that the
+    kernel does not depend on the regular lattice's identical element gradients)."""
     spec = CONFIGS[name]
+    if jitter is not None:
+        import dataclasses
+        spec = dataclasses.replace(spec, jitter=float(jitter))
     X, conn = make_mesh(spec, n, z_range)
     cfg = dict(name=name, spec=spec, elem_type=spec.elem_type, n=n or spec.n,
                X=X, conn=np.ascontiguousarray(conn), n_nodes=X.shape[0],

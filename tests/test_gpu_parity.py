@@ -327,3 +327,21 @@ def test_parity_full_size_sampled_variants(variant):
            "cann_two_vectors": lambda: gen.anisotropic(gen.cann_params(3, seed=8, n_in=9), gen.A_FIBRE,
                                                        gen.A_SHEET)}[variant]()
     sampled_rows_check("c3", n_samples=8, ncm=ncm)
+
+
+@pytest.mark.parametrize("kind,n,w", [("hex", 3, 64), ("hex", 2, 128), ("tet", 2, 64)])
+def test_forward_sweep_saturated_inner_layer(kind, n, w):
+    """Forward sweep with half of layer 2 saturated (biases -800: sigma_2 underflows to ~1e-308) and
+    large adjoints (output weights x 20, |lambda_2| >> 6): the inner layer's Hessian term
+    lambda (1 - s)/s P P^T must stay finite (1/s of s clamped at 2^-500) and match
+    the oracle."""
+    case = small_case(kind, n, w, 3)
+    m = case["ncm"]
+    m["b"] = m["b"].copy()
+    m["b"][1, ::2] = -800.0
+    m["a"] = m["a"] * 20.0
+    lib, r, v, rp, ci = run_gpu(case)
+    ro, vo, orp, oci, bad = run_oracle(case)
+    assert np.isfinite(r).all() and np.isfinite(v).all()
+    assert np.array_equal(rp, orp) and np.array_equal(ci, oci)
+    assert rel(r, ro) <= TOL and rel(v, vo) <= TOL, (rel(r, ro), rel(v, vo))

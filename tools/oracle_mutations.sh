@@ -45,7 +45,11 @@ mut "H[4] = -m->gt[1] / ((K[1] + 3.0) * (K[1] + 3.0));" "H[4] = m->gt[1] / ((K[1
 # ICKAN: De Boor recursion and spline derivatives
 mut "if (t[i + p + 1] > t[i + 1]) v += (t[i + p + 1] - x) / (t[i + p + 1] - t[i + 1]) * B[(p - 1) * nt + i + 1];" "if (t[i + p + 1] > t[i + 1]) v += (t[i + p + 1] - x) / (t[i + p + 1] - t[i]) * B[(p - 1) * nt + i + 1];"
 mut "for (int q = 0; q < nk; q++) d2y[i][p * nk + q] += w * (d2 * dz[j][p] * dz[j][q] + d1 * d2z[j][p * nk + q]);" "for (int q = 0; q < nk; q++) d2y[i][p * nk + q] += w * (d2 * dz[j][p] * dz[j][q]);"
-# anisotropic I4 / I5 (the paper's G-tensor table)
-mut "G[4][i * 3 + j] = a[i] * Ba[j] + Ba[i] * a[j];  /* 2 sym(a (x) B a) */" "G[4][i * 3 + j] = a[i] * Ba[j] + B[i * 3 + j];"
-mut "GG[4][x] = 0.5 * (B[i * 3 + k] * A[j * 3 + l] + B[i * 3 + l] * A[j * 3 + k]) +" "GG[4][x] = 0.5 * (B[i * 3 + k] * A[j * 3 + l] + B[i * 3 + l] * A[j * 3 + k]) * 0.0 +"
+# anisotropic I4,ij / I5,ij (the paper's G-tensor table, several structural vectors)
+mut "G[m5][i * 3 + j] = 0.5 * (ai[i] * Baj[j] + Baj[i] * ai[j]) + 0.5 * (aj[i] * Bai[j] + Bai[i] * aj[j]);" "G[m5][i * 3 + j] = 0.5 * (ai[i] * Baj[j] + Baj[i] * ai[j]) + 0.5 * (aj[i] * Bai[j] + B[i * 3 + j]);"
+mut "GG[m5][x] = 0.5 * (B[i * 3 + k] * As[j * 3 + l] + B[i * 3 + l] * As[j * 3 + k]) +" "GG[m5][x] = 0.5 * (B[i * 3 + k] * As[j * 3 + l] + B[i * 3 + l] * As[j * 3 + k]) * 0.0 +"
+# reading R28: the table's literal G^{5,ij} = 2 sym(a_i (x) B a_j) for i != j
+mut "G[m5][i * 3 + j] = 0.5 * (ai[i] * Baj[j] + Baj[i] * ai[j]) + 0.5 * (aj[i] * Bai[j] + Bai[i] * aj[j]);" "G[m5][i * 3 + j] = (ai[i] * Baj[j] + Baj[i] * ai[j]);"
+mut "i4 += Ai[I] * CAj[I];   /* A_i.C A_j */" "i4 += Ai[I] * CAi[I];   /* A_i.C A_j */"
+mut "G[m4][i * 3 + j] = As[i * 3 + j];" "G[m4][i * 3 + j] = ai[i] * aj[j];"
 exit $fail
