@@ -88,6 +88,15 @@
 #ifndef COMMET_WS_PAR7
 #define COMMET_WS_PAR7 0  // warp-specialised kernel: stage 7a split over the four element warps (measured: c3 9.52 -> 9.78 ms)
 #endif
+#ifndef COMMET_POST_PAR_NET1
+#define COMMET_POST_PAR_NET1 1  // analytic networks: stage 7a split over the four warps (GT c3 -12 %, CANN -9 %)
+#endif
+#ifndef COMMET_ELEM_HALF_NET1
+#define COMMET_ELEM_HALF_NET1 1  // analytic networks, hex8: stage 8 by (element, i-half) (GT / CANN c3 -1 %)
+#endif
+#ifndef COMMET_Q_KIN3
+#define COMMET_Q_KIN3 16  // qps per batch of the two-vector (9-input) kernels
+#endif
 #ifndef COMMET_PINGPONG
 #define COMMET_PINGPONG 0  // measured neutral (c3 10.31 vs 10.26 ms): barriers kept
 #endif
@@ -1321,7 +1330,10 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
 #endif
     // ICNN, 3 inputs: four warps cooperate (warp = part of post_qp, lane = qp); otherwise one
     // thread per qp
-    constexpr bool PAR7 = COMMET_POST_PAR && C::NET == 0 && C::KIN < 2 && C::NWARP == 4;
+    // (analytic networks: the CANN / Gent-Thomas instantiation (16 qps) only -- every warp repeats the
+    // per-qp network, which for the ICKAN's forward mode (32 qps) costs more than it saves: 5.8 -> 9.3 ms)
+    constexpr bool PAR7 = ((COMMET_POST_PAR && C::NET == 0) || (COMMET_POST_PAR_NET1 && C::NET == 1 && C::Q == 16)) &&
+                          C::KIN < 2 && C::NWARP == 4;
 #ifdef COMMET_EXP_SKIP_7A  // timing experiments only
     if (false) {
 #else
@@ -1394,7 +1406,7 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
     //      Y_q[J][b] = sum_L A_q[(i,J),(k,L)] dN_q[b][L] formed in the B fragment (3 FMA per
     //      element); M = a, N = b, K = (q, J); r_e; RED scatter (+ mirror for i < k)
     {
-      if constexpr (NEN == 8 && COMMET_ELEM_HALF) {
+      if constexpr (NEN == 8 && (COMMET_ELEM_HALF || (C::NET == 1 && COMMET_ELEM_HALF_NET1))) {
       // hex8: one warp per (element, i-half), the (i, k) blocks (0,0) (0,1) (0,2) or (1,1) (1,2)
       // (2,2) at once -- the dN/dX operands and the scatter metadata of the lane's node pair are
       // loaded once for the three
@@ -2072,11 +2084,13 @@ static int launch_k(const AsmArgs& a, cudaStream_t st, int* launches) {
       }
     if (a.ncm.net == 0 && a.ncm.w == 64) return launch_cfg<Cfg<64, 16, NEN, NQ, 3, 0, 0>>(a, st, launches);
     if (a.ncm.net == 0 && a.ncm.w == 128) return launch_cfg<Cfg<128, 8, NEN, NQ, 3, 0, 0>>(a, st, launches);
+    if (a.ncm.net == 1 || a.ncm.net == 2)  // CANN / Gent-Thomas (element-stage tuning)
+      return launch_cfg<Cfg<16, 16, NEN, NQ, COMMET_ANALYTIC_MINB, 1, 0>>(a, st, launches);
   }
   return (int)cudaErrorInvalidValue;
 #else
   if constexpr (K == 3) {  // two structural vectors, 9 inputs: the per-qp (analytic) networks only
-    if (a.ncm.net != 0) return launch_cfg<Cfg<16, 32, NEN, NQ, 2, 1, K>>(a, st, launches);
+    if (a.ncm.net != 0) return launch_cfg<Cfg<16, COMMET_Q_KIN3, NEN, NQ, 2, 1, K>>(a, st, launches);
     return (int)cudaErrorInvalidValue;  // (an ICNN on 9 inputs is refused at setup)
   } else {
   if constexpr (K == 2) {  // 5 inputs: packed 5x5 Hessians and the extended F-space factors

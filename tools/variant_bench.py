@@ -28,6 +28,9 @@ def main():
         "ickan 3-6-6-1": gen.ickan_params(),
         "ickan anisotropic 5-4-1": gen.anisotropic(gen.ickan_params((5, 4, 1), nb=7, seed=7)),
         "icnn 64x3 anisotropic": gen.anisotropic(gen.ncm_weights(64, 3, 0.3, 14, 10.0, n_in=5)),
+        "cann two vectors (9 inputs)": gen.anisotropic(gen.cann_params(3, seed=8, n_in=9), gen.A_FIBRE, gen.A_SHEET),
+        "ickan two vectors 9-4-1": gen.anisotropic(gen.ickan_params((9, 4, 1), nb=7, seed=9), gen.A_FIBRE,
+                                                   gen.A_SHEET),
     }
     u = torch.from_numpy(cfg["u"]).cuda()
     nq = cfg["conn"].shape[0] * 8
