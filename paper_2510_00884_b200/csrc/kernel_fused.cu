@@ -55,8 +55,11 @@
 #ifndef COMMET_ICKAN_MINB
 #define COMMET_ICKAN_MINB 2
 #endif
+#ifndef COMMET_ANALYTIC_Q
+#define COMMET_ANALYTIC_Q 32  // qps per batch of the CANN / Gent-Thomas instantiation (round 2: 32 with the split stage 7a, GT -8 %, CANN -15 %)
+#endif
 #ifndef COMMET_ANALYTIC_MINB
-#define COMMET_ANALYTIC_MINB 4  // CTAs per SM of the analytic-network (NET = 1) kernels (measured: GT +7 %, CANN +4 % over 3)
+#define COMMET_ANALYTIC_MINB 3  // CTAs per SM of the CANN / GT kernels (round 2 at 32 qps: 3 as fast as 4 for GT, CANN -2 %)
 #endif
 #ifndef COMMET_FWD
 #define COMMET_FWD 1  // forward value+Jacobian sweep, Hessian terms in the backward pass (L <= 3, no skips)
@@ -96,6 +99,9 @@
 #endif
 #ifndef COMMET_Q_KIN3
 #define COMMET_Q_KIN3 16  // qps per batch of the two-vector (9-input) kernels
+#endif
+#ifndef COMMET_EB
+#define COMMET_EB 1  // network batches per element batch (ICNN assembly)
 #endif
 #ifndef COMMET_PINGPONG
 #define COMMET_PINGPONG 0  // measured neutral (c3 10.31 vs 10.26 ms): barriers kept
@@ -230,7 +236,14 @@ struct Cfg {
   // 10.64 ms; round 2 with the layer count a template parameter (unrolled, short live ranges)
   // and 1/s by rcp + Newton instead of an IEEE division: c3 10.34 -> 9.84 ms, c4 39.86 -> 37.85.
   static constexpr bool FWDC = COMMET_FWD && W >= COMMET_FWD_MINW && NET == 0 && NK == 3 && !COMMET_PINGPONG;
-  static constexpr int TB_FWD = COMMET_ACT_TB;     // activation table bits on the forward-sweep path
+  // element batches: the element stages (0-1, 7-8) run on EB network batches at once -- QE qps,
+  // EE elements -- while the network stages (2-6) run batch by batch (ICNN assembly, Q <= 16)
+  static constexpr int EB = (NET == 0 && MODE == 0 && !WS && Q <= 16) ? COMMET_EB : 1;
+  static constexpr int QE = EB * Q, EE = QE / NQ, NKH = NK + NH;
+  static_assert(QE <= 32, "stage-1 threads (one per qp) must sit in warp 0");
+  // activation table bits on the forward-sweep path (the 256-entry tables do not fit beside the
+  // element buffers of two batches)
+  static constexpr int TB_FWD = EB > 1 ? 6 : COMMET_ACT_TB;
   static constexpr int LDA = (FWDC ? 4 : NK) * Q + 4;  // act row stride (= 4 mod 16: conflict-free B frags)
   static constexpr int LDS = Q + 2;                // s/c row stride (2-way conflicts at most)
   static_assert(W % 8 == 0 && Q % 8 == 0 && Q % NQ == 0, "tile");
@@ -249,7 +262,7 @@ template <class C>
 struct Smem {
   // per-qp stride of the stage-7a outputs (odd: bank spread); anisotropic: 5 factor pairs
   static constexpr int PS = C::KIN == 3 ? kPostAniso2 : (C::KIN == 2 ? kPostAniso : 101);
-  int act, sb, cb, qF, qk, qg, qH, hred, gsk, gN, ue, wq, qN, tab, qP, post, X, qA, total;
+  int act, sb, cb, qF, qk, qg, qH, hred, gsk, gN, ue, wq, qN, tab, qgH, qP, post, X, qA, total;
   // fwd: the forward-sweep path runs (C::FWDC, 2 <= L <= 3, no hidden skips): no c buffers
   __host__ __device__ static bool fwd_path(int L, bool skips) { return C::FWDC && L >= 2 && L <= 3 && !skips; }
   __host__ __device__ Smem(int L, bool skips = false) {
@@ -261,26 +274,27 @@ struct Smem {
     sb = o;  o += icnn ? (L > 1 ? L - 1 : 0) * C::W * C::LDS : 0;   // s_l, l = 1..L-1
     cb = o;  o += icnn && !fwd ? (L > 1 ? L - 1 : 1) * C::W * C::LDS : 0;   // c_l, l = 2..L (L == 1: c_1)
     const int dead = o;
-    qF = o;  o += C::Q * 9;
-    qk = o;  o += C::Q * C::NK;
+    qF = o;  o += C::QE * 9;
+    qk = o;  o += C::QE * C::NK;
     qg = o;  o += C::Q * C::NK;
     qH = o;  o += C::Q * C::NH;
     hred = o; o += (C::JMG + (C::FWDC ? C::VMG : 0)) * C::Q * C::NH;  // H partials per warp row group
     // (the adjoint-pass g/H_1 partials, VMG x Q x 9, live in act: dead at that point)
-    gsk = o; o += C::Q * C::NK;
-    gN = o;  o += C::Q * C::NEN * 3;
-    ue = o;  o += C::E * C::NEN * 3;
-    wq = o;  o += C::Q;
+    gsk = o; o += C::QE * C::NK;
+    gN = o;  o += C::QE * C::NEN * 3;
+    ue = o;  o += C::EE * C::NEN * 3;
+    wq = o;  o += C::QE;
     qN = o;  o += C::NPR * C::Q;
     tab = o; o += fwd ? ActTab<C::TB_FWD>::SIZE : ActTab<6>::SIZE;
+    qgH = o; o += C::EB > 1 ? C::QE * C::NKH : 0;  // (g, H) of each network batch for the element stage
     o = (o + 1) & ~1;
-    const int xs = C::DMMA_ELEM ? 0 : C::Q * C::NEN * 27;  // X only for the scalar element path
-    const int px = C::Q * PS > xs ? C::Q * PS : xs;
-    const int need = C::Q * 9 + px + C::Q * 81;
+    const int xs = C::DMMA_ELEM ? 0 : C::QE * C::NEN * 27;  // X only for the scalar element path
+    const int px = C::QE * PS > xs ? C::QE * PS : xs;
+    const int need = C::QE * 9 + px + C::QE * 81;
     int base = 0;
     if (need > dead) { base = o; o += need; }
     qP = base;
-    post = X = base + C::Q * 9;
+    post = X = base + C::QE * 9;
     qA = post + px;
     total = o;
   }
@@ -726,7 +740,9 @@ __device__ __forceinline__ void layer1(const NcmDev& m, int L, bool fwd, const d
 
 template <class C>
 __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
-  constexpr int W = C::W, Q = C::Q, NEN = C::NEN, NQ = C::NQ, E = C::E;
+  constexpr int W = C::W, Q = C::Q, NEN = C::NEN, NQ = C::NQ;
+  // element-level sizes (stages 0-1, 7-8: EB network batches at once); the network stages use Q
+  constexpr int QE = C::QE, EE = C::EE;
   constexpr int LDA = C::LDA, LDS = C::LDS, KT2 = C::KT2;
   extern __shared__ __align__(16) double smem[];
   const int L = A.ncm.L;
@@ -745,6 +761,7 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
   double* swq = smem + sm.wq;
   double* qNp = smem + sm.qN;
   double* stab = smem + sm.tab;
+  double* qgH = smem + sm.qgH;
   double* qA = smem + sm.qA;
   double* qP = smem + sm.qP;
   double* post = smem + sm.post;
@@ -755,7 +772,7 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
   const NcmDev& m = A.ncm;
   const bool skips = m.skip_h != nullptr;
   const bool fwd = Smem<C>::fwd_path(L, skips);
-  const int64_t n_batches = (A.el_count + E - 1) / E;
+  const int64_t n_batches = (A.el_count + EE - 1) / EE;
   const size_t frag_layer = (size_t)2 * W * W;  // W and W^T fragments per hidden layer
   {  // the activation table of this path (256 entries on the forward sweep, 64 otherwise)
     const int tb0 = fwd ? act_tab_offset<C::TB_FWD>() : 0, tbn = fwd ? ActTab<C::TB_FWD>::SIZE : ActTab<6>::SIZE;
@@ -773,16 +790,16 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
   double trc_max = 0.0;  // running max of tr C = I1 over this thread's qps (stage 1 threads)
 #if COMMET_PREFETCH
   // register prefetch of one batch's element inputs: (a) dN/dX, w, conn; (b) the u gather
-  constexpr int NG2 = E * NQ * NEN * 3 / 2, NU = E * NEN * 3;
+  constexpr int NG2 = EE * NQ * NEN * 3 / 2, NU = EE * NEN * 3;
   constexpr int PG = (NG2 + C::NTHR - 1) / C::NTHR, PU = (NU + C::NTHR - 1) / C::NTHR;
   double2 pf_g[PG];
   double pf_u[PU], pf_w = 0.0;
   int pf_c[PU];
 
   auto pf_load_a = [&](int64_t b) {
-    const int64_t f0 = A.el_begin + b * E;
+    const int64_t f0 = A.el_begin + b * EE;
     const int64_t frem = A.el_begin + A.el_count - f0;
-    const int fne = frem < E ? (int)frem : E;
+    const int fne = frem < EE ? (int)frem : EE;
     const double2* src = reinterpret_cast<const double2*>(A.gradN + (size_t)f0 * NQ * NEN * 3);
     const int n2 = fne * NQ * NEN * 3 / 2;
 #pragma unroll
@@ -796,7 +813,7 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
       const int e = x / (NEN * 3), ai = x % (NEN * 3);
       pf_c[i] = (x < NU && e < fne) ? __ldg(A.conn + (f0 + e) * NEN + ai / 3) : -1;  // raw: no use here
     }
-    if (tid < Q) pf_w = tid < fne * NQ ? __ldg(A.qp_w + f0 * NQ + tid) : 0.0;
+    if (tid < QE) pf_w = tid < fne * NQ ? __ldg(A.qp_w + f0 * NQ + tid) : 0.0;
   };
   auto pf_load_b = [&]() {
 #pragma unroll
@@ -815,7 +832,7 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
       const int x = tid + i * C::NTHR;
       if (x < NU) sue[x] = pf_u[i];
     }
-    if (tid < Q) swq[tid] = pf_w;
+    if (tid < QE) swq[tid] = pf_w;
   };
 #endif
 
@@ -826,9 +843,9 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
   };
 
   for (int64_t batch = blockIdx.x; batch < n_batches; batch += gridDim.x) {
-    const int64_t e0 = A.el_begin + batch * E;
+    const int64_t e0 = A.el_begin + batch * EE;
     const int64_t rem = A.el_begin + A.el_count - e0;
-    const int ne = rem < E ? (int)rem : E;
+    const int ne = rem < EE ? (int)rem : EE;
     int cur = 0;  // act column block holding the current layer's input (value / adjoint passes)
 #ifdef COMMET_DEBUG_CHECKS
     // race / stale-read check (debug builds, tools/race_check.py): every shared buffer except the
@@ -862,13 +879,13 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
       const double2* src = reinterpret_cast<const double2*>(A.gradN + (size_t)e0 * NQ * NEN * 3);
       double2* dst = reinterpret_cast<double2*>(sgN);
       const int n2 = ne * NQ * NEN * 3 / 2;
-      for (int x = tid; x < E * NQ * NEN * 3 / 2; x += C::NTHR)
+      for (int x = tid; x < EE * NQ * NEN * 3 / 2; x += C::NTHR)
         dst[x] = x < n2 ? __ldg(src + x) : make_double2(0.0, 0.0);
-      for (int x = tid; x < E * NEN * 3; x += C::NTHR) {
+      for (int x = tid; x < EE * NEN * 3; x += C::NTHR) {
         const int e = x / (NEN * 3), ai = x % (NEN * 3);
         sue[x] = e < ne ? __ldg(A.u + 3 * (int64_t)__ldg(A.conn + (e0 + e) * NEN + ai / 3) + ai % 3) : 0.0;
       }
-      for (int x = tid; x < Q; x += C::NTHR) swq[x] = x < ne * NQ ? __ldg(A.qp_w + e0 * NQ + x) : 0.0;
+      for (int x = tid; x < QE; x += C::NTHR) swq[x] = x < ne * NQ ? __ldg(A.qp_w + e0 * NQ + x) : 0.0;
     }
 #endif
     }  // MODE
@@ -876,7 +893,7 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
     STAGE_MARK(0)
 
     // ---- stage 1: kinematics ------------------------------------------------------
-    if (tid < Q) {
+    if (tid < QE) {
       const int q = tid, e = q / NQ;
       const double* gq = sgN + q * NEN * 3;
       const double* ue = sue + e * NEN * 3;
@@ -930,6 +947,13 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
 #endif
     STAGE_MARK(1)
 
+    // ---- stages 2-6, once per network batch of Q qps (EB of them per element batch) ----------
+    double* const qk_all = qk;
+    double* const gsk_all = gsk;
+    for (int h = 0; h < C::EB; h++) {
+    double* qk = qk_all + h * Q * C::NK;    // this network batch's inputs and skip gradients
+    double* gsk = gsk_all + h * Q * C::NK;
+    (void)qk; (void)gsk;
 #ifdef COMMET_EXP_SKIP_NCM
     if (false) {
 #endif
@@ -1318,6 +1342,28 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
 #ifdef COMMET_EXP_SKIP_NCM
     }
 #endif
+    if constexpr (C::EB > 1) {  // (g, H) of this network batch for the element stage
+      if (tid < Q) {
+        const int q = tid;
+        double* o = qgH + (h * Q + q) * C::NKH;
+#pragma unroll
+        for (int x = 0; x < C::NK; x++) o[x] = qg[q * C::NK + x];
+#pragma unroll
+        for (int x = 0; x < C::NH; x++) {
+          double v = qH[q * C::NH + x];
+          if (L > 1)
+#pragma unroll
+            for (int r = 0; r < C::JMG; r++) v += hred[(r * Q + q) * C::NH + x];
+          if constexpr (C::FWDC)
+            if (fwd && L == 3)
+#pragma unroll
+              for (int r = 0; r < C::VMG; r++) v += hred[((C::JMG + r) * Q + q) * C::NH + x];
+          o[C::NK + x] = v;
+        }
+      }
+      __syncthreads();
+    }
+    }  // network batches
 #ifdef COMMET_EXP_SKIP_ELEM
     if (false) {
 #endif
@@ -1332,16 +1378,21 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
     // thread per qp
     // (analytic networks: the CANN / Gent-Thomas instantiation (16 qps) only -- every warp repeats the
     // per-qp network, which for the ICKAN's forward mode (32 qps) costs more than it saves: 5.8 -> 9.3 ms)
-    constexpr bool PAR7 = ((COMMET_POST_PAR && C::NET == 0) || (COMMET_POST_PAR_NET1 && C::NET == 1 && C::Q == 16)) &&
+    constexpr bool PAR7 = ((COMMET_POST_PAR && C::NET == 0) || (COMMET_POST_PAR_NET1 && C::NET == 1 && C::MINB == COMMET_ANALYTIC_MINB)) &&
                           C::KIN < 2 && C::NWARP == 4;
 #ifdef COMMET_EXP_SKIP_7A  // timing experiments only
     if (false) {
 #else
-    if (PAR7 ? lane < Q : tid < Q) {
+    if (PAR7 ? lane < QE : tid < QE) {
 #endif
       const int q = PAR7 ? lane : tid;
       double gq[C::NK], H6[C::NH];
-      if constexpr (C::NET == 0) {
+      if constexpr (C::NET == 0 && C::EB > 1) {
+#pragma unroll
+        for (int x = 0; x < C::NK; x++) gq[x] = qgH[q * C::NKH + x];
+#pragma unroll
+        for (int x = 0; x < C::NH; x++) H6[x] = qgH[q * C::NKH + C::NK + x];
+      } else if constexpr (C::NET == 0) {
 #pragma unroll
         for (int x = 0; x < C::NK; x++) gq[x] = qg[q * C::NK + x];
 #pragma unroll
@@ -1379,11 +1430,11 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
     // ---- stage 7b: A_q (81 entries, scaled by w), one (q, iJ) row per item ------------------
     // (three rows per item only with 16+ qps per batch: at Q = 8 the 24 items leave most threads
     // idle -- measured c4 38.0 -> 40.3 ms -- while at Q = 16 it is 0.2 % faster)
-    if constexpr (C::KIN >= 2 || !COMMET_ROWS3 || C::Q < 16) {
+    if constexpr (C::KIN >= 2 || !COMMET_ROWS3 || QE < 16) {
 #ifdef COMMET_EXP_SKIP_7B  // timing experiments only
     for (int it = tid; it < 0; it += C::NTHR) {
 #else
-    for (int it = tid; it < Q * 9; it += C::NTHR) {
+    for (int it = tid; it < QE * 9; it += C::NTHR) {
 #endif
       const int q = it / 9, iJ = it % 9;
       if constexpr (C::KIN >= 2)
@@ -1392,7 +1443,7 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
         tangent_row(post + q * PS, iJ, qA + q * 81 + iJ * 9);
     }
     } else {  // three rows (i, J = 0..2) per item: the qp's factors loaded once for the three
-      for (int it = tid; it < Q * 3; it += C::NTHR)
+      for (int it = tid; it < QE * 3; it += C::NTHR)
         tangent_rows_i(post + (it / 3) * PS, it % 3, qA + (it / 3) * 81 + (it % 3) * 27);
     }
     __syncthreads();
@@ -1523,7 +1574,7 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
     }
     } else {
     // ---- stage 8a: X[q][a][i][kL] = sum_J dN_aJ A_q[iJ][kL] -----------------------------------
-    for (int it = tid; it < Q * 3 * NEN; it += C::NTHR) {
+    for (int it = tid; it < QE * 3 * NEN; it += C::NTHR) {
       const int a = it % NEN, qi = it / NEN, i = qi % 3, q = qi / 3;
       const double* ga = sgN + (q * NEN + a) * 3;
       const double g0 = ga[0], g1 = ga[1], g2 = ga[2];
@@ -2085,7 +2136,7 @@ static int launch_k(const AsmArgs& a, cudaStream_t st, int* launches) {
     if (a.ncm.net == 0 && a.ncm.w == 64) return launch_cfg<Cfg<64, 16, NEN, NQ, 3, 0, 0>>(a, st, launches);
     if (a.ncm.net == 0 && a.ncm.w == 128) return launch_cfg<Cfg<128, 8, NEN, NQ, 3, 0, 0>>(a, st, launches);
     if (a.ncm.net == 1 || a.ncm.net == 2)  // CANN / Gent-Thomas (element-stage tuning)
-      return launch_cfg<Cfg<16, 16, NEN, NQ, COMMET_ANALYTIC_MINB, 1, 0>>(a, st, launches);
+      return launch_cfg<Cfg<16, COMMET_ANALYTIC_Q, NEN, NQ, COMMET_ANALYTIC_MINB, 1, 0>>(a, st, launches);
   }
   return (int)cudaErrorInvalidValue;
 #else
@@ -2098,7 +2149,9 @@ static int launch_k(const AsmArgs& a, cudaStream_t st, int* launches) {
   } else {
     if (a.ncm.net == 3)  // ICKAN: its per-qp forward mode needs the registers (4 CTAs/SM: spills, -14 %)
       return launch_cfg<Cfg<16, 32, NEN, NQ, COMMET_ICKAN_MINB, 1, K>>(a, st, launches);
-    if (a.ncm.net != 0) return launch_cfg<Cfg<16, 16, NEN, NQ, COMMET_ANALYTIC_MINB, 1, K>>(a, st, launches);
+    // (tet10 keeps 16 qps: its scalar element stage's X buffer grows with the batch)
+    if (a.ncm.net != 0)
+      return launch_cfg<Cfg<16, NEN == 8 ? COMMET_ANALYTIC_Q : 16, NEN, NQ, COMMET_ANALYTIC_MINB, 1, K>>(a, st, launches);
   }
   // the forward-sweep ICNN (w = 64 / 128, L = 2 or 3, no hidden skips) on hex8: warp-specialised
   // kernel (tet10 keeps the one-role kernel: its scalar element stage needs the aliased X buffer)
