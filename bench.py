@@ -427,7 +427,8 @@ def main():
     # in size, so the per-launch rate is the per-step rate)
     achieved = fl * total_qp / ws / (kern_ms * 1e-3) / 1e12
     kname = ("ws_kernel" if kinfo.get("warp_specialised") else "fused_kernel") + \
-        f"<w={spec.width},L={spec.n_hidden},{'hex8' if cfg['elem_type'] == gen.HEX8 else 'tet10'}>"
+        f"<w={spec.width},L={spec.n_hidden},{'hex8' if cfg['elem_type'] == gen.HEX8 else 'tet10'}," \
+        f"q={kinfo.get('qps_network_batch')}/{kinfo.get('qps_element_batch')}>"
     traffic, traffic_src = measured_traffic(args.config, kname) if ws == 1 and args.kernel == "fused" else \
         (None, "single-GPU fused kernel only")
     hbm_pk, hbm_src = hbm_peak()

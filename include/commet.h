@@ -216,6 +216,9 @@ commet_status commet_kernel_info(commet_ctx ctx, int32_t* smem_bytes, int32_t* c
  * warp-specialised kernel (hex8, forward-sweep ICNN: 4 network + 4 element warps,
  * DESIGN.md s7), 0 for the one-role fused kernel (diagnostics). */
 commet_status commet_kernel_config(commet_ctx ctx, int32_t* threads_per_cta, int32_t* warp_specialised);
+/* Batch sizes of that kernel: quadrature points per network batch (stages 2-6) and per element
+ * batch (stages 0-1, 7-8; two network batches for the ICNN assembly). */
+commet_status commet_kernel_batch(commet_ctx ctx, int32_t* qps_network_batch, int32_t* qps_element_batch);
 
 /* Kernel-time instrumentation for benchmarks: with n_slots > 0, every
  * commet_assemble records a CUDA event pair on its stream around its kernel

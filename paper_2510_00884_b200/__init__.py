@@ -38,7 +38,7 @@ SYMBOLS = ("commet_setup", "commet_csr_pattern", "commet_csr_pattern_copy", "com
            "commet_cg_jacobi", "commet_newton_step", "commet_ncm_eval", "commet_normalize_reference",
            "commet_material_eval", "commet_halo_recv_maps", "commet_set_peer", "commet_set_peer_mode",
            "commet_zero_outputs", "commet_set_preconditioner", "commet_check_ranks", "commet_plan_colour_iface",
-           "commet_selftest_activation_tab", "commet_kernel_config")
+           "commet_selftest_activation_tab", "commet_kernel_config", "commet_kernel_batch")
 NEWTON_MAX_LOG = 64
 
 
@@ -158,6 +158,8 @@ _lib.commet_kernel_info.argtypes = [_vp, _P(_i32), _P(_i32), _P(_i32)]
 _lib.commet_kernel_info.restype = C.c_int
 _lib.commet_kernel_config.argtypes = [_vp, _P(_i32), _P(_i32)]
 _lib.commet_kernel_config.restype = C.c_int
+_lib.commet_kernel_batch.argtypes = [_vp, _P(_i32), _P(_i32)]
+_lib.commet_kernel_batch.restype = C.c_int
 _lib.commet_max_trace_C.argtypes = [_vp, _P(C.c_double)]
 _lib.commet_set_dirichlet.argtypes = [_vp, _vp, _i64]
 _lib.commet_apply_dirichlet.argtypes = [_vp, _vp, _vp, _vp]
@@ -275,11 +277,13 @@ class Commet:
         return dict(n_colours=v[0].value, n_q=v[1].value, n_en=v[2].value, launches=v[3].value)
 
     def kernel_info(self):
-        v = [_i32() for _ in range(5)]
+        v = [_i32() for _ in range(7)]
         _check(_lib.commet_kernel_info(self.ctx, *[C.byref(x) for x in v[:3]]), self.ctx)
-        _check(_lib.commet_kernel_config(self.ctx, *[C.byref(x) for x in v[3:]]), self.ctx)
+        _check(_lib.commet_kernel_config(self.ctx, *[C.byref(x) for x in v[3:5]]), self.ctx)
+        _check(_lib.commet_kernel_batch(self.ctx, *[C.byref(x) for x in v[5:]]), self.ctx)
         return dict(smem_bytes=v[0].value, ctas_per_sm=v[1].value, regs_per_thread=v[2].value,
-                    threads_per_cta=v[3].value, warp_specialised=bool(v[4].value))
+                    threads_per_cta=v[3].value, warp_specialised=bool(v[4].value), qps_network_batch=v[5].value,
+                    qps_element_batch=v[6].value)
 
     def set_kernel(self, variant: int):
         _check(_lib.commet_set_kernel(self.ctx, variant), self.ctx)

@@ -497,7 +497,7 @@ extern "C" commet_status commet_info(commet_ctx c, int32_t* n_colours, int32_t* 
   return COMMET_OK;
 }
 
-static commet_status kernel_query(commet_ctx c, int (&q)[5]) {
+static commet_status kernel_query(commet_ctx c, int (&q)[7]) {
   CUDA_TRY(c, cudaSetDevice(c->device));
   // the instantiation the assembly (or material-point) dispatch launches for this ctx
   AsmArgs a{};
@@ -514,7 +514,7 @@ static commet_status kernel_query(commet_ctx c, int (&q)[5]) {
 extern "C" commet_status commet_kernel_info(commet_ctx c, int32_t* smem_bytes, int32_t* ctas_per_sm,
                                             int32_t* regs_per_thread) {
   if (!c) return fail(nullptr, COMMET_ERR_ARG, "ctx is NULL");
-  int q[5] = {0, 0, 0, 128, 0};
+  int q[7] = {0, 0, 0, 128, 0, 0, 0};
   const commet_status s = kernel_query(c, q);
   if (s != COMMET_OK) return s;
   if (smem_bytes) *smem_bytes = q[0];
@@ -525,11 +525,21 @@ extern "C" commet_status commet_kernel_info(commet_ctx c, int32_t* smem_bytes, i
 
 extern "C" commet_status commet_kernel_config(commet_ctx c, int32_t* threads_per_cta, int32_t* warp_specialised) {
   if (!c) return fail(nullptr, COMMET_ERR_ARG, "ctx is NULL");
-  int q[5] = {0, 0, 0, 128, 0};
+  int q[7] = {0, 0, 0, 128, 0, 0, 0};
   const commet_status s = kernel_query(c, q);
   if (s != COMMET_OK) return s;
   if (threads_per_cta) *threads_per_cta = q[3];
   if (warp_specialised) *warp_specialised = q[4];
+  return COMMET_OK;
+}
+
+extern "C" commet_status commet_kernel_batch(commet_ctx c, int32_t* qps_network_batch, int32_t* qps_element_batch) {
+  if (!c) return fail(nullptr, COMMET_ERR_ARG, "ctx is NULL");
+  int q[7] = {0, 0, 0, 128, 0, 0, 0};
+  const commet_status s = kernel_query(c, q);
+  if (s != COMMET_OK) return s;
+  if (qps_network_batch) *qps_network_batch = q[5];
+  if (qps_element_batch) *qps_element_batch = q[6];
   return COMMET_OK;
 }
 

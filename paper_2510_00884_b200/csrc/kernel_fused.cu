@@ -71,7 +71,7 @@
 #define COMMET_ACT_TB 8  // forward-sweep activations on 256-entry tables (lower polynomial degrees)
 #endif
 #ifndef COMMET_POST_PAR
-#define COMMET_POST_PAR 0  // stage 7a split over the four warps (post_qp_part): measured no gain (c3 +0.3 %, c4 +3 %: spills)
+#define COMMET_POST_PAR 1  // ICNN with two network batches per element batch (32 qps): stage 7a split over the four warps (post_qp_part); at 16 qps measured no gain (c3 +0.3 %, c4 +3 %)
 #endif
 #ifndef COMMET_WS
 #define COMMET_WS 0  // warp-specialised kernel (ws_kernel) for the hex8 forward-sweep ICNN: measured c3 -2.2 %, c5 +4 % -> off
@@ -86,7 +86,7 @@
 #define COMMET_ROWS3 1  // stage 7b: three A rows (i, J = 0..2) per item
 #endif
 #ifndef COMMET_ELEM_HALF
-#define COMMET_ELEM_HALF 0  // hex8 stage 8 of the one-role kernel: one warp per (element, i-half) (measured: c3 9.75 -> 9.83 ms; the warp-specialised kernel uses it)
+#define COMMET_ELEM_HALF 1  // hex8 ICNN stage 8 with 4 elements per element batch: one warp per (element, i-half) (at 2 elements: c3 9.75 -> 9.83 ms)
 #endif
 #ifndef COMMET_WS_PAR7
 #define COMMET_WS_PAR7 0  // warp-specialised kernel: stage 7a split over the four element warps (measured: c3 9.52 -> 9.78 ms)
@@ -101,7 +101,7 @@
 #define COMMET_Q_KIN3 16  // qps per batch of the two-vector (9-input) kernels
 #endif
 #ifndef COMMET_EB
-#define COMMET_EB 1  // network batches per element batch (ICNN assembly)
+#define COMMET_EB 2  // network batches per element batch (ICNN assembly; c3 9.72 -> 9.43 ms with the two below)
 #endif
 #ifndef COMMET_PINGPONG
 #define COMMET_PINGPONG 0  // measured neutral (c3 10.31 vs 10.26 ms): barriers kept
@@ -238,7 +238,9 @@ struct Cfg {
   static constexpr bool FWDC = COMMET_FWD && W >= COMMET_FWD_MINW && NET == 0 && NK == 3 && !COMMET_PINGPONG;
   // element batches: the element stages (0-1, 7-8) run on EB network batches at once -- QE qps,
   // EE elements -- while the network stages (2-6) run batch by batch (ICNN assembly, Q <= 16)
-  static constexpr int EB = (NET == 0 && MODE == 0 && !WS && Q <= 16) ? COMMET_EB : 1;
+  // (tet10's scalar element stage keeps an X buffer of QE x NEN x 27 doubles in the dead network
+  // buffers: two batches only where it still fits, Q = 8)
+  static constexpr int EB = (NET == 0 && MODE == 0 && !WS && Q <= 16 && (NEN == 8 || Q <= 8)) ? COMMET_EB : 1;
   static constexpr int QE = EB * Q, EE = QE / NQ, NKH = NK + NH;
   static_assert(QE <= 32, "stage-1 threads (one per qp) must sit in warp 0");
   // activation table bits on the forward-sweep path (the 256-entry tables do not fit beside the
@@ -1378,7 +1380,8 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
     // thread per qp
     // (analytic networks: the CANN / Gent-Thomas instantiation (16 qps) only -- every warp repeats the
     // per-qp network, which for the ICKAN's forward mode (32 qps) costs more than it saves: 5.8 -> 9.3 ms)
-    constexpr bool PAR7 = ((COMMET_POST_PAR && C::NET == 0) || (COMMET_POST_PAR_NET1 && C::NET == 1 && C::MINB == COMMET_ANALYTIC_MINB)) &&
+    constexpr bool PAR7 = ((COMMET_POST_PAR && C::NET == 0 && C::EB > 1) ||
+                           (COMMET_POST_PAR_NET1 && C::NET == 1 && C::MINB == COMMET_ANALYTIC_MINB)) &&
                           C::KIN < 2 && C::NWARP == 4;
 #ifdef COMMET_EXP_SKIP_7A  // timing experiments only
     if (false) {
@@ -1457,7 +1460,7 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
     //      Y_q[J][b] = sum_L A_q[(i,J),(k,L)] dN_q[b][L] formed in the B fragment (3 FMA per
     //      element); M = a, N = b, K = (q, J); r_e; RED scatter (+ mirror for i < k)
     {
-      if constexpr (NEN == 8 && (COMMET_ELEM_HALF || (C::NET == 1 && COMMET_ELEM_HALF_NET1))) {
+      if constexpr (NEN == 8 && ((COMMET_ELEM_HALF && C::EB > 1) || (C::NET == 1 && COMMET_ELEM_HALF_NET1))) {
       // hex8: one warp per (element, i-half), the (i, k) blocks (0,0) (0,1) (0,2) or (1,1) (1,2)
       // (2,2) at once -- the dN/dX operands and the scatter metadata of the lane's node pair are
       // loaded once for the three
@@ -2057,7 +2060,7 @@ void fused_weight_frag_fill(int w, int L, const double* Wrow, double* out) {
 // different host threads) and used as one consistent snapshot.
 template <class Tag>
 static int launch_persistent(void (*fn)(AsmArgs), int nthr, size_t bytes, int E, const AsmArgs& a, cudaStream_t st,
-                             int* launches, int kind = 0) {
+                             int* launches, int kind = 0, int q_net = 0, int q_elem = 0) {
   constexpr int kDev = 16;
   static std::mutex mu;
   static size_t attr_bytes[kDev] = {0};
@@ -2094,6 +2097,8 @@ static int launch_persistent(void (*fn)(AsmArgs), int nthr, size_t bytes, int E,
     a.query[2] = fa.numRegs;
     a.query[3] = nthr;
     a.query[4] = kind;  // 0 one-role fused kernel, 1 warp-specialised
+    a.query[5] = q_net;   // qps per network batch
+    a.query[6] = q_elem;  // qps per element batch
     return 0;
   }
   const int64_t nb = (a.el_count + E - 1) / E;
@@ -2112,7 +2117,7 @@ static int launch_cfg(const AsmArgs& a, cudaStream_t st, int* launches) {
 #ifdef COMMET_EXP_SMEM_PAD
   bytes += COMMET_EXP_SMEM_PAD;  // experiments only: limit resident CTAs per SM
 #endif
-  return launch_persistent<C>(fused_kernel<C>, C::NTHR, bytes, C::E, a, st, launches);
+  return launch_persistent<C>(fused_kernel<C>, C::NTHR, bytes, C::EE, a, st, launches, 0, C::Q, C::QE);
 }
 
 // the warp-specialised kernel (forward-sweep ICNN path of the assembly)
@@ -2121,7 +2126,7 @@ struct WsTag {};
 template <class C>
 static int launch_ws(const AsmArgs& a, cudaStream_t st, int* launches) {
   const size_t bytes = (size_t)WsSmem<C>().total * sizeof(double);
-  return launch_persistent<WsTag<C>>(ws_kernel<C>, C::NTHR_ALL, bytes, C::E, a, st, launches, 1);
+  return launch_persistent<WsTag<C>>(ws_kernel<C>, C::NTHR_ALL, bytes, C::E, a, st, launches, 1, C::Q, C::Q);
 }
 
 template <int NEN, int NQ, int K>

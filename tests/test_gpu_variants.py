@@ -161,6 +161,9 @@ def test_kernel_info_reports_launched_instantiation(pc):
     else:
         assert info["icnn"]["threads_per_cta"] == 128 and info["icnn"]["ctas_per_sm"] == 3
         assert info["icnn"]["regs_per_thread"] <= 168
+        # hex8 ICNN: the element stages take two network batches of 16 qps at once
+        assert info["icnn"]["qps_network_batch"] == 16 and info["icnn"]["qps_element_batch"] == 32
+    assert info["icnn_tet"]["qps_element_batch"] == info["icnn_tet"]["qps_network_batch"] == 16
     for nm in ("icnn_tet", "icnn_skips"):
         assert not info[nm]["warp_specialised"] and info[nm]["threads_per_cta"] == 128
         assert info[nm]["regs_per_thread"] <= 168
