@@ -19,7 +19,7 @@ import tempfile
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 LIB = os.environ.get("COMMET_LIB") or os.path.join(ROOT, "paper_2510_00884_b200", "libcommet.so")
 CSRC = os.path.join(ROOT, "paper_2510_00884_b200", "csrc")
-DEFAULT_K = "_ZN6commet12fused_kernelINS_3CfgILi64ELi16ELi8ELi8ELi3ELi0ELi0ELi0ELi4EEEEEvNS_7AsmArgsE"
+DEFAULT_K = "_ZN6commet12fused_kernelINS_3CfgILi64ELi16ELi8ELi8ELi3ELi0ELi0ELi0ELi4ELi0EEEEEvNS_7AsmArgsE"
 
 
 def line_table(kernel):
