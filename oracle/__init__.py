@@ -38,7 +38,7 @@ class _Ncm(C.Structure):
                 ("kan_nb", C.c_int32), ("kan_k", C.c_int32), ("kan_grid", C.c_void_p), ("kan_w", C.c_void_p),
                 ("kan_c", C.c_void_p), ("a0", C.c_double * 3), ("n_sv", C.c_int32), ("a1", C.c_double * 3)]
 
-KIN = {"standard": 0, "isochoric": 1, "anisotropic": 2}
+KIN = {"standard": 0, "isochoric": 1, "anisotropic": 2, "isochoric_anisotropic": 3}
 NET = {"icnn": 0, "cann": 1, "gent_thomas": 2, "ickan": 3}
 
 

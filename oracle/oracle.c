@@ -38,7 +38,8 @@ typedef struct {
   const double* skip_hidden; /* [L-1][w][3] or NULL: B^(k), k = 2..L */
   double kappa;              /* volumetric penalty kappa (J-1)^2 */
   double ref_shift;          /* s0: W -= s0 (J-1) (off when 0) */
-  int32_t kinematics;        /* 0: K = (I1-3, I2-3, J-1); 1: isochoric (Ibar1-3, Ibar2-3, J-1) (App. A.2.2) */
+  int32_t kinematics;        /* 0: K = (I1-3, I2-3, J-1); 1: isochoric (Ibar1-3, Ibar2-3, J-1) (App. A.2.2);
+                                2: anisotropic (App. A.2.1); 3: isochoric anisotropic (App. A.2.2 with Ibar4/5,ij) */
   int32_t network;           /* 0: ICNN (Eq. icnn, Alg. 4); 1: CANN (Eq. cann-def); 2: Gent-Thomas (App. C) */
   int32_t cann_n;            /* CANN: branches per kinematic input */
   const int32_t* cann_f;     /* CANN [3][n][3]: f0 (0 id, 1 Macaulay, 2 abs), f1 power (1..3),
@@ -52,7 +53,7 @@ typedef struct {
   const double* kan_grid;    /* [R][2] xmin, xmax */
   const double* kan_w;       /* [edges] */
   const double* kan_c;       /* [edges][nb] */
-  double a0[3];              /* anisotropic kinematics (kinematics = 2): structural vector A0 (reference) */
+  double a0[3];              /* anisotropic kinematics (kinematics = 2, 3): structural vector A0 (reference) */
   int32_t n_sv;              /* anisotropic: number of structural vectors, 1 (0 = 1) or 2 (a0, a1) */
   double a1[3];              /* anisotropic, n_sv = 2: the second structural vector */
 } oracle_ncm;
@@ -548,6 +549,107 @@ static void anisotropic_S_CC(const oracle_ncm* m, const double F[9], double Jd, 
 }
 
 /*
+ * Isochoric anisotropic kinematics (App. A.2.2, the set
+ * Ibar_m, m in {1, 2, (4,ij), (5,ij)}, with the App. A.2.1 table's I4,ij / I5,ij rows; reading R29):
+ *   Fbar = J^-1/3 F, Bbar = Fbar Fbar^T, abar_i = Fbar A_i;  Ibar_m = I3^e_m I_m,
+ *   e_m = -1/3 (m = 1, (4,ij)), -2/3 (m = 2, (5,ij))
+ *   Ibar1 = tr Bbar, Ibar2 = (tr Bbar^2 - tr(Bbar^2))/2, Ibar4,ij = abar_i.abar_j, Ibar5,ij = abar_i.Bbar abar_j
+ *   Gbar1 = Bbar, GGbar1 = O;  Gbar2 = Bbar tr Bbar - Bbar^2, GGbar2 = Bbar(x)Bbar - Bbar(x)_Bbar
+ *   Gbar4,ij = sym(abar_i (x) abar_j), GGbar4,ij = O
+ *   Gbar5,ij = sym(abar_i (x) Bbar abar_j) + sym(abar_j (x) Bbar abar_i)       (R28, R29: Bbar, not B)
+ *   GGbar5,ij = Bbar (x)_ sym(abar_i (x) abar_j) + sym(abar_i (x) abar_j) (x)_ Bbar
+ *   G^m = Gbar^m + e_m Ibar_m I
+ *   GG^m = GGbar^m + e_m (I(x)Gbar^m + Gbar^m(x)I + Ibar_m (e_m I(x)I - I(x)_I))
+ *   J: G = J/2 I, GG = J/4 (I(x)I - 2 I(x)_I)
+ * inputs in the order (Ibar1, Ibar2, J, per pair Ibar4,ij, Ibar5,ij); then tau, c and the pull-back
+ * (spatial_to_material).
+ */
+static void isochoric_anisotropic_S_CC(const oracle_ncm* m, const double F[9], double Jd, const double* g,
+                                       const double* H, double S[9], double CC[81]) {
+  const double* A[2];
+  int pi[3], pj[3];
+  const int np = aniso_pairs(m, A, pi, pj), nk = 3 + 2 * np;
+  const double c13 = pow(Jd, -1.0 / 3.0);
+  double Fb[9], Bb[9], Bb2[9], ab[2][3], Bab[2][3];
+  for (int x = 0; x < 9; x++) Fb[x] = c13 * F[x];
+  for (int i = 0; i < 3; i++)
+    for (int j = 0; j < 3; j++)
+      Bb[i * 3 + j] = Fb[i * 3] * Fb[j * 3] + Fb[i * 3 + 1] * Fb[j * 3 + 1] + Fb[i * 3 + 2] * Fb[j * 3 + 2];
+  for (int i = 0; i < 3; i++)
+    for (int j = 0; j < 3; j++) Bb2[i * 3 + j] = Bb[i * 3] * Bb[j] + Bb[i * 3 + 1] * Bb[3 + j] + Bb[i * 3 + 2] * Bb[6 + j];
+  for (int v = 0; v < 2; v++)
+    for (int i = 0; i < 3; i++) ab[v][i] = Fb[i * 3] * A[v][0] + Fb[i * 3 + 1] * A[v][1] + Fb[i * 3 + 2] * A[v][2];
+  for (int v = 0; v < 2; v++)
+    for (int i = 0; i < 3; i++) Bab[v][i] = Bb[i * 3] * ab[v][0] + Bb[i * 3 + 1] * ab[v][1] + Bb[i * 3 + 2] * ab[v][2];
+  const double Ib1 = Bb[0] + Bb[4] + Bb[8];
+  double Ib[9], e[9], Gb[9][9], GGb[9][81], G[9][9], GG[9][81];
+  Ib[0] = Ib1;
+  Ib[1] = 0.5 * (Ib1 * Ib1 - (Bb2[0] + Bb2[4] + Bb2[8]));
+  e[0] = -1.0 / 3.0;
+  e[1] = -2.0 / 3.0;
+  for (int ij = 0; ij < 9; ij++) {
+    Gb[0][ij] = Bb[ij];
+    Gb[1][ij] = Bb[ij] * Ib1 - Bb2[ij];
+  }
+  for (int i = 0; i < 3; i++)
+    for (int j = 0; j < 3; j++)
+      for (int k = 0; k < 3; k++)
+        for (int l = 0; l < 3; l++) {
+          GGb[0][I4(i, j, k, l)] = 0.0;
+          GGb[1][I4(i, j, k, l)] = Bb[i * 3 + j] * Bb[k * 3 + l] -
+                                   0.5 * (Bb[i * 3 + k] * Bb[j * 3 + l] + Bb[i * 3 + l] * Bb[j * 3 + k]);
+        }
+  for (int p = 0; p < np; p++) {
+    const double *ai = ab[pi[p]], *aj = ab[pj[p]], *Bai = Bab[pi[p]], *Baj = Bab[pj[p]];
+    const int m4 = 3 + 2 * p, m5 = 4 + 2 * p;
+    double As[9];
+    Ib[m4] = ai[0] * aj[0] + ai[1] * aj[1] + ai[2] * aj[2];
+    Ib[m5] = ai[0] * Baj[0] + ai[1] * Baj[1] + ai[2] * Baj[2];
+    e[m4] = -1.0 / 3.0;
+    e[m5] = -2.0 / 3.0;
+    for (int i = 0; i < 3; i++)
+      for (int j = 0; j < 3; j++) {
+        As[i * 3 + j] = 0.5 * (ai[i] * aj[j] + aj[i] * ai[j]);
+        Gb[m4][i * 3 + j] = As[i * 3 + j];
+        Gb[m5][i * 3 + j] = 0.5 * (ai[i] * Baj[j] + Baj[i] * ai[j]) + 0.5 * (aj[i] * Bai[j] + Bai[i] * aj[j]);
+      }
+    for (int i = 0; i < 3; i++)
+      for (int j = 0; j < 3; j++)
+        for (int k = 0; k < 3; k++)
+          for (int l = 0; l < 3; l++) {
+            const int x = I4(i, j, k, l);
+            GGb[m4][x] = 0.0;
+            GGb[m5][x] = 0.5 * (Bb[i * 3 + k] * As[j * 3 + l] + Bb[i * 3 + l] * As[j * 3 + k]) +
+                         0.5 * (As[i * 3 + k] * Bb[j * 3 + l] + As[i * 3 + l] * Bb[j * 3 + k]);
+          }
+  }
+  for (int mm = 0; mm < nk; mm++) {
+    if (mm == 2) continue;
+    for (int i = 0; i < 3; i++)
+      for (int j = 0; j < 3; j++) {
+        G[mm][i * 3 + j] = Gb[mm][i * 3 + j] + e[mm] * Ib[mm] * (i == j);
+        for (int k = 0; k < 3; k++)
+          for (int l = 0; l < 3; l++) {
+            const double II = (double)((i == j) * (k == l));
+            const double IsI = 0.5 * ((i == k) * (j == l) + (i == l) * (j == k));
+            GG[mm][I4(i, j, k, l)] =
+                GGb[mm][I4(i, j, k, l)] +
+                e[mm] * ((i == j) * Gb[mm][k * 3 + l] + Gb[mm][i * 3 + j] * (k == l) + Ib[mm] * (e[mm] * II - IsI));
+          }
+      }
+  }
+  for (int i = 0; i < 3; i++)
+    for (int j = 0; j < 3; j++) {
+      G[2][i * 3 + j] = 0.5 * Jd * (i == j);
+      for (int k = 0; k < 3; k++)
+        for (int l = 0; l < 3; l++)
+          GG[2][I4(i, j, k, l)] = 0.25 * Jd * ((double)((i == j) * (k == l)) -
+                                                 ((i == k) * (j == l) + (i == l) * (j == k)));
+    }
+  spatial_to_material(F, nk, G, GG, g, H, S, CC);
+}
+
+/*
  * F (row-major F[i*3+J]) -> k, W, g, H (incl. penalty), S, CC, P, A.
  * Kinematic layer in material form:
  *   h1 = dI1/dC = I,  h2 = dI2/dC = I1 I - C,  h3 = dJ/dC = J/2 C^-1
@@ -587,14 +689,18 @@ double oracle_material_point(const oracle_ncm* m, const double F[9], double k_ou
   double I2 = 0.5 * (I1 * I1 - trC2);
   double Jd = det3(F);
   inv3(C, Ci);
-  if (m->kinematics == 2) { /* anisotropic: K = (I1-3, I2-3, J-1, per pair I4,ij - A_i.A_j, I5,ij - A_i.A_j) */
+  if (m->kinematics == 2 || m->kinematics == 3) {
+    /* anisotropic: K = (I1-3, I2-3, J-1, per pair I4,ij - A_i.A_j, I5,ij - A_i.A_j);
+     * isochoric anisotropic (3): K = (Ibar1-3, Ibar2-3, J-1, per pair Ibar4,ij - A_i.A_j, Ibar5,ij - A_i.A_j),
+     * Ibar1 = J^-2/3 I1, Ibar2 = J^-4/3 I2, Ibar4,ij = J^-2/3 I4,ij, Ibar5,ij = J^-4/3 I5,ij (App. A.2.2) */
+    const double a23 = m->kinematics == 3 ? pow(Jd, -2.0 / 3.0) : 1.0;
     const double* Av[2];
     int pi[3], pj[3];
     const int np = aniso_pairs(m, Av, pi, pj), nk = 3 + 2 * np;
     double CA[2][3];
     for (int v = 0; v < 2; v++)
       for (int I = 0; I < 3; I++) CA[v][I] = C[I * 3] * Av[v][0] + C[I * 3 + 1] * Av[v][1] + C[I * 3 + 2] * Av[v][2];
-    double kN[9] = {I1 - 3.0, I2 - 3.0, Jd - 1.0, 0, 0, 0, 0, 0, 0};
+    double kN[9] = {a23 * I1 - 3.0, a23 * a23 * I2 - 3.0, Jd - 1.0, 0, 0, 0, 0, 0, 0};
     for (int p = 0; p < np; p++) {
       const double *Ai = Av[pi[p]], *Aj = Av[pj[p]], *CAi = CA[pi[p]], *CAj = CA[pj[p]];
       double i4 = 0.0, i5 = 0.0, aa = 0.0;
@@ -603,15 +709,18 @@ double oracle_material_point(const oracle_ncm* m, const double F[9], double k_ou
         i5 += CAi[I] * CAj[I];  /* A_i.C^2 A_j = (C A_i).(C A_j) */
         aa += Ai[I] * Aj[I];
       }
-      kN[3 + 2 * p] = i4 - aa;
-      kN[4 + 2 * p] = i5 - aa;
+      kN[3 + 2 * p] = a23 * i4 - aa;
+      kN[4 + 2 * p] = a23 * a23 * i5 - aa;
     }
     double NN, gN[9], HN[81];
     if (oracle_ncm_eval_n(m, nk, kN, &NN, gN, HN) != 0) return ncm_failed(k_out, W_out, g_out, H_out, S, CC, P, A);
     const double WN = NN + m->kappa * (Jd - 1.0) * (Jd - 1.0) - m->ref_shift * (Jd - 1.0);
     gN[2] += 2.0 * m->kappa * (Jd - 1.0) - m->ref_shift;
     HN[2 * nk + 2] += 2.0 * m->kappa;
-    anisotropic_S_CC(m, F, Jd, gN, HN, S, CC);
+    if (m->kinematics == 3)
+      isochoric_anisotropic_S_CC(m, F, Jd, gN, HN, S, CC);
+    else
+      anisotropic_S_CC(m, F, Jd, gN, HN, S, CC);
     for (int i = 0; i < 3; i++)
       for (int J = 0; J < 3; J++) {
         double t = 0.0;

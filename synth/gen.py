@@ -268,11 +268,12 @@ def cann_params(n_branch: int = 4, seed: int = SEED_W, kinematics: str = "standa
                 skip_out=None, skip_hidden=None, cann_f=f, cann_w1=w1, cann_w2=w2, kappa=float(kappa), ref_shift=0.0)
 
 
-def anisotropic(ncm: dict, a0=(0.6, 0.8, 0.0), a1=None) -> dict:
+def anisotropic(ncm: dict, a0=(0.6, 0.8, 0.0), a1=None, isochoric: bool = False) -> dict:
     """The same network on anisotropic inputs K = (I1-3, I2-3, J-1, then per pair i <= j of the
     structural vectors I4,ij - A_i.A_j, I5,ij - A_i.A_j): one vector A0 (unit: I4-1, I5-1, 5
-    inputs), or two (A0, A1: pairs 00, 01, 11, 9 inputs; e.g. a fibre and a sheet direction)."""
-    d = dict(ncm, kinematics="anisotropic", a0=np.array(a0, np.float64))
+    inputs), or two (A0, A1: pairs 00, 01, 11, 9 inputs; e.g. a fibre and a sheet direction).
+    isochoric=True: the isochoric versions Ibar1, Ibar2, Ibar4,ij, Ibar5,ij (App. A.2.2)."""
+    d = dict(ncm, kinematics="isochoric_anisotropic" if isochoric else "anisotropic", a0=np.array(a0, np.float64))
     if a1 is not None:
         d["a1"] = np.array(a1, np.float64)
     return d

@@ -159,18 +159,22 @@ def energy_hd(F: list, ncm: dict):
     J = (F[0][0] * F[1][1] * F[2][2] + F[0][1] * F[1][2] * F[2][0] + F[0][2] * F[1][0] * F[2][1]
          - F[0][2] * F[1][1] * F[2][0] - F[0][0] * F[1][2] * F[2][1] - F[0][1] * F[1][0] * F[2][2])
     k = [I1 - 3.0, I2 - 3.0, J - 1.0]
-    if ncm.get("kinematics", "standard") == "anisotropic":
+    kin = ncm.get("kinematics", "standard")
+    if kin in ("anisotropic", "isochoric_anisotropic"):
         # Eq. standard-inv-II: I4,ij = A_i . C A_j, I5,ij = A_i . C^2 A_j over the pairs i <= j
-        # of the structural vectors; inputs I4,ij - A_i.A_j, I5,ij - A_i.A_j (zero at F = I)
+        # of the structural vectors; inputs I4,ij - A_i.A_j, I5,ij - A_i.A_j (zero at F = I).
+        # Isochoric (App. A.2.2): Ibar_m = I3^e_m I_m, e = -1/3 (I1, I4,ij), -2/3 (I2, I5,ij); I3^-1/3 = J^-2/3
+        s1 = hd_pow(J, -2.0 / 3.0) if kin == "isochoric_anisotropic" else HD(1.0)
+        s2 = s1 * s1
         vecs = [np.asarray(ncm["a0"], float)] + ([np.asarray(ncm["a1"], float)] if ncm.get("a1") is not None else [])
         CAs = [[sum((Cm[I][Jx] * v[Jx] for Jx in range(3)), HD(0.0)) for I in range(3)] for v in vecs]
-        k = [I1 - 3.0, I2 - 3.0, J - 1.0]
+        k = [s1 * I1 - 3.0, s2 * I2 - 3.0, J - 1.0]
         for i in range(len(vecs)):
             for j in range(i, len(vecs)):
                 aa = float(vecs[i] @ vecs[j])
                 I4 = sum((vecs[i][I] * CAs[j][I] for I in range(3)), HD(0.0))
                 I5 = sum((CAs[i][I] * CAs[j][I] for I in range(3)), HD(0.0))
-                k += [I4 - aa, I5 - aa]
+                k += [s1 * I4 - aa, s2 * I5 - aa]
     if ncm.get("kinematics", "standard") == "isochoric":
         a23 = hd_pow(J, -2.0 / 3.0)
         k = [a23 * I1 - 3.0, a23 * a23 * I2 - 3.0, J - 1.0]

@@ -35,6 +35,13 @@ VARIANTS = {
     "cann_two_vectors": lambda: anisotropic(cann_params(3, seed=8, n_in=9), A_FIBRE, A_SHEET),
     "ickan_two_vectors": lambda: anisotropic(ickan_params((9, 4, 1), nb=7, seed=9), A_FIBRE, A_SHEET),
     "icnn_two_vectors": lambda: anisotropic(ncm_weights(8, 2, 0.3, 17, 10.0, n_in=9), A_FIBRE, (0.0, 0.6, 0.8)),
+    # isochoric anisotropic inputs Ibar1, Ibar2, J, Ibar4,ij, Ibar5,ij (App. A.2.2, reading R29)
+    "icnn_iso_anisotropic": lambda: anisotropic(ncm_weights(8, 2, 0.3, 19, 10.0, n_in=5), isochoric=True),
+    "cann_iso_anisotropic": lambda: anisotropic(cann_params(4, seed=10, n_in=5), isochoric=True),
+    "cann_iso_two_vectors": lambda: anisotropic(cann_params(3, seed=12, n_in=9), A_FIBRE, (0.0, 0.6, 0.8),
+                                                isochoric=True),
+    "ickan_iso_two_vectors": lambda: anisotropic(ickan_params((9, 4, 1), nb=7, seed=13), A_FIBRE, A_SHEET,
+                                                 isochoric=True),
 }
 
 
@@ -59,6 +66,62 @@ def test_isochoric_invariance_and_objectivity():
             assert np.abs(kc[:2] - k[:2]).max() < 1e-13            # Ibar_m(cF) = Ibar_m(F)
         kq = oracle.material_point(m, rot(rng) @ F)["k"]
         assert np.abs(kq - k).max() < 1e-13
+
+
+def _isochoric_only(m, nk):
+    """The same model with no dependence on J: the network's J column (W1[:, 2] / the CANN's
+    branch weights of input 3) zeroed and kappa = 0, so W = N(Ibar...) depends on Cbar = J^-2/3 C only."""
+    m = dict(m, kappa=0.0)
+    if m.get("network", "icnn") == "cann":
+        w2 = np.array(m["cann_w2"], float)
+        w2[2] = 0.0
+        m["cann_w2"] = w2
+    else:
+        W1 = np.array(m["W1"], float)
+        W1[:, 2] = 0.0
+        m["W1"] = W1
+    return m
+
+
+@pytest.mark.parametrize("name,nk", [("icnn_iso_anisotropic", 5), ("cann_iso_anisotropic", 5),
+                                     ("cann_iso_two_vectors", 9)])
+def test_isochoric_anisotropic_deviatoric_stress(name, nk):
+    """An energy of the isochoric invariants alone is invariant under F -> cF, so the Kirchhoff
+    stress is deviatoric: P : F = tr(tau) = 0 for every F; differentiating P(F) : F = 0 once more
+    gives A : F + P = 0 (sum over iJ of F_iJ A_iJkL = -P_kL) -- a pin of the whole isochoric
+    G / GG table (App. A.2.2) independent of the hyper-dual derivatives."""
+    m = _isochoric_only(VARIANTS[name](), nk)
+    rng = np.random.default_rng(31)
+    for _ in range(4):
+        F = rand_F(rng)
+        o = oracle.material_point(m, F)
+        P, A = o["P"], o["A"]
+        assert abs(np.sum(P * F)) < 1e-13 * np.abs(P).max()
+        assert np.abs(np.einsum("ij,ijkl->kl", F, A) + P).max() < 1e-13 * np.abs(A).max()
+        # and the inputs are scale-invariant (except J - 1, input 3)
+        k1 = oracle.material_point(m, 1.37 * F)["k"]
+        assert np.abs(k1[:2] - o["k"][:2]).max() < 1e-13
+
+
+def test_isochoric_anisotropic_inputs_closed_form():
+    """Ibar4 = J^-2/3 A0.C A0 and Ibar5 = J^-4/3 A0.C^2 A0 (App. A.2.2 with e = -1/3, -2/3), checked
+    through the CANN's linear branch: a one-branch identity / x^1 / linear CANN gives
+    N = sum_m w2 w1 K_m, so W - kappa (J-1)^2 recovers sum_m c_m K_m."""
+    c = np.array([0.3, 0.2, 0.0, 0.5, 0.7])
+    m = dict(network="cann", kinematics="isochoric_anisotropic", width=8, n_hidden=1, W1=None, W=None, b=None,
+             a=None, skip_out=None, skip_hidden=None, cann_f=np.tile(np.array([0, 1, 0], np.int32), (5, 1, 1)),
+             cann_w1=np.ones((5, 1)), cann_w2=c[:, None].copy(), kappa=0.0, ref_shift=0.0,
+             a0=np.array([0.6, 0.8, 0.0]))
+    rng = np.random.default_rng(5)
+    A0 = m["a0"]
+    for _ in range(3):
+        F = rand_F(rng)
+        C = F.T @ F
+        J = np.linalg.det(F)
+        I1, I2 = np.trace(C), 0.5 * (np.trace(C) ** 2 - np.trace(C @ C))
+        K = [J ** (-2 / 3) * I1 - 3, J ** (-4 / 3) * I2 - 3, J - 1,
+             J ** (-2 / 3) * A0 @ C @ A0 - 1, J ** (-4 / 3) * A0 @ C @ C @ A0 - 1]
+        assert abs(oracle.material_point(m, F)["W"] - c @ K) < 1e-14
 
 
 # ---- CANN -------------------------------------------------------------------------

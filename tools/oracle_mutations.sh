@@ -52,4 +52,11 @@ mut "GG[m5][x] = 0.5 * (B[i * 3 + k] * As[j * 3 + l] + B[i * 3 + l] * As[j * 3 +
 mut "G[m5][i * 3 + j] = 0.5 * (ai[i] * Baj[j] + Baj[i] * ai[j]) + 0.5 * (aj[i] * Bai[j] + Bai[i] * aj[j]);" "G[m5][i * 3 + j] = (ai[i] * Baj[j] + Baj[i] * ai[j]);"
 mut "i4 += Ai[I] * CAj[I];   /* A_i.C A_j */" "i4 += Ai[I] * CAi[I];   /* A_i.C A_j */"
 mut "G[m4][i * 3 + j] = As[i * 3 + j];" "G[m4][i * 3 + j] = ai[i] * aj[j];"
+# isochoric anisotropic (App. A.2.2 with Ibar4,ij / Ibar5,ij; reading R29)
+mut "kN[4 + 2 * p] = a23 * a23 * i5 - aa;" "kN[4 + 2 * p] = a23 * i5 - aa;"
+mut "    e[m5] = -2.0 / 3.0;" "    e[m5] = -1.0 / 3.0;"
+mut "Bab[v][i] = Bb[i * 3] * ab[v][0] + Bb[i * 3 + 1] * ab[v][1] + Bb[i * 3 + 2] * ab[v][2];" "Bab[v][i] = (Bb[i * 3] * ab[v][0] + Bb[i * 3 + 1] * ab[v][1] + Bb[i * 3 + 2] * ab[v][2]) / (c13 * c13);"
+mut "GGb[m5][x] = 0.5 * (Bb[i * 3 + k] * As[j * 3 + l] + Bb[i * 3 + l] * As[j * 3 + k]) +" "GGb[m5][x] = 0.5 * (Bb[i * 3 + k] * As[j * 3 + l] + Bb[i * 3 + l] * As[j * 3 + k]) * 0.0 +"
+mut "Gb[m4][i * 3 + j] = As[i * 3 + j];" "Gb[m4][i * 3 + j] = ai[i] * aj[j];"
+mut "    if (mm == 2) continue;" "    if (mm == 2 || mm >= 3) continue;"
 exit $fail
