@@ -111,7 +111,11 @@ typedef struct {
   /* ---- variants; a zero-initialised tail = the ICNN on k above ---- */
   int32_t kinematics;          /* COMMET_KIN_STANDARD: k = (I1-3, I2-3, J-1); COMMET_KIN_ANISOTROPIC: see a0;
                                   COMMET_KIN_ISOCHORIC: k = (Ibar1-3, Ibar2-3, J-1), Ibar1 = J^-2/3 I1,
-                                  Ibar2 = J^-4/3 I2 (App. A.2.2) */
+                                  Ibar2 = J^-4/3 I2 (App. A.2.2);
+                                  COMMET_KIN_ISOCHORIC_ANISOTROPIC: the anisotropic inputs below on the
+                                  isochoric set Ibar = {1, 2, (4,ij), (5,ij)} of App. A.2.2:
+                                  (Ibar1-3, Ibar2-3, J-1, Ibar4,ij - A_i.A_j, Ibar5,ij - A_i.A_j),
+                                  Ibar4,ij = J^-2/3 I4,ij, Ibar5,ij = J^-4/3 I5,ij (reading R29) */
   int32_t network;             /* COMMET_NET_ICNN (the fields above), COMMET_NET_CANN, COMMET_NET_GENT_THOMAS */
   int32_t cann_n;              /* CANN: branches per kinematic input, 1..16 */
   const int32_t* cann_f;       /* CANN host [n_in][cann_n][3] (n_in = 3, or 5 anisotropic): f0 (0 x, 1 <x>, 2 |x|), f1 power (1..3),
@@ -132,7 +136,7 @@ typedef struct {
   const double* kan_grid;      /* host [R][2]: xmin, xmax of layer r's inputs */
   const double* kan_w;         /* host [edges]: spline weights, edges in (r, i, j) order */
   const double* kan_c;         /* host [edges][kan_nb]: control points */
-  /* COMMET_KIN_ANISOTROPIC: n_sv structural vectors A_v (reference configuration): a0, and a1
+  /* COMMET_KIN_ANISOTROPIC (and _ISOCHORIC_ANISOTROPIC): n_sv structural vectors A_v (reference configuration): a0, and a1
    * when n_sv = 2 (n_sv 0 or 1: a0 only).  The network inputs are k = (I1-3, I2-3, J-1, then for
    * each pair i <= j in the order (0,0), (0,1), (1,1): I4,ij - A_i.A_j, I5,ij - A_i.A_j) with
    * I4,ij = A_i.C A_j, I5,ij = A_i.C^2 A_j (Eq. standard-inv-II; App. A.2.1 table,
@@ -144,7 +148,7 @@ typedef struct {
   double a1[3];
 } commet_ncm_desc;
 
-enum { COMMET_KIN_STANDARD = 0, COMMET_KIN_ISOCHORIC = 1, COMMET_KIN_ANISOTROPIC = 2 };
+enum { COMMET_KIN_STANDARD = 0, COMMET_KIN_ISOCHORIC = 1, COMMET_KIN_ANISOTROPIC = 2, COMMET_KIN_ISOCHORIC_ANISOTROPIC = 3 };
 enum { COMMET_NET_ICNN = 0, COMMET_NET_CANN = 1, COMMET_NET_GENT_THOMAS = 2, COMMET_NET_ICKAN = 3 };
 
 /* Kernel variants (commet_set_kernel).  FUSED is the product path; SIMPLE is

@@ -62,15 +62,17 @@ class NcmDesc(C.Structure):
                 ("kan_c", C.c_void_p), ("a0", C.c_double * 3), ("n_sv", C.c_int32), ("a1", C.c_double * 3)]
 
 
-KIN_STANDARD, KIN_ISOCHORIC, KIN_ANISOTROPIC = 0, 1, 2
+KIN_STANDARD, KIN_ISOCHORIC, KIN_ANISOTROPIC, KIN_ISOCHORIC_ANISOTROPIC = 0, 1, 2, 3
 NET_ICNN, NET_CANN, NET_GENT_THOMAS, NET_ICKAN = 0, 1, 2, 3
-_KIN = {"standard": KIN_STANDARD, "isochoric": KIN_ISOCHORIC, "anisotropic": KIN_ANISOTROPIC}
+_KIN = {"standard": KIN_STANDARD, "isochoric": KIN_ISOCHORIC, "anisotropic": KIN_ANISOTROPIC,
+        "isochoric_anisotropic": KIN_ISOCHORIC_ANISOTROPIC}
 _NET = {"icnn": NET_ICNN, "cann": NET_CANN, "gent_thomas": NET_GENT_THOMAS, "ickan": NET_ICKAN}
 
 
 def ncm_desc(ncm: dict):
     """-> (NcmDesc, keepalive).  ncm keys: width, n_hidden, W1, W, b, a, optional skip_out,
-    skip_hidden, kappa, ref_shift, kinematics ("standard" | "isochoric"), network ("icnn" |
+    skip_hidden, kappa, ref_shift, kinematics ("standard" | "isochoric" | "anisotropic" |
+    "isochoric_anisotropic"), network ("icnn" |
     "cann" | "gent_thomas"), cann_f [3, n, 3] int, cann_w1 / cann_w2 [3, n], gt [3]."""
     arrs = {k: _f64(ncm.get(k)) for k in ("W1", "W", "b", "a", "skip_out", "skip_hidden", "cann_w1", "cann_w2",
                                           "kan_grid", "kan_w", "kan_c")}

@@ -38,11 +38,13 @@ extern "C" commet_status commet_setup(const commet_mesh_desc* mesh, const commet
   commet_ctx C = c.get();
   // NCM arguments (host checks, before any CUDA call)
   const int net = ncm->network, kin = ncm->kinematics;
-  if (kin != COMMET_KIN_STANDARD && kin != COMMET_KIN_ISOCHORIC && kin != COMMET_KIN_ANISOTROPIC)
+  if (kin != COMMET_KIN_STANDARD && kin != COMMET_KIN_ISOCHORIC && kin != COMMET_KIN_ANISOTROPIC &&
+      kin != COMMET_KIN_ISOCHORIC_ANISOTROPIC)
     return fail(C, COMMET_ERR_ARG, "kinematics %d unknown", kin);
   // anisotropic: one structural vector (a0; n_sv 0 or 1) -> 5 inputs, two (a0, a1) -> 9 inputs
-  const int n_sv = kin == COMMET_KIN_ANISOTROPIC ? (ncm->n_sv > 1 ? ncm->n_sv : 1) : 0;
-  if (kin == COMMET_KIN_ANISOTROPIC && (ncm->n_sv < 0 || ncm->n_sv > 2))
+  const bool aniso = kin == COMMET_KIN_ANISOTROPIC || kin == COMMET_KIN_ISOCHORIC_ANISOTROPIC;
+  const int n_sv = aniso ? (ncm->n_sv > 1 ? ncm->n_sv : 1) : 0;
+  if (aniso && (ncm->n_sv < 0 || ncm->n_sv > 2))
     return fail(C, COMMET_ERR_ARG, "n_sv %d not in 0..2 (structural vectors)", ncm->n_sv);
   const int nk = n_sv == 2 ? 9 : (n_sv == 1 ? 5 : 3);  // network inputs
   if (nk > 3 && net == COMMET_NET_GENT_THOMAS)
@@ -195,13 +197,14 @@ extern "C" commet_status commet_setup(const commet_mesh_desc* mesh, const commet
   fill_act_table(tab.data());
   if ((s = upload(C, c->act_tab, tab.data(), tab.size(), st))) return s;
   c->ncm = NcmDev{L, w, c->W1.p, c->b.p, c->a.p, c->skip_out.p, c->skip_h.p, c->Wrow.p, c->Wfrag.p,
-                  c->act_tab.p, ncm->kappa, ncm->ref_shift, kin, net,
+                  c->act_tab.p, ncm->kappa, ncm->ref_shift, aniso ? (int)COMMET_KIN_ANISOTROPIC : kin, net,
                   net == COMMET_NET_CANN ? ncm->cann_n : 0, c->cann_f.p, c->cann_w1.p, c->cann_w2.p,
                   {ncm->gt[0], ncm->gt[1], ncm->gt[2]},
                   net == COMMET_NET_ICKAN ? ncm->kan_layers : 0, net == COMMET_NET_ICKAN ? ncm->kan_nb : 0,
                   {0, 0, 0, 0, 0}, c->kan_grid.p, c->kan_w.p, c->kan_c.p, {ncm->a0[0], ncm->a0[1], ncm->a0[2]},
                   {n_sv == 2 ? ncm->a1[0] : 0.0, n_sv == 2 ? ncm->a1[1] : 0.0, n_sv == 2 ? ncm->a1[2] : 0.0}};
   if (n_sv == 2) c->ncm.kin = 3;  // internal: anisotropic with two structural vectors
+  c->ncm.aniso_iso = kin == COMMET_KIN_ISOCHORIC_ANISOTROPIC;  // internal: kin 2 / 3 on the isochoric inputs
   if (net == COMMET_NET_ICKAN)
     for (int r = 0; r <= ncm->kan_layers; r++) c->ncm.kan_width[r] = ncm->kan_width[r];
   CUDA_TRY(C, c->bad.alloc(1));

@@ -400,6 +400,8 @@ __device__ __forceinline__ void material_outputs(const AsmArgs& A, const NcmDev&
     Kin kin;
     kinematics(qF + q * 9, kin);
     if constexpr (C::KIN == 1) isochoric_to_standard(kin, gq, H6);
+    if constexpr (C::KIN >= 2)
+      if (m.aniso_iso) isochoric_aniso_to_standard<C::NSV>(kin, m.a0, m.a1, gq, H6);
     const double jm1 = kin.J - 1.0;
     const double Wv = N + m.kappa * jm1 * jm1 - m.ref_shift * jm1;
     gq[2] += 2.0 * m.kappa * jm1 - m.ref_shift;
@@ -927,7 +929,7 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
       for (int x = 0; x < 9; x++) qF[q * 9 + x] = F[x];
       if constexpr (C::KIN >= 2) {  // anisotropic inputs (+ I4,ij, I5,ij per vector pair)
         double kb[C::NK];
-        anisotropic_inputs<C::NSV>(kin, m.a0, m.a1, kb);
+        anisotropic_inputs<C::NSV>(kin, m.a0, m.a1, kb, m.aniso_iso);
 #pragma unroll
         for (int x = 0; x < C::NK; x++) qk[q * C::NK + x] = kb[x];
       } else if constexpr (C::KIN == 1) {  // isochoric inputs (App. A.2.2)
@@ -1416,6 +1418,8 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
       Kin kin;
       kinematics(qF + q * 9, kin);
       if constexpr (C::KIN == 1) isochoric_to_standard(kin, gq, H6);
+      if constexpr (C::KIN >= 2)
+        if (m.aniso_iso) isochoric_aniso_to_standard<C::NSV>(kin, m.a0, m.a1, gq, H6);
       gq[2] += 2.0 * m.kappa * (kin.J - 1.0) - m.ref_shift;
       H6[packed_index(C::NK, 2, 2)] += 2.0 * m.kappa;
       if constexpr (C::KIN >= 2)
@@ -1882,6 +1886,8 @@ __device__ __forceinline__ void ws_element(const AsmArgs& A, double* smem, int64
       Kin kin;
       kinematics(sm.qF(smem, s) + q * 9, kin);
       if constexpr (C::KIN == 1) isochoric_to_standard(kin, gq, H6);
+      if constexpr (C::KIN >= 2)
+        if (m.aniso_iso) isochoric_aniso_to_standard<C::NSV>(kin, m.a0, m.a1, gq, H6);
       gq[2] += 2.0 * m.kappa * (kin.J - 1.0) - m.ref_shift;
       H6[5] += 2.0 * m.kappa;
       if constexpr (PAR)

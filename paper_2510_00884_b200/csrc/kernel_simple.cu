@@ -44,11 +44,13 @@ __global__ void __launch_bounds__(64) simple_kernel(AsmArgs A) {
     trc = fmax(trc, kin.I1);
     double kv[9] = {kin.I1 - 3.0, kin.I2 - 3.0, kin.J - 1.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
     if (A.ncm.kin == 1) isochoric_inputs(kin, kv);
-    if (A.ncm.kin == 2) anisotropic_inputs<1>(kin, A.ncm.a0, A.ncm.a1, kv);
-    if (A.ncm.kin == 3) anisotropic_inputs<2>(kin, A.ncm.a0, A.ncm.a1, kv);
+    if (A.ncm.kin == 2) anisotropic_inputs<1>(kin, A.ncm.a0, A.ncm.a1, kv, A.ncm.aniso_iso);
+    if (A.ncm.kin == 3) anisotropic_inputs<2>(kin, A.ncm.a0, A.ncm.a1, kv, A.ncm.aniso_iso);
     double g[9], H6[45];
     ncm_point(A.ncm, kv, g, H6);
     if (A.ncm.kin == 1) isochoric_to_standard(kin, g, H6);
+    if (A.ncm.kin == 2 && A.ncm.aniso_iso) isochoric_aniso_to_standard<1>(kin, A.ncm.a0, A.ncm.a1, g, H6);
+    if (A.ncm.kin == 3 && A.ncm.aniso_iso) isochoric_aniso_to_standard<2>(kin, A.ncm.a0, A.ncm.a1, g, H6);
     const int nk = A.ncm.kin == 2 ? 5 : (A.ncm.kin == 3 ? 9 : 3);
     g[2] += 2.0 * A.ncm.kappa * (kin.J - 1.0) - A.ncm.ref_shift;
     H6[packed_index(nk, 2, 2)] += 2.0 * A.ncm.kappa;

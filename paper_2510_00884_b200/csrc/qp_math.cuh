@@ -292,8 +292,13 @@ struct Aniso {
 constexpr int kPostAniso = Aniso<1>::SIZE;   // 135
 constexpr int kPostAniso2 = Aniso<2>::SIZE;  // 215
 
+__host__ __device__ constexpr int packed_index(int n, int p, int q) { return p * n - p * (p - 1) / 2 + (q - p); }
+
+// I4,ij = A_i.C A_j and I5,ij = A_i.C^2 A_j per pair p (Eq. standard-inv-II), and A_i.A_j
 template <int NSV>
-__device__ __forceinline__ void anisotropic_inputs(const Kin& k, const double* a0, const double* a1, double* kk) {
+__device__ __forceinline__ void aniso_invariants(const Kin& k, const double* a0, const double* a1,
+                                                 double (&I4)[Aniso<NSV>::NP], double (&I5)[Aniso<NSV>::NP],
+                                                 double (&aa)[Aniso<NSV>::NP]) {
   using AN = Aniso<NSV>;
   const double* Av[2] = {a0, a1};
   double CA[NSV][3];
@@ -301,19 +306,94 @@ __device__ __forceinline__ void anisotropic_inputs(const Kin& k, const double* a
   for (int v = 0; v < NSV; v++)
 #pragma unroll
     for (int I = 0; I < 3; I++) CA[v][I] = k.C[I * 3] * Av[v][0] + k.C[I * 3 + 1] * Av[v][1] + k.C[I * 3 + 2] * Av[v][2];
-  kk[0] = k.I1 - 3.0;
-  kk[1] = k.I2 - 3.0;
-  kk[2] = k.J - 1.0;
 #pragma unroll
   for (int p = 0; p < AN::NP; p++) {
     const int i = AN::pi(p), j = AN::pj(p);
-    const double aa = Av[i][0] * Av[j][0] + Av[i][1] * Av[j][1] + Av[i][2] * Av[j][2];
-    kk[3 + 2 * p] = Av[i][0] * CA[j][0] + Av[i][1] * CA[j][1] + Av[i][2] * CA[j][2] - aa;
-    kk[4 + 2 * p] = CA[i][0] * CA[j][0] + CA[i][1] * CA[j][1] + CA[i][2] * CA[j][2] - aa;
+    aa[p] = Av[i][0] * Av[j][0] + Av[i][1] * Av[j][1] + Av[i][2] * Av[j][2];
+    I4[p] = Av[i][0] * CA[j][0] + Av[i][1] * CA[j][1] + Av[i][2] * CA[j][2];
+    I5[p] = CA[i][0] * CA[j][0] + CA[i][1] * CA[j][1] + CA[i][2] * CA[j][2];
   }
 }
 
-__host__ __device__ constexpr int packed_index(int n, int p, int q) { return p * n - p * (p - 1) / 2 + (q - p); }
+// network inputs; iso: the isochoric set of App. A.2.2 (reading R29):
+// (Ibar1-3, Ibar2-3, J-1, Ibar4,ij - A_i.A_j, Ibar5,ij - A_i.A_j), Ibar_m = J^(2 e_m) I_m with
+// e = -1/3 for I1, I4 and -2/3 for I2, I5
+template <int NSV>
+__device__ __forceinline__ void anisotropic_inputs(const Kin& k, const double* a0, const double* a1, double* kk,
+                                                   bool iso = false) {
+  using AN = Aniso<NSV>;
+  double I4[AN::NP], I5[AN::NP], aa[AN::NP];
+  aniso_invariants<NSV>(k, a0, a1, I4, I5, aa);
+  const double s1 = iso ? 1.0 / (cbrt(k.J) * cbrt(k.J)) : 1.0, s2 = s1 * s1;
+  kk[0] = s1 * k.I1 - 3.0;
+  kk[1] = s2 * k.I2 - 3.0;
+  kk[2] = k.J - 1.0;
+#pragma unroll
+  for (int p = 0; p < AN::NP; p++) {
+    kk[3 + 2 * p] = s1 * I4[p] - aa[p];
+    kk[4 + 2 * p] = s2 * I5[p] - aa[p];
+  }
+}
+
+// in place: g[NK], H[NK(NK+1)/2] (packed upper) from the isochoric anisotropic inputs' derivatives to
+// the standard anisotropic inputs' (I1, I2, J, I4,ij, I5,ij), by the chain rule through
+// Ibar_m = J^(q_m) I_m (q = -2/3 for m = 1, 4; -4/3 for m = 2, 5):
+//   g_m = a_m gb_m, g_J = gb_J + sum_m c_m gb_m, c_m = q_m Ibar_m / J, a_m = J^(q_m);
+//   H_mn = a_m a_n Hb_mn, H_mJ = a_m t_m + q_m a_m gb_m / J, t_m = Hb_mJ + sum_n Hb_mn c_n;
+//   H_JJ = t_J + sum_m c_m t_m + sum_m q_m (q_m - 1) Ibar_m gb_m / J^2
+// (the three-input case is isochoric_to_standard below, term for term)
+template <int NSV>
+__device__ __forceinline__ void isochoric_aniso_to_standard(const Kin& k, const double* a0, const double* a1,
+                                                            double* __restrict__ g, double* __restrict__ H) {
+  using AN = Aniso<NSV>;
+  constexpr int NK = AN::NK;
+  double I4[AN::NP], I5[AN::NP], aa[AN::NP];
+  aniso_invariants<NSV>(k, a0, a1, I4, I5, aa);
+  const double s1 = 1.0 / (cbrt(k.J) * cbrt(k.J)), s2 = s1 * s1, iJ = 1.0 / k.J;
+  double al[NK], qm[NK], c[NK];
+#pragma unroll
+  for (int m = 0; m < NK; m++) {
+    const bool two = m == 1 || (m >= 3 && ((m - 3) & 1));  // I2, I5,ij: exponent -4/3
+    const double Im = m == 0 ? k.I1 : m == 1 ? k.I2 : m == 2 ? 0.0 : ((m - 3) & 1) ? I5[(m - 3) >> 1] : I4[(m - 3) >> 1];
+    al[m] = m == 2 ? 1.0 : (two ? s2 : s1);
+    qm[m] = m == 2 ? 0.0 : (two ? -4.0 / 3.0 : -2.0 / 3.0);
+    c[m] = m == 2 ? 1.0 : qm[m] * al[m] * Im * iJ;  // c_J = 1 folds Hb_mJ into t_m
+  }
+  double t[NK];
+#pragma unroll
+  for (int m = 0; m < NK; m++) {
+    double s = 0.0;
+#pragma unroll
+    for (int n = 0; n < NK; n++) s += H[packed_index(NK, m < n ? m : n, m < n ? n : m)] * c[n];
+    t[m] = s;
+  }
+  double hjj = t[2], gj = g[2];
+#pragma unroll
+  for (int m = 0; m < NK; m++) {
+    if (m == 2) continue;
+    hjj += c[m] * t[m] + qm[m] * (qm[m] - 1.0) * (c[m] / qm[m]) * iJ * g[m];  // c_m / q_m = Ibar_m / J
+    gj += c[m] * g[m];
+  }
+#pragma unroll
+  for (int m = 0; m < NK; m++)
+#pragma unroll
+    for (int n = m; n < NK; n++) {
+      double& h = H[packed_index(NK, m, n)];
+      if (m == 2 && n == 2)
+        h = hjj;
+      else if (n == 2)
+        h = al[m] * t[m] + qm[m] * al[m] * iJ * g[m];
+      else if (m == 2)
+        h = al[n] * t[n] + qm[n] * al[n] * iJ * g[n];
+      else
+        h *= al[m] * al[n];
+    }
+#pragma unroll
+  for (int m = 0; m < NK; m++)
+    if (m != 2) g[m] *= al[m];
+  g[2] = gj;
+}
+
 
 template <int NSV>
 __device__ __forceinline__ void post_qp_aniso(const Kin& k, const double* a0, const double* a1,

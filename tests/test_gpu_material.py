@@ -46,6 +46,11 @@ MODELS = {
     "cann_anisotropic": lambda: anisotropic(cann_params(4, seed=6, n_in=5)),
     "icnn_anisotropic_32x2": lambda: anisotropic(ncm_weights(32, 2, 0.3, 15, 10.0, n_in=5)),
     "cann_two_vectors": lambda: anisotropic(cann_params(3, seed=8, n_in=9), A_FIBRE, A_SHEET),
+    "icnn_isochoric_anisotropic_32x2": lambda: anisotropic(ncm_weights(32, 2, 0.3, 23, 10.0, n_in=5), isochoric=True),
+    # (seed 6: every -ln(1 - w1 x) branch stays inside its domain x < 1/w1 at the 53 random F below;
+    # seeds 21 / 24 leave it at one point and both sides return NaN there)
+    "cann_isochoric_two_vectors": lambda: anisotropic(cann_params(3, seed=6, n_in=9), A_FIBRE, A_SHEET,
+                                                      isochoric=True),
 }
 
 

@@ -316,7 +316,7 @@ def test_parity_c5_sampled():
 
 
 @pytest.mark.parametrize("variant", ["icnn_isochoric", "icnn_anisotropic", "cann_anisotropic", "ickan",
-                                     "cann_two_vectors"])
+                                     "cann_two_vectors", "icnn_isochoric_anisotropic", "cann_isochoric_two_vectors"])
 def test_parity_full_size_sampled_variants(variant):
     """The variants' instantiations at the c3 size (2.1M qp, the persistent grid of the bench):
     sampled complete rows against the oracle."""
@@ -325,7 +325,11 @@ def test_parity_full_size_sampled_variants(variant):
            "cann_anisotropic": lambda: gen.anisotropic(gen.cann_params(4, seed=6, n_in=5)),
            "ickan": lambda: gen.ickan_params(),
            "cann_two_vectors": lambda: gen.anisotropic(gen.cann_params(3, seed=8, n_in=9), gen.A_FIBRE,
-                                                       gen.A_SHEET)}[variant]()
+                                                       gen.A_SHEET),
+           "icnn_isochoric_anisotropic": lambda: gen.anisotropic(gen.ncm_weights(64, 3, 0.3, 20, 10.0, n_in=5),
+                                                                 isochoric=True),
+           "cann_isochoric_two_vectors": lambda: gen.anisotropic(gen.cann_params(3, seed=21, n_in=9), gen.A_FIBRE,
+                                                                 (0.0, 0.6, 0.8), isochoric=True)}[variant]()
     sampled_rows_check("c3", n_samples=8, ncm=ncm)
 
 

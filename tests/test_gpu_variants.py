@@ -46,6 +46,15 @@ VARIANTS = {
     # two structural vectors (pairs 00, 01, 11: 9 inputs, Eq. standard-inv-II), one pair not orthogonal
     "cann_two_vectors": lambda: anisotropic(cann_params(3, seed=8, n_in=9), A_FIBRE, A_SHEET),
     "ickan_two_vectors": lambda: anisotropic(ickan_params((9, 4, 1), nb=7, seed=9), A_FIBRE, (0.0, 0.6, 0.8)),
+    # isochoric anisotropic inputs (App. A.2.2: Ibar1, Ibar2, J, Ibar4,ij, Ibar5,ij; reading R29)
+    "cann_isochoric_anisotropic": lambda: anisotropic(cann_params(4, seed=17, n_in=5), isochoric=True),
+    "ickan_isochoric_anisotropic": lambda: anisotropic(ickan_params((5, 4, 1), nb=7, seed=18), isochoric=True),
+    "icnn_isochoric_anisotropic_16x2": lambda: anisotropic(ncm_weights(16, 2, 0.3, 19, 10.0, n_in=5), isochoric=True),
+    "icnn_isochoric_anisotropic_64x3": lambda: anisotropic(ncm_weights(64, 3, 0.3, 20, 10.0, n_in=5), isochoric=True),
+    "cann_isochoric_two_vectors": lambda: anisotropic(cann_params(3, seed=21, n_in=9), A_FIBRE, (0.0, 0.6, 0.8),
+                                                      isochoric=True),
+    "ickan_isochoric_two_vectors": lambda: anisotropic(ickan_params((9, 4, 1), nb=7, seed=22), A_FIBRE, A_SHEET,
+                                                       isochoric=True),
 }
 
 
@@ -175,9 +184,10 @@ def test_kernel_info_reports_launched_instantiation(pc):
     assert info["cann"]["ctas_per_sm"] >= 3 and info["cann"]["smem_bytes"] < info["icnn"]["smem_bytes"]
 
 
-def test_normalize_reference_rejects_anisotropic(pc):
+@pytest.mark.parametrize("name", ["cann_anisotropic", "cann_isochoric_anisotropic"])
+def test_normalize_reference_rejects_anisotropic(pc, name):
     mesh, _ = _mesh(HEX8, 1)
-    lib = pc.Commet(mesh, VARIANTS["cann_anisotropic"]())
+    lib = pc.Commet(mesh, VARIANTS[name]())
     with pytest.raises(pc.CommetError):
         lib.normalize_reference()
 
