@@ -100,6 +100,12 @@
 #ifndef COMMET_Q_KIN3
 #define COMMET_Q_KIN3 16  // qps per batch of the two-vector (9-input) kernels
 #endif
+#ifndef COMMET_META_EARLY
+#define COMMET_META_EARLY 0  // hex8 stage 8 by (element, i-half): scatter metadata, first hop (lrow, slots) issued at the end of stage 7a (1) or its start (2), the second (row starts, degrees) before the K_e DMMAs; 0: both after them (measured: 1 / 2 slower -- GT c3 1.57 -> 1.60 / 1.64 ms, ICNN c3 9.50 -> 9.74 / 9.78, c5 635 -> 646; r02_ab_meta_early.txt)
+#endif
+#ifndef COMMET_RS
+#define COMMET_RS 1  // forward sweep: Hessian / gradient partials reduced over the tile rows by reduce-scatter shuffles
+#endif
 #ifndef COMMET_EB
 #define COMMET_EB 2  // network batches per element batch (ICNN assembly; c3 9.72 -> 9.43 ms with the two below)
 #endif
@@ -126,6 +132,43 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                : "+d"(c[0]), "+d"(c[1])
                : "d"(a), "d"(b));
+}
+
+// Sum of v[0..N) over the 8 lanes of a warp that share lane & 3 (the 8 rows g of a DMMA accumulator
+// tile), scattered over those lanes (reduce-scatter, xor 16 / 8 / 4): ceil(N/2) + ceil(N/4) + ceil(N/8)
+// shuffles instead of 3N for a full butterfly.  On return lane (g = lane >> 2) owns the sums of the
+// entries rs_index<N>(g, i), i < RS3 (entries >= N are zero padding; rs_index < 0 marks them).
+template <int N> struct RS {
+  static constexpr int K1 = (N + 1) / 2, K2 = (K1 + 1) / 2, K3 = (K2 + 1) / 2;
+};
+template <int N>
+__device__ __forceinline__ int rs_index(int g, int i) {
+  constexpr int K1 = RS<N>::K1, K2 = RS<N>::K2, K3 = RS<N>::K3;
+  const int b4 = (g >> 2) & 1, b3 = (g >> 1) & 1, b2 = g & 1;
+  const int l3 = b2 * K3 + i, l2 = b3 * K2 + l3, idx = b4 * K1 + l2;
+  return (l3 < K2 && l2 < K1 && idx < N) ? idx : -1;
+}
+template <int N>
+__device__ __forceinline__ void reduce_scatter8(const double (&v)[N], double (&out)[RS<N>::K3]) {
+  constexpr int K1 = RS<N>::K1, K2 = RS<N>::K2, K3 = RS<N>::K3;
+  const int lane = threadIdx.x & 31;
+  const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
+  double w1[K1], w2[K2];
+#pragma unroll
+  for (int i = 0; i < K1; i++) {
+    const double lo = v[i], hi = i + K1 < N ? v[i + K1] : 0.0;
+    w1[i] = (b4 ? hi : lo) + __shfl_xor_sync(0xffffffffu, b4 ? lo : hi, 16);
+  }
+#pragma unroll
+  for (int i = 0; i < K2; i++) {
+    const double lo = w1[i], hi = i + K2 < K1 ? w1[i + K2] : 0.0;
+    w2[i] = (b3 ? hi : lo) + __shfl_xor_sync(0xffffffffu, b3 ? lo : hi, 8);
+  }
+#pragma unroll
+  for (int i = 0; i < K3; i++) {
+    const double lo = w2[i], hi = i + K3 < K2 ? w2[i + K3] : 0.0;
+    out[i] = (b2 ? hi : lo) + __shfl_xor_sync(0xffffffffu, b2 ? lo : hi, 4);
+  }
 }
 
 // CTA-wide barrier of the network stages: __syncthreads, or in the warp-specialised kernel the
@@ -535,6 +578,19 @@ __device__ __forceinline__ void fwd_sweep(const NcmDev& m, double* act, double* 
       }
       net_sync<C>();
     }
+    if constexpr (COMMET_RS) {
+      double v[12], o[RS<12>::K3];
+#pragma unroll
+      for (int h = 0; h < 2; h++)
+#pragma unroll
+        for (int x = 0; x < 6; x++) v[h * 6 + x] = hp[h][x];
+      reduce_scatter8<12>(v, o);
+#pragma unroll
+      for (int i = 0; i < RS<12>::K3; i++) {
+        const int idx = rs_index<12>(g, i);
+        if (idx >= 0) hred[(jm * Q + qb * 8 + 2 * t + idx / 6) * 6 + idx % 6] = o[i];
+      }
+    } else {
 #pragma unroll
     for (int h = 0; h < 2; h++)
 #pragma unroll
@@ -550,6 +606,7 @@ __device__ __forceinline__ void fwd_sweep(const NcmDev& m, double* act, double* 
       for (int h = 0; h < 2; h++)
 #pragma unroll
         for (int x = 0; x < 6; x++) hred[(jm * Q + qb * 8 + 2 * t + h) * 6 + x] = hp[h][x];
+    }
     }
     if constexpr (C::MODE == 1) {
 #pragma unroll
@@ -604,6 +661,25 @@ __device__ __forceinline__ void fwd_sweep(const NcmDev& m, double* act, double* 
               act[j * LDA + q] = lam * s;  // mu_2
             }
         }
+        if constexpr (COMMET_RS) {
+          constexpr int NV = C::NT_V * 12;
+          double v[NV], o[RS<NV>::K3];
+#pragma unroll
+          for (int jj = 0; jj < C::NT_V; jj++)
+#pragma unroll
+            for (int h = 0; h < 2; h++)
+#pragma unroll
+              for (int x = 0; x < 6; x++) v[(jj * 2 + h) * 6 + x] = hb[jj][h][x];
+          reduce_scatter8<NV>(v, o);
+#pragma unroll
+          for (int i = 0; i < RS<NV>::K3; i++) {
+            const int idx = rs_index<NV>(g, i);
+            if (idx >= 0) {
+              const int jh = idx / 6;
+              hred[((C::JMG + vm) * Q + (vn * C::NT_V + jh / 2) * 8 + 2 * t + (jh & 1)) * 6 + idx % 6] = o[i];
+            }
+          }
+        } else {
 #pragma unroll
         for (int jj = 0; jj < C::NT_V; jj++)
 #pragma unroll
@@ -624,6 +700,7 @@ __device__ __forceinline__ void fwd_sweep(const NcmDev& m, double* act, double* 
 #pragma unroll
               for (int x = 0; x < 6; x++)
                 hred[((C::JMG + vm) * Q + ncol[jj] + 2 * t + h) * 6 + x] = hb[jj][h][x];
+        }
         }
       } else {  // l == 2: mu_1, c_1 -> partials of g = W1^T mu_1 and H_1 = W1^T diag(c_1) W1
         double pg[C::NT_V][2][9];
@@ -652,6 +729,25 @@ __device__ __forceinline__ void fwd_sweep(const NcmDev& m, double* act, double* 
               P9[6] += c1 * w1; P9[7] += c1 * w2; P9[8] += c * w2 * w2;
             }
         }
+        if constexpr (COMMET_RS) {  // act is dead now: partials at (vm, q)
+          constexpr int NV = C::NT_V * 18;
+          double v[NV], o[RS<NV>::K3];
+#pragma unroll
+          for (int jj = 0; jj < C::NT_V; jj++)
+#pragma unroll
+            for (int h = 0; h < 2; h++)
+#pragma unroll
+              for (int x = 0; x < 9; x++) v[(jj * 2 + h) * 9 + x] = pg[jj][h][x];
+          reduce_scatter8<NV>(v, o);
+#pragma unroll
+          for (int i = 0; i < RS<NV>::K3; i++) {
+            const int idx = rs_index<NV>(g, i);
+            if (idx >= 0) {
+              const int jh = idx / 9;
+              act[(vm * Q + (vn * C::NT_V + jh / 2) * 8 + 2 * t + (jh & 1)) * 9 + idx % 9] = o[i];
+            }
+          }
+        } else {
 #pragma unroll
         for (int jj = 0; jj < C::NT_V; jj++)
 #pragma unroll
@@ -671,6 +767,7 @@ __device__ __forceinline__ void fwd_sweep(const NcmDev& m, double* act, double* 
             for (int h = 0; h < 2; h++)
 #pragma unroll
               for (int x = 0; x < 9; x++) act[(vm * Q + ncol[jj] + 2 * t + h) * 9 + x] = pg[jj][h][x];
+        }
         }
       }
       net_sync<C>();
@@ -1148,6 +1245,25 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
                 }
               }
           }
+          if constexpr (COMMET_RS && NK == 3) {
+            constexpr int NV = C::NT_V * 2 * NP;
+            double v[NV], o[RS<NV>::K3];
+#pragma unroll
+            for (int jj = 0; jj < C::NT_V; jj++)
+#pragma unroll
+              for (int h = 0; h < 2; h++)
+#pragma unroll
+                for (int x = 0; x < NP; x++) v[(jj * 2 + h) * NP + x] = pg[jj][h][x];
+            reduce_scatter8<NV>(v, o);
+#pragma unroll
+            for (int i = 0; i < RS<NV>::K3; i++) {
+              const int idx = rs_index<NV>(g, i);
+              if (idx >= 0) {
+                const int jh = idx / NP;
+                act[part_at(vm, ncol[0] + (jh / 2) * 8 + 2 * t + (jh & 1), idx % NP)] = o[i];
+              }
+            }
+          } else {
 #pragma unroll
           for (int jj = 0; jj < C::NT_V; jj++)
 #pragma unroll
@@ -1167,6 +1283,7 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
               for (int h = 0; h < 2; h++)
 #pragma unroll
                 for (int x = 0; x < C::NP; x++) act[part_at(vm, ncol[jj] + 2 * t + h, x)] = pg[jj][h][x];
+          }
           }
         }
         __syncthreads();
@@ -1321,6 +1438,19 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
         __syncthreads();
       }
       // reduce over the 8 row-groups g of the warp (lane bits 2..4)
+      if constexpr (COMMET_RS && NK == 3) {
+        double v[2 * NH], o[RS<2 * NH>::K3];
+#pragma unroll
+        for (int h = 0; h < 2; h++)
+#pragma unroll
+          for (int x = 0; x < NH; x++) v[h * NH + x] = hp[h][x];
+        reduce_scatter8<2 * NH>(v, o);
+#pragma unroll
+        for (int i = 0; i < RS<2 * NH>::K3; i++) {
+          const int idx = rs_index<2 * NH>(g, i);
+          if (idx >= 0) hred[(jm * Q + qb * 8 + 2 * t + idx / NH) * NH + idx % NH] = o[i];
+        }
+      } else {
 #pragma unroll
       for (int h = 0; h < 2; h++)
 #pragma unroll
@@ -1336,6 +1466,7 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
         for (int h = 0; h < 2; h++)
 #pragma unroll
           for (int x = 0; x < NH; x++) hred[(jm * Q + qb * 8 + 2 * t + h) * NH + x] = hp[h][x];
+      }
       }
       __syncthreads();
     }
@@ -1378,6 +1509,32 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
 #if COMMET_PREFETCH
     if (batch + gridDim.x < n_batches) pf_load_a(batch + gridDim.x);
 #endif
+    // stage 8's scatter metadata (hex8, one warp per (element, i-half) task): the first hop of the
+    // lrow -> node_rs / node_deg chain and the slots, issued ahead so the L2 round trips overlap
+    // stage 7 instead of stalling the scatter (ncu, Gent-Thomas c3: 21 % of the warp samples were
+    // long-scoreboard waits on this chain)
+    constexpr bool HALF8 = C::DMMA_ELEM && NEN == 8 &&
+                           ((COMMET_ELEM_HALF && C::EB > 1) || (C::NET == 1 && COMMET_ELEM_HALF_NET1));
+    constexpr bool MDE = HALF8 && COMMET_META_EARLY > 0;
+    constexpr int TH8 = (2 * EE + C::NWARP - 1) / C::NWARP;  // stage-8 tasks per warp
+    int md_la[TH8], md_lb[TH8][2], md_sab[TH8][2], md_sba[TH8][2];
+    auto meta_hop1 = [&]() {
+#pragma unroll
+      for (int x = 0; x < TH8; x++) {
+        const int task = warp + x * C::NWARP;
+        const bool ok = task < ne * 2;
+        const int64_t el = e0 + (ok ? task >> 1 : 0);
+        md_la[x] = ok ? __ldg(A.lrow + el * NEN + g) : 0;
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+          const int b = 2 * t + h;
+          md_lb[x][h] = ok ? __ldg(A.lrow + el * NEN + b) : 0;
+          md_sab[x][h] = ok ? 3 * (int)__ldg(A.slot + ((size_t)el * NEN + g) * NEN + b) : 0;
+          md_sba[x][h] = ok ? 3 * (int)__ldg(A.slot + ((size_t)el * NEN + b) * NEN + g) : 0;
+        }
+      }
+    };
+    if constexpr (MDE && COMMET_META_EARLY == 2) meta_hop1();
     // ICNN, 3 inputs: four warps cooperate (warp = part of post_qp, lane = qp); otherwise one
     // thread per qp
     // (analytic networks: the CANN / Gent-Thomas instantiation (16 qps) only -- every warp repeats the
@@ -1429,6 +1586,7 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
       else
         post_qp(kin, gq, H6, swq[q], post + q * PS, qP + q * 9);
     }
+    if constexpr (MDE && COMMET_META_EARLY == 1) meta_hop1();
 #if !defined(COMMET_DEBUG_DROP) || COMMET_DEBUG_DROP != 1  // (planted race: tools/race_check.py)
     __syncthreads();
 #endif
@@ -1469,7 +1627,26 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
       // (2,2) at once -- the dN/dX operands and the scatter metadata of the lane's node pair are
       // loaded once for the three
       constexpr int KS = NQ * 3 / 4;
-      for (int task = warp; task < ne * 2; task += C::NWARP) {
+      // second hop of the metadata for all of this warp's tasks, before the first task's DMMAs
+      int64_t md_rsa[TH8], md_mb[TH8][2];
+      int md_sa[TH8], md_sb3[TH8][2];
+      if constexpr (MDE) {
+#pragma unroll
+        for (int x = 0; x < TH8; x++) {
+          const bool ok = warp + x * C::NWARP < ne * 2;
+          md_rsa[x] = ok ? __ldg(A.node_rs + md_la[x]) : 0;
+          md_sa[x] = ok ? 3 * __ldg(A.node_deg + md_la[x]) : 0;
+#pragma unroll
+          for (int h = 0; h < 2; h++) {
+            md_sb3[x][h] = ok ? 3 * __ldg(A.node_deg + md_lb[x][h]) : 0;
+            md_mb[x][h] = ok ? __ldg(A.node_rs + md_lb[x][h]) + md_sba[x][h] : 0;
+          }
+        }
+      }
+#pragma unroll
+      for (int x = 0; x < TH8; x++) {
+        const int task = warp + x * C::NWARP;
+        if (task >= ne * 2) break;
         const int e = task >> 1, i0 = task & 1;
         double c[3][2];
 #pragma unroll
@@ -1491,16 +1668,17 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
         }
         const int64_t el = e0 + e;
         const int a = g;
-        const int64_t la = __ldg(A.lrow + el * NEN + a);
-        const int64_t rsa = __ldg(A.node_rs + la);
-        const int sa = 3 * __ldg(A.node_deg + la);
+        const int64_t la = MDE ? md_la[x] : __ldg(A.lrow + el * NEN + a);
+        const int64_t rsa = MDE ? md_rsa[x] : __ldg(A.node_rs + la);
+        const int sa = MDE ? md_sa[x] : 3 * __ldg(A.node_deg + la);
 #pragma unroll
         for (int h = 0; h < 2; h++) {
           const int b = 2 * t + h;
-          const int sab = 3 * (int)__ldg(A.slot + ((size_t)el * NEN + a) * NEN + b);
-          const int64_t lb = __ldg(A.lrow + el * NEN + b);
-          const int sb3 = 3 * __ldg(A.node_deg + lb);
-          const int64_t mb = __ldg(A.node_rs + lb) + 3 * (int)__ldg(A.slot + ((size_t)el * NEN + b) * NEN + a);
+          const int sab = MDE ? md_sab[x][h] : 3 * (int)__ldg(A.slot + ((size_t)el * NEN + a) * NEN + b);
+          const int64_t lb = MDE ? md_lb[x][h] : __ldg(A.lrow + el * NEN + b);
+          const int sb3 = MDE ? md_sb3[x][h] : 3 * __ldg(A.node_deg + lb);
+          const int64_t mb =
+              MDE ? md_mb[x][h] : __ldg(A.node_rs + lb) + 3 * (int)__ldg(A.slot + ((size_t)el * NEN + b) * NEN + a);
 #pragma unroll
           for (int ik = 0; ik < 3; ik++) {
             const int i = i0 ? (ik < 2 ? 1 : 2) : 0;

@@ -21,7 +21,7 @@ def run(path, cfg, steps=20):
                   cfg["qp_w"].ctypes.data, 0, cfg["n_nodes"], 1, 0, None, 0, None, None,
                   int(os.environ.get("AB_ORDER", "0")))
     m = cfg["ncm"]
-    net = os.environ.get("AB_NET")  # variants: gt | cann | ickan | cann5 | ickan5 | icnn5
+    net = os.environ.get("AB_NET")  # variants: gt | cann | ickan | cann5 | ickan5 | icnn5 | icnnwWxL
     if net == "gt":
         m = gen.gent_thomas_params()
     elif net == "cann":
@@ -32,6 +32,9 @@ def run(path, cfg, steps=20):
         m = gen.anisotropic(gen.cann_params(4, n_in=5))
     elif net == "ickan5":
         m = gen.anisotropic(gen.ickan_params((5, 4, 1), nb=7, seed=7))
+    elif net and net.startswith("icnnw"):  # e.g. icnnw32x2: the 3-pass ICNN instantiations (w <= 32)
+        w_, l_ = net[5:].split("x")
+        m = gen.ncm_weights(int(w_), int(l_), 0.3, 12, 10.0)
     elif net == "icnn5":
         m = gen.anisotropic(gen.ncm_weights(64, 3, 0.3, 14, 10.0, n_in=5))
     import paper_2510_00884_b200 as pc

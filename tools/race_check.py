@@ -49,6 +49,12 @@ def cases():
         ("cann anisotropic tet10", gen.TET10, 2, gen.anisotropic(gen.cann_params(4, seed=6, n_in=5))),
         ("gent-thomas tet10", gen.TET10, 3, gen.gent_thomas_params()),
         ("ickan hex8", gen.HEX8, 3, gen.ickan_params()),
+        ("cann two vectors hex8", gen.HEX8, 3, gen.anisotropic(gen.cann_params(3, seed=8, n_in=9), gen.A_FIBRE,
+                                                                gen.A_SHEET)),
+        ("icnn64x3 isochoric anisotropic hex8", gen.HEX8, 3,
+         gen.anisotropic(w(64, 3, 0.3, 20, 10.0, n_in=5), isochoric=True)),
+        ("cann isochoric two vectors tet10", gen.TET10, 2,
+         gen.anisotropic(gen.cann_params(3, seed=21, n_in=9), gen.A_FIBRE, (0.0, 0.6, 0.8), isochoric=True)),
     ]
 
 
