@@ -106,6 +106,20 @@
 #ifndef COMMET_RS
 #define COMMET_RS 1  // forward sweep: Hessian / gradient partials reduced over the tile rows by reduce-scatter shuffles
 #endif
+#ifndef COMMET_L2_EF
+#define COMMET_L2_EF 0  // streamed element data and the scatter with an L2 evict-first policy (measured: c5 -0.1 %, c3 -0.3 %, c4 +0.3 %, Gent-Thomas c3 +4.7 % -> off; r02_ab_l2_hints.txt)
+#endif
+#ifndef COMMET_L2_EL
+#define COMMET_L2_EL 0  // weight fragments with an L2 evict-last policy (with EF: c5 -0.2 %, c3 -0.5 % -> off)
+#endif
+#ifndef COMMET_KUNROLL
+#define COMMET_KUNROLL 2  // k-loop unroll of the network GEMMs (0: full; 2 measured c5 603 -> 588 ms, c4 -0.9 %, c3 +0.4 %: the fully unrolled GEMMs overflow the instruction cache, r02_ab_kunroll.txt)
+#endif
+#define COMMET_PRAGMA(x) _Pragma(#x)
+#define COMMET_UNROLL(n) COMMET_PRAGMA(unroll n)
+#ifndef COMMET_FWD_LOOP
+#define COMMET_FWD_LOOP 0  // forward sweep: layer loop kept rolled (1) or unrolled (0) (1 measured: spills 104 -> 240 B, c3 +4.9 %, c5 +3.3 %; r02_ab_fwd_loop.txt)
+#endif
 #ifndef COMMET_EB
 #define COMMET_EB 2  // network batches per element batch (ICNN assembly; c3 9.72 -> 9.43 ms with the two below)
 #endif
@@ -231,8 +245,61 @@ __device__ __forceinline__ double* rout(const AsmArgs& A, int64_t la, int i) {
 }
 
 __device__ __forceinline__ double2 ldg2(const double* p) {
+#if COMMET_L2_EL  // hidden-layer weight fragments: kept in L2 ahead of the streamed data
+  uint64_t pol;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  double2 v;
+  asm("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(pol));
+  return v;
+#else
   return __ldg(reinterpret_cast<const double2*>(p));
+#endif
 }
+
+// Streamed element data (dN/dX, w, conn, u, scatter metadata: each word read once per colour
+// launch) and the CSR / residual scatter: L2 evict-first, so the lines that ARE reused -- the
+// hidden-layer weight fragments, the activation tables and the kernel's own instructions -- are
+// not evicted by the stream (at c5 the streamed data is ~60 GB per assembly against a 126 MB L2;
+// ncu showed 12 % of the warp samples waiting on instruction fetch there against 5 % at c3)
+#if COMMET_L2_EF
+__device__ __forceinline__ uint64_t l2_first() {
+  uint64_t pol;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ double2 ld_stream(const double2* p) {
+  double2 v;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(l2_first()));
+  return v;
+}
+__device__ __forceinline__ double ld_stream(const double* p) {
+  double v;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(l2_first()));
+  return v;
+}
+__device__ __forceinline__ int32_t ld_stream(const int32_t* p) {
+  int32_t v;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(l2_first()));
+  return v;
+}
+__device__ __forceinline__ int64_t ld_stream(const int64_t* p) {
+  int64_t v;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.b64 %0, [%1], %2;" : "=l"(v) : "l"(p), "l"(l2_first()));
+  return v;
+}
+__device__ __forceinline__ uint8_t ld_stream(const uint8_t* p) {
+  uint16_t v;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.u8 %0, [%1], %2;" : "=h"(v) : "l"(p), "l"(l2_first()));
+  return (uint8_t)v;
+}
+__device__ __forceinline__ void red_add(double* a, double v) {
+  asm volatile("red.global.add.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(a), "d"(v), "l"(l2_first()));
+}
+#else
+template <class T>
+__device__ __forceinline__ T ld_stream(const T* p) { return __ldg(p); }
+__device__ __forceinline__ void red_add(double* a, double v) { atomicAdd(a, v); }
+#endif
 
 // ---------------------------------------------------------------------------
 // compile-time tiling
@@ -364,7 +431,11 @@ __device__ __forceinline__ void warp_gemm(const double* __restrict__ Af, int mt0
   for (int p = 0; p < PD - 1 && p < KT2; p++)
 #pragma unroll
     for (int i = 0; i < MT; i++) a[p][i] = ldg2(ap + ((size_t)i * KT2 + p) * 64);
+#if COMMET_KUNROLL  // partial unroll (a multiple of PD: the ring indices stay static): smaller code
+  COMMET_UNROLL(COMMET_KUNROLL)
+#else
 #pragma unroll
+#endif
   for (int kt2 = 0; kt2 < KT2; kt2++) {
     const int cur = kt2 % PD;
     if (kt2 + PD - 1 < KT2) {
@@ -536,7 +607,11 @@ __device__ __forceinline__ void fwd_sweep(const NcmDev& m, double* act, double* 
     for (int h = 0; h < 2; h++)
 #pragma unroll
       for (int x = 0; x < 6; x++) hp[h][x] = 0.0;
+#if COMMET_FWD_LOOP
+#pragma unroll 1
+#else
 #pragma unroll
+#endif
     for (int l = 2; l <= L; l++) {
       double acc[C::MT_J][4][2];
       warp_gemm<C::MT_J, 4, KT2, C::PD_J>(m.Wfrag + (l - 2) * frag_layer, mt0, act, LDA, ncol, acc);
@@ -906,20 +981,20 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
 #pragma unroll
     for (int i = 0; i < PG; i++) {
       const int x = tid + i * C::NTHR;
-      pf_g[i] = x < n2 ? __ldg(src + x) : make_double2(0.0, 0.0);
+      pf_g[i] = x < n2 ? ld_stream(src + x) : make_double2(0.0, 0.0);
     }
 #pragma unroll
     for (int i = 0; i < PU; i++) {
       const int x = tid + i * C::NTHR;
       const int e = x / (NEN * 3), ai = x % (NEN * 3);
-      pf_c[i] = (x < NU && e < fne) ? __ldg(A.conn + (f0 + e) * NEN + ai / 3) : -1;  // raw: no use here
+      pf_c[i] = (x < NU && e < fne) ? ld_stream(A.conn + (f0 + e) * NEN + ai / 3) : -1;  // raw: no use here
     }
-    if (tid < QE) pf_w = tid < fne * NQ ? __ldg(A.qp_w + f0 * NQ + tid) : 0.0;
+    if (tid < QE) pf_w = tid < fne * NQ ? ld_stream(A.qp_w + f0 * NQ + tid) : 0.0;
   };
   auto pf_load_b = [&]() {
 #pragma unroll
     for (int i = 0; i < PU; i++)
-      pf_u[i] = pf_c[i] >= 0 ? __ldg(A.u + 3 * (int64_t)pf_c[i] + (tid + i * C::NTHR) % 3) : 0.0;
+      pf_u[i] = pf_c[i] >= 0 ? ld_stream(A.u + 3 * (int64_t)pf_c[i] + (tid + i * C::NTHR) % 3) : 0.0;
   };
   auto pf_store = [&]() {
     double2* dst = reinterpret_cast<double2*>(sgN);
@@ -984,9 +1059,9 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
         dst[x] = x < n2 ? __ldg(src + x) : make_double2(0.0, 0.0);
       for (int x = tid; x < EE * NEN * 3; x += C::NTHR) {
         const int e = x / (NEN * 3), ai = x % (NEN * 3);
-        sue[x] = e < ne ? __ldg(A.u + 3 * (int64_t)__ldg(A.conn + (e0 + e) * NEN + ai / 3) + ai % 3) : 0.0;
+        sue[x] = e < ne ? ld_stream(A.u + 3 * (int64_t)ld_stream(A.conn + (e0 + e) * NEN + ai / 3) + ai % 3) : 0.0;
       }
-      for (int x = tid; x < QE; x += C::NTHR) swq[x] = x < ne * NQ ? __ldg(A.qp_w + e0 * NQ + x) : 0.0;
+      for (int x = tid; x < QE; x += C::NTHR) swq[x] = x < ne * NQ ? ld_stream(A.qp_w + e0 * NQ + x) : 0.0;
     }
 #endif
     }  // MODE
@@ -1524,13 +1599,13 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
         const int task = warp + x * C::NWARP;
         const bool ok = task < ne * 2;
         const int64_t el = e0 + (ok ? task >> 1 : 0);
-        md_la[x] = ok ? __ldg(A.lrow + el * NEN + g) : 0;
+        md_la[x] = ok ? ld_stream(A.lrow + el * NEN + g) : 0;
 #pragma unroll
         for (int h = 0; h < 2; h++) {
           const int b = 2 * t + h;
-          md_lb[x][h] = ok ? __ldg(A.lrow + el * NEN + b) : 0;
-          md_sab[x][h] = ok ? 3 * (int)__ldg(A.slot + ((size_t)el * NEN + g) * NEN + b) : 0;
-          md_sba[x][h] = ok ? 3 * (int)__ldg(A.slot + ((size_t)el * NEN + b) * NEN + g) : 0;
+          md_lb[x][h] = ok ? ld_stream(A.lrow + el * NEN + b) : 0;
+          md_sab[x][h] = ok ? 3 * (int)ld_stream(A.slot + ((size_t)el * NEN + g) * NEN + b) : 0;
+          md_sba[x][h] = ok ? 3 * (int)ld_stream(A.slot + ((size_t)el * NEN + b) * NEN + g) : 0;
         }
       }
     };
@@ -1634,12 +1709,12 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
 #pragma unroll
         for (int x = 0; x < TH8; x++) {
           const bool ok = warp + x * C::NWARP < ne * 2;
-          md_rsa[x] = ok ? __ldg(A.node_rs + md_la[x]) : 0;
-          md_sa[x] = ok ? 3 * __ldg(A.node_deg + md_la[x]) : 0;
+          md_rsa[x] = ok ? ld_stream(A.node_rs + md_la[x]) : 0;
+          md_sa[x] = ok ? 3 * ld_stream(A.node_deg + md_la[x]) : 0;
 #pragma unroll
           for (int h = 0; h < 2; h++) {
-            md_sb3[x][h] = ok ? 3 * __ldg(A.node_deg + md_lb[x][h]) : 0;
-            md_mb[x][h] = ok ? __ldg(A.node_rs + md_lb[x][h]) + md_sba[x][h] : 0;
+            md_sb3[x][h] = ok ? 3 * ld_stream(A.node_deg + md_lb[x][h]) : 0;
+            md_mb[x][h] = ok ? ld_stream(A.node_rs + md_lb[x][h]) + md_sba[x][h] : 0;
           }
         }
       }
@@ -1668,23 +1743,23 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
         }
         const int64_t el = e0 + e;
         const int a = g;
-        const int64_t la = MDE ? md_la[x] : __ldg(A.lrow + el * NEN + a);
-        const int64_t rsa = MDE ? md_rsa[x] : __ldg(A.node_rs + la);
-        const int sa = MDE ? md_sa[x] : 3 * __ldg(A.node_deg + la);
+        const int64_t la = MDE ? md_la[x] : ld_stream(A.lrow + el * NEN + a);
+        const int64_t rsa = MDE ? md_rsa[x] : ld_stream(A.node_rs + la);
+        const int sa = MDE ? md_sa[x] : 3 * ld_stream(A.node_deg + la);
 #pragma unroll
         for (int h = 0; h < 2; h++) {
           const int b = 2 * t + h;
-          const int sab = MDE ? md_sab[x][h] : 3 * (int)__ldg(A.slot + ((size_t)el * NEN + a) * NEN + b);
-          const int64_t lb = MDE ? md_lb[x][h] : __ldg(A.lrow + el * NEN + b);
-          const int sb3 = MDE ? md_sb3[x][h] : 3 * __ldg(A.node_deg + lb);
+          const int sab = MDE ? md_sab[x][h] : 3 * (int)ld_stream(A.slot + ((size_t)el * NEN + a) * NEN + b);
+          const int64_t lb = MDE ? md_lb[x][h] : ld_stream(A.lrow + el * NEN + b);
+          const int sb3 = MDE ? md_sb3[x][h] : 3 * ld_stream(A.node_deg + lb);
           const int64_t mb =
-              MDE ? md_mb[x][h] : __ldg(A.node_rs + lb) + 3 * (int)__ldg(A.slot + ((size_t)el * NEN + b) * NEN + a);
+              MDE ? md_mb[x][h] : ld_stream(A.node_rs + lb) + 3 * (int)ld_stream(A.slot + ((size_t)el * NEN + b) * NEN + a);
 #pragma unroll
           for (int ik = 0; ik < 3; ik++) {
             const int i = i0 ? (ik < 2 ? 1 : 2) : 0;
             const int k = i0 ? (ik < 2 ? ik + 1 : 2) : ik;
-            atomicAdd(vout(A, la, rsa + i * sa + sab + k), c[ik][h]);
-            if (i < k) atomicAdd(vout(A, lb, mb + k * sb3 + i), c[ik][h]);
+            red_add(vout(A, la, rsa + i * sa + sab + k), c[ik][h]);
+            if (i < k) red_add(vout(A, lb, mb + k * sb3 + i), c[ik][h]);
           }
         }
       }
@@ -1724,19 +1799,19 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
 #else
         if (a < NEN) {
 #endif
-          const int64_t la = __ldg(A.lrow + el * NEN + a);
-          const int64_t rsa = __ldg(A.node_rs + la);
-          const int sa = 3 * __ldg(A.node_deg + la);
+          const int64_t la = ld_stream(A.lrow + el * NEN + a);
+          const int64_t rsa = ld_stream(A.node_rs + la);
+          const int sa = 3 * ld_stream(A.node_deg + la);
 #pragma unroll
           for (int h = 0; h < 2; h++) {
             const int b = 8 * nt + 2 * t + h;
             if (b < NEN) {
-              atomicAdd(vout(A, la, rsa + i * sa + 3 * (int)__ldg(A.slot + ((size_t)el * NEN + a) * NEN + b) + k), c[h]);
+              red_add(vout(A, la, rsa + i * sa + 3 * (int)ld_stream(A.slot + ((size_t)el * NEN + a) * NEN + b) + k), c[h]);
               if (i < k) {
-                const int64_t lb = __ldg(A.lrow + el * NEN + b);
-                const int sb3 = 3 * __ldg(A.node_deg + lb);
-                atomicAdd(vout(A, lb, __ldg(A.node_rs + lb) + k * sb3 +
-                                          3 * (int)__ldg(A.slot + ((size_t)el * NEN + b) * NEN + a) + i),
+                const int64_t lb = ld_stream(A.lrow + el * NEN + b);
+                const int sb3 = 3 * ld_stream(A.node_deg + lb);
+                red_add(vout(A, lb, ld_stream(A.node_rs + lb) + k * sb3 +
+                                          3 * (int)ld_stream(A.slot + ((size_t)el * NEN + b) * NEN + a) + i),
                           c[h]);
               }
             }
@@ -1754,7 +1829,7 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
           const double* ga = sgN + (q * NEN + a) * 3;
           rr += qP[q * 9 + i * 3] * ga[0] + qP[q * 9 + i * 3 + 1] * ga[1] + qP[q * 9 + i * 3 + 2] * ga[2];
         }
-        atomicAdd(rout(A, __ldg(A.lrow + (e0 + e) * NEN + a), i), rr);
+        red_add(rout(A, ld_stream(A.lrow + (e0 + e) * NEN + a), i), rr);
       }
     }
     } else {
@@ -1795,20 +1870,20 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
           }
         }
         const int64_t el = e0 + e;
-        const int64_t la = __ldg(A.lrow + el * NEN + a), lb = __ldg(A.lrow + el * NEN + b);
-        const int sa = 3 * __ldg(A.node_deg + la);
-        const int64_t dst = __ldg(A.node_rs + la) + i * sa + 3 * (int)__ldg(A.slot + ((size_t)el * NEN + a) * NEN + b);
-        atomicAdd(vout(A, la, dst), K0);
-        atomicAdd(vout(A, la, dst + 1), K1);
-        atomicAdd(vout(A, la, dst + 2), K2);
+        const int64_t la = ld_stream(A.lrow + el * NEN + a), lb = ld_stream(A.lrow + el * NEN + b);
+        const int sa = 3 * ld_stream(A.node_deg + la);
+        const int64_t dst = ld_stream(A.node_rs + la) + i * sa + 3 * (int)ld_stream(A.slot + ((size_t)el * NEN + a) * NEN + b);
+        red_add(vout(A, la, dst), K0);
+        red_add(vout(A, la, dst + 1), K1);
+        red_add(vout(A, la, dst + 2), K2);
         if (b == a) {
-          atomicAdd(rout(A, la, i), rr);
+          red_add(rout(A, la, i), rr);
         } else {
-          const int sb3 = 3 * __ldg(A.node_deg + lb);
-          const int64_t mir = __ldg(A.node_rs + lb) + 3 * (int)__ldg(A.slot + ((size_t)el * NEN + b) * NEN + a) + i;
-          atomicAdd(vout(A, lb, mir), K0);
-          atomicAdd(vout(A, lb, mir + sb3), K1);
-          atomicAdd(vout(A, lb, mir + 2 * sb3), K2);
+          const int sb3 = 3 * ld_stream(A.node_deg + lb);
+          const int64_t mir = ld_stream(A.node_rs + lb) + 3 * (int)ld_stream(A.slot + ((size_t)el * NEN + b) * NEN + a) + i;
+          red_add(vout(A, lb, mir), K0);
+          red_add(vout(A, lb, mir + sb3), K1);
+          red_add(vout(A, lb, mir + 2 * sb3), K2);
         }
       }
     }
@@ -1999,14 +2074,14 @@ __device__ __forceinline__ void ws_element(const AsmArgs& A, double* smem, int64
     for (int i = 0; i < PU; i++) {
       const int x = etid + i * NTE;
       const int e = x / (NEN * 3), ai = x % (NEN * 3);
-      cn[i] = (x < NU && e < fne) ? __ldg(A.conn + (f0 + e) * NEN + ai / 3) : -1;
+      cn[i] = (x < NU && e < fne) ? ld_stream(A.conn + (f0 + e) * NEN + ai / 3) : -1;
     }
 #pragma unroll
-    for (int i = 0; i < PU; i++) ru[i] = cn[i] >= 0 ? __ldg(A.u + 3 * (int64_t)cn[i] + (etid + i * NTE) % 3) : 0.0;
+    for (int i = 0; i < PU; i++) ru[i] = cn[i] >= 0 ? ld_stream(A.u + 3 * (int64_t)cn[i] + (etid + i * NTE) % 3) : 0.0;
 #pragma unroll
     for (int i = 0; i < PW; i++) {
       const int x = etid + i * NTE;
-      rw[i] = x < fne * NQ ? __ldg(A.qp_w + f0 * NQ + x) : 0.0;
+      rw[i] = x < fne * NQ ? ld_stream(A.qp_w + f0 * NQ + x) : 0.0;
     }
   };
   auto store = [&](int s) {
@@ -2118,22 +2193,22 @@ __device__ __forceinline__ void ws_element(const AsmArgs& A, double* smem, int64
 #else
         {
 #endif
-        const int64_t la = __ldg(A.lrow + el * NEN + a);
-        const int64_t rsa = __ldg(A.node_rs + la);
-        const int sa = 3 * __ldg(A.node_deg + la);
+        const int64_t la = ld_stream(A.lrow + el * NEN + a);
+        const int64_t rsa = ld_stream(A.node_rs + la);
+        const int sa = 3 * ld_stream(A.node_deg + la);
 #pragma unroll
         for (int h = 0; h < 2; h++) {
           const int b = 2 * t + h;
-          const int sab = 3 * (int)__ldg(A.slot + ((size_t)el * NEN + a) * NEN + b);
-          const int64_t lb = __ldg(A.lrow + el * NEN + b);
-          const int sb3 = 3 * __ldg(A.node_deg + lb);
-          const int64_t mb = __ldg(A.node_rs + lb) + 3 * (int)__ldg(A.slot + ((size_t)el * NEN + b) * NEN + a);
+          const int sab = 3 * (int)ld_stream(A.slot + ((size_t)el * NEN + a) * NEN + b);
+          const int64_t lb = ld_stream(A.lrow + el * NEN + b);
+          const int sb3 = 3 * ld_stream(A.node_deg + lb);
+          const int64_t mb = ld_stream(A.node_rs + lb) + 3 * (int)ld_stream(A.slot + ((size_t)el * NEN + b) * NEN + a);
 #pragma unroll
           for (int ik = 0; ik < 3; ik++) {
             const int i = i0 ? (ik < 2 ? 1 : 2) : 0;
             const int k = i0 ? (ik < 2 ? ik + 1 : 2) : ik;
-            atomicAdd(vout(A, la, rsa + i * sa + sab + k), c[ik][h]);
-            if (i < k) atomicAdd(vout(A, lb, mb + k * sb3 + i), c[ik][h]);
+            red_add(vout(A, la, rsa + i * sa + sab + k), c[ik][h]);
+            if (i < k) red_add(vout(A, lb, mb + k * sb3 + i), c[ik][h]);
           }
         }
         }
@@ -2148,7 +2223,7 @@ __device__ __forceinline__ void ws_element(const AsmArgs& A, double* smem, int64
           const double* ga = sgN + (q * NEN + a) * 3;
           rr += qP[q * 9 + i * 3] * ga[0] + qP[q * 9 + i * 3 + 1] * ga[1] + qP[q * 9 + i * 3 + 2] * ga[2];
         }
-        atomicAdd(rout(A, __ldg(A.lrow + (e0 + e) * NEN + a), i), rr);
+        red_add(rout(A, ld_stream(A.lrow + (e0 + e) * NEN + a), i), rr);
       }
     }
 #ifdef COMMET_EXP_SKIP_ELEM

@@ -1,0 +1,9 @@
+set -u
+O=gpurun_out/r2s4
+mkdir -p $O
+L="tools/ab/libcommet_ef0.so tools/ab/libcommet_ef1.so tools/ab/libcommet_ef1el1.so"
+timeout 1500 python tools/ab_bench.py c5 $L > $O/ab_l2_c5.txt 2>&1
+timeout 600 python tools/ab_bench.py c3 $L > $O/ab_l2_c3.txt 2>&1
+AB_NET=gt timeout 600 python tools/ab_bench.py c3 $L > $O/ab_l2_gt.txt 2>&1
+timeout 600 python tools/ab_bench.py c4 $L > $O/ab_l2_c4.txt 2>&1
+cat $O/ab_l2_*.txt
