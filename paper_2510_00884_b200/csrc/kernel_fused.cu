@@ -120,6 +120,15 @@
 #ifndef COMMET_FWD_LOOP
 #define COMMET_FWD_LOOP 0  // forward sweep: layer loop kept rolled (1) or unrolled (0) (1 measured: spills 104 -> 240 B, c3 +4.9 %, c5 +3.3 %; r02_ab_fwd_loop.txt)
 #endif
+#ifndef COMMET_BPF
+#define COMMET_BPF 1  // network GEMMs: B fragments loaded one half k-step ahead (measured c3 -0.8 %, c5 -0.35 %, c4 +0.1 %; r02_ab_bpf.txt)
+#endif
+#ifndef COMMET_E8_UNROLL
+#define COMMET_E8_UNROLL 2  // ICNN hex8 stage 8 (element, i-half): unroll of the (q, J) k-loop (0: full; 2 measured c3 -1.9 %, c5 -2.8 %, spills 92 -> 0 B; the analytic networks keep the full unroll: Gent-Thomas +3.7 %, CANN +4.4 % with 2; r02_ab_e8.txt)
+#endif
+#ifndef COMMET_T7_ROLL
+#define COMMET_T7_ROLL 0  // stage 7b three-rows item: the k loop rolled (smaller code; measured c3 +0.7 %, c5 +0.7 % -> off)
+#endif
 #ifndef COMMET_EB
 #define COMMET_EB 2  // network batches per element batch (ICNN assembly; c3 9.72 -> 9.43 ms with the two below)
 #endif
@@ -427,6 +436,11 @@ __device__ __forceinline__ void warp_gemm(const double* __restrict__ Af, int mt0
   const double* ap = Af + (size_t)mt0 * KT2 * 64 + lane * 2;
   const double* bp = act + t * lda + g;
   double2 a[PD][MT];
+#if COMMET_BPF
+  double bn[NT];
+#pragma unroll
+  for (int j = 0; j < NT; j++) bn[j] = bp[ncol[j]];
+#endif
 #pragma unroll
   for (int p = 0; p < PD - 1 && p < KT2; p++)
 #pragma unroll
@@ -442,6 +456,23 @@ __device__ __forceinline__ void warp_gemm(const double* __restrict__ Af, int mt0
 #pragma unroll
       for (int i = 0; i < MT; i++) a[(kt2 + PD - 1) % PD][i] = ldg2(ap + ((size_t)i * KT2 + kt2 + PD - 1) * 64);
     }
+#if COMMET_BPF  // B fragments of the next half k-step loaded before this one's DMMAs
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+      double b[NT];
+#pragma unroll
+      for (int j = 0; j < NT; j++) b[j] = bn[j];
+      if (h == 0 || kt2 + 1 < KT2) {
+        const double* bk = bp + (kt2 * 8 + h * 4 + 4) * lda;
+#pragma unroll
+        for (int j = 0; j < NT; j++) bn[j] = bk[ncol[j]];
+      }
+#pragma unroll
+      for (int i = 0; i < MT; i++)
+#pragma unroll
+        for (int j = 0; j < NT; j++) dmma(acc[i][j], h ? a[cur][i].y : a[cur][i].x, b[j]);
+    }
+#else
 #pragma unroll
     for (int h = 0; h < 2; h++) {
       const double* bk = bp + (kt2 * 8 + h * 4) * lda;
@@ -453,6 +484,7 @@ __device__ __forceinline__ void warp_gemm(const double* __restrict__ Af, int mt0
 #pragma unroll
         for (int j = 0; j < NT; j++) dmma(acc[i][j], h ? a[cur][i].y : a[cur][i].x, b[j]);
     }
+#endif
   }
 }
 
@@ -1726,7 +1758,8 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
         double c[3][2];
 #pragma unroll
         for (int ik = 0; ik < 3; ik++) c[ik][0] = c[ik][1] = 0.0;
-#pragma unroll
+        constexpr int E8U = (C::NET == 0 && COMMET_E8_UNROLL) ? COMMET_E8_UNROLL : KS;
+#pragma unroll E8U
         for (int kt = 0; kt < KS; kt++) {
           const int kk = 4 * kt + t, q = e * NQ + kk / 3, J = kk % 3;
           const double* Gg = sgN + (q * NEN + g) * 3;  // node a = b_row = g of the fragments

@@ -229,7 +229,11 @@ __device__ __forceinline__ void tangent_rows_i(const double* __restrict__ post, 
     p[J][1] = post[36 + i * 3 + J];
     p[J][2] = post[45 + i * 3 + J];
   }
+#if COMMET_T7_ROLL
+#pragma unroll 1
+#else
 #pragma unroll
+#endif
   for (int kk = 0; kk < 3; kk++) {
     double FkJ[3], GkJ[3];
 #pragma unroll
