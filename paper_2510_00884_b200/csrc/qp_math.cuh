@@ -668,7 +668,8 @@ __device__ __forceinline__ double analytic_value(int net, int n, const int32_t* 
 //       polynomial of degree 5 (N = 64) / 4 (N = 256);
 //   log1p(e) = log c_j + log1p(r2), c_j = 1 + j/N nearest to u = 1 + e, r2 = u/c_j - 1,
 //       |r2| <= 1/(2N), log1p by its series to degree 7 / 6, the rounding of u corrected;
-//   1/u = (1/c_j) / (1 + r2) by the series 1 - r2 + ... - r2^7 / - r2^5.
+//   1/u = (1/c_j) / (1 + r2) by the series 1 - r2 + ... - r2^7 / - r2^5 (COMMET_SIG_RCP = 0), or
+//       by rcp.approx + two Newton steps (COMMET_SIG_RCP = 1, the default: off the table, 4 fp64 ops).
 // Truncation errors, relative: 6e-18 / 3.7e-17 (exp), 2.2e-16 / 1.2e-17 (log1p: r2^(d+1)/(d+1)
 // relative to log1p(r2) ~ r2 when j = 0), 2e-17 / 5.7e-17 (1/u).  The fused kernels whose shared memory allows it use N = 256
 // (4 fp64 ops per neuron fewer, measured on the round-2 A/B); the rest N = 64.
@@ -710,6 +711,18 @@ __device__ __forceinline__ double exp_neg_abs(double y, const double* __restrict
   return __hiloint2double(__double2hiint(e) + (k >> TB) * 1048576, __double2loint(e));  // * 2^(k >> TB)
 }
 
+#ifndef COMMET_SIG_RCP
+#define COMMET_SIG_RCP 1  // sigmoid 1/(1 + e) by the MUFU reciprocal + two Newton steps instead of the table series (measured c3 -0.5 %, c4 -0.3 %, c5 -0.6 %; r02_ab_sig_rcp.txt)
+#endif
+// 1/u for u in [1, 2]: rcp.approx (MUFU, off the fp64 datapath) and two Newton steps (relative
+// error eps0^4 + rounding: ~2 ulp), 4 fp64 ops instead of the 1/c_j table series (7-9)
+__device__ __forceinline__ double rcp_u12(double u) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(u));
+  r = fma(r, fma(-u, r, 1.0), r);
+  return fma(r, fma(-u, r, 1.0), r);
+}
+
 template <int TB>
 __device__ __forceinline__ void softplus_sig_t(double y, const double* __restrict__ tab, double& z, double& s) {
   constexpr int N = ActTab<TB>::N;
@@ -721,26 +734,31 @@ __device__ __forceinline__ void softplus_sig_t(double y, const double* __restric
   const double invc = tab[N + j], logc = tab[2 * N + 1 + j];
   const double r2 = fma(u, invc, -1.0);
   const double r2s = r2 * r2;
-  double q, v;
+  double q, v = 0.0;
   if constexpr (TB == 6) {
     q = fma(r2, 1.0 / 7.0, -1.0 / 6.0);
     q = fma(q, r2, 0.2);
     q = fma(q, r2, -0.25);
     q = fma(q, r2, 1.0 / 3.0);
     q = fma(q, r2, -0.5);
-    const double r4 = r2s * r2s;
-    v = (1.0 - r2) * (1.0 + r2s) * (1.0 + r4);  // 1/(1 + r2), error r2^8
+    if constexpr (!COMMET_SIG_RCP) {
+      const double r4 = r2s * r2s;
+      v = (1.0 - r2) * (1.0 + r2s) * (1.0 + r4);  // 1/(1 + r2), error r2^8
+    }
   } else {  // degree 6: at j = 0 (e < 1/512) z = log1p(r2) ~ r2, so the RELATIVE error is r2^6/7
     q = fma(r2, -1.0 / 6.0, 0.2);
     q = fma(q, r2, -0.25);
     q = fma(q, r2, 1.0 / 3.0);
     q = fma(q, r2, -0.5);
-    v = (1.0 - r2) * (fma(r2s, r2s, r2s) + 1.0);  // 1/(1 + r2), error r2^6
+    if constexpr (!COMMET_SIG_RCP) v = (1.0 - r2) * (fma(r2s, r2s, r2s) + 1.0);  // 1/(1 + r2), error r2^6
   }
   const double lp = fma(q, r2s, r2);                 // log1p(r2)
   const double d = e - (u - 1.0);                    // rounding error of u (exact)
   z = fmax(y, 0.0) + (logc + fma(d, invc, lp));      // max(y,0) + log1p(e)
-  s = (y >= 0.0 ? 1.0 : e) * (invc * v);
+  if constexpr (COMMET_SIG_RCP)
+    s = (y >= 0.0 ? 1.0 : e) * rcp_u12(u);
+  else
+    s = (y >= 0.0 ? 1.0 : e) * (invc * v);
 }
 
 // sigmoid only (the last hidden layer needs s, not z): e = exp(-|y|) and 1/(1+e) as above
@@ -751,6 +769,7 @@ __device__ __forceinline__ double sigmoid_t(double y, const double* __restrict__
   int k;
   const double e = exp_neg_abs<TB>(y, tab, k);
   const double u = 1.0 + e;
+  if constexpr (COMMET_SIG_RCP) return (y >= 0.0 ? 1.0 : e) * rcp_u12(u);  // as in softplus_sig_t
   const int j = __double2loint(fma(e, (double)N, MAGIC));
   const double invc = tab[N + j];
   const double r2 = fma(u, invc, -1.0);
