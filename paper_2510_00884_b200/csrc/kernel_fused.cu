@@ -129,6 +129,12 @@
 #ifndef COMMET_T7_ROLL
 #define COMMET_T7_ROLL 0  // stage 7b three-rows item: the k loop rolled (smaller code; measured c3 +0.7 %, c5 +0.7 % -> off)
 #endif
+#ifndef COMMET_ACT_TB_EB
+#define COMMET_ACT_TB_EB 6  // activation table bits of the two-batch kernels (8 fits only with COMMET_FUSE_GH; measured with it: c3 +0.6 %, c5 +0.2 % -> 6)
+#endif
+#ifndef COMMET_FUSE_GH
+#define COMMET_FUSE_GH 0  // forward sweep + two-batch element stage: (g, H) written straight into qgH (one barrier and the qg / qH / gsk buffers fewer; measured c3 +0.1-0.3 %, c5 +0.15 % (8 B spill) -> off; r02_ab_fuse_gh.txt)
+#endif
 #ifndef COMMET_EB
 #define COMMET_EB 2  // network batches per element batch (ICNN assembly; c3 9.72 -> 9.43 ms with the two below)
 #endif
@@ -364,7 +370,7 @@ struct Cfg {
   static_assert(QE <= 32, "stage-1 threads (one per qp) must sit in warp 0");
   // activation table bits on the forward-sweep path (the 256-entry tables do not fit beside the
   // element buffers of two batches)
-  static constexpr int TB_FWD = EB > 1 ? 6 : COMMET_ACT_TB;
+  static constexpr int TB_FWD = EB > 1 ? COMMET_ACT_TB_EB : COMMET_ACT_TB;
   static constexpr int LDA = (FWDC ? 4 : NK) * Q + 4;  // act row stride (= 4 mod 16: conflict-free B frags)
   static constexpr int LDS = Q + 2;                // s/c row stride (2-way conflicts at most)
   static_assert(W % 8 == 0 && Q % 8 == 0 && Q % NQ == 0, "tile");
@@ -386,6 +392,7 @@ struct Smem {
   int act, sb, cb, qF, qk, qg, qH, hred, gsk, gN, ue, wq, qN, tab, qgH, qP, post, X, qA, total;
   // fwd: the forward-sweep path runs (C::FWDC, 2 <= L <= 3, no hidden skips): no c buffers
   __host__ __device__ static bool fwd_path(int L, bool skips) { return C::FWDC && L >= 2 && L <= 3 && !skips; }
+  __host__ __device__ static bool fused_gh(int L, bool skips) { return COMMET_FUSE_GH && C::EB > 1 && fwd_path(L, skips); }
   __host__ __device__ Smem(int L, bool skips = false) {
     const bool fwd = fwd_path(L, skips);
     int o = 0;
@@ -397,11 +404,14 @@ struct Smem {
     const int dead = o;
     qF = o;  o += C::QE * 9;
     qk = o;  o += C::QE * C::NK;
-    qg = o;  o += C::Q * C::NK;
-    qH = o;  o += C::Q * C::NH;
+    // (forward sweep with the two-batch element stage: (g, H) go straight to qgH and the hidden-skip
+    // gradients are zero -- no qg / qH / gsk, which leaves room for the 256-entry activation tables)
+    const bool fgh = fused_gh(L, skips);
+    qg = o;  o += fgh ? 0 : C::Q * C::NK;
+    qH = o;  o += fgh ? 0 : C::Q * C::NH;
     hred = o; o += (C::JMG + (C::FWDC ? C::VMG : 0)) * C::Q * C::NH;  // H partials per warp row group
     // (the adjoint-pass g/H_1 partials, VMG x Q x 9, live in act: dead at that point)
-    gsk = o; o += C::QE * C::NK;
+    gsk = o; o += fgh ? 0 : C::QE * C::NK;
     gN = o;  o += C::QE * C::NEN * 3;
     ue = o;  o += C::EE * C::NEN * 3;
     wq = o;  o += C::QE;
@@ -623,7 +633,8 @@ __device__ __forceinline__ double rcp_nr(double x) {
 
 template <class C, int L>
 __device__ __forceinline__ void fwd_sweep(const NcmDev& m, double* act, double* sb, double* hred, double* qg,
-                                          double* qH, const double* gsk, const double* stab, double* qNp) {
+                                          double* qH, const double* gsk, const double* stab, double* qNp,
+                                          double* qgH_h = nullptr) {
   constexpr int W = C::W, Q = C::Q, LDA = C::LDA, LDS = C::LDS, KT2 = C::KT2;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
   const size_t frag_layer = (size_t)2 * W * W;
@@ -890,12 +901,30 @@ __device__ __forceinline__ void fwd_sweep(const NcmDev& m, double* act, double* 
     for (int r = 0; r < C::VMG; r++)
 #pragma unroll
       for (int x = 0; x < 9; x++) v[x] += act[(r * Q + q) * 9 + x];
+    if (qgH_h) {  // two-batch element stage: (g, H) of this network batch straight into qgH, the
+                  // row-group partials of hred added in the order of the separate copy (no hidden
+                  // skips on this path: gsk = 0)
+      double* o = qgH_h + q * C::NKH;
 #pragma unroll
-    for (int x = 0; x < 3; x++) qg[q * 3 + x] = v[x] + gsk[q * 3 + x] + __ldg(m.skip_out + x);
+      for (int x = 0; x < 3; x++) o[x] = v[x] + 0.0 + __ldg(m.skip_out + x);
 #pragma unroll
-    for (int x = 0; x < 6; x++) qH[q * 6 + x] = v[3 + x];
+      for (int x = 0; x < 6; x++) {
+        double hv = v[3 + x];
+#pragma unroll
+        for (int r = 0; r < C::JMG; r++) hv += hred[(r * Q + q) * 6 + x];
+        if (L == 3)
+#pragma unroll
+          for (int r = 0; r < C::VMG; r++) hv += hred[((C::JMG + r) * Q + q) * 6 + x];
+        o[3 + x] = hv;
+      }
+    } else {
+#pragma unroll
+      for (int x = 0; x < 3; x++) qg[q * 3 + x] = v[x] + gsk[q * 3 + x] + __ldg(m.skip_out + x);
+#pragma unroll
+      for (int x = 0; x < 6; x++) qH[q * 6 + x] = v[3 + x];
+    }
   }
-  net_sync<C>();
+  if (!qgH_h) net_sync<C>();  // (fused: the caller's barrier after the batch orders qgH and act)
 }
 
 // ---- stage 2: layer 1 (3 -> W), elementwise.  Each thread: one qp, neurons j0, j0 + NTHR/Q, ...
@@ -980,6 +1009,7 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
   const NcmDev& m = A.ncm;
   const bool skips = m.skip_h != nullptr;
   const bool fwd = Smem<C>::fwd_path(L, skips);
+  const bool fgh = Smem<C>::fused_gh(L, skips);  // forward sweep, two-batch element stage: (g, H) into qgH
   const int64_t n_batches = (A.el_count + EE - 1) / EE;
   const size_t frag_layer = (size_t)2 * W * W;  // W and W^T fragments per hidden layer
   {  // the activation table of this path (256 entries on the forward sweep, 64 otherwise)
@@ -1147,8 +1177,9 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
         qk[q * 3 + 1] = kin.I2 - 3.0;
         qk[q * 3 + 2] = kin.J - 1.0;
       }
+      if (!fgh)
 #pragma unroll
-      for (int x = 0; x < C::NK; x++) gsk[q * C::NK + x] = 0.0;
+        for (int x = 0; x < C::NK; x++) gsk[q * C::NK + x] = 0.0;
     }
 #if !defined(COMMET_DEBUG_DROP) || COMMET_DEBUG_DROP != 2  // (planted race: tools/race_check.py)
     __syncthreads();
@@ -1175,8 +1206,9 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
 
     if constexpr (C::FWDC) {
       if (fwd) {
-        if (L == 3) fwd_sweep<C, 3>(m, act, sb, hred, qg, qH, gsk, stab, qNp);
-        else fwd_sweep<C, 2>(m, act, sb, hred, qg, qH, gsk, stab, qNp);
+        double* const gh = fgh ? qgH + h * Q * C::NKH : nullptr;
+        if (L == 3) fwd_sweep<C, 3>(m, act, sb, hred, qg, qH, gsk, stab, qNp, gh);
+        else fwd_sweep<C, 2>(m, act, sb, hred, qg, qH, gsk, stab, qNp, gh);
       }
     }
     if (!fwd) {
@@ -1585,7 +1617,7 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
     }
 #endif
     if constexpr (C::EB > 1) {  // (g, H) of this network batch for the element stage
-      if (tid < Q) {
+      if (!fgh && tid < Q) {
         const int q = tid;
         double* o = qgH + (h * Q + q) * C::NKH;
 #pragma unroll

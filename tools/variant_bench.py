@@ -31,6 +31,10 @@ def main():
         "cann two vectors (9 inputs)": gen.anisotropic(gen.cann_params(3, seed=8, n_in=9), gen.A_FIBRE, gen.A_SHEET),
         "ickan two vectors 9-4-1": gen.anisotropic(gen.ickan_params((9, 4, 1), nb=7, seed=9), gen.A_FIBRE,
                                                    gen.A_SHEET),
+        "icnn 64x3 isochoric anisotropic": gen.anisotropic(gen.ncm_weights(64, 3, 0.3, 20, 10.0, n_in=5),
+                                                           isochoric=True),
+        "cann isochoric two vectors (9 inputs)": gen.anisotropic(gen.cann_params(3, seed=21, n_in=9), gen.A_FIBRE,
+                                                                 (0.0, 0.6, 0.8), isochoric=True),
     }
     u = torch.from_numpy(cfg["u"]).cuda()
     nq = cfg["conn"].shape[0] * 8
