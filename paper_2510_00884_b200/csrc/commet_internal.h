@@ -43,7 +43,8 @@ struct NcmDev {
   const double* kan_c;     // [edges][nb]
   double a0[3];            // anisotropic kinematics: structural vector (reference configuration)
   double a1[3];            // anisotropic kinematics, two vectors (kin 3): the second structural vector
-  int aniso_iso;           // anisotropic kinematics (kin 2, 3) on the isochoric inputs (App. A.2.2, R29)
+  int aniso_iso;           // anisotropic kinematics (kin 2, 3) on the isochoric inputs (App. A.2.2, R29): the fused
+                           // kernel dispatches the compile-time KIN 4 / 5 instantiations, the simple kernel branches
 };
 
 struct AsmArgs {

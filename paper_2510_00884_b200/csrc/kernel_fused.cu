@@ -321,7 +321,8 @@ __device__ __forceinline__ void red_add(double* a, double v) { atomicAdd(a, v); 
 // ---------------------------------------------------------------------------
 // NET_: 0 = ICNN (DMMA network stages 2-6), 1 = analytic inner network (CANN or
 // Gent-Thomas, evaluated per qp in stage 7a; W is then unused).  KIN_: 0 standard
-// invariants, 1 isochoric (compile-time, so the standard path carries no extra code)
+// invariants, 1 isochoric, 2 / 3 anisotropic with one / two structural vectors, 4 / 5 the same on the
+// isochoric inputs (all compile-time, so the standard path carries no extra code)
 // MODE_: 0 = FE assembly; 1 = material points (F in; Psi, tau, c out; NEN = NQ = 1)
 // WS_: warp-specialised kernel (ws_kernel): the NW_ network warps are joined by NWE element warps
 // that run stages 7-8 of batch b (and load the inputs of batch b + 2) while the network warps
@@ -334,8 +335,11 @@ struct Cfg {
   static constexpr int NWE = WS ? COMMET_WS_NWE : 0, NTHR_ALL = 32 * (NW_ + NWE);
   // network inputs per qp: 3 (standard / isochoric invariants) or 5 (anisotropic: + I4, I5)
   // (KIN 2: one structural vector, 5 inputs; KIN 3: two vectors, 9 inputs -- App. A.2.1)
-  static constexpr int NSV = KIN == 3 ? 2 : 1;
-  static constexpr int NK = KIN == 2 ? 5 : (KIN == 3 ? 9 : 3), NH = NK * (NK + 1) / 2;
+  // (KIN 4 / 5: the same on the isochoric inputs Ibar1, Ibar2, J, Ibar4,ij, Ibar5,ij -- App. A.2.2,
+  //  compile-time so the plain anisotropic kernels carry none of the chain rule)
+  static constexpr bool ISO_A = KIN >= 4;
+  static constexpr int NSV = (KIN == 3 || KIN == 5) ? 2 : 1;
+  static constexpr int NK = KIN >= 2 ? (NSV == 2 ? 9 : 5) : 3, NH = NK * (NK + 1) / 2;
   static constexpr int NP = NK + NH;  // adjoint-pass partials per qp: g (NK) and H_1 (NH)
   static constexpr int NWARP = NW_, NTHR = 32 * NW_;
   static constexpr int MINB = MINB_;               // CTAs per SM the register budget targets (3: <= 168 regs)
@@ -388,7 +392,7 @@ struct Cfg {
 template <class C>
 struct Smem {
   // per-qp stride of the stage-7a outputs (odd: bank spread); anisotropic: 5 factor pairs
-  static constexpr int PS = C::KIN == 3 ? kPostAniso2 : (C::KIN == 2 ? kPostAniso : 101);
+  static constexpr int PS = C::KIN >= 2 ? (C::NSV == 2 ? kPostAniso2 : kPostAniso) : 101;
   int act, sb, cb, qF, qk, qg, qH, hred, gsk, gN, ue, wq, qN, tab, qgH, qP, post, X, qA, total;
   // fwd: the forward-sweep path runs (C::FWDC, 2 <= L <= 3, no hidden skips): no c buffers
   __host__ __device__ static bool fwd_path(int L, bool skips) { return C::FWDC && L >= 2 && L <= 3 && !skips; }
@@ -557,7 +561,7 @@ __device__ __forceinline__ void material_outputs(const AsmArgs& A, const NcmDev&
     kinematics(qF + q * 9, kin);
     if constexpr (C::KIN == 1) isochoric_to_standard(kin, gq, H6);
     if constexpr (C::KIN >= 2)
-      if (m.aniso_iso) isochoric_aniso_to_standard<C::NSV>(kin, m.a0, m.a1, gq, H6);
+      if constexpr (C::ISO_A) isochoric_aniso_to_standard<C::NSV>(kin, m.a0, m.a1, gq, H6);
     const double jm1 = kin.J - 1.0;
     const double Wv = N + m.kappa * jm1 * jm1 - m.ref_shift * jm1;
     gq[2] += 2.0 * m.kappa * jm1 - m.ref_shift;
@@ -1163,7 +1167,7 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
       for (int x = 0; x < 9; x++) qF[q * 9 + x] = F[x];
       if constexpr (C::KIN >= 2) {  // anisotropic inputs (+ I4,ij, I5,ij per vector pair)
         double kb[C::NK];
-        anisotropic_inputs<C::NSV>(kin, m.a0, m.a1, kb, m.aniso_iso);
+        anisotropic_inputs<C::NSV>(kin, m.a0, m.a1, kb, C::ISO_A);
 #pragma unroll
         for (int x = 0; x < C::NK; x++) qk[q * C::NK + x] = kb[x];
       } else if constexpr (C::KIN == 1) {  // isochoric inputs (App. A.2.2)
@@ -1715,7 +1719,7 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
       kinematics(qF + q * 9, kin);
       if constexpr (C::KIN == 1) isochoric_to_standard(kin, gq, H6);
       if constexpr (C::KIN >= 2)
-        if (m.aniso_iso) isochoric_aniso_to_standard<C::NSV>(kin, m.a0, m.a1, gq, H6);
+        if constexpr (C::ISO_A) isochoric_aniso_to_standard<C::NSV>(kin, m.a0, m.a1, gq, H6);
       gq[2] += 2.0 * m.kappa * (kin.J - 1.0) - m.ref_shift;
       H6[packed_index(C::NK, 2, 2)] += 2.0 * m.kappa;
       if constexpr (C::KIN >= 2)
@@ -1782,7 +1786,11 @@ __global__ void __launch_bounds__(C::NTHR, C::MINB) fused_kernel(AsmArgs A) {
           }
         }
       }
+#if COMMET_META_EARLY
 #pragma unroll
+#else
+#pragma unroll 1  // (a rolled task loop: the unrolled one costs Gent-Thomas ~1 % in instruction footprint)
+#endif
       for (int x = 0; x < TH8; x++) {
         const int task = warp + x * C::NWARP;
         if (task >= ne * 2) break;
@@ -2205,7 +2213,7 @@ __device__ __forceinline__ void ws_element(const AsmArgs& A, double* smem, int64
       kinematics(sm.qF(smem, s) + q * 9, kin);
       if constexpr (C::KIN == 1) isochoric_to_standard(kin, gq, H6);
       if constexpr (C::KIN >= 2)
-        if (m.aniso_iso) isochoric_aniso_to_standard<C::NSV>(kin, m.a0, m.a1, gq, H6);
+        if constexpr (C::ISO_A) isochoric_aniso_to_standard<C::NSV>(kin, m.a0, m.a1, gq, H6);
       gq[2] += 2.0 * m.kappa * (kin.J - 1.0) - m.ref_shift;
       H6[5] += 2.0 * m.kappa;
       if constexpr (PAR)
@@ -2469,11 +2477,11 @@ static int launch_k(const AsmArgs& a, cudaStream_t st, int* launches) {
   }
   return (int)cudaErrorInvalidValue;
 #else
-  if constexpr (K == 3) {  // two structural vectors, 9 inputs: the per-qp (analytic) networks only
+  if constexpr (K == 3 || K == 5) {  // two structural vectors, 9 inputs: the per-qp (analytic) networks only
     if (a.ncm.net != 0) return launch_cfg<Cfg<16, COMMET_Q_KIN3, NEN, NQ, 2, 1, K>>(a, st, launches);
     return (int)cudaErrorInvalidValue;  // (an ICNN on 9 inputs is refused at setup)
   } else {
-  if constexpr (K == 2) {  // 5 inputs: packed 5x5 Hessians and the extended F-space factors
+  if constexpr (K == 2 || K == 4) {  // 5 inputs: packed 5x5 Hessians and the extended F-space factors
     if (a.ncm.net != 0) return launch_cfg<Cfg<16, 32, NEN, NQ, 2, 1, K>>(a, st, launches);
   } else {
     if (a.ncm.net == 3)  // ICKAN: its per-qp forward mode needs the registers (4 CTAs/SM: spills, -14 %)
@@ -2484,14 +2492,14 @@ static int launch_k(const AsmArgs& a, cudaStream_t st, int* launches) {
   }
   // the forward-sweep ICNN (w = 64 / 128, L = 2 or 3, no hidden skips) on hex8: warp-specialised
   // kernel (tet10 keeps the one-role kernel: its scalar element stage needs the aliased X buffer)
-  if constexpr (K != 2 && NEN == 8 && COMMET_WS) {
+  if constexpr (K < 2 && NEN == 8 && COMMET_WS) {
     if (a.ncm.L >= 2 && a.ncm.L <= 3 && a.ncm.skip_h == nullptr) {
       if (a.ncm.w == 64) return launch_ws<Cfg<64, 16, NEN, NQ, 2, 0, K, 0, 4, 1>>(a, st, launches);
       if (a.ncm.w == 128) return launch_ws<Cfg<128, 8, NEN, NQ, 2, 0, K, 0, 4, 1>>(a, st, launches);
     }
   }
   // 5-input ICNN: the Jacobian pass carries 5 columns and 15 Hessian partials -> 2 CTAs/SM
-  constexpr int MB = K == 2 ? 2 : 3;
+  constexpr int MB = K >= 2 ? 2 : 3;
   switch (a.ncm.w) {
     case 8: return launch_cfg<Cfg<8, 32, NEN, NQ, MB, 0, K>>(a, st, launches);
     case 16: return launch_cfg<Cfg<16, 16, NEN, NQ, MB, 0, K>>(a, st, launches);
@@ -2510,12 +2518,12 @@ static int launch_mat_k(const AsmArgs& a, cudaStream_t st) {
 #ifdef COMMET_AB_MIN
   return (int)cudaErrorInvalidValue;
 #else
-  if constexpr (K == 3) {  // two structural vectors: analytic networks only
+  if constexpr (K == 3 || K == 5) {  // two structural vectors: analytic networks only
     if (a.ncm.net != 0) return launch_cfg<Cfg<16, 16, 1, 1, 2, 1, K, 1>>(a, st, nullptr);
     return (int)cudaErrorInvalidValue;
   } else {
   if (a.ncm.net != 0) return launch_cfg<Cfg<16, 16, 1, 1, 3, 1, K, 1>>(a, st, nullptr);
-  constexpr int MB = K == 2 ? 2 : 3;
+  constexpr int MB = K >= 2 ? 2 : 3;
   switch (a.ncm.w) {
     case 8: return launch_cfg<Cfg<8, 32, 1, 1, MB, 0, K, 1>>(a, st, nullptr);
     case 16: return launch_cfg<Cfg<16, 16, 1, 1, MB, 0, K, 1>>(a, st, nullptr);
@@ -2531,6 +2539,8 @@ static int launch_mat_k(const AsmArgs& a, cudaStream_t st) {
 int launch_material(const AsmArgs& a, void* stream) {
   if (a.el_count <= 0) return 0;
   cudaStream_t st = (cudaStream_t)stream;
+  if (a.ncm.kin >= 2 && a.ncm.aniso_iso)  // isochoric anisotropic: the KIN 4 / 5 instantiations
+    return a.ncm.kin == 3 ? launch_mat_k<5>(a, st) : launch_mat_k<4>(a, st);
   if (a.ncm.kin == 3) return launch_mat_k<3>(a, st);
   return a.ncm.kin == 2 ? launch_mat_k<2>(a, st) : a.ncm.kin == 1 ? launch_mat_k<1>(a, st) : launch_mat_k<0>(a, st);
 }
@@ -2540,6 +2550,8 @@ static int launch_et(const AsmArgs& a, cudaStream_t st, int* launches) {
 #ifdef COMMET_AB_MIN
   return launch_k<NEN, NQ, 0>(a, st, launches);
 #else
+  if (a.ncm.kin >= 2 && a.ncm.aniso_iso)  // isochoric anisotropic: the KIN 4 / 5 instantiations
+    return a.ncm.kin == 3 ? launch_k<NEN, NQ, 5>(a, st, launches) : launch_k<NEN, NQ, 4>(a, st, launches);
   if (a.ncm.kin == 3) return launch_k<NEN, NQ, 3>(a, st, launches);
   if (a.ncm.kin == 2) return launch_k<NEN, NQ, 2>(a, st, launches);
   return a.ncm.kin == 1 ? launch_k<NEN, NQ, 1>(a, st, launches) : launch_k<NEN, NQ, 0>(a, st, launches);
