@@ -77,3 +77,36 @@ def test_null_context_calls_fail_cleanly():
     assert pc._lib.commet_assemble(None, None, None, None, None) == pc.COMMET_ERR_ARG
     assert pc._lib.commet_check(None, None) == pc.COMMET_ERR_ARG
     pc._lib.commet_destroy(None)
+
+
+@pytest.mark.parametrize("kin,n_sv,net,expect", [
+    (7, 0, 0, "kinematics 7 unknown"),
+    (3, 3, 0, "n_sv 3 not in 0..2"),                       # isochoric anisotropic, too many vectors
+    (3, 1, 2, "anisotropic kinematics need an ICNN, CANN or ICKAN"),  # Gent-Thomas on 5 inputs
+    (3, 2, 0, "two structural vectors (9 inputs): CANN or ICKAN"),   # ICNN on 9 inputs
+])
+def test_setup_rejects_bad_kinematics(kin, n_sv, net, expect):
+    """Host validation of the kinematics ids (commet.h COMMET_KIN_*; 3 = isochoric anisotropic,
+    App. A.2.2 / DESIGN R29) before any CUDA call."""
+    import paper_2510_00884_b200 as pc
+    from synth.gen import hex_mesh, shape_gradients
+    X, conn = hex_mesh(2)
+    gN, w = shape_gradients(X, conn, 0)
+    nd, keep = _ncm(16, 2)
+    nd.kinematics, nd.n_sv, nd.network = kin, n_sv, net
+    md = _desc(conn, gN, w, X.shape[0])
+    ctx = C.c_void_p()
+    st = pc._lib.commet_setup(C.byref(md), C.byref(nd), 0, None, None, C.byref(ctx))
+    assert st == pc.COMMET_ERR_ARG and not ctx.value
+    assert expect in pc._lib.commet_last_error(None).decode()
+
+
+def test_binding_kinematics_names():
+    """The binding's names map onto the header's ids (no GPU needed)."""
+    import paper_2510_00884_b200 as pc
+    from synth.gen import anisotropic, cann_params, A_FIBRE, A_SHEET
+    src = open(os.path.join(ROOT, "include", "commet.h")).read()
+    ids = dict(re.findall(r"(COMMET_KIN_[A-Z_]+) = (\d+)", src))
+    assert int(ids["COMMET_KIN_ISOCHORIC_ANISOTROPIC"]) == pc.KIN_ISOCHORIC_ANISOTROPIC == 3
+    nd, _ = pc.ncm_desc(anisotropic(cann_params(3, n_in=9), A_FIBRE, A_SHEET, isochoric=True))
+    assert nd.kinematics == 3 and nd.n_sv == 2 and list(nd.a1) == list(A_SHEET)
