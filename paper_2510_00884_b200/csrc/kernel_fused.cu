@@ -135,6 +135,9 @@
 #ifndef COMMET_FUSE_GH
 #define COMMET_FUSE_GH 0  // forward sweep + two-batch element stage: (g, H) written straight into qgH (one barrier and the qg / qH / gsk buffers fewer; measured c3 +0.1-0.3 %, c5 +0.15 % (8 B spill) -> off; r02_ab_fuse_gh.txt)
 #endif
+#ifndef COMMET_VSTORE
+#define COMMET_VSTORE 1  // forward-sweep epilogue: the two qps of a lane stored with one 16-byte store per row (c3 -0.8 %, c4 -0.7 %, c5 564 -> 560 ms; r02_ab_vstore.txt)
+#endif
 #ifndef COMMET_EB
 #define COMMET_EB 2  // network batches per element batch (ICNN assembly; c3 9.72 -> 9.43 ms with the two below)
 #endif
@@ -668,6 +671,21 @@ __device__ __forceinline__ void fwd_sweep(const NcmDev& m, double* act, double* 
         const int j = (mt0 + i) * 8 + g;
         const double bj = __ldg(m.b + (l - 1) * W + j);
         const double aj = __ldg(m.a + j);
+#if COMMET_VSTORE
+        if (l < L) {  // both qps of the lane (q, q + 1: 16-byte aligned) with one vector store per row
+          const int q = qb * 8 + 2 * t;
+          double z[2], s[2];
+#pragma unroll
+          for (int h = 0; h < 2; h++) softplus_sig_t<C::TB_FWD>(acc[i][0][h] + bj, stab, z[h], s[h]);
+          *reinterpret_cast<double2*>(sb + ((l - 1) * W + j) * LDS + q) = make_double2(s[0], s[1]);
+          double* ar = act + j * LDA + q;
+          *reinterpret_cast<double2*>(ar) = make_double2(z[0], z[1]);
+#pragma unroll
+          for (int c = 1; c < 4; c++)
+            *reinterpret_cast<double2*>(ar + c * Q) = make_double2(s[0] * acc[i][c][0], s[1] * acc[i][c][1]);
+          continue;
+        }
+#endif
 #pragma unroll
         for (int h = 0; h < 2; h++) {
           const int q = qb * 8 + 2 * t + h;
