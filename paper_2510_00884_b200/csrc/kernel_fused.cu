@@ -138,6 +138,9 @@
 #ifndef COMMET_VSTORE
 #define COMMET_VSTORE 1  // forward-sweep epilogue: the two qps of a lane stored with one 16-byte store per row (c3 -0.8 %, c4 -0.7 %, c5 564 -> 560 ms; r02_ab_vstore.txt)
 #endif
+#ifndef COMMET_VSTORE2
+#define COMMET_VSTORE2 1  // forward-sweep backward epilogue (layer 3): 16-byte shared loads / stores of a lane's two qps  (c3 -0.1 %, c4 / c5 neutral; r02_ab_vstore2.txt)
+#endif
 #ifndef COMMET_EB
 #define COMMET_EB 2  // network batches per element batch (ICNN assembly; c3 9.72 -> 9.43 ms with the two below)
 #endif
@@ -784,22 +787,47 @@ __device__ __forceinline__ void fwd_sweep(const NcmDev& m, double* act, double* 
         for (int i = 0; i < C::MT_V; i++) {
           const int j = (mt0 + i) * 8 + g;
 #pragma unroll
-          for (int jj = 0; jj < C::NT_V; jj++)
+          for (int jj = 0; jj < C::NT_V; jj++) {
+#if COMMET_VSTORE2  // the lane's two qps (q, q + 1) with 16-byte shared loads / stores
+            const int q0 = ncol[jj] + 2 * t;
+            const double2 s2 = *reinterpret_cast<const double2*>(sb + ((l - 2) * W + j) * LDS + q0);
+            const double2 Pa = *reinterpret_cast<const double2*>(act + j * LDA + Q + q0);
+            const double2 Pb = *reinterpret_cast<const double2*>(act + j * LDA + 2 * Q + q0);
+            const double2 Pc = *reinterpret_cast<const double2*>(act + j * LDA + 3 * Q + q0);
+            double mu[2];
+#endif
 #pragma unroll
             for (int h = 0; h < 2; h++) {
               const int q = ncol[jj] + 2 * t + h;
               const double lam = acc[i][jj][h];
+#if COMMET_VSTORE2
+              const double s = h ? s2.y : s2.x;
+#else
               const double s = sb[((l - 2) * W + j) * LDS + q];
+#endif
               // c_2 J_2 J_2^T = lam (1 - s)/s P P^T.  1/s of s clamped at 2^-500: finite for any lam
               // the weights can produce (a neuron with s < 2^-500 contributes < 1e-150 either way)
               const double k2 = lam * (1.0 - s) * rcp_nr(fmax(s, 0x1p-500));
+#if COMMET_VSTORE2
+              const double P0 = h ? Pa.y : Pa.x, P1 = h ? Pb.y : Pb.x, P2 = h ? Pc.y : Pc.x;
+              (void)q;
+#else
               const double P0 = act[j * LDA + Q + q], P1 = act[j * LDA + 2 * Q + q], P2 = act[j * LDA + 3 * Q + q];
+#endif
               const double c0 = k2 * P0, c1 = k2 * P1, c2 = k2 * P2;
               double* hh = hb[jj][h];
               hh[0] += c0 * P0; hh[1] += c0 * P1; hh[2] += c0 * P2;
               hh[3] += c1 * P1; hh[4] += c1 * P2; hh[5] += c2 * P2;
+#if COMMET_VSTORE2
+              mu[h] = lam * s;
+#else
               act[j * LDA + q] = lam * s;  // mu_2
+#endif
             }
+#if COMMET_VSTORE2
+            *reinterpret_cast<double2*>(act + j * LDA + q0) = make_double2(mu[0], mu[1]);  // mu_2
+#endif
+          }
         }
         if constexpr (COMMET_RS) {
           constexpr int NV = C::NT_V * 12;
