@@ -187,6 +187,28 @@ commet_status commet_csr_pattern_copy(commet_ctx ctx, int64_t* row_ptr, int32_t*
 commet_status commet_assemble(commet_ctx ctx, const double* u, double* residual,
                               double* csr_values, void* cuda_stream);
 
+/* Assemble on HOST buffers (the end-to-end call; the same r / K as commet_assemble,
+ * Eq. r-quad / k-quad): u_host fp64 [3*n_nodes] is read, residual_host
+ * fp64 [n_rows] and csr_values_host fp64 [nnz] are written.  The caller owns the host
+ * buffers; pinned memory (cudaHostAlloc / cudaHostRegister) makes the copies
+ * asynchronous, pageable memory works but serialises them.  Asynchronous: the call
+ * enqueues the upload of u (internal copy stream), the assembly (cuda_stream) and the
+ * read-back (two internal copy streams, the CSR values in 8 chunks) and returns; the
+ * host outputs are valid after commet_host_wait.  The ctx owns two device staging sets
+ * (allocated on the first call: 2 x (u + residual + CSR values) doubles; freed by
+ * commet_destroy), used alternately, so call s's read-back and call s+1's upload overlap
+ * call s+1's assembly.  The caller must not modify u_host, nor read the outputs, before
+ * commet_host_wait; successive calls writing the same host outputs complete in call
+ * order.  COMMET_ERR_ARG for NULL buffers, a material-only ctx or peer mode;
+ * COMMET_ERR_OOM if the staging sets do not fit.  det F <= 0: commet_check. */
+commet_status commet_assemble_host(commet_ctx ctx, const double* u_host, double* residual_host,
+                                   double* csr_values_host, void* cuda_stream);
+
+/* Completion of every commet_assemble_host call issued so far: with cuda_stream != NULL
+ * that stream waits (device side) for the read-backs; with NULL the host blocks until
+ * they are done.  COMMET_OK if no host call was made. */
+commet_status commet_host_wait(commet_ctx ctx, void* cuda_stream);
+
 /* Synchronises the ctx's last assemble stream; *first_bad_qp = this rank's
  * lowest e*n_q+q (local element index) with det F <= 0, else -1.  Returns
  * COMMET_ERR_DOMAIN if some det F <= 0 (R10), else COMMET_OK.

@@ -38,7 +38,8 @@ SYMBOLS = ("commet_setup", "commet_csr_pattern", "commet_csr_pattern_copy", "com
            "commet_cg_jacobi", "commet_newton_step", "commet_ncm_eval", "commet_normalize_reference",
            "commet_material_eval", "commet_halo_recv_maps", "commet_set_peer", "commet_set_peer_mode",
            "commet_zero_outputs", "commet_set_preconditioner", "commet_check_ranks", "commet_plan_colour_iface",
-           "commet_selftest_activation_tab", "commet_kernel_config", "commet_kernel_batch")
+           "commet_selftest_activation_tab", "commet_kernel_config", "commet_kernel_batch",
+           "commet_assemble_host", "commet_host_wait")
 NEWTON_MAX_LOG = 64
 
 
@@ -169,6 +170,10 @@ _lib.commet_cg_jacobi.argtypes = [_vp, _vp, _vp, _vp, C.c_double, _i32, _P(_i32)
 _lib.commet_newton_step.argtypes = [_vp, _vp, _P(NewtonCfg), _vp, _P(NewtonReport), _vp]
 _lib.commet_ncm_eval.argtypes = [_vp, _vp, _vp, _vp, _i64, _vp]
 _lib.commet_normalize_reference.argtypes = [_vp, _P(C.c_double)]
+_lib.commet_assemble_host.argtypes = [_vp, _vp, _vp, _vp, _vp]
+_lib.commet_assemble_host.restype = C.c_int
+_lib.commet_host_wait.argtypes = [_vp, _vp]
+_lib.commet_host_wait.restype = C.c_int
 _lib.commet_material_eval.argtypes = [_vp, _vp, _i64, _vp, _vp, _vp, _vp]
 _lib.commet_material_eval.restype = C.c_int
 _lib.commet_halo_recv_maps.argtypes = [_vp, _i32, _P(_vp), _P(_vp)]
@@ -318,6 +323,30 @@ class Commet:
         _check(_lib.commet_assemble(self.ctx, u.data_ptr(), residual.data_ptr(), values.data_ptr(),
                                     st.cuda_stream), self.ctx)
         return residual, values
+
+    def _host_f64(self, x, n, name):
+        t = self.torch
+        if not (isinstance(x, t.Tensor) and x.device.type == "cpu" and x.dtype == t.float64
+                and x.is_contiguous()):
+            raise TypeError(f"{name} must be a contiguous cpu float64 tensor (pinned for asynchronous copies)")
+        if x.numel() != n:
+            raise ValueError(f"{name} has {x.numel()} entries, expected {n}")
+
+    def assemble_host(self, u_host, residual_host, values_host, stream=None):
+        """commet_assemble_host: host u in, host residual / CSR values out (asynchronous: the
+        outputs are valid after host_wait).  The library uploads, assembles and reads back."""
+        t = self.torch
+        self._host_f64(u_host, 3 * self.n_nodes, "u_host")
+        self._host_f64(residual_host, self.n_rows, "residual_host")
+        self._host_f64(values_host, self.nnz, "values_host")
+        st = stream if stream is not None else t.cuda.current_stream(self.device)
+        _check(_lib.commet_assemble_host(self.ctx, u_host.data_ptr(), residual_host.data_ptr(),
+                                         values_host.data_ptr(), st.cuda_stream), self.ctx)
+        return residual_host, values_host
+
+    def host_wait(self, stream=None):
+        """commet_host_wait: stream waits for every issued assemble_host read-back (None: the host blocks)."""
+        _check(_lib.commet_host_wait(self.ctx, stream.cuda_stream if stream is not None else None), self.ctx)
 
     def set_timing(self, n_slots: int):
         _check(_lib.commet_set_timing(self.ctx, n_slots), self.ctx)

@@ -414,6 +414,87 @@ extern "C" commet_status commet_assemble(commet_ctx c, const double* u, double* 
   return COMMET_OK;
 }
 
+// ---- end-to-end call on host buffers (DESIGN.md s9 "e2e") ------------------------------------
+// Step s uses staging set k = s % 2: the upload of u waits for the assembly of step s-2 (the last
+// reader of u[k]), the assembly waits for the upload and for the read-back of step s-2 (the last
+// reader of r[k], v[k]); the read-back of step s runs on the copy streams behind its assembly.
+// So step s's read-back and step s+1's upload overlap step s+1's assembly.
+static commet_status host_pipe_init(commet_ctx c) {
+  const Plan& p = c->plan;
+  HostPipe* h = new HostPipe();
+  c->host = h;
+  for (int k = 0; k < 2; k++) {
+    CUDA_TRY(c, h->u[k].alloc(3 * p.n_nodes));
+    CUDA_TRY(c, h->r[k].alloc(3 * p.n_owned));
+    CUDA_TRY(c, h->v[k].alloc(p.nnz));
+    CUDA_TRY(c, cudaEventCreateWithFlags(&h->done_h[k], cudaEventDisableTiming));
+    CUDA_TRY(c, cudaEventCreateWithFlags(&h->done_c[k], cudaEventDisableTiming));
+    for (int i = 0; i < HostPipe::kCopyStreams; i++)
+      CUDA_TRY(c, cudaEventCreateWithFlags(&h->done_d[k][i], cudaEventDisableTiming));
+  }
+  CUDA_TRY(c, cudaStreamCreateWithFlags(&h->h2d, cudaStreamNonBlocking));
+  for (int i = 0; i < HostPipe::kCopyStreams; i++) CUDA_TRY(c, cudaStreamCreateWithFlags(&h->d2h[i], cudaStreamNonBlocking));
+  return COMMET_OK;
+}
+
+extern "C" commet_status commet_assemble_host(commet_ctx c, const double* u_host, double* residual_host,
+                                              double* csr_values_host, void* cuda_stream) {
+  if (!c) return fail(nullptr, COMMET_ERR_ARG, "ctx is NULL");
+  const Plan& p = c->plan;
+  if (c->material_only) return fail(c, COMMET_ERR_ARG, "ctx was set up without a mesh (material points only)");
+  if (c->peer) return fail(c, COMMET_ERR_ARG, "commet_assemble_host: peer mode writes into registered device outputs");
+  if (!u_host || (p.n_owned && !residual_host) || (p.nnz && !csr_values_host))
+    return fail(c, COMMET_ERR_ARG, "u_host, residual_host or csr_values_host is NULL");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  if (!c->host) {
+    commet_status s = host_pipe_init(c);
+    if (s != COMMET_OK) {
+      delete c->host;
+      c->host = nullptr;
+      return s;
+    }
+  }
+  HostPipe* h = c->host;
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  const int k = (int)(h->n_calls % 2);
+  const bool reuse = h->n_calls >= 2;
+  if (reuse) CUDA_TRY(c, cudaStreamWaitEvent(h->h2d, h->done_c[k], 0));
+  CUDA_TRY(c, cudaMemcpyAsync(h->u[k].p, u_host, 3 * p.n_nodes * sizeof(double), cudaMemcpyHostToDevice, h->h2d));
+  CUDA_TRY(c, cudaEventRecord(h->done_h[k], h->h2d));
+  CUDA_TRY(c, cudaStreamWaitEvent(st, h->done_h[k], 0));
+  if (reuse)
+    for (int i = 0; i < HostPipe::kCopyStreams; i++) CUDA_TRY(c, cudaStreamWaitEvent(st, h->done_d[k][i], 0));
+  commet_status s = commet_assemble(c, h->u[k].p, h->r[k].p, h->v[k].p, cuda_stream);
+  if (s != COMMET_OK) return s;
+  CUDA_TRY(c, cudaEventRecord(h->done_c[k], st));
+  for (int i = 0; i < HostPipe::kCopyStreams; i++) CUDA_TRY(c, cudaStreamWaitEvent(h->d2h[i], h->done_c[k], 0));
+  if (p.n_owned)
+    CUDA_TRY(c, cudaMemcpyAsync(residual_host, h->r[k].p, 3 * p.n_owned * sizeof(double), cudaMemcpyDeviceToHost,
+                                h->d2h[0]));
+  for (int j = 0; j < HostPipe::kChunks; j++) {  // one copy engine per stream: chunks round-robin
+    const int64_t a0 = p.nnz * j / HostPipe::kChunks, a1 = p.nnz * (j + 1) / HostPipe::kChunks;
+    if (a1 > a0)
+      CUDA_TRY(c, cudaMemcpyAsync(csr_values_host + a0, h->v[k].p + a0, (a1 - a0) * sizeof(double),
+                                  cudaMemcpyDeviceToHost, h->d2h[j % HostPipe::kCopyStreams]));
+  }
+  for (int i = 0; i < HostPipe::kCopyStreams; i++) CUDA_TRY(c, cudaEventRecord(h->done_d[k][i], h->d2h[i]));
+  h->n_calls++;
+  return COMMET_OK;
+}
+
+extern "C" commet_status commet_host_wait(commet_ctx c, void* cuda_stream) {
+  if (!c) return fail(nullptr, COMMET_ERR_ARG, "ctx is NULL");
+  if (!c->host) return COMMET_OK;
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  for (int k = 0; k < 2 && k < c->host->n_calls; k++)
+    for (int i = 0; i < HostPipe::kCopyStreams; i++) {
+      if (st) CUDA_TRY(c, cudaStreamWaitEvent(st, c->host->done_d[k][i], 0));
+      else CUDA_TRY(c, cudaEventSynchronize(c->host->done_d[k][i]));
+    }
+  return COMMET_OK;
+}
+
 // cross-rank key of a rank's first bad qp: (rank, flat index) in one word, ordered by rank first
 static constexpr int kBadIdxBits = 44;
 

@@ -34,6 +34,27 @@ struct DevBuf {
 }  // namespace commet_detail
 using commet_detail::DevBuf;
 
+// commet_assemble_host: two device staging sets (u, residual, CSR values) and the copy streams
+// that overlap step s's read-back and step s+1's upload with step s+1's assembly
+struct HostPipe {
+  static constexpr int kCopyStreams = 2, kChunks = 8;  // CSR values read back in kChunks pieces
+  DevBuf<double> u[2], r[2], v[2];
+  cudaStream_t h2d = nullptr, d2h[kCopyStreams] = {};
+  cudaEvent_t done_h[2] = {}, done_c[2] = {}, done_d[2][kCopyStreams] = {};
+  int64_t n_calls = 0;
+  ~HostPipe() {  // the copies still in flight finish before their buffers go
+    if (h2d) cudaStreamSynchronize(h2d);
+    for (auto s : d2h) if (s) cudaStreamSynchronize(s);
+    if (h2d) cudaStreamDestroy(h2d);
+    for (auto s : d2h) if (s) cudaStreamDestroy(s);
+    for (int k = 0; k < 2; k++) {
+      if (done_h[k]) cudaEventDestroy(done_h[k]);
+      if (done_c[k]) cudaEventDestroy(done_c[k]);
+      for (auto e : done_d[k]) if (e) cudaEventDestroy(e);
+    }
+  }
+};
+
 struct SolverWork;  // solver.cu: Dirichlet set, CG / Newton workspace
 void solver_work_free(SolverWork* w);
 
@@ -71,12 +92,14 @@ struct commet_ctx_s {
   DevBuf<int64_t> peer_vmap, peer_rmap;
   DevBuf<float> barrier_buf;
   SolverWork* solver = nullptr;
+  HostPipe* host = nullptr;  // commet_assemble_host staging, allocated on first use
   NcmDev ncm{};
   // timing ring
   std::vector<cudaEvent_t> ev0, ev1;
   int64_t n_assembled = 0;
   ~commet_ctx_s() {
     solver_work_free(solver);
+    delete host;
     if (ev_iface) cudaEventDestroy(ev_iface);
     if (ev_comm) cudaEventDestroy(ev_comm);
     if (comm_stream) cudaStreamDestroy(comm_stream);
