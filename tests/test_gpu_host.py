@@ -86,3 +86,26 @@ def test_host_call_argument_errors(pc):
     assert L.commet_assemble_host(mat.ctx, u_host.data_ptr(), r_host.data_ptr(), r_host.data_ptr(),
                                   None) == pc.COMMET_ERR_ARG
     assert b"material" in L.commet_last_error(mat.ctx)
+
+
+def test_destroy_with_copies_in_flight(pc):
+    """commet_destroy right after commet_assemble_host (no host_wait): the staging sets are freed only
+    after their copies finish, and a new ctx on the same device assembles correctly."""
+    cfg = gen.make_config("c2")
+    u_host = torch.from_numpy(cfg["u"]).pin_memory()
+    for _ in range(2):
+        lib = pc.from_config(cfg, device=0)
+        r_host = torch.empty(lib.n_rows, dtype=torch.float64).pin_memory()
+        v_host = torch.empty(lib.nnz, dtype=torch.float64).pin_memory()
+        for _ in range(3):
+            lib.assemble_host(u_host, r_host, v_host)
+        lib.close()
+    torch.cuda.synchronize()
+    lib = pc.from_config(cfg, device=0)
+    r_host = torch.empty(lib.n_rows, dtype=torch.float64).pin_memory()
+    v_host = torch.empty(lib.nnz, dtype=torch.float64).pin_memory()
+    lib.assemble_host(u_host, r_host, v_host)
+    lib.host_wait()
+    r, v = lib.assemble(u_host.cuda())
+    torch.cuda.synchronize()
+    assert torch.equal(r_host, r.cpu()) and torch.equal(v_host, v.cpu())
