@@ -423,6 +423,8 @@ static commet_status host_pipe_init(commet_ctx c) {
   const Plan& p = c->plan;
   HostPipe* h = new HostPipe();
   c->host = h;
+  if (const char* e = getenv("COMMET_HOST_COPY_STREAMS")) h->n_streams = std::max(1, std::min(HostPipe::kCopyStreams, atoi(e)));
+  if (const char* e = getenv("COMMET_HOST_CHUNKS")) h->n_chunks = std::max(1, std::min(1024, atoi(e)));
   for (int k = 0; k < 2; k++) {
     CUDA_TRY(c, h->u[k].alloc(3 * p.n_nodes));
     CUDA_TRY(c, h->r[k].alloc(3 * p.n_owned));
@@ -463,21 +465,21 @@ extern "C" commet_status commet_assemble_host(commet_ctx c, const double* u_host
   CUDA_TRY(c, cudaEventRecord(h->done_h[k], h->h2d));
   CUDA_TRY(c, cudaStreamWaitEvent(st, h->done_h[k], 0));
   if (reuse)
-    for (int i = 0; i < HostPipe::kCopyStreams; i++) CUDA_TRY(c, cudaStreamWaitEvent(st, h->done_d[k][i], 0));
+    for (int i = 0; i < h->n_streams; i++) CUDA_TRY(c, cudaStreamWaitEvent(st, h->done_d[k][i], 0));
   commet_status s = commet_assemble(c, h->u[k].p, h->r[k].p, h->v[k].p, cuda_stream);
   if (s != COMMET_OK) return s;
   CUDA_TRY(c, cudaEventRecord(h->done_c[k], st));
-  for (int i = 0; i < HostPipe::kCopyStreams; i++) CUDA_TRY(c, cudaStreamWaitEvent(h->d2h[i], h->done_c[k], 0));
+  for (int i = 0; i < h->n_streams; i++) CUDA_TRY(c, cudaStreamWaitEvent(h->d2h[i], h->done_c[k], 0));
   if (p.n_owned)
     CUDA_TRY(c, cudaMemcpyAsync(residual_host, h->r[k].p, 3 * p.n_owned * sizeof(double), cudaMemcpyDeviceToHost,
                                 h->d2h[0]));
-  for (int j = 0; j < HostPipe::kChunks; j++) {  // one copy engine per stream: chunks round-robin
-    const int64_t a0 = p.nnz * j / HostPipe::kChunks, a1 = p.nnz * (j + 1) / HostPipe::kChunks;
+  for (int j = 0; j < h->n_chunks; j++) {  // one copy engine per stream: chunks round-robin
+    const int64_t a0 = p.nnz * j / h->n_chunks, a1 = p.nnz * (j + 1) / h->n_chunks;
     if (a1 > a0)
       CUDA_TRY(c, cudaMemcpyAsync(csr_values_host + a0, h->v[k].p + a0, (a1 - a0) * sizeof(double),
-                                  cudaMemcpyDeviceToHost, h->d2h[j % HostPipe::kCopyStreams]));
+                                  cudaMemcpyDeviceToHost, h->d2h[j % h->n_streams]));
   }
-  for (int i = 0; i < HostPipe::kCopyStreams; i++) CUDA_TRY(c, cudaEventRecord(h->done_d[k][i], h->d2h[i]));
+  for (int i = 0; i < h->n_streams; i++) CUDA_TRY(c, cudaEventRecord(h->done_d[k][i], h->d2h[i]));
   h->n_calls++;
   return COMMET_OK;
 }
@@ -488,7 +490,7 @@ extern "C" commet_status commet_host_wait(commet_ctx c, void* cuda_stream) {
   CUDA_TRY(c, cudaSetDevice(c->device));
   cudaStream_t st = (cudaStream_t)cuda_stream;
   for (int k = 0; k < 2 && k < c->host->n_calls; k++)
-    for (int i = 0; i < HostPipe::kCopyStreams; i++) {
+    for (int i = 0; i < c->host->n_streams; i++) {
       if (st) CUDA_TRY(c, cudaStreamWaitEvent(st, c->host->done_d[k][i], 0));
       else CUDA_TRY(c, cudaEventSynchronize(c->host->done_d[k][i]));
     }

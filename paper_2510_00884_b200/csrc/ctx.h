@@ -37,7 +37,10 @@ using commet_detail::DevBuf;
 // commet_assemble_host: two device staging sets (u, residual, CSR values) and the copy streams
 // that overlap step s's read-back and step s+1's upload with step s+1's assembly
 struct HostPipe {
-  static constexpr int kCopyStreams = 2, kChunks = 8;  // CSR values read back in kChunks pieces
+  // read-back streams (one copy engine each) and CSR-value chunks, round-robin over the streams;
+  // COMMET_HOST_COPY_STREAMS / COMMET_HOST_CHUNKS override the defaults (A/B)
+  static constexpr int kCopyStreams = 4;
+  int n_streams = 2, n_chunks = 8;
   DevBuf<double> u[2], r[2], v[2];
   cudaStream_t h2d = nullptr, d2h[kCopyStreams] = {};
   cudaEvent_t done_h[2] = {}, done_c[2] = {}, done_d[2][kCopyStreams] = {};
