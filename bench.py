@@ -105,6 +105,41 @@ def hbm_bytes_per_element(elem_type: int, nnz_per_el: float, dofs_per_el: float)
 # ---------------------------------------------------------------------------
 # distributed helpers
 # ---------------------------------------------------------------------------
+def gpu_local_cpus(device: int):
+    """CPUs of the GPU's NUMA node (sysfs local_cpulist of its PCI function), or None if unknown."""
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        bus = pynvml.nvmlDeviceGetPciInfo(pynvml.nvmlDeviceGetHandleByIndex(device)).busId
+        bus = (bus.decode() if isinstance(bus, bytes) else bus).lower()
+        cpus = set()
+        with open(f"/sys/bus/pci/devices/{bus[-12:]}/local_cpulist") as f:
+            for part in f.read().strip().split(","):
+                a, _, b = part.partition("-")
+                cpus.update(range(int(a), int(b or a) + 1))
+        return cpus & os.sched_getaffinity(0) or None
+    except Exception:
+        return None
+
+
+class numa_local:
+    """Allocate pinned host buffers from the GPU's NUMA node: the pages of a cudaHostAlloc are placed
+    by the allocating thread (first touch), and a remote node puts the inter-socket link in front of
+    every host<->device copy.  Restores the process's CPU affinity on exit."""
+
+    def __init__(self, device: int):
+        self.cpus = gpu_local_cpus(device)
+
+    def __enter__(self):
+        self.saved = os.sched_getaffinity(0)
+        if self.cpus:
+            os.sched_setaffinity(0, self.cpus)
+        return self
+
+    def __exit__(self, *exc):
+        os.sched_setaffinity(0, self.saved)
+
+
 def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -318,7 +353,8 @@ def main():
     kinfo = lib.kernel_info()
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream(dev)
-    u_host = torch.from_numpy(cfg["u"]).pin_memory()
+    with numa_local(local) as nl:
+        u_host = torch.from_numpy(cfg["u"]).pin_memory()
     u = u_host.to(dev)
     r, v = lib.alloc_outputs()
     peer = ws > 1 and args.exchange == "peer"
@@ -362,8 +398,9 @@ def main():
         n_rows, nnz = r.numel(), v.numel()
         del r, v
         torch.cuda.empty_cache()
-        r_host = torch.empty(n_rows, dtype=torch.float64).pin_memory()
-        v_host = torch.empty(nnz, dtype=torch.float64).pin_memory()
+        with numa_local(local):
+            r_host = torch.empty(n_rows, dtype=torch.float64).pin_memory()
+            v_host = torch.empty(nnz, dtype=torch.float64).pin_memory()
         lib.assemble_host(u_host, r_host, v_host, stream)  # allocates the staging sets (untimed)
         lib.host_wait()
         if ws > 1:
@@ -384,13 +421,15 @@ def main():
         e2e = dict(value=spec_total_qp(args.config, n_el, n_q, ws) / (ms_e2e * 1e-3), unit="qp/s",
                    h2d_bytes_per_step=u_host.numel() * 8, d2h_bytes_per_step=(n_rows + nnz) * 8,
                    ms_per_step=ms_e2e,
+                   host_buffers_cpus=(f"GPU-local NUMA node, {len(nl.cpus)} CPUs" if nl.cpus else "affinity unchanged"),
                    note="commet_assemble_host on pinned host buffers (C ABI): per call the library uploads "
                         "u, assembles and reads r + CSR values back; two device staging sets overlap call "
                         "s's read-back and call s+1's upload with call s+1's assembly")
         del r_host, v_host
     elif not args.no_e2e:  # peer mode: the peers hold this rank's registered (r, v)
-        r_host = torch.empty(r.numel(), dtype=torch.float64).pin_memory()
-        v_host = torch.empty(v.numel(), dtype=torch.float64).pin_memory()
+        with numa_local(local):
+            r_host = torch.empty(r.numel(), dtype=torch.float64).pin_memory()
+            v_host = torch.empty(v.numel(), dtype=torch.float64).pin_memory()
         # peer mode: the peers hold this rank's registered (r, v), so one output set (the
         # read-back of step s finishes before step s+1 assembles)
         sets = [(r, v), (r, v) if peer else lib.alloc_outputs()]
